@@ -1,0 +1,113 @@
+/* psvd.h — C ABI of the B200-native streaming-SVD library (libpsvd.so).
+ *
+ * Drop-in boundary for the hot path of the reference `parsvd` package
+ * (arXiv 2108.08845 / PyParSVD, /root/reference/pkg/src/parsvd).  The
+ * reference is pure Python + numpy; its "FFI" for this path is numpy's
+ * LAPACK/BLAS calls inside the functions cited per entry point below.  The
+ * Python package paper_2108_08845_b200 binds these symbols with ctypes and
+ * mirrors the reference's public functions (StreamConfig/StreamState/
+ * stream_initialize/stream_incorporate/stream_all, parallel_stream_*,
+ * gather_modes, RandomSketchConfig/low_rank_svd).
+ *
+ * Conventions
+ *   - All matrices are column-major fp64 device memory with an explicit
+ *     leading dimension (snapshot-contiguous, as the reference's PARSVD01
+ *     file and wire formats, io.py:1-13 / comm.py:9-13).  Leading
+ *     dimensions must be even and base pointers 16-byte aligned (128-bit
+ *     loads); the Python layer pads when needed.
+ *   - The caller owns every buffer passed in; the library owns only its
+ *     context workspace.
+ *   - Every call is asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream) and never synchronizes with the host, except
+ *     psvd_read_status.
+ *   - Return codes: PSVD_OK, PSVD_EINVAL (-> ValueError), PSVD_ENOCONV
+ *     (-> ConvergenceError, linalg.py:117-121), PSVD_ECUDA (-> RuntimeError).
+ *   - One context per device per host thread; a context is not thread-safe.
+ */
+#ifndef PSVD_H_
+#define PSVD_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSVD_OK 0
+#define PSVD_EINVAL 1
+#define PSVD_ENOCONV 2
+#define PSVD_ECUDA 3
+
+/* device status bits (psvd_read_status) */
+#define PSVD_ST_NONFINITE 1  /* a non-finite entry reached the update (linalg.py:76-77 ValueError) */
+#define PSVD_ST_NOCONVERGE 2 /* small factorization failed (linalg.py:117-121 ConvergenceError) */
+#define PSVD_ST_RESCUE 4     /* orthogonality-drift rescue ran (streaming.py:106-115) */
+#define PSVD_ST_RANKDEF 8    /* a kept singular value is exactly zero */
+#define PSVD_ST_CHOLFAIL 16  /* sketch Cholesky needed the shifted retry */
+
+typedef struct psvd_ctx psvd_ctx;
+
+int psvd_version(void);
+int psvd_create(int device, psvd_ctx** out);
+int psvd_destroy(psvd_ctx* ctx);
+const char* psvd_last_error(psvd_ctx* ctx);
+
+/* Copy the context's device status word to *status (synchronizes `stream`);
+ * reset != 0 clears it afterwards (stream-ordered). */
+int psvd_read_status(psvd_ctx* ctx, int* status, int reset, void* stream);
+
+/* ---- deterministic streaming update (streaming.py:63-116, dsvd.py:205-242) ----
+ *
+ * Panel C = [ff * U * diag(sigma) | A] with U (M x Kc, ld ldu), A (M x B, ld lda),
+ * Kc = 0 for stream_initialize (then U, sigma are ignored).
+ */
+
+/* Local Gram G = C^T C (n x n, n = Kc + B, col-major ld n) — replaces the
+ * np.concatenate + np.linalg.qr R-factor of streaming.py:97-98 / dsvd.py:187
+ * (G = R^T R).  Reduction order is fixed: bitwise reproducible. */
+int psvd_gram(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, const double* sigma, double ff,
+              int Kc, const double* A, int64_t lda, int B, double* G, void* stream);
+
+/* Core factorization of a (summed) Gram: top-K eigenpairs, sigma_k =
+ * sqrt(lambda_k) descending (= svd_full(R).s, linalg.py:107-123), the
+ * reference sign rule on U_R (linalg.py:81-91) and the recompose weights
+ * W (n x K, col-major ld n) such that U_new = [U | A] * W
+ * (= q @ u[:, order] of streaming.py:102-103).  sigma_out: device, K. */
+int psvd_core_eig(psvd_ctx* ctx, const double* G, int n, const double* sigma_in, double ff, int Kc, int K,
+                  double* W, double* sigma_out, void* stream);
+
+/* U_out (M x K, ld ldo) = [U | A] * W; optionally UtU (K x K) = U_out^T U_out
+ * for the drift check.  U_out must not alias U or A. */
+int psvd_recompose(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, int Kc, const double* A,
+                   int64_t lda, int B, const double* W, int K, double* U_out, int64_t ldo, double* UtU,
+                   void* stream);
+
+/* Drift rescue of streaming.py:106-115 driven by UtU on the device: if
+ * max|UtU - I| > tol, U <- qr(U).q reordered and sigma <- sigma*|diag r|
+ * reordered (stable descending); otherwise a no-op.  In place. */
+int psvd_drift_rescue(psvd_ctx* ctx, int64_t M, double* U, int64_t ldu, int K, const double* UtU,
+                      double* sigma, double tol, void* stream);
+
+/* One whole single-GPU update = gram + core_eig + recompose (+ drift rescue
+ * when rescue != 0): stream_initialize (Kc = 0) / stream_incorporate. */
+int psvd_stream_update(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, const double* sigma,
+                       double ff, int Kc, const double* A, int64_t lda, int B, int K, int rescue,
+                       double* U_out, int64_t ldo, double* sigma_out, void* stream);
+
+/* ---- row-parallel helpers ---- */
+
+/* out (n x n) = sum_r parts[r] in rank order (parts: P contiguous n x n blocks);
+ * used after an allgather so every GPU holds bitwise-identical sums. */
+int psvd_sum_ordered(psvd_ctx* ctx, const double* parts, int P, int64_t count, double* out, void* stream);
+
+/* ---- input generation (datagen.py:49-90 formula, device side) ----
+ * out(i, j) = burgers u(x[row0 + i], t[col0 + j]) with x = linspace(0, length, grid),
+ * t = linspace(0, t_final, n_snap); i < rows, j < cols; col-major ld ldo. */
+int psvd_burgers(psvd_ctx* ctx, double* out, int64_t ldo, int64_t row0, int64_t rows, int64_t grid,
+                 int col0, int cols, int n_snap, double length, double t_final, double reynolds,
+                 void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSVD_H_ */

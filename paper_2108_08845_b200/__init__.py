@@ -1,0 +1,16 @@
+"""B200-native streaming / row-parallel / randomized SVD (arXiv 2108.08845).
+
+Drop-in for the hot path of the reference `parsvd` package: the same public
+names for the streaming update, its row-parallel counterpart and the
+randomized sketch configuration, computed by hand-written sm_100a FP64
+kernels (libpsvd.so, include/psvd.h) on state that stays in HBM.
+"""
+
+from .datagen import burgers_device, burgers_matrix, burgers_solution, partition_bounds  # noqa: F401
+from .dsvd import (LocalModes, RankContext, gather_modes, parallel_stream_incorporate,  # noqa: F401
+                   parallel_stream_initialize)
+from .errors import CapacityError, CollectiveTimeout, ConvergenceError, DegenerateModeError  # noqa: F401
+from .linalg import RandomSketchConfig  # noqa: F401
+from .streaming import StreamConfig, StreamState, stream_all, stream_incorporate, stream_initialize  # noqa: F401
+
+__version__ = "0.1.0"

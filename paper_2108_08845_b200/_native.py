@@ -1,0 +1,214 @@
+"""ctypes binding of libpsvd.so (include/psvd.h) and device-buffer plumbing.
+
+The product path has no CPU fallback: if the library or a CUDA device is
+missing, every compute entry point raises.  torch is used only to own device
+memory and streams (plumbing); all arithmetic on the hot path happens in the
+library's kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import threading
+
+import numpy as np
+import torch
+
+from .errors import ConvergenceError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libpsvd.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "psvd.h")
+
+PSVD_OK, PSVD_EINVAL, PSVD_ENOCONV, PSVD_ECUDA = 0, 1, 2, 3
+ST_NONFINITE, ST_NOCONVERGE, ST_RESCUE, ST_RANKDEF, ST_CHOLFAIL = 1, 2, 4, 8, 16
+
+_c_i64 = ctypes.c_int64
+_c_int = ctypes.c_int
+_c_dbl = ctypes.c_double
+_vp = ctypes.c_void_p
+
+# name -> (restype, argtypes); mirrors include/psvd.h
+_SIGS = {
+    "psvd_version": (_c_int, []),
+    "psvd_create": (_c_int, [_c_int, ctypes.POINTER(_vp)]),
+    "psvd_destroy": (_c_int, [_vp]),
+    "psvd_last_error": (ctypes.c_char_p, [_vp]),
+    "psvd_read_status": (_c_int, [_vp, ctypes.POINTER(_c_int), _c_int, _vp]),
+    "psvd_gram": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_int, _vp, _c_i64, _c_int, _vp, _vp]),
+    "psvd_core_eig": (_c_int, [_vp, _vp, _c_int, _vp, _c_dbl, _c_int, _c_int, _vp, _vp, _vp]),
+    "psvd_recompose": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _vp, _c_int, _vp,
+                                _c_i64, _vp, _vp]),
+    "psvd_drift_rescue": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _vp, _vp, _c_dbl, _vp]),
+    "psvd_stream_update": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_int, _vp, _c_i64, _c_int,
+                                    _c_int, _c_int, _vp, _c_i64, _vp, _vp]),
+    "psvd_sum_ordered": (_c_int, [_vp, _vp, _c_int, _c_i64, _vp, _vp]),
+    "psvd_burgers": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_dbl,
+                              _c_dbl, _c_dbl, _vp]),
+}
+
+_lib = None
+_lock = threading.RLock()
+_ctxs = {}
+
+
+def header_symbols():
+    """Function names declared in include/psvd.h."""
+    with open(HEADER) as f:
+        txt = f.read()
+    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(psvd_\w+)\s*\(", txt, re.M)))
+
+
+def lib():
+    """Load libpsvd.so (raises if it was not built — there is no fallback)."""
+    global _lib
+    if _lib is None:
+        with _lock:
+            if _lib is None:
+                if not os.path.exists(LIB_PATH):
+                    raise RuntimeError(
+                        f"{LIB_PATH} is missing: build it with "
+                        "`python -c 'import __graft_entry__ as g; g.build()'` (nvcc, sm_100a)")
+                L = ctypes.CDLL(LIB_PATH)
+                for name, (res, args) in _SIGS.items():
+                    fn = getattr(L, name)
+                    fn.restype = res
+                    fn.argtypes = args
+                _lib = L
+    return _lib
+
+
+def _raise(rc, ctx):
+    msg = lib().psvd_last_error(ctx).decode(errors="replace")
+    if rc == PSVD_EINVAL:
+        raise ValueError(msg)
+    if rc == PSVD_ENOCONV:
+        raise ConvergenceError(msg)
+    raise RuntimeError(f"libpsvd CUDA error: {msg}")
+
+
+def call(name, ctx, *args):
+    rc = getattr(lib(), name)(ctx, *args)
+    if rc != PSVD_OK:
+        _raise(rc, ctx)
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2108_08845_b200 needs a CUDA device (B200, sm_100a); no CPU fallback")
+
+
+def context(device=None):
+    """The library context of a CUDA device (created once per process)."""
+    require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index or 0)
+    idx = dev.index
+    if idx not in _ctxs:
+        with _lock:
+            if idx not in _ctxs:
+                p = _vp()
+                rc = lib().psvd_create(idx, ctypes.byref(p))
+                if rc != PSVD_OK:
+                    raise RuntimeError(f"psvd_create failed on cuda:{idx} (rc={rc})")
+                _ctxs[idx] = p
+    return _ctxs[idx]
+
+
+def stream_ptr(device=None):
+    return _vp(torch.cuda.current_stream(device).cuda_stream)
+
+
+def read_status(ctx, reset=True, device=None):
+    st = _c_int(0)
+    call("psvd_read_status", ctx, ctypes.byref(st), int(reset), stream_ptr(device))
+    return st.value
+
+
+def ptr(t):
+    return _vp(t.data_ptr()) if t is not None else _vp(0)
+
+
+# --------------------------------------------------------------------- device matrices
+
+class DevMat:
+    """Column-major fp64 device matrix: `t` is the (rows x cols) torch view with
+    strides (1, ld); ld is even and the base 16-byte aligned (the library's
+    128-bit loads)."""
+
+    __slots__ = ("t", "rows", "cols", "ld")
+
+    def __init__(self, t, ld):
+        self.t = t
+        self.rows, self.cols = t.shape
+        self.ld = ld
+
+    @classmethod
+    def empty(cls, rows, cols, device):
+        ld = rows + (rows & 1)
+        buf = torch.empty((max(cols, 1), ld), dtype=torch.float64, device=device)
+        return cls(buf[:cols, :rows].T, ld)
+
+    @property
+    def view(self):
+        return self.t
+
+    def data_ptr(self):
+        return self.t.data_ptr()
+
+
+def _aligned_colmajor(t):
+    m, n = t.shape
+    if t.stride(0) != 1 and m > 1:
+        return None
+    ld = t.stride(1) if n > 1 else m + (m & 1)
+    if ld < m or ld % 2 or t.data_ptr() % 16:
+        return None
+    return DevMat(t, ld)
+
+
+def as_device_colmajor(a, device, name="a"):
+    """Coerce an array-like / tensor to a DevMat on `device` (copying only if needed).
+    Validation follows linalg.py:65-78 (2-D, positive dims); the finiteness
+    check runs on the device inside the update (status bit NONFINITE)."""
+    if isinstance(a, DevMat):
+        return a
+    if isinstance(a, torch.Tensor):
+        t = a
+        if t.dim() != 2:
+            raise ValueError(f"{name} must be 2-D, got {t.dim()}-D")
+        if min(t.shape) < 1:
+            raise ValueError(f"{name} must have positive dimensions, got {tuple(t.shape)}")
+        if t.device.type == "cuda" and t.dtype == torch.float64:
+            dm = _aligned_colmajor(t)
+            if dm is not None:
+                return dm
+        t = t.to(device=device, dtype=torch.float64)
+        out = DevMat.empty(t.shape[0], t.shape[1], device)
+        out.view.copy_(t)
+        return out
+    arr = np.asarray(a, dtype=np.float64)
+    if arr.ndim != 2:
+        raise ValueError(f"{name} must be 2-D, got {arr.ndim}-D")
+    if min(arr.shape) < 1:
+        raise ValueError(f"{name} must have positive dimensions, got {arr.shape}")
+    m, n = arr.shape
+    out = DevMat.empty(m, n, device)
+    if arr.flags.f_contiguous:
+        out.view.T.copy_(torch.from_numpy(arr.T))
+    else:
+        # row-major host data: upload as-is, transpose on the device
+        host = torch.from_numpy(np.ascontiguousarray(arr))
+        out.view.copy_(host.to(device))
+    return out
+
+
+def as_device_vector(v, device, n=None, name="v"):
+    if isinstance(v, torch.Tensor):
+        t = v.to(device=device, dtype=torch.float64).reshape(-1).contiguous()
+    else:
+        t = torch.as_tensor(np.asarray(v, dtype=np.float64).reshape(-1)).to(device)
+    if n is not None and t.numel() != n:
+        raise ValueError(f"{name} has {t.numel()} entries, expected {n}")
+    return t

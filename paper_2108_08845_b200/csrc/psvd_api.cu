@@ -1,0 +1,439 @@
+// C ABI (include/psvd.h): context, workspace, pass planning and the update
+// orchestration.  Everything is enqueued on the caller's stream; nothing here
+// synchronizes with the host except psvd_read_status.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <algorithm>
+
+#include "../../include/psvd.h"
+#include "psvd_small.cuh"
+#include "psvd_tall.cuh"
+
+using namespace psvd;
+
+namespace {
+
+struct Buf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+constexpr int SMEM_LIMIT = 227 * 1024;
+
+}  // namespace
+
+struct psvd_ctx {
+  int device = 0;
+  int num_sms = 148;
+  std::string err;
+  int* d_status = nullptr;  // device status word
+  int* d_gate = nullptr;
+  int* h_status = nullptr;  // pinned
+  Buf partial, tiles, gram, eigws, wbuf, utu, tbuf, dvec, colmax;
+};
+
+namespace {
+
+int fail(psvd_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+int cuda_check(psvd_ctx* c, const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, PSVD_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+  return PSVD_OK;
+}
+
+// Grow-only workspace.  Growth synchronizes the device (rare; warm-up sizes it).
+int ensure(psvd_ctx* c, Buf& b, size_t bytes) {
+  if (b.bytes >= bytes) return PSVD_OK;
+  if (b.ptr) {
+    cudaDeviceSynchronize();
+    cudaFree(b.ptr);
+    b.ptr = nullptr;
+    b.bytes = 0;
+  }
+  size_t want = std::max<size_t>(bytes, 4096);
+  if (cudaMalloc(&b.ptr, want) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, PSVD_ECUDA, "workspace allocation of %zu bytes failed", want);
+  }
+  b.bytes = want;
+  return PSVD_OK;
+}
+
+inline int rup(int x, int m) { return (x + m - 1) / m * m; }
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int check_mat(psvd_ctx* c, const char* name, const double* p, int64_t ld, int64_t M, int cols) {
+  if (cols == 0) return PSVD_OK;
+  if (p == nullptr) return fail(c, PSVD_EINVAL, "%s is null", name);
+  if (ld < M) return fail(c, PSVD_EINVAL, "%s: leading dimension %lld < rows %lld", name, (long long)ld, (long long)M);
+  if (ld % 2 != 0) return fail(c, PSVD_EINVAL, "%s: leading dimension %lld must be even", name, (long long)ld);
+  if (!aligned16(p)) return fail(c, PSVD_EINVAL, "%s: base pointer must be 16-byte aligned", name);
+  return PSVD_OK;
+}
+
+// A planned tall pass: params + reduce map + grid.
+struct Pass {
+  TallParams p;
+  ReduceMap map;
+  int grid = 0;
+  int NB = 0;
+};
+
+// Fill the warp plans / reduce map for a tile list (I <= J, 32-col blocks of [P | Y]).
+int plan_tiles(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& tiles) {
+  const int nt = (int)tiles.size();
+  memset(ps.p.plan, 0, sizeof(ps.p.plan));
+  memset(&ps.map, 0, sizeof(ps.map));
+  if (nt == 0) {
+    ps.p.nslices = 1;
+    return PSVD_OK;
+  }
+  if (nt > MAX_OUT_TILES) return fail(c, PSVD_EINVAL, "too many Gram tiles (%d)", nt);
+  const int nwarp_needed = (nt + 1) / 2;
+  const int nslices = (nwarp_needed + NWARP - 1) / NWARP;
+  if (nslices > MAX_SLICES) return fail(c, PSVD_EINVAL, "panel too wide (%d tiles)", nt);
+  ps.p.nslices = nslices;
+  const int per = (nt + nslices - 1) / nslices;
+  ps.map.nout = nt;
+  for (int s = 0; s < nslices; ++s) {
+    const int t0 = s * per, t1 = std::min(nt, t0 + per);
+    const int ns = t1 - t0;
+    if (ns <= 0) continue;
+    if (ns >= NWARP) {
+      for (int w = 0; w < NWARP; ++w) {
+        WarpPlan& wp = ps.p.plan[s][w];
+        wp.ksplit = 1;
+        wp.kpart = 0;
+        for (int t = 0; t < 2; ++t) {
+          const int li = w + t * NWARP;
+          if (li < ns) {
+            wp.ti[wp.ntile] = (signed char)tiles[t0 + li].first;
+            wp.tj[wp.ntile] = (signed char)tiles[t0 + li].second;
+            const int o = t0 + li;
+            ps.map.src[o][ps.map.nsrc[o]++] = (unsigned char)(s * SLOTS + w * 2 + wp.ntile);
+            wp.ntile++;
+          }
+        }
+      }
+    } else {
+      int ksplit = 1;
+      while (ksplit * 2 * ns <= NWARP) ksplit *= 2;
+      for (int w = 0; w < ns * ksplit; ++w) {
+        WarpPlan& wp = ps.p.plan[s][w];
+        const int li = w % ns;
+        wp.ksplit = (unsigned char)ksplit;
+        wp.kpart = (unsigned char)(w / ns);
+        wp.ti[0] = (signed char)tiles[t0 + li].first;
+        wp.tj[0] = (signed char)tiles[t0 + li].second;
+        wp.ntile = 1;
+        const int o = t0 + li;
+        ps.map.src[o][ps.map.nsrc[o]++] = (unsigned char)(s * SLOTS + w * 2);
+      }
+    }
+  }
+  for (int o = 0; o < nt; ++o) ps.map.out_id[o] = (short)(tiles[o].first * ps.NB + tiles[o].second);
+  return PSVD_OK;
+}
+
+// Common pass setup.  segs: panel segments; w/W: optional Y = P[:, wlo:wlo+wk] * W.
+int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, int wlo, int wk, int w,
+              const double* W, int64_t ldw, bool gram_pp, bool gram_yy, bool gram_py) {
+  memset(&ps.p, 0, sizeof(ps.p));
+  TallParams& p = ps.p;
+  p.M = M;
+  p.nseg = (int)segs.size();
+  int np = 0;
+  for (size_t i = 0; i < segs.size(); ++i) {
+    p.seg[i] = segs[i];
+    np += segs[i].ncols;
+  }
+  p.np = np;
+  int np_pad = rup(std::max(np, 1), 32);
+  if (w > 0) np_pad = std::max(np_pad, rup(wlo + rup(wk, 4), 32));
+  p.np_pad = np_pad;
+  p.W = W;
+  p.ldw = ldw;
+  p.wlo = wlo;
+  p.wk = wk;
+  p.w = w;
+  p.w_pad = w > 0 ? rup(w, 8) : 0;
+  if (w > MAX_W) return fail(c, PSVD_EINVAL, "Y width %d exceeds %d", w, MAX_W);
+  // stage height: 32 rows unless the smem budget forces 16
+  p.ks = 32;
+  if (tall_smem_bytes(32, np_pad, wk, w) > (size_t)SMEM_LIMIT) p.ks = 16;
+  if (tall_smem_bytes(p.ks, np_pad, wk, w) > (size_t)SMEM_LIMIT)
+    return fail(c, PSVD_EINVAL, "panel of %d columns (+%d) does not fit shared memory", np, w);
+  const int NBp = np_pad / 32, NBy = w > 0 ? rup(w, 32) / 32 : 0;
+  ps.NB = NBp + NBy;
+  std::vector<std::pair<int, int>> tiles;
+  if (gram_pp)
+    for (int I = 0; I < NBp; ++I)
+      for (int J = I; J < NBp; ++J) tiles.push_back({I, J});
+  if (gram_py)
+    for (int I = 0; I < NBp; ++I)
+      for (int J = 0; J < NBy; ++J) tiles.push_back({I, NBp + J});
+  if (gram_yy)
+    for (int I = 0; I < NBy; ++I)
+      for (int J = I; J < NBy; ++J) tiles.push_back({NBp + I, NBp + J});
+  int rc = plan_tiles(c, ps, tiles);
+  if (rc) return rc;
+  // grid: one CTA per SM (1 CTA/SM by smem), chunks of 32-row multiples
+  const int64_t stages32 = (M + 31) / 32;
+  int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(stages32, c->num_sms / p.nslices));
+  int64_t rows = (stages32 + nchunks - 1) / nchunks * 32;
+  nchunks = (M + rows - 1) / rows;
+  p.rows_per_cta = rows;
+  ps.grid = (int)(nchunks * p.nslices);
+  ps.map.nchunks = (int)nchunks;
+  ps.map.nslices = p.nslices;
+  if (!tiles.empty()) {
+    int rc2 = ensure(c, c->partial, sizeof(double) * (size_t)ps.grid * SLOTS * 1024);
+    if (rc2) return rc2;
+    rc2 = ensure(c, c->tiles, sizeof(double) * (size_t)ps.NB * ps.NB * 1024);
+    if (rc2) return rc2;
+    p.partial = (double*)c->partial.ptr;
+  }
+  return PSVD_OK;
+}
+
+int run_pass(psvd_ctx* c, Pass& ps, cudaStream_t st) {
+  launch_tall(ps.p, ps.grid, st);
+  int rc = cuda_check(c, "tall pass");
+  if (rc) return rc;
+  if (ps.map.nout > 0) {
+    launch_tall_reduce((const double*)c->partial.ptr, ps.map, (double*)c->tiles.ptr, st);
+    rc = cuda_check(c, "tall reduce");
+  }
+  return rc;
+}
+
+__global__ void make_dvec_kernel(const double* __restrict__ sigma, double ff, int Kc, int n, double* d) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) d[i] = i < Kc ? ff * sigma[i] : 1.0;
+}
+
+int make_dvec(psvd_ctx* c, const double* sigma, double ff, int Kc, int n, cudaStream_t st) {
+  int rc = ensure(c, c->dvec, sizeof(double) * (size_t)std::max(n, 1));
+  if (rc) return rc;
+  make_dvec_kernel<<<(n + 255) / 256, 256, 0, st>>>(sigma, ff, Kc, n, (double*)c->dvec.ptr);
+  return cuda_check(c, "dvec");
+}
+
+std::vector<Seg> panel(const double* U, int64_t ldu, int Kc, const double* A, int64_t lda, int B) {
+  std::vector<Seg> s;
+  if (Kc > 0) s.push_back(Seg{U, ldu, Kc, 0});
+  if (B > 0) s.push_back(Seg{A, lda, B, 0});
+  return s;
+}
+
+__global__ void sum_ordered_kernel(const double* __restrict__ parts, int P, int64_t count, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double s = 0.0;
+  for (int r = 0; r < P; ++r) s += parts[(int64_t)r * count + i];
+  out[i] = s;
+}
+
+// log(1 + exp(v)) exactly as numpy's logaddexp(0, v) branches (npy_logaddexp)
+__device__ double logaddexp0(double v) {
+  if (v == 0.0) return 0.6931471805599453;  // LOGE2
+  return v > 0.0 ? v + log1p(exp(-v)) : log1p(exp(v));
+}
+
+__global__ void burgers_kernel(double* __restrict__ out, int64_t ldo, int64_t row0, int64_t rows, int64_t grid,
+                               int col0, int cols, int n_snap, double length, double t_final, double re) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (i >= rows || j >= cols) return;
+  const int64_t gi = row0 + i;
+  const int gj = col0 + j;
+  // numpy.linspace: fl(k * step) + start, last sample pinned to stop
+  const double dx = length / (double)(grid - 1);
+  const double x = (gi == grid - 1) ? length : (double)gi * dx;
+  const double dt = n_snap > 1 ? t_final / (double)(n_snap - 1) : 0.0;
+  const double t = (n_snap > 1 && gj == n_snap - 1) ? t_final : (double)gj * dt;
+  const double expo = 0.5 * (log1p(t) - re / 8.0) + re * x * x / (4.0 * (t + 1.0));
+  out[(int64_t)j * ldo + i] = (x / (t + 1.0)) * exp(-logaddexp0(expo));
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+
+extern "C" {
+
+int psvd_version(void) { return 1; }
+
+int psvd_create(int device, psvd_ctx** out) {
+  if (!out) return PSVD_EINVAL;
+  *out = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    cudaGetLastError();
+    return PSVD_ECUDA;
+  }
+  psvd_ctx* c = new psvd_ctx();
+  c->device = device;
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  if (cudaMalloc(&c->d_status, 2 * sizeof(int)) != cudaSuccess || cudaMallocHost(&c->h_status, sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    delete c;
+    return PSVD_ECUDA;
+  }
+  c->d_gate = c->d_status + 1;
+  cudaMemset(c->d_status, 0, 2 * sizeof(int));
+  cudaDeviceSynchronize();
+  *out = c;
+  return PSVD_OK;
+}
+
+int psvd_destroy(psvd_ctx* c) {
+  if (!c) return PSVD_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  Buf* bufs[] = {&c->partial, &c->tiles, &c->gram, &c->eigws, &c->wbuf, &c->utu, &c->tbuf, &c->dvec, &c->colmax};
+  for (Buf* b : bufs)
+    if (b->ptr) cudaFree(b->ptr);
+  cudaFree(c->d_status);
+  cudaFreeHost(c->h_status);
+  delete c;
+  return PSVD_OK;
+}
+
+const char* psvd_last_error(psvd_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int psvd_read_status(psvd_ctx* c, int* status, int reset, void* stream) {
+  if (!c || !status) return PSVD_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemcpyAsync(c->h_status, c->d_status, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (reset) cudaMemsetAsync(c->d_status, 0, sizeof(int), st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check(c, "read status");
+  *status = *c->h_status;
+  return cuda_check(c, "read status");
+}
+
+int psvd_gram(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const double* sigma, double ff, int Kc,
+              const double* A, int64_t lda, int B, double* G, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (M < 1 || B < 0 || Kc < 0 || Kc + B < 1) return fail(c, PSVD_EINVAL, "bad shape M=%lld Kc=%d B=%d", (long long)M, Kc, B);
+  int rc;
+  if ((rc = check_mat(c, "U", U, ldu, M, Kc)) || (rc = check_mat(c, "A", A, lda, M, B))) return rc;
+  if (Kc > 0 && sigma == nullptr) return fail(c, PSVD_EINVAL, "sigma is null");
+  if (G == nullptr) return fail(c, PSVD_EINVAL, "G is null");
+  const int n = Kc + B;
+  Pass ps;
+  if ((rc = plan_pass(c, ps, M, panel(U, ldu, Kc, A, lda, B), 0, 0, 0, nullptr, 0, true, false, false))) return rc;
+  if ((rc = run_pass(c, ps, st))) return rc;
+  if ((rc = make_dvec(c, sigma, ff, Kc, n, st))) return rc;
+  launch_extract_sym((const double*)c->tiles.ptr, ps.NB, 0, n, (const double*)c->dvec.ptr, G, st);
+  return cuda_check(c, "extract gram");
+}
+
+int psvd_core_eig(psvd_ctx* c, const double* G, int n, const double* sigma_in, double ff, int Kc, int K, double* W,
+                  double* sigma_out, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 1 || K < 1 || K > n || Kc < 0 || Kc > n) return fail(c, PSVD_EINVAL, "bad core shape n=%d K=%d Kc=%d", n, K, Kc);
+  if (!G || !W || !sigma_out || (Kc > 0 && !sigma_in)) return fail(c, PSVD_EINVAL, "null pointer");
+  if (K > 1024) return fail(c, PSVD_EINVAL, "K=%d too large", K);
+  int rc;
+  if ((rc = make_dvec(c, sigma_in, ff, Kc, n, st))) return rc;
+  if ((rc = ensure(c, c->eigws, sizeof(double) * eig_workspace_doubles(n, K)))) return rc;
+  launch_eig_topk(G, n, K, (const double*)c->dvec.ptr, W, sigma_out, (double*)c->eigws.ptr, c->d_status, st);
+  return cuda_check(c, "core eig");
+}
+
+int psvd_recompose(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, int Kc, const double* A, int64_t lda, int B,
+                   const double* W, int K, double* U_out, int64_t ldo, double* UtU, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if (M < 1 || K < 1 || Kc + B < 1) return fail(c, PSVD_EINVAL, "bad shape");
+  if ((rc = check_mat(c, "U", U, ldu, M, Kc)) || (rc = check_mat(c, "A", A, lda, M, B)) ||
+      (rc = check_mat(c, "U_out", U_out, ldo, M, K)))
+    return rc;
+  const int n = Kc + B;
+  Pass ps;
+  if ((rc = plan_pass(c, ps, M, panel(U, ldu, Kc, A, lda, B), 0, n, K, W, n, false, UtU != nullptr, false))) return rc;
+  ps.p.Yout = U_out;
+  ps.p.ldy = ldo;
+  if ((rc = run_pass(c, ps, st))) return rc;
+  if (UtU) {
+    launch_extract_sym((const double*)c->tiles.ptr, ps.NB, ps.p.np_pad, K, nullptr, UtU, st);
+    rc = cuda_check(c, "extract UtU");
+  }
+  return rc;
+}
+
+int psvd_drift_rescue(psvd_ctx* c, int64_t M, double* U, int64_t ldu, int K, const double* UtU, double* sigma,
+                      double tol, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if ((rc = check_mat(c, "U", U, ldu, M, K))) return rc;
+  if (K > MAX_W) return fail(c, PSVD_EINVAL, "K=%d too large for the rescue pass", K);
+  if ((rc = ensure(c, c->tbuf, sizeof(double) * (size_t)K * K))) return rc;
+  launch_drift_check(UtU, K, tol, sigma, (double*)c->tbuf.ptr, c->d_gate, c->d_status, st);
+  if ((rc = cuda_check(c, "drift check"))) return rc;
+  Pass ps;
+  if ((rc = plan_pass(c, ps, M, {Seg{U, ldu, K, 0}}, 0, K, K, (const double*)c->tbuf.ptr, K, false, false, false)))
+    return rc;
+  ps.p.Yout = U;  // in place: every stage is fully staged in smem before its rows are rewritten
+  ps.p.ldy = ldu;
+  ps.p.gate = c->d_gate;
+  return run_pass(c, ps, st);
+}
+
+int psvd_stream_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const double* sigma, double ff, int Kc,
+                       const double* A, int64_t lda, int B, int K, int rescue, double* U_out, int64_t ldo,
+                       double* sigma_out, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  const int n = Kc + B;
+  if (K < 1 || K > n) return fail(c, PSVD_EINVAL, "K=%d must be in [1, %d]", K, n);
+  int rc;
+  if ((rc = ensure(c, c->gram, sizeof(double) * (size_t)n * n))) return rc;
+  if ((rc = ensure(c, c->wbuf, sizeof(double) * (size_t)n * K))) return rc;
+  if ((rc = ensure(c, c->utu, sizeof(double) * (size_t)K * K))) return rc;
+  double* G = (double*)c->gram.ptr;
+  double* W = (double*)c->wbuf.ptr;
+  double* UtU = rescue ? (double*)c->utu.ptr : nullptr;
+  if ((rc = psvd_gram(c, M, U, ldu, sigma, ff, Kc, A, lda, B, G, stream))) return rc;
+  if ((rc = psvd_core_eig(c, G, n, sigma, ff, Kc, K, W, sigma_out, stream))) return rc;
+  if ((rc = psvd_recompose(c, M, U, ldu, Kc, A, lda, B, W, K, U_out, ldo, UtU, stream))) return rc;
+  if (rescue) rc = psvd_drift_rescue(c, M, U_out, ldo, K, UtU, sigma_out, 1e-8, stream);
+  return rc;
+}
+
+int psvd_sum_ordered(psvd_ctx* c, const double* parts, int P, int64_t count, double* out, void* stream) {
+  if (!c || !parts || !out || P < 1 || count < 0) return fail(c, PSVD_EINVAL, "bad sum_ordered args");
+  if (count == 0) return PSVD_OK;
+  sum_ordered_kernel<<<(unsigned)((count + 255) / 256), 256, 0, (cudaStream_t)stream>>>(parts, P, count, out);
+  return cuda_check(c, "sum ordered");
+}
+
+int psvd_burgers(psvd_ctx* c, double* out, int64_t ldo, int64_t row0, int64_t rows, int64_t grid, int col0, int cols,
+                 int n_snap, double length, double t_final, double reynolds, void* stream) {
+  if (!c || !out || rows < 0 || cols < 0 || grid < 2 || n_snap < 1 || ldo < rows || row0 < 0 || row0 + rows > grid ||
+      col0 < 0 || col0 + cols > n_snap)
+    return fail(c, PSVD_EINVAL, "bad burgers args");
+  if (rows == 0 || cols == 0) return PSVD_OK;
+  dim3 g((unsigned)((rows + 255) / 256), (unsigned)cols);
+  burgers_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(out, ldo, row0, rows, grid, col0, cols, n_snap, length, t_final,
+                                                       reynolds);
+  return cuda_check(c, "burgers");
+}
+
+}  // extern "C"

@@ -1,0 +1,59 @@
+// Shared device helpers for the streaming-SVD kernels (sm_100a, fp64).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/psvd.h"
+
+#define PSVD_DEV __device__ __forceinline__
+
+// FP64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col).  On sm_100a this is
+// SASS DMMA.8x8x4 (tcgen05 has no f64 kind — SURVEY F7).  Fragment map
+// (verified on B200, profiles/fp64_peaks_r01.jsonl): lane = 4*g + t,
+//   a = A[g][t], b = B[t][g], d{0,1} = D[g][2t + {0,1}].
+PSVD_DEV void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+// 16-byte global->shared async copy with zero fill of the bytes past src_bytes.
+PSVD_DEV void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+PSVD_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+PSVD_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+PSVD_DEV double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+PSVD_DEV double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide sum with a caller-provided scratch of >= 32 doubles; result on all threads.
+PSVD_DEV double block_sum(double v, double* scratch) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) scratch[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = lane < nw ? scratch[lane] : 0.0;
+    r = warp_sum(r);
+    if (lane == 0) scratch[0] = r;
+  }
+  __syncthreads();
+  r = scratch[0];
+  __syncthreads();
+  return r;
+}
+
+// Status word bits (PSVD_ST_*) are defined in include/psvd.h.

@@ -1,0 +1,493 @@
+// Small-core kernels (one CTA each).  See psvd_small.cuh.
+//
+// The deterministic streaming update needs the top-K singular triplets of the
+// (K+B) x (K+B) core.  We reach them through the Gram G = C^T C of the panel
+// C = [ff U S | A] (G = R^T R for the reference's R, streaming.py:98-99):
+//   1. Householder tridiagonalization of G (packed lower triangle in smem),
+//   2. top-K eigenvalues by 33-point multisection of Sturm counts (one warp
+//      per eigenvalue),
+//   3. eigenvectors of T by the twisted (forward/backward LDL^T) factorization
+//      at the index of minimal |gamma| (one thread per eigenvalue), re-
+//      orthogonalized (MGS twice) inside clusters of close eigenvalues,
+//   4. back-transformation through the Householder reflectors,
+//   5. R = chol(G + delta I) and the reference's sign rule on U_R = R V S^-1
+//      (linalg.py:81-91), giving W = V S^-1 diag(sign) for the recompose.
+#include <cfloat>
+#include "psvd_small.cuh"
+
+namespace psvd {
+
+__device__ __forceinline__ int pidx(int n, int r, int c) {  // r >= c, column-packed lower
+  return c * n - (c * (c - 1)) / 2 + (r - c);
+}
+
+// ---------------------------------------------------------------- extraction
+
+__global__ void extract_sym_kernel(const double* __restrict__ tiles, int NB, int c0, int n,
+                                   const double* __restrict__ d, double* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n * n) return;
+  const int i = (int)(idx % n), j = (int)(idx / n);
+  int gi = c0 + i, gj = c0 + j;
+  if (gi > gj) { const int t = gi; gi = gj; gj = t; }  // always read the upper element: exact symmetry
+  const int I = gi >> 5, J = gj >> 5;
+  double v = tiles[((size_t)I * NB + J) * 1024 + (gi & 31) * 32 + (gj & 31)];
+  if (d != nullptr) v = d[i] * d[j] * v;
+  out[idx] = v;
+}
+
+__global__ void extract_rect_kernel(const double* __restrict__ tiles, int NB, int r0, int nr, int c0, int nc,
+                                    const double* __restrict__ d, double* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)nr * nc) return;
+  const int i = (int)(idx % nr), j = (int)(idx / nr);
+  const int gi = r0 + i, gj = c0 + j;
+  const int I = gi >> 5, J = gj >> 5;
+  double v = tiles[((size_t)I * NB + J) * 1024 + (gi & 31) * 32 + (gj & 31)];
+  if (d != nullptr) v = d[i] * v;
+  out[idx] = v;
+}
+
+void launch_extract_sym(const double* tiles, int NB, int c0, int n, const double* d, double* out,
+                        cudaStream_t st) {
+  const int64_t tot = (int64_t)n * n;
+  extract_sym_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(tiles, NB, c0, n, d, out);
+}
+
+void launch_extract_rect(const double* tiles, int NB, int r0, int nr, int c0, int nc, const double* d,
+                         double* out, cudaStream_t st) {
+  const int64_t tot = (int64_t)nr * nc;
+  extract_rect_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(tiles, NB, r0, nr, c0, nc, d, out);
+}
+
+// ---------------------------------------------------------------- eigensolver
+
+size_t eig_workspace_doubles(int n, int K) {
+  return (size_t)n * (n + 1) / 2 + (size_t)n * K + 2 * (size_t)n * K + 64;
+}
+
+__device__ __forceinline__ double fix_pivot(double q, double pivmin) {
+  return fabs(q) < pivmin ? (q < 0.0 ? -pivmin : pivmin) : q;
+}
+
+// deterministic pseudo-random start vector entry in (-1, 1)
+__device__ __forceinline__ double prand(unsigned a, unsigned b) {
+  unsigned h = a * 0x9E3779B1u ^ (b + 0x7F4A7C15u) * 0x85EBCA77u;
+  h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12; h *= 0x297A2D39u; h ^= h >> 15;
+  return ((double)h / 4294967296.0) * 2.0 - 1.0;
+}
+
+template <bool SMEM>
+__global__ void __launch_bounds__(SMALL_THREADS, 1)
+eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __restrict__ dscale,
+                double* __restrict__ W, double* __restrict__ sigma_out, double* __restrict__ ws,
+                int* __restrict__ status) {
+  extern __shared__ double sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nthr = blockDim.x, nwarps = nthr >> 5;
+  const unsigned full = 0xffffffffu;
+  const size_t npk = (size_t)n * (n + 1) / 2;
+  double* Lp = SMEM ? sm : ws;
+  double* vec = SMEM ? sm + npk : sm;       // small vectors always in smem
+  double* v = vec;
+  double* p = v + n;
+  double* dd = p + n;
+  double* ee = dd + n;
+  double* tau = ee + n;
+  double* e2 = tau + n;
+  double* lam = e2 + n;                     // K
+  double* red = lam + K;                    // 64 scratch
+  int* clus = reinterpret_cast<int*>(red + 64);  // K cluster leaders
+  double* Z = ws + npk;                     // n x K (col-major, ld n)
+  double* Dp = Z + (size_t)n * K;           // K x n
+  double* Dm = Dp + (size_t)n * K;          // K x n
+
+  // ---- A: load the lower triangle
+  for (int64_t idx = tid; idx < (int64_t)n * n; idx += nthr) {
+    const int i = (int)(idx % n), j = (int)(idx / n);
+    if (i >= j) Lp[pidx(n, i, j)] = G[idx];
+  }
+  __syncthreads();
+
+  // ---- B: Householder tridiagonalization (lower, dsytd2-style)
+  for (int j = 0; j + 2 < n; ++j) {
+    const int m = n - j - 1;
+    const int cj = pidx(n, j, j);
+    double part = 0.0;
+    for (int i = 1 + tid; i < m; i += nthr) {
+      const double x = Lp[cj + 1 + i];
+      part += x * x;
+    }
+    const double xn2 = block_sum(part, red);
+    const double alpha = Lp[cj + 1];
+    if (xn2 == 0.0) {
+      if (tid == 0) { tau[j] = 0.0; ee[j] = alpha; dd[j] = Lp[cj]; }
+      __syncthreads();
+      continue;
+    }
+    const double beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+    const double tj = (beta - alpha) / beta;
+    const double scl = 1.0 / (alpha - beta);
+    for (int i = tid; i < m; i += nthr) v[i] = (i == 0) ? 1.0 : Lp[cj + 1 + i] * scl;
+    if (tid == 0) { tau[j] = tj; ee[j] = beta; dd[j] = Lp[cj]; }
+    __syncthreads();
+    for (int i = 1 + tid; i < m; i += nthr) Lp[cj + 1 + i] = v[i];
+    // p = tau * A22 * v, four threads per row (fixed order -> deterministic)
+    for (int base = 0; base < m; base += nthr / 4) {
+      const int row = base + (tid >> 2), q4 = tid & 3;
+      double s = 0.0;
+      if (row < m) {
+        const int gr = j + 1 + row;
+        for (int k = q4; k < m; k += 4) {
+          const int gk = j + 1 + k;
+          const double a = (k <= row) ? Lp[pidx(n, gr, gk)] : Lp[pidx(n, gk, gr)];
+          s = fma(a, v[k], s);
+        }
+      }
+      s += __shfl_xor_sync(full, s, 1);
+      s += __shfl_xor_sync(full, s, 2);
+      if (row < m && q4 == 0) p[row] = tj * s;
+    }
+    __syncthreads();
+    part = 0.0;
+    for (int i = tid; i < m; i += nthr) part += p[i] * v[i];
+    const double pv = block_sum(part, red);
+    const double kc = -0.5 * tj * pv;
+    for (int i = tid; i < m; i += nthr) p[i] = fma(kc, v[i], p[i]);  // w
+    __syncthreads();
+    for (int c = warp; c < m; c += nwarps) {
+      const int b0 = pidx(n, j + 1 + c, j + 1 + c);
+      const double vc = v[c], wc = p[c];
+      for (int r = c + lane; r < m; r += 32) Lp[b0 + (r - c)] -= v[r] * wc + p[r] * vc;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (n >= 2) {
+      dd[n - 2] = Lp[pidx(n, n - 2, n - 2)];
+      ee[n - 2] = Lp[pidx(n, n - 1, n - 2)];
+      tau[n - 2] = 0.0;
+    }
+    dd[n - 1] = Lp[pidx(n, n - 1, n - 1)];
+    ee[n - 1] = 0.0;
+    tau[n - 1] = 0.0;
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += nthr) e2[i] = (i + 1 < n) ? ee[i] * ee[i] : 0.0;
+  __syncthreads();
+
+  // ---- C: Gerschgorin bounds, multisection bisection (one warp per eigenvalue)
+  double glo = DBL_MAX, ghi = -DBL_MAX, emax2 = 0.0;
+  for (int i = lane; i < n; i += 32) {
+    const double r = (i > 0 ? fabs(ee[i - 1]) : 0.0) + (i + 1 < n ? fabs(ee[i]) : 0.0);
+    glo = fmin(glo, dd[i] - r);
+    ghi = fmax(ghi, dd[i] + r);
+    emax2 = fmax(emax2, e2[i]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    glo = fmin(glo, __shfl_xor_sync(full, glo, o));
+    ghi = fmax(ghi, __shfl_xor_sync(full, ghi, o));
+    emax2 = fmax(emax2, __shfl_xor_sync(full, emax2, o));
+  }
+  const double tnorm = fmax(fabs(glo), fabs(ghi));
+  const double pivmin = DBL_MIN * fmax(1.0, emax2);
+  glo -= 2.0 * DBL_EPSILON * tnorm * n + 2.0 * pivmin;
+  ghi += 2.0 * DBL_EPSILON * tnorm * n + 2.0 * pivmin;
+  for (int k = warp; k < K; k += nwarps) {
+    const int aidx = n - 1 - k;  // ascending index of the k-th largest
+    double lo = glo, hi = ghi;
+    for (int it = 0; it < 80; ++it) {
+      const double x = lo + (hi - lo) * ((double)(lane + 1) / 33.0);
+      double q = fix_pivot(dd[0] - x, pivmin);
+      int cnt = q < 0.0;
+      for (int i = 1; i < n; ++i) {
+        q = fix_pivot((dd[i] - x) - e2[i - 1] / q, pivmin);
+        cnt += q < 0.0;
+      }
+      const unsigned mask = __ballot_sync(full, cnt > aidx);
+      const int f = mask ? __ffs(mask) - 1 : 32;
+      const double xf = __shfl_sync(full, x, f & 31);
+      const double xb = __shfl_sync(full, x, (f + 31) & 31);
+      const double nhi = f < 32 ? xf : hi;
+      const double nlo = f > 0 ? xb : lo;
+      const bool stall = (nhi == hi && nlo == lo);
+      lo = nlo;
+      hi = nhi;
+      if (stall || hi - lo <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi)) + pivmin) break;
+    }
+    if (lane == 0) lam[k] = 0.5 * (lo + hi);
+  }
+  __syncthreads();
+
+  // ---- D: twisted-factorization eigenvectors of T (one thread per eigenvalue)
+  for (int k = tid; k < K; k += nthr) {
+    const double lk = lam[k];
+    double* dp = Dp + (size_t)k * n;
+    double* dm = Dm + (size_t)k * n;
+    double q = fix_pivot(dd[0] - lk, pivmin);
+    dp[0] = q;
+    for (int i = 1; i < n; ++i) {
+      q = fix_pivot((dd[i] - lk) - e2[i - 1] / q, pivmin);
+      dp[i] = q;
+    }
+    q = fix_pivot(dd[n - 1] - lk, pivmin);
+    dm[n - 1] = q;
+    for (int i = n - 2; i >= 0; --i) {
+      q = fix_pivot((dd[i] - lk) - e2[i] / q, pivmin);
+      dm[i] = q;
+    }
+    int r = 0;
+    double gbest = DBL_MAX;
+    for (int i = 0; i < n; ++i) {
+      const double gm = fabs(dp[i] + dm[i] - (dd[i] - lk));
+      if (gm < gbest) { gbest = gm; r = i; }
+    }
+    double* z = Z + (size_t)k * n;
+    z[r] = 1.0;
+    for (int i = r - 1; i >= 0; --i) z[i] = -ee[i] * z[i + 1] / dp[i];
+    for (int i = r + 1; i < n; ++i) z[i] = -ee[i - 1] * z[i - 1] / dm[i];
+  }
+  // cluster leaders: consecutive eigenvalues closer than 1e-3 ||T|| (dstein's ORTOL)
+  if (tid == 0) {
+    int lead = 0;
+    for (int k = 0; k < K; ++k) {
+      if (k > 0 && lam[k - 1] - lam[k] > 1e-3 * tnorm) lead = k;
+      clus[k] = lead;
+    }
+  }
+  __syncthreads();
+
+  // ---- E: normalize; MGS (twice) inside clusters; rescue collapsed vectors
+  for (int k0 = warp; k0 < K; k0 += nwarps) {
+    if (clus[k0] != k0) continue;  // this warp owns the cluster led by k0
+    int kend = k0 + 1;
+    while (kend < K && clus[kend] == k0) ++kend;
+    for (int k = k0; k < kend; ++k) {
+      double* z = Z + (size_t)k * n;
+      for (int attempt = 0; attempt < 3; ++attempt) {
+        double s = 0.0;
+        for (int i = lane; i < n; i += 32) s += z[i] * z[i];
+        double nrm = sqrt(warp_sum(s));
+        for (int i = lane; i < n; i += 32) z[i] /= nrm;
+        __syncwarp();
+        for (int pass = 0; pass < 2; ++pass) {
+          for (int q2 = k0; q2 < k; ++q2) {
+            const double* zq = Z + (size_t)q2 * n;
+            double c = 0.0;
+            for (int i = lane; i < n; i += 32) c += zq[i] * z[i];
+            c = warp_sum(c);
+            for (int i = lane; i < n; i += 32) z[i] -= c * zq[i];
+            __syncwarp();
+          }
+        }
+        s = 0.0;
+        for (int i = lane; i < n; i += 32) s += z[i] * z[i];
+        nrm = sqrt(warp_sum(s));
+        if (nrm > 0.5) {
+          for (int i = lane; i < n; i += 32) z[i] /= nrm;
+          __syncwarp();
+          break;
+        }
+        // collapsed (degenerate cluster): two steps of LDL^T inverse iteration from a
+        // pseudo-random start, re-orthogonalized on the next attempt
+        const double* dp = Dp + (size_t)k * n;
+        for (int i = lane; i < n; i += 32) z[i] = prand(k * 7919u + attempt, i);
+        __syncwarp();
+        for (int step = 0; step < 2; ++step) {
+          if (lane == 0) {
+            for (int i = 1; i < n; ++i) z[i] -= (ee[i - 1] / dp[i - 1]) * z[i - 1];
+            for (int i = 0; i < n; ++i) z[i] /= dp[i];
+            for (int i = n - 2; i >= 0; --i) z[i] -= (ee[i] / dp[i]) * z[i + 1];
+            double mx = 0.0;
+            for (int i = 0; i < n; ++i) mx = fmax(mx, fabs(z[i]));
+            if (mx > 0.0) for (int i = 0; i < n; ++i) z[i] /= mx;
+          }
+          __syncwarp();
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- F: back-transform Z <- H_0 ... H_{n-3} Z  (warp per column, no block sync)
+  for (int k = warp; k < K; k += nwarps) {
+    double* z = Z + (size_t)k * n;
+    for (int j = n - 3; j >= 0; --j) {
+      const double tj = tau[j];
+      if (tj == 0.0) continue;
+      const int cj = pidx(n, j, j);
+      double s = 0.0;
+      for (int i = j + 2 + lane; i < n; i += 32) s += Lp[cj + (i - j)] * z[i];
+      s = warp_sum(s) + z[j + 1];
+      s *= tj;
+      if (lane == 0) z[j + 1] -= s;
+      for (int i = j + 2 + lane; i < n; i += 32) z[i] -= s * Lp[cj + (i - j)];
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+
+  // ---- G: R = chol(G + delta I), delta = 10 n eps max(diag G).
+  // The reference's R is Householder's (well-determined only in the rows
+  // where |R_ii| >> sqrt(eps)|C|); an unshifted Cholesky of the Gram turns the
+  // remaining rows into O(1) garbage that can win the sign rule's argmax.
+  // The shift bounds those rows by ~sqrt(delta) (their true U_R entries are
+  // below ~1e-7 kappa_k anyway) and leaves the well-determined rows unchanged
+  // to O(delta / R_ii^2).
+  double dmax = 0.0;
+  for (int i = tid; i < n; i += nthr) dmax = fmax(dmax, G[(size_t)i * n + i]);
+  dmax = warp_max(dmax);
+  if (lane == 0) red[warp] = dmax;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int w = 0; w < nwarps; ++w) m = fmax(m, red[w]);
+    red[40] = m;
+  }
+  __syncthreads();
+  const double delta = 10.0 * (double)n * DBL_EPSILON * red[40];
+  for (int64_t idx = tid; idx < (int64_t)n * n; idx += nthr) {
+    const int i = (int)(idx % n), j = (int)(idx / n);
+    if (i >= j) Lp[pidx(n, i, j)] = G[idx] + (i == j ? delta : 0.0);
+  }
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    const int ck = pidx(n, k, k);
+    const double piv = Lp[ck];
+    __syncthreads();
+    const bool ok = piv > 0.0;
+    const double rk = ok ? sqrt(piv) : 0.0;
+    for (int i = tid; i < n - k; i += nthr) Lp[ck + i] = ok ? (i == 0 ? rk : Lp[ck + i] / rk) : 0.0;
+    __syncthreads();
+    if (ok) {
+      for (int c = k + 1 + warp; c < n; c += nwarps) {
+        const int bc = pidx(n, c, c);
+        const double lck = Lp[ck + (c - k)];
+        for (int r = c + lane; r < n; r += 32) Lp[bc + (r - c)] -= Lp[ck + (r - k)] * lck;
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- H: sign rule on U_R = R V (R = L^T), weights, singular values
+  for (int k = warp; k < K; k += nwarps) {
+    const double* z = Z + (size_t)k * n;
+    double best_abs = -1.0, best_val = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const int ci = pidx(n, i, i);
+      double s = 0.0;
+      for (int jj = i + lane; jj < n; jj += 32) s += Lp[ci + (jj - i)] * z[jj];
+      s = warp_sum(s);
+      if (fabs(s) > best_abs) { best_abs = fabs(s); best_val = s; }
+    }
+    const double sg = best_val < 0.0 ? -1.0 : 1.0;
+    const double sk = sqrt(fmax(lam[k], 0.0));
+    const double inv = sk > 0.0 ? sg / sk : 0.0;
+    if (sk == 0.0 && lane == 0) atomicOr(status, PSVD_ST_RANKDEF);
+    for (int i = lane; i < n; i += 32) W[(size_t)k * n + i] = (dscale ? dscale[i] : 1.0) * z[i] * inv;
+    if (lane == 0) sigma_out[k] = sk;
+  }
+  if (tid == 0) {
+    for (int i = 0; i < n; ++i)
+      if (!isfinite(dd[i]) || !isfinite(G[(size_t)i * n + i])) { atomicOr(status, PSVD_ST_NONFINITE); break; }
+  }
+}
+
+void launch_eig_topk(const double* G, int n, int K, const double* dscale, double* W, double* sigma,
+                     double* ws, int* status, cudaStream_t st) {
+  const size_t vec = (size_t)6 * n + K + 64 + (K + 1) / 2 + 2;
+  if (n <= EIG_NMAX_SMEM) {
+    const size_t smem = ((size_t)n * (n + 1) / 2 + vec) * sizeof(double);
+    cudaFuncSetAttribute(eig_topk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    eig_topk_kernel<true><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status);
+  } else {
+    const size_t smem = vec * sizeof(double);
+    cudaFuncSetAttribute(eig_topk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    eig_topk_kernel<false><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status);
+  }
+}
+
+// ---------------------------------------------------------------- drift check / rescue
+
+__global__ void __launch_bounds__(1024, 1)
+drift_check_kernel(const double* __restrict__ UtU, int K, double tol, double* __restrict__ sigma,
+                   double* __restrict__ T, int* __restrict__ gate, int* __restrict__ status) {
+  extern __shared__ double sm[];
+  double* A = sm;               // K x K
+  double* X = A + K * K;        // K x K (inverse of rr)
+  double* vals = X + K * K;     // K
+  double* red = vals + K;       // 64
+  int* order = reinterpret_cast<int*>(red + 64);
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  double dev = 0.0;
+  for (int idx = tid; idx < K * K; idx += nthr) {
+    const double a = UtU[idx];
+    A[idx] = a;
+    const int i = idx % K, j = idx / K;
+    dev = fmax(dev, fabs(a - (i == j ? 1.0 : 0.0)));
+  }
+  dev = warp_max(dev);
+  if ((tid & 31) == 0) red[tid >> 5] = dev;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int w = 0; w < (nthr + 31) / 32; ++w) m = fmax(m, red[w]);
+    red[40] = m;
+  }
+  __syncthreads();
+  if (!(red[40] > tol)) {
+    if (tid == 0) *gate = 0;
+    return;
+  }
+  // Cholesky A = L L^T (upper rr = L^T), column by column
+  for (int k = 0; k < K; ++k) {
+    if (tid == 0) A[k * K + k] = sqrt(fmax(A[k * K + k], 0.0));
+    __syncthreads();
+    const double rk = A[k * K + k];
+    for (int i = k + 1 + tid; i < K; i += nthr) A[k * K + i] = rk > 0.0 ? A[k * K + i] / rk : 0.0;
+    __syncthreads();
+    for (int idx = tid; idx < K * K; idx += nthr) {
+      const int i = idx % K, j = idx / K;
+      if (j > k && i >= j) A[j * K + i] -= A[k * K + i] * A[k * K + j];
+    }
+    __syncthreads();
+  }
+  // X = rr^{-1}, rr upper with rr[i][j] = L[j][i] = A[i*K + j] (i <= j)
+  for (int j = tid; j < K; j += nthr) {
+    for (int i = K - 1; i >= 0; --i) {
+      double s = (i == j) ? 1.0 : 0.0;
+      for (int q = i + 1; q <= j; ++q) s -= A[i * K + q] * X[j * K + q];
+      const double d = A[i * K + i];
+      X[j * K + i] = (i <= j && d != 0.0) ? s / d : 0.0;
+    }
+  }
+  for (int k = tid; k < K; k += nthr) vals[k] = sigma[k] * fabs(A[k * K + k]);
+  __syncthreads();
+  if (tid == 0) {
+    for (int k = 0; k < K; ++k) order[k] = k;
+    for (int a = 1; a < K; ++a) {  // stable insertion sort, descending
+      const int oa = order[a];
+      int b = a - 1;
+      while (b >= 0 && vals[order[b]] < vals[oa]) { order[b + 1] = order[b]; --b; }
+      order[b + 1] = oa;
+    }
+    *gate = 1;
+    atomicOr(status, PSVD_ST_RESCUE);
+  }
+  __syncthreads();
+  for (int idx = tid; idx < K * K; idx += nthr) {
+    const int i = idx % K, c = idx / K;
+    T[(size_t)c * K + i] = X[order[c] * K + i];
+  }
+  for (int c = tid; c < K; c += nthr) sigma[c] = vals[order[c]];
+}
+
+void launch_drift_check(const double* UtU, int K, double tol, double* sigma, double* T, int* gate,
+                        int* status, cudaStream_t st) {
+  const size_t smem = (2 * (size_t)K * K + K + 64 + (K + 1) / 2 + 1) * sizeof(double);
+  cudaFuncSetAttribute(drift_check_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  drift_check_kernel<<<1, 1024, smem, st>>>(UtU, K, tol, sigma, T, gate, status);
+}
+
+}  // namespace psvd

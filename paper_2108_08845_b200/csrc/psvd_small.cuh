@@ -1,0 +1,39 @@
+// Small-core kernels: one CTA, operate on n x n (n <= a few hundred) data that
+// the tall passes reduced out of the M-row panel.  They run on the device
+// stream between the tall passes, so an update never syncs with the host.
+#pragma once
+#include "psvd_common.cuh"
+
+namespace psvd {
+
+constexpr int SMALL_THREADS = 1024;
+constexpr int EIG_NMAX_SMEM = 224;   // packed lower triangle kept in shared memory up to this n
+
+// Extract the n x n Gram block (rows/cols [c0, c0+n) of the combined column space)
+// from reduced 32x32 tiles (tile id I*NB+J, I <= J computed), scaled symmetrically
+// by d (length n, may be null): out[i][j] = d_i d_j T(c0+i, c0+j).  col-major, ld n.
+void launch_extract_sym(const double* tiles, int NB, int c0, int n, const double* d, double* out,
+                        cudaStream_t st);
+// Extract the rectangular block rows [r0, r0+nr) x cols [c0, c0+nc) (r-block <= c-block),
+// scaled by row factors d (length nr, may be null).  col-major, ld nr.
+void launch_extract_rect(const double* tiles, int NB, int r0, int nr, int c0, int nc, const double* d,
+                         double* out, cudaStream_t st);
+
+// Top-K eigenpairs of the symmetric PSD n x n matrix G (col-major, ld n) and the
+// recompose weights of the streaming update:
+//   sigma_k = sqrt(lambda_k) (descending), V_k eigenvectors,
+//   sign_k from the reference's rule applied to U_R = R V Sigma^-1 with
+//   R = chol(G) (the R of qr(C), diag >= 0 — linalg.py:94-104, 81-91),
+//   W[:, k] = dscale .* V[:, k] * sign_k / sigma_k   (dscale may be null).
+// ws: global scratch of eig_workspace_doubles(n, K) doubles.
+size_t eig_workspace_doubles(int n, int K);
+void launch_eig_topk(const double* G, int n, int K, const double* dscale, double* W, double* sigma,
+                     double* ws, int* status, cudaStream_t st);
+
+// Drift check of streaming.py:106-115 on the K x K Gram UtU = U_new^T U_new:
+// if max|UtU - I| > tol: T = rr^{-1}[:, order] with rr = chol(UtU) (= qr(U).R),
+// sigma <- (sigma * |diag rr|)[order] (stable descending), *gate = 1; else *gate = 0.
+void launch_drift_check(const double* UtU, int K, double tol, double* sigma, double* T, int* gate,
+                        int* status, cudaStream_t st);
+
+}  // namespace psvd

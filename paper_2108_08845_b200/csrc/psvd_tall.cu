@@ -1,0 +1,264 @@
+// Tall-panel pass kernels (see psvd_tall.cuh for the contract).
+#include "psvd_tall.cuh"
+
+namespace psvd {
+
+__host__ __device__ static inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+size_t tall_smem_bytes(int ks, int np_pad, int wk, int w) {
+  const int ksp = ks + 4;
+  size_t b = 0;
+  b += sizeof(const double*) * (size_t)np_pad;  // column base pointers
+  b = (b + 15) / 16 * 16;
+  b += sizeof(double) * 2 * (size_t)np_pad * ksp;  // double-buffered panel stage
+  if (w > 0) {
+    b += sizeof(double) * (size_t)round_up(w, 32) * ksp;                    // Y stage
+    b += sizeof(double) * (size_t)round_up(wk, 4) * (round_up(w, 8) + 4);   // W
+  }
+  return b;
+}
+
+template <int KS, int MAXCB>
+__global__ void __launch_bounds__(NTHR, 1) tall_pass_kernel(const TallParams p) {
+  constexpr int KSP = KS + 4;   // = 4 (mod 16)
+  constexpr int RB = KS / 8;    // 8-row blocks per stage
+  constexpr int CG = NWARP / RB;  // warp groups over Y column blocks
+  if (p.gate != nullptr && *p.gate == 0) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int slice = blockIdx.x % p.nslices;
+  const int64_t chunk = blockIdx.x / p.nslices;
+  const int64_t row_begin = chunk * p.rows_per_cta;
+  const int64_t row_end = min(p.M, row_begin + p.rows_per_cta);
+  const int np_pad = p.np_pad, w_pad = p.w_pad;
+  const bool has_y = p.w > 0;
+  const int wk_pad = (p.wk + 3) & ~3;
+  const int wsp = w_pad + 4;
+  const int ycols = has_y ? round_up(p.w, 32) : 0;
+
+  const double** colptr = reinterpret_cast<const double**>(smem_raw);
+  size_t off = ((sizeof(const double*) * (size_t)np_pad) + 15) / 16 * 16;
+  double* sP = reinterpret_cast<double*>(smem_raw + off);
+  off += sizeof(double) * 2 * (size_t)np_pad * KSP;
+  double* sY = reinterpret_cast<double*>(smem_raw + off);
+  double* sW = sY + (size_t)ycols * KSP;
+
+  for (int c = tid; c < np_pad; c += NTHR) {
+    const double* ptr = nullptr;
+    int base = 0;
+    for (int s = 0; s < p.nseg; ++s) {
+      if (c >= base && c < base + p.seg[s].ncols) ptr = p.seg[s].ptr + (int64_t)(c - base) * p.seg[s].ld;
+      base += p.seg[s].ncols;
+    }
+    colptr[c] = ptr;
+  }
+  {  // zero the padded panel columns of both buffers (never written by cp.async)
+    const int padn = (np_pad - p.np) * KSP;
+    for (int i = tid; i < 2 * padn; i += NTHR) {
+      const int b = i / padn, r = i % padn;
+      sP[(size_t)b * np_pad * KSP + (size_t)p.np * KSP + r] = 0.0;
+    }
+  }
+  if (has_y) {
+    for (int i = tid; i < ycols * KSP; i += NTHR) sY[i] = 0.0;
+    for (int i = tid; i < wk_pad * wsp; i += NTHR) {
+      const int k = i / wsp, o = i % wsp;
+      sW[i] = (k < p.wk && o < p.w) ? p.W[(int64_t)o * p.ldw + k] : 0.0;
+    }
+  }
+  __syncthreads();
+
+  const int64_t nstage = row_end > row_begin ? (row_end - row_begin + KS - 1) / KS : 0;
+  const int nchunk16 = p.np * (KS / 2);
+
+  auto prefetch = [&](int64_t s, int buf) {
+    const int64_t r0 = row_begin + s * KS;
+    double* dst_base = sP + (size_t)buf * np_pad * KSP;
+    for (int q = tid; q < nchunk16; q += NTHR) {
+      const int c = q / (KS / 2), pc = q % (KS / 2);
+      const int64_t r = r0 + 2 * pc;
+      const int64_t valid = row_end - r;
+      const int bytes = valid >= 2 ? 16 : (valid == 1 ? 8 : 0);
+      const double* src = colptr[c] + (bytes > 0 ? r : row_begin);
+      cp_async16(dst_base + (size_t)c * KSP + 2 * pc, src, bytes);
+    }
+  };
+
+  const WarpPlan wp = p.plan[slice][warp];
+  double acc[2][4][4][2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t)
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[t][a][b][0] = acc[t][a][b][1] = 0.0;
+
+  double cm_val = 0.0, cm_abs = -1.0;
+  int64_t cm_row = -1;
+  const bool do_cm = has_y && p.colmax != nullptr && slice == 0 && tid < p.w;
+
+  if (nstage > 0) prefetch(0, 0);
+  cp_async_commit();
+
+  for (int64_t s = 0; s < nstage; ++s) {
+    const int buf = (int)(s & 1);
+    if (s + 1 < nstage) prefetch(s + 1, buf ^ 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* P = sP + (size_t)buf * np_pad * KSP;
+    const int64_t r0 = row_begin + s * KS;
+
+    if (has_y) {
+      // Y(KS x w_pad) = P[:, wlo:wlo+wk] * W on DMMA; warp -> row block rb, column blocks cb0 + CG*j
+      const int rb = warp % RB, cb0 = warp / RB, ncb = w_pad >> 3;
+      double ya[MAXCB][2];
+#pragma unroll
+      for (int j = 0; j < MAXCB; ++j) ya[j][0] = ya[j][1] = 0.0;
+      const double* pa = P + (size_t)(p.wlo + tq) * KSP + rb * 8 + g;
+      const double* pb = sW + (size_t)tq * wsp + g;
+      for (int k0 = 0; k0 < wk_pad; k0 += 4) {
+        const double a = pa[(size_t)k0 * KSP];
+#pragma unroll
+        for (int j = 0; j < MAXCB; ++j) {
+          const int cb = cb0 + CG * j;
+          if (cb < ncb) dmma884(ya[j][0], ya[j][1], a, pb[(size_t)k0 * wsp + cb * 8]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < MAXCB; ++j) {
+        const int cb = cb0 + CG * j;
+        if (cb < ncb) {
+          sY[(size_t)(cb * 8 + 2 * tq) * KSP + rb * 8 + g] = ya[j][0];
+          sY[(size_t)(cb * 8 + 2 * tq + 1) * KSP + rb * 8 + g] = ya[j][1];
+        }
+      }
+      __syncthreads();
+      if (slice == 0) {
+        if (p.Yout != nullptr) {
+          for (int q = tid; q < p.w * (KS / 2); q += NTHR) {
+            const int o = q / (KS / 2), pc = q % (KS / 2);
+            const int64_t r = r0 + 2 * pc;
+            double* dst = p.Yout + (int64_t)o * p.ldy + r;
+            const double v0 = sY[(size_t)o * KSP + 2 * pc], v1 = sY[(size_t)o * KSP + 2 * pc + 1];
+            if (r + 1 < row_end) {
+              *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+            } else if (r < row_end) {
+              dst[0] = v0;
+            }
+          }
+        }
+        if (do_cm) {
+          const int nr = (int)((row_end - r0) < KS ? (row_end - r0) : KS);
+          for (int r = 0; r < nr; ++r) {
+            const double v = sY[(size_t)tid * KSP + r];
+            if (fabs(v) > cm_abs) {
+              cm_abs = fabs(v);
+              cm_val = v;
+              cm_row = r0 + r;
+            }
+          }
+        }
+      }
+    }
+
+    // Gram tiles over the combined [P | Y] column space
+    if (wp.ntile > 0) {
+      for (int kk = wp.kpart; kk < KS / 4; kk += wp.ksplit) {
+        const int k0 = kk * 4;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          if (t < wp.ntile) {
+            const int I = wp.ti[t], J = wp.tj[t];
+            const double* bI = (I * 32 < np_pad) ? P + (size_t)I * 32 * KSP : sY + (size_t)(I * 32 - np_pad) * KSP;
+            const double* bJ = (J * 32 < np_pad) ? P + (size_t)J * 32 * KSP : sY + (size_t)(J * 32 - np_pad) * KSP;
+            double fa[4], fb[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              fa[q] = bI[(size_t)(q * 8 + g) * KSP + k0 + tq];
+              fb[q] = bJ[(size_t)(q * 8 + g) * KSP + k0 + tq];
+            }
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < 4; ++b) dmma884(acc[t][a][b][0], acc[t][a][b][1], fa[a], fb[b]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+
+  if (wp.ntile > 0) {
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      if (t < wp.ntile) {
+        double* dst = p.partial + ((size_t)blockIdx.x * SLOTS + warp * 2 + t) * 1024;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            *reinterpret_cast<double2*>(dst + (a * 8 + g) * 32 + b * 8 + 2 * tq) =
+                make_double2(acc[t][a][b][0], acc[t][a][b][1]);
+      }
+    }
+  }
+  if (do_cm) {
+    double* dst = p.colmax + ((size_t)chunk * p.w + tid) * 2;
+    dst[0] = cm_val;
+    dst[1] = (double)(cm_row + p.row_offset);
+  }
+}
+
+__global__ void tall_reduce_kernel(const double* __restrict__ partial, const ReduceMap map,
+                                   double* __restrict__ tiles) {
+  const int o = blockIdx.y;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= map.nout || e >= 1024) return;
+  double s = 0.0;
+  const int ns = map.nsrc[o];
+  for (int c = 0; c < map.nchunks; ++c) {
+    for (int i = 0; i < ns; ++i) {
+      const int sl = map.src[o][i] / SLOTS, slot = map.src[o][i] % SLOTS;
+      s += partial[((size_t)(c * map.nslices + sl) * SLOTS + slot) * 1024 + e];
+    }
+  }
+  tiles[(size_t)map.out_id[o] * 1024 + e] = s;
+}
+
+template <int KS>
+static void launch_ks(const TallParams& p, int grid, size_t smem, cudaStream_t st) {
+  const int ncb = p.w_pad / 8;
+  constexpr int CG = NWARP / (KS / 8);
+  if ((ncb + CG - 1) / CG <= 1) {
+    cudaFuncSetAttribute(tall_pass_kernel<KS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    tall_pass_kernel<KS, 1><<<grid, NTHR, smem, st>>>(p);
+  } else if ((ncb + CG - 1) / CG <= 2) {
+    cudaFuncSetAttribute(tall_pass_kernel<KS, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    tall_pass_kernel<KS, 2><<<grid, NTHR, smem, st>>>(p);
+  } else if ((ncb + CG - 1) / CG <= 4) {
+    cudaFuncSetAttribute(tall_pass_kernel<KS, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    tall_pass_kernel<KS, 4><<<grid, NTHR, smem, st>>>(p);
+  } else {
+    cudaFuncSetAttribute(tall_pass_kernel<KS, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    tall_pass_kernel<KS, 8><<<grid, NTHR, smem, st>>>(p);
+  }
+}
+
+void launch_tall(const TallParams& p, int grid, cudaStream_t st) {
+  const size_t smem = tall_smem_bytes(p.ks, p.np_pad, p.wk, p.w);
+  if (p.ks == 32)
+    launch_ks<32>(p, grid, smem, st);
+  else
+    launch_ks<16>(p, grid, smem, st);
+}
+
+void launch_tall_reduce(const double* partial, const ReduceMap& map, double* tiles, cudaStream_t st) {
+  if (map.nout == 0) return;
+  dim3 grid(1024 / 256, map.nout);
+  tall_reduce_kernel<<<grid, 256, 0, st>>>(partial, map, tiles);
+}
+
+}  // namespace psvd

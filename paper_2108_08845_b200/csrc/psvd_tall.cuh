@@ -1,0 +1,79 @@
+// Tall-panel pass: the one kernel family that touches the M-row data.
+//
+// A "panel" P is the virtual column concatenation of up to 4 column-major
+// device matrices (segments), e.g. [U | A_batch] = the reference's
+// np.concatenate([ff*U*S, A]) (streaming.py:97-98) without materializing it,
+// or [U | A | Y] for the randomized passes.  One pass streams P in 32-row
+// stages through shared memory (cp.async, double buffered) and, per stage:
+//
+//   1. optionally forms Y = P[:, wlo:wlo+wk] * W on FP64 tensor cores (DMMA),
+//      W small (wk x w) and resident in smem; Y goes to smem, optionally to
+//      global (coalesced) and into a running per-column (max|y|, row) argmax;
+//   2. accumulates a selected set of 32x32 tiles of the Gram matrix of the
+//      combined column space [P | Y] in registers (DMMA), e.g. the upper
+//      triangle of P^T P (deterministic update), Y^T Y and P^T Y (sketch).
+//
+// Per-CTA partial tiles are summed across CTAs in a fixed order by
+// tall_reduce (bitwise reproducible; no atomics), so replicated small
+// factorizations on every GPU see identical input.
+#pragma once
+#include "psvd_common.cuh"
+
+namespace psvd {
+
+// rows per stage KS is a template parameter (32, or 16 when the panel + W do not
+// fit 227 KB); the smem column stride KS + 4 is 4 (mod 16) -> conflict-free fragments.
+constexpr int NWARP = 8;
+constexpr int NTHR = NWARP * 32;
+constexpr int MAX_SEG = 4;
+constexpr int SLOTS = 16;    // partial tile slots per CTA (8 warps x 2 tiles)
+constexpr int MAX_SLICES = 4;
+constexpr int MAX_OUT_TILES = 64;
+constexpr int MAX_W = 128;   // widest Y
+
+struct Seg {
+  const double* ptr;
+  int64_t ld;
+  int ncols;
+  int pad_;
+};
+
+struct WarpPlan {
+  signed char ti[2], tj[2];  // 32-column block indices into [P | Y]
+  unsigned char ntile, kpart, ksplit, pad_;
+};
+
+struct TallParams {
+  int64_t M;
+  int64_t rows_per_cta;  // multiple of 32
+  int ks;                // rows per stage (32 or 16)
+  int nseg;
+  Seg seg[MAX_SEG];
+  int np, np_pad;        // panel columns; padded to a multiple of 32 (start of the Y block)
+  const double* W;       // Y = P[:, wlo:wlo+wk] * W; W col-major (wk x w), ld ldw; w == 0 -> no Y
+  int64_t ldw;
+  int wlo, wk, w, w_pad;  // w_pad = round8(w) columns computed; S_Y holds round32(w) columns
+  double* Yout;          // optional global copy of Y (col-major, ld ldy)
+  int64_t ldy;
+  int nslices;
+  WarpPlan plan[MAX_SLICES][NWARP];
+  double* partial;       // [grid][SLOTS][1024]
+  double* colmax;        // optional [grid][w][2] = (signed value at max |y|, global row)
+  int64_t row_offset;    // global row index of local row 0 (multi-GPU argmax)
+  const int* gate;       // optional: skip the pass unless *gate != 0
+};
+
+struct ReduceMap {
+  int nout;
+  int nchunks, nslices;
+  short out_id[MAX_OUT_TILES];                    // destination tile id (I * NB + J)
+  unsigned char nsrc[MAX_OUT_TILES];
+  unsigned char src[MAX_OUT_TILES][2 * NWARP];    // slice * SLOTS + slot
+};
+
+size_t tall_smem_bytes(int ks, int np_pad, int wk, int w);
+
+void launch_tall(const TallParams& p, int grid, cudaStream_t st);
+void launch_tall_reduce(const double* partial, const ReduceMap& map, double* tiles, cudaStream_t st);
+
+}  // namespace psvd

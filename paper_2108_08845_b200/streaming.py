@@ -1,0 +1,157 @@
+"""Streaming truncated SVD over column batches — B200 drop-in for the
+reference's streaming.py (StreamConfig/StreamState/stream_initialize/
+stream_incorporate/stream_all, /root/reference/pkg/src/parsvd/streaming.py:28-133).
+
+Same update rule, same validation errors, same sign convention; the state
+lives in HBM (torch CUDA tensors) and every update is a fixed sequence of
+libpsvd kernels on the current stream:
+
+    Gram of the virtual panel [ff*U*S | A]  ->  top-K eigen + sign rule (one CTA)
+    ->  recompose U_new = [U | A] W  (+ U_new^T U_new)  ->  drift rescue (gated)
+
+The optional `sketch` field (a RandomSketchConfig) selects the randomized
+update: each step is low_rank_svd of [ff*U*S | A].
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _native as nat
+from .linalg import RandomSketchConfig, randomized_update
+
+# streaming.py:25 — re-orthonormalize when max|U^T U - I| exceeds this
+ORTHO_DRIFT_TOL = 1e-8
+
+
+@dataclass(frozen=True)
+class StreamConfig:
+    """k_modes kept per update, forget factor in (0, 1], nominal batch width
+    (streaming.py:28-50).  `sketch` (B200 extension) switches to the
+    randomized update; None keeps the reference's deterministic rule."""
+
+    k_modes: int
+    forget_factor: float = 0.95
+    batch_columns: int = 1
+    sketch: Optional[RandomSketchConfig] = None
+
+    def __post_init__(self):
+        if self.k_modes < 1:
+            raise ValueError(f"k_modes must be >= 1, got {self.k_modes}")
+        if not 0.0 < self.forget_factor <= 1.0:
+            raise ValueError(f"forget_factor must be in (0, 1], got {self.forget_factor}")
+        if self.batch_columns < 1:
+            raise ValueError(f"batch_columns must be >= 1, got {self.batch_columns}")
+        if self.sketch is not None and self.sketch.target_rank != self.k_modes:
+            raise ValueError(
+                f"sketch target_rank {self.sketch.target_rank} must equal k_modes {self.k_modes}")
+
+
+@dataclass(frozen=True)
+class StreamState:
+    """modes (M x K, orthonormal columns; a column-major CUDA tensor view),
+    singular_values (K, descending, CUDA), iteration count (streaming.py:53-60).
+    numpy arrays are accepted on input and moved to the device."""
+
+    modes: torch.Tensor
+    singular_values: torch.Tensor
+    iteration: int
+
+    def numpy(self):
+        """(modes, singular_values) as host numpy arrays."""
+        return (self.modes.detach().cpu().numpy().copy(),
+                self.singular_values.detach().cpu().numpy().copy())
+
+
+def _device_of(*objs):
+    for o in objs:
+        if isinstance(o, torch.Tensor) and o.device.type == "cuda":
+            return o.device
+        if isinstance(o, nat.DevMat):
+            return o.t.device
+    nat.require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _check_status(ctx, device, what):
+    st = nat.read_status(ctx, reset=True, device=device)
+    if st & nat.ST_NONFINITE:
+        raise ValueError(f"{what} contains non-finite entries")
+    return st
+
+
+def deterministic_update(U, sigma, A, k, ff, rescue, device, check=True):
+    """One deterministic update on the device.  U: DevMat or None (initialize),
+    sigma: (Kc,) CUDA tensor, A: DevMat.  Returns (DevMat M x k, sigma (k,))."""
+    ctx = nat.context(device)
+    with torch.cuda.device(device):
+        st = nat.stream_ptr(device)
+        M, B = A.rows, A.cols
+        kc = 0 if U is None else U.cols
+        out = nat.DevMat.empty(M, k, device)
+        sig = torch.empty(k, dtype=torch.float64, device=device)
+        nat.call("psvd_stream_update", ctx, M,
+                 nat._vp(U.data_ptr() if U is not None else 0), U.ld if U is not None else 0,
+                 nat.ptr(sigma if U is not None else None), float(ff), kc,
+                 nat._vp(A.data_ptr()), A.ld, B, k, int(bool(rescue)),
+                 nat._vp(out.data_ptr()), out.ld, nat.ptr(sig), st)
+        if check:
+            _check_status(ctx, device, "a_new" if U is not None else "a0")
+    return out, sig
+
+
+def stream_initialize(a0, config, device=None):
+    """Initial state from the first batch (streaming.py:63-78)."""
+    dev = torch.device(device) if device is not None else _device_of(a0)
+    A = nat.as_device_colmajor(a0, dev, "a0")
+    k = config.k_modes
+    if A.cols < k:
+        raise ValueError(f"initial batch has {A.cols} columns, need at least k_modes={k}")
+    if A.rows < k:
+        raise ValueError(f"initial batch has {A.rows} rows, need at least k_modes={k}")
+    if config.sketch is not None:
+        u, s = randomized_update(None, None, A, config.sketch, config.forget_factor, dev)
+    else:
+        u, s = deterministic_update(None, None, A, k, config.forget_factor, False, dev)
+    return StreamState(u.view, s, 0)
+
+
+def stream_incorporate(state, a_new, config):
+    """Fold one batch into the state (streaming.py:81-116)."""
+    dev = _device_of(state.modes, a_new)
+    k = config.k_modes
+    modes = state.modes
+    if modes.ndim != 2:
+        raise ValueError("state.modes must be 2-D")
+    if modes.shape[1] != k:
+        raise ValueError(f"state carries {modes.shape[1]} modes, config wants {k}")
+    A = nat.as_device_colmajor(a_new, dev, "a_new")
+    if A.rows != modes.shape[0]:
+        raise ValueError(f"batch rows {A.rows} != mode rows {modes.shape[0]}")
+    U = nat.as_device_colmajor(modes, dev, "modes")
+    sigma = nat.as_device_vector(state.singular_values, dev, k, "singular_values")
+    if config.sketch is not None:
+        u, s = randomized_update(U, sigma, A, config.sketch, config.forget_factor, dev)
+    else:
+        u, s = deterministic_update(U, sigma, A, k, config.forget_factor, True, dev)
+    return StreamState(u.view, s, state.iteration + 1)
+
+
+def stream_all(batches, config, device=None):
+    """Initialize on the first batch, incorporate the rest (streaming.py:119-133).
+    Returns (final_state, history) with the singular values after every step."""
+    state = None
+    history = []
+    for batch in batches:
+        if state is None:
+            state = stream_initialize(batch, config, device)
+        else:
+            state = stream_incorporate(state, batch, config)
+        history.append(state.singular_values.clone())
+    if state is None:
+        raise ValueError("batch stream is empty")
+    return state, history
