@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""bench.py — snapshot GB/s through the streaming-SVD update (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "config 2"): analytic Burgers snapshots,
+2^20 grid rows x 800 snapshots, streamed in batches of 200 (init + 3
+incorporates), K = 10 modes, forget factor 0.95, fp64, rows partitioned over
+the GPUs with the reference's partition_bounds (strong scaling: total work
+fixed).  One "step" = one full pass of the stream (4 updates, 6.7 GB of
+snapshots).  Inputs (6.7 GB) are far larger than L2 (126 MB), so no flush is
+needed between steps.
+
+  python bench.py [--gpus N --steps K --warmup W] [--path det|rand] [--impl reference]
+
+--impl reference times the reference algorithm's CPU implementation (the
+numpy oracle port under oracle/, all host threads) on a bounded row sample of
+the same workload; under torchrun only rank 0 runs it.
+"""
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GRID = 1 << 20
+SNAPS = 800
+BATCH = 200
+K = 10
+FF = 0.95
+HBM_PEAK = None  # filled from MEASURED_PEAKS.json
+FP64_PEAK_TFLOPS = 37.0  # measured DMMA m8n8k4 peak on this pool's B200 (profiles/fp64_peaks_r01.jsonl)
+
+
+def load_peaks():
+    global HBM_PEAK
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            HBM_PEAK = float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        HBM_PEAK = 6650.0, "fallback (B200_PROFILING.md)"
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peaks_r01.jsonl")) as f:
+            for line in f:
+                d = json.loads(line)
+                if d.get("test") == "dmma_peak":
+                    globals()["FP64_PEAK_TFLOPS"] = max(FP64_PEAK_TFLOPS if d.get("warps_per_block") != 4 else 0,
+                                                        d["tflops"])
+    except Exception:
+        pass
+
+
+def args_():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--path", default="det", choices=["det", "rand"])
+    ap.add_argument("--rows", type=int, default=GRID)
+    ap.add_argument("--cpu-rows", type=int, default=1 << 17, help="row sample for the CPU baseline")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while running."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "samples": len(self.rows), "reasons": reasons}
+
+
+# ------------------------------------------------------------------ CPU reference
+
+def cpu_reference_gbs(rows, path, steps=1, warmup=0):
+    """The reference algorithm's CPU implementation (oracle port, numpy/LAPACK,
+    all host threads) on a `rows`-row sample of the workload.  Returns
+    (GB/s, seconds per step)."""
+    import oracle
+    a = oracle.burgers_matrix(GRID, SNAPS, rows=(0, rows))  # the first `rows` grid rows of config 2
+    batches = [np.ascontiguousarray(a[:, i:i + BATCH]) for i in range(0, SNAPS, BATCH)]
+
+    def one():
+        if path == "det":
+            oracle.ref_stream_all(batches, K, FF)
+        else:
+            oracle.ref_rand_stream_all(batches, K, FF, 10, 1, 0)
+
+    for _ in range(warmup):
+        one()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        one()
+    dt = (time.perf_counter() - t0) / steps
+    return 8.0 * rows * SNAPS / dt / 1e9, dt
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    rows = a.cpu_rows
+    gbs_steps = []
+    ws = []
+    for i in range(a.warmup + a.steps):
+        g, dt = cpu_reference_gbs(rows, a.path)
+        (ws if i < a.warmup else gbs_steps).append((g, dt))
+    value = float(np.mean([g for g, _ in gbs_steps]))
+    ms = float(np.mean([dt for _, dt in gbs_steps])) * 1e3
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": metric_name(a.path), "value": round(value, 4), "unit": "GB/s",
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 2),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (analytic Burgers, host-generated)", "config": config_dict(a, rows),
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                         "sample": f"first {rows} of {GRID} grid rows x {SNAPS} snapshots, init + 3 incorporates "
+                                   f"(oracle/core.py, numpy {np.__version__} LAPACK/BLAS, all {cores} host threads)"},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def metric_name(path):
+    return ("snapshot GB/s through streaming-SVD update (Burgers 2^20 x 800, B=200, K=10, ff=0.95, "
+            + ("deterministic" if path == "det" else "randomized p=10 q=1") + ")")
+
+
+def config_dict(a, rows=None):
+    return {"workload": f"config2-burgers-2^20x800-{a.path}", "rows": rows or a.rows, "snapshots": SNAPS,
+            "batch": BATCH, "k": K, "ff": FF, "path": "deterministic" if a.path == "det" else "randomized",
+            "parallelism": f"row-partition x{a.gpus}", "l2": "inputs 6.7 GB >> 126 MB L2, no flush"}
+
+
+# ------------------------------------------------------------------ our arm
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2108_08845_b200 as p
+    from paper_2108_08845_b200 import _native as nat
+    from paper_2108_08845_b200.dsvd import RankContext, allreduce_ordered
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    ctxr = RankContext()
+    lo, hi = p.partition_bounds(a.rows, world)[rank]
+    M = hi - lo
+    D = p.burgers_device(a.rows, SNAPS, rows=(lo, hi), device=dev)  # M x 800 col-major, resident in HBM
+    c = nat.context(dev)
+    stream = torch.cuda.current_stream(dev)
+    st = nat._vp(stream.cuda_stream)
+    ld = D.ld
+
+    def col_ptr(j):
+        return nat._vp(D.data_ptr() + 8 * ld * j)
+
+    Ubuf = [nat.DevMat.empty(M, K, dev) for _ in range(2)]
+    sig = [torch.zeros(K, dtype=torch.float64, device=dev) for _ in range(2)]
+    nmax = K + BATCH
+    G = torch.empty((nmax, nmax), dtype=torch.float64, device=dev)
+    W = torch.empty((K, nmax), dtype=torch.float64, device=dev)
+    gram_ev = []
+    Gloc = {n: torch.empty((n, n), dtype=torch.float64, device=dev) for n in (BATCH, K + BATCH)}
+
+    def step(record=False):
+        cur = 0
+        for b in range(SNAPS // BATCH):
+            kc = 0 if b == 0 else K
+            n = kc + BATCH
+            Uin, Uout = Ubuf[cur], Ubuf[cur ^ 1]
+            if world == 1:
+                e0 = e1 = None
+                if record:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                nat.call("psvd_gram", c, M, nat._vp(Uin.data_ptr()), Uin.ld, nat.ptr(sig[cur]), FF, kc,
+                         col_ptr(b * BATCH), ld, BATCH, nat.ptr(G), st)
+                if record:
+                    e1.record(stream)
+                    gram_ev.append((e0, e1, M * n * (n + 1)))
+                nat.call("psvd_core_eig", c, nat.ptr(G), n, nat.ptr(sig[cur]), FF, kc, K, nat.ptr(W),
+                         nat.ptr(sig[cur ^ 1]), st)
+                utu = G  # reuse as K x K scratch
+                nat.call("psvd_recompose", c, M, nat._vp(Uin.data_ptr()), Uin.ld, kc, col_ptr(b * BATCH), ld,
+                         BATCH, nat.ptr(W), K, nat._vp(Uout.data_ptr()), Uout.ld,
+                         nat.ptr(utu) if b > 0 else nat._vp(0), st)
+                if b > 0:
+                    nat.call("psvd_drift_rescue", c, M, nat._vp(Uout.data_ptr()), Uout.ld, K, nat.ptr(utu),
+                             nat.ptr(sig[cur ^ 1]), 1e-8, st)
+            else:
+                Gl = Gloc[n]
+                if record:
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                nat.call("psvd_gram", c, M, nat._vp(Uin.data_ptr()), Uin.ld, nat.ptr(sig[cur]), FF, kc,
+                         col_ptr(b * BATCH), ld, BATCH, nat.ptr(Gl), st)
+                if record:
+                    e1.record(stream)
+                    gram_ev.append((e0, e1, M * n * (n + 1)))
+                Gs = allreduce_ordered(Gl, ctxr)
+                nat.call("psvd_core_eig", c, nat.ptr(Gs), n, nat.ptr(sig[cur]), FF, kc, K, nat.ptr(W),
+                         nat.ptr(sig[cur ^ 1]), st)
+                nat.call("psvd_recompose", c, M, nat._vp(Uin.data_ptr()), Uin.ld, kc, col_ptr(b * BATCH), ld,
+                         BATCH, nat.ptr(W), K, nat._vp(Uout.data_ptr()), Uout.ld, nat._vp(0), st)
+            cur ^= 1
+        return Ubuf[cur], sig[cur]
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    status = nat.read_status(c)
+    assert not (status & nat.ST_NONFINITE), "non-finite input"
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    launches0 = nat.lib().psvd_launch_count(c)
+    with ClockSampler(local) as clk:
+        barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(stream)
+        for _ in range(a.steps):
+            step(record=True)
+        t1.record(stream)
+        barrier()
+    launches = nat.lib().psvd_launch_count(c) - launches0
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    ms_step = ms / a.steps
+    snap_bytes = 8.0 * a.rows * SNAPS  # whole job, all ranks
+    value = snap_bytes / (ms_step * 1e-3) / 1e9
+
+    gram_ms = [e0.elapsed_time(e1) for e0, e1, _ in gram_ev]
+    gram_flops = [f for _, _, f in gram_ev]
+    g_ach = sum(gram_flops) / (sum(gram_ms) * 1e-3) / 1e12
+    alg_bytes_step = sum(8.0 * M * (2 * BATCH + 3 * (0 if b == 0 else K)) for b in range(SNAPS // BATCH))
+    hbm_ach = alg_bytes_step / (ms_step * 1e-3) / 1e9  # per GPU
+    gram_share = sum(gram_ms) / ms
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_gram_r01.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": metric_name(a.path), "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (analytic Burgers, device-generated; same formula as the host generator)",
+        "config": config_dict(a),
+        "roofline": {"bound": "tensor", "kernel": "psvd_gram (tall_pass_kernel DMMA Gram of [ff*U*S | A])",
+                     "achieved": round(g_ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": round(g_ach / FP64_PEAK_TFLOPS, 4), "traffic": traffic,
+                     "peak_source": "measured DMMA.8x8x4 peak (profiles/fp64_peaks_r01.jsonl); "
+                                    "MEASURED_PEAKS.json has no FP64 entry",
+                     "flops_per_launch": "M*n*(n+1) (upper triangle of C^T C), n = K + B",
+                     "share_of_step": round(gram_share, 4)},
+        "hbm_roofline": {"achieved": round(hbm_ach, 1), "peak": HBM_PEAK[0], "unit": "GB/s",
+                         "frac": round(hbm_ach / HBM_PEAK[0], 4), "peak_source": HBM_PEAK[1],
+                         "bytes_per_step": "sum over updates of 8*M*(2B+3K) per GPU"},
+        "gpu_launches": int(launches),
+    }
+    line["clocks"] = clk.summary()
+
+    # ---- end to end through the public API with host (pinned) buffers
+    if not a.no_e2e:
+        line["e2e"] = e2e(a, p, D, M, dev, world, ctxr)
+
+    if world == 1 and rank == 0 and not a.no_cpu:
+        g, dt = cpu_reference_gbs(a.cpu_rows, a.path)
+        cores = os.cpu_count()
+        line["cpu_baseline"] = {"value": round(g, 4), "unit": "GB/s", "cores": cores, "kind": "port",
+                                "sample": f"first {a.cpu_rows} grid rows x {SNAPS} snapshots, init + 3 incorporates"
+                                          f" ({dt:.1f} s; oracle/core.py numpy LAPACK, {cores} threads)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def e2e(a, p, D, M, dev, world, ctxr):
+    """Same metric through the public API (stream_initialize / stream_incorporate,
+    parallel_* at N > 1) with the snapshot batches in pinned host memory: every
+    step copies its batches host->device and reads the modes + sigma back."""
+    import torch
+    import torch.distributed as dist
+
+    host = torch.empty((SNAPS, M), dtype=torch.float64, pin_memory=True)  # column-major M x 800
+    host.copy_(D.view.T)
+    cfg = p.StreamConfig(k_modes=K, forget_factor=FF, batch_columns=BATCH)
+    batches = [host[i:i + BATCH].T for i in range(0, SNAPS, BATCH)]
+
+    def one():
+        if world == 1:
+            st = p.stream_initialize(batches[0], cfg, device=dev)
+            for bt in batches[1:]:
+                st = p.stream_incorporate(st, bt, cfg)
+            m, s = st.modes, st.singular_values
+        else:
+            st = p.parallel_stream_initialize(ctxr, batches[0].to(dev), cfg)
+            for bt in batches[1:]:
+                st = p.parallel_stream_incorporate(ctxr, st, bt.to(dev), cfg)
+            m, s = st.modes, st.singular_values
+        return m.cpu(), s.cpu()
+
+    one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    n = max(1, min(a.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(n):
+        out = one()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / n
+    if world > 1:
+        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+    return {"value": round(8.0 * a.rows * SNAPS / dt / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": int(8 * M * SNAPS), "d2h_bytes_per_step": int(out[0].numel() * 8 + out[1].numel() * 8),
+            "ms_per_step": round(dt * 1e3, 2), "steps": n,
+            "path": "public API stream_initialize/stream_incorporate from pinned host batches"}
+
+
+def main():
+    a = args_()
+    load_peaks()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

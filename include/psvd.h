@@ -52,6 +52,9 @@ int psvd_create(int device, psvd_ctx** out);
 int psvd_destroy(psvd_ctx* ctx);
 const char* psvd_last_error(psvd_ctx* ctx);
 
+/* Number of kernels this context has enqueued so far (launch accounting). */
+long long psvd_launch_count(psvd_ctx* ctx);
+
 /* Copy the context's device status word to *status (synchronizes `stream`);
  * reset != 0 clears it afterwards (stream-ordered). */
 int psvd_read_status(psvd_ctx* ctx, int* status, int reset, void* stream);

@@ -36,6 +36,7 @@ _SIGS = {
     "psvd_create": (_c_int, [_c_int, ctypes.POINTER(_vp)]),
     "psvd_destroy": (_c_int, [_vp]),
     "psvd_last_error": (ctypes.c_char_p, [_vp]),
+    "psvd_launch_count": (ctypes.c_longlong, [_vp]),
     "psvd_read_status": (_c_int, [_vp, ctypes.POINTER(_c_int), _c_int, _vp]),
     "psvd_gram": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_int, _vp, _c_i64, _c_int, _vp, _vp]),
     "psvd_core_eig": (_c_int, [_vp, _vp, _c_int, _vp, _c_dbl, _c_int, _c_int, _vp, _vp, _vp]),
@@ -58,7 +59,7 @@ def header_symbols():
     """Function names declared in include/psvd.h."""
     with open(HEADER) as f:
         txt = f.read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(psvd_\w+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|long long|const char\*)\s+(psvd_\w+)\s*\(", txt, re.M)))
 
 
 def lib():
@@ -184,9 +185,12 @@ def as_device_colmajor(a, device, name="a"):
             dm = _aligned_colmajor(t)
             if dm is not None:
                 return dm
-        t = t.to(device=device, dtype=torch.float64)
         out = DevMat.empty(t.shape[0], t.shape[1], device)
-        out.view.copy_(t)
+        if t.device.type == "cpu":
+            # one H2D copy straight into the column-major buffer (async from pinned memory)
+            out.view.copy_(t.to(torch.float64), non_blocking=t.is_pinned())
+        else:
+            out.view.copy_(t)
         return out
     arr = np.asarray(a, dtype=np.float64)
     if arr.ndim != 2:

@@ -32,6 +32,7 @@ struct psvd_ctx {
   int* d_status = nullptr;  // device status word
   int* d_gate = nullptr;
   int* h_status = nullptr;  // pinned
+  long long launches = 0;   // kernels enqueued by this context (bench evidence)
   Buf partial, tiles, gram, eigws, wbuf, utu, tbuf, dvec, colmax;
 };
 
@@ -211,6 +212,7 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
 
 int run_pass(psvd_ctx* c, Pass& ps, cudaStream_t st) {
   launch_tall(ps.p, ps.grid, st);
+  c->launches += 1 + (ps.map.nout > 0);
   int rc = cuda_check(c, "tall pass");
   if (rc) return rc;
   if (ps.map.nout > 0) {
@@ -229,6 +231,7 @@ int make_dvec(psvd_ctx* c, const double* sigma, double ff, int Kc, int n, cudaSt
   int rc = ensure(c, c->dvec, sizeof(double) * (size_t)std::max(n, 1));
   if (rc) return rc;
   make_dvec_kernel<<<(n + 255) / 256, 256, 0, st>>>(sigma, ff, Kc, n, (double*)c->dvec.ptr);
+  c->launches++;
   return cuda_check(c, "dvec");
 }
 
@@ -314,6 +317,8 @@ int psvd_destroy(psvd_ctx* c) {
 
 const char* psvd_last_error(psvd_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
+long long psvd_launch_count(psvd_ctx* c) { return c ? c->launches : -1; }
+
 int psvd_read_status(psvd_ctx* c, int* status, int reset, void* stream) {
   if (!c || !status) return PSVD_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
@@ -339,6 +344,7 @@ int psvd_gram(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const double
   if ((rc = run_pass(c, ps, st))) return rc;
   if ((rc = make_dvec(c, sigma, ff, Kc, n, st))) return rc;
   launch_extract_sym((const double*)c->tiles.ptr, ps.NB, 0, n, (const double*)c->dvec.ptr, G, st);
+  c->launches++;
   return cuda_check(c, "extract gram");
 }
 
@@ -353,6 +359,7 @@ int psvd_core_eig(psvd_ctx* c, const double* G, int n, const double* sigma_in, d
   if ((rc = make_dvec(c, sigma_in, ff, Kc, n, st))) return rc;
   if ((rc = ensure(c, c->eigws, sizeof(double) * eig_workspace_doubles(n, K)))) return rc;
   launch_eig_topk(G, n, K, (const double*)c->dvec.ptr, W, sigma_out, (double*)c->eigws.ptr, c->d_status, st);
+  c->launches++;
   return cuda_check(c, "core eig");
 }
 
@@ -373,6 +380,7 @@ int psvd_recompose(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, int Kc,
   if ((rc = run_pass(c, ps, st))) return rc;
   if (UtU) {
     launch_extract_sym((const double*)c->tiles.ptr, ps.NB, ps.p.np_pad, K, nullptr, UtU, st);
+    c->launches++;
     rc = cuda_check(c, "extract UtU");
   }
   return rc;
@@ -387,6 +395,7 @@ int psvd_drift_rescue(psvd_ctx* c, int64_t M, double* U, int64_t ldu, int K, con
   if (K > MAX_W) return fail(c, PSVD_EINVAL, "K=%d too large for the rescue pass", K);
   if ((rc = ensure(c, c->tbuf, sizeof(double) * (size_t)K * K))) return rc;
   launch_drift_check(UtU, K, tol, sigma, (double*)c->tbuf.ptr, c->d_gate, c->d_status, st);
+  c->launches++;
   if ((rc = cuda_check(c, "drift check"))) return rc;
   Pass ps;
   if ((rc = plan_pass(c, ps, M, {Seg{U, ldu, K, 0}}, 0, K, K, (const double*)c->tbuf.ptr, K, false, false, false)))
@@ -421,6 +430,7 @@ int psvd_sum_ordered(psvd_ctx* c, const double* parts, int P, int64_t count, dou
   if (!c || !parts || !out || P < 1 || count < 0) return fail(c, PSVD_EINVAL, "bad sum_ordered args");
   if (count == 0) return PSVD_OK;
   sum_ordered_kernel<<<(unsigned)((count + 255) / 256), 256, 0, (cudaStream_t)stream>>>(parts, P, count, out);
+  c->launches++;
   return cuda_check(c, "sum ordered");
 }
 
