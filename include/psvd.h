@@ -55,6 +55,10 @@ const char* psvd_last_error(psvd_ctx* ctx);
 /* Number of kernels this context has enqueued so far (launch accounting). */
 long long psvd_launch_count(psvd_ctx* ctx);
 
+/* Diagnostics: SM clock64() stamps of the 9 phase boundaries of the last
+ * core eigensolver launch (synchronous copy). */
+int psvd_eig_phase_cycles(psvd_ctx* ctx, long long* out9);
+
 /* Copy the context's device status word to *status (synchronizes `stream`);
  * reset != 0 clears it afterwards (stream-ordered). */
 int psvd_read_status(psvd_ctx* ctx, int* status, int reset, void* stream);

@@ -31,6 +31,7 @@ struct psvd_ctx {
   std::string err;
   int* d_status = nullptr;  // device status word
   int* d_gate = nullptr;
+  long long* d_timers = nullptr;  // eig phase clocks (diagnostics)
   int* h_status = nullptr;  // pinned
   long long launches = 0;   // kernels enqueued by this context (bench evidence)
   Buf partial, tiles, gram, eigws, wbuf, utu, tbuf, dvec, colmax;
@@ -296,6 +297,10 @@ int psvd_create(int device, psvd_ctx** out) {
     return PSVD_ECUDA;
   }
   c->d_gate = c->d_status + 1;
+  if (cudaMalloc(&c->d_timers, 16 * sizeof(long long)) != cudaSuccess) {
+    cudaGetLastError();
+    return PSVD_ECUDA;
+  }
   cudaMemset(c->d_status, 0, 2 * sizeof(int));
   cudaDeviceSynchronize();
   *out = c;
@@ -310,6 +315,7 @@ int psvd_destroy(psvd_ctx* c) {
   for (Buf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
   cudaFree(c->d_status);
+  cudaFree(c->d_timers);
   cudaFreeHost(c->h_status);
   delete c;
   return PSVD_OK;
@@ -318,6 +324,13 @@ int psvd_destroy(psvd_ctx* c) {
 const char* psvd_last_error(psvd_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 long long psvd_launch_count(psvd_ctx* c) { return c ? c->launches : -1; }
+
+int psvd_eig_phase_cycles(psvd_ctx* c, long long* out9) {
+  if (!c || !out9) return PSVD_EINVAL;
+  if (cudaMemcpy(out9, c->d_timers, 9 * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return cuda_check(c, "eig timers");
+  return PSVD_OK;
+}
 
 int psvd_read_status(psvd_ctx* c, int* status, int reset, void* stream) {
   if (!c || !status) return PSVD_EINVAL;
@@ -354,11 +367,12 @@ int psvd_core_eig(psvd_ctx* c, const double* G, int n, const double* sigma_in, d
   cudaStream_t st = (cudaStream_t)stream;
   if (n < 1 || K < 1 || K > n || Kc < 0 || Kc > n) return fail(c, PSVD_EINVAL, "bad core shape n=%d K=%d Kc=%d", n, K, Kc);
   if (!G || !W || !sigma_out || (Kc > 0 && !sigma_in)) return fail(c, PSVD_EINVAL, "null pointer");
-  if (K > 1024) return fail(c, PSVD_EINVAL, "K=%d too large", K);
+  if (!eig_supported(n, K)) return fail(c, PSVD_EINVAL, "core of size %d with K=%d is not supported", n, K);
   int rc;
   if ((rc = make_dvec(c, sigma_in, ff, Kc, n, st))) return rc;
   if ((rc = ensure(c, c->eigws, sizeof(double) * eig_workspace_doubles(n, K)))) return rc;
-  launch_eig_topk(G, n, K, (const double*)c->dvec.ptr, W, sigma_out, (double*)c->eigws.ptr, c->d_status, st);
+  launch_eig_topk(G, n, K, (const double*)c->dvec.ptr, W, sigma_out, (double*)c->eigws.ptr, c->d_status,
+                  c->d_timers, st);
   c->launches++;
   return cuda_check(c, "core eig");
 }

@@ -81,7 +81,7 @@ template <bool SMEM>
 __global__ void __launch_bounds__(SMALL_THREADS, 1)
 eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __restrict__ dscale,
                 double* __restrict__ W, double* __restrict__ sigma_out, double* __restrict__ ws,
-                int* __restrict__ status) {
+                int* __restrict__ status, long long* __restrict__ timers) {
   extern __shared__ double sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nthr = blockDim.x, nwarps = nthr >> 5;
@@ -101,6 +101,10 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
   double* Z = ws + npk;                     // n x K (col-major, ld n)
   double* Dp = Z + (size_t)n * K;           // K x n
   double* Dm = Dp + (size_t)n * K;          // K x n
+  auto stamp = [&](int i) {
+    if (timers != nullptr && tid == 0) timers[i] = clock64();
+  };
+  stamp(0);
 
   // ---- A: load the lower triangle
   for (int64_t idx = tid; idx < (int64_t)n * n; idx += nthr) {
@@ -109,6 +113,7 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
   }
   __syncthreads();
 
+  stamp(1);
   // ---- B: Householder tridiagonalization (lower, dsytd2-style)
   for (int j = 0; j + 2 < n; ++j) {
     const int m = n - j - 1;
@@ -176,6 +181,7 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
   for (int i = tid; i < n; i += nthr) e2[i] = (i + 1 < n) ? ee[i] * ee[i] : 0.0;
   __syncthreads();
 
+  stamp(2);
   // ---- C: Gerschgorin bounds, multisection bisection (one warp per eigenvalue)
   double glo = DBL_MAX, ghi = -DBL_MAX, emax2 = 0.0;
   for (int i = lane; i < n; i += 32) {
@@ -220,6 +226,7 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
   }
   __syncthreads();
 
+  stamp(3);
   // ---- D: twisted-factorization eigenvectors of T (one thread per eigenvalue)
   for (int k = tid; k < K; k += nthr) {
     const double lk = lam[k];
@@ -258,6 +265,7 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
   }
   __syncthreads();
 
+  stamp(4);
   // ---- E: normalize; MGS (twice) inside clusters; rescue collapsed vectors
   for (int k0 = warp; k0 < K; k0 += nwarps) {
     if (clus[k0] != k0) continue;  // this warp owns the cluster led by k0
@@ -310,6 +318,7 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
   }
   __syncthreads();
 
+  stamp(5);
   // ---- F: back-transform Z <- H_0 ... H_{n-3} Z  (warp per column, no block sync)
   for (int k = warp; k < K; k += nwarps) {
     double* z = Z + (size_t)k * n;
@@ -328,6 +337,7 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
   }
   __syncthreads();
 
+  stamp(6);
   // ---- G: R = chol(G + delta I), delta = 10 n eps max(diag G).
   // The reference's R is Householder's (well-determined only in the rows
   // where |R_ii| >> sqrt(eps)|C|); an unshifted Cholesky of the Gram turns the
@@ -370,6 +380,7 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
     __syncthreads();
   }
 
+  stamp(7);
   // ---- H: sign rule on U_R = R V (R = L^T), weights, singular values
   for (int k = warp; k < K; k += nwarps) {
     const double* z = Z + (size_t)k * n;
@@ -392,19 +403,23 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
     for (int i = 0; i < n; ++i)
       if (!isfinite(dd[i]) || !isfinite(G[(size_t)i * n + i])) { atomicOr(status, PSVD_ST_NONFINITE); break; }
   }
+  __syncthreads();
+  stamp(8);
 }
 
+bool eig_supported(int n, int K) { return n >= 1 && K >= 1 && K <= n && K <= 1024; }
+
 void launch_eig_topk(const double* G, int n, int K, const double* dscale, double* W, double* sigma,
-                     double* ws, int* status, cudaStream_t st) {
+                     double* ws, int* status, long long* timers, cudaStream_t st) {
   const size_t vec = (size_t)6 * n + K + 64 + (K + 1) / 2 + 2;
   if (n <= EIG_NMAX_SMEM) {
     const size_t smem = ((size_t)n * (n + 1) / 2 + vec) * sizeof(double);
     cudaFuncSetAttribute(eig_topk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    eig_topk_kernel<true><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status);
+    eig_topk_kernel<true><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers);
   } else {
     const size_t smem = vec * sizeof(double);
     cudaFuncSetAttribute(eig_topk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    eig_topk_kernel<false><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status);
+    eig_topk_kernel<false><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers);
   }
 }
 

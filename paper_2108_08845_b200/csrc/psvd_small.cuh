@@ -27,8 +27,10 @@ void launch_extract_rect(const double* tiles, int NB, int r0, int nr, int c0, in
 //   W[:, k] = dscale .* V[:, k] * sign_k / sigma_k   (dscale may be null).
 // ws: global scratch of eig_workspace_doubles(n, K) doubles.
 size_t eig_workspace_doubles(int n, int K);
+// timers (optional, device): clock64() at the 9 phase boundaries (diagnostics).
 void launch_eig_topk(const double* G, int n, int K, const double* dscale, double* W, double* sigma,
-                     double* ws, int* status, cudaStream_t st);
+                     double* ws, int* status, long long* timers, cudaStream_t st);
+bool eig_supported(int n, int K);
 
 // Drift check of streaming.py:106-115 on the K x K Gram UtU = U_new^T U_new:
 // if max|UtU - I| > tol: T = rr^{-1}[:, order] with rr = chol(UtU) (= qr(U).R),
