@@ -101,6 +101,20 @@ int psvd_stream_update(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, c
                        double ff, int Kc, const double* A, int64_t lda, int B, int K, int rescue,
                        double* U_out, int64_t ldo, double* sigma_out, void* stream);
 
+/* ---- randomized streaming update (low_rank_svd of the panel,
+ * linalg.py:126-162) ----
+ * U_out, sigma_out = low_rank_svd([ff U diag(sigma) | A], target_rank = K,
+ * sketch width l = K + oversampling, q power iterations) with the Gaussian
+ * test matrix Omega (n x l, n = Kc + B, col-major ld n) supplied by the caller
+ * (the reference's Philox(seed).standard_normal((n, l)), linalg.py:141-142).
+ * Range basis by SVQB (eigen-orthonormalization of the sketch Gram,
+ * numerically null directions dropped) + one CholeskyQR refinement pass, projection B = Q^T C, one-sided
+ * Jacobi SVD of B, and the tall sign rule on U (global argmax per column,
+ * lowest row on ties, linalg.py:81-91, 161).  Kc = 0 for the first batch. */
+int psvd_rand_update(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, const double* sigma, double ff,
+                     int Kc, const double* A, int64_t lda, int B, int K, int l, int q, const double* Omega,
+                     double* U_out, int64_t ldo, double* sigma_out, void* stream);
+
 /* ---- row-parallel helpers ---- */
 
 /* out (n x n) = sum_r parts[r] in rank order (parts: P contiguous n x n blocks);

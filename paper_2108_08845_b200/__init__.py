@@ -10,7 +10,7 @@ from .datagen import burgers_device, burgers_matrix, burgers_solution, partition
 from .dsvd import (LocalModes, RankContext, gather_modes, parallel_stream_incorporate,  # noqa: F401
                    parallel_stream_initialize)
 from .errors import CapacityError, CollectiveTimeout, ConvergenceError, DegenerateModeError  # noqa: F401
-from .linalg import RandomSketchConfig  # noqa: F401
+from .linalg import RandomSketchConfig, low_rank_svd  # noqa: F401
 from .streaming import StreamConfig, StreamState, stream_all, stream_incorporate, stream_initialize  # noqa: F401
 
 __version__ = "0.1.0"

@@ -46,6 +46,8 @@ _SIGS = {
     "psvd_drift_rescue": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _vp, _vp, _c_dbl, _vp]),
     "psvd_stream_update": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_int, _vp, _c_i64, _c_int,
                                     _c_int, _c_int, _vp, _c_i64, _vp, _vp]),
+    "psvd_rand_update": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_int, _vp, _c_i64, _c_int, _c_int,
+                                  _c_int, _c_int, _vp, _vp, _c_i64, _vp, _vp]),
     "psvd_sum_ordered": (_c_int, [_vp, _vp, _c_int, _c_i64, _vp, _vp]),
     "psvd_burgers": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_dbl,
                               _c_dbl, _c_dbl, _vp]),

@@ -35,6 +35,7 @@ struct psvd_ctx {
   int* h_status = nullptr;  // pinned
   long long launches = 0;   // kernels enqueued by this context (bench evidence)
   Buf partial, tiles, gram, eigws, wbuf, utu, tbuf, dvec, colmax;
+  Buf ybuf, rsmall, jacws;  // randomized path: sketch Y (M x l), small matrices, Jacobi scratch
 };
 
 namespace {
@@ -152,7 +153,7 @@ int plan_tiles(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& ti
 
 // Common pass setup.  segs: panel segments; w/W: optional Y = P[:, wlo:wlo+wk] * W.
 int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, int wlo, int wk, int w,
-              const double* W, int64_t ldw, bool gram_pp, bool gram_yy, bool gram_py) {
+              const double* W, int64_t ldw, bool gram_pp, bool gram_yy, bool gram_py, int py_cols = -1) {
   memset(&ps.p, 0, sizeof(ps.p));
   TallParams& p = ps.p;
   p.M = M;
@@ -185,7 +186,7 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
     for (int I = 0; I < NBp; ++I)
       for (int J = I; J < NBp; ++J) tiles.push_back({I, J});
   if (gram_py)
-    for (int I = 0; I < NBp; ++I)
+    for (int I = 0; I < (py_cols < 0 ? NBp : (py_cols + 31) / 32); ++I)
       for (int J = 0; J < NBy; ++J) tiles.push_back({I, NBp + J});
   if (gram_yy)
     for (int I = 0; I < NBy; ++I)
@@ -311,7 +312,8 @@ int psvd_destroy(psvd_ctx* c) {
   if (!c) return PSVD_OK;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  Buf* bufs[] = {&c->partial, &c->tiles, &c->gram, &c->eigws, &c->wbuf, &c->utu, &c->tbuf, &c->dvec, &c->colmax};
+  Buf* bufs[] = {&c->partial, &c->tiles, &c->gram, &c->eigws, &c->wbuf, &c->utu, &c->tbuf, &c->dvec, &c->colmax,
+                 &c->ybuf, &c->rsmall, &c->jacws};
   for (Buf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
   cudaFree(c->d_status);
@@ -438,6 +440,119 @@ int psvd_stream_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, con
   if ((rc = psvd_recompose(c, M, U, ldu, Kc, A, lda, B, W, K, U_out, ldo, UtU, stream))) return rc;
   if (rescue) rc = psvd_drift_rescue(c, M, U_out, ldo, K, UtU, sigma_out, 1e-8, stream);
   return rc;
+}
+
+// SVQB orthonormalizer of a sketch Gram: T = V diag(1/sqrt(lambda)) with numerically
+// null directions (sigma below rank_tol * sigma_max) dropped (zero columns).
+static int svqb(psvd_ctx* c, const double* Gs, int l, double* T, double* sig_scratch, cudaStream_t st) {
+  int rc = ensure(c, c->eigws, sizeof(double) * eig_workspace_doubles(l, l));
+  if (rc) return rc;
+  launch_eig_topk(Gs, l, l, nullptr, T, sig_scratch, (double*)c->eigws.ptr, c->d_status, nullptr, st, 1e-7);
+  c->launches++;
+  return cuda_check(c, "svqb");
+}
+
+int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const double* sigma, double ff, int Kc,
+                     const double* A, int64_t lda, int B, int K, int l, int q, const double* Omega, double* U_out,
+                     int64_t ldo, double* sigma_out, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = Kc + B;
+  int rc;
+  if (M < 1 || B < 1 || Kc < 0 || K < 1 || l < K || q < 0) return fail(c, PSVD_EINVAL, "bad randomized shape");
+  if (l > std::min<int64_t>(M, n))
+    return fail(c, PSVD_EINVAL, "sketch width %d exceeds min(a.shape) = %lld", l, (long long)std::min<int64_t>(M, n));
+  if (l > MAX_W) return fail(c, PSVD_EINVAL, "sketch width %d exceeds %d", l, MAX_W);
+  if ((rc = check_mat(c, "U", U, ldu, M, Kc)) || (rc = check_mat(c, "A", A, lda, M, B)) ||
+      (rc = check_mat(c, "U_out", U_out, ldo, M, K)))
+    return rc;
+  if (!Omega || !sigma_out || (Kc > 0 && !sigma)) return fail(c, PSVD_EINVAL, "null pointer");
+  const int64_t ldy = M + (M & 1);
+  if ((rc = ensure(c, c->ybuf, sizeof(double) * (size_t)ldy * l))) return rc;
+  // small buffers: W0 (n x l), G1, T1, G2, T2 (l x l), X, Z, Z1, Qz, Bt (n x l), S (l), J (l x l), Wf (l x K), sign (K)
+  const size_t nl = (size_t)n * l, ll = (size_t)l * l;
+  if ((rc = ensure(c, c->rsmall, sizeof(double) * (6 * nl + 6 * ll + 2 * l + (size_t)l * K + K + 64)))) return rc;
+  double* base = (double*)c->rsmall.ptr;
+  double* W0 = base;
+  double* X = W0 + nl;
+  double* Z = X + nl;
+  double* Z1 = Z + nl;
+  double* Qz = Z1 + nl;
+  double* Bt = Qz + nl;
+  double* G1 = Bt + nl;
+  double* T1 = G1 + ll;
+  double* G2 = T1 + ll;
+  double* T2 = G2 + ll;
+  double* J = T2 + ll;
+  double* Tz = J + ll;
+  double* S = Tz + ll;
+  double* sscr = S + l;
+  double* Wf = sscr + l;
+  double* sgn = Wf + (size_t)l * K;
+  double* Y = (double*)c->ybuf.ptr;
+  if ((rc = ensure(c, c->jacws, sizeof(double) * jacobi_workspace_doubles(n, l)))) return rc;
+  if ((rc = make_dvec(c, sigma, ff, Kc, n, st))) return rc;
+  const double* d = (const double*)c->dvec.ptr;
+  launch_scale_rows(Omega, n, n, l, d, W0, n, st);  // Y = [ff U S | A] Omega = [U | A] (D Omega)
+  c->launches++;
+  std::vector<Seg> pa = panel(U, ldu, Kc, A, lda, B);
+  std::vector<Seg> pb = pa;
+  pb.push_back(Seg{Y, ldy, l, 0});
+  for (int it = 0; it <= q; ++it) {
+    // pass A: Y = P W0, Y^T Y
+    Pass ps;
+    if ((rc = plan_pass(c, ps, M, pa, 0, n, l, W0, n, false, true, false))) return rc;
+    ps.p.Yout = Y;
+    ps.p.ldy = ldy;
+    if ((rc = run_pass(c, ps, st))) return rc;
+    launch_extract_sym((const double*)c->tiles.ptr, ps.NB, ps.p.np_pad, l, nullptr, G1, st);
+    c->launches++;
+    if ((rc = svqb(c, G1, l, T1, sscr, st))) return rc;
+    // pass B: Y <- Y T1 (in place), (Y^T Y, D P^T Y)
+    Pass pb_;
+    if ((rc = plan_pass(c, pb_, M, pb, n, l, l, T1, l, false, true, true, n))) return rc;
+    pb_.p.Yout = Y;
+    pb_.p.ldy = ldy;
+    if ((rc = run_pass(c, pb_, st))) return rc;
+    launch_extract_sym((const double*)c->tiles.ptr, pb_.NB, pb_.p.np_pad, l, nullptr, G2, st);
+    launch_extract_rect((const double*)c->tiles.ptr, pb_.NB, 0, n, pb_.p.np_pad, l, d, X, st);
+    c->launches += 2;
+    launch_chol_inv(G2, l, T2, st);  // refinement pass: G2 ~ I, Cholesky is exact enough
+    c->launches++;
+    // Z = C^T Q = (D P^T Y1) T2 = X T2  (= B^T after the last iteration)
+    launch_small_gemm(X, n, 0, T2, l, (it < q) ? Z : Bt, n, n, l, l, nullptr, st);
+    c->launches++;
+    if (it < q) {  // power iteration: Qz = orth(Z) by SVQB twice, next sketch W0 = D Qz
+      launch_small_gemm(Z, n, 1, Z, n, G1, l, l, n, l, nullptr, st);
+      c->launches++;
+      if ((rc = svqb(c, G1, l, Tz, sscr, st))) return rc;
+      launch_small_gemm(Z, n, 0, Tz, l, Z1, n, n, l, l, nullptr, st);
+      launch_small_gemm(Z1, n, 1, Z1, n, G1, l, l, n, l, nullptr, st);
+      launch_chol_inv(G1, l, Tz, st);
+      c->launches += 3;
+      launch_small_gemm(Z1, n, 0, Tz, l, Qz, n, n, l, l, nullptr, st);
+      launch_scale_rows(Qz, n, n, l, d, W0, n, st);
+      c->launches += 2;
+    }
+  }
+  // small SVD of B = Q^T C (l x n) through B^T = Bt: U_B = J, S descending
+  launch_jacobi_svd(Bt, n, l, S, J, (double*)c->jacws.ptr, c->d_status, st);
+  // U = Q U_B[:, :K] = Y1 (T2 J[:, :K])
+  launch_small_gemm(T2, l, 0, J, l, Wf, l, l, l, K, nullptr, st);
+  c->launches += 2;
+  Pass pc;
+  if ((rc = plan_pass(c, pc, M, {Seg{Y, ldy, l, 0}}, 0, l, K, Wf, l, false, false, false))) return rc;
+  const int nchunks = pc.map.nchunks;
+  if ((rc = ensure(c, c->colmax, sizeof(double) * (size_t)nchunks * K * 2))) return rc;
+  pc.p.Yout = U_out;
+  pc.p.ldy = ldo;
+  pc.p.colmax = (double*)c->colmax.ptr;
+  if ((rc = run_pass(c, pc, st))) return rc;
+  launch_colmax_sign((const double*)c->colmax.ptr, nchunks, K, sgn, st);
+  launch_scale_cols(U_out, ldo, M, K, sgn, st);
+  cudaMemcpyAsync(sigma_out, S, sizeof(double) * K, cudaMemcpyDeviceToDevice, st);
+  c->launches += 2;
+  return cuda_check(c, "randomized update");
 }
 
 int psvd_sum_ordered(psvd_ctx* c, const double* parts, int P, int64_t count, double* out, void* stream) {

@@ -1,0 +1,245 @@
+// Small kernels of the randomized update (reference linalg.py:126-162 composed
+// per batch): one-sided Jacobi SVD of the projected core, tiny
+// dense products, and the tall sign rule (linalg.py:161, 81-91).
+#include <cfloat>
+#include "psvd_small.cuh"
+
+namespace psvd {
+
+// ---------------------------------------------------------------- small dense GEMM
+// C (m x k2) = op(A) (m x k1) * B (k1 x k2), col-major; op(A) = A (lda rows) or A^T.
+// One thread per output entry, fixed summation order (deterministic).
+__global__ void small_gemm_kernel(const double* __restrict__ A, int lda, int transA, const double* __restrict__ B,
+                                  int ldb, double* __restrict__ C, int ldc, int m, int k1, int k2,
+                                  const double* __restrict__ rowscale) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)m * k2) return;
+  const int i = (int)(idx % m), j = (int)(idx / m);
+  double s = 0.0;
+  if (transA) {
+    for (int k = 0; k < k1; ++k) s = fma(A[(size_t)i * lda + k], B[(size_t)j * ldb + k], s);
+  } else {
+    for (int k = 0; k < k1; ++k) s = fma(A[(size_t)k * lda + i], B[(size_t)j * ldb + k], s);
+  }
+  if (rowscale) s *= rowscale[i];
+  C[(size_t)j * ldc + i] = s;
+}
+
+void launch_small_gemm(const double* A, int lda, int transA, const double* B, int ldb, double* C, int ldc, int m,
+                       int k1, int k2, const double* rowscale, cudaStream_t st) {
+  const int64_t tot = (int64_t)m * k2;
+  small_gemm_kernel<<<(unsigned)((tot + 127) / 128), 128, 0, st>>>(A, lda, transA, B, ldb, C, ldc, m, k1, k2,
+                                                                    rowscale);
+}
+
+// ---------------------------------------------------------------- one-sided Jacobi SVD
+// Z (n x l, col-major ld n) = V S J^T.  Outputs S (l, descending) and J (l x l,
+// col-major, columns in the order of S): for Z = B^T (B = Q^T C) J is U_B of
+// svd(B).  Parallel round-robin ordering, one warp per column pair.
+template <bool SMEM>
+__global__ void __launch_bounds__(1024, 1)
+jacobi_svd_kernel(const double* __restrict__ Zin, int n, int l, double* __restrict__ S, double* __restrict__ Jout,
+                  double* __restrict__ ws, int* __restrict__ status) {
+  extern __shared__ double sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int le = l + (l & 1);  // even number of columns (a zero column pads odd l)
+  double* Z = SMEM ? sm : ws;
+  double* J = SMEM ? sm + (size_t)n * le : sm;
+  double* nrm = J + (size_t)le * le;
+  int* order = reinterpret_cast<int*>(nrm + le);
+  int* flag = order + le + 1;
+  for (int64_t i = tid; i < (int64_t)n * le; i += blockDim.x) {
+    const int c = (int)(i / n);
+    Z[i] = c < l ? Zin[i] : 0.0;
+  }
+  for (int i = tid; i < le * le; i += blockDim.x) J[i] = (i % le == i / le) ? 1.0 : 0.0;
+  __syncthreads();
+  const int npair = le / 2;
+  for (int sweep = 0; sweep < 40; ++sweep) {
+    if (tid == 0) *flag = 0;
+    __syncthreads();
+    for (int r = 0; r < le - 1; ++r) {
+      for (int k = warp; k < npair; k += nwarps) {
+        int p, q;
+        if (k == 0) {
+          p = le - 1;
+          q = r;
+        } else {
+          p = (r + k) % (le - 1);
+          q = (r - k + le - 1) % (le - 1);
+        }
+        if (p > q) { const int t = p; p = q; q = t; }
+        double* zp = Z + (size_t)p * n;
+        double* zq = Z + (size_t)q * n;
+        double a = 0.0, b = 0.0, c = 0.0;
+        for (int i = lane; i < n; i += 32) {
+          const double x = zp[i], y = zq[i];
+          a = fma(x, x, a);
+          b = fma(y, y, b);
+          c = fma(x, y, c);
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        c = warp_sum(c);
+        if (c != 0.0 && fabs(c) > DBL_EPSILON * sqrt(a * b)) {
+          const double zeta = (b - a) / (2.0 * c);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+          for (int i = lane; i < n; i += 32) {
+            const double x = zp[i], y = zq[i];
+            zp[i] = cs * x - sn * y;
+            zq[i] = sn * x + cs * y;
+          }
+          double* jp = J + (size_t)p * le;
+          double* jq = J + (size_t)q * le;
+          for (int i = lane; i < le; i += 32) {
+            const double x = jp[i], y = jq[i];
+            jp[i] = cs * x - sn * y;
+            jq[i] = sn * x + cs * y;
+          }
+          if (lane == 0) *flag = 1;
+        }
+      }
+      __syncthreads();
+    }
+    const int f = *flag;
+    __syncthreads();
+    if (f == 0) break;
+    if (sweep == 39 && tid == 0) atomicOr(status, PSVD_ST_NOCONVERGE);
+  }
+  for (int c = warp; c < le; c += nwarps) {
+    double s = 0.0;
+    for (int i = lane; i < n; i += 32) s = fma(Z[(size_t)c * n + i], Z[(size_t)c * n + i], s);
+    s = warp_sum(s);
+    if (lane == 0) nrm[c] = sqrt(s);
+  }
+  __syncthreads();
+  if (tid == 0) {  // stable sort by descending singular value
+    for (int c = 0; c < le; ++c) order[c] = c;
+    for (int a = 1; a < le; ++a) {
+      const int oa = order[a];
+      int b = a - 1;
+      while (b >= 0 && nrm[order[b]] < nrm[oa]) { order[b + 1] = order[b]; --b; }
+      order[b + 1] = oa;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < l; i += blockDim.x) S[i] = nrm[order[i]];
+  for (int i = tid; i < l * l; i += blockDim.x) {
+    const int r = i % l, c = i / l;
+    Jout[(size_t)c * l + r] = J[(size_t)order[c] * le + r];
+  }
+}
+
+size_t jacobi_workspace_doubles(int n, int l) { return (size_t)n * (l + 1); }
+
+void launch_jacobi_svd(const double* Z, int n, int l, double* S, double* J, double* ws, int* status, cudaStream_t st) {
+  const int le = l + (l & 1);
+  const size_t small = (size_t)le * le + le + le + 8;
+  const size_t limit = 227 * 1024 / sizeof(double);
+  if ((size_t)n * le + small <= limit) {
+    const size_t smem = ((size_t)n * le + small) * sizeof(double);
+    cudaFuncSetAttribute(jacobi_svd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    jacobi_svd_kernel<true><<<1, 1024, smem, st>>>(Z, n, l, S, J, ws, status);
+  } else {
+    const size_t smem = small * sizeof(double);
+    cudaFuncSetAttribute(jacobi_svd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    jacobi_svd_kernel<false><<<1, 1024, smem, st>>>(Z, n, l, S, J, ws, status);
+  }
+}
+
+// ---------------------------------------------------------------- Cholesky refinement
+// T = R^{-1} for R = chol(G) (upper, G = R^T R, l <= 128).  Used for the second
+// orthonormalization pass of a sketch whose Gram is already ~I (CholeskyQR2's
+// refinement step); columns of a numerically null direction (pivot <= tiny)
+// are zeroed, matching the first (SVQB) pass which dropped them.
+__global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restrict__ G, int l, double* __restrict__ T) {
+  extern __shared__ double sm[];
+  double* R = sm;          // l x l col-major, upper used
+  double* X = R + l * l;   // inverse
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  double dmax = 0.0;
+  for (int i = 0; i < l; ++i) dmax = fmax(dmax, G[(size_t)i * l + i]);
+  const double tiny = 64.0 * DBL_EPSILON * dmax;
+  for (int idx = tid; idx < l * l; idx += nthr) R[idx] = G[idx];
+  __syncthreads();
+  // right-looking Cholesky on the upper triangle: R[k][j] for j >= k
+  for (int k = 0; k < l; ++k) {
+    const double piv = R[(size_t)k * l + k];
+    const bool ok = piv > tiny;
+    const double rk = ok ? sqrt(piv) : 0.0;
+    __syncthreads();
+    for (int j = k + tid; j < l; j += nthr) R[(size_t)j * l + k] = ok ? (j == k ? rk : R[(size_t)j * l + k] / rk) : 0.0;
+    __syncthreads();
+    for (int idx = tid; idx < l * l; idx += nthr) {
+      const int i = idx % l, j = idx / l;
+      if (i > k && j >= i) R[(size_t)j * l + i] -= R[(size_t)i * l + k] * R[(size_t)j * l + k];
+    }
+    __syncthreads();
+  }
+  // X = R^{-1} (upper): column j by back substitution, zero rows for zero pivots
+  for (int j = tid; j < l; j += nthr) {
+    for (int i = l - 1; i >= 0; --i) {
+      double s = (i == j) ? 1.0 : 0.0;
+      for (int q = i + 1; q <= j; ++q) s -= R[(size_t)q * l + i] * X[(size_t)j * l + q];
+      const double d = R[(size_t)i * l + i];
+      X[(size_t)j * l + i] = (i <= j && d != 0.0) ? s / d : 0.0;
+    }
+  }
+  __syncthreads();
+  for (int idx = tid; idx < l * l; idx += nthr) T[idx] = X[idx];
+}
+
+void launch_chol_inv(const double* G, int l, double* T, cudaStream_t st) {
+  const size_t smem = 2 * (size_t)l * l * sizeof(double);
+  cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  chol_inv_kernel<<<1, 1024, smem, st>>>(G, l, T);
+}
+
+// ---------------------------------------------------------------- tall sign rule
+// colmax: [nchunks][K][2] = (signed value at max |u|, global row) per chunk in row
+// order; the first chunk wins ties (lowest row, numpy argmax).  sign = +1 for >= 0.
+__global__ void colmax_sign_kernel(const double* __restrict__ colmax, int nchunks, int K, double* __restrict__ sign) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  double best = -1.0, val = 0.0;
+  for (int c = 0; c < nchunks; ++c) {
+    const double v = colmax[((size_t)c * K + k) * 2];
+    if (fabs(v) > best) {
+      best = fabs(v);
+      val = v;
+    }
+  }
+  sign[k] = val < 0.0 ? -1.0 : 1.0;
+}
+
+void launch_colmax_sign(const double* colmax, int nchunks, int K, double* sign, cudaStream_t st) {
+  colmax_sign_kernel<<<(K + 127) / 128, 128, 0, st>>>(colmax, nchunks, K, sign);
+}
+
+__global__ void scale_cols_kernel(double* __restrict__ U, int64_t ld, int64_t M, int K, const double* __restrict__ s) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int k = blockIdx.y;
+  if (i >= M || k >= K) return;
+  if (s[k] < 0.0) U[(size_t)k * ld + i] = -U[(size_t)k * ld + i];
+}
+
+void launch_scale_cols(double* U, int64_t ld, int64_t M, int K, const double* s, cudaStream_t st) {
+  dim3 g((unsigned)((M + 255) / 256), (unsigned)K);
+  scale_cols_kernel<<<g, 256, 0, st>>>(U, ld, M, K, s);
+}
+
+__global__ void scale_rows_kernel(const double* __restrict__ X, int ldx, int m, int k, const double* __restrict__ d,
+                                  double* __restrict__ Y, int ldy) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)m * k) return;
+  const int i = (int)(idx % m), j = (int)(idx / m);
+  Y[(size_t)j * ldy + i] = d[i] * X[(size_t)j * ldx + i];
+}
+
+void launch_scale_rows(const double* X, int ldx, int m, int k, const double* d, double* Y, int ldy, cudaStream_t st) {
+  const int64_t tot = (int64_t)m * k;
+  scale_rows_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(X, ldx, m, k, d, Y, ldy);
+}
+
+}  // namespace psvd

@@ -81,7 +81,7 @@ template <bool SMEM>
 __global__ void __launch_bounds__(SMALL_THREADS, 1)
 eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __restrict__ dscale,
                 double* __restrict__ W, double* __restrict__ sigma_out, double* __restrict__ ws,
-                int* __restrict__ status, long long* __restrict__ timers) {
+                int* __restrict__ status, long long* __restrict__ timers, double rank_tol) {
   extern __shared__ double sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nthr = blockDim.x, nwarps = nthr >> 5;
@@ -394,8 +394,10 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
     }
     const double sg = best_val < 0.0 ? -1.0 : 1.0;
     const double sk = sqrt(fmax(lam[k], 0.0));
-    const double inv = sk > 0.0 ? sg / sk : 0.0;
-    if (sk == 0.0 && lane == 0) atomicOr(status, PSVD_ST_RANKDEF);
+    const double s0 = sqrt(fmax(lam[0], 0.0));
+    const bool keep = sk > 0.0 && sk > rank_tol * s0;  // rank_tol > 0: drop numerically null directions
+    const double inv = keep ? sg / sk : 0.0;
+    if (sk == 0.0 && rank_tol == 0.0 && lane == 0) atomicOr(status, PSVD_ST_RANKDEF);
     for (int i = lane; i < n; i += 32) W[(size_t)k * n + i] = (dscale ? dscale[i] : 1.0) * z[i] * inv;
     if (lane == 0) sigma_out[k] = sk;
   }
@@ -410,16 +412,16 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
 bool eig_supported(int n, int K) { return n >= 1 && K >= 1 && K <= n && K <= 1024; }
 
 void launch_eig_topk(const double* G, int n, int K, const double* dscale, double* W, double* sigma,
-                     double* ws, int* status, long long* timers, cudaStream_t st) {
+                     double* ws, int* status, long long* timers, cudaStream_t st, double rank_tol) {
   const size_t vec = (size_t)6 * n + K + 64 + (K + 1) / 2 + 2;
   if (n <= EIG_NMAX_SMEM) {
     const size_t smem = ((size_t)n * (n + 1) / 2 + vec) * sizeof(double);
     cudaFuncSetAttribute(eig_topk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    eig_topk_kernel<true><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers);
+    eig_topk_kernel<true><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers, rank_tol);
   } else {
     const size_t smem = vec * sizeof(double);
     cudaFuncSetAttribute(eig_topk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    eig_topk_kernel<false><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers);
+    eig_topk_kernel<false><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers, rank_tol);
   }
 }
 

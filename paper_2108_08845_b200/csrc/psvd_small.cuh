@@ -29,7 +29,7 @@ void launch_extract_rect(const double* tiles, int NB, int r0, int nr, int c0, in
 size_t eig_workspace_doubles(int n, int K);
 // timers (optional, device): clock64() at the 9 phase boundaries (diagnostics).
 void launch_eig_topk(const double* G, int n, int K, const double* dscale, double* W, double* sigma,
-                     double* ws, int* status, long long* timers, cudaStream_t st);
+                     double* ws, int* status, long long* timers, cudaStream_t st, double rank_tol = 0.0);
 bool eig_supported(int n, int K);
 
 // Drift check of streaming.py:106-115 on the K x K Gram UtU = U_new^T U_new:
@@ -37,5 +37,15 @@ bool eig_supported(int n, int K);
 // sigma <- (sigma * |diag rr|)[order] (stable descending), *gate = 1; else *gate = 0.
 void launch_drift_check(const double* UtU, int K, double tol, double* sigma, double* T, int* gate,
                         int* status, cudaStream_t st);
+
+// ---- randomized-update helpers (psvd_rand.cu)
+void launch_small_gemm(const double* A, int lda, int transA, const double* B, int ldb, double* C, int ldc, int m,
+                       int k1, int k2, const double* rowscale, cudaStream_t st);
+size_t jacobi_workspace_doubles(int n, int l);
+void launch_jacobi_svd(const double* Z, int n, int l, double* S, double* J, double* ws, int* status, cudaStream_t st);
+void launch_chol_inv(const double* G, int l, double* T, cudaStream_t st);
+void launch_colmax_sign(const double* colmax, int nchunks, int K, double* sign, cudaStream_t st);
+void launch_scale_cols(double* U, int64_t ld, int64_t M, int K, const double* s, cudaStream_t st);
+void launch_scale_rows(const double* X, int ldx, int m, int k, const double* d, double* Y, int ldy, cudaStream_t st);
 
 }  // namespace psvd

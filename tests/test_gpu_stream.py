@@ -230,3 +230,49 @@ def test_parallel_golden_via_rank_emulation(golden):
         U, sig = newU, s_new
     modes = torch.cat([u.view for u in U], 0).cpu().numpy()
     _assert_parity(modes, sig.cpu().numpy(), g["modes"], g["sigma"])
+
+
+# ---------------------------------------------------------------- randomized path (R8/R9)
+
+@pytest.mark.parametrize("q", [0, 1])
+def test_randomized_stream_golden(golden, q):
+    p = _pkg()
+    g = golden("rand_burgers2048")
+    a = p.burgers_matrix(2048, 800)
+    sk = p.RandomSketchConfig(target_rank=10, oversampling=10, power_iterations=q, seed=0)
+    cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200, sketch=sk)
+    state, hist = p.stream_all(_batches(a, 200), cfg)
+    modes, sigma = _np(state)
+    for h, gh in zip(hist, g[f"q{q}_history"]):
+        assert oracle.sigma_rel_err(h.cpu().numpy(), gh) <= SIG_TOL
+    _assert_parity(modes, sigma, g[f"q{q}_modes"], g[f"q{q}_sigma"])
+
+
+def test_low_rank_svd_small_golden(golden):
+    p = _pkg()
+    g = golden("rand_small")
+    u, s = p.low_rank_svd(g["lowrank_a"], p.RandomSketchConfig(target_rank=3, oversampling=5, power_iterations=1,
+                                                               seed=1))
+    _assert_parity(u.cpu().numpy(), s.cpu().numpy(), g["lowrank_u"], g["lowrank_s"])
+    u, s = p.low_rank_svd(g["gauss_a"], p.RandomSketchConfig(target_rank=4, oversampling=2, power_iterations=0,
+                                                             seed=99))
+    _assert_parity(u.cpu().numpy(), s.cpu().numpy(), g["gauss_u"], g["gauss_s"], sig_tol=1e-10, ang_tol=1e-8)
+
+
+@pytest.mark.parametrize("rows,k,p_,q,ff", [(65536, 10, 10, 1, 0.95), (30011, 16, 8, 0, 0.9), (5000, 30, 10, 2, 1.0)])
+def test_randomized_vs_oracle(rows, k, p_, q, ff):
+    p = _pkg()
+    a = oracle.burgers_matrix(rows, 800)[:, :600]
+    ref_m, ref_s, _ = oracle.ref_rand_stream_all(_batches(a, 200), k, ff, p_, q, 3)
+    sk = p.RandomSketchConfig(target_rank=k, oversampling=p_, power_iterations=q, seed=3)
+    st, _ = p.stream_all(_batches(a, 200), p.StreamConfig(k_modes=k, forget_factor=ff, batch_columns=200, sketch=sk))
+    m, s = _np(st)
+    _assert_parity(m, s, ref_m, ref_s)
+
+
+def test_randomized_validation():
+    p = _pkg()
+    with pytest.raises(ValueError):
+        p.low_rank_svd(np.eye(4), p.RandomSketchConfig(target_rank=3, oversampling=2))
+    with pytest.raises(ValueError):
+        p.StreamConfig(k_modes=4, sketch=p.RandomSketchConfig(target_rank=3))
