@@ -59,7 +59,7 @@ def load_peaks():
 def args_():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--path", default="det", choices=["det", "rand"])
@@ -67,6 +67,7 @@ def args_():
     ap.add_argument("--cpu-rows", type=int, default=1 << 17, help="row sample for the CPU baseline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-rand", action="store_true")
     return ap.parse_args()
 
 
@@ -333,6 +334,9 @@ def run_ours(a):
     if not a.no_e2e:
         line["e2e"] = e2e(a, p, D, M, dev, world, ctxr)
 
+    if world == 1 and not a.no_rand:
+        line["randomized"] = {f"q{qq}": time_randomized(a, D, M, dev, c, stream, qq) for qq in (0, 1)}
+
     if world == 1 and rank == 0 and not a.no_cpu:
         g, dt = cpu_reference_gbs(a.cpu_rows, a.path)
         cores = os.cpu_count()
@@ -344,6 +348,44 @@ def run_ours(a):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def time_randomized(a, D, M, dev, c, stream, q):
+    """Device-resident randomized stream (R9: low_rank_svd of [ff U S | A_i] per
+    batch, p = 10, seed 0) over the same 4 batches; snapshot GB/s."""
+    import torch
+    from paper_2108_08845_b200 import _native as nat
+    from paper_2108_08845_b200.linalg import RandomSketchConfig, device_omega
+    sk = RandomSketchConfig(target_rank=K, oversampling=10, power_iterations=q, seed=0)
+    l = sk.sketch_width
+    st = nat._vp(stream.cuda_stream)
+    om = {n: device_omega(n, sk, dev) for n in (BATCH, K + BATCH)}
+    Ub = [nat.DevMat.empty(M, K, dev) for _ in range(2)]
+    sig = [torch.zeros(K, dtype=torch.float64, device=dev) for _ in range(2)]
+
+    def step():
+        cur = 0
+        for b in range(SNAPS // BATCH):
+            kc = 0 if b == 0 else K
+            nat.call("psvd_rand_update", c, M, nat._vp(Ub[cur].data_ptr()), Ub[cur].ld, nat.ptr(sig[cur]), FF, kc,
+                     nat._vp(D.data_ptr() + 8 * D.ld * b * BATCH), D.ld, BATCH, K, l, q, nat.ptr(om[kc + BATCH]),
+                     nat._vp(Ub[cur ^ 1].data_ptr()), Ub[cur ^ 1].ld, nat.ptr(sig[cur ^ 1]), st)
+            cur ^= 1
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(a.steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / a.steps
+    passes = 2 * (q + 1)
+    alg = sum(8.0 * M * (passes * (BATCH + (0 if b == 0 else K)) + K) for b in range(SNAPS // BATCH))
+    return {"value": round(8.0 * a.rows * SNAPS / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms, 4),
+            "sketch": f"K={K} p=10 q={q} seed=0", "hbm_frac": round(alg / (ms * 1e-3) / 1e9 / HBM_PEAK[0], 4)}
 
 
 def e2e(a, p, D, M, dev, world, ctxr):
