@@ -89,6 +89,13 @@ int psvd_recompose(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, int K
                    int64_t lda, int B, const double* W, int K, double* U_out, int64_t ldo, double* UtU,
                    void* stream);
 
+/* Rayleigh refinement after a recompose: with UtU = U^T U (K x K, summed over
+ * ranks in the row-parallel case), sigma_k <- sigma_k * sqrt(UtU_kk) (= ||C v_k||),
+ * U[:, k] /= sqrt(UtU_kk), UtU normalized in place.  Second-order accurate in
+ * the Gram eigenvector error (sqrt(lambda) alone is eps*kappa^2). */
+int psvd_refine_normalize(psvd_ctx* ctx, int64_t M, double* U, int64_t ldu, int K, double* UtU, double* sigma,
+                          void* stream);
+
 /* Drift rescue of streaming.py:106-115 driven by UtU on the device: if
  * max|UtU - I| > tol, U <- qr(U).q reordered and sigma <- sigma*|diag r|
  * reordered (stable descending); otherwise a no-op.  In place. */
@@ -100,6 +107,19 @@ int psvd_drift_rescue(psvd_ctx* ctx, int64_t M, double* U, int64_t ldu, int K, c
 int psvd_stream_update(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, const double* sigma,
                        double ff, int Kc, const double* A, int64_t lda, int B, int K, int rescue,
                        double* U_out, int64_t ldo, double* sigma_out, void* stream);
+
+/* Whole deterministic stream (stream_all, streaming.py:119-133, or its
+ * continuation from a state when Kc == K) over nb batches A[b] (M x B[b],
+ * device pointers in a host array).  Same per-batch arithmetic as
+ * psvd_stream_update; the A^T A Gram of batch b+1 runs on a low-priority
+ * internal stream while the core solve of batch b runs on a high-priority
+ * one.  Updates alternate between U_a and U_b (M x K, ld ldo; U_in must not
+ * alias U_a); *final_buf receives 0 or 1.  sigma_hist: device, nb x K (the
+ * singular values after every step).  Ordered after prior work on `stream`
+ * and joined back into it. */
+int psvd_stream_run(psvd_ctx* ctx, int64_t M, const double* U_in, int64_t ldu, const double* sigma_in, int Kc,
+                    int nb, const double* const* A, const int64_t* lda, const int* B, int K, double ff, int rescue,
+                    double* U_a, double* U_b, int64_t ldo, double* sigma_hist, int* final_buf, void* stream);
 
 /* ---- randomized streaming update (low_rank_svd of the panel,
  * linalg.py:126-162) ----

@@ -13,4 +13,6 @@ from .errors import CapacityError, CollectiveTimeout, ConvergenceError, Degenera
 from .linalg import RandomSketchConfig, low_rank_svd  # noqa: F401
 from .streaming import StreamConfig, StreamState, stream_all, stream_incorporate, stream_initialize  # noqa: F401
 
+from . import streaming  # noqa: F401,E402  (module access: STREAM_WINDOW)
+
 __version__ = "0.1.0"

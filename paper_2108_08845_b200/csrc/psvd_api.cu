@@ -7,6 +7,7 @@
 #include <string>
 #include <vector>
 #include <algorithm>
+#include <cstdlib>
 
 #include "../../include/psvd.h"
 #include "psvd_small.cuh"
@@ -36,6 +37,9 @@ struct psvd_ctx {
   long long launches = 0;   // kernels enqueued by this context (bench evidence)
   Buf partial, tiles, gram, eigws, wbuf, utu, tbuf, dvec, colmax;
   Buf ybuf, rsmall, jacws;  // randomized path: sketch Y (M x l), small matrices, Jacobi scratch
+  Buf partial2, tiles2[2];  // A^T A passes on the low-priority stream (double-buffered tiles)
+  cudaStream_t s_hi = nullptr, s_lo = nullptr;  // pipelined stream_run: critical chain / look-ahead Grams
+  cudaEvent_t ev_aa[2] = {nullptr, nullptr}, ev_asm[2] = {nullptr, nullptr}, ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace {
@@ -93,10 +97,12 @@ struct Pass {
   ReduceMap map;
   int grid = 0;
   int NB = 0;
+  Buf* part = nullptr;  // partial-tile workspace of the stream this pass runs on
+  Buf* tl = nullptr;    // reduced tiles
 };
 
 // Fill the warp plans / reduce map for a tile list (I <= J, 32-col blocks of [P | Y]).
-int plan_tiles(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& tiles) {
+int plan_tiles(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& tiles, bool allow_ksplit) {
   const int nt = (int)tiles.size();
   memset(ps.p.plan, 0, sizeof(ps.p.plan));
   memset(&ps.map, 0, sizeof(ps.map));
@@ -133,7 +139,7 @@ int plan_tiles(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& ti
       }
     } else {
       int ksplit = 1;
-      while (ksplit * 2 * ns <= NWARP) ksplit *= 2;
+      while (allow_ksplit && ksplit * 2 * ns <= NWARP) ksplit *= 2;
       for (int w = 0; w < ns * ksplit; ++w) {
         WarpPlan& wp = ps.p.plan[s][w];
         const int li = w % ns;
@@ -153,8 +159,11 @@ int plan_tiles(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& ti
 
 // Common pass setup.  segs: panel segments; w/W: optional Y = P[:, wlo:wlo+wk] * W.
 int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, int wlo, int wk, int w,
-              const double* W, int64_t ldw, bool gram_pp, bool gram_yy, bool gram_py, int py_cols = -1) {
+              const double* W, int64_t ldw, bool gram_pp, bool gram_yy, bool gram_py, int py_cols = -1,
+              int pp_rows = -1, Buf* part = nullptr, Buf* tl = nullptr, int max_ctas = 0) {
   memset(&ps.p, 0, sizeof(ps.p));
+  ps.part = part ? part : &c->partial;
+  ps.tl = tl ? tl : &c->tiles;
   TallParams& p = ps.p;
   p.M = M;
   p.nseg = (int)segs.size();
@@ -183,7 +192,7 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
   ps.NB = NBp + NBy;
   std::vector<std::pair<int, int>> tiles;
   if (gram_pp)
-    for (int I = 0; I < NBp; ++I)
+    for (int I = 0; I < (pp_rows < 0 ? NBp : std::min(NBp, (pp_rows + 31) / 32)); ++I)
       for (int J = I; J < NBp; ++J) tiles.push_back({I, J});
   if (gram_py)
     for (int I = 0; I < (py_cols < 0 ? NBp : (py_cols + 31) / 32); ++I)
@@ -191,11 +200,13 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
   if (gram_yy)
     for (int I = 0; I < NBy; ++I)
       for (int J = I; J < NBy; ++J) tiles.push_back({NBp + I, NBp + J});
-  int rc = plan_tiles(c, ps, tiles);
+  // k-splitting only pays for FP64-heavy Gram-only passes; Y passes are HBM-bound
+  int rc = plan_tiles(c, ps, tiles, w == 0);
   if (rc) return rc;
   // grid: one CTA per SM (1 CTA/SM by smem), chunks of 32-row multiples
   const int64_t stages32 = (M + 31) / 32;
-  int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(stages32, c->num_sms / p.nslices));
+  const int ctas = max_ctas > 0 ? std::min(max_ctas, c->num_sms) : c->num_sms;
+  int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(stages32, std::max(1, ctas / p.nslices)));
   int64_t rows = (stages32 + nchunks - 1) / nchunks * 32;
   nchunks = (M + rows - 1) / rows;
   p.rows_per_cta = rows;
@@ -203,11 +214,11 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
   ps.map.nchunks = (int)nchunks;
   ps.map.nslices = p.nslices;
   if (!tiles.empty()) {
-    int rc2 = ensure(c, c->partial, sizeof(double) * (size_t)ps.grid * SLOTS * 1024);
+    int rc2 = ensure(c, *ps.part, sizeof(double) * (size_t)ps.grid * SLOTS * 1024);
     if (rc2) return rc2;
-    rc2 = ensure(c, c->tiles, sizeof(double) * (size_t)ps.NB * ps.NB * 1024);
+    rc2 = ensure(c, *ps.tl, sizeof(double) * (size_t)ps.NB * ps.NB * 1024);
     if (rc2) return rc2;
-    p.partial = (double*)c->partial.ptr;
+    p.partial = (double*)ps.part->ptr;
   }
   return PSVD_OK;
 }
@@ -218,7 +229,7 @@ int run_pass(psvd_ctx* c, Pass& ps, cudaStream_t st) {
   int rc = cuda_check(c, "tall pass");
   if (rc) return rc;
   if (ps.map.nout > 0) {
-    launch_tall_reduce((const double*)c->partial.ptr, ps.map, (double*)c->tiles.ptr, st);
+    launch_tall_reduce((const double*)ps.part->ptr, ps.map, (double*)ps.tl->ptr, st);
     rc = cuda_check(c, "tall reduce");
   }
   return rc;
@@ -242,6 +253,12 @@ std::vector<Seg> panel(const double* U, int64_t ldu, int Kc, const double* A, in
   if (Kc > 0) s.push_back(Seg{U, ldu, Kc, 0});
   if (B > 0) s.push_back(Seg{A, lda, B, 0});
   return s;
+}
+
+__global__ void stamp_kernel(unsigned long long* out) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = t;
 }
 
 __global__ void sum_ordered_kernel(const double* __restrict__ parts, int P, int64_t count, double* __restrict__ out) {
@@ -303,6 +320,18 @@ int psvd_create(int device, psvd_ctx** out) {
     return PSVD_ECUDA;
   }
   cudaMemset(c->d_status, 0, 2 * sizeof(int));
+  {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);  // numerically: hi <= lo (smaller = higher priority)
+    cudaStreamCreateWithPriority(&c->s_hi, cudaStreamNonBlocking, hi);
+    cudaStreamCreateWithPriority(&c->s_lo, cudaStreamNonBlocking, lo);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventCreateWithFlags(&c->ev_aa[i], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&c->ev_asm[i], cudaEventDisableTiming);
+    }
+    cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+  }
   cudaDeviceSynchronize();
   *out = c;
   return PSVD_OK;
@@ -313,9 +342,17 @@ int psvd_destroy(psvd_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   Buf* bufs[] = {&c->partial, &c->tiles, &c->gram, &c->eigws, &c->wbuf, &c->utu, &c->tbuf, &c->dvec, &c->colmax,
-                 &c->ybuf, &c->rsmall, &c->jacws};
+                 &c->ybuf, &c->rsmall, &c->jacws, &c->partial2, &c->tiles2[0], &c->tiles2[1]};
   for (Buf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
+  if (c->s_hi) cudaStreamDestroy(c->s_hi);
+  if (c->s_lo) cudaStreamDestroy(c->s_lo);
+  for (int i = 0; i < 2; ++i) {
+    if (c->ev_aa[i]) cudaEventDestroy(c->ev_aa[i]);
+    if (c->ev_asm[i]) cudaEventDestroy(c->ev_asm[i]);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   cudaFree(c->d_status);
   cudaFree(c->d_timers);
   cudaFreeHost(c->h_status);
@@ -409,7 +446,7 @@ int psvd_drift_rescue(psvd_ctx* c, int64_t M, double* U, int64_t ldu, int K, con
   int rc;
   if ((rc = check_mat(c, "U", U, ldu, M, K))) return rc;
   if (K > MAX_W) return fail(c, PSVD_EINVAL, "K=%d too large for the rescue pass", K);
-  if ((rc = ensure(c, c->tbuf, sizeof(double) * (size_t)K * K))) return rc;
+  if ((rc = ensure(c, c->tbuf, sizeof(double) * ((size_t)K * K + K)))) return rc;
   launch_drift_check(UtU, K, tol, sigma, (double*)c->tbuf.ptr, c->d_gate, c->d_status, st);
   c->launches++;
   if ((rc = cuda_check(c, "drift check"))) return rc;
@@ -421,6 +458,22 @@ int psvd_drift_rescue(psvd_ctx* c, int64_t M, double* U, int64_t ldu, int K, con
   ps.p.gate = c->d_gate;
   return run_pass(c, ps, st);
 }
+
+}  // extern "C"
+
+// sigma_k <- ||C v_k|| and unit columns (Rayleigh refinement), UtU normalized in place
+static int refine_normalize(psvd_ctx* c, int64_t M, double* U, int64_t ld, int K, double* UtU, double* sigma,
+                            cudaStream_t st) {
+  int rc = ensure(c, c->tbuf, sizeof(double) * ((size_t)K * K + K));
+  if (rc) return rc;
+  double* scale = (double*)c->tbuf.ptr + (size_t)K * K;
+  launch_normalize_gram(UtU, K, sigma, scale, st);
+  launch_scale_cols(U, ld, M, K, scale, st);
+  c->launches += 2;
+  return cuda_check(c, "refine");
+}
+
+extern "C" {
 
 int psvd_stream_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const double* sigma, double ff, int Kc,
                        const double* A, int64_t lda, int B, int K, int rescue, double* U_out, int64_t ldo,
@@ -434,10 +487,11 @@ int psvd_stream_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, con
   if ((rc = ensure(c, c->utu, sizeof(double) * (size_t)K * K))) return rc;
   double* G = (double*)c->gram.ptr;
   double* W = (double*)c->wbuf.ptr;
-  double* UtU = rescue ? (double*)c->utu.ptr : nullptr;
+  double* UtU = (double*)c->utu.ptr;
   if ((rc = psvd_gram(c, M, U, ldu, sigma, ff, Kc, A, lda, B, G, stream))) return rc;
   if ((rc = psvd_core_eig(c, G, n, sigma, ff, Kc, K, W, sigma_out, stream))) return rc;
   if ((rc = psvd_recompose(c, M, U, ldu, Kc, A, lda, B, W, K, U_out, ldo, UtU, stream))) return rc;
+  if ((rc = refine_normalize(c, M, U_out, ldo, K, UtU, sigma_out, (cudaStream_t)stream))) return rc;
   if (rescue) rc = psvd_drift_rescue(c, M, U_out, ldo, K, UtU, sigma_out, 1e-8, stream);
   return rc;
 }
@@ -553,6 +607,142 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
   cudaMemcpyAsync(sigma_out, S, sizeof(double) * K, cudaMemcpyDeviceToDevice, st);
   c->launches += 2;
   return cuda_check(c, "randomized update");
+}
+
+// Whole stream with look-ahead: the A^T A Gram of batch b+1 runs on a
+// low-priority stream (one SM left free) while the one-CTA core solve of batch
+// b runs on the high-priority stream; U^T [U | A_{b+1}] is a narrow pass after
+// the recompose.  Same arithmetic as psvd_stream_update per batch.
+int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, const double* sigma_in, int Kc,
+                    int nb, const double* const* A, const int64_t* lda, const int* B, int K, double ff, int rescue,
+                    double* U_a, double* U_b, int64_t ldo, double* sigma_hist, int* final_buf, void* stream) {
+  if (!c || nb < 1 || !A || !lda || !B || !U_a || !U_b || !sigma_hist || !final_buf)
+    return fail(c, PSVD_EINVAL, "bad stream_run arguments");
+  if (Kc != 0 && Kc != K) return fail(c, PSVD_EINVAL, "initial state carries %d modes, K=%d", Kc, K);
+  if (Kc > 0 && (!U_in || !sigma_in)) return fail(c, PSVD_EINVAL, "null initial state");
+  if (U_in == U_a) return fail(c, PSVD_EINVAL, "U_in must not alias U_a");
+  int rc;
+  for (int b = 0; b < nb; ++b) {
+    if ((rc = check_mat(c, "A", A[b], lda[b], M, B[b]))) return rc;
+    if (B[b] < 1) return fail(c, PSVD_EINVAL, "empty batch");
+  }
+  if ((rc = check_mat(c, "U_a", U_a, ldo, M, K)) || (rc = check_mat(c, "U_b", U_b, ldo, M, K))) return rc;
+  if (Kc == 0 && B[0] < K) return fail(c, PSVD_EINVAL, "initial batch has %d columns, need at least k_modes=%d", B[0], K);
+  int nmax = 0;
+  for (int b = 0; b < nb; ++b) nmax = std::max(nmax, K + B[b]);
+  if ((rc = ensure(c, c->gram, sizeof(double) * (size_t)nmax * nmax))) return rc;
+  if ((rc = ensure(c, c->wbuf, sizeof(double) * (size_t)nmax * K))) return rc;
+  if ((rc = ensure(c, c->utu, sizeof(double) * (size_t)K * K))) return rc;
+  if ((rc = ensure(c, c->dvec, sizeof(double) * (size_t)nmax))) return rc;
+  if ((rc = ensure(c, c->eigws, sizeof(double) * eig_workspace_doubles(nmax, K)))) return rc;
+  if ((rc = ensure(c, c->tbuf, sizeof(double) * ((size_t)K * K + K)))) return rc;
+  cudaStream_t user = (cudaStream_t)stream, hi = c->s_hi, lo = c->s_lo;
+  // PSVD_TRACE=1: timeline of the two streams on stderr (diagnostics; %globaltimer stamps)
+  static const bool trace = getenv("PSVD_TRACE") != nullptr;
+  std::vector<std::string> tl;
+  unsigned long long* tbuf = nullptr;
+  if (trace) cudaMallocManaged(&tbuf, 256 * sizeof(unsigned long long));
+  auto mark = [&](const char* what, int b, cudaStream_t s_) {
+    if (!trace || tl.size() >= 256) return;
+    stamp_kernel<<<1, 1, 0, s_>>>(tbuf + tl.size());
+    tl.push_back(std::string(what) + "[" + std::to_string(b) + "]");
+  };
+  mark("start", 0, user);
+  cudaEventRecord(c->ev_fork, user);
+  cudaStreamWaitEvent(hi, c->ev_fork, 0);
+  cudaStreamWaitEvent(lo, c->ev_fork, 0);
+  double* G = (double*)c->gram.ptr;
+  double* W = (double*)c->wbuf.ptr;
+  double* UtU = (double*)c->utu.ptr;
+  double* bufs[2] = {U_a, U_b};
+  int nbaa[2] = {0, 0};
+  int nbua = 0;
+  // A^T A of batch j on the low-priority stream into tiles2[j & 1]
+  auto aa_pass = [&](int j) -> int {
+    if (j >= 2) cudaStreamWaitEvent(lo, c->ev_asm[j & 1], 0);  // tiles2[j&1] consumed by batch j-2's assembly
+    Pass pa;
+    int r = plan_pass(c, pa, M, {Seg{A[j], lda[j], B[j], 0}}, 0, 0, 0, nullptr, 0, true, false, false, -1, -1,
+                      &c->partial2, &c->tiles2[j & 1], c->num_sms - 2);
+    if (r) return r;
+    nbaa[j & 1] = pa.NB;
+    mark("lo:aa_begin", j, lo);
+    if ((r = run_pass(c, pa, lo))) return r;
+    mark("lo:aa_end", j, lo);
+    cudaEventRecord(c->ev_aa[j & 1], lo);
+    return PSVD_OK;
+  };
+  if ((rc = aa_pass(0))) return rc;
+  const double* Uprev = Kc > 0 ? U_in : nullptr;
+  int64_t ldprev = Kc > 0 ? ldu : 0;
+  const double* sprev = Kc > 0 ? sigma_in : nullptr;
+  int cur = 0;
+  if (Kc > 0) {  // U^T [U | A_0] for the initial state
+    Pass pu;
+    if ((rc = plan_pass(c, pu, M, {Seg{U_in, ldu, K, 0}, Seg{A[0], lda[0], B[0], 0}}, 0, 0, 0, nullptr, 0, true,
+                        false, false, -1, K)))
+      return rc;
+    nbua = pu.NB;
+    if ((rc = run_pass(c, pu, hi))) return rc;
+  }
+  for (int b = 0; b < nb; ++b) {
+    if (b + 1 < nb && (rc = aa_pass(b + 1))) return rc;
+    const int kc = (b == 0) ? Kc : K;
+    const int n = kc + B[b];
+    cudaStreamWaitEvent(hi, c->ev_aa[b & 1], 0);
+    mark("hi:eig_begin", b, hi);
+    if ((rc = make_dvec(c, sprev, ff, kc, n, hi))) return rc;
+    launch_assemble_gram((const double*)c->tiles.ptr, nbua, (const double*)c->tiles2[b & 1].ptr, nbaa[b & 1], kc,
+                         B[b], (const double*)c->dvec.ptr, G, hi);
+    c->launches++;
+    cudaEventRecord(c->ev_asm[b & 1], hi);
+    double* sig_b = sigma_hist + (size_t)b * K;
+    launch_eig_topk(G, n, K, (const double*)c->dvec.ptr, W, sig_b, (double*)c->eigws.ptr, c->d_status, c->d_timers,
+                    hi);
+    c->launches++;
+    if ((rc = cuda_check(c, "core eig"))) return rc;
+    mark("hi:eig_end", b, hi);
+    double* Uout = bufs[cur];
+    const bool resc = rescue && kc > 0;
+    if ((rc = psvd_recompose(c, M, Uprev, ldprev, kc, A[b], lda[b], B[b], W, K, Uout, ldo, UtU, hi))) return rc;
+    if ((rc = refine_normalize(c, M, Uout, ldo, K, UtU, sig_b, hi))) return rc;
+    if (resc && (rc = psvd_drift_rescue(c, M, Uout, ldo, K, UtU, sig_b, 1e-8, hi))) return rc;
+    mark("hi:recompose_end", b, hi);
+    if (b + 1 < nb) {  // U^T U and U^T A_{b+1} (first tile rows of the Gram of [U | A_{b+1}])
+      Pass pu;
+      if ((rc = plan_pass(c, pu, M, {Seg{Uout, ldo, K, 0}, Seg{A[b + 1], lda[b + 1], B[b + 1], 0}}, 0, 0, 0, nullptr,
+                          0, true, false, false, -1, K)))
+        return rc;
+      nbua = pu.NB;
+      if ((rc = run_pass(c, pu, hi))) return rc;
+      mark("hi:ua_end", b + 1, hi);
+    }
+    Uprev = Uout;
+    ldprev = ldo;
+    sprev = sig_b;
+    *final_buf = cur;
+    cur ^= 1;
+  }
+  cudaEventRecord(c->ev_join, lo);
+  cudaStreamWaitEvent(user, c->ev_join, 0);
+  cudaEventRecord(c->ev_join, hi);
+  cudaStreamWaitEvent(user, c->ev_join, 0);
+  if (trace) {
+    mark("end", 0, user);
+    cudaDeviceSynchronize();
+    for (size_t i = 0; i < tl.size(); ++i)
+      fprintf(stderr, "psvd_trace %-18s %9.3f ms\n", tl[i].c_str(), (double)(tbuf[i] - tbuf[0]) * 1e-6);
+    cudaFree(tbuf);
+  }
+  return cuda_check(c, "stream_run");
+}
+
+int psvd_refine_normalize(psvd_ctx* c, int64_t M, double* U, int64_t ldu, int K, double* UtU, double* sigma,
+                          void* stream) {
+  if (!c) return PSVD_EINVAL;
+  int rc;
+  if ((rc = check_mat(c, "U", U, ldu, M, K))) return rc;
+  if (!UtU || !sigma || K > 1024) return fail(c, PSVD_EINVAL, "bad refine arguments");
+  return refine_normalize(c, M, U, ldu, K, UtU, sigma, (cudaStream_t)stream);
 }
 
 int psvd_sum_ordered(psvd_ctx* c, const double* parts, int P, int64_t count, double* out, void* stream) {

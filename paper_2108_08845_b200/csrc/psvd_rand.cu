@@ -210,7 +210,7 @@ __global__ void colmax_sign_kernel(const double* __restrict__ colmax, int nchunk
       val = v;
     }
   }
-  sign[k] = val < 0.0 ? -1.0 : 1.0;
+  sign[k] = val < 0.0 ? -1.0 : 1.0;  // applied with scale_cols (multiplies by +-1)
 }
 
 void launch_colmax_sign(const double* colmax, int nchunks, int K, double* sign, cudaStream_t st) {
@@ -221,7 +221,8 @@ __global__ void scale_cols_kernel(double* __restrict__ U, int64_t ld, int64_t M,
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int k = blockIdx.y;
   if (i >= M || k >= K) return;
-  if (s[k] < 0.0) U[(size_t)k * ld + i] = -U[(size_t)k * ld + i];
+  const double f = s[k];
+  if (f != 1.0) U[(size_t)k * ld + i] *= f;
 }
 
 void launch_scale_cols(double* U, int64_t ld, int64_t M, int K, const double* s, cudaStream_t st) {

@@ -54,6 +54,32 @@ void launch_extract_sym(const double* tiles, int NB, int c0, int n, const double
   extract_sym_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(tiles, NB, c0, n, d, out);
 }
 
+// G (n x n, n = K + B) = [[d d^T .* (U^T U), d .* (U^T A)], [., A^T A]] from the tiles of the
+// narrow [U | A] pass (first tile rows) and of the A^T A pass.
+__global__ void assemble_gram_kernel(const double* __restrict__ tua, int nbua, const double* __restrict__ taa,
+                                     int nbaa, int K, int B, const double* __restrict__ d, double* __restrict__ G) {
+  const int n = K + B;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n * n) return;
+  int i = (int)(idx % n), j = (int)(idx / n);
+  if (i > j) { const int t = i; i = j; j = t; }
+  double v;
+  if (i < K) {
+    v = tua[((size_t)(i >> 5) * nbua + (j >> 5)) * 1024 + (i & 31) * 32 + (j & 31)] * d[i];
+    if (j < K) v *= d[j];
+  } else {
+    const int a = i - K, b = j - K;
+    v = taa[((size_t)(a >> 5) * nbaa + (b >> 5)) * 1024 + (a & 31) * 32 + (b & 31)];
+  }
+  G[idx] = v;
+}
+
+void launch_assemble_gram(const double* tua, int nbua, const double* taa, int nbaa, int K, int B, const double* d,
+                          double* G, cudaStream_t st) {
+  const int64_t tot = (int64_t)(K + B) * (K + B);
+  assemble_gram_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(tua, nbua, taa, nbaa, K, B, d, G);
+}
+
 void launch_extract_rect(const double* tiles, int NB, int r0, int nr, int c0, int nc, const double* d,
                          double* out, cudaStream_t st) {
   const int64_t tot = (int64_t)nr * nc;
@@ -423,6 +449,33 @@ void launch_eig_topk(const double* G, int n, int K, const double* dscale, double
     cudaFuncSetAttribute(eig_topk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     eig_topk_kernel<false><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers, rank_tol);
   }
+}
+
+// ---------------------------------------------------------------- Rayleigh refinement
+// U = C V S^-1 from the Gram route has ||u_k|| = ||C v_k|| / s_k, and ||C v_k|| is
+// the Rayleigh estimate of the singular value (second-order accurate in the
+// eigenvector error, vs eps*kappa^2 for sqrt(lambda)).  sigma_k <- ||C v_k||,
+// UtU <- D^-1 UtU D^-1 (D = diag ||u_k||) and scale_k = 1 / ||u_k|| for the columns.
+__global__ void normalize_gram_kernel(double* __restrict__ UtU, int K, double* __restrict__ sigma,
+                                      double* __restrict__ scale) {
+  __shared__ double nk[1024];
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    const double d = UtU[(size_t)k * K + k];
+    nk[k] = d > 0.0 ? sqrt(d) : 1.0;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < K * K; idx += blockDim.x) {
+    const int i = idx % K, j = idx / K;
+    UtU[idx] = UtU[idx] / (nk[i] * nk[j]);
+  }
+  for (int k = threadIdx.x; k < K; k += blockDim.x) {
+    sigma[k] *= nk[k];
+    scale[k] = 1.0 / nk[k];
+  }
+}
+
+void launch_normalize_gram(double* UtU, int K, double* sigma, double* scale, cudaStream_t st) {
+  normalize_gram_kernel<<<1, 1024, 0, st>>>(UtU, K, sigma, scale);
 }
 
 // ---------------------------------------------------------------- drift check / rescue

@@ -14,6 +14,9 @@ constexpr int EIG_NMAX_SMEM = 224;   // packed lower triangle kept in shared mem
 // by d (length n, may be null): out[i][j] = d_i d_j T(c0+i, c0+j).  col-major, ld n.
 void launch_extract_sym(const double* tiles, int NB, int c0, int n, const double* d, double* out,
                         cudaStream_t st);
+// Assemble the streaming Gram from the narrow [U | A] pass tiles and the A^T A pass tiles.
+void launch_assemble_gram(const double* tua, int nbua, const double* taa, int nbaa, int K, int B, const double* d,
+                          double* G, cudaStream_t st);
 // Extract the rectangular block rows [r0, r0+nr) x cols [c0, c0+nc) (r-block <= c-block),
 // scaled by row factors d (length nr, may be null).  col-major, ld nr.
 void launch_extract_rect(const double* tiles, int NB, int r0, int nr, int c0, int nc, const double* d,
@@ -31,6 +34,9 @@ size_t eig_workspace_doubles(int n, int K);
 void launch_eig_topk(const double* G, int n, int K, const double* dscale, double* W, double* sigma,
                      double* ws, int* status, long long* timers, cudaStream_t st, double rank_tol = 0.0);
 bool eig_supported(int n, int K);
+
+// Rayleigh refinement of sigma from the recomposed columns' norms (see psvd_small.cu).
+void launch_normalize_gram(double* UtU, int K, double* sigma, double* scale, cudaStream_t st);
 
 // Drift check of streaming.py:106-115 on the K x K Gram UtU = U_new^T U_new:
 // if max|UtU - I| > tol: T = rr^{-1}[:, order] with rr = chol(UtU) (= qr(U).R),

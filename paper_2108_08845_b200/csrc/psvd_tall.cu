@@ -212,20 +212,31 @@ __global__ void __launch_bounds__(NTHR, 1) tall_pass_kernel(const TallParams p) 
   }
 }
 
-__global__ void tall_reduce_kernel(const double* __restrict__ partial, const ReduceMap map,
-                                   double* __restrict__ tiles) {
+// Fixed-order reduction of the per-CTA partial tiles: block (32 elements of one
+// output tile) x 8 warps; warp w sums sources w, w+8, ... (chunk-major order),
+// then the 8 warp sums are added in warp order.  Bitwise reproducible.
+__global__ void __launch_bounds__(256) tall_reduce_kernel(const double* __restrict__ partial, const ReduceMap map,
+                                                          double* __restrict__ tiles) {
+  __shared__ double red[8][33];
   const int o = blockIdx.y;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= map.nout || e >= 1024) return;
-  double s = 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
   const int ns = map.nsrc[o];
-  for (int c = 0; c < map.nchunks; ++c) {
-    for (int i = 0; i < ns; ++i) {
-      const int sl = map.src[o][i] / SLOTS, slot = map.src[o][i] % SLOTS;
-      s += partial[((size_t)(c * map.nslices + sl) * SLOTS + slot) * 1024 + e];
-    }
+  const int total = map.nchunks * ns;
+  double s = 0.0;
+  for (int q = warp; q < total; q += 8) {
+    const int c = q / ns, i = q % ns;
+    const int sl = map.src[o][i] / SLOTS, slot = map.src[o][i] % SLOTS;
+    s += partial[((size_t)(c * map.nslices + sl) * SLOTS + slot) * 1024 + e];
   }
-  tiles[(size_t)map.out_id[o] * 1024 + e] = s;
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0) {
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) t += red[w][lane];
+    tiles[(size_t)map.out_id[o] * 1024 + e] = t;
+  }
 }
 
 template <int KS>
@@ -257,7 +268,7 @@ void launch_tall(const TallParams& p, int grid, cudaStream_t st) {
 
 void launch_tall_reduce(const double* partial, const ReduceMap& map, double* tiles, cudaStream_t st) {
   if (map.nout == 0) return;
-  dim3 grid(1024 / 256, map.nout);
+  dim3 grid(1024 / 32, map.nout);
   tall_reduce_kernel<<<grid, 256, 0, st>>>(partial, map, tiles);
 }
 

@@ -15,6 +15,7 @@ update: each step is low_rank_svd of [ff*U*S | A].
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 from typing import Optional
 
@@ -141,17 +142,74 @@ def stream_incorporate(state, a_new, config):
     return StreamState(u.view, s, state.iteration + 1)
 
 
+STREAM_WINDOW = 8  # batches resident on the device per pipelined run
+
+
+def _run_window(state, mats, config, dev):
+    """Deterministic updates over device batches `mats` with look-ahead
+    (psvd_stream_run): the next batch's A^T A overlaps the current core solve."""
+    k = config.k_modes
+    M = mats[0].rows
+    for m in mats:
+        if m.rows != M:
+            raise ValueError(f"batch rows {m.rows} != mode rows {M}")
+    if state is None and mats[0].cols < k:
+        raise ValueError(f"initial batch has {mats[0].cols} columns, need at least k_modes={k}")
+    if state is None and M < k:
+        raise ValueError(f"initial batch has {M} rows, need at least k_modes={k}")
+    ctx = nat.context(dev)
+    nb = len(mats)
+    with torch.cuda.device(dev):
+        if state is not None:
+            U = nat.as_device_colmajor(state.modes, dev, "modes")
+            sig = nat.as_device_vector(state.singular_values, dev, k, "singular_values")
+            kc, uptr, uld, sptr = k, nat._vp(U.data_ptr()), U.ld, nat.ptr(sig)
+        else:
+            U = sig = None
+            kc, uptr, uld, sptr = 0, nat._vp(0), 0, nat._vp(0)
+        outs = [nat.DevMat.empty(M, k, dev) for _ in range(2)]
+        hist = torch.empty((nb, k), dtype=torch.float64, device=dev)
+        A = (nat._vp * nb)(*[nat._vp(m.data_ptr()) for m in mats])
+        lda = (ctypes.c_int64 * nb)(*[m.ld for m in mats])
+        B = (ctypes.c_int * nb)(*[m.cols for m in mats])
+        fin = ctypes.c_int(0)
+        nat.call("psvd_stream_run", ctx, M, uptr, uld, sptr, kc, nb, A, lda, B, k, float(config.forget_factor), 1,
+                 nat._vp(outs[0].data_ptr()), nat._vp(outs[1].data_ptr()), outs[0].ld, nat.ptr(hist),
+                 ctypes.byref(fin), nat.stream_ptr(dev))
+        _check_status(ctx, dev, "a_new")
+    it0 = -1 if state is None else state.iteration
+    new_state = StreamState(outs[fin.value].view, hist[nb - 1].clone(), it0 + nb)
+    return new_state, [hist[i] for i in range(nb)]
+
+
 def stream_all(batches, config, device=None):
     """Initialize on the first batch, incorporate the rest (streaming.py:119-133).
-    Returns (final_state, history) with the singular values after every step."""
+    Returns (final_state, history) with the singular values after every step.
+    Deterministic streams run in windows of STREAM_WINDOW resident batches
+    through the pipelined psvd_stream_run; randomized ones update per batch."""
     state = None
     history = []
-    for batch in batches:
-        if state is None:
-            state = stream_initialize(batch, config, device)
-        else:
-            state = stream_incorporate(state, batch, config)
-        history.append(state.singular_values.clone())
+    if config.sketch is not None:
+        for batch in batches:
+            if state is None:
+                state = stream_initialize(batch, config, device)
+            else:
+                state = stream_incorporate(state, batch, config)
+            history.append(state.singular_values.clone())
+    else:
+        dev = None if device is None else torch.device(device)
+        window = []
+        for batch in batches:
+            if dev is None:
+                dev = _device_of(batch)
+            window.append(nat.as_device_colmajor(batch, dev, "a0" if state is None and not window else "a_new"))
+            if len(window) == STREAM_WINDOW:
+                state, h = _run_window(state, window, config, dev)
+                history.extend(h)
+                window = []
+        if window:
+            state, h = _run_window(state, window, config, dev)
+            history.extend(h)
     if state is None:
         raise ValueError("batch stream is empty")
     return state, history

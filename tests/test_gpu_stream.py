@@ -182,9 +182,35 @@ def test_parallel_single_rank_matches_serial():
     st = p.parallel_stream_initialize(ctx, a[:, :200], cfg)
     for c in (200, 400):
         st = p.parallel_stream_incorporate(ctx, st, a[:, c:c + 200], cfg)
-    ser, _ = p.stream_all(_batches(a, 200), cfg)
+    # per-update serial chain: same kernels, bitwise equal (test_dsvd.py:214-229 property)
+    ser = p.stream_initialize(a[:, :200], cfg)
+    for c in (200, 400):
+        ser = p.stream_incorporate(ser, a[:, c:c + 200], cfg)
     assert torch.equal(st.modes, ser.modes)
+    assert torch.equal(st.singular_values, ser.singular_values)
     assert torch.equal(p.gather_modes(ctx, st), st.modes.contiguous())
+    # the pipelined stream_all assembles the same Gram from two passes: parity, not bits
+    pipe, _ = p.stream_all(_batches(a, 200), cfg)
+    m1, s1 = pipe.numpy()
+    m2, s2 = ser.numpy()
+    _assert_parity(m1, s1, m2, s2, sig_tol=1e-13, ang_tol=1e-12)
+
+
+def test_stream_all_windows_and_continuation():
+    p = _pkg()
+    a = oracle.burgers_matrix(6000, 800)
+    ref_m, ref_s, ref_h = oracle.ref_stream_all(_batches(a, 50), 10, 0.95)
+    old = p.streaming.STREAM_WINDOW
+    try:
+        p.streaming.STREAM_WINDOW = 3  # 16 batches -> windows 3,3,3,3,3,1 chained through the state
+        st, hist = p.stream_all(_batches(a, 50), p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=50))
+    finally:
+        p.streaming.STREAM_WINDOW = old
+    m, s = _np(st)
+    _assert_parity(m, s, ref_m, ref_s)
+    assert st.iteration == 15 and len(hist) == 16
+    for h, rh in zip(hist, ref_h):
+        assert oracle.sigma_rel_err(h.cpu().numpy(), rh) <= SIG_TOL
 
 
 def test_parallel_golden_via_rank_emulation(golden):
