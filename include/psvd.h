@@ -55,9 +55,10 @@ const char* psvd_last_error(psvd_ctx* ctx);
 /* Number of kernels this context has enqueued so far (launch accounting). */
 long long psvd_launch_count(psvd_ctx* ctx);
 
-/* Diagnostics: SM clock64() stamps of the 9 phase boundaries of the last
- * core eigensolver launch (synchronous copy). */
-int psvd_eig_phase_cycles(psvd_ctx* ctx, long long* out9);
+/* Diagnostics (with PSVD_EIG_TIMERS set in the environment): SM clock64()
+ * stamps of the 9 phase boundaries of the last core eigensolver launch and 5
+ * tridiagonalization sub-phase sums (14 entries; synchronous copy). */
+int psvd_eig_phase_cycles(psvd_ctx* ctx, long long* out14);
 
 /* Copy the context's device status word to *status (synchronizes `stream`);
  * reset != 0 clears it afterwards (stream-ordered). */

@@ -39,6 +39,8 @@ struct psvd_ctx {
   Buf ybuf, rsmall, jacws;  // randomized path: sketch Y (M x l), small matrices, Jacobi scratch
   Buf partial2, tiles2[2];  // A^T A passes on the low-priority stream (double-buffered tiles)
   cudaStream_t s_hi = nullptr, s_lo = nullptr;  // pipelined stream_run: critical chain / look-ahead Grams
+  cudaStream_t s_aux = nullptr;                  // concurrent LDL^T of the split core solve
+  cudaEvent_t ev_ldlt_fork = nullptr, ev_ldlt_join = nullptr;
   cudaEvent_t ev_aa[2] = {nullptr, nullptr}, ev_asm[2] = {nullptr, nullptr}, ev_fork = nullptr, ev_join = nullptr;
 };
 
@@ -97,12 +99,14 @@ struct Pass {
   ReduceMap map;
   int grid = 0;
   int NB = 0;
+  bool ws = false;      // warp-specialized Gram kernel
   Buf* part = nullptr;  // partial-tile workspace of the stream this pass runs on
   Buf* tl = nullptr;    // reduced tiles
 };
 
 // Fill the warp plans / reduce map for a tile list (I <= J, 32-col blocks of [P | Y]).
-int plan_tiles(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& tiles, bool allow_ksplit) {
+int plan_tiles(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& tiles, bool allow_ksplit,
+               int warps_avail = NWARP) {
   const int nt = (int)tiles.size();
   memset(ps.p.plan, 0, sizeof(ps.p.plan));
   memset(&ps.map, 0, sizeof(ps.map));
@@ -111,8 +115,8 @@ int plan_tiles(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& ti
     return PSVD_OK;
   }
   if (nt > MAX_OUT_TILES) return fail(c, PSVD_EINVAL, "too many Gram tiles (%d)", nt);
-  const int nwarp_needed = (nt + 1) / 2;
-  const int nslices = (nwarp_needed + NWARP - 1) / NWARP;
+  const int nwarp_needed = (nt + TPW - 1) / TPW;
+  const int nslices = (nwarp_needed + warps_avail - 1) / warps_avail;
   if (nslices > MAX_SLICES) return fail(c, PSVD_EINVAL, "panel too wide (%d tiles)", nt);
   ps.p.nslices = nslices;
   const int per = (nt + nslices - 1) / nslices;
@@ -121,25 +125,25 @@ int plan_tiles(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& ti
     const int t0 = s * per, t1 = std::min(nt, t0 + per);
     const int ns = t1 - t0;
     if (ns <= 0) continue;
-    if (ns >= NWARP) {
-      for (int w = 0; w < NWARP; ++w) {
+    if (ns >= warps_avail) {
+      for (int w = 0; w < warps_avail; ++w) {
         WarpPlan& wp = ps.p.plan[s][w];
         wp.ksplit = 1;
         wp.kpart = 0;
-        for (int t = 0; t < 2; ++t) {
-          const int li = w + t * NWARP;
+        for (int t = 0; t < TPW; ++t) {
+          const int li = w + t * warps_avail;
           if (li < ns) {
             wp.ti[wp.ntile] = (signed char)tiles[t0 + li].first;
             wp.tj[wp.ntile] = (signed char)tiles[t0 + li].second;
             const int o = t0 + li;
-            ps.map.src[o][ps.map.nsrc[o]++] = (unsigned char)(s * SLOTS + w * 2 + wp.ntile);
+            ps.map.src[o][ps.map.nsrc[o]++] = (unsigned char)(s * SLOTS + w * TPW + wp.ntile);
             wp.ntile++;
           }
         }
       }
     } else {
       int ksplit = 1;
-      while (allow_ksplit && ksplit * 2 * ns <= NWARP) ksplit *= 2;
+      while (allow_ksplit && ksplit * 2 * ns <= warps_avail) ksplit *= 2;
       for (int w = 0; w < ns * ksplit; ++w) {
         WarpPlan& wp = ps.p.plan[s][w];
         const int li = w % ns;
@@ -149,7 +153,7 @@ int plan_tiles(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& ti
         wp.tj[0] = (signed char)tiles[t0 + li].second;
         wp.ntile = 1;
         const int o = t0 + li;
-        ps.map.src[o][ps.map.nsrc[o]++] = (unsigned char)(s * SLOTS + w * 2);
+        ps.map.src[o][ps.map.nsrc[o]++] = (unsigned char)(s * SLOTS + w * TPW);
       }
     }
   }
@@ -160,7 +164,7 @@ int plan_tiles(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& ti
 // Common pass setup.  segs: panel segments; w/W: optional Y = P[:, wlo:wlo+wk] * W.
 int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, int wlo, int wk, int w,
               const double* W, int64_t ldw, bool gram_pp, bool gram_yy, bool gram_py, int py_cols = -1,
-              int pp_rows = -1, Buf* part = nullptr, Buf* tl = nullptr, int max_ctas = 0) {
+              int pp_rows = -1, Buf* part = nullptr, Buf* tl = nullptr, int max_ctas = 0, int py_lo = 0) {
   memset(&ps.p, 0, sizeof(ps.p));
   ps.part = part ? part : &c->partial;
   ps.tl = tl ? tl : &c->tiles;
@@ -170,6 +174,8 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
   int np = 0;
   for (size_t i = 0; i < segs.size(); ++i) {
     p.seg[i] = segs[i];
+    if (segs[i].col0 == 1) np = rup(np, 32);  // request: start this segment on a 32-column block
+    p.seg[i].col0 = np;
     np += segs[i].ncols;
   }
   p.np = np;
@@ -185,8 +191,10 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
   if (w > MAX_W) return fail(c, PSVD_EINVAL, "Y width %d exceeds %d", w, MAX_W);
   // stage height: 32 rows unless the smem budget forces 16
   p.ks = 32;
-  if (tall_smem_bytes(32, np_pad, wk, w) > (size_t)SMEM_LIMIT) p.ks = 16;
-  if (tall_smem_bytes(p.ks, np_pad, wk, w) > (size_t)SMEM_LIMIT)
+  p.nstage = 3;
+  if (tall_smem_bytes(32, np_pad, wk, w, 3) > (size_t)SMEM_LIMIT) p.nstage = 2;
+  if (tall_smem_bytes(32, np_pad, wk, w, 2) > (size_t)SMEM_LIMIT) p.ks = 16;
+  if (tall_smem_bytes(p.ks, np_pad, wk, w, p.nstage) > (size_t)SMEM_LIMIT)
     return fail(c, PSVD_EINVAL, "panel of %d columns (+%d) does not fit shared memory", np, w);
   const int NBp = np_pad / 32, NBy = w > 0 ? rup(w, 32) / 32 : 0;
   ps.NB = NBp + NBy;
@@ -195,13 +203,17 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
     for (int I = 0; I < (pp_rows < 0 ? NBp : std::min(NBp, (pp_rows + 31) / 32)); ++I)
       for (int J = I; J < NBp; ++J) tiles.push_back({I, J});
   if (gram_py)
-    for (int I = 0; I < (py_cols < 0 ? NBp : (py_cols + 31) / 32); ++I)
+    for (int I = py_lo; I < (py_cols < 0 ? NBp : (py_cols + 31) / 32); ++I)
       for (int J = 0; J < NBy; ++J) tiles.push_back({I, NBp + J});
   if (gram_yy)
     for (int I = 0; I < NBy; ++I)
       for (int J = I; J < NBy; ++J) tiles.push_back({NBp + I, NBp + J});
-  // k-splitting only pays for FP64-heavy Gram-only passes; Y passes are HBM-bound
-  int rc = plan_tiles(c, ps, tiles, w == 0);
+  // narrow tiles: all Gram tiles end in the Y block and Y has <= 16 columns
+  p.narrow = (w > 0 && w <= 16 && !gram_pp && !tiles.empty()) ? 1 : 0;
+  // Gram-only passes with enough tiles run warp-specialized (one producer warp, no k-split)
+  ps.ws = (w == 0 && (int)tiles.size() >= 8 &&
+           gram_ws_smem_bytes(np_pad, 3) <= (size_t)SMEM_LIMIT);
+  int rc = ps.ws ? plan_tiles(c, ps, tiles, false, NWARP - 1) : plan_tiles(c, ps, tiles, w == 0);
   if (rc) return rc;
   // grid: one CTA per SM (1 CTA/SM by smem), chunks of 32-row multiples
   const int64_t stages32 = (M + 31) / 32;
@@ -224,7 +236,10 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
 }
 
 int run_pass(psvd_ctx* c, Pass& ps, cudaStream_t st) {
-  launch_tall(ps.p, ps.grid, st);
+  if (ps.ws)
+    launch_gram_ws(ps.p, ps.grid, st);
+  else
+    launch_tall(ps.p, ps.grid, st);
   c->launches += 1 + (ps.map.nout > 0);
   int rc = cuda_check(c, "tall pass");
   if (rc) return rc;
@@ -293,6 +308,11 @@ __global__ void burgers_kernel(double* __restrict__ out, int64_t ldo, int64_t ro
 
 }  // namespace
 
+static int core_solve(psvd_ctx* c, const double* G, int n, int K, const double* dscale, double* W, double* sigma,
+                      cudaStream_t st, long long* timers);
+static int refine_normalize(psvd_ctx* c, int64_t M, double* U, int64_t ld, int K, double* UtU, double* sigma,
+                            cudaStream_t st);
+
 // ============================================================================ C ABI
 
 extern "C" {
@@ -325,6 +345,9 @@ int psvd_create(int device, psvd_ctx** out) {
     cudaDeviceGetStreamPriorityRange(&lo, &hi);  // numerically: hi <= lo (smaller = higher priority)
     cudaStreamCreateWithPriority(&c->s_hi, cudaStreamNonBlocking, hi);
     cudaStreamCreateWithPriority(&c->s_lo, cudaStreamNonBlocking, lo);
+    cudaStreamCreateWithPriority(&c->s_aux, cudaStreamNonBlocking, hi);
+    cudaEventCreateWithFlags(&c->ev_ldlt_fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_ldlt_join, cudaEventDisableTiming);
     for (int i = 0; i < 2; ++i) {
       cudaEventCreateWithFlags(&c->ev_aa[i], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&c->ev_asm[i], cudaEventDisableTiming);
@@ -347,6 +370,9 @@ int psvd_destroy(psvd_ctx* c) {
     if (b->ptr) cudaFree(b->ptr);
   if (c->s_hi) cudaStreamDestroy(c->s_hi);
   if (c->s_lo) cudaStreamDestroy(c->s_lo);
+  if (c->s_aux) cudaStreamDestroy(c->s_aux);
+  if (c->ev_ldlt_fork) cudaEventDestroy(c->ev_ldlt_fork);
+  if (c->ev_ldlt_join) cudaEventDestroy(c->ev_ldlt_join);
   for (int i = 0; i < 2; ++i) {
     if (c->ev_aa[i]) cudaEventDestroy(c->ev_aa[i]);
     if (c->ev_asm[i]) cudaEventDestroy(c->ev_asm[i]);
@@ -366,7 +392,7 @@ long long psvd_launch_count(psvd_ctx* c) { return c ? c->launches : -1; }
 
 int psvd_eig_phase_cycles(psvd_ctx* c, long long* out9) {
   if (!c || !out9) return PSVD_EINVAL;
-  if (cudaMemcpy(out9, c->d_timers, 9 * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+  if (cudaMemcpy(out9, c->d_timers, 14 * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
     return cuda_check(c, "eig timers");
   return PSVD_OK;
 }
@@ -410,10 +436,8 @@ int psvd_core_eig(psvd_ctx* c, const double* G, int n, const double* sigma_in, d
   int rc;
   if ((rc = make_dvec(c, sigma_in, ff, Kc, n, st))) return rc;
   if ((rc = ensure(c, c->eigws, sizeof(double) * eig_workspace_doubles(n, K)))) return rc;
-  launch_eig_topk(G, n, K, (const double*)c->dvec.ptr, W, sigma_out, (double*)c->eigws.ptr, c->d_status,
-                  c->d_timers, st);
-  c->launches++;
-  return cuda_check(c, "core eig");
+  static const bool eig_timers = getenv("PSVD_EIG_TIMERS") != nullptr;  // diagnostics: phase clocks
+  return core_solve(c, G, n, K, (const double*)c->dvec.ptr, W, sigma_out, st, eig_timers ? c->d_timers : nullptr);
 }
 
 int psvd_recompose(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, int Kc, const double* A, int64_t lda, int B,
@@ -460,6 +484,28 @@ int psvd_drift_rescue(psvd_ctx* c, int64_t M, double* U, int64_t ldu, int K, con
 }
 
 }  // extern "C"
+
+// Core solve of a Gram: eig (+ concurrent LDL^T on the aux stream when the split path applies)
+static int core_solve(psvd_ctx* c, const double* G, int n, int K, const double* dscale, double* W, double* sigma,
+                      cudaStream_t st, long long* timers) {
+  int rc = ensure(c, c->eigws, sizeof(double) * eig_workspace_doubles(n, K));
+  if (rc) return rc;
+  double* ws = (double*)c->eigws.ptr;
+  if (eig_split_supported(n, K) && timers == nullptr) {
+    cudaEventRecord(c->ev_ldlt_fork, st);
+    cudaStreamWaitEvent(c->s_aux, c->ev_ldlt_fork, 0);
+    launch_ldlt_pack(G, n, ws, c->s_aux);  // packed L in the (unused in smem mode) first n(n+1)/2 doubles
+    cudaEventRecord(c->ev_ldlt_join, c->s_aux);
+    launch_eig_topk(G, n, K, dscale, W, sigma, ws, c->d_status, nullptr, st, 0.0, 1);
+    cudaStreamWaitEvent(st, c->ev_ldlt_join, 0);
+    launch_sign_weights(ws, ws + (size_t)n * (n + 1) / 2, sigma, n, K, dscale, W, sigma, c->d_status, 0.0, st);
+    c->launches += 3;
+  } else {
+    launch_eig_topk(G, n, K, dscale, W, sigma, ws, c->d_status, timers, st);
+    c->launches++;
+  }
+  return cuda_check(c, "core solve");
+}
 
 // sigma_k <- ||C v_k|| and unit columns (Rayleigh refinement), UtU normalized in place
 static int refine_normalize(psvd_ctx* c, int64_t M, double* U, int64_t ld, int K, double* UtU, double* sigma,
@@ -656,20 +702,51 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
   double* UtU = (double*)c->utu.ptr;
   double* bufs[2] = {U_a, U_b};
   int nbaa[2] = {0, 0};
-  int nbua = 0;
+  int nbua = 0, fused_a0 = 0, fused_y = 0;
+  bool prev_resc = false;
   // A^T A of batch j on the low-priority stream into tiles2[j & 1]
+  // The look-ahead Gram is cut into row sub-ranges launched back to back: CTAs of a
+  // low-priority kernel cannot be preempted, so short launches let the high-priority
+  // recompose / U^T A passes take the SMs between them.  All sub-ranges write disjoint
+  // partial sets and one fixed-order reduction sums them (bitwise reproducible).
+  const int nsub = (int)std::max<int64_t>(1, std::min<int64_t>(4, M / 65536));
   auto aa_pass = [&](int j) -> int {
     if (j >= 2) cudaStreamWaitEvent(lo, c->ev_asm[j & 1], 0);  // tiles2[j&1] consumed by batch j-2's assembly
-    Pass pa;
-    int r = plan_pass(c, pa, M, {Seg{A[j], lda[j], B[j], 0}}, 0, 0, 0, nullptr, 0, true, false, false, -1, -1,
-                      &c->partial2, &c->tiles2[j & 1], c->num_sms - 2);
-    if (r) return r;
-    nbaa[j & 1] = pa.NB;
+    const int64_t rows_sub = (M + nsub - 1) / nsub / 32 * 32 + 32;
+    Pass first;
+    size_t part_off = 0;
+    int nchunks_total = 0;
     mark("lo:aa_begin", j, lo);
-    if ((r = run_pass(c, pa, lo))) return r;
+    for (int k = 0; k < nsub; ++k) {
+      const int64_t r0 = (int64_t)k * rows_sub;
+      if (r0 >= M) break;
+      const int64_t mk = std::min(M, r0 + rows_sub) - r0;
+      Pass pa;
+      int r = plan_pass(c, pa, mk, {Seg{A[j] + r0, lda[j], B[j], 0}}, 0, 0, 0, nullptr, 0, true, false, false, -1,
+                        -1, &c->partial2, &c->tiles2[j & 1], c->num_sms - 2);
+      if (r) return r;
+      const size_t need = part_off + (size_t)pa.grid * SLOTS * 1024;
+      if (k == 0) {  // size the partial buffer for all sub-ranges once
+        if ((r = ensure(c, c->partial2, sizeof(double) * need * nsub))) return r;
+        first = pa;
+      }
+      pa.p.partial = (double*)c->partial2.ptr + part_off;
+      if (pa.ws)
+        launch_gram_ws(pa.p, pa.grid, lo);
+      else
+        launch_tall(pa.p, pa.grid, lo);
+      c->launches++;
+      if ((r = cuda_check(c, "look-ahead gram"))) return r;
+      part_off += (size_t)pa.grid * SLOTS * 1024;
+      nchunks_total += pa.map.nchunks;
+    }
+    first.map.nchunks = nchunks_total;
+    launch_tall_reduce((const double*)c->partial2.ptr, first.map, (double*)c->tiles2[j & 1].ptr, lo);
+    c->launches++;
+    nbaa[j & 1] = first.NB;
     mark("lo:aa_end", j, lo);
     cudaEventRecord(c->ev_aa[j & 1], lo);
-    return PSVD_OK;
+    return cuda_check(c, "look-ahead reduce");
   };
   if ((rc = aa_pass(0))) return rc;
   const double* Uprev = Kc > 0 ? U_in : nullptr;
@@ -691,31 +768,47 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
     cudaStreamWaitEvent(hi, c->ev_aa[b & 1], 0);
     mark("hi:eig_begin", b, hi);
     if ((rc = make_dvec(c, sprev, ff, kc, n, hi))) return rc;
-    launch_assemble_gram((const double*)c->tiles.ptr, nbua, (const double*)c->tiles2[b & 1].ptr, nbaa[b & 1], kc,
-                         B[b], (const double*)c->dvec.ptr, G, hi);
+    if (b == 0) {
+      launch_assemble_gram((const double*)c->tiles.ptr, nbua, (const double*)c->tiles2[b & 1].ptr, nbaa[b & 1], kc,
+                           B[b], (const double*)c->dvec.ptr, G, hi);
+    } else {
+      const double* tb = (const double*)c->tbuf.ptr;
+      launch_assemble_gram_fused((const double*)c->tiles.ptr, nbua, fused_a0, fused_y, UtU, tb + (size_t)K * K,
+                                 prev_resc ? c->d_gate : nullptr, tb, (const double*)c->tiles2[b & 1].ptr,
+                                 nbaa[b & 1], K, B[b], (const double*)c->dvec.ptr, G, hi);
+    }
     c->launches++;
     cudaEventRecord(c->ev_asm[b & 1], hi);
     double* sig_b = sigma_hist + (size_t)b * K;
-    launch_eig_topk(G, n, K, (const double*)c->dvec.ptr, W, sig_b, (double*)c->eigws.ptr, c->d_status, c->d_timers,
-                    hi);
-    c->launches++;
-    if ((rc = cuda_check(c, "core eig"))) return rc;
+    if ((rc = core_solve(c, G, n, K, (const double*)c->dvec.ptr, W, sig_b, hi, nullptr))) return rc;
     mark("hi:eig_end", b, hi);
     double* Uout = bufs[cur];
     const bool resc = rescue && kc > 0;
-    if ((rc = psvd_recompose(c, M, Uprev, ldprev, kc, A[b], lda[b], B[b], W, K, Uout, ldo, UtU, hi))) return rc;
+    if (b + 1 < nb) {
+      // fused: U_b = [U_{b-1} | A_b] W, with U_b^T U_b and U_b^T A_{b+1} from the same pass
+      std::vector<Seg> segs = panel(Uprev, ldprev, kc, A[b], lda[b], B[b]);
+      segs.push_back(Seg{A[b + 1], lda[b + 1], B[b + 1], 1});
+      Pass pf;
+      const int wk = kc + B[b];
+      const int a0 = rup(wk, 32) / 32;
+      if ((rc = plan_pass(c, pf, M, segs, 0, wk, K, W, wk, false, true, true, a0 * 32 + B[b + 1], -1, nullptr, nullptr,
+                          0, a0)))
+        return rc;
+      pf.p.Yout = Uout;
+      pf.p.ldy = ldo;
+      if ((rc = run_pass(c, pf, hi))) return rc;
+      launch_extract_sym((const double*)c->tiles.ptr, pf.NB, pf.p.np_pad, K, nullptr, UtU, hi);
+      c->launches++;
+      nbua = pf.NB;
+      fused_a0 = a0;
+      fused_y = pf.p.np_pad / 32;
+    } else {
+      if ((rc = psvd_recompose(c, M, Uprev, ldprev, kc, A[b], lda[b], B[b], W, K, Uout, ldo, UtU, hi))) return rc;
+    }
     if ((rc = refine_normalize(c, M, Uout, ldo, K, UtU, sig_b, hi))) return rc;
     if (resc && (rc = psvd_drift_rescue(c, M, Uout, ldo, K, UtU, sig_b, 1e-8, hi))) return rc;
+    prev_resc = resc;
     mark("hi:recompose_end", b, hi);
-    if (b + 1 < nb) {  // U^T U and U^T A_{b+1} (first tile rows of the Gram of [U | A_{b+1}])
-      Pass pu;
-      if ((rc = plan_pass(c, pu, M, {Seg{Uout, ldo, K, 0}, Seg{A[b + 1], lda[b + 1], B[b + 1], 0}}, 0, 0, 0, nullptr,
-                          0, true, false, false, -1, K)))
-        return rc;
-      nbua = pu.NB;
-      if ((rc = run_pass(c, pu, hi))) return rc;
-      mark("hi:ua_end", b + 1, hi);
-    }
     Uprev = Uout;
     ldprev = ldo;
     sprev = sig_b;

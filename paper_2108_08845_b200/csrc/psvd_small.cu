@@ -80,6 +80,62 @@ void launch_assemble_gram(const double* tua, int nbua, const double* taa, int nb
   assemble_gram_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(tua, nbua, taa, nbaa, K, B, d, G);
 }
 
+// Streaming Gram for batch b+1 from the fused recompose pass of batch b:
+//   UU = Uhat^T Uhat (already normalized by the Rayleigh refinement, K x K),
+//   UA(k, j) = scale_k * (A_{b+1}^T Y)(j, k) read from the tiles (block a0 + j/32, Y block yb),
+//   and, when the drift rescue ran (*gate), U <- U T:  UU <- T^T UU T,  UA <- T^T UA.
+//   G = [[d d^T .* UU, d .* UA], [., A^T A]].
+__global__ void assemble_gram_fused_kernel(const double* __restrict__ tf, int nbf, int a0, int yb,
+                                           const double* __restrict__ UU, const double* __restrict__ scale,
+                                           const int* __restrict__ gate, const double* __restrict__ T,
+                                           const double* __restrict__ taa, int nbaa, int K, int B,
+                                           const double* __restrict__ d, double* __restrict__ G) {
+  const int n = K + B;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)n * n) return;
+  int i = (int)(idx % n), j = (int)(idx / n);
+  if (i > j) { const int t = i; i = j; j = t; }
+  const bool rot = gate != nullptr && *gate != 0;
+  double v;
+  if (j < K) {
+    if (!rot) {
+      v = UU[(size_t)j * K + i];
+    } else {
+      v = 0.0;
+      for (int a = 0; a < K; ++a) {
+        double s = 0.0;
+        for (int b2 = 0; b2 < K; ++b2) s += UU[(size_t)b2 * K + a] * T[(size_t)j * K + b2];
+        v += T[(size_t)i * K + a] * s;
+      }
+    }
+    v *= d[i] * d[j];
+  } else if (i < K) {
+    const int col = j - K;
+    auto ua = [&](int k) {
+      return scale[k] * tf[((size_t)(a0 + (col >> 5)) * nbf + yb + (k >> 5)) * 1024 + (col & 31) * 32 + (k & 31)];
+    };
+    if (!rot) {
+      v = ua(i);
+    } else {
+      v = 0.0;
+      for (int k = 0; k < K; ++k) v += T[(size_t)i * K + k] * ua(k);
+    }
+    v *= d[i];
+  } else {
+    const int a = i - K, b = j - K;
+    v = taa[((size_t)(a >> 5) * nbaa + (b >> 5)) * 1024 + (a & 31) * 32 + (b & 31)];
+  }
+  G[idx] = v;
+}
+
+void launch_assemble_gram_fused(const double* tf, int nbf, int a0, int yb, const double* UU, const double* scale,
+                                const int* gate, const double* T, const double* taa, int nbaa, int K, int B,
+                                const double* d, double* G, cudaStream_t st) {
+  const int64_t tot = (int64_t)(K + B) * (K + B);
+  assemble_gram_fused_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(tf, nbf, a0, yb, UU, scale, gate, T, taa,
+                                                                             nbaa, K, B, d, G);
+}
+
 void launch_extract_rect(const double* tiles, int NB, int r0, int nr, int c0, int nc, const double* d,
                          double* out, cudaStream_t st) {
   const int64_t tot = (int64_t)nr * nc;
@@ -103,11 +159,16 @@ __device__ __forceinline__ double prand(unsigned a, unsigned b) {
   return ((double)h / 4294967296.0) * 2.0 - 1.0;
 }
 
-template <bool SMEM>
-__global__ void __launch_bounds__(SMALL_THREADS, 1)
+// FAST (n <= EIG_FAST_NMAX, 512 threads): phases B and G are column-oriented with
+// lane-owned rows (row r lives in lane r % 32, slot r / 32, of every warp): the
+// trailing update of column j-1 and the symmetric mat-vec of column j are one
+// sweep where each element costs LDS + 2 FMA + STS + 2 FMA and the vectors
+// v, w sit in registers; row sums are combined across warps in a fixed order.
+template <bool SMEM, bool FAST>
+__global__ void __launch_bounds__(FAST ? EIG_FAST_THREADS : SMALL_THREADS, 1)
 eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __restrict__ dscale,
                 double* __restrict__ W, double* __restrict__ sigma_out, double* __restrict__ ws,
-                int* __restrict__ status, long long* __restrict__ timers, double rank_tol) {
+                int* __restrict__ status, long long* __restrict__ timers, double rank_tol, int split) {
   extern __shared__ double sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nthr = blockDim.x, nwarps = nthr >> 5;
@@ -124,6 +185,18 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
   double* lam = e2 + n;                     // K
   double* red = lam + K;                    // 64 scratch
   int* clus = reinterpret_cast<int*>(red + 64);  // K cluster leaders
+  // FAST-only arrays (after clus): column starts, double-buffered v / w, row partials
+  constexpr int NT = (EIG_FAST_NMAX + 31) / 32;
+  const int npad = ((n + 31) / 32) * 32;
+  double* fbase = red + 64 + (K + 1) / 2 + 1;
+  int* cs = reinterpret_cast<int*>(fbase);                 // n ints
+  double* vsA = fbase + (n + 1) / 2 + 1;
+  double* vsB = vsA + npad;
+  double* wsv = vsB + npad;
+  double* ydot = wsv + npad;
+  double* psm = ydot + npad;
+  double* ypart = psm + npad;                              // [nwarps][npad]
+  double* scal = ypart + (size_t)(FAST ? EIG_FAST_THREADS / 32 : 0) * npad;  // 8 scalars
   double* Z = ws + npk;                     // n x K (col-major, ld n)
   double* Dp = Z + (size_t)n * K;           // K x n
   double* Dm = Dp + (size_t)n * K;          // K x n
@@ -140,6 +213,149 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
   __syncthreads();
 
   stamp(1);
+  if constexpr (FAST) {
+    // ---- B (fast): column-oriented Householder tridiagonalization, lane-owned rows
+    for (int c = tid; c < n; c += nthr) cs[c] = pidx(n, c, c);
+    for (int i = tid; i < npad; i += nthr) { vsA[i] = 0.0; vsB[i] = 0.0; wsv[i] = 0.0; ydot[i] = 0.0; }
+    __syncthreads();
+    double vO[NT], wO[NT], vN[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) { vO[t] = 0.0; wO[t] = 0.0; vN[t] = 0.0; }
+    double* vs_old = vsA;
+    double* vs_new = vsB;
+    long long sub[5] = {0, 0, 0, 0, 0}, tsub = 0;
+    auto tick = [&](int i) {  // diagnostics only (timers != null): barrier-accurate sub-phase clocks
+      if (timers == nullptr) return;
+      __syncthreads();
+      const long long now = clock64();
+      if (i >= 0) sub[i] += now - tsub;
+      tsub = now;
+    };
+    tick(-1);
+    for (int j = 0; j + 2 < n; ++j) {
+      // (a) column j: apply step j-1's update (rows >= j), then alpha and ||A[j+2:, j]||^2
+      if (warp == (j % nwarps)) {
+        const double wj = wsv[j], vj = vs_old[j];
+        double part = 0.0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int r = lane + 32 * t;
+          if (r >= j && r < n) {
+            const int a = cs[j] + (r - j);
+            const double x = Lp[a] - (vO[t] * wj + wO[t] * vj);
+            Lp[a] = x;
+            if (r >= j + 2) part = fma(x, x, part);
+          }
+        }
+        part = warp_sum(part);
+        if (lane == 0) scal[0] = part;
+      }
+      __syncthreads();
+      tick(0);
+      // (b) reflector of column j (every lane derives its own v rows; threads r publish v)
+      const double xn2 = scal[0];
+      const double alpha = Lp[cs[j] + 1];
+      double tj = 0.0, beta = alpha, scl = 0.0;
+      if (xn2 != 0.0) {
+        beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+        tj = (beta - alpha) / beta;
+        scl = 1.0 / (alpha - beta);
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const int r = lane + 32 * t;
+        vN[t] = (tj == 0.0 || r < j + 1 || r >= n) ? 0.0 : (r == j + 1 ? 1.0 : Lp[cs[j] + (r - j)] * scl);
+      }
+      __syncthreads();  // all reads of column j done before it is overwritten with the reflector
+      for (int r = tid; r < npad; r += nthr) {
+        double vr = 0.0;
+        if (tj != 0.0 && r >= j + 1 && r < n) {
+          if (r == j + 1) {
+            vr = 1.0;
+          } else {
+            vr = Lp[cs[j] + (r - j)] * scl;
+            Lp[cs[j] + (r - j)] = vr;
+          }
+        }
+        vs_new[r] = vr;
+      }
+      if (tid == 0) { dd[j] = Lp[cs[j]]; ee[j] = beta; tau[j] = tj; }
+      __syncthreads();
+      tick(1);
+      // (c) fused sweep over columns c >= j+1: update with (v_old, w_old), symv with v_new
+      double yp[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) yp[t] = 0.0;
+      for (int c = j + 1 + ((warp - (j + 1)) % nwarps + nwarps) % nwarps; c < n; c += nwarps) {
+        const double wpc = wsv[c], vpc = vs_old[c], vnc = vs_new[c];
+        const int base = cs[c] - c;
+        double dot = 0.0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int r = lane + 32 * t;
+          if (r >= c && r < n) {
+            const double x = Lp[base + r] - (vO[t] * wpc + wO[t] * vpc);
+            Lp[base + r] = x;
+            yp[t] = fma(x, vnc, yp[t]);
+            if (r > c) dot = fma(x, vN[t], dot);
+          }
+        }
+        dot = warp_sum(dot);
+        if (lane == 0) ydot[c] = dot;
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const int r = lane + 32 * t;
+        if (r < npad) ypart[(size_t)warp * npad + r] = yp[t];
+      }
+      __syncthreads();
+      tick(2);
+      // (d) p = tau * y (rows >= j+1), partials of p.v
+      double pv = 0.0;
+      for (int r = tid; r < npad; r += nthr) {
+        double y = 0.0;
+        if (r >= j + 1 && r < n) {
+          for (int w = 0; w < nwarps; ++w) y += ypart[(size_t)w * npad + r];
+          y += ydot[r];
+        }
+        const double pr = tj * y;
+        psm[r] = pr;
+        pv = fma(pr, vs_new[r], pv);
+      }
+      pv = warp_sum(pv);
+      if (lane == 0) red[warp] = pv;
+      __syncthreads();
+      tick(3);
+      // (e) w = p + kc v (kc = -tau/2 p.v); registers for own rows, smem for column values
+      double ptv = lane < nwarps ? red[lane] : 0.0;
+      ptv = warp_sum(ptv);
+      const double kc = -0.5 * tj * ptv;
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const int r = lane + 32 * t;
+        vO[t] = vN[t];
+        wO[t] = (r < npad) ? fma(kc, vs_new[r], psm[r]) : 0.0;
+      }
+      __syncthreads();  // every lane has read psm / red / old wsv
+      for (int r = tid; r < npad; r += nthr) wsv[r] = fma(kc, vs_new[r], psm[r]);
+      double* tmp = vs_old;
+      vs_old = vs_new;
+      vs_new = tmp;
+      __syncthreads();
+      tick(4);
+    }
+    if (timers != nullptr && tid == 0)
+      for (int i = 0; i < 5; ++i) timers[9 + i] = sub[i];
+    // pending update of the trailing 2x2 block with the last reflector
+    if (n >= 3 && tid == 0) {
+      for (int c = n - 2; c < n; ++c)
+        for (int r = c; r < n; ++r) {
+          const int a = cs[c] + (r - c);
+          Lp[a] -= vs_old[r] * wsv[c] + wsv[r] * vs_old[c];
+        }
+    }
+    __syncthreads();
+  } else {
   // ---- B: Householder tridiagonalization (lower, dsytd2-style)
   for (int j = 0; j + 2 < n; ++j) {
     const int m = n - j - 1;
@@ -192,6 +408,7 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
       for (int r = c + lane; r < m; r += 32) Lp[b0 + (r - c)] -= v[r] * wc + p[r] * vc;
     }
     __syncthreads();
+  }
   }
   if (tid == 0) {
     if (n >= 2) {
@@ -364,6 +581,14 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
   __syncthreads();
 
   stamp(6);
+  if (split) {  // phases G/H run in ldlt_pack_kernel (concurrently) and sign_weights_kernel
+    for (int k = tid; k < K; k += nthr) sigma_out[k] = sqrt(fmax(lam[k], 0.0));
+    if (tid == 0) {
+      for (int i = 0; i < n; ++i)
+        if (!isfinite(dd[i]) || !isfinite(G[(size_t)i * n + i])) { atomicOr(status, PSVD_ST_NONFINITE); break; }
+    }
+    return;
+  }
   // ---- G: R = chol(G + delta I), delta = 10 n eps max(diag G).
   // The reference's R is Householder's (well-determined only in the rows
   // where |R_ii| >> sqrt(eps)|C|); an unshifted Cholesky of the Gram turns the
@@ -388,6 +613,39 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
     if (i >= j) Lp[pidx(n, i, j)] = G[idx] + (i == j ? delta : 0.0);
   }
   __syncthreads();
+  if constexpr (FAST) {
+    // LDL^T, one barrier per column: column k is read-only in step k; rows lane-owned.
+    // Stored: diagonal D_k and the unscaled column A'[r][k] = L[r][k] D_k; R = D^-1/2 A'^T.
+    for (int k = 0; k + 1 < n; ++k) {
+      const double piv = Lp[cs[k]];
+      if (piv > 0.0) {
+        const double ipiv = 1.0 / piv;
+        double lr[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int r = lane + 32 * t;
+          lr[t] = (r > k && r < n) ? Lp[cs[k] + (r - k)] : 0.0;
+        }
+        for (int c = k + 1 + ((warp - (k + 1)) % nwarps + nwarps) % nwarps; c < n; c += nwarps) {
+          const double lc = Lp[cs[k] + (c - k)] * ipiv;
+          const int base = cs[c] - c;
+#pragma unroll
+          for (int t = 0; t < NT; ++t) {
+            const int r = lane + 32 * t;
+            if (r >= c && r < n) Lp[base + r] -= lr[t] * lc;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // convert to the Cholesky form used by phase H: column k -> A'[r][k] / sqrt(D_k)
+    for (int k = warp; k < n; k += nwarps) {
+      const double dk = Lp[cs[k]];
+      const double inv = dk > 0.0 ? 1.0 / sqrt(dk) : 0.0;
+      for (int r = k + lane; r < n; r += 32) Lp[cs[k] + (r - k)] *= inv;
+    }
+    __syncthreads();
+  } else {
   for (int k = 0; k < n; ++k) {
     const int ck = pidx(n, k, k);
     const double piv = Lp[ck];
@@ -406,6 +664,7 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
     __syncthreads();
   }
 
+  }
   stamp(7);
   // ---- H: sign rule on U_R = R V (R = L^T), weights, singular values
   for (int k = warp; k < K; k += nwarps) {
@@ -438,17 +697,148 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
 bool eig_supported(int n, int K) { return n >= 1 && K >= 1 && K <= n && K <= 1024; }
 
 void launch_eig_topk(const double* G, int n, int K, const double* dscale, double* W, double* sigma,
-                     double* ws, int* status, long long* timers, cudaStream_t st, double rank_tol) {
+                     double* ws, int* status, long long* timers, cudaStream_t st, double rank_tol, int split) {
+  const int npad = (n + 31) / 32 * 32;
   const size_t vec = (size_t)6 * n + K + 64 + (K + 1) / 2 + 2;
-  if (n <= EIG_NMAX_SMEM) {
-    const size_t smem = ((size_t)n * (n + 1) / 2 + vec) * sizeof(double);
-    cudaFuncSetAttribute(eig_topk_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    eig_topk_kernel<true><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers, rank_tol);
+  const size_t fast_extra = (size_t)(n + 1) / 2 + 1 + 5 * (size_t)npad + (size_t)(EIG_FAST_THREADS / 32) * npad + 8;
+  const size_t npk = (size_t)n * (n + 1) / 2;
+  const size_t limit = 227 * 1024;
+  if (n <= EIG_FAST_NMAX && (npk + vec + fast_extra) * sizeof(double) <= limit) {
+    const size_t smem = (npk + vec + fast_extra) * sizeof(double);
+    cudaFuncSetAttribute(eig_topk_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    eig_topk_kernel<true, true><<<1, EIG_FAST_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers,
+                                                                    rank_tol, split);
+  } else if (n <= EIG_NMAX_SMEM) {
+    const size_t smem = (npk + vec) * sizeof(double);
+    cudaFuncSetAttribute(eig_topk_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    eig_topk_kernel<true, false><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers,
+                                                                  rank_tol, 0);
   } else {
     const size_t smem = vec * sizeof(double);
-    cudaFuncSetAttribute(eig_topk_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    eig_topk_kernel<false><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers, rank_tol);
+    cudaFuncSetAttribute(eig_topk_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    eig_topk_kernel<false, false><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers,
+                                                                   rank_tol, 0);
   }
+}
+
+// ---------------------------------------------------------------- split core: LDL^T and sign/weights
+// The sign rule's factor R = chol(G + delta I) depends only on G, so it runs as its
+// own one-CTA kernel on an auxiliary stream, concurrently with the eigensolver.
+bool eig_split_supported(int n, int K) {
+  const size_t npk = (size_t)n * (n + 1) / 2;
+  return n <= EIG_FAST_NMAX && (npk + n) * sizeof(double) <= 227 * 1024 && K <= 1024;
+}
+
+__global__ void __launch_bounds__(EIG_FAST_THREADS, 1)
+ldlt_pack_kernel(const double* __restrict__ G, int n, double* __restrict__ Lout) {
+  extern __shared__ double sm[];
+  constexpr int NT = (EIG_FAST_NMAX + 31) / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x, nwarps = nthr >> 5;
+  const size_t npk = (size_t)n * (n + 1) / 2;
+  double* Lp = sm;
+  int* cs = reinterpret_cast<int*>(sm + npk);
+  double* red = sm + npk + (n + 1) / 2 + 1;
+  for (int c = tid; c < n; c += nthr) cs[c] = pidx(n, c, c);
+  double dmax = 0.0;
+  for (int i = tid; i < n; i += nthr) dmax = fmax(dmax, G[(size_t)i * n + i]);
+  dmax = warp_max(dmax);
+  if (lane == 0) red[warp] = dmax;
+  __syncthreads();
+  double gmax = 0.0;
+  for (int w = 0; w < nwarps; ++w) gmax = fmax(gmax, red[w]);
+  const double delta = 10.0 * (double)n * DBL_EPSILON * gmax;  // see the eigensolver's phase G
+  for (int64_t idx = tid; idx < (int64_t)n * n; idx += nthr) {
+    const int i = (int)(idx % n), j = (int)(idx / n);
+    if (i >= j) Lp[cs[j] + (i - j)] = G[idx] + (i == j ? delta : 0.0);
+  }
+  __syncthreads();
+  for (int k = 0; k + 1 < n; ++k) {
+    const double piv = Lp[cs[k]];
+    if (piv > 0.0) {
+      const double ipiv = 1.0 / piv;
+      double lr[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const int r = lane + 32 * t;
+        lr[t] = (r > k && r < n) ? Lp[cs[k] + (r - k)] : 0.0;
+      }
+      for (int c = k + 1 + ((warp - (k + 1)) % nwarps + nwarps) % nwarps; c < n; c += nwarps) {
+        const double lc = Lp[cs[k] + (c - k)] * ipiv;
+        const int base = cs[c] - c;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int r = lane + 32 * t;
+          if (r >= c && r < n) Lp[base + r] -= lr[t] * lc;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int k = warp; k < n; k += nwarps) {  // Cholesky columns A'[r][k] / sqrt(D_k), packed to global
+    const double dk = Lp[cs[k]];
+    const double inv = dk > 0.0 ? 1.0 / sqrt(dk) : 0.0;
+    for (int r = k + lane; r < n; r += 32) Lout[cs[k] + (r - k)] = Lp[cs[k] + (r - k)] * inv;
+  }
+}
+
+__global__ void __launch_bounds__(EIG_FAST_THREADS, 1)
+sign_weights_kernel(const double* __restrict__ Lg, const double* __restrict__ Z, const double* __restrict__ sigma_in,
+                    int n, int K, const double* __restrict__ dscale, double* __restrict__ W,
+                    double* __restrict__ sigma_out, int* __restrict__ status, double rank_tol) {
+  extern __shared__ double sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x, nwarps = nthr >> 5;
+  const size_t npk = (size_t)n * (n + 1) / 2;
+  double* Lp = sm;
+  for (size_t i = tid; i < npk; i += nthr) Lp[i] = Lg[i];
+  __syncthreads();
+  // U_R[i][k] = (R v_k)_i = sum_{j >= i} L[j][i] z_k[j]: thread per (i, k), written to W as scratch
+  for (int q = tid; q < n * K; q += nthr) {
+    const int i = q % n, k = q / n;
+    const int ci = pidx(n, i, i);
+    const double* z = Z + (size_t)k * n;
+    double s = 0.0;
+    for (int jj = i; jj < n; ++jj) s = fma(Lp[ci + (jj - i)], z[jj], s);
+    W[(size_t)k * n + i] = s;
+  }
+  __syncthreads();
+  for (int k = warp; k < K; k += nwarps) {
+    double ba = -1.0, bv = 0.0;
+    int bi = n;
+    for (int i = lane; i < n; i += 32) {
+      const double u = W[(size_t)k * n + i];
+      if (fabs(u) > ba) { ba = fabs(u); bv = u; bi = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {  // max |u|, lowest row on ties (numpy argmax)
+      const double oa = __shfl_xor_sync(0xffffffffu, ba, o);
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (oa > ba || (oa == ba && oi < bi)) { ba = oa; bv = ov; bi = oi; }
+    }
+    const double sg = bv < 0.0 ? -1.0 : 1.0;
+    const double sk = sigma_in[k];
+    const double s0 = sigma_in[0];
+    const bool keep = sk > 0.0 && sk > rank_tol * s0;
+    const double inv = keep ? sg / sk : 0.0;
+    if (sk == 0.0 && rank_tol == 0.0 && lane == 0) atomicOr(status, PSVD_ST_RANKDEF);
+    __syncwarp();
+    const double* z = Z + (size_t)k * n;
+    for (int i = lane; i < n; i += 32) W[(size_t)k * n + i] = (dscale ? dscale[i] : 1.0) * z[i] * inv;
+    if (lane == 0 && sigma_out != sigma_in) sigma_out[k] = sk;
+  }
+}
+
+void launch_ldlt_pack(const double* G, int n, double* Lout, cudaStream_t st) {
+  const size_t smem = ((size_t)n * (n + 1) / 2 + (n + 1) / 2 + 1 + 32) * sizeof(double);
+  cudaFuncSetAttribute(ldlt_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  ldlt_pack_kernel<<<1, EIG_FAST_THREADS, smem, st>>>(G, n, Lout);
+}
+
+void launch_sign_weights(const double* Lg, const double* Z, const double* sigma, int n, int K, const double* dscale,
+                         double* W, double* sigma_out, int* status, double rank_tol, cudaStream_t st) {
+  const size_t smem = ((size_t)n * (n + 1) / 2) * sizeof(double);
+  cudaFuncSetAttribute(sign_weights_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  sign_weights_kernel<<<1, EIG_FAST_THREADS, smem, st>>>(Lg, Z, sigma, n, K, dscale, W, sigma_out, status, rank_tol);
 }
 
 // ---------------------------------------------------------------- Rayleigh refinement

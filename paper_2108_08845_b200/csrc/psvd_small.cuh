@@ -8,6 +8,8 @@ namespace psvd {
 
 constexpr int SMALL_THREADS = 1024;
 constexpr int EIG_NMAX_SMEM = 224;   // packed lower triangle kept in shared memory up to this n
+constexpr int EIG_FAST_NMAX = 216;   // column-oriented lane-owned-rows path (7 rows per lane, 16 warps)
+constexpr int EIG_FAST_THREADS = 512;
 
 // Extract the n x n Gram block (rows/cols [c0, c0+n) of the combined column space)
 // from reduced 32x32 tiles (tile id I*NB+J, I <= J computed), scaled symmetrically
@@ -17,6 +19,9 @@ void launch_extract_sym(const double* tiles, int NB, int c0, int n, const double
 // Assemble the streaming Gram from the narrow [U | A] pass tiles and the A^T A pass tiles.
 void launch_assemble_gram(const double* tua, int nbua, const double* taa, int nbaa, int K, int B, const double* d,
                           double* G, cudaStream_t st);
+void launch_assemble_gram_fused(const double* tf, int nbf, int a0, int yb, const double* UU, const double* scale,
+                                const int* gate, const double* T, const double* taa, int nbaa, int K, int B,
+                                const double* d, double* G, cudaStream_t st);
 // Extract the rectangular block rows [r0, r0+nr) x cols [c0, c0+nc) (r-block <= c-block),
 // scaled by row factors d (length nr, may be null).  col-major, ld nr.
 void launch_extract_rect(const double* tiles, int NB, int r0, int nr, int c0, int nc, const double* d,
@@ -32,7 +37,15 @@ void launch_extract_rect(const double* tiles, int NB, int r0, int nr, int c0, in
 size_t eig_workspace_doubles(int n, int K);
 // timers (optional, device): clock64() at the 9 phase boundaries (diagnostics).
 void launch_eig_topk(const double* G, int n, int K, const double* dscale, double* W, double* sigma,
-                     double* ws, int* status, long long* timers, cudaStream_t st, double rank_tol = 0.0);
+                     double* ws, int* status, long long* timers, cudaStream_t st, double rank_tol = 0.0,
+                     int split = 0);
+// Split core (n <= EIG_FAST_NMAX): eig with split = 1 leaves Z in ws + n(n+1)/2 and sqrt(lambda)
+// in sigma; ldlt_pack (concurrent, needs only G) writes chol(G + delta I) packed to Lout;
+// sign_weights then applies the sign rule and writes W.
+bool eig_split_supported(int n, int K);
+void launch_ldlt_pack(const double* G, int n, double* Lout, cudaStream_t st);
+void launch_sign_weights(const double* Lg, const double* Z, const double* sigma, int n, int K, const double* dscale,
+                         double* W, double* sigma_out, int* status, double rank_tol, cudaStream_t st);
 bool eig_supported(int n, int K);
 
 // Rayleigh refinement of sigma from the recomposed columns' norms (see psvd_small.cu).

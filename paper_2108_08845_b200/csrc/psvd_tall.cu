@@ -5,12 +5,12 @@ namespace psvd {
 
 __host__ __device__ static inline int round_up(int x, int m) { return (x + m - 1) / m * m; }
 
-size_t tall_smem_bytes(int ks, int np_pad, int wk, int w) {
+size_t tall_smem_bytes(int ks, int np_pad, int wk, int w, int nstage) {
   const int ksp = ks + 4;
   size_t b = 0;
   b += sizeof(const double*) * (size_t)np_pad;  // column base pointers
   b = (b + 15) / 16 * 16;
-  b += sizeof(double) * 2 * (size_t)np_pad * ksp;  // double-buffered panel stage
+  b += sizeof(double) * nstage * (size_t)np_pad * ksp;  // multi-buffered panel stages
   if (w > 0) {
     b += sizeof(double) * (size_t)round_up(w, 32) * ksp;                    // Y stage
     b += sizeof(double) * (size_t)round_up(wk, 4) * (round_up(w, 8) + 4);   // W
@@ -18,7 +18,10 @@ size_t tall_smem_bytes(int ks, int np_pad, int wk, int w) {
   return b;
 }
 
-template <int KS, int MAXCB>
+// NJB: 8-column blocks computed per Gram tile column (4 = full 32x32 tile; 2 when
+// every tile's column block is a Y block of <= 16 columns, e.g. U^T U and A^T U
+// for K <= 16 — halves the DMMA work of the fused recompose pass).
+template <int KS, int MAXCB, int NS, int NJB>
 __global__ void __launch_bounds__(NTHR, 1) tall_pass_kernel(const TallParams p) {
   constexpr int KSP = KS + 4;   // = 4 (mod 16)
   constexpr int RB = KS / 8;    // 8-row blocks per stage
@@ -40,25 +43,23 @@ __global__ void __launch_bounds__(NTHR, 1) tall_pass_kernel(const TallParams p) 
   const double** colptr = reinterpret_cast<const double**>(smem_raw);
   size_t off = ((sizeof(const double*) * (size_t)np_pad) + 15) / 16 * 16;
   double* sP = reinterpret_cast<double*>(smem_raw + off);
-  off += sizeof(double) * 2 * (size_t)np_pad * KSP;
+  off += sizeof(double) * NS * (size_t)np_pad * KSP;
   double* sY = reinterpret_cast<double*>(smem_raw + off);
   double* sW = sY + (size_t)ycols * KSP;
 
   for (int c = tid; c < np_pad; c += NTHR) {
     const double* ptr = nullptr;
-    int base = 0;
     for (int s = 0; s < p.nseg; ++s) {
-      if (c >= base && c < base + p.seg[s].ncols) ptr = p.seg[s].ptr + (int64_t)(c - base) * p.seg[s].ld;
-      base += p.seg[s].ncols;
+      const int c0 = p.seg[s].col0;
+      if (c >= c0 && c < c0 + p.seg[s].ncols) ptr = p.seg[s].ptr + (int64_t)(c - c0) * p.seg[s].ld;
     }
     colptr[c] = ptr;
   }
-  {  // zero the padded panel columns of both buffers (never written by cp.async)
-    const int padn = (np_pad - p.np) * KSP;
-    for (int i = tid; i < 2 * padn; i += NTHR) {
-      const int b = i / padn, r = i % padn;
-      sP[(size_t)b * np_pad * KSP + (size_t)p.np * KSP + r] = 0.0;
-    }
+  __syncthreads();
+  // zero the padding columns (no source) of every stage buffer; cp.async never writes them
+  for (int i = tid; i < NS * np_pad * KSP; i += NTHR) {
+    const int c = (i / KSP) % np_pad;
+    if (colptr[c] == nullptr) sP[i] = 0.0;
   }
   if (has_y) {
     for (int i = tid; i < ycols * KSP; i += NTHR) sY[i] = 0.0;
@@ -80,15 +81,16 @@ __global__ void __launch_bounds__(NTHR, 1) tall_pass_kernel(const TallParams p) 
       const int64_t r = r0 + 2 * pc;
       const int64_t valid = row_end - r;
       const int bytes = valid >= 2 ? 16 : (valid == 1 ? 8 : 0);
-      const double* src = colptr[c] + (bytes > 0 ? r : row_begin);
-      cp_async16(dst_base + (size_t)c * KSP + 2 * pc, src, bytes);
+      const double* cp = colptr[c];
+      if (cp == nullptr) continue;  // padding column: stays zero
+      cp_async16(dst_base + (size_t)c * KSP + 2 * pc, cp + (bytes > 0 ? r : row_begin), bytes);
     }
   };
 
   const WarpPlan wp = p.plan[slice][warp];
-  double acc[2][4][4][2];
+  double acc[TPW][4][4][2];
 #pragma unroll
-  for (int t = 0; t < 2; ++t)
+  for (int t = 0; t < TPW; ++t)
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -98,33 +100,55 @@ __global__ void __launch_bounds__(NTHR, 1) tall_pass_kernel(const TallParams p) 
   int64_t cm_row = -1;
   const bool do_cm = has_y && p.colmax != nullptr && slice == 0 && tid < p.w;
 
-  if (nstage > 0) prefetch(0, 0);
-  cp_async_commit();
+  // NS-stage cp.async pipeline: stage s lives in buffer s % NS; the barrier at the top of
+  // iteration s also retires iteration s-1, whose buffer the new prefetch reuses
+#pragma unroll
+  for (int s0 = 0; s0 < NS - 1; ++s0) {
+    if (s0 < nstage) prefetch(s0, s0);
+    cp_async_commit();
+  }
 
   for (int64_t s = 0; s < nstage; ++s) {
-    const int buf = (int)(s & 1);
-    if (s + 1 < nstage) prefetch(s + 1, buf ^ 1);
-    cp_async_commit();
-    cp_async_wait<1>();
+    const int buf = (int)(s % NS);
+    cp_async_wait<NS - 2>();
     __syncthreads();
+    if (s + NS - 1 < nstage) prefetch(s + NS - 1, (int)((s + NS - 1) % NS));
+    cp_async_commit();
     const double* P = sP + (size_t)buf * np_pad * KSP;
     const int64_t r0 = row_begin + s * KS;
 
     if (has_y) {
       // Y(KS x w_pad) = P[:, wlo:wlo+wk] * W on DMMA; warp -> row block rb, column blocks cb0 + CG*j
       const int rb = warp % RB, cb0 = warp / RB, ncb = w_pad >> 3;
-      double ya[MAXCB][2];
+      double ya[MAXCB][2], yb[MAXCB][2];  // two accumulator chains (even / odd k-steps)
 #pragma unroll
-      for (int j = 0; j < MAXCB; ++j) ya[j][0] = ya[j][1] = 0.0;
+      for (int j = 0; j < MAXCB; ++j) ya[j][0] = ya[j][1] = yb[j][0] = yb[j][1] = 0.0;
       const double* pa = P + (size_t)(p.wlo + tq) * KSP + rb * 8 + g;
       const double* pb = sW + (size_t)tq * wsp + g;
-      for (int k0 = 0; k0 < wk_pad; k0 += 4) {
-        const double a = pa[(size_t)k0 * KSP];
+      int k0 = 0;
+      for (; k0 + 8 <= wk_pad; k0 += 8) {
+        const double a0 = pa[(size_t)k0 * KSP], a1 = pa[(size_t)(k0 + 4) * KSP];
 #pragma unroll
         for (int j = 0; j < MAXCB; ++j) {
           const int cb = cb0 + CG * j;
-          if (cb < ncb) dmma884(ya[j][0], ya[j][1], a, pb[(size_t)k0 * wsp + cb * 8]);
+          if (cb < ncb) {
+            dmma884(ya[j][0], ya[j][1], a0, pb[(size_t)k0 * wsp + cb * 8]);
+            dmma884(yb[j][0], yb[j][1], a1, pb[(size_t)(k0 + 4) * wsp + cb * 8]);
+          }
         }
+      }
+      if (k0 < wk_pad) {
+        const double a0 = pa[(size_t)k0 * KSP];
+#pragma unroll
+        for (int j = 0; j < MAXCB; ++j) {
+          const int cb = cb0 + CG * j;
+          if (cb < ncb) dmma884(ya[j][0], ya[j][1], a0, pb[(size_t)k0 * wsp + cb * 8]);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < MAXCB; ++j) {
+        ya[j][0] += yb[j][0];
+        ya[j][1] += yb[j][1];
       }
 #pragma unroll
       for (int j = 0; j < MAXCB; ++j) {
@@ -164,11 +188,33 @@ __global__ void __launch_bounds__(NTHR, 1) tall_pass_kernel(const TallParams p) 
     }
 
     // Gram tiles over the combined [P | Y] column space
-    if (wp.ntile > 0) {
+    if (wp.ntile > 0 && wp.ksplit == 1) {
+#pragma unroll
+      for (int kk = 0; kk < KS / 4; ++kk) {
+        const int k0 = kk * 4;
+#pragma unroll
+        for (int t = 0; t < TPW; ++t) {
+          if (t < wp.ntile) {
+            const int I = wp.ti[t], J = wp.tj[t];
+            const double* bI = (I * 32 < np_pad) ? P + (size_t)I * 32 * KSP : sY + (size_t)(I * 32 - np_pad) * KSP;
+            const double* bJ = (J * 32 < np_pad) ? P + (size_t)J * 32 * KSP : sY + (size_t)(J * 32 - np_pad) * KSP;
+            double fa[4], fb[NJB];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) fa[q] = bI[(size_t)(q * 8 + g) * KSP + k0 + tq];
+#pragma unroll
+            for (int q = 0; q < NJB; ++q) fb[q] = bJ[(size_t)(q * 8 + g) * KSP + k0 + tq];
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+              for (int b = 0; b < NJB; ++b) dmma884(acc[t][a][b][0], acc[t][a][b][1], fa[a], fb[b]);
+          }
+        }
+      }
+    } else if (wp.ntile > 0) {
       for (int kk = wp.kpart; kk < KS / 4; kk += wp.ksplit) {
         const int k0 = kk * 4;
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
+        for (int t = 0; t < TPW; ++t) {
           if (t < wp.ntile) {
             const int I = wp.ti[t], J = wp.tj[t];
             const double* bI = (I * 32 < np_pad) ? P + (size_t)I * 32 * KSP : sY + (size_t)(I * 32 - np_pad) * KSP;
@@ -187,15 +233,14 @@ __global__ void __launch_bounds__(NTHR, 1) tall_pass_kernel(const TallParams p) 
         }
       }
     }
-    __syncthreads();
   }
   cp_async_wait<0>();
 
   if (wp.ntile > 0) {
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
+    for (int t = 0; t < TPW; ++t) {
       if (t < wp.ntile) {
-        double* dst = p.partial + ((size_t)blockIdx.x * SLOTS + warp * 2 + t) * 1024;
+        double* dst = p.partial + ((size_t)blockIdx.x * SLOTS + warp * TPW + t) * 1024;
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -215,6 +260,128 @@ __global__ void __launch_bounds__(NTHR, 1) tall_pass_kernel(const TallParams p) 
 // Fixed-order reduction of the per-CTA partial tiles: block (32 elements of one
 // output tile) x 8 warps; warp w sums sources w, w+8, ... (chunk-major order),
 // then the 8 warp sums are added in warp order.  Bitwise reproducible.
+// ---------------------------------------------------------------- warp-specialized Gram
+// Gram-only passes (no Y): warp NWARP-1 streams 32-row stages into an NS-deep
+// ring with cp.async + mbarrier (full[b]: 32 producer lanes, empty[b]: the
+// consumer warps); warps 0..NWARP-2 each own one 32x32 tile and never wait on
+// a CTA barrier, so the DMMA pipe is not drained at stage boundaries.
+size_t gram_ws_smem_bytes(int np_pad, int ns) {
+  size_t b = sizeof(const double*) * (size_t)np_pad;
+  b = (b + 15) / 16 * 16;
+  b += 2 * ns * sizeof(uint64_t);
+  b = (b + 15) / 16 * 16;
+  return b + sizeof(double) * ns * (size_t)np_pad * 36;
+}
+
+template <int NS>
+__global__ void __launch_bounds__(NTHR, 1) gram_ws_kernel(const TallParams p) {
+  constexpr int KS = 32, KSP = 36;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int slice = blockIdx.x % p.nslices;
+  const int64_t chunk = blockIdx.x / p.nslices;
+  const int64_t row_begin = chunk * p.rows_per_cta;
+  const int64_t row_end = min(p.M, row_begin + p.rows_per_cta);
+  const int np_pad = p.np_pad;
+  const double** colptr = reinterpret_cast<const double**>(smem_raw);
+  size_t off = ((sizeof(const double*) * (size_t)np_pad) + 15) / 16 * 16;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + off);
+  uint64_t* empty = full + NS;
+  off += (2 * NS * sizeof(uint64_t) + 15) / 16 * 16;
+  double* sP = reinterpret_cast<double*>(smem_raw + off);
+  constexpr int PROD = NWARP - 1;
+  int ncons = 0;  // consumer warps of this slice (all arrive on `empty`)
+  for (int w = 0; w < PROD; ++w) ncons += p.plan[slice][w].ntile > 0;
+  for (int c = tid; c < np_pad; c += NTHR) {
+    const double* ptr = nullptr;
+    for (int s = 0; s < p.nseg; ++s) {
+      const int c0 = p.seg[s].col0;
+      if (c >= c0 && c < c0 + p.seg[s].ncols) ptr = p.seg[s].ptr + (int64_t)(c - c0) * p.seg[s].ld;
+    }
+    colptr[c] = ptr;
+  }
+  __syncthreads();
+  // zero the padding columns (no source) of every stage buffer; cp.async never writes them
+  for (int i = tid; i < NS * np_pad * KSP; i += NTHR) {
+    const int c = (i / KSP) % np_pad;
+    if (colptr[c] == nullptr) sP[i] = 0.0;
+  }
+  if (tid == 0) {
+    for (int b = 0; b < NS; ++b) {
+      mbar_init(&full[b], 32);
+      mbar_init(&empty[b], (unsigned)max(ncons, 1));
+    }
+  }
+  __syncthreads();
+  const int64_t nstage = row_end > row_begin ? (row_end - row_begin + KS - 1) / KS : 0;
+
+  if (warp == PROD) {
+    const int nchunk16 = p.np * (KS / 2);
+    for (int64_t s = 0; s < nstage; ++s) {
+      const int b = (int)(s % NS);
+      if (s >= NS) mbar_wait(&empty[b], (unsigned)(((s / NS) - 1) & 1));
+      const int64_t r0 = row_begin + s * KS;
+      double* dst_base = sP + (size_t)b * np_pad * KSP;
+      for (int q = lane; q < nchunk16; q += 32) {
+        const int c = q >> 4, pc = q & 15;
+        const int64_t r = r0 + 2 * pc;
+        const int64_t valid = row_end - r;
+        const int bytes = valid >= 2 ? 16 : (valid == 1 ? 8 : 0);
+        const double* cp = colptr[c];
+        if (cp == nullptr) continue;
+        cp_async16(dst_base + (size_t)c * KSP + 2 * pc, cp + (bytes > 0 ? r : row_begin), bytes);
+      }
+      cp_async_mbar_arrive(&full[b]);
+    }
+    cp_async_wait<0>();
+    return;
+  }
+
+  const WarpPlan wp = p.plan[slice][warp];
+  if (wp.ntile == 0) return;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+  const int I = wp.ti[0], J = wp.tj[0];
+  for (int64_t s = 0; s < nstage; ++s) {
+    const int b = (int)(s % NS);
+    mbar_wait(&full[b], (unsigned)((s / NS) & 1));
+    const double* P = sP + (size_t)b * np_pad * KSP;
+    const double* bI = P + (size_t)I * 32 * KSP + g * KSP + tq;
+    const double* bJ = P + (size_t)J * 32 * KSP + g * KSP + tq;
+#pragma unroll
+    for (int kk = 0; kk < KS / 4; ++kk) {
+      double fa[4], fb[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        fa[q] = bI[(size_t)q * 8 * KSP + kk * 4];
+        fb[q] = bJ[(size_t)q * 8 * KSP + kk * 4];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dmma884(acc[a][c][0], acc[a][c][1], fa[a], fb[c]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);
+  }
+  double* dst = p.partial + ((size_t)blockIdx.x * SLOTS + warp * TPW) * 1024;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      *reinterpret_cast<double2*>(dst + (a * 8 + g) * 32 + c * 8 + 2 * tq) = make_double2(acc[a][c][0], acc[a][c][1]);
+}
+
+void launch_gram_ws(const TallParams& p, int grid, cudaStream_t st) {
+  const size_t smem = gram_ws_smem_bytes(p.np_pad, 3);
+  cudaFuncSetAttribute(gram_ws_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  gram_ws_kernel<3><<<grid, NTHR, smem, st>>>(p);
+}
+
 __global__ void __launch_bounds__(256) tall_reduce_kernel(const double* __restrict__ partial, const ReduceMap map,
                                                           double* __restrict__ tiles) {
   __shared__ double red[8][33];
@@ -239,31 +406,41 @@ __global__ void __launch_bounds__(256) tall_reduce_kernel(const double* __restri
   }
 }
 
-template <int KS>
+template <int KS, int NS, int NJB>
 static void launch_ks(const TallParams& p, int grid, size_t smem, cudaStream_t st) {
   const int ncb = p.w_pad / 8;
   constexpr int CG = NWARP / (KS / 8);
-  if ((ncb + CG - 1) / CG <= 1) {
-    cudaFuncSetAttribute(tall_pass_kernel<KS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    tall_pass_kernel<KS, 1><<<grid, NTHR, smem, st>>>(p);
-  } else if ((ncb + CG - 1) / CG <= 2) {
-    cudaFuncSetAttribute(tall_pass_kernel<KS, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    tall_pass_kernel<KS, 2><<<grid, NTHR, smem, st>>>(p);
-  } else if ((ncb + CG - 1) / CG <= 4) {
-    cudaFuncSetAttribute(tall_pass_kernel<KS, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    tall_pass_kernel<KS, 4><<<grid, NTHR, smem, st>>>(p);
-  } else {
-    cudaFuncSetAttribute(tall_pass_kernel<KS, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    tall_pass_kernel<KS, 8><<<grid, NTHR, smem, st>>>(p);
-  }
+  const int per = (ncb + CG - 1) / CG;
+#define PSVD_LAUNCH(MCB)                                                                                   \
+  do {                                                                                                     \
+    cudaFuncSetAttribute(tall_pass_kernel<KS, MCB, NS, NJB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    tall_pass_kernel<KS, MCB, NS, NJB><<<grid, NTHR, smem, st>>>(p);                                       \
+  } while (0)
+  if (per <= 1)
+    PSVD_LAUNCH(1);
+  else if (per <= 2)
+    PSVD_LAUNCH(2);
+  else
+    PSVD_LAUNCH(4);  // w <= MAX_W = 128 -> at most 16 column blocks over CG = 4 warp groups
+#undef PSVD_LAUNCH
 }
 
 void launch_tall(const TallParams& p, int grid, cudaStream_t st) {
-  const size_t smem = tall_smem_bytes(p.ks, p.np_pad, p.wk, p.w);
-  if (p.ks == 32)
-    launch_ks<32>(p, grid, smem, st);
-  else
-    launch_ks<16>(p, grid, smem, st);
+  const size_t smem = tall_smem_bytes(p.ks, p.np_pad, p.wk, p.w, p.nstage);
+  if (p.narrow) {
+    if (p.ks == 32 && p.nstage == 3)
+      launch_ks<32, 3, 2>(p, grid, smem, st);
+    else if (p.ks == 32)
+      launch_ks<32, 2, 2>(p, grid, smem, st);
+    else
+      launch_ks<16, 2, 2>(p, grid, smem, st);
+  } else if (p.ks == 32 && p.nstage == 3) {
+    launch_ks<32, 3, 4>(p, grid, smem, st);
+  } else if (p.ks == 32) {
+    launch_ks<32, 2, 4>(p, grid, smem, st);
+  } else {
+    launch_ks<16, 2, 4>(p, grid, smem, st);
+  }
 }
 
 void launch_tall_reduce(const double* partial, const ReduceMap& map, double* tiles, cudaStream_t st) {

@@ -23,10 +23,11 @@ namespace psvd {
 
 // rows per stage KS is a template parameter (32, or 16 when the panel + W do not
 // fit 227 KB); the smem column stride KS + 4 is 4 (mod 16) -> conflict-free fragments.
-constexpr int NWARP = 8;
+constexpr int NWARP = 16;  // 4 warps per SMSP keep the DMMA pipe fed through LDS/barrier latency
 constexpr int NTHR = NWARP * 32;
+constexpr int TPW = 1;     // Gram tiles per warp (64 accumulator doubles -> <= 128 registers)
 constexpr int MAX_SEG = 4;
-constexpr int SLOTS = 16;    // partial tile slots per CTA (8 warps x 2 tiles)
+constexpr int SLOTS = NWARP * TPW;  // partial tile slots per CTA
 constexpr int MAX_SLICES = 4;
 constexpr int MAX_OUT_TILES = 64;
 constexpr int MAX_W = 128;   // widest Y
@@ -35,7 +36,7 @@ struct Seg {
   const double* ptr;
   int64_t ld;
   int ncols;
-  int pad_;
+  int col0;  // first column in the panel space (plan_pass fills it; pass 1 on input = align to 32)
 };
 
 struct WarpPlan {
@@ -47,6 +48,8 @@ struct TallParams {
   int64_t M;
   int64_t rows_per_cta;  // multiple of 32
   int ks;                // rows per stage (32 or 16)
+  int nstage;            // cp.async pipeline depth (2 or 3)
+  int narrow;            // every Gram tile's column block is a Y block of <= 16 columns (NJB = 2)
   int nseg;
   Seg seg[MAX_SEG];
   int np, np_pad;        // panel columns; padded to a multiple of 32 (start of the Y block)
@@ -68,12 +71,15 @@ struct ReduceMap {
   int nchunks, nslices;
   short out_id[MAX_OUT_TILES];                    // destination tile id (I * NB + J)
   unsigned char nsrc[MAX_OUT_TILES];
-  unsigned char src[MAX_OUT_TILES][2 * NWARP];    // slice * SLOTS + slot
+  unsigned char src[MAX_OUT_TILES][NWARP];        // slice * SLOTS + slot
 };
 
-size_t tall_smem_bytes(int ks, int np_pad, int wk, int w);
+size_t tall_smem_bytes(int ks, int np_pad, int wk, int w, int nstage);
 
 void launch_tall(const TallParams& p, int grid, cudaStream_t st);
+// Warp-specialized Gram-only pass (w == 0, KS = 32, <= NWARP-1 tiles per slice, ksplit == 1).
+size_t gram_ws_smem_bytes(int np_pad, int ns);
+void launch_gram_ws(const TallParams& p, int grid, cudaStream_t st);
 void launch_tall_reduce(const double* partial, const ReduceMap& map, double* tiles, cudaStream_t st);
 
 }  // namespace psvd

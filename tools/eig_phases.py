@@ -19,11 +19,12 @@ def main(n=210, K=10):
     for _ in range(10):
         nat.call("psvd_core_eig", c, nat.ptr(G), n, nat._vp(0), 1.0, 0, K, nat.ptr(W), nat.ptr(s), st)
     e1.record(); torch.cuda.synchronize()
-    t = (ctypes.c_longlong * 9)()
+    t = (ctypes.c_longlong * 14)()
     nat.lib().psvd_eig_phase_cycles(c, t)
     names = ["load", "tridiag", "bisect", "twisted", "mgs", "backxf", "ldlt", "sign+W"]
     d = [t[i + 1] - t[i] for i in range(8)]
     print(f"n={n} K={K}: {e0.elapsed_time(e1)/10*1e3:.1f} us/launch; cycles", dict(zip(names, d)), "total", t[8] - t[0])
+    print("tridiag sub-phases (a..e):", [t[9 + i] for i in range(5)])
     ref = np.linalg.svd(a, compute_uv=False)[:K]
     print("sigma rel err", np.max(np.abs(s.cpu().numpy() - ref) / ref))
 
