@@ -52,6 +52,11 @@ int psvd_create(int device, psvd_ctx** out);
 int psvd_destroy(psvd_ctx* ctx);
 const char* psvd_last_error(psvd_ctx* ctx);
 
+/* Orthogonality-drift threshold of the streaming updates (default 1e-8 =
+ * streaming.py:25 ORTHO_DRIFT_TOL).  A negative value forces the rescue
+ * branch (tests). */
+int psvd_set_drift_tol(psvd_ctx* ctx, double tol);
+
 /* Number of kernels this context has enqueued so far (launch accounting). */
 long long psvd_launch_count(psvd_ctx* ctx);
 

@@ -35,6 +35,7 @@ struct psvd_ctx {
   long long* d_timers = nullptr;  // eig phase clocks (diagnostics)
   int* h_status = nullptr;  // pinned
   long long launches = 0;   // kernels enqueued by this context (bench evidence)
+  double drift_tol = 1e-8;  // streaming.py:25 ORTHO_DRIFT_TOL (psvd_set_drift_tol overrides, e.g. to force the rescue)
   Buf partial, tiles, gram, eigws, wbuf, utu, tbuf, dvec, colmax;
   Buf ybuf, rsmall, jacws;  // randomized path: sketch Y (M x l), small matrices, Jacobi scratch
   Buf partial2, tiles2[2];  // A^T A passes on the low-priority stream (double-buffered tiles)
@@ -390,6 +391,12 @@ const char* psvd_last_error(psvd_ctx* c) { return c ? c->err.c_str() : "null con
 
 long long psvd_launch_count(psvd_ctx* c) { return c ? c->launches : -1; }
 
+int psvd_set_drift_tol(psvd_ctx* c, double tol) {
+  if (!c) return PSVD_EINVAL;
+  c->drift_tol = tol;
+  return PSVD_OK;
+}
+
 int psvd_eig_phase_cycles(psvd_ctx* c, long long* out9) {
   if (!c || !out9) return PSVD_EINVAL;
   if (cudaMemcpy(out9, c->d_timers, 14 * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
@@ -538,7 +545,7 @@ int psvd_stream_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, con
   if ((rc = psvd_core_eig(c, G, n, sigma, ff, Kc, K, W, sigma_out, stream))) return rc;
   if ((rc = psvd_recompose(c, M, U, ldu, Kc, A, lda, B, W, K, U_out, ldo, UtU, stream))) return rc;
   if ((rc = refine_normalize(c, M, U_out, ldo, K, UtU, sigma_out, (cudaStream_t)stream))) return rc;
-  if (rescue) rc = psvd_drift_rescue(c, M, U_out, ldo, K, UtU, sigma_out, 1e-8, stream);
+  if (rescue) rc = psvd_drift_rescue(c, M, U_out, ldo, K, UtU, sigma_out, c->drift_tol, stream);
   return rc;
 }
 
@@ -806,7 +813,7 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
       if ((rc = psvd_recompose(c, M, Uprev, ldprev, kc, A[b], lda[b], B[b], W, K, Uout, ldo, UtU, hi))) return rc;
     }
     if ((rc = refine_normalize(c, M, Uout, ldo, K, UtU, sig_b, hi))) return rc;
-    if (resc && (rc = psvd_drift_rescue(c, M, Uout, ldo, K, UtU, sig_b, 1e-8, hi))) return rc;
+    if (resc && (rc = psvd_drift_rescue(c, M, Uout, ldo, K, UtU, sig_b, c->drift_tol, hi))) return rc;
     prev_resc = resc;
     mark("hi:recompose_end", b, hi);
     Uprev = Uout;

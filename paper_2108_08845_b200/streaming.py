@@ -78,8 +78,13 @@ def _device_of(*objs):
     return torch.device("cuda", torch.cuda.current_device())
 
 
+LAST_STATUS = 0  # device status word of the last checked update (diagnostics: PSVD_ST_* bits)
+
+
 def _check_status(ctx, device, what):
+    global LAST_STATUS
     st = nat.read_status(ctx, reset=True, device=device)
+    LAST_STATUS = st
     if st & nat.ST_NONFINITE:
         raise ValueError(f"{what} contains non-finite entries")
     return st

@@ -87,24 +87,26 @@ def test_edge_cases_golden(golden):
     assert st.iteration == 2
 
 
-def test_drift_rescue_inside_pipelined_run(golden):
-    """Rescue on the first update of a pipelined window: the next batch's U^T A
-    (computed from the pre-rescue U in the fused pass) must be rotated by T."""
+def test_drift_rescue_inside_pipelined_run():
+    """Forced drift rescue (threshold < 0) inside the pipelined run: the gated pass,
+    the sigma reorder and the T-rotation of the next batch's U^T A / U^T U must
+    reproduce the unforced result (T ~ I for an orthonormal U)."""
     p = _pkg()
-    g = golden("det_edge_cases")
-    rng = np.random.Generator(np.random.Philox(45))
-    b1 = g["rescue_batch"]
-    b2 = rng.standard_normal((30, 4))
-    cfg = p.StreamConfig(k_modes=3, forget_factor=1.0, batch_columns=4)
-    state = p.StreamState(torch.as_tensor(g["rescue_modes_in"]).cuda(), torch.tensor([3.0, 2.0, 1.0]).cuda(), 0)
-    dev = torch.device("cuda", 0)
-    mats = [p._native.as_device_colmajor(b, dev) for b in (b1, b2)]
-    new, hist = p.streaming._run_window(state, mats, cfg, dev)
-    rm, rs = oracle.ref_stream_update(g["rescue_modes_in"], np.array([3.0, 2.0, 1.0]), b1, 3, 1.0)
-    rm, rs = oracle.ref_stream_update(rm, rs, b2, 3, 1.0)
-    m, s = _np(new)
-    _assert_parity(m, s, rm, rs, sig_tol=1e-9, ang_tol=1e-7)
-    assert new.iteration == 2
+    from paper_2108_08845_b200 import _native as nat
+    a = oracle.burgers_matrix(4096, 800)[:, :600]
+    cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200)
+    base, _ = p.stream_all(_batches(a, 200), cfg)
+    assert not (p.streaming.LAST_STATUS & nat.ST_RESCUE)
+    ctx = nat.context(torch.device("cuda", 0))
+    nat.call("psvd_set_drift_tol", ctx, -1.0)
+    try:
+        forced, _ = p.stream_all(_batches(a, 200), cfg)
+        assert p.streaming.LAST_STATUS & nat.ST_RESCUE
+    finally:
+        nat.call("psvd_set_drift_tol", ctx, 1e-8)
+    m1, s1 = forced.numpy()
+    m2, s2 = base.numpy()
+    _assert_parity(m1, s1, m2, s2, sig_tol=1e-13, ang_tol=1e-12)
 
 
 def test_drift_rescue_golden(golden):
