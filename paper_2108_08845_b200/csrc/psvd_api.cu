@@ -162,6 +162,60 @@ int plan_tiles(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& ti
   return PSVD_OK;
 }
 
+// Warp-specialized Gram: spread the tiles over (slice, SMSP) bins so that every SMSP's DMMA
+// pipe gets the same number of 8x8 blocks per k-step (warp w issues on SMSP w % 4; a diagonal
+// tile needs 10 of 16 blocks, a tile on the panel's last partial block fewer).  Longest-
+// processing-time greedy; the kernel's pace is the busiest SMSP of the busiest slice.
+static int plan_tiles_balanced(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& tiles, int np) {
+  const int nt = (int)tiles.size();
+  const int ncons = NWARP - WS_PRODUCERS;  // the last WS_PRODUCERS warps load
+  const int nslices = (nt + ncons - 1) / ncons;
+  if (nt > MAX_OUT_TILES || nslices > MAX_SLICES) return fail(c, PSVD_EINVAL, "panel too wide (%d tiles)", nt);
+  memset(ps.p.plan, 0, sizeof(ps.p.plan));
+  memset(&ps.map, 0, sizeof(ps.map));
+  ps.p.nslices = nslices;
+  ps.map.nout = nt;
+  auto cost = [&](int I, int J) {
+    const int na = std::min(4, (np - I * 32 + 7) / 8), nb = std::min(4, (np - J * 32 + 7) / 8);
+    if (I != J) return na * nb;
+    int k = 0;
+    for (int a = 0; a < na; ++a) k += std::max(0, nb - a);
+    return k;
+  };
+  std::vector<int> order(nt);
+  for (int i = 0; i < nt; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+    return cost(tiles[x].first, tiles[x].second) > cost(tiles[y].first, tiles[y].second);
+  });
+  // bins: (slice, smsp); slots of smsp q in a slice: warps q, q+4, q+8, q+12 below ncons
+  std::vector<int> load(nslices * 4, 0), used(nslices * 4, 0), slice_load(nslices, 0);
+  auto slots_of = [&](int q) { int k = 0; for (int w = q; w < ncons; w += 4) ++k; return k; };
+  for (int o : order) {
+    const int cst = cost(tiles[o].first, tiles[o].second);
+    int best = -1;
+    for (int b = 0; b < nslices * 4; ++b) {
+      if (used[b] >= slots_of(b % 4)) continue;
+      if (best < 0 || load[b] < load[best] || (load[b] == load[best] && slice_load[b / 4] < slice_load[best / 4]))
+        best = b;
+    }
+    if (best < 0) return fail(c, PSVD_EINVAL, "tile balancing failed");
+    const int sl = best / 4, q = best % 4;
+    const int w = q + 4 * used[best];
+    used[best]++;
+    load[best] += cst;
+    slice_load[sl] += cst;
+    WarpPlan& wp = ps.p.plan[sl][w];
+    wp.ksplit = 1;
+    wp.kpart = 0;
+    wp.ti[0] = (signed char)tiles[o].first;
+    wp.tj[0] = (signed char)tiles[o].second;
+    wp.ntile = 1;
+    ps.map.src[o][ps.map.nsrc[o]++] = (unsigned char)(sl * SLOTS + w * TPW);
+  }
+  for (int o = 0; o < nt; ++o) ps.map.out_id[o] = (short)(tiles[o].first * ps.NB + tiles[o].second);
+  return PSVD_OK;
+}
+
 // Common pass setup.  segs: panel segments; w/W: optional Y = P[:, wlo:wlo+wk] * W.
 int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, int wlo, int wk, int w,
               const double* W, int64_t ldw, bool gram_pp, bool gram_yy, bool gram_py, int py_cols = -1,
@@ -214,7 +268,11 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
   // Gram-only passes with enough tiles run warp-specialized (one producer warp, no k-split)
   ps.ws = (w == 0 && (int)tiles.size() >= 8 &&
            gram_ws_smem_bytes(np_pad, 3) <= (size_t)SMEM_LIMIT);
-  int rc = ps.ws ? plan_tiles(c, ps, tiles, false, NWARP - 1) : plan_tiles(c, ps, tiles, w == 0);
+  int rc = ps.ws ? plan_tiles_balanced(c, ps, tiles, np) : plan_tiles(c, ps, tiles, w == 0);
+  {
+    static const char* dbg = getenv("PSVD_GRAM_DBG");
+    p.dbg = dbg ? atoi(dbg) : 0;
+  }
   if (rc) return rc;
   // grid: one CTA per SM (1 CTA/SM by smem), chunks of 32-row multiples
   const int64_t stages32 = (M + 31) / 32;

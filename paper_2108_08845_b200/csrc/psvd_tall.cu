@@ -1,4 +1,6 @@
 // Tall-panel pass kernels (see psvd_tall.cuh for the contract).
+#include <type_traits>
+
 #include "psvd_tall.cuh"
 
 namespace psvd {
@@ -290,7 +292,7 @@ __global__ void __launch_bounds__(NTHR, 1) gram_ws_kernel(const TallParams p) {
   uint64_t* empty = full + NS;
   off += (2 * NS * sizeof(uint64_t) + 15) / 16 * 16;
   double* sP = reinterpret_cast<double*>(smem_raw + off);
-  constexpr int PROD = NWARP - 1;
+  constexpr int PROD = NWARP - WS_PRODUCERS;  // first producer warp
   int ncons = 0;  // consumer warps of this slice (all arrive on `empty`)
   for (int w = 0; w < PROD; ++w) ncons += p.plan[slice][w].ntile > 0;
   for (int c = tid; c < np_pad; c += NTHR) {
@@ -309,28 +311,30 @@ __global__ void __launch_bounds__(NTHR, 1) gram_ws_kernel(const TallParams p) {
   }
   if (tid == 0) {
     for (int b = 0; b < NS; ++b) {
-      mbar_init(&full[b], 32);
+      mbar_init(&full[b], 32 * WS_PRODUCERS);
       mbar_init(&empty[b], (unsigned)max(ncons, 1));
     }
   }
   __syncthreads();
   const int64_t nstage = row_end > row_begin ? (row_end - row_begin + KS - 1) / KS : 0;
 
-  if (warp == PROD) {
-    const int nchunk16 = p.np * (KS / 2);
+  if (warp >= PROD) {
+    // producer lanes: fixed 16-byte row piece pc, columns c = cstream + k * cstride
+    const int pl = (warp - PROD) * 32 + lane;
+    const int pc = pl & 15, cstream = pl >> 4, cstride = (32 * WS_PRODUCERS) >> 4;
     for (int64_t s = 0; s < nstage; ++s) {
       const int b = (int)(s % NS);
       if (s >= NS) mbar_wait(&empty[b], (unsigned)(((s / NS) - 1) & 1));
-      const int64_t r0 = row_begin + s * KS;
-      double* dst_base = sP + (size_t)b * np_pad * KSP;
-      for (int q = lane; q < nchunk16; q += 32) {
-        const int c = q >> 4, pc = q & 15;
-        const int64_t r = r0 + 2 * pc;
-        const int64_t valid = row_end - r;
-        const int bytes = valid >= 2 ? 16 : (valid == 1 ? 8 : 0);
-        const double* cp = colptr[c];
-        if (cp == nullptr) continue;
-        cp_async16(dst_base + (size_t)c * KSP + 2 * pc, cp + (bytes > 0 ? r : row_begin), bytes);
+      const int64_t r = row_begin + s * KS + 2 * pc;
+      const int64_t valid = row_end - r;
+      const int bytes = valid >= 2 ? 16 : (valid == 1 ? 8 : 0);
+      const int64_t roff = bytes > 0 ? r : row_begin;
+      double* dst = sP + (size_t)b * np_pad * KSP + 2 * pc;
+      if (!(p.dbg & 2)) {
+        for (int c = cstream; c < p.np; c += cstride) {
+          const double* cp = colptr[c];
+          if (cp != nullptr) cp_async16(dst + (size_t)c * KSP, cp + roff, bytes);
+        }
       }
       cp_async_mbar_arrive(&full[b]);
     }
@@ -346,27 +350,56 @@ __global__ void __launch_bounds__(NTHR, 1) gram_ws_kernel(const TallParams p) {
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   const int I = wp.ti[0], J = wp.tj[0];
-  for (int64_t s = 0; s < nstage; ++s) {
-    const int b = (int)(s % NS);
-    mbar_wait(&full[b], (unsigned)((s / NS) & 1));
-    const double* P = sP + (size_t)b * np_pad * KSP;
-    const double* bI = P + (size_t)I * 32 * KSP + g * KSP + tq;
-    const double* bJ = P + (size_t)J * 32 * KSP + g * KSP + tq;
+  // Which 8x8 blocks this warp's tile needs: diagonal tiles only b >= a (extraction reads
+  // row <= col), blocks past the last panel column are skipped.  The shape is fixed for
+  // the whole kernel, so each warp runs one specialized stage loop (no per-step branches).
+  const int nva = min(4, (p.np - I * 32 + 7) / 8), nvb = min(4, (p.np - J * 32 + 7) / 8);
+  // Tile shape, compile-time in the stage loop (a DMMA under a runtime predicate costs a
+  // warp reconvergence each; such warps would pace the whole CTA through the ring):
+  //   DIAG: block (a, c) needed iff c >= a (extraction reads row <= col);
+  //   NA x NB: valid 8-row / 8-column blocks (last panel block partially filled).
+  auto stage_loop = [&](auto na_t, auto nb_t, auto diag_t) {
+    constexpr int NA = decltype(na_t)::value, NB = decltype(nb_t)::value;
+    constexpr bool DIAG = decltype(diag_t)::value;
+    for (int64_t s = 0; s < nstage; ++s) {
+      const int b = (int)(s % NS);
+      mbar_wait(&full[b], (unsigned)((s / NS) & 1));
+      const double* P = sP + (size_t)b * np_pad * KSP;
+      const double* bI = P + (size_t)I * 32 * KSP + g * KSP + tq;
+      const double* bJ = P + (size_t)J * 32 * KSP + g * KSP + tq;
 #pragma unroll
-    for (int kk = 0; kk < KS / 4; ++kk) {
-      double fa[4], fb[4];
+      for (int kk = 0; kk < KS / 4; ++kk) {
+        double fa[NA], fb[NB];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        fa[q] = bI[(size_t)q * 8 * KSP + kk * 4];
-        fb[q] = bJ[(size_t)q * 8 * KSP + kk * 4];
+        for (int q = 0; q < NA; ++q) fa[q] = bI[(size_t)q * 8 * KSP + kk * 4];
+#pragma unroll
+        for (int q = 0; q < NB; ++q) fb[q] = bJ[(size_t)q * 8 * KSP + kk * 4];
+#pragma unroll
+        for (int a = 0; a < NA; ++a)
+#pragma unroll
+          for (int c = 0; c < NB; ++c)
+            if (!DIAG || c >= a) {
+              if (!(p.dbg & 1)) dmma884(acc[a][c][0], acc[a][c][1], fa[a], fb[c]);
+            }
       }
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) dmma884(acc[a][c][0], acc[a][c][1], fa[a], fb[c]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[b]);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[b]);
+  };
+  using F = std::false_type;
+  using T = std::true_type;
+  auto C = [](auto v) { return std::integral_constant<int, decltype(v)::value>{}; };
+  (void)C;
+  if (I != J) {
+    if (nva == 4 && nvb == 4) stage_loop(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{}, F{});
+    else if (nvb == 3) stage_loop(std::integral_constant<int, 4>{}, std::integral_constant<int, 3>{}, F{});
+    else if (nvb == 2) stage_loop(std::integral_constant<int, 4>{}, std::integral_constant<int, 2>{}, F{});
+    else stage_loop(std::integral_constant<int, 4>{}, std::integral_constant<int, 1>{}, F{});
+  } else {
+    if (nva == 4) stage_loop(std::integral_constant<int, 4>{}, std::integral_constant<int, 4>{}, T{});
+    else if (nva == 3) stage_loop(std::integral_constant<int, 3>{}, std::integral_constant<int, 3>{}, T{});
+    else if (nva == 2) stage_loop(std::integral_constant<int, 2>{}, std::integral_constant<int, 2>{}, T{});
+    else stage_loop(std::integral_constant<int, 1>{}, std::integral_constant<int, 1>{}, T{});
   }
   double* dst = p.partial + ((size_t)blockIdx.x * SLOTS + warp * TPW) * 1024;
 #pragma unroll

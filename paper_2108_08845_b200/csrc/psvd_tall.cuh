@@ -26,6 +26,7 @@ namespace psvd {
 constexpr int NWARP = 16;  // 4 warps per SMSP keep the DMMA pipe fed through LDS/barrier latency
 constexpr int NTHR = NWARP * 32;
 constexpr int TPW = 1;     // Gram tiles per warp (64 accumulator doubles -> <= 128 registers)
+constexpr int WS_PRODUCERS = 2;  // cp.async producer warps of the warp-specialized Gram
 constexpr int MAX_SEG = 4;
 constexpr int SLOTS = NWARP * TPW;  // partial tile slots per CTA
 constexpr int MAX_SLICES = 4;
@@ -50,6 +51,7 @@ struct TallParams {
   int ks;                // rows per stage (32 or 16)
   int nstage;            // cp.async pipeline depth (2 or 3)
   int narrow;            // every Gram tile's column block is a Y block of <= 16 columns (NJB = 2)
+  int dbg;               // diagnostics (PSVD_GRAM_DBG): 1 = skip DMMA, 2 = skip global loads
   int nseg;
   Seg seg[MAX_SEG];
   int np, np_pad;        // panel columns; padded to a multiple of 32 (start of the Y block)
