@@ -41,7 +41,7 @@ struct psvd_ctx {
   Buf partial2, tiles2[2];  // A^T A passes on the low-priority stream (double-buffered tiles)
   cudaStream_t s_hi = nullptr, s_lo = nullptr;  // pipelined stream_run: critical chain / look-ahead Grams
   cudaStream_t s_aux = nullptr;                  // concurrent LDL^T of the split core solve
-  cudaEvent_t ev_ldlt_fork = nullptr, ev_ldlt_join = nullptr;
+  cudaEvent_t ev_ldlt_fork = nullptr, ev_ldlt_join = nullptr, ev_eig_start = nullptr;
   cudaEvent_t ev_aa[2] = {nullptr, nullptr}, ev_asm[2] = {nullptr, nullptr}, ev_fork = nullptr, ev_join = nullptr;
 };
 
@@ -407,6 +407,7 @@ int psvd_create(int device, psvd_ctx** out) {
     cudaStreamCreateWithPriority(&c->s_aux, cudaStreamNonBlocking, hi);
     cudaEventCreateWithFlags(&c->ev_ldlt_fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_ldlt_join, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_eig_start, cudaEventDisableTiming);
     for (int i = 0; i < 2; ++i) {
       cudaEventCreateWithFlags(&c->ev_aa[i], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&c->ev_asm[i], cudaEventDisableTiming);
@@ -432,6 +433,7 @@ int psvd_destroy(psvd_ctx* c) {
   if (c->s_aux) cudaStreamDestroy(c->s_aux);
   if (c->ev_ldlt_fork) cudaEventDestroy(c->ev_ldlt_fork);
   if (c->ev_ldlt_join) cudaEventDestroy(c->ev_ldlt_join);
+  if (c->ev_eig_start) cudaEventDestroy(c->ev_eig_start);
   for (int i = 0; i < 2; ++i) {
     if (c->ev_aa[i]) cudaEventDestroy(c->ev_aa[i]);
     if (c->ev_asm[i]) cudaEventDestroy(c->ev_asm[i]);
@@ -777,6 +779,9 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
   const int nsub = (int)std::max<int64_t>(1, std::min<int64_t>(4, M / 65536));
   auto aa_pass = [&](int j) -> int {
     if (j >= 2) cudaStreamWaitEvent(lo, c->ev_asm[j & 1], 0);  // tiles2[j&1] consumed by batch j-2's assembly
+    // start A^T A of batch j with the core solve of batch j-1: it then overlaps that one-SM
+    // solve (the longer of the two) instead of competing with the recompose pass for SMs
+    if (j >= 1) cudaStreamWaitEvent(lo, c->ev_eig_start, 0);
     const int64_t rows_sub = (M + nsub - 1) / nsub / 32 * 32 + 32;
     Pass first;
     size_t part_off = 0;
@@ -827,10 +832,11 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
     if ((rc = run_pass(c, pu, hi))) return rc;
   }
   for (int b = 0; b < nb; ++b) {
-    if (b + 1 < nb && (rc = aa_pass(b + 1))) return rc;
     const int kc = (b == 0) ? Kc : K;
     const int n = kc + B[b];
     cudaStreamWaitEvent(hi, c->ev_aa[b & 1], 0);
+    cudaEventRecord(c->ev_eig_start, hi);
+    if (b + 1 < nb && (rc = aa_pass(b + 1))) return rc;
     mark("hi:eig_begin", b, hi);
     if ((rc = make_dvec(c, sprev, ff, kc, n, hi))) return rc;
     if (b == 0) {
