@@ -101,6 +101,9 @@ struct Pass {
   int grid = 0;
   int NB = 0;
   bool ws = false;      // warp-specialized Gram kernel
+  bool tma = false;     // warp-specialized TMA pass (narrow panels)
+  TmaMaps maps;
+  TmaExtra x;
   Buf* part = nullptr;  // partial-tile workspace of the stream this pass runs on
   Buf* tl = nullptr;    // reduced tiles
 };
@@ -216,6 +219,30 @@ static int plan_tiles_balanced(psvd_ctx* c, Pass& ps, const std::vector<std::pai
   return PSVD_OK;
 }
 
+// TMA pass: tiles on the Gram warps TMA_GRAM_WARP0.., one tile each, no k-split.
+static int plan_tiles_tma(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& tiles) {
+  const int nt = (int)tiles.size();
+  memset(ps.p.plan, 0, sizeof(ps.p.plan));
+  memset(&ps.map, 0, sizeof(ps.map));
+  const int nslices = std::max(1, (nt + TMA_GRAM_WARPS - 1) / TMA_GRAM_WARPS);
+  if (nt > MAX_OUT_TILES || nslices > MAX_SLICES) return fail(c, PSVD_EINVAL, "panel too wide (%d tiles)", nt);
+  ps.p.nslices = nslices;
+  ps.map.nout = nt;
+  const int per = (nt + nslices - 1) / nslices;
+  for (int o = 0; o < nt; ++o) {
+    const int sl = o / per, w = TMA_GRAM_WARP0 + o % per;
+    WarpPlan& wp = ps.p.plan[sl][w];
+    wp.ksplit = 1;
+    wp.kpart = 0;
+    wp.ti[0] = (signed char)tiles[o].first;
+    wp.tj[0] = (signed char)tiles[o].second;
+    wp.ntile = 1;
+    ps.map.src[o][ps.map.nsrc[o]++] = (unsigned char)(sl * SLOTS + w * TPW);
+    ps.map.out_id[o] = (short)(tiles[o].first * ps.NB + tiles[o].second);
+  }
+  return PSVD_OK;
+}
+
 // Common pass setup.  segs: panel segments; w/W: optional Y = P[:, wlo:wlo+wk] * W.
 int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, int wlo, int wk, int w,
               const double* W, int64_t ldw, bool gram_pp, bool gram_yy, bool gram_py, int py_cols = -1,
@@ -226,12 +253,38 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
   TallParams& p = ps.p;
   p.M = M;
   p.nseg = (int)segs.size();
-  int np = 0;
-  for (size_t i = 0; i < segs.size(); ++i) {
-    p.seg[i] = segs[i];
-    if (segs[i].col0 == 1) np = rup(np, 32);  // request: start this segment on a 32-column block
-    p.seg[i].col0 = np;
-    np += segs[i].ncols;
+  // Narrow passes (Y of <= 16 columns, Gram tiles only against Y) run on the TMA kernel,
+  // whose segments start on 8-column boundaries; P-tiles at explicit blocks (py_lo >= 0)
+  // need that layout to coincide with the contiguous one.
+  static const bool no_tma = getenv("PSVD_NO_TMA") != nullptr;
+  bool tma = !no_tma && w > 0 && w <= 16 && !gram_pp && tma_available();
+  auto layout = [&](int align) {
+    int n_ = 0;
+    for (size_t i = 0; i < segs.size(); ++i) {
+      p.seg[i] = segs[i];
+      n_ = (segs[i].col0 == 1) ? rup(n_, 32) : rup(n_, align);  // col0 == 1: start on a 32-column block
+      p.seg[i].col0 = n_;
+      n_ += segs[i].ncols;
+    }
+    return n_;
+  };
+  int np = layout(1);
+  if (tma) {
+    std::vector<int> c1(segs.size());
+    for (size_t i = 0; i < segs.size(); ++i) c1[i] = p.seg[i].col0;
+    const int np8 = layout(8);
+    bool same = true;
+    for (size_t i = 0; i < segs.size(); ++i) same = same && c1[i] == p.seg[i].col0;
+    for (size_t i = 0; i < segs.size(); ++i)
+      tma = tma && aligned16(segs[i].ptr) && segs[i].ld % 2 == 0 && segs[i].ncols > 0;
+    if (gram_py && py_lo >= 0 && !same) tma = false;
+    if (tma && tma_pass_smem_bytes(rup(np8, 32), rup(wk, 8) + 8 * (int)segs.size()) > (size_t)SMEM_LIMIT) tma = false;
+    np = tma ? np8 : layout(1);
+  }
+  if (py_lo < 0) {  // P-tiles over the last segment (its own 32-column block)
+    const Seg& l = p.seg[segs.size() - 1];
+    py_lo = l.col0 / 32;
+    py_cols = l.col0 + l.ncols;
   }
   p.np = np;
   int np_pad = rup(std::max(np, 1), 32);
@@ -244,13 +297,15 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
   p.w = w;
   p.w_pad = w > 0 ? rup(w, 8) : 0;
   if (w > MAX_W) return fail(c, PSVD_EINVAL, "Y width %d exceeds %d", w, MAX_W);
-  // stage height: 32 rows unless the smem budget forces 16
+  // stage height: 32 rows unless the smem budget forces 16 (the TMA pass has its own 16-row ring)
   p.ks = 32;
   p.nstage = 3;
-  if (tall_smem_bytes(32, np_pad, wk, w, 3) > (size_t)SMEM_LIMIT) p.nstage = 2;
-  if (tall_smem_bytes(32, np_pad, wk, w, 2) > (size_t)SMEM_LIMIT) p.ks = 16;
-  if (tall_smem_bytes(p.ks, np_pad, wk, w, p.nstage) > (size_t)SMEM_LIMIT)
-    return fail(c, PSVD_EINVAL, "panel of %d columns (+%d) does not fit shared memory", np, w);
+  if (!tma) {
+    if (tall_smem_bytes(32, np_pad, wk, w, 3) > (size_t)SMEM_LIMIT) p.nstage = 2;
+    if (tall_smem_bytes(32, np_pad, wk, w, 2) > (size_t)SMEM_LIMIT) p.ks = 16;
+    if (tall_smem_bytes(p.ks, np_pad, wk, w, p.nstage) > (size_t)SMEM_LIMIT)
+      return fail(c, PSVD_EINVAL, "panel of %d columns (+%d) does not fit shared memory", np, w);
+  }
   const int NBp = np_pad / 32, NBy = w > 0 ? rup(w, 32) / 32 : 0;
   ps.NB = NBp + NBy;
   std::vector<std::pair<int, int>> tiles;
@@ -268,7 +323,10 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
   // Gram-only passes with enough tiles run warp-specialized (one producer warp, no k-split)
   ps.ws = (w == 0 && (int)tiles.size() >= 8 &&
            gram_ws_smem_bytes(np_pad, 3) <= (size_t)SMEM_LIMIT);
-  int rc = ps.ws ? plan_tiles_balanced(c, ps, tiles, np) : plan_tiles(c, ps, tiles, w == 0);
+  ps.tma = tma;
+  if (tma) p.narrow = 1;
+  int rc = tma ? plan_tiles_tma(c, ps, tiles)
+               : ps.ws ? plan_tiles_balanced(c, ps, tiles, np) : plan_tiles(c, ps, tiles, w == 0);
   {
     static const char* dbg = getenv("PSVD_GRAM_DBG");
     p.dbg = dbg ? atoi(dbg) : 0;
@@ -291,11 +349,14 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
     if (rc2) return rc2;
     p.partial = (double*)ps.part->ptr;
   }
+  if (tma && tma_pass_prepare(p, ps.maps, ps.x) != 0) return fail(c, PSVD_ECUDA, "TMA descriptor setup failed");
   return PSVD_OK;
 }
 
 int run_pass(psvd_ctx* c, Pass& ps, cudaStream_t st) {
-  if (ps.ws)
+  if (ps.tma)
+    launch_pass_tma(ps.p, ps.maps, ps.x, ps.grid, st);
+  else if (ps.ws)
     launch_gram_ws(ps.p, ps.grid, st);
   else
     launch_tall(ps.p, ps.grid, st);
@@ -861,13 +922,31 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
       segs.push_back(Seg{A[b + 1], lda[b + 1], B[b + 1], 1});
       Pass pf;
       const int wk = kc + B[b];
-      const int a0 = rup(wk, 32) / 32;
-      if ((rc = plan_pass(c, pf, M, segs, 0, wk, K, W, wk, false, true, true, a0 * 32 + B[b + 1], -1, nullptr, nullptr,
-                          0, a0)))
+      if ((rc = plan_pass(c, pf, M, segs, 0, wk, K, W, wk, false, true, true, -1, -1, nullptr, nullptr, 0, -1)))
         return rc;
+      const int a0 = pf.p.seg[pf.p.nseg - 1].col0 / 32;
       pf.p.Yout = Uout;
       pf.p.ldy = ldo;
       if ((rc = run_pass(c, pf, hi))) return rc;
+      if (getenv("PSVD_DUMP_FUSED")) {  // diagnostics: tiles + Y of the fused pass
+        cudaStreamSynchronize(hi);
+        std::vector<double> h((size_t)pf.NB * pf.NB * 1024), y((size_t)M * K);
+        cudaMemcpy(h.data(), c->tiles.ptr, h.size() * 8, cudaMemcpyDeviceToHost);
+        cudaMemcpy2D(y.data(), M * 8, Uout, ldo * 8, M * 8, K, cudaMemcpyDeviceToHost);
+        char fn[256];
+        snprintf(fn, sizeof(fn), "%s_%d.bin", getenv("PSVD_DUMP_FUSED"), b);
+        FILE* f = fopen(fn, "wb");
+        int hdr[4] = {pf.NB, a0, pf.p.np_pad / 32, (int)M};
+        fwrite(hdr, 4, 4, f);
+        fwrite(h.data(), 8, h.size(), f);
+        fwrite(y.data(), 8, y.size(), f);
+        std::vector<double> u((size_t)M * K, 0.0), wv((size_t)wk * K);
+        if (kc > 0) cudaMemcpy2D(u.data(), M * 8, Uprev, ldprev * 8, M * 8, K, cudaMemcpyDeviceToHost);
+        cudaMemcpy(wv.data(), W, wv.size() * 8, cudaMemcpyDeviceToHost);
+        fwrite(u.data(), 8, u.size(), f);
+        fwrite(wv.data(), 8, wv.size(), f);
+        fclose(f);
+      }
       launch_extract_sym((const double*)c->tiles.ptr, pf.NB, pf.p.np_pad, K, nullptr, UtU, hi);
       c->launches++;
       nbua = pf.NB;

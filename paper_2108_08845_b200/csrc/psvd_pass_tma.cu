@@ -1,0 +1,377 @@
+// Warp-specialized TMA pass for narrow panels (see psvd_tall.cuh, "narrow").
+//
+// One CTA per SM streams its row chunk of the panel P = [seg_0 | seg_1 | ...] in
+// 16-row stages.  Each stage is one 2-D TMA box per segment (16 rows x <= 256
+// columns, 128-byte swizzle: column c of a stage is 128 contiguous bytes whose
+// 16-byte chunks are XOR-ed with c & 7), landing in an NS-deep ring signalled by
+// mbarriers (complete_tx).  Warp roles:
+//
+//   warp 15      producer: one lane issues the stage's TMA boxes once the ring
+//                slot is released;
+//   warps 0..3   Y = P[:, W rows] * W on DMMA, one 8x8 output block each
+//                (row block rb, column block cb), two accumulator chains; Y goes
+//                to a double-buffered swizzled smem tile, to global (slice 0) and
+//                into the per-column argmax of |y|;
+//   warps 4..14  Gram tiles (I, Y) of [P | Y]: A^T Y and Y^T Y, one 32x16 tile each,
+//                compile-time block shape (no per-DMMA predicates).
+//
+// No CTA-wide barrier inside the stage loop: full / empty (panel ring), ydone /
+// yfree (Y double buffer) mbarriers only.  Results are bitwise identical run to
+// run (fixed per-warp accumulation order, fixed-order tall_reduce afterwards).
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstring>
+#include <type_traits>
+
+#include "psvd_tall.cuh"
+
+namespace psvd {
+
+namespace {
+
+constexpr int TKS = 16;       // rows per stage = one 128-byte swizzled column
+constexpr int TNS = 3;        // ring depth
+constexpr int YWARPS = 4;     // Y warps (rb, cb) in {0,1}^2
+constexpr int PROD_WARP = NWARP - 1;
+constexpr int WSP = 20;       // sW row stride (doubles): 2 wavefronts per B-fragment load
+
+PSVD_DEV uint32_t saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+PSVD_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(saddr(bar)), "r"(bytes) : "memory");
+}
+
+PSVD_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+          "r"(saddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(saddr(bar))
+      : "memory");
+}
+
+// element (column c, stage row k) of a 128B-swizzled 16-row stage, in doubles
+PSVD_DEV int swz(int c, int k) { return c * 16 + ((((k >> 1) ^ (c & 7)) << 1) | (k & 1)); }
+
+}  // namespace
+
+size_t tma_pass_smem_bytes(int np_pad, int kp_span) {
+  size_t b = 1024;  // alignment slack for the 1024-byte swizzle atoms
+  b += sizeof(double) * (size_t)TNS * np_pad * TKS;  // panel ring
+  b += sizeof(double) * 2 * 16 * TKS;                // Y double buffer (<= 16 columns)
+  b += sizeof(double) * (size_t)kp_span * WSP;       // W
+  b += 64 * sizeof(uint64_t);                        // barriers
+  b += sizeof(double) * 2 * 16 * 3;                  // argmax scratch
+  return b;
+}
+
+__global__ void __launch_bounds__(NTHR, 1)
+    pass_tma_kernel(const __grid_constant__ TallParams p, const __grid_constant__ TmaMaps maps, const TmaExtra x) {
+  if (p.gate != nullptr && *p.gate == 0) return;  // gated pass (drift rescue) not needed
+  extern __shared__ unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int slice = blockIdx.x % p.nslices;
+  const int64_t chunk = blockIdx.x / p.nslices;
+  const int64_t row_begin = chunk * p.rows_per_cta;
+  const int64_t row_end = min(p.M, row_begin + p.rows_per_cta);
+  const int np_pad = p.np_pad;
+  const int kspan = x.kp_hi - x.kp_lo;
+  const int ncb = p.w_pad >> 3;  // Y column blocks (1 or 2)
+
+  unsigned char* base = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
+  double* sP = reinterpret_cast<double*>(base);
+  double* sY = sP + (size_t)TNS * np_pad * TKS;
+  double* sW = sY + 2 * 16 * TKS;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sW + (size_t)kspan * WSP);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + TNS;
+  uint64_t* ydone = bars + 2 * TNS;
+  uint64_t* yfree = ydone + 2;
+  double* cmx = reinterpret_cast<double*>(bars + 64);  // [2 rb][16 cols][val, abs, row]
+
+  int ngram = 0;
+  for (int w = YWARPS; w < PROD_WARP; ++w) ngram += p.plan[slice][w].ntile > 0;
+  const int ny = 2 * ncb;
+
+  // one-time setup: zero the panel columns no TMA box writes (alignment gaps), the Y
+  // buffers (columns >= w stay zero), stage W with zero rows for gap columns
+  for (int i = tid; i < TNS * np_pad; i += NTHR) {
+    const int c = i % np_pad;
+    if (!x.written[c >> 3]) {
+      double* col = sP + (size_t)i * TKS;
+#pragma unroll
+      for (int k = 0; k < TKS; ++k) col[k] = 0.0;
+    }
+  }
+  for (int i = tid; i < 2 * 16 * TKS; i += NTHR) sY[i] = 0.0;
+  for (int i = tid; i < kspan * WSP; i += NTHR) {
+    const int kk = i / WSP, o = i % WSP;
+    const int pc = x.kp_lo + kk;  // physical panel column
+    double v = 0.0;
+    if (o < p.w) {
+      for (int s = 0; s < p.nseg; ++s) {
+        const int c0 = p.seg[s].col0;
+        if (x.wrow0[s] != TMA_NOT_IN_W && pc >= c0 && pc < c0 + p.seg[s].ncols) {
+          const int wr = x.wrow0[s] + (pc - c0);
+          if (wr >= 0 && wr < p.wk) v = p.W[(int64_t)o * p.ldw + wr];
+        }
+      }
+    }
+    sW[i] = v;
+  }
+  if (tid == 0) {
+    for (int b = 0; b < TNS; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], (unsigned)(ny + ngram));
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&ydone[b], 32u * ny);
+      mbar_init(&yfree[b], (unsigned)max(32 * ngram, 1));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // zero fills before the first TMA writes
+  __syncthreads();
+  const int64_t nstage = row_end > row_begin ? (row_end - row_begin + TKS - 1) / TKS : 0;
+
+  if (warp == PROD_WARP) {
+    if (lane == 0) {
+      for (int64_t s = 0; s < nstage; ++s) {
+        const int b = (int)(s % TNS);
+        if (s >= TNS) mbar_wait(&empty[b], (unsigned)(((s / TNS) - 1) & 1));
+        mbar_expect_tx(&full[b], x.stage_bytes);
+        double* dst = sP + (size_t)b * np_pad * TKS;
+        const int r0 = (int)(row_begin + s * TKS);
+        for (int o = 0; o < x.nops; ++o)
+          tma_load_2d(dst + (size_t)x.op_pcol[o] * TKS, &maps.m[x.op_seg[o]], r0, x.op_col[o], &full[b]);
+      }
+    }
+    return;
+  }
+
+  if (warp < YWARPS) {
+    // ---------------------------------------------------------------- Y warps
+    const int rb = warp & 1, cb = warp >> 1;
+    if (cb >= ncb) return;
+    double cm_val[2] = {0.0, 0.0}, cm_abs[2] = {-1.0, -1.0};
+    int64_t cm_row[2] = {-1, -1};
+    const bool do_y = slice == 0;
+    for (int64_t s = 0; s < nstage; ++s) {
+      const int b = (int)(s % TNS), yb = (int)(s & 1);
+      mbar_wait(&full[b], (unsigned)((s / TNS) & 1));
+      const double* P = sP + (size_t)b * np_pad * TKS;
+      double ya0 = 0.0, ya1 = 0.0, yb0 = 0.0, yb1 = 0.0;
+      const int kr = rb * 8 + g;
+      const double* wb = sW + (size_t)tq * WSP + cb * 8 + g;
+      int k0 = x.kp_lo;
+      for (; k0 + 8 <= x.kp_hi; k0 += 8) {
+        const double a0 = P[swz(k0 + tq, kr)], a1 = P[swz(k0 + 4 + tq, kr)];
+        const double b0 = wb[(size_t)(k0 - x.kp_lo) * WSP], b1 = wb[(size_t)(k0 + 4 - x.kp_lo) * WSP];
+        dmma884(ya0, ya1, a0, b0);
+        dmma884(yb0, yb1, a1, b1);
+      }
+      if (k0 < x.kp_hi) {  // kp span is a multiple of 4
+        dmma884(ya0, ya1, P[swz(k0 + tq, kr)], wb[(size_t)(k0 - x.kp_lo) * WSP]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[b]);  // panel slot no longer read by this warp
+      const double y0 = ya0 + yb0, y1 = ya1 + yb1;
+      if (s >= 2 && ngram > 0) mbar_wait(&yfree[yb], (unsigned)(((s >> 1) - 1) & 1));
+      double* Ys = sY + (size_t)yb * 16 * TKS;
+      const int o0 = cb * 8 + 2 * tq;
+      Ys[swz(o0, kr)] = y0;
+      Ys[swz(o0 + 1, kr)] = y1;
+      mbar_arrive(&ydone[yb]);
+      const int64_t r = row_begin + s * TKS + kr;
+      if (do_y && r < row_end) {
+        if (p.Yout != nullptr) {
+          if (o0 < p.w) p.Yout[(int64_t)o0 * p.ldy + r] = y0;
+          if (o0 + 1 < p.w) p.Yout[(int64_t)(o0 + 1) * p.ldy + r] = y1;
+        }
+        if (p.colmax != nullptr) {
+          if (fabs(y0) > cm_abs[0]) { cm_abs[0] = fabs(y0); cm_val[0] = y0; cm_row[0] = r; }
+          if (fabs(y1) > cm_abs[1]) { cm_abs[1] = fabs(y1); cm_val[1] = y1; cm_row[1] = r; }
+        }
+      }
+    }
+    if (do_y && p.colmax != nullptr) {
+      // combine over g (lanes 4 apart), ties to the smaller row (first occurrence)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+#pragma unroll
+        for (int off = 4; off < 32; off <<= 1) {
+          const double oa = __shfl_xor_sync(0xffffffffu, cm_abs[e], off);
+          const double ov = __shfl_xor_sync(0xffffffffu, cm_val[e], off);
+          const long long orow = __shfl_xor_sync(0xffffffffu, (long long)cm_row[e], off);
+          if (oa > cm_abs[e] || (oa == cm_abs[e] && orow >= 0 && (cm_row[e] < 0 || orow < cm_row[e]))) {
+            cm_abs[e] = oa; cm_val[e] = ov; cm_row[e] = orow;
+          }
+        }
+      }
+      if (g == 0) {
+        for (int e = 0; e < 2; ++e) {
+          double* d = cmx + ((size_t)rb * 16 + cb * 8 + 2 * tq + e) * 3;
+          d[0] = cm_val[e]; d[1] = cm_abs[e]; d[2] = (double)cm_row[e];
+        }
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"r"(32 * ny) : "memory");
+      if (rb == 0 && g == 0) {
+        for (int e = 0; e < 2; ++e) {
+          const int o = cb * 8 + 2 * tq + e;
+          if (o >= p.w) continue;
+          const double* d0 = cmx + (size_t)o * 3;
+          const double* d1 = cmx + ((size_t)16 + o) * 3;
+          const bool take1 = d1[1] > d0[1] || (d1[1] == d0[1] && d1[2] >= 0 && (d0[2] < 0 || d1[2] < d0[2]));
+          const double* d = take1 ? d1 : d0;
+          double* dst = p.colmax + ((size_t)chunk * p.w + o) * 2;
+          dst[0] = d[0];
+          dst[1] = d[2] + (double)p.row_offset;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------------- Gram warps
+  const WarpPlan wp = p.plan[slice][warp];
+  if (wp.ntile == 0) return;
+  const int I = wp.ti[0], J = wp.tj[0];
+  const bool i_is_y = I * 32 >= np_pad;
+  const int na = i_is_y ? ncb : min(4, (p.np - I * 32 + 7) / 8);
+  double acc[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+  (void)J;
+  auto stage_loop = [&](auto na_t, auto nb_t) {
+    constexpr int NA = decltype(na_t)::value, NB = decltype(nb_t)::value;
+    for (int64_t s = 0; s < nstage; ++s) {
+      const int b = (int)(s % TNS), yb = (int)(s & 1);
+      mbar_wait(&full[b], (unsigned)((s / TNS) & 1));
+      mbar_wait(&ydone[yb], (unsigned)((s >> 1) & 1));
+      const double* Ys = sY + (size_t)yb * 16 * TKS;
+      const double* Abase = i_is_y ? Ys : sP + (size_t)b * np_pad * TKS + (size_t)I * 32 * TKS;
+#pragma unroll
+      for (int kk = 0; kk < TKS / 4; ++kk) {
+        const int k = kk * 4 + tq;
+        double fa[NA], fb[NB];
+#pragma unroll
+        for (int q = 0; q < NA; ++q) fa[q] = Abase[swz(q * 8 + g, k)];
+#pragma unroll
+        for (int q = 0; q < NB; ++q) fb[q] = Ys[swz(q * 8 + g, k)];
+#pragma unroll
+        for (int a = 0; a < NA; ++a)
+#pragma unroll
+          for (int c = 0; c < NB; ++c) dmma884(acc[a][c][0], acc[a][c][1], fa[a], fb[c]);
+      }
+      mbar_arrive(&yfree[yb]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[b]);
+    }
+  };
+  using I1 = std::integral_constant<int, 1>;
+  using I2 = std::integral_constant<int, 2>;
+  using I3 = std::integral_constant<int, 3>;
+  using I4 = std::integral_constant<int, 4>;
+  if (ncb == 2) {
+    if (na == 4) stage_loop(I4{}, I2{});
+    else if (na == 3) stage_loop(I3{}, I2{});
+    else if (na == 2) stage_loop(I2{}, I2{});
+    else stage_loop(I1{}, I2{});
+  } else {
+    if (na == 4) stage_loop(I4{}, I1{});
+    else if (na == 3) stage_loop(I3{}, I1{});
+    else if (na == 2) stage_loop(I2{}, I1{});
+    else stage_loop(I1{}, I1{});
+  }
+  double* dst = p.partial + ((size_t)blockIdx.x * SLOTS + warp * TPW) * 1024;
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const double v0 = c < 2 ? acc[a][c & 1][0] : 0.0, v1 = c < 2 ? acc[a][c & 1][1] : 0.0;
+      *reinterpret_cast<double2*>(dst + (a * 8 + g) * 32 + c * 8 + 2 * tq) = make_double2(v0, v1);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- host side
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+    cudaGetLastError();
+  }
+  return fn;
+}
+
+bool tma_available() { return encode_fn() != nullptr; }
+
+int tma_pass_prepare(const TallParams& p, TmaMaps& maps, TmaExtra& x) {
+  EncodeTiledFn enc = encode_fn();
+  if (!enc) return -1;
+  memset(&x, 0, sizeof(x));
+  int nops = 0;
+  uint32_t bytes = 0;
+  int logical = 0;
+  int kp_lo = 1 << 30, kp_hi = 0;
+  for (int s = 0; s < p.nseg; ++s) {
+    const Seg& sg = p.seg[s];
+    if ((sg.col0 & 7) != 0 || (reinterpret_cast<uintptr_t>(sg.ptr) & 15) != 0 || (sg.ld & 1) != 0) return -1;
+    const int bw = std::min(256, (sg.ncols + 7) / 8 * 8);
+    cuuint64_t dims[2] = {(cuuint64_t)p.M, (cuuint64_t)sg.ncols};
+    cuuint64_t strides[1] = {(cuuint64_t)sg.ld * sizeof(double)};
+    cuuint32_t box[2] = {(cuuint32_t)TKS, (cuuint32_t)bw};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&maps.m[s], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(sg.ptr), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return -1;
+    for (int c = 0; c < sg.ncols; c += bw) {
+      if (nops >= TMA_MAX_OPS) return -1;
+      x.op_seg[nops] = (short)s;
+      x.op_col[nops] = (short)c;
+      x.op_pcol[nops] = (short)(sg.col0 + c);
+      for (int q = (sg.col0 + c) >> 3; q < (sg.col0 + c + bw) >> 3 && q < TMA_MAX_BLK; ++q) x.written[q] = 1;
+      bytes += (uint32_t)(TKS * bw * sizeof(double));
+      ++nops;
+    }
+    // W rows: logical column range [logical, logical + ncols) against [wlo, wlo + wk)
+    x.wrow0[s] = TMA_NOT_IN_W;
+    const int lo = std::max(logical, p.wlo), hi = std::min(logical + sg.ncols, p.wlo + p.wk);
+    if (p.w > 0 && lo < hi) {
+      x.wrow0[s] = logical - p.wlo;  // may be negative when the W range starts inside the segment
+      kp_lo = std::min(kp_lo, sg.col0 + (lo - logical));
+      kp_hi = std::max(kp_hi, sg.col0 + (hi - logical));
+    }
+    logical += sg.ncols;
+  }
+  if (p.w > 0) {
+    x.kp_lo = kp_lo / 8 * 8;
+    x.kp_hi = (kp_hi + 3) / 4 * 4;
+  }
+  x.nops = nops;
+  x.stage_bytes = bytes;
+  return 0;
+}
+
+void launch_pass_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x, int grid, cudaStream_t st) {
+  const size_t smem = tma_pass_smem_bytes(p.np_pad, x.kp_hi - x.kp_lo);
+  cudaFuncSetAttribute(pass_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  pass_tma_kernel<<<grid, NTHR, smem, st>>>(p, maps, x);
+}
+
+}  // namespace psvd

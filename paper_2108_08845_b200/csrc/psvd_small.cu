@@ -188,7 +188,7 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
   // FAST-only arrays (after clus): column starts, double-buffered v / w, row partials
   constexpr int NT = (EIG_FAST_NMAX + 31) / 32;
   const int npad = ((n + 31) / 32) * 32;
-  double* fbase = red + 64 + (K + 1) / 2 + 1;
+  double* fbase = red + 64 + K + 1;
   int* cs = reinterpret_cast<int*>(fbase);                 // n ints
   double* vsA = fbase + (n + 1) / 2 + 1;
   double* vsB = vsA + npad;
@@ -196,7 +196,6 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
   double* ydot = wsv + npad;
   double* psm = ydot + npad;
   double* ypart = psm + npad;                              // [nwarps][npad]
-  double* scal = ypart + (size_t)(FAST ? EIG_FAST_THREADS / 32 : 0) * npad;  // 8 scalars
   double* Z = ws + npk;                     // n x K (col-major, ld n)
   double* Dp = Z + (size_t)n * K;           // K x n
   double* Dm = Dp + (size_t)n * K;          // K x n
@@ -216,7 +215,7 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
   if constexpr (FAST) {
     // ---- B (fast): column-oriented Householder tridiagonalization, lane-owned rows
     for (int c = tid; c < n; c += nthr) cs[c] = pidx(n, c, c);
-    for (int i = tid; i < npad; i += nthr) { vsA[i] = 0.0; vsB[i] = 0.0; wsv[i] = 0.0; ydot[i] = 0.0; }
+    for (int i = tid; i < npad; i += nthr) { vsA[i] = 0.0; vsB[i] = 0.0; wsv[i] = 0.0; ydot[i] = 0.0; psm[i] = 0.0; }
     __syncthreads();
     double vO[NT], wO[NT], vN[NT];
 #pragma unroll
@@ -232,66 +231,86 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
       tsub = now;
     };
     tick(-1);
+    // Per column j, three barriers:
+    //   (e+a) every thread: w_{j-1} = p + kc v_{j-1} (registers + smem);  the owner warp of
+    //         column j applies step j-1's update to it and turns it into reflector v_j
+    //   (c)   fused sweep over columns > j: update with (v_{j-1}, w_{j-1}), symv with v_j
+    //   (d)   p = tau_j y, partials of p.v
     for (int j = 0; j + 2 < n; ++j) {
-      // (a) column j: apply step j-1's update (rows >= j), then alpha and ||A[j+2:, j]||^2
-      if (warp == (j % nwarps)) {
-        const double wj = wsv[j], vj = vs_old[j];
-        double part = 0.0;
+      double kc = 0.0;
+      if (j > 0) {
+        double ptv = lane < nwarps ? red[lane] : 0.0;
+        ptv = warp_sum(ptv);
+        kc = -0.5 * tau[j - 1] * ptv;
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           const int r = lane + 32 * t;
+          vO[t] = vN[t];
+          wO[t] = (r < npad) ? fma(kc, vN[t], psm[r]) : 0.0;
+        }
+        for (int r = tid; r < npad; r += nthr) wsv[r] = fma(kc, vs_old[r], psm[r]);
+      }
+      if (warp == (j % nwarps)) {
+        const double vj = vs_old[j];
+        const double wj = fma(kc, vj, psm[j]);
+        double part = 0.0, xa = 0.0;
+        double xs[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int r = lane + 32 * t;
+          xs[t] = 0.0;
+          if (32 * t + 31 < j) continue;
           if (r >= j && r < n) {
-            const int a = cs[j] + (r - j);
-            const double x = Lp[a] - (vO[t] * wj + wO[t] * vj);
-            Lp[a] = x;
+            const double x = Lp[cs[j] + (r - j)] - (vO[t] * wj + wO[t] * vj);
+            xs[t] = x;
             if (r >= j + 2) part = fma(x, x, part);
+            if (r == j + 1) xa = x;
+            if (r == j) dd[j] = x;
           }
         }
-        part = warp_sum(part);
-        if (lane == 0) scal[0] = part;
+        const double xn2 = warp_sum(part);
+        const double alpha = __shfl_sync(full, xa, (j + 1) & 31);
+        double tj = 0.0, beta = alpha, scl = 0.0;
+        if (xn2 != 0.0) {
+          beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+          tj = (beta - alpha) / beta;
+          scl = 1.0 / (alpha - beta);
+        }
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int r = lane + 32 * t;
+          double vr = 0.0;
+          if (tj != 0.0 && r >= j + 1 && r < n) vr = (r == j + 1) ? 1.0 : xs[t] * scl;
+          if (r < npad) vs_new[r] = vr;
+          if (r >= j && r < n) Lp[cs[j] + (r - j)] = (r >= j + 2 && tj != 0.0) ? vr : xs[t];
+        }
+        if (lane == 0) { ee[j] = beta; tau[j] = tj; }
       }
       __syncthreads();
       tick(0);
-      // (b) reflector of column j (every lane derives its own v rows; threads r publish v)
-      const double xn2 = scal[0];
-      const double alpha = Lp[cs[j] + 1];
-      double tj = 0.0, beta = alpha, scl = 0.0;
-      if (xn2 != 0.0) {
-        beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-        tj = (beta - alpha) / beta;
-        scl = 1.0 / (alpha - beta);
-      }
+      const double tj = tau[j];
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
         const int r = lane + 32 * t;
-        vN[t] = (tj == 0.0 || r < j + 1 || r >= n) ? 0.0 : (r == j + 1 ? 1.0 : Lp[cs[j] + (r - j)] * scl);
+        vN[t] = r < npad ? vs_new[r] : 0.0;
       }
-      __syncthreads();  // all reads of column j done before it is overwritten with the reflector
-      for (int r = tid; r < npad; r += nthr) {
-        double vr = 0.0;
-        if (tj != 0.0 && r >= j + 1 && r < n) {
-          if (r == j + 1) {
-            vr = 1.0;
-          } else {
-            vr = Lp[cs[j] + (r - j)] * scl;
-            Lp[cs[j] + (r - j)] = vr;
-          }
-        }
-        vs_new[r] = vr;
-      }
-      if (tid == 0) { dd[j] = Lp[cs[j]]; ee[j] = beta; tau[j] = tj; }
-      __syncthreads();
       tick(1);
       // (c) fused sweep over columns c >= j+1: update with (v_old, w_old), symv with v_new
       double yp[NT];
 #pragma unroll
       for (int t = 0; t < NT; ++t) yp[t] = 0.0;
-      for (int c = j + 1 + ((warp - (j + 1)) % nwarps + nwarps) % nwarps; c < n; c += nwarps) {
+      // two columns per iteration: independent dot chains / warp reductions overlap
+      for (int c = j + 1 + ((warp - (j + 1)) % nwarps + nwarps) % nwarps; c < n; c += 2 * nwarps) {
+        const int c1 = c + nwarps;
+        const bool has1 = c1 < n;
+        const int c1s = has1 ? c1 : c;
         const double wpc = wsv[c], vpc = vs_old[c], vnc = vs_new[c];
-        const int base = cs[c] - c;
-        double dot = 0.0;
+        const double wpc1 = wsv[c1s], vpc1 = vs_old[c1s], vnc1 = has1 ? vs_new[c1s] : 0.0;
+        const int base = cs[c] - c, base1 = cs[c1s] - c1s;
+        double dot = 0.0, dot1 = 0.0;
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
+          if (32 * t + 31 < c) continue;  // warp-uniform: whole slot above the diagonal
           const int r = lane + 32 * t;
           if (r >= c && r < n) {
             const double x = Lp[base + r] - (vO[t] * wpc + wO[t] * vpc);
@@ -299,9 +318,22 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
             yp[t] = fma(x, vnc, yp[t]);
             if (r > c) dot = fma(x, vN[t], dot);
           }
+          if (has1 && r >= c1 && r < n) {
+            const double x = Lp[base1 + r] - (vO[t] * wpc1 + wO[t] * vpc1);
+            Lp[base1 + r] = x;
+            yp[t] = fma(x, vnc1, yp[t]);
+            if (r > c1) dot1 = fma(x, vN[t], dot1);
+          }
         }
-        dot = warp_sum(dot);
-        if (lane == 0) ydot[c] = dot;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          dot += __shfl_xor_sync(full, dot, o);
+          dot1 += __shfl_xor_sync(full, dot1, o);
+        }
+        if (lane == 0) {
+          ydot[c] = dot;
+          if (has1) ydot[c1] = dot1;
+        }
       }
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
@@ -324,35 +356,28 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
       }
       pv = warp_sum(pv);
       if (lane == 0) red[warp] = pv;
-      __syncthreads();
-      tick(3);
-      // (e) w = p + kc v (kc = -tau/2 p.v); registers for own rows, smem for column values
-      double ptv = lane < nwarps ? red[lane] : 0.0;
-      ptv = warp_sum(ptv);
-      const double kc = -0.5 * tj * ptv;
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        const int r = lane + 32 * t;
-        vO[t] = vN[t];
-        wO[t] = (r < npad) ? fma(kc, vs_new[r], psm[r]) : 0.0;
-      }
-      __syncthreads();  // every lane has read psm / red / old wsv
-      for (int r = tid; r < npad; r += nthr) wsv[r] = fma(kc, vs_new[r], psm[r]);
       double* tmp = vs_old;
       vs_old = vs_new;
       vs_new = tmp;
       __syncthreads();
-      tick(4);
+      tick(3);
     }
     if (timers != nullptr && tid == 0)
       for (int i = 0; i < 5; ++i) timers[9 + i] = sub[i];
-    // pending update of the trailing 2x2 block with the last reflector
-    if (n >= 3 && tid == 0) {
-      for (int c = n - 2; c < n; ++c)
-        for (int r = c; r < n; ++r) {
-          const int a = cs[c] + (r - c);
-          Lp[a] -= vs_old[r] * wsv[c] + wsv[r] * vs_old[c];
-        }
+    // w of the last reflector, then the pending update of the trailing 2x2 block
+    if (n >= 3) {
+      double ptv = lane < nwarps ? red[lane] : 0.0;
+      ptv = warp_sum(ptv);
+      const double kc = -0.5 * tau[n - 3] * ptv;
+      for (int r = tid; r < npad; r += nthr) wsv[r] = fma(kc, vs_old[r], psm[r]);
+      __syncthreads();
+      if (tid == 0) {
+        for (int c = n - 2; c < n; ++c)
+          for (int r = c; r < n; ++r) {
+            const int a = cs[c] + (r - c);
+            Lp[a] -= vs_old[r] * wsv[c] + wsv[r] * vs_old[c];
+          }
+      }
     }
     __syncthreads();
   } else {
@@ -470,34 +495,67 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
   __syncthreads();
 
   stamp(3);
-  // ---- D: twisted-factorization eigenvectors of T (one thread per eigenvalue)
-  for (int k = tid; k < K; k += nthr) {
+  // ---- D: twisted-factorization eigenvectors of T: forward (dp) and backward (dm)
+  // recurrences on two threads per eigenvalue, twist index = first argmin |gamma_r|
+  // (warp per eigenvalue), then the two halves of z on two threads again.
+  int* rsel = clus + K;  // K ints after the cluster leaders
+  for (int u = tid; u < 2 * K; u += nthr) {
+    const int k = u % K;
     const double lk = lam[k];
-    double* dp = Dp + (size_t)k * n;
-    double* dm = Dm + (size_t)k * n;
-    double q = fix_pivot(dd[0] - lk, pivmin);
-    dp[0] = q;
-    for (int i = 1; i < n; ++i) {
-      q = fix_pivot((dd[i] - lk) - e2[i - 1] / q, pivmin);
-      dp[i] = q;
+    if (u < K) {
+      double* dp = Dp + (size_t)k * n;
+      double q = fix_pivot(dd[0] - lk, pivmin);
+      dp[0] = q;
+      for (int i = 1; i < n; ++i) {
+        q = fix_pivot((dd[i] - lk) - e2[i - 1] / q, pivmin);
+        dp[i] = q;
+      }
+    } else {
+      double* dm = Dm + (size_t)k * n;
+      double q = fix_pivot(dd[n - 1] - lk, pivmin);
+      dm[n - 1] = q;
+      for (int i = n - 2; i >= 0; --i) {
+        q = fix_pivot((dd[i] - lk) - e2[i] / q, pivmin);
+        dm[i] = q;
+      }
     }
-    q = fix_pivot(dd[n - 1] - lk, pivmin);
-    dm[n - 1] = q;
-    for (int i = n - 2; i >= 0; --i) {
-      q = fix_pivot((dd[i] - lk) - e2[i] / q, pivmin);
-      dm[i] = q;
-    }
-    int r = 0;
-    double gbest = DBL_MAX;
-    for (int i = 0; i < n; ++i) {
-      const double gm = fabs(dp[i] + dm[i] - (dd[i] - lk));
-      if (gm < gbest) { gbest = gm; r = i; }
-    }
-    double* z = Z + (size_t)k * n;
-    z[r] = 1.0;
-    for (int i = r - 1; i >= 0; --i) z[i] = -ee[i] * z[i + 1] / dp[i];
-    for (int i = r + 1; i < n; ++i) z[i] = -ee[i - 1] * z[i - 1] / dm[i];
   }
+  __syncthreads();
+  for (int k = warp; k < K; k += nwarps) {
+    const double lk = lam[k];
+    const double* dp = Dp + (size_t)k * n;
+    const double* dm = Dm + (size_t)k * n;
+    double gb = DBL_MAX;
+    int rb = n;
+    for (int i = lane; i < n; i += 32) {
+      const double gm = fabs(dp[i] + dm[i] - (dd[i] - lk));
+      if (gm < gb) { gb = gm; rb = i; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double og = __shfl_xor_sync(full, gb, o);
+      const int orr = __shfl_xor_sync(full, rb, o);
+      if (og < gb || (og == gb && orr < rb)) { gb = og; rb = orr; }
+    }
+    if (lane == 0) rsel[k] = rb;
+  }
+  __syncthreads();
+  for (int u = tid; u < 2 * K; u += nthr) {
+    const int k = u % K;
+    const int r = rsel[k];
+    double* z = Z + (size_t)k * n;
+    if (u < K) {
+      const double* dp = Dp + (size_t)k * n;
+      double zi = 1.0;
+      z[r] = 1.0;
+      for (int i = r - 1; i >= 0; --i) { zi = -ee[i] * zi / dp[i]; z[i] = zi; }
+    } else {
+      const double* dm = Dm + (size_t)k * n;
+      double zi = 1.0;
+      for (int i = r + 1; i < n; ++i) { zi = -ee[i - 1] * zi / dm[i]; z[i] = zi; }
+    }
+  }
+  __syncthreads();
   // cluster leaders: consecutive eigenvalues closer than 1e-3 ||T|| (dstein's ORTOL)
   if (tid == 0) {
     int lead = 0;
@@ -563,19 +621,54 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
 
   stamp(5);
   // ---- F: back-transform Z <- H_0 ... H_{n-3} Z  (warp per column, no block sync)
-  for (int k = warp; k < K; k += nwarps) {
-    double* z = Z + (size_t)k * n;
-    for (int j = n - 3; j >= 0; --j) {
-      const double tj = tau[j];
-      if (tj == 0.0) continue;
-      const int cj = pidx(n, j, j);
-      double s = 0.0;
-      for (int i = j + 2 + lane; i < n; i += 32) s += Lp[cj + (i - j)] * z[i];
-      s = warp_sum(s) + z[j + 1];
-      s *= tj;
-      if (lane == 0) z[j + 1] -= s;
-      for (int i = j + 2 + lane; i < n; i += 32) z[i] -= s * Lp[cj + (i - j)];
-      __syncwarp();
+  if constexpr (FAST) {
+    // z in registers (lane-owned rows), reflector j read from column j of the packed storage
+    for (int k = warp; k < K; k += nwarps) {
+      double* zg = Z + (size_t)k * n;
+      double zr[NT];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const int r = lane + 32 * t;
+        zr[t] = r < n ? zg[r] : 0.0;
+      }
+      for (int j = n - 3; j >= 0; --j) {
+        const double tj = tau[j];
+        if (tj == 0.0) continue;
+        const int base = cs[j] - j;
+        double vr[NT];
+        double s = 0.0;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+          const int r = lane + 32 * t;
+          if (32 * t + 31 < j + 1) { vr[t] = 0.0; continue; }
+          vr[t] = (r == j + 1) ? 1.0 : ((r >= j + 2 && r < n) ? Lp[base + r] : 0.0);
+          s = fma(vr[t], zr[t], s);
+        }
+        s = warp_sum(s) * tj;
+#pragma unroll
+        for (int t = 0; t < NT; ++t) zr[t] = fma(-s, vr[t], zr[t]);
+      }
+#pragma unroll
+      for (int t = 0; t < NT; ++t) {
+        const int r = lane + 32 * t;
+        if (r < n) zg[r] = zr[t];
+      }
+    }
+  } else {
+    for (int k = warp; k < K; k += nwarps) {
+      double* z = Z + (size_t)k * n;
+      for (int j = n - 3; j >= 0; --j) {
+        const double tj = tau[j];
+        if (tj == 0.0) continue;
+        const int cj = pidx(n, j, j);
+        double s = 0.0;
+        for (int i = j + 2 + lane; i < n; i += 32) s += Lp[cj + (i - j)] * z[i];
+        s = warp_sum(s) + z[j + 1];
+        s *= tj;
+        if (lane == 0) z[j + 1] -= s;
+        for (int i = j + 2 + lane; i < n; i += 32) z[i] -= s * Lp[cj + (i - j)];
+        __syncwarp();
+      }
     }
   }
   __syncthreads();
@@ -699,7 +792,7 @@ bool eig_supported(int n, int K) { return n >= 1 && K >= 1 && K <= n && K <= 102
 void launch_eig_topk(const double* G, int n, int K, const double* dscale, double* W, double* sigma,
                      double* ws, int* status, long long* timers, cudaStream_t st, double rank_tol, int split) {
   const int npad = (n + 31) / 32 * 32;
-  const size_t vec = (size_t)6 * n + K + 64 + (K + 1) / 2 + 2;
+  const size_t vec = (size_t)6 * n + K + 64 + K + 2;  // ... + clus (K ints) + rsel (K ints)
   const size_t fast_extra = (size_t)(n + 1) / 2 + 1 + 5 * (size_t)npad + (size_t)(EIG_FAST_THREADS / 32) * npad + 8;
   const size_t npk = (size_t)n * (n + 1) / 2;
   const size_t limit = 227 * 1024;

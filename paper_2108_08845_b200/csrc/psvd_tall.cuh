@@ -17,6 +17,8 @@
 // tall_reduce (bitwise reproducible; no atomics), so replicated small
 // factorizations on every GPU see identical input.
 #pragma once
+#include <cuda.h>
+
 #include "psvd_common.cuh"
 
 namespace psvd {
@@ -83,5 +85,28 @@ void launch_tall(const TallParams& p, int grid, cudaStream_t st);
 size_t gram_ws_smem_bytes(int np_pad, int ns);
 void launch_gram_ws(const TallParams& p, int grid, cudaStream_t st);
 void launch_tall_reduce(const double* partial, const ReduceMap& map, double* tiles, cudaStream_t st);
+
+// Warp-specialized TMA pass for narrow panels (w <= 16, Gram tiles only against Y):
+// every segment starts on an 8-column boundary of the panel (1024-byte swizzle atoms).
+constexpr int TMA_MAX_OPS = 16;
+constexpr int TMA_NOT_IN_W = -(1 << 30);
+constexpr int TMA_MAX_BLK = 192;  // 8-column blocks of the panel
+constexpr int TMA_GRAM_WARP0 = 4;                 // warps 0..3 form Y
+constexpr int TMA_GRAM_WARPS = NWARP - 1 - TMA_GRAM_WARP0;  // last warp is the TMA producer
+struct TmaMaps {
+  CUtensorMap m[MAX_SEG];
+};
+struct TmaExtra {
+  int nops;
+  short op_seg[TMA_MAX_OPS], op_col[TMA_MAX_OPS], op_pcol[TMA_MAX_OPS];
+  int wrow0[MAX_SEG];        // W row of the segment's first column (TMA_NOT_IN_W: outside Y's range)
+  int kp_lo, kp_hi;          // Y's k range in physical panel columns
+  unsigned stage_bytes;
+  unsigned char written[TMA_MAX_BLK];  // 8-column panel blocks covered by a TMA box
+};
+bool tma_available();
+size_t tma_pass_smem_bytes(int np_pad, int kp_span);
+int tma_pass_prepare(const TallParams& p, TmaMaps& maps, TmaExtra& x);
+void launch_pass_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x, int grid, cudaStream_t st);
 
 }  // namespace psvd

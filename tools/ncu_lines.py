@@ -23,7 +23,9 @@ def main(csvf, cubin, func, top=40):
     rows = list(csv.reader(open(csvf)))
     hdr = rows[1]
     ia, ie, iss = hdr.index("Address"), hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
-    data = [r for r in rows[2:] if len(r) >= len(hdr)]
+    data = [r for r in rows[2:] if len(r) >= len(hdr) and re.fullmatch(r"(0x)?[0-9a-fA-F]+", r[ia])]
+    end = next((i for i in range(1, len(data)) if int(data[i][ia], 16) < int(data[i - 1][ia], 16)), len(data))
+    data = data[:end]  # first kernel only
     start = int(data[0][ia], 16)
     lm = line_map(cubin, func)
     agg = collections.defaultdict(lambda: [0, 0])
