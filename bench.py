@@ -330,7 +330,7 @@ def run_ours(a):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (analytic Burgers, device-generated; same formula as the host generator)",
         "config": config_dict(a),
-        "roofline": {"bound": "tensor", "kernel": "psvd_gram (tall_pass_kernel DMMA Gram of [ff*U*S | A])",
+        "roofline": {"bound": "tensor", "kernel": "psvd_gram (gram_ws_kernel: warp-specialized DMMA Gram of [ff*U*S | A])",
                      "achieved": round(g_ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": round(g_ach / FP64_PEAK_TFLOPS, 4), "traffic": traffic,
                      "peak_source": "measured DMMA.8x8x4 peak (profiles/fp64_peaks_r01.jsonl); "
