@@ -234,7 +234,7 @@ def run_ours(a):
             # whole stream through psvd_stream_run (look-ahead A^T A on a second stream)
             nat.call("psvd_stream_run", c, M, nat._vp(0), 0, nat._vp(0), 0, nb, Aptr, Ald, Bc, K, FF, 1,
                      nat._vp(Ubuf[0].data_ptr()), nat._vp(Ubuf[1].data_ptr()), Ubuf[0].ld, nat.ptr(hist),
-                     ctypes.byref(fin), st)
+                     ctypes.byref(fin), None, st)
             return Ubuf[fin.value], hist[nb - 1]
         cur = 0
         for b in range(nb):
@@ -403,9 +403,10 @@ def time_randomized(a, D, M, dev, c, stream, q):
 
 
 def e2e(a, p, D, M, dev, world, ctxr):
-    """Same metric through the public API (stream_initialize / stream_incorporate,
-    parallel_* at N > 1) with the snapshot batches in pinned host memory: every
-    step copies its batches host->device and reads the modes + sigma back."""
+    """Same metric through the public API (stream_all at N = 1, parallel_stream_* at
+    N > 1) with the snapshot batches in pinned host memory: every step copies its
+    batches host->device (overlapped with the updates on a side stream) and reads
+    the modes + sigma back (StreamState.to_host: one dense copy into pinned memory)."""
     import torch
     import torch.distributed as dist
 
@@ -416,10 +417,9 @@ def e2e(a, p, D, M, dev, world, ctxr):
 
     def one():
         if world == 1:
-            st = p.stream_initialize(batches[0], cfg, device=dev)
-            for bt in batches[1:]:
-                st = p.stream_incorporate(st, bt, cfg)
-            m, s = st.modes, st.singular_values
+            # stream_all: pinned batches upload on a side stream, overlapping the pipelined updates
+            st, _ = p.stream_all(batches, cfg, device=dev)
+            return st.to_host()
         else:
             st = p.parallel_stream_initialize(ctxr, batches[0].to(dev), cfg)
             for bt in batches[1:]:
@@ -444,7 +444,7 @@ def e2e(a, p, D, M, dev, world, ctxr):
     return {"value": round(8.0 * a.rows * SNAPS / dt / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": int(8 * M * SNAPS), "d2h_bytes_per_step": int(out[0].numel() * 8 + out[1].numel() * 8),
             "ms_per_step": round(dt * 1e3, 2), "steps": n,
-            "path": "public API stream_initialize/stream_incorporate from pinned host batches"}
+            "path": "public API stream_all (N=1) / parallel_stream_* (N>1) from pinned host batches"}
 
 
 def main():

@@ -122,10 +122,13 @@ int psvd_stream_update(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, c
  * one.  Updates alternate between U_a and U_b (M x K, ld ldo; U_in must not
  * alias U_a); *final_buf receives 0 or 1.  sigma_hist: device, nb x K (the
  * singular values after every step).  Ordered after prior work on `stream`
- * and joined back into it. */
+ * and joined back into it.  batch_ready (optional, nb cudaEvent_t or NULL
+ * entries): batch j is read only after its event, so host->device copies of
+ * later batches can overlap the updates of earlier ones. */
 int psvd_stream_run(psvd_ctx* ctx, int64_t M, const double* U_in, int64_t ldu, const double* sigma_in, int Kc,
                     int nb, const double* const* A, const int64_t* lda, const int* B, int K, double ff, int rescue,
-                    double* U_a, double* U_b, int64_t ldo, double* sigma_hist, int* final_buf, void* stream);
+                    double* U_a, double* U_b, int64_t ldo, double* sigma_hist, int* final_buf,
+                    void* const* batch_ready, void* stream);
 
 /* ---- randomized streaming update (low_rank_svd of the panel,
  * linalg.py:126-162) ----

@@ -50,7 +50,7 @@ _SIGS = {
                                     _c_int, _c_int, _vp, _c_i64, _vp, _vp]),
     "psvd_stream_run": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_int, _c_int, ctypes.POINTER(_vp),
                                  ctypes.POINTER(_c_i64), ctypes.POINTER(_c_int), _c_int, _c_dbl, _c_int, _vp, _vp,
-                                 _c_i64, _vp, ctypes.POINTER(_c_int), _vp]),
+                                 _c_i64, _vp, ctypes.POINTER(_c_int), ctypes.POINTER(_vp), _vp]),
     "psvd_rand_update": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_int, _vp, _c_i64, _c_int, _c_int,
                                   _c_int, _c_int, _vp, _vp, _c_i64, _vp, _vp]),
     "psvd_sum_ordered": (_c_int, [_vp, _vp, _c_int, _c_i64, _vp, _vp]),
@@ -214,6 +214,49 @@ def as_device_colmajor(a, device, name="a"):
         host = torch.from_numpy(np.ascontiguousarray(arr))
         out.view.copy_(host.to(device))
     return out
+
+
+def to_host_colmajor(t, pinned=True):
+    """D2H of a (column-major) CUDA matrix as ONE dense copy into (pinned) host memory;
+    returns a column-major CPU view with the same shape."""
+    if t.device.type != "cuda":
+        return t
+    m, n = t.shape
+    if t.stride(0) == 1 and t.stride(1) >= m:
+        src = t.T if t.stride(1) == m else t.T.contiguous()  # (n, m) row-major == column-major (m, n)
+    else:
+        src = t.T.contiguous()
+    host = torch.empty((n, m), dtype=t.dtype, pin_memory=pinned)
+    host.copy_(src)
+    return host.T
+
+
+_COPY_STREAMS = {}
+
+
+def copy_stream(device):
+    """Side stream for host->device batch uploads (one per device)."""
+    key = torch.device(device).index
+    if key not in _COPY_STREAMS:
+        _COPY_STREAMS[key] = torch.cuda.Stream(device=device)
+    return _COPY_STREAMS[key]
+
+
+def upload_async(a, device, name="a"):
+    """(DevMat, ready event) for a pinned host fp64 matrix: the copy runs on the copy
+    stream and the buffer is marked as used by the current stream.  Any other input
+    goes through as_device_colmajor and returns (DevMat, None)."""
+    if (isinstance(a, torch.Tensor) and a.device.type == "cpu" and a.dtype == torch.float64 and a.dim() == 2
+            and min(a.shape) >= 1 and a.is_pinned()):
+        cs = copy_stream(device)
+        with torch.cuda.device(device), torch.cuda.stream(cs):
+            out = DevMat.empty(a.shape[0], a.shape[1], device)
+            out.view.copy_(a, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(cs)
+        out.t.record_stream(torch.cuda.current_stream(device))
+        return out, ev
+    return as_device_colmajor(a, device, name), None
 
 
 def as_device_vector(v, device, n=None, name="v"):

@@ -789,7 +789,7 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
 // the recompose.  Same arithmetic as psvd_stream_update per batch.
 int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, const double* sigma_in, int Kc,
                     int nb, const double* const* A, const int64_t* lda, const int* B, int K, double ff, int rescue,
-                    double* U_a, double* U_b, int64_t ldo, double* sigma_hist, int* final_buf, void* stream) {
+                    double* U_a, double* U_b, int64_t ldo, double* sigma_hist, int* final_buf, void* const* batch_ready, void* stream) {
   if (!c || nb < 1 || !A || !lda || !B || !U_a || !U_b || !sigma_hist || !final_buf)
     return fail(c, PSVD_EINVAL, "bad stream_run arguments");
   if (Kc != 0 && Kc != K) return fail(c, PSVD_EINVAL, "initial state carries %d modes, K=%d", Kc, K);
@@ -843,6 +843,7 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
     // start A^T A of batch j with the core solve of batch j-1: it then overlaps that one-SM
     // solve (the longer of the two) instead of competing with the recompose pass for SMs
     if (j >= 1) cudaStreamWaitEvent(lo, c->ev_eig_start, 0);
+    if (batch_ready && batch_ready[j]) cudaStreamWaitEvent(lo, (cudaEvent_t)batch_ready[j], 0);
     const int64_t rows_sub = (M + nsub - 1) / nsub / 32 * 32 + 32;
     Pass first;
     size_t part_off = 0;
@@ -885,6 +886,7 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
   const double* sprev = Kc > 0 ? sigma_in : nullptr;
   int cur = 0;
   if (Kc > 0) {  // U^T [U | A_0] for the initial state
+    if (batch_ready && batch_ready[0]) cudaStreamWaitEvent(hi, (cudaEvent_t)batch_ready[0], 0);
     Pass pu;
     if ((rc = plan_pass(c, pu, M, {Seg{U_in, ldu, K, 0}, Seg{A[0], lda[0], B[0], 0}}, 0, 0, 0, nullptr, 0, true,
                         false, false, -1, K)))
@@ -920,6 +922,7 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
       // fused: U_b = [U_{b-1} | A_b] W, with U_b^T U_b and U_b^T A_{b+1} from the same pass
       std::vector<Seg> segs = panel(Uprev, ldprev, kc, A[b], lda[b], B[b]);
       segs.push_back(Seg{A[b + 1], lda[b + 1], B[b + 1], 1});
+      if (batch_ready && batch_ready[b + 1]) cudaStreamWaitEvent(hi, (cudaEvent_t)batch_ready[b + 1], 0);
       Pass pf;
       const int wk = kc + B[b];
       if ((rc = plan_pass(c, pf, M, segs, 0, wk, K, W, wk, false, true, true, -1, -1, nullptr, nullptr, 0, -1)))

@@ -62,10 +62,16 @@ class StreamState:
     singular_values: torch.Tensor
     iteration: int
 
+    def to_host(self, pinned=True):
+        """(modes, singular_values) as CPU tensors; modes is a column-major view filled
+        by one dense device-to-host copy (into pinned memory by default)."""
+        return (nat.to_host_colmajor(self.modes.detach(), pinned),
+                self.singular_values.detach().cpu())
+
     def numpy(self):
-        """(modes, singular_values) as host numpy arrays."""
-        return (self.modes.detach().cpu().numpy().copy(),
-                self.singular_values.detach().cpu().numpy().copy())
+        """(modes, singular_values) as host numpy arrays (modes Fortran-ordered)."""
+        m, s = self.to_host(pinned=True)
+        return np.array(m.numpy(), order="F", copy=True), s.numpy().copy()
 
 
 def _device_of(*objs):
@@ -150,9 +156,10 @@ def stream_incorporate(state, a_new, config):
 STREAM_WINDOW = 8  # batches resident on the device per pipelined run
 
 
-def _run_window(state, mats, config, dev):
+def _run_window(state, mats, config, dev, ready=None):
     """Deterministic updates over device batches `mats` with look-ahead
-    (psvd_stream_run): the next batch's A^T A overlaps the current core solve."""
+    (psvd_stream_run): the next batch's A^T A overlaps the current core solve.
+    `ready`: per-batch upload events (or None) the device work waits on."""
     k = config.k_modes
     M = mats[0].rows
     for m in mats:
@@ -178,9 +185,12 @@ def _run_window(state, mats, config, dev):
         lda = (ctypes.c_int64 * nb)(*[m.ld for m in mats])
         B = (ctypes.c_int * nb)(*[m.cols for m in mats])
         fin = ctypes.c_int(0)
+        rd = None
+        if ready is not None and any(e is not None for e in ready):
+            rd = (nat._vp * nb)(*[nat._vp(e.cuda_event if e is not None else 0) for e in ready])
         nat.call("psvd_stream_run", ctx, M, uptr, uld, sptr, kc, nb, A, lda, B, k, float(config.forget_factor), 1,
                  nat._vp(outs[0].data_ptr()), nat._vp(outs[1].data_ptr()), outs[0].ld, nat.ptr(hist),
-                 ctypes.byref(fin), nat.stream_ptr(dev))
+                 ctypes.byref(fin), rd, nat.stream_ptr(dev))
         _check_status(ctx, dev, "a_new")
     it0 = -1 if state is None else state.iteration
     new_state = StreamState(outs[fin.value].view, hist[nb - 1].clone(), it0 + nb)
@@ -191,7 +201,8 @@ def stream_all(batches, config, device=None):
     """Initialize on the first batch, incorporate the rest (streaming.py:119-133).
     Returns (final_state, history) with the singular values after every step.
     Deterministic streams run in windows of STREAM_WINDOW resident batches
-    through the pipelined psvd_stream_run; randomized ones update per batch."""
+    through the pipelined psvd_stream_run (pinned host batches are uploaded on a
+    side stream, overlapping the updates); randomized ones update per batch."""
     state = None
     history = []
     if config.sketch is not None:
@@ -203,17 +214,20 @@ def stream_all(batches, config, device=None):
             history.append(state.singular_values.clone())
     else:
         dev = None if device is None else torch.device(device)
-        window = []
+        window, ready = [], []
         for batch in batches:
             if dev is None:
                 dev = _device_of(batch)
-            window.append(nat.as_device_colmajor(batch, dev, "a0" if state is None and not window else "a_new"))
+            # pinned host batches upload on a side stream: later copies overlap earlier updates
+            m, ev = nat.upload_async(batch, dev, "a0" if state is None and not window else "a_new")
+            window.append(m)
+            ready.append(ev)
             if len(window) == STREAM_WINDOW:
-                state, h = _run_window(state, window, config, dev)
+                state, h = _run_window(state, window, config, dev, ready)
                 history.extend(h)
-                window = []
+                window, ready = [], []
         if window:
-            state, h = _run_window(state, window, config, dev)
+            state, h = _run_window(state, window, config, dev, ready)
             history.extend(h)
     if state is None:
         raise ValueError("batch stream is empty")

@@ -235,6 +235,30 @@ def test_stream_all_windows_and_continuation():
         assert oracle.sigma_rel_err(h.cpu().numpy(), rh) <= SIG_TOL
 
 
+def test_stream_all_pinned_host_batches_overlap_copies():
+    """Pinned host batches upload on the copy stream (per-batch ready events passed to
+    psvd_stream_run): bitwise the same result as device-resident batches, in windows."""
+    p = _pkg()
+    a = oracle.burgers_matrix(8192, 800)
+    cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=100)
+    dev_b = [torch.from_numpy(np.asfortranarray(a[:, c:c + 100])).cuda() for c in range(0, 800, 100)]
+    host = torch.empty((800, 8192), dtype=torch.float64).pin_memory()
+    host.copy_(torch.from_numpy(a.T.copy()))
+    pin_b = [host[c:c + 100].T for c in range(0, 800, 100)]  # column-major pinned views
+    old = p.streaming.STREAM_WINDOW
+    try:
+        p.streaming.STREAM_WINDOW = 3
+        s1, h1 = p.stream_all(dev_b, cfg)
+        s2, h2 = p.stream_all(pin_b, cfg)
+    finally:
+        p.streaming.STREAM_WINDOW = old
+    assert torch.equal(s1.modes, s2.modes) and torch.equal(s1.singular_values, s2.singular_values)
+    assert all(torch.equal(x, y) for x, y in zip(h1, h2))
+    ref_m, ref_s, _ = oracle.ref_stream_all(_batches(a, 100), 10, 0.95)
+    m, s = _np(s2)
+    _assert_parity(m, s, ref_m, ref_s)
+
+
 def test_parallel_golden_via_rank_emulation(golden):
     """4-rank golden (run_simulated of the reference) reproduced by summing the
     per-rank Grams exactly as the NCCL path does (allgather + ordered sum)."""
