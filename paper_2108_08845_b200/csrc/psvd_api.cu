@@ -11,6 +11,7 @@
 
 #include "../../include/psvd.h"
 #include "psvd_small.cuh"
+#include "psvd_gemm.cuh"
 #include "psvd_tall.cuh"
 
 using namespace psvd;
@@ -38,6 +39,7 @@ struct psvd_ctx {
   double drift_tol = 1e-8;  // streaming.py:25 ORTHO_DRIFT_TOL (psvd_set_drift_tol overrides, e.g. to force the rescue)
   Buf partial, tiles, gram, eigws, wbuf, utu, tbuf, dvec, colmax;
   Buf ybuf, rsmall, jacws;  // randomized path: sketch Y (M x l), small matrices, Jacobi scratch
+  Buf ybuf2;                // wide randomized path: second sketch buffer (Y T1 out of place)
   Buf partial2, tiles2[2];  // A^T A passes on the low-priority stream (double-buffered tiles)
   cudaStream_t s_hi = nullptr, s_lo = nullptr;  // pipelined stream_run: critical chain / look-ahead Grams
   cudaStream_t s_aux = nullptr;                  // concurrent LDL^T of the split core solve
@@ -486,7 +488,7 @@ int psvd_destroy(psvd_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   Buf* bufs[] = {&c->partial, &c->tiles, &c->gram, &c->eigws, &c->wbuf, &c->utu, &c->tbuf, &c->dvec, &c->colmax,
-                 &c->ybuf, &c->rsmall, &c->jacws, &c->partial2, &c->tiles2[0], &c->tiles2[1]};
+                 &c->ybuf, &c->ybuf2, &c->rsmall, &c->jacws, &c->partial2, &c->tiles2[0], &c->tiles2[1]};
   for (Buf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
   if (c->s_hi) cudaStreamDestroy(c->s_hi);
@@ -690,7 +692,6 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
   if (M < 1 || B < 1 || Kc < 0 || K < 1 || l < K || q < 0) return fail(c, PSVD_EINVAL, "bad randomized shape");
   if (l > std::min<int64_t>(M, n))
     return fail(c, PSVD_EINVAL, "sketch width %d exceeds min(a.shape) = %lld", l, (long long)std::min<int64_t>(M, n));
-  if (l > MAX_W) return fail(c, PSVD_EINVAL, "sketch width %d exceeds %d", l, MAX_W);
   if ((rc = check_mat(c, "U", U, ldu, M, Kc)) || (rc = check_mat(c, "A", A, lda, M, B)) ||
       (rc = check_mat(c, "U_out", U_out, ldo, M, K)))
     return rc;
@@ -723,9 +724,63 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
   const double* d = (const double*)c->dvec.ptr;
   launch_scale_rows(Omega, n, n, l, d, W0, n, st);  // Y = [ff U S | A] Omega = [U | A] (D Omega)
   c->launches++;
+  // Panels too wide for the fused passes (sketch + Gram tiles in one read, W resident in smem)
+  // take the tall-skinny GEMM route: same sequence of products, one product per launch.
   std::vector<Seg> pa = panel(U, ldu, Kc, A, lda, B);
   std::vector<Seg> pb = pa;
   pb.push_back(Seg{Y, ldy, l, 0});
+  bool wide = l > MAX_W || getenv("PSVD_FORCE_WIDE") != nullptr;
+  if (!wide) {  // dry-run plans of the fused passes (no launches): wide when they do not fit
+    Pass t1, t2;
+    wide = plan_pass(c, t1, M, pa, 0, n, l, W0, n, false, true, false) != PSVD_OK ||
+           plan_pass(c, t2, M, pb, n, l, l, T1, l, false, true, true, n) != PSVD_OK;
+  }
+  if (wide) {
+    if ((rc = ensure(c, c->ybuf2, sizeof(double) * (size_t)ldy * l))) return rc;
+    double* Y2 = (double*)c->ybuf2.ptr;
+    const size_t part = std::max(tgemm_tn_partial_doubles(M, n, l, c->num_sms), tgemm_tn_partial_doubles(M, l, l, c->num_sms));
+    if ((rc = ensure(c, c->partial, sizeof(double) * part))) return rc;
+    double* pbuf = (double*)c->partial.ptr;
+    std::vector<GemmSeg> gp;
+    if (Kc > 0) gp.push_back(GemmSeg{U, ldu, Kc});
+    gp.push_back(GemmSeg{A, lda, B});
+    const GemmSeg gy{Y, ldy, l}, gy2{Y2, ldy, l};
+    for (int it = 0; it <= q; ++it) {
+      launch_tgemm_nn(M, gp.data(), (int)gp.size(), W0, n, l, Y, ldy, st);           // Y = P W0
+      launch_tgemm_tn(M, &gy, 1, Y, ldy, l, nullptr, G1, l, pbuf, c->num_sms, st);    // G1 = Y^T Y
+      c->launches += 3;
+      if ((rc = svqb(c, G1, l, T1, sscr, st))) return rc;
+      launch_tgemm_nn(M, &gy, 1, T1, l, l, Y2, ldy, st);                              // Y1 = Y T1
+      launch_tgemm_tn(M, &gy2, 1, Y2, ldy, l, nullptr, G2, l, pbuf, c->num_sms, st);  // G2 = Y1^T Y1
+      launch_tgemm_tn(M, gp.data(), (int)gp.size(), Y2, ldy, l, d, X, n, pbuf, c->num_sms, st);  // X = D P^T Y1
+      c->launches += 5;
+      launch_chol_inv(G2, l, T2, st);
+      launch_small_gemm(X, n, 0, T2, l, (it < q) ? Z : Bt, n, n, l, l, nullptr, st);
+      c->launches += 2;
+      if (it < q) {
+        launch_small_gemm(Z, n, 1, Z, n, G1, l, l, n, l, nullptr, st);
+        c->launches++;
+        if ((rc = svqb(c, G1, l, Tz, sscr, st))) return rc;
+        launch_small_gemm(Z, n, 0, Tz, l, Z1, n, n, l, l, nullptr, st);
+        launch_small_gemm(Z1, n, 1, Z1, n, G1, l, l, n, l, nullptr, st);
+        launch_chol_inv(G1, l, Tz, st);
+        launch_small_gemm(Z1, n, 0, Tz, l, Qz, n, n, l, l, nullptr, st);
+        launch_scale_rows(Qz, n, n, l, d, W0, n, st);
+        c->launches += 5;
+      }
+    }
+    launch_jacobi_svd(Bt, n, l, S, J, (double*)c->jacws.ptr, c->d_status, st);
+    launch_small_gemm(T2, l, 0, J, l, Wf, l, l, l, K, nullptr, st);
+    launch_tgemm_nn(M, &gy2, 1, Wf, l, K, U_out, ldo, st);  // U = Y1 (T2 U_B[:, :K])
+    const int64_t nch = colmax_rows_chunks(M);
+    if ((rc = ensure(c, c->colmax, sizeof(double) * (size_t)nch * K * 2))) return rc;
+    launch_colmax_rows(U_out, ldo, M, K, 0, (double*)c->colmax.ptr, st);
+    launch_colmax_sign((const double*)c->colmax.ptr, (int)nch, K, sgn, st);
+    launch_scale_cols(U_out, ldo, M, K, sgn, st);
+    cudaMemcpyAsync(sigma_out, S, sizeof(double) * K, cudaMemcpyDeviceToDevice, st);
+    c->launches += 6;
+    return cuda_check(c, "randomized update (wide)");
+  }
   for (int it = 0; it <= q; ++it) {
     // pass A: Y = P W0, Y^T Y
     Pass ps;

@@ -60,3 +60,75 @@ def partition_bounds(rows, world_size):
         out.append((lo, hi))
         lo = hi
     return out
+
+
+# ---------------------------------------------------------------------------
+# Builder-defined synthetic configs (not in the reference).
+# Conventions pinned here (the SURVEY lists them as open):
+#   * all draws come from numpy Generator(Philox(seed)), in the order documented per function;
+#   * "N(0, s)" noise means standard deviation s;
+#   * Gaussian factors are NOT orthonormalized: U_f ~ N(0, 1/M), V_f ~ N(0, 1/T), so the
+#     singular values of the signal are the prescribed ones up to O(sqrt(r/M)) relative;
+#   * snapshots are generated column by column from the factors, so any column range
+#     (a batch) can be produced alone with the same bytes as the full matrix.
+
+
+def weather_matrix(n_snapshots=1024, nlat=721, nlon=1440, n_modes=60, rho=0.9, noise=1e-3, seed=1, cols=None):
+    """Config 3: weather-like field on an nlat x nlon grid (rows lat-major).
+    Modes sin(a*lat) * cos(b*lon + phi) with lat in [-pi/2, pi/2] (inclusive), lon in
+    [0, 2*pi) (exclusive), integers a, b in 1..12, phi ~ U[0, 2pi); AR(1) coefficients
+    c_i(t) = rho c_i(t-1) + sqrt(1-rho^2) e, c_i(0) ~ N(0,1), amplitudes 10 * 0.85^i.
+    Draw order from Philox(seed): a, b, phi (n_modes each), c(0), innovations
+    (n_modes x (T-1)); noise per column (_column_noise)."""
+    g = np.random.Generator(np.random.Philox(seed))
+    a = g.integers(1, 13, n_modes)
+    b = g.integers(1, 13, n_modes)
+    phi = g.uniform(0.0, 2.0 * np.pi, n_modes)
+    c = np.empty((n_modes, n_snapshots))
+    c[:, 0] = g.standard_normal(n_modes)
+    innov = g.standard_normal((n_modes, n_snapshots - 1))
+    for t in range(1, n_snapshots):
+        c[:, t] = rho * c[:, t - 1] + np.sqrt(1.0 - rho * rho) * innov[:, t - 1]
+    amp = 10.0 * 0.85 ** np.arange(n_modes)
+    lat = np.linspace(-0.5 * np.pi, 0.5 * np.pi, nlat)
+    lon = np.linspace(0.0, 2.0 * np.pi, nlon, endpoint=False)
+    c0, c1 = cols if cols is not None else (0, n_snapshots)
+    space = (np.sin(np.outer(lat, a))[:, None, :] * np.cos(lon[None, :, None] * b[None, None, :] + phi)).reshape(
+        nlat * nlon, n_modes)
+    out = space @ (amp[:, None] * c[:, c0:c1])
+    out += noise * _column_noise(nlat * nlon, c0, c1, seed)
+    return np.asfortranarray(out)
+
+
+def _column_noise(rows, c0, c1, seed):
+    """N(0,1) noise, column j from its own Philox stream (key = (seed + 1000) * 2^32 + j),
+    so any column range reproduces the same bytes as the full matrix."""
+    out = np.empty((rows, c1 - c0), order="F")
+    for j in range(c0, c1):
+        out[:, j - c0] = np.random.Generator(np.random.Philox(key=(seed + 1000) * 2**32 + j)).standard_normal(rows)
+    return out
+
+
+def factor_matrix(rows, n_snapshots, sigma, noise, seed, cols=None):
+    """Configs 4 / 5: A = U_f diag(sigma) V_f^T + noise * N(0,1), Gaussian factors
+    U_f ~ N(0, 1/rows) (rows x r), V_f ~ N(0, 1/n_snapshots) (n_snapshots x r), drawn in
+    that order from Philox(seed); noise per column (_column_noise)."""
+    sigma = np.asarray(sigma, dtype=np.float64)
+    r = sigma.size
+    g = np.random.Generator(np.random.Philox(seed))
+    U = g.standard_normal((rows, r)) / np.sqrt(rows)
+    V = g.standard_normal((n_snapshots, r)) / np.sqrt(n_snapshots)
+    c0, c1 = cols if cols is not None else (0, n_snapshots)
+    out = U @ (sigma[:, None] * V[c0:c1].T)
+    out += noise * _column_noise(rows, c0, c1, seed)
+    return np.asfortranarray(out)
+
+
+def weak_scaling_matrix(rows, n_snapshots=4096, cols=None):
+    """Config 4: rank-200 signal, sigma_i = i^-1.5 (i = 1..200), noise 1e-4, seed 2."""
+    return factor_matrix(rows, n_snapshots, np.arange(1, 201, dtype=np.float64) ** -1.5, 1e-4, 2, cols)
+
+
+def stress_matrix(rows, n_snapshots=2048, cols=None):
+    """Config 5: sigma_i = 1 / (1 + 0.01 i) for i < 512, noise 1e-6, seed 3."""
+    return factor_matrix(rows, n_snapshots, 1.0 / (1.0 + 0.01 * np.arange(512, dtype=np.float64)), 1e-6, 3, cols)

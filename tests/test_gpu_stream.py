@@ -348,3 +348,61 @@ def test_randomized_validation():
         p.low_rank_svd(np.eye(4), p.RandomSketchConfig(target_rank=3, oversampling=2))
     with pytest.raises(ValueError):
         p.StreamConfig(k_modes=4, sketch=p.RandomSketchConfig(target_rank=3))
+
+
+# ---------------------------------------------------------------- builder-defined configs 3-5
+# at reduced rows against the oracle; the shapes (K, B, p) are the configs' own.
+
+def _gap_mask(ref_s, thresh=1e-3):
+    gaps = np.minimum(np.abs(np.diff(np.r_[np.inf, ref_s])), np.abs(np.diff(np.r_[ref_s, 0.0]))) / ref_s
+    return gaps >= thresh
+
+
+def _config_parity(a, K, B, ff, sketch=None, q=1):
+    p = _pkg()
+    batches = _batches(a, B)
+    sk = None if sketch is None else p.RandomSketchConfig(target_rank=K, oversampling=sketch, power_iterations=q,
+                                                           seed=0)
+    st, hist = p.stream_all(batches, p.StreamConfig(k_modes=K, forget_factor=ff, batch_columns=B, sketch=sk))
+    if sketch is None:
+        rm, rs, rh = oracle.ref_stream_all(batches, K, ff)
+    else:
+        rm, rs, rh = oracle.ref_rand_stream_all(batches, K, ff, sketch, q, 0)
+    m, s = _np(st)
+    assert oracle.sigma_rel_err(s, rs) <= SIG_TOL
+    ang = oracle.mode_angles(m, rm)
+    mask = _gap_mask(rs)  # per-mode angles are defined for modes with relative gap >= 1e-3
+    assert mask.sum() >= K // 2
+    assert np.max(ang[mask]) <= ANG_TOL, ang
+    assert oracle.sine_angles(m, rm).max() <= 1e-6  # whole-subspace angle
+    for h, r in zip(hist, rh):
+        assert oracle.sigma_rel_err(h.cpu().numpy(), r) <= SIG_TOL
+
+
+def test_config5_stress_deterministic():
+    from paper_2108_08845_b200 import datagen as dg
+    _config_parity(dg.stress_matrix(1 << 14, 512), K=64, B=128, ff=1.0)
+
+
+def test_config3_weather_randomized_wide():
+    from paper_2108_08845_b200 import datagen as dg
+    _config_parity(dg.weather_matrix(512, nlat=91, nlon=180), K=50, B=256, ff=0.95, sketch=10)
+
+
+def test_config4_weak_randomized_wide():
+    from paper_2108_08845_b200 import datagen as dg
+    _config_parity(dg.weak_scaling_matrix(1 << 13, 1024), K=100, B=512, ff=0.95, sketch=10)
+
+
+def test_wide_randomized_route_matches_fused(monkeypatch):
+    """The tall-skinny GEMM route (forced) and the fused passes agree to rounding."""
+    p = _pkg()
+    a = oracle.burgers_matrix(20000, 400)
+    cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200,
+                         sketch=p.RandomSketchConfig(target_rank=10, oversampling=10, power_iterations=1, seed=0))
+    s1, _ = p.stream_all(_batches(a, 200), cfg)
+    monkeypatch.setenv("PSVD_FORCE_WIDE", "1")
+    s2, _ = p.stream_all(_batches(a, 200), cfg)
+    m1, g1 = _np(s1)
+    m2, g2 = _np(s2)
+    _assert_parity(m2, g2, m1, g1, sig_tol=1e-13, ang_tol=1e-11)
