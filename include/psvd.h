@@ -57,6 +57,18 @@ const char* psvd_last_error(psvd_ctx* ctx);
  * branch (tests). */
 int psvd_set_drift_tol(psvd_ctx* ctx, double tol);
 
+/* Row-partitioned randomized update: collective hooks the
+ * library calls, in stream order on `stream`, at the exchange points of
+ * psvd_rand_update — allreduce (sum in rank order, in place) of Y^T Y (l x l),
+ * (Y T)^T (Y T) (l x l) and D P^T Y (n x l), and an allgather of the per-rank
+ * (value, global row) argmax pairs (K x 2) for the tall sign rule.  row_offset
+ * is the global index of this rank's first row.  Pass NULL hooks to go back to
+ * the single-GPU update.  The hooks return 0 on success. */
+typedef int (*psvd_allreduce_fn)(void* user, double* buf, int64_t count, void* stream);
+typedef int (*psvd_allgather_fn)(void* user, const double* send, int64_t count, double* recv, void* stream);
+int psvd_set_exchange(psvd_ctx* ctx, psvd_allreduce_fn allreduce, psvd_allgather_fn allgather, void* user,
+                      int nranks, int64_t row_offset);
+
 /* Number of kernels this context has enqueued so far (launch accounting). */
 long long psvd_launch_count(psvd_ctx* ctx);
 

@@ -38,6 +38,7 @@ _SIGS = {
     "psvd_last_error": (ctypes.c_char_p, [_vp]),
     "psvd_launch_count": (ctypes.c_longlong, [_vp]),
     "psvd_set_drift_tol": (_c_int, [_vp, _c_dbl]),
+    "psvd_set_exchange": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_i64]),
     "psvd_eig_phase_cycles": (_c_int, [_vp, ctypes.POINTER(ctypes.c_longlong)]),
     "psvd_read_status": (_c_int, [_vp, ctypes.POINTER(_c_int), _c_int, _vp]),
     "psvd_gram": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_int, _vp, _c_i64, _c_int, _vp, _vp]),
@@ -229,6 +230,24 @@ def to_host_colmajor(t, pinned=True):
     host = torch.empty((n, m), dtype=t.dtype, pin_memory=pinned)
     host.copy_(src)
     return host.T
+
+
+# collective hooks of psvd_set_exchange (include/psvd.h)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(_c_int, _vp, _vp, _c_i64, _vp)
+ALLGATHER_FN = ctypes.CFUNCTYPE(_c_int, _vp, _vp, _c_i64, _vp, _vp)
+
+
+class _CudaBuffer:
+    """Zero-copy view of a raw device pointer (for torch.as_tensor)."""
+
+    def __init__(self, ptr, count):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def wrap_device(ptr, count, device):
+    """fp64 CUDA tensor aliasing `count` doubles at device pointer `ptr`."""
+    return torch.as_tensor(_CudaBuffer(ptr, count), device=device)
 
 
 _COPY_STREAMS = {}

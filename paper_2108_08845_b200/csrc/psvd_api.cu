@@ -40,6 +40,12 @@ struct psvd_ctx {
   Buf partial, tiles, gram, eigws, wbuf, utu, tbuf, dvec, colmax;
   Buf ybuf, rsmall, jacws;  // randomized path: sketch Y (M x l), small matrices, Jacobi scratch
   Buf ybuf2;                // wide randomized path: second sketch buffer (Y T1 out of place)
+  Buf xpairs;               // row-partitioned sign rule: local and gathered argmax pairs
+  psvd_allreduce_fn ex_allreduce = nullptr;  // row-partitioned randomized update (psvd_set_exchange)
+  psvd_allgather_fn ex_allgather = nullptr;
+  void* ex_user = nullptr;
+  int ex_nranks = 1;
+  int64_t ex_row_offset = 0;
   Buf partial2, tiles2[2];  // A^T A passes on the low-priority stream (double-buffered tiles)
   cudaStream_t s_hi = nullptr, s_lo = nullptr;  // pipelined stream_run: critical chain / look-ahead Grams
   cudaStream_t s_aux = nullptr;                  // concurrent LDL^T of the split core solve
@@ -488,7 +494,7 @@ int psvd_destroy(psvd_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   Buf* bufs[] = {&c->partial, &c->tiles, &c->gram, &c->eigws, &c->wbuf, &c->utu, &c->tbuf, &c->dvec, &c->colmax,
-                 &c->ybuf, &c->ybuf2, &c->rsmall, &c->jacws, &c->partial2, &c->tiles2[0], &c->tiles2[1]};
+                 &c->ybuf, &c->ybuf2, &c->xpairs, &c->rsmall, &c->jacws, &c->partial2, &c->tiles2[0], &c->tiles2[1]};
   for (Buf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
   if (c->s_hi) cudaStreamDestroy(c->s_hi);
@@ -513,6 +519,19 @@ int psvd_destroy(psvd_ctx* c) {
 const char* psvd_last_error(psvd_ctx* c) { return c ? c->err.c_str() : "null context"; }
 
 long long psvd_launch_count(psvd_ctx* c) { return c ? c->launches : -1; }
+
+int psvd_set_exchange(psvd_ctx* c, psvd_allreduce_fn allreduce, psvd_allgather_fn allgather, void* user, int nranks,
+                      int64_t row_offset) {
+  if (!c) return PSVD_EINVAL;
+  if ((allreduce == nullptr) != (allgather == nullptr) || nranks < 1 || row_offset < 0)
+    return fail(c, PSVD_EINVAL, "bad exchange hooks");
+  c->ex_allreduce = allreduce;
+  c->ex_allgather = allgather;
+  c->ex_user = user;
+  c->ex_nranks = allreduce ? nranks : 1;
+  c->ex_row_offset = allreduce ? row_offset : 0;
+  return PSVD_OK;
+}
 
 int psvd_set_drift_tol(psvd_ctx* c, double tol) {
   if (!c) return PSVD_EINVAL;
@@ -674,6 +693,32 @@ int psvd_stream_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, con
 
 // SVQB orthonormalizer of a sketch Gram: T = V diag(1/sqrt(lambda)) with numerically
 // null directions (sigma below rank_tol * sigma_max) dropped (zero columns).
+// exchange points of the row-partitioned randomized update (no-ops on one GPU)
+static int ex_allreduce(psvd_ctx* c, double* buf, int64_t count, cudaStream_t st) {
+  if (!c->ex_allreduce) return PSVD_OK;
+  if (c->ex_allreduce(c->ex_user, buf, count, (void*)st) != 0) return fail(c, PSVD_ECUDA, "allreduce hook failed");
+  return PSVD_OK;
+}
+
+// sign rule over ranks: local per-chunk pairs -> one pair per column -> allgather -> sign
+static int exchange_sign(psvd_ctx* c, const double* local_pairs, int nchunks, int K, double* sgn, cudaStream_t st) {
+  if (!c->ex_allgather) {
+    launch_colmax_sign(local_pairs, nchunks, K, sgn, st);
+    c->launches++;
+    return PSVD_OK;
+  }
+  int rc;
+  if ((rc = ensure(c, c->xpairs, sizeof(double) * (size_t)(c->ex_nranks + 1) * K * 2))) return rc;
+  double* mine = (double*)c->xpairs.ptr;
+  double* all = mine + (size_t)K * 2;
+  launch_colmax_reduce(local_pairs, nchunks, K, mine, st);
+  if (c->ex_allgather(c->ex_user, mine, (int64_t)K * 2, all, (void*)st) != 0)
+    return fail(c, PSVD_ECUDA, "allgather hook failed");
+  launch_colmax_sign(all, c->ex_nranks, K, sgn, st);  // rank order = global row order: first rank wins ties
+  c->launches += 2;
+  return PSVD_OK;
+}
+
 static int svqb(psvd_ctx* c, const double* Gs, int l, double* T, double* sig_scratch, cudaStream_t st) {
   int rc = ensure(c, c->eigws, sizeof(double) * eig_workspace_doubles(l, l));
   if (rc) return rc;
@@ -749,11 +794,13 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
       launch_tgemm_nn(M, gp.data(), (int)gp.size(), W0, n, l, Y, ldy, st);           // Y = P W0
       launch_tgemm_tn(M, &gy, 1, Y, ldy, l, nullptr, G1, l, pbuf, c->num_sms, st);    // G1 = Y^T Y
       c->launches += 3;
+      if ((rc = ex_allreduce(c, G1, (int64_t)l * l, st))) return rc;
       if ((rc = svqb(c, G1, l, T1, sscr, st))) return rc;
       launch_tgemm_nn(M, &gy, 1, T1, l, l, Y2, ldy, st);                              // Y1 = Y T1
       launch_tgemm_tn(M, &gy2, 1, Y2, ldy, l, nullptr, G2, l, pbuf, c->num_sms, st);  // G2 = Y1^T Y1
       launch_tgemm_tn(M, gp.data(), (int)gp.size(), Y2, ldy, l, d, X, n, pbuf, c->num_sms, st);  // X = D P^T Y1
       c->launches += 5;
+      if ((rc = ex_allreduce(c, G2, (int64_t)l * l, st)) || (rc = ex_allreduce(c, X, (int64_t)n * l, st))) return rc;
       launch_chol_inv(G2, l, T2, st);
       launch_small_gemm(X, n, 0, T2, l, (it < q) ? Z : Bt, n, n, l, l, nullptr, st);
       c->launches += 2;
@@ -774,11 +821,11 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
     launch_tgemm_nn(M, &gy2, 1, Wf, l, K, U_out, ldo, st);  // U = Y1 (T2 U_B[:, :K])
     const int64_t nch = colmax_rows_chunks(M);
     if ((rc = ensure(c, c->colmax, sizeof(double) * (size_t)nch * K * 2))) return rc;
-    launch_colmax_rows(U_out, ldo, M, K, 0, (double*)c->colmax.ptr, st);
-    launch_colmax_sign((const double*)c->colmax.ptr, (int)nch, K, sgn, st);
+    launch_colmax_rows(U_out, ldo, M, K, c->ex_row_offset, (double*)c->colmax.ptr, st);
+    if ((rc = exchange_sign(c, (const double*)c->colmax.ptr, (int)nch, K, sgn, st))) return rc;
     launch_scale_cols(U_out, ldo, M, K, sgn, st);
     cudaMemcpyAsync(sigma_out, S, sizeof(double) * K, cudaMemcpyDeviceToDevice, st);
-    c->launches += 6;
+    c->launches += 5;
     return cuda_check(c, "randomized update (wide)");
   }
   for (int it = 0; it <= q; ++it) {
@@ -790,6 +837,7 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
     if ((rc = run_pass(c, ps, st))) return rc;
     launch_extract_sym((const double*)c->tiles.ptr, ps.NB, ps.p.np_pad, l, nullptr, G1, st);
     c->launches++;
+    if ((rc = ex_allreduce(c, G1, (int64_t)l * l, st))) return rc;
     if ((rc = svqb(c, G1, l, T1, sscr, st))) return rc;
     // pass B: Y <- Y T1 (in place), (Y^T Y, D P^T Y)
     Pass pb_;
@@ -800,6 +848,7 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
     launch_extract_sym((const double*)c->tiles.ptr, pb_.NB, pb_.p.np_pad, l, nullptr, G2, st);
     launch_extract_rect((const double*)c->tiles.ptr, pb_.NB, 0, n, pb_.p.np_pad, l, d, X, st);
     c->launches += 2;
+    if ((rc = ex_allreduce(c, G2, (int64_t)l * l, st)) || (rc = ex_allreduce(c, X, (int64_t)n * l, st))) return rc;
     launch_chol_inv(G2, l, T2, st);  // refinement pass: G2 ~ I, Cholesky is exact enough
     c->launches++;
     // Z = C^T Q = (D P^T Y1) T2 = X T2  (= B^T after the last iteration)
@@ -830,11 +879,12 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
   pc.p.Yout = U_out;
   pc.p.ldy = ldo;
   pc.p.colmax = (double*)c->colmax.ptr;
+  pc.p.row_offset = c->ex_row_offset;
   if ((rc = run_pass(c, pc, st))) return rc;
-  launch_colmax_sign((const double*)c->colmax.ptr, nchunks, K, sgn, st);
+  if ((rc = exchange_sign(c, (const double*)c->colmax.ptr, nchunks, K, sgn, st))) return rc;
   launch_scale_cols(U_out, ldo, M, K, sgn, st);
   cudaMemcpyAsync(sigma_out, S, sizeof(double) * K, cudaMemcpyDeviceToDevice, st);
-  c->launches += 2;
+  c->launches += 1;
   return cuda_check(c, "randomized update");
 }
 

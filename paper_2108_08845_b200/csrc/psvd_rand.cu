@@ -213,6 +213,27 @@ __global__ void colmax_sign_kernel(const double* __restrict__ colmax, int nchunk
   sign[k] = val < 0.0 ? -1.0 : 1.0;  // applied with scale_cols (multiplies by +-1)
 }
 
+// one (value, row) pair per column from the per-chunk pairs (first chunk wins ties)
+__global__ void colmax_reduce_kernel(const double* __restrict__ colmax, int nchunks, int K, double* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  double best = -1.0, val = 0.0, row = -1.0;
+  for (int c = 0; c < nchunks; ++c) {
+    const double v = colmax[((size_t)c * K + k) * 2];
+    if (fabs(v) > best) {
+      best = fabs(v);
+      val = v;
+      row = colmax[((size_t)c * K + k) * 2 + 1];
+    }
+  }
+  out[(size_t)k * 2] = val;
+  out[(size_t)k * 2 + 1] = row;
+}
+
+void launch_colmax_reduce(const double* colmax, int nchunks, int K, double* out, cudaStream_t st) {
+  colmax_reduce_kernel<<<(K + 127) / 128, 128, 0, st>>>(colmax, nchunks, K, out);
+}
+
 void launch_colmax_sign(const double* colmax, int nchunks, int K, double* sign, cudaStream_t st) {
   colmax_sign_kernel<<<(K + 127) / 128, 128, 0, st>>>(colmax, nchunks, K, sign);
 }

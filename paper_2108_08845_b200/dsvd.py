@@ -15,10 +15,17 @@ Here (one process per GPU, torch.distributed over NCCL):
 Two small collectives per update (n*n*8 = 353 KB at n = 210, K*K*8) replace
 gather + P-1 sends + broadcast.  Like the reference there is no drift rescue
 on this path (dsvd.py:220-242).
+
+With `config.sketch` set the update is the randomized one with the
+row-partitioned exchange of §8(e): the library calls back (psvd_set_exchange)
+for the rank-ordered sums of Y^T Y, (Y T)^T (Y T) and D P^T Y and for the
+allgather of the per-rank argmax pairs of the tall sign rule; Omega is the
+replicated host draw, so every rank runs the identical small factorizations.
 """
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import torch
@@ -71,6 +78,86 @@ def allreduce_ordered(t, ctx):
     return out
 
 
+class _Exchange:
+    """ctypes hooks (psvd_set_exchange) running the rank-ordered allreduce / the
+    allgather on this RankContext, ordered on the library's stream."""
+
+    def __init__(self, ctx, dev):
+        self.ctx, self.dev = ctx, dev
+        self.error = None
+        self.ar = nat.ALLREDUCE_FN(self._allreduce)
+        self.ag = nat.ALLGATHER_FN(self._allgather)
+
+    def _stream(self, stream):
+        if not stream:  # the legacy default stream
+            return torch.cuda.default_stream(self.dev)
+        return torch.cuda.ExternalStream(stream, device=self.dev)
+
+    def _device_collectives(self):
+        return dist.get_backend(self.ctx.group) == "nccl"
+
+    def _allreduce(self, user, ptr, count, stream):
+        try:
+            t = nat.wrap_device(ptr, count, self.dev)
+            with torch.cuda.stream(self._stream(stream)):
+                if self._device_collectives():
+                    t.copy_(allreduce_ordered(t, self.ctx))
+                else:  # gloo: stage through the host (blocking copies keep the stream order)
+                    t.copy_(allreduce_ordered(t.cpu(), self.ctx).to(self.dev))
+            return 0
+        except Exception as e:  # noqa: BLE001 - reported through the return code
+            self.error = e
+            return 1
+
+    def _allgather(self, user, send, count, recv, stream):
+        try:
+            src = nat.wrap_device(send, count, self.dev)
+            dst = nat.wrap_device(recv, count * self.ctx.world_size, self.dev)
+            with torch.cuda.stream(self._stream(stream)):
+                if self._device_collectives():
+                    dist.all_gather_into_tensor(dst, src, group=self.ctx.group)
+                else:
+                    parts = [torch.empty(int(count), dtype=torch.float64) for _ in range(self.ctx.world_size)]
+                    dist.all_gather(parts, src.cpu(), group=self.ctx.group)
+                    dst.copy_(torch.cat(parts).to(self.dev))
+            return 0
+        except Exception as e:  # noqa: BLE001
+            self.error = e
+            return 1
+
+
+def _row_offset(ctx, rows, dev):
+    """Global index of this rank's first row (prefix sum of the local row counts)."""
+    if ctx.world_size == 1:
+        return 0, rows
+    t = torch.tensor([rows], dtype=torch.int64,
+                     device=dev if dist.get_backend(ctx.group) == "nccl" else "cpu")
+    parts = [torch.zeros_like(t) for _ in range(ctx.world_size)]
+    dist.all_gather(parts, t, group=ctx.group)
+    counts = [int(x.item()) for x in parts]
+    return sum(counts[:ctx.rank]), sum(counts)
+
+
+def _parallel_rand_update(ctx, U, sigma, A, sketch, ff, dev):
+    from .linalg import randomized_update
+    c = nat.context(dev)
+    off, total = _row_offset(ctx, A.rows, dev)
+    if ctx.world_size == 1:
+        return randomized_update(U, sigma, A, sketch, ff, dev)
+    ex = _Exchange(ctx, dev)
+    nat.call("psvd_set_exchange", c, ctypes.cast(ex.ar, nat._vp), ctypes.cast(ex.ag, nat._vp), None,
+             ctx.world_size, off)
+    try:
+        out = randomized_update(U, sigma, A, sketch, ff, dev, total_rows=total)
+    except RuntimeError:
+        if ex.error is not None:
+            raise ex.error
+        raise
+    finally:
+        nat.call("psvd_set_exchange", c, None, None, None, 1, 0)
+    return out
+
+
 def _parallel_update(ctx, U, sigma, A, k, ff, dev):
     c = nat.context(dev)
     with torch.cuda.device(dev):
@@ -113,7 +200,10 @@ def parallel_stream_initialize(ctx, a0_local, config):
     k = config.k_modes
     if A.cols < k:
         raise ValueError(f"initial batch has {A.cols} columns, need at least k_modes={k}")
-    out, sig = _parallel_update(ctx, None, None, A, k, config.forget_factor, dev)
+    if config.sketch is not None:
+        out, sig = _parallel_rand_update(ctx, None, None, A, config.sketch, config.forget_factor, dev)
+    else:
+        out, sig = _parallel_update(ctx, None, None, A, k, config.forget_factor, dev)
     return LocalModes(out.view, sig)
 
 
@@ -128,7 +218,10 @@ def parallel_stream_incorporate(ctx, state, a_new_local, config):
         raise ValueError(f"batch rows {A.rows} != mode rows {state.modes.shape[0]}")
     U = nat.as_device_colmajor(state.modes, dev, "modes")
     sigma = nat.as_device_vector(state.singular_values, dev, k, "singular_values")
-    out, sig = _parallel_update(ctx, U, sigma, A, k, config.forget_factor, dev)
+    if config.sketch is not None:
+        out, sig = _parallel_rand_update(ctx, U, sigma, A, config.sketch, config.forget_factor, dev)
+    else:
+        out, sig = _parallel_update(ctx, U, sigma, A, k, config.forget_factor, dev)
     return LocalModes(out.view, sig)
 
 

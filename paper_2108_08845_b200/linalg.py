@@ -64,9 +64,10 @@ def device_omega(n_cols, config, device):
     return om
 
 
-def randomized_update(U, sigma, A, sketch, ff, device, check=True):
+def randomized_update(U, sigma, A, sketch, ff, device, check=True, total_rows=None):
     """One randomized step: low_rank_svd([ff*U*diag(sigma) | A], sketch) on the
     device (linalg.py:150-162 composed per batch).  U: DevMat or None.
+    total_rows: rows of the whole (row-partitioned) panel for the width check.
     Returns (DevMat M x K, sigma (K,))."""
     import torch
     from . import _native as nat
@@ -74,8 +75,9 @@ def randomized_update(U, sigma, A, sketch, ff, device, check=True):
     M, B = A.rows, A.cols
     kc = 0 if U is None else U.cols
     n = kc + B
-    if l > min(M, n):
-        raise ValueError(f"sketch width {l} exceeds min(a.shape) = {min(M, n)}")
+    rows = M if total_rows is None else total_rows
+    if l > min(rows, n):
+        raise ValueError(f"sketch width {l} exceeds min(a.shape) = {min(rows, n)}")
     om = device_omega(n, sketch, device)
     ctx = nat.context(device)
     with torch.cuda.device(device):

@@ -34,6 +34,9 @@ def _worker(rank, world, port, q):
 
         ctx = RankContext()
         assert (ctx.rank, ctx.world_size) == (rank, world)
+        from paper_2108_08845_b200.dsvd import _row_offset
+        # global row offset of the randomized exchange (argmax rows are global)
+        assert _row_offset(ctx, 100 + rank, "cpu") == (sum(100 + r for r in range(rank)), sum(100 + r for r in range(world)))
         a = oracle.burgers_matrix(2048, 800)
         lo, hi = partition_bounds(a.shape[0], world)[rank]
         k, ff = 10, 0.95

@@ -406,3 +406,66 @@ def test_wide_randomized_route_matches_fused(monkeypatch):
     m1, g1 = _np(s1)
     m2, g2 = _np(s2)
     _assert_parity(m2, g2, m1, g1, sig_tol=1e-13, ang_tol=1e-11)
+
+
+def _rand_rank_worker(rank, world, port, q):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2108_08845_b200 as p
+        a = oracle.burgers_matrix(6001, 600)
+        lo, hi = p.partition_bounds(a.shape[0], world)[rank]
+        cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200,
+                             sketch=p.RandomSketchConfig(target_rank=10, oversampling=10, power_iterations=1, seed=0))
+        ctx = p.RankContext()
+        st = p.parallel_stream_initialize(ctx, a[lo:hi, :200], cfg)
+        for c0 in (200, 400):
+            st = p.parallel_stream_incorporate(ctx, st, a[lo:hi, c0:c0 + 200], cfg)
+        full = p.gather_modes(ctx, st)
+        if rank == 0:
+            q.put((full.cpu().numpy(), st.singular_values.cpu().numpy()))
+    except Exception as e:  # report instead of leaving the parent waiting
+        q.put(("error", repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_parallel_randomized_two_ranks_match_serial_oracle():
+    """Row-partitioned randomized stream (§8(e)): two ranks (two processes sharing this
+    GPU, gloo host-staged exchange through the library's collective hooks) reproduce
+    the serial R9 composition on the whole matrix."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rand_rank_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    m, s_ = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=120)
+    assert not (isinstance(m, str) and m == "error"), s_
+    assert all(pr.exitcode == 0 for pr in procs)
+    a = oracle.burgers_matrix(6001, 600)
+    rm, rs, _ = oracle.ref_rand_stream_all(_batches(a, 200), 10, 0.95, 10, 1, 0)
+    _assert_parity(m, s_, rm, rs)
+
+
+def test_parallel_randomized_single_rank_is_serial():
+    p = _pkg()
+    a = oracle.burgers_matrix(4096, 400)
+    cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200,
+                         sketch=p.RandomSketchConfig(target_rank=10, oversampling=10, power_iterations=1, seed=0))
+    ctx = p.RankContext()
+    st = p.parallel_stream_initialize(ctx, a[:, :200], cfg)
+    st = p.parallel_stream_incorporate(ctx, st, a[:, 200:], cfg)
+    ser = p.stream_incorporate(p.stream_initialize(a[:, :200], cfg), a[:, 200:], cfg)
+    assert torch.equal(st.modes, ser.modes) and torch.equal(st.singular_values, ser.singular_values)
