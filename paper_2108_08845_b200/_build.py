@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libpsvd.so")
-SOURCES = ["psvd_tall.cu", "psvd_pass_tma.cu", "psvd_gemm.cu", "psvd_small.cu", "psvd_rand.cu", "psvd_api.cu"]
+SOURCES = ["psvd_tall.cu", "psvd_pass_tma.cu", "psvd_gemm.cu", "psvd_small.cu", "psvd_subspace.cu", "psvd_rand.cu", "psvd_api.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 

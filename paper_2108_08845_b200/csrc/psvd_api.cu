@@ -41,6 +41,8 @@ struct psvd_ctx {
   Buf ybuf, rsmall, jacws;  // randomized path: sketch Y (M x l), small matrices, Jacobi scratch
   Buf ybuf2;                // wide randomized path: second sketch buffer (Y T1 out of place)
   Buf xpairs;               // row-partitioned sign rule: local and gathered argmax pairs
+  Buf ssws;                 // subspace-iteration core solve: Q, W, H, eig(H) scratch
+  int* d_ssgate = nullptr;  // 1: the subspace path did not converge, run the full solver
   psvd_allreduce_fn ex_allreduce = nullptr;  // row-partitioned randomized update (psvd_set_exchange)
   psvd_allgather_fn ex_allgather = nullptr;
   void* ex_user = nullptr;
@@ -457,17 +459,18 @@ int psvd_create(int device, psvd_ctx** out) {
   psvd_ctx* c = new psvd_ctx();
   c->device = device;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
-  if (cudaMalloc(&c->d_status, 2 * sizeof(int)) != cudaSuccess || cudaMallocHost(&c->h_status, sizeof(int)) != cudaSuccess) {
+  if (cudaMalloc(&c->d_status, 4 * sizeof(int)) != cudaSuccess || cudaMallocHost(&c->h_status, sizeof(int)) != cudaSuccess) {
     cudaGetLastError();
     delete c;
     return PSVD_ECUDA;
   }
   c->d_gate = c->d_status + 1;
+  c->d_ssgate = c->d_status + 2;
   if (cudaMalloc(&c->d_timers, 16 * sizeof(long long)) != cudaSuccess) {
     cudaGetLastError();
     return PSVD_ECUDA;
   }
-  cudaMemset(c->d_status, 0, 2 * sizeof(int));
+  cudaMemset(c->d_status, 0, 4 * sizeof(int));
   {
     int lo = 0, hi = 0;
     cudaDeviceGetStreamPriorityRange(&lo, &hi);  // numerically: hi <= lo (smaller = higher priority)
@@ -494,7 +497,7 @@ int psvd_destroy(psvd_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   Buf* bufs[] = {&c->partial, &c->tiles, &c->gram, &c->eigws, &c->wbuf, &c->utu, &c->tbuf, &c->dvec, &c->colmax,
-                 &c->ybuf, &c->ybuf2, &c->xpairs, &c->rsmall, &c->jacws, &c->partial2, &c->tiles2[0], &c->tiles2[1]};
+                 &c->ybuf, &c->ybuf2, &c->xpairs, &c->ssws, &c->rsmall, &c->jacws, &c->partial2, &c->tiles2[0], &c->tiles2[1]};
   for (Buf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
   if (c->s_hi) cudaStreamDestroy(c->s_hi);
@@ -645,7 +648,16 @@ static int core_solve(psvd_ctx* c, const double* G, int n, int K, const double* 
     cudaStreamWaitEvent(c->s_aux, c->ev_ldlt_fork, 0);
     launch_ldlt_pack(G, n, ws, c->s_aux);  // packed L in the (unused in smem mode) first n(n+1)/2 doubles
     cudaEventRecord(c->ev_ldlt_join, c->s_aux);
-    launch_eig_topk(G, n, K, dscale, W, sigma, ws, c->d_status, nullptr, st, 0.0, 1);
+    static const bool no_ss = getenv("PSVD_NO_SUBSPACE") != nullptr;
+    if (!no_ss && subspace_supported(n, K)) {
+      // subspace-iteration fast path; the full solver below is gated off when it converged
+      if ((rc = ensure(c, c->ssws, sizeof(double) * subspace_workspace_doubles(n)))) return rc;
+      launch_subspace_eig(G, n, K, (double*)c->ssws.ptr, ws + (size_t)n * (n + 1) / 2, sigma, c->d_ssgate, st);
+      launch_eig_topk(G, n, K, dscale, W, sigma, ws, c->d_status, nullptr, st, 0.0, 1, c->d_ssgate);
+      c->launches += 4;
+    } else {
+      launch_eig_topk(G, n, K, dscale, W, sigma, ws, c->d_status, nullptr, st, 0.0, 1);
+    }
     cudaStreamWaitEvent(st, c->ev_ldlt_join, 0);
     launch_sign_weights(ws, ws + (size_t)n * (n + 1) / 2, sigma, n, K, dscale, W, sigma, c->d_status, 0.0, st);
     c->launches += 3;

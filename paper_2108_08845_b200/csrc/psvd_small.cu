@@ -168,7 +168,9 @@ template <bool SMEM, bool FAST>
 __global__ void __launch_bounds__(FAST ? EIG_FAST_THREADS : SMALL_THREADS, 1)
 eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __restrict__ dscale,
                 double* __restrict__ W, double* __restrict__ sigma_out, double* __restrict__ ws,
-                int* __restrict__ status, long long* __restrict__ timers, double rank_tol, int split) {
+                int* __restrict__ status, long long* __restrict__ timers, double rank_tol, int split,
+                const int* __restrict__ gate) {
+  if (gate != nullptr && *gate == 0) return;  // the subspace fast path already converged
   extern __shared__ double sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nthr = blockDim.x, nwarps = nthr >> 5;
@@ -312,17 +314,20 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
         for (int t = 0; t < NT; ++t) {
           if (32 * t + 31 < c) continue;  // warp-uniform: whole slot above the diagonal
           const int r = lane + 32 * t;
-          if (r >= c && r < n) {
-            const double x = Lp[base + r] - (vO[t] * wpc + wO[t] * vpc);
-            Lp[base + r] = x;
-            yp[t] = fma(x, vnc, yp[t]);
-            if (r > c) dot = fma(x, vN[t], dot);
-          }
-          if (has1 && r >= c1 && r < n) {
-            const double x = Lp[base1 + r] - (vO[t] * wpc1 + wO[t] * vpc1);
-            Lp[base1 + r] = x;
-            yp[t] = fma(x, vnc1, yp[t]);
-            if (r > c1) dot1 = fma(x, vN[t], dot1);
+          // branch-free body: loads from a clamped address, predicated store, masked sums
+          const bool in0 = r >= c && r < n;
+          const int a0 = in0 ? base + r : base + c;
+          const double x = Lp[a0] - (vO[t] * wpc + wO[t] * vpc);
+          if (in0) Lp[a0] = x;
+          yp[t] = fma(in0 ? x : 0.0, vnc, yp[t]);
+          dot = fma(r > c && r < n ? x : 0.0, vN[t], dot);
+          if (has1) {
+            const bool in1 = r >= c1 && r < n;
+            const int a1 = in1 ? base1 + r : base1 + c1s;
+            const double x1 = Lp[a1] - (vO[t] * wpc1 + wO[t] * vpc1);
+            if (in1) Lp[a1] = x1;
+            yp[t] = fma(in1 ? x1 : 0.0, vnc1, yp[t]);
+            dot1 = fma(r > c1 && r < n ? x1 : 0.0, vN[t], dot1);
           }
         }
 #pragma unroll
@@ -640,8 +645,10 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
           const int r = lane + 32 * t;
-          if (32 * t + 31 < j + 1) { vr[t] = 0.0; continue; }
-          vr[t] = (r == j + 1) ? 1.0 : ((r >= j + 2 && r < n) ? Lp[base + r] : 0.0);
+          if (32 * t + 31 < j + 1) { vr[t] = 0.0; continue; }  // warp-uniform
+          const bool in = r >= j + 2 && r < n;
+          const double lv = Lp[in ? base + r : base + j];     // clamped address, no branch
+          vr[t] = in ? lv : (r == j + 1 ? 1.0 : 0.0);
           s = fma(vr[t], zr[t], s);
         }
         s = warp_sum(s) * tj;
@@ -790,7 +797,8 @@ eig_topk_kernel(const double* __restrict__ G, int n, int K, const double* __rest
 bool eig_supported(int n, int K) { return n >= 1 && K >= 1 && K <= n && K <= 1024; }
 
 void launch_eig_topk(const double* G, int n, int K, const double* dscale, double* W, double* sigma,
-                     double* ws, int* status, long long* timers, cudaStream_t st, double rank_tol, int split) {
+                     double* ws, int* status, long long* timers, cudaStream_t st, double rank_tol, int split,
+                     const int* gate) {
   const int npad = (n + 31) / 32 * 32;
   const size_t vec = (size_t)6 * n + K + 64 + K + 2;  // ... + clus (K ints) + rsel (K ints)
   const size_t fast_extra = (size_t)(n + 1) / 2 + 1 + 5 * (size_t)npad + (size_t)(EIG_FAST_THREADS / 32) * npad + 8;
@@ -800,17 +808,17 @@ void launch_eig_topk(const double* G, int n, int K, const double* dscale, double
     const size_t smem = (npk + vec + fast_extra) * sizeof(double);
     cudaFuncSetAttribute(eig_topk_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     eig_topk_kernel<true, true><<<1, EIG_FAST_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers,
-                                                                    rank_tol, split);
+                                                                    rank_tol, split, gate);
   } else if (n <= EIG_NMAX_SMEM) {
     const size_t smem = (npk + vec) * sizeof(double);
     cudaFuncSetAttribute(eig_topk_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     eig_topk_kernel<true, false><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers,
-                                                                  rank_tol, 0);
+                                                                  rank_tol, 0, gate);
   } else {
     const size_t smem = vec * sizeof(double);
     cudaFuncSetAttribute(eig_topk_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     eig_topk_kernel<false, false><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers,
-                                                                   rank_tol, 0);
+                                                                   rank_tol, 0, gate);
   }
 }
 

@@ -38,7 +38,21 @@ size_t eig_workspace_doubles(int n, int K);
 // timers (optional, device): clock64() at the 9 phase boundaries (diagnostics).
 void launch_eig_topk(const double* G, int n, int K, const double* dscale, double* W, double* sigma,
                      double* ws, int* status, long long* timers, cudaStream_t st, double rank_tol = 0.0,
-                     int split = 0);
+                     int split = 0, const int* gate = nullptr);
+
+// Subspace-iteration fast path (psvd_subspace.cu): Ritz pairs of G from span(G^2 Q0), block 32.
+// Writes Z (n x K, ld n) and sigma = sqrt(theta) like the split-mode solver and sets *gate = 0
+// when every residual ||G x_k - theta_k x_k|| <= SS_TOL * theta_0, else *gate = 1 (the gated
+// full solver then runs).  ss_ws: subspace_workspace_doubles(n) doubles.
+constexpr int SS_P = 32;
+constexpr int SS_THREADS = 512;
+constexpr int SS_KMAX = 12;
+constexpr int SS_ITERS = 2;
+constexpr double SS_TOL = 2e-14;
+bool subspace_supported(int n, int K);
+size_t subspace_workspace_doubles(int n);
+void launch_subspace_eig(const double* G, int n, int K, double* ss_ws, double* Zout, double* sigma_out, int* gate,
+                         cudaStream_t st);
 // Split core (n <= EIG_FAST_NMAX): eig with split = 1 leaves Z in ws + n(n+1)/2 and sqrt(lambda)
 // in sigma; ldlt_pack (concurrent, needs only G) writes chol(G + delta I) packed to Lout;
 // sign_weights then applies the sign rule and writes W.
