@@ -69,6 +69,11 @@ typedef int (*psvd_allgather_fn)(void* user, const double* send, int64_t count, 
 int psvd_set_exchange(psvd_ctx* ctx, psvd_allreduce_fn allreduce, psvd_allgather_fn allgather, void* user,
                       int nranks, int64_t row_offset);
 
+/* Which core solver produced the last split-mode core solve (diagnostics, syncs the
+ * device): *full = 0 when the subspace-iteration fast path converged, 1 when the
+ * gated full Householder solver ran. */
+int psvd_last_core_path(psvd_ctx* ctx, int* full);
+
 /* Number of kernels this context has enqueued so far (launch accounting). */
 long long psvd_launch_count(psvd_ctx* ctx);
 

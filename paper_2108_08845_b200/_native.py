@@ -39,6 +39,7 @@ _SIGS = {
     "psvd_launch_count": (ctypes.c_longlong, [_vp]),
     "psvd_set_drift_tol": (_c_int, [_vp, _c_dbl]),
     "psvd_set_exchange": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_i64]),
+    "psvd_last_core_path": (_c_int, [_vp, ctypes.POINTER(_c_int)]),
     "psvd_eig_phase_cycles": (_c_int, [_vp, ctypes.POINTER(ctypes.c_longlong)]),
     "psvd_read_status": (_c_int, [_vp, ctypes.POINTER(_c_int), _c_int, _vp]),
     "psvd_gram": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_int, _vp, _c_i64, _c_int, _vp, _vp]),

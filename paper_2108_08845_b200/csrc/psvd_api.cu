@@ -536,6 +536,13 @@ int psvd_set_exchange(psvd_ctx* c, psvd_allreduce_fn allreduce, psvd_allgather_f
   return PSVD_OK;
 }
 
+int psvd_last_core_path(psvd_ctx* c, int* full) {
+  if (!c || !full) return PSVD_EINVAL;
+  if (cudaMemcpy(full, c->d_ssgate, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return cuda_check(c, "core path");
+  return PSVD_OK;
+}
+
 int psvd_set_drift_tol(psvd_ctx* c, double tol) {
   if (!c) return PSVD_EINVAL;
   c->drift_tol = tol;
@@ -656,6 +663,7 @@ static int core_solve(psvd_ctx* c, const double* G, int n, int K, const double* 
       launch_eig_topk(G, n, K, dscale, W, sigma, ws, c->d_status, nullptr, st, 0.0, 1, c->d_ssgate);
       c->launches += 4;
     } else {
+      cudaMemsetAsync(c->d_ssgate, 0xff, sizeof(int), st);  // reads as "full solver"
       launch_eig_topk(G, n, K, dscale, W, sigma, ws, c->d_status, nullptr, st, 0.0, 1);
     }
     cudaStreamWaitEvent(st, c->ev_ldlt_join, 0);

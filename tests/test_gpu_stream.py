@@ -469,3 +469,30 @@ def test_parallel_randomized_single_rank_is_serial():
     st = p.parallel_stream_incorporate(ctx, st, a[:, 200:], cfg)
     ser = p.stream_incorporate(p.stream_initialize(a[:, :200], cfg), a[:, 200:], cfg)
     assert torch.equal(st.modes, ser.modes) and torch.equal(st.singular_values, ser.singular_values)
+
+
+def test_core_solver_paths_both_exercised_and_exact():
+    """The subspace-iteration fast path converges on the low-rank Burgers Gram; on a flat
+    Gaussian spectrum its residual gate fails and the full solver runs.  Both match the oracle."""
+    import ctypes
+    p = _pkg()
+    from paper_2108_08845_b200 import _native as nat
+    dev = torch.device("cuda", 0)
+    c = nat.context(dev)
+    full = ctypes.c_int(-1)
+    a = oracle.burgers_matrix(20000, 400)
+    cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200)
+    st = p.stream_incorporate(p.stream_initialize(a[:, :200], cfg), a[:, 200:], cfg)
+    nat.call("psvd_last_core_path", c, ctypes.byref(full))
+    assert full.value == 0
+    rm, rs, _ = oracle.ref_stream_all(_batches(a, 200), 10, 0.95)
+    m, s = _np(st)
+    _assert_parity(m, s, rm, rs)
+    rng = np.random.default_rng(5)
+    g = rng.standard_normal((3000, 400))
+    st = p.stream_incorporate(p.stream_initialize(g[:, :200], cfg), g[:, 200:], cfg)
+    nat.call("psvd_last_core_path", c, ctypes.byref(full))
+    assert full.value != 0
+    rm, rs, _ = oracle.ref_stream_all(_batches(g, 200), 10, 0.95)
+    m, s = _np(st)
+    _assert_parity(m, s, rm, rs)
