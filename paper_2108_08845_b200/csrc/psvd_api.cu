@@ -112,6 +112,7 @@ struct Pass {
   int NB = 0;
   bool ws = false;      // warp-specialized Gram kernel
   bool tma = false;     // warp-specialized TMA pass (narrow panels)
+  bool gtma = false;    // TMA-fed Gram-only pass
   TmaMaps maps;
   TmaExtra x;
   Buf* part = nullptr;  // partial-tile workspace of the stream this pass runs on
@@ -179,9 +180,9 @@ int plan_tiles(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& ti
 // pipe gets the same number of 8x8 blocks per k-step (warp w issues on SMSP w % 4; a diagonal
 // tile needs 10 of 16 blocks, a tile on the panel's last partial block fewer).  Longest-
 // processing-time greedy; the kernel's pace is the busiest SMSP of the busiest slice.
-static int plan_tiles_balanced(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& tiles, int np) {
+static int plan_tiles_balanced(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& tiles, int np,
+                                int ncons = NWARP - WS_PRODUCERS) {  // the last warps load
   const int nt = (int)tiles.size();
-  const int ncons = NWARP - WS_PRODUCERS;  // the last WS_PRODUCERS warps load
   const int nslices = (nt + ncons - 1) / ncons;
   if (nt > MAX_OUT_TILES || nslices > MAX_SLICES) return fail(c, PSVD_EINVAL, "panel too wide (%d tiles)", nt);
   memset(ps.p.plan, 0, sizeof(ps.p.plan));
@@ -333,9 +334,17 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
   // Gram-only passes with enough tiles run warp-specialized (one producer warp, no k-split)
   ps.ws = (w == 0 && (int)tiles.size() >= 8 &&
            gram_ws_smem_bytes(np_pad, 3) <= (size_t)SMEM_LIMIT);
+  if (ps.ws && !no_tma && tma_available() && gram_tma_smem_bytes(np_pad) <= (size_t)SMEM_LIMIT) {
+    // TMA-fed Gram when every segment already starts on an 8-column boundary
+    bool ok = true;
+    for (int i = 0; i < p.nseg; ++i)
+      ok = ok && (p.seg[i].col0 & 7) == 0 && aligned16(p.seg[i].ptr) && p.seg[i].ld % 2 == 0 && p.seg[i].ncols > 0;
+    ps.gtma = ok;
+  }
   ps.tma = tma;
   if (tma) p.narrow = 1;
   int rc = tma ? plan_tiles_tma(c, ps, tiles)
+               : ps.gtma ? plan_tiles_balanced(c, ps, tiles, np, TMA_GRAM_CONS)
                : ps.ws ? plan_tiles_balanced(c, ps, tiles, np) : plan_tiles(c, ps, tiles, w == 0);
   {
     static const char* dbg = getenv("PSVD_GRAM_DBG");
@@ -359,13 +368,16 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
     if (rc2) return rc2;
     p.partial = (double*)ps.part->ptr;
   }
-  if (tma && tma_pass_prepare(p, ps.maps, ps.x) != 0) return fail(c, PSVD_ECUDA, "TMA descriptor setup failed");
+  if ((tma || ps.gtma) && tma_pass_prepare(p, ps.maps, ps.x) != 0)
+    return fail(c, PSVD_ECUDA, "TMA descriptor setup failed");
   return PSVD_OK;
 }
 
 int run_pass(psvd_ctx* c, Pass& ps, cudaStream_t st) {
   if (ps.tma)
     launch_pass_tma(ps.p, ps.maps, ps.x, ps.grid, st);
+  else if (ps.gtma)
+    launch_gram_tma(ps.p, ps.maps, ps.x, ps.grid, st);
   else if (ps.ws)
     launch_gram_ws(ps.p, ps.grid, st);
   else
@@ -988,7 +1000,9 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
         first = pa;
       }
       pa.p.partial = (double*)c->partial2.ptr + part_off;
-      if (pa.ws)
+      if (pa.gtma)
+        launch_gram_tma(pa.p, pa.maps, pa.x, pa.grid, lo);
+      else if (pa.ws)
         launch_gram_ws(pa.p, pa.grid, lo);
       else
         launch_tall(pa.p, pa.grid, lo);

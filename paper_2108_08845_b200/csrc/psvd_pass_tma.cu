@@ -297,6 +297,140 @@ __global__ void __launch_bounds__(NTHR, 1)
   }
 }
 
+
+// ---------------------------------------------------------------- TMA Gram (w == 0)
+// Gram-only pass fed by TMA: 32-row stages (two 16-row 128B-swizzled boxes per segment)
+// in a GNS-deep ring; warp 15 lane 0 issues the boxes, warps 0..14 each own one 32x32
+// tile (compile-time block shape, as gram_ws_kernel) and never meet at a CTA barrier.
+constexpr int GNS = 3;
+
+size_t gram_tma_smem_bytes(int np_pad) {
+  return 1024 + sizeof(double) * (size_t)GNS * 2 * np_pad * TKS + 2 * GNS * sizeof(uint64_t) + 64;
+}
+
+__global__ void __launch_bounds__(NTHR, 1)
+    gram_tma_kernel(const __grid_constant__ TallParams p, const __grid_constant__ TmaMaps maps, const TmaExtra x) {
+  if (p.gate != nullptr && *p.gate == 0) return;
+  extern __shared__ unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int slice = blockIdx.x % p.nslices;
+  const int64_t chunk = blockIdx.x / p.nslices;
+  const int64_t row_begin = chunk * p.rows_per_cta;
+  const int64_t row_end = min(p.M, row_begin + p.rows_per_cta);
+  const int np_pad = p.np_pad;
+  unsigned char* base = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
+  double* sP = reinterpret_cast<double*>(base);  // [stage][half][np_pad][16]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sP + (size_t)GNS * 2 * np_pad * TKS);
+  uint64_t* empty = full + GNS;
+  int ncons = 0;
+  for (int w = 0; w < PROD_WARP; ++w) ncons += p.plan[slice][w].ntile > 0;
+  for (int i = tid; i < GNS * 2 * np_pad; i += NTHR) {
+    const int c = i % np_pad;
+    if (!x.written[c >> 3]) {
+      double* col = sP + (size_t)i * TKS;
+#pragma unroll
+      for (int k = 0; k < TKS; ++k) col[k] = 0.0;
+    }
+  }
+  if (tid == 0) {
+    for (int b = 0; b < GNS; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], (unsigned)max(ncons, 1));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncthreads();
+  const int64_t nstage = row_end > row_begin ? (row_end - row_begin + 2 * TKS - 1) / (2 * TKS) : 0;
+
+  if (warp == PROD_WARP) {
+    if (lane == 0) {
+      for (int64_t s = 0; s < nstage; ++s) {
+        const int b = (int)(s % GNS);
+        if (s >= GNS) mbar_wait(&empty[b], (unsigned)(((s / GNS) - 1) & 1));
+        mbar_expect_tx(&full[b], 2 * x.stage_bytes);
+        for (int h = 0; h < 2; ++h) {
+          double* dst = sP + ((size_t)b * 2 + h) * np_pad * TKS;
+          const int r0 = (int)(row_begin + s * 2 * TKS + h * TKS);
+          for (int o = 0; o < x.nops; ++o)
+            tma_load_2d(dst + (size_t)x.op_pcol[o] * TKS, &maps.m[x.op_seg[o]], r0, x.op_col[o], &full[b]);
+        }
+      }
+    }
+    return;
+  }
+  const WarpPlan wp = p.plan[slice][warp];
+  if (wp.ntile == 0) return;
+  double acc[4][4][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+  const int I = wp.ti[0], J = wp.tj[0];
+  const int nva = min(4, (p.np - I * 32 + 7) / 8), nvb = min(4, (p.np - J * 32 + 7) / 8);
+  auto stage_loop = [&](auto na_t, auto nb_t, auto diag_t) {
+    constexpr int NA = decltype(na_t)::value, NB = decltype(nb_t)::value;
+    constexpr bool DIAG = decltype(diag_t)::value;
+    for (int64_t s = 0; s < nstage; ++s) {
+      const int b = (int)(s % GNS);
+      mbar_wait(&full[b], (unsigned)((s / GNS) & 1));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double* H = sP + ((size_t)b * 2 + h) * np_pad * TKS;
+        const double* bI = H + (size_t)I * 32 * TKS;
+        const double* bJ = H + (size_t)J * 32 * TKS;
+#pragma unroll
+        for (int kk = 0; kk < TKS / 4; ++kk) {
+          const int k = kk * 4 + tq;
+          double fa[NA], fb[NB];
+#pragma unroll
+          for (int q = 0; q < NA; ++q) fa[q] = bI[swz(q * 8 + g, k)];
+#pragma unroll
+          for (int q = 0; q < NB; ++q) fb[q] = bJ[swz(q * 8 + g, k)];
+#pragma unroll
+          for (int a = 0; a < NA; ++a)
+#pragma unroll
+            for (int c = 0; c < NB; ++c)
+              if (!DIAG || c >= a) dmma884(acc[a][c][0], acc[a][c][1], fa[a], fb[c]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[b]);
+    }
+  };
+  using F = std::false_type;
+  using T = std::true_type;
+  using I1 = std::integral_constant<int, 1>;
+  using I2 = std::integral_constant<int, 2>;
+  using I3 = std::integral_constant<int, 3>;
+  using I4 = std::integral_constant<int, 4>;
+  if (I != J) {
+    if (nvb == 4) stage_loop(I4{}, I4{}, F{});
+    else if (nvb == 3) stage_loop(I4{}, I3{}, F{});
+    else if (nvb == 2) stage_loop(I4{}, I2{}, F{});
+    else stage_loop(I4{}, I1{}, F{});
+    (void)nva;
+  } else {
+    if (nva == 4) stage_loop(I4{}, I4{}, T{});
+    else if (nva == 3) stage_loop(I3{}, I3{}, T{});
+    else if (nva == 2) stage_loop(I2{}, I2{}, T{});
+    else stage_loop(I1{}, I1{}, T{});
+  }
+  double* dst = p.partial + ((size_t)blockIdx.x * SLOTS + warp * TPW) * 1024;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      *reinterpret_cast<double2*>(dst + (a * 8 + g) * 32 + c * 8 + 2 * tq) = make_double2(acc[a][c][0], acc[a][c][1]);
+}
+
+void launch_gram_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x, int grid, cudaStream_t st) {
+  const size_t smem = gram_tma_smem_bytes(p.np_pad);
+  cudaFuncSetAttribute(gram_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  gram_tma_kernel<<<grid, NTHR, smem, st>>>(p, maps, x);
+}
+
 // ---------------------------------------------------------------- host side
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

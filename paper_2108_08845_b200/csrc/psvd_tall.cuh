@@ -108,5 +108,9 @@ bool tma_available();
 size_t tma_pass_smem_bytes(int np_pad, int kp_span);
 int tma_pass_prepare(const TallParams& p, TmaMaps& maps, TmaExtra& x);
 void launch_pass_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x, int grid, cudaStream_t st);
+// TMA-fed Gram-only pass (w == 0, segments on 8-column boundaries, <= NWARP - 1 tiles per slice)
+constexpr int TMA_GRAM_CONS = NWARP - 1;
+size_t gram_tma_smem_bytes(int np_pad);
+void launch_gram_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x, int grid, cudaStream_t st);
 
 }  // namespace psvd
