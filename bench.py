@@ -262,12 +262,13 @@ def run_ours(a):
         return Ubuf[cur], sig[cur]
 
     def gram_probe():
-        """Gram-kernel duration on its own (same shape as one incorporate's Gram)."""
-        n = K + BATCH
+        """The dominant kernel on its own: the batch Gram A^T A (M x B, the look-ahead pass of
+        psvd_stream_run; psvd_gram with Kc = 0 runs the same TMA-fed Gram kernel in one launch)."""
+        n = BATCH
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(5):
-            nat.call("psvd_gram", c, M, nat._vp(Ubuf[0].data_ptr()), Ubuf[0].ld, nat.ptr(sig[0]), FF, K,
+            nat.call("psvd_gram", c, M, nat._vp(0), 0, nat._vp(0), FF, 0,
                      col_ptr(BATCH), ld, BATCH, nat.ptr(Gloc[n]), st)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -330,12 +331,12 @@ def run_ours(a):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (analytic Burgers, device-generated; same formula as the host generator)",
         "config": config_dict(a),
-        "roofline": {"bound": "tensor", "kernel": "psvd_gram (gram_ws_kernel: warp-specialized DMMA Gram of [ff*U*S | A])",
+        "roofline": {"bound": "tensor", "kernel": "gram_tma_kernel (batch Gram A^T A on DMMA, TMA-fed; psvd_gram probe)",
                      "achieved": round(g_ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": round(g_ach / FP64_PEAK_TFLOPS, 4), "traffic": traffic,
                      "peak_source": "measured DMMA.8x8x4 peak (profiles/fp64_peaks_r01.jsonl); "
                                     "MEASURED_PEAKS.json has no FP64 entry",
-                     "flops_per_launch": "M*n*(n+1) (upper triangle of C^T C), n = K + B",
+                     "flops_per_launch": "M*n*(n+1) (upper triangle of A^T A), n = B",
                      "share_of_step": round(gram_share, 4)},
         "hbm_roofline": {"achieved": round(hbm_ach, 1), "peak": HBM_PEAK[0], "unit": "GB/s",
                          "frac": round(hbm_ach / HBM_PEAK[0], 4), "peak_source": HBM_PEAK[1],
