@@ -230,18 +230,19 @@ static int plan_tiles_balanced(psvd_ctx* c, Pass& ps, const std::vector<std::pai
   return PSVD_OK;
 }
 
-// TMA pass: tiles on the Gram warps TMA_GRAM_WARP0.., one tile each, no k-split.
+// TMA pass: tiles on the Gram warps (after the 2*ncb Y warps), one tile each, no k-split.
 static int plan_tiles_tma(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& tiles) {
   const int nt = (int)tiles.size();
   memset(ps.p.plan, 0, sizeof(ps.p.plan));
   memset(&ps.map, 0, sizeof(ps.map));
-  const int nslices = std::max(1, (nt + TMA_GRAM_WARPS - 1) / TMA_GRAM_WARPS);
+  const int warp0 = 2 * (ps.p.w_pad / 8), nwarps = NWARP - 1 - warp0;
+  const int nslices = std::max(1, (nt + nwarps - 1) / nwarps);
   if (nt > MAX_OUT_TILES || nslices > MAX_SLICES) return fail(c, PSVD_EINVAL, "panel too wide (%d tiles)", nt);
   ps.p.nslices = nslices;
   ps.map.nout = nt;
   const int per = (nt + nslices - 1) / nslices;
   for (int o = 0; o < nt; ++o) {
-    const int sl = o / per, w = TMA_GRAM_WARP0 + o % per;
+    const int sl = o / per, w = warp0 + o % per;
     WarpPlan& wp = ps.p.plan[sl][w];
     wp.ksplit = 1;
     wp.kpart = 0;
@@ -268,7 +269,7 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
   // whose segments start on 8-column boundaries; P-tiles at explicit blocks (py_lo >= 0)
   // need that layout to coincide with the contiguous one.
   static const bool no_tma = getenv("PSVD_NO_TMA") != nullptr;
-  bool tma = !no_tma && w > 0 && w <= 16 && !gram_pp && tma_available();
+  bool tma = !no_tma && w > 0 && w <= TMA_MAX_Y && !gram_pp && tma_available();
   auto layout = [&](int align) {
     int n_ = 0;
     for (size_t i = 0; i < segs.size(); ++i) {
@@ -751,11 +752,14 @@ static int exchange_sign(psvd_ctx* c, const double* local_pairs, int nchunks, in
   return PSVD_OK;
 }
 
+// SVQB weights T = V diag(lambda^-1/2) of the l x l sketch Gram (numerically null directions
+// dropped at 1e-7 relative), from a one-sided Jacobi eigen-decomposition of the Gram.
 static int svqb(psvd_ctx* c, const double* Gs, int l, double* T, double* sig_scratch, cudaStream_t st) {
-  int rc = ensure(c, c->eigws, sizeof(double) * eig_workspace_doubles(l, l));
+  int rc = ensure(c, c->eigws, sizeof(double) * std::max(eig_workspace_doubles(l, l), jacobi_workspace_doubles(l, l)));
   if (rc) return rc;
-  launch_eig_topk(Gs, l, l, nullptr, T, sig_scratch, (double*)c->eigws.ptr, c->d_status, nullptr, st, 1e-7);
-  c->launches++;
+  launch_jacobi_svd(Gs, l, l, sig_scratch, T, (double*)c->eigws.ptr, c->d_status, st);
+  launch_svqb_scale(T, sig_scratch, l, 1e-7, st);
+  c->launches += 2;
   return cuda_check(c, "svqb");
 }
 

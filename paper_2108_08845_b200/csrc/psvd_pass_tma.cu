@@ -32,9 +32,9 @@ namespace {
 
 constexpr int TKS = 16;       // rows per stage = one 128-byte swizzled column
 constexpr int TNS = 3;        // ring depth
-constexpr int YWARPS = 4;     // Y warps (rb, cb) in {0,1}^2
+constexpr int YMAXC = 32;     // widest Y of the narrow pass (4 column blocks)
 constexpr int PROD_WARP = NWARP - 1;
-constexpr int WSP = 20;       // sW row stride (doubles): 2 wavefronts per B-fragment load
+constexpr int WSP = YMAXC + 4;  // sW row stride (doubles, = 4 mod 16): 2 wavefronts per B-fragment load
 
 PSVD_DEV uint32_t saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -58,10 +58,10 @@ PSVD_DEV int swz(int c, int k) { return c * 16 + ((((k >> 1) ^ (c & 7)) << 1) | 
 size_t tma_pass_smem_bytes(int np_pad, int kp_span) {
   size_t b = 1024;  // alignment slack for the 1024-byte swizzle atoms
   b += sizeof(double) * (size_t)TNS * np_pad * TKS;  // panel ring
-  b += sizeof(double) * 2 * 16 * TKS;                // Y double buffer (<= 16 columns)
+  b += sizeof(double) * 2 * YMAXC * TKS;             // Y double buffer (<= 32 columns)
   b += sizeof(double) * (size_t)kp_span * WSP;       // W
   b += 64 * sizeof(uint64_t);                        // barriers
-  b += sizeof(double) * 2 * 16 * 3;                  // argmax scratch
+  b += sizeof(double) * 2 * YMAXC * 3;               // argmax scratch
   return b;
 }
 
@@ -77,22 +77,22 @@ __global__ void __launch_bounds__(NTHR, 1)
   const int64_t row_end = min(p.M, row_begin + p.rows_per_cta);
   const int np_pad = p.np_pad;
   const int kspan = x.kp_hi - x.kp_lo;
-  const int ncb = p.w_pad >> 3;  // Y column blocks (1 or 2)
+  const int ncb = p.w_pad >> 3;  // Y column blocks (1..4); warps 0 .. 2*ncb-1 form Y
 
   unsigned char* base = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
   double* sP = reinterpret_cast<double*>(base);
   double* sY = sP + (size_t)TNS * np_pad * TKS;
-  double* sW = sY + 2 * 16 * TKS;
+  double* sW = sY + 2 * YMAXC * TKS;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sW + (size_t)kspan * WSP);
   uint64_t* full = bars;
   uint64_t* empty = bars + TNS;
   uint64_t* ydone = bars + 2 * TNS;
   uint64_t* yfree = ydone + 2;
-  double* cmx = reinterpret_cast<double*>(bars + 64);  // [2 rb][16 cols][val, abs, row]
+  double* cmx = reinterpret_cast<double*>(bars + 64);  // [2 rb][32 cols][val, abs, row]
 
   int ngram = 0;
-  for (int w = YWARPS; w < PROD_WARP; ++w) ngram += p.plan[slice][w].ntile > 0;
   const int ny = 2 * ncb;
+  for (int w = ny; w < PROD_WARP; ++w) ngram += p.plan[slice][w].ntile > 0;
 
   // one-time setup: zero the panel columns no TMA box writes (alignment gaps), the Y
   // buffers (columns >= w stay zero), stage W with zero rows for gap columns
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       for (int k = 0; k < TKS; ++k) col[k] = 0.0;
     }
   }
-  for (int i = tid; i < 2 * 16 * TKS; i += NTHR) sY[i] = 0.0;
+  for (int i = tid; i < 2 * YMAXC * TKS; i += NTHR) sY[i] = 0.0;
   for (int i = tid; i < kspan * WSP; i += NTHR) {
     const int kk = i / WSP, o = i % WSP;
     const int pc = x.kp_lo + kk;  // physical panel column
@@ -150,10 +150,9 @@ __global__ void __launch_bounds__(NTHR, 1)
     return;
   }
 
-  if (warp < YWARPS) {
+  if (warp < ny) {
     // ---------------------------------------------------------------- Y warps
     const int rb = warp & 1, cb = warp >> 1;
-    if (cb >= ncb) return;
     double cm_val[2] = {0.0, 0.0}, cm_abs[2] = {-1.0, -1.0};
     int64_t cm_row[2] = {-1, -1};
     const bool do_y = slice == 0;
@@ -178,7 +177,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       if (lane == 0) mbar_arrive(&empty[b]);  // panel slot no longer read by this warp
       const double y0 = ya0 + yb0, y1 = ya1 + yb1;
       if (s >= 2 && ngram > 0) mbar_wait(&yfree[yb], (unsigned)(((s >> 1) - 1) & 1));
-      double* Ys = sY + (size_t)yb * 16 * TKS;
+      double* Ys = sY + (size_t)yb * YMAXC * TKS;
       const int o0 = cb * 8 + 2 * tq;
       Ys[swz(o0, kr)] = y0;
       Ys[swz(o0 + 1, kr)] = y1;
@@ -211,7 +210,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       }
       if (g == 0) {
         for (int e = 0; e < 2; ++e) {
-          double* d = cmx + ((size_t)rb * 16 + cb * 8 + 2 * tq + e) * 3;
+          double* d = cmx + ((size_t)rb * YMAXC + cb * 8 + 2 * tq + e) * 3;
           d[0] = cm_val[e]; d[1] = cm_abs[e]; d[2] = (double)cm_row[e];
         }
       }
@@ -221,7 +220,7 @@ __global__ void __launch_bounds__(NTHR, 1)
           const int o = cb * 8 + 2 * tq + e;
           if (o >= p.w) continue;
           const double* d0 = cmx + (size_t)o * 3;
-          const double* d1 = cmx + ((size_t)16 + o) * 3;
+          const double* d1 = cmx + ((size_t)YMAXC + o) * 3;
           const bool take1 = d1[1] > d0[1] || (d1[1] == d0[1] && d1[2] >= 0 && (d0[2] < 0 || d1[2] < d0[2]));
           const double* d = take1 ? d1 : d0;
           double* dst = p.colmax + ((size_t)chunk * p.w + o) * 2;
@@ -236,22 +235,21 @@ __global__ void __launch_bounds__(NTHR, 1)
   // ---------------------------------------------------------------- Gram warps
   const WarpPlan wp = p.plan[slice][warp];
   if (wp.ntile == 0) return;
-  const int I = wp.ti[0], J = wp.tj[0];
+  const int I = wp.ti[0];
   const bool i_is_y = I * 32 >= np_pad;
   const int na = i_is_y ? ncb : min(4, (p.np - I * 32 + 7) / 8);
-  double acc[4][2][2];
+  double acc[4][4][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int c = 0; c < 2; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
-  (void)J;
+    for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
   auto stage_loop = [&](auto na_t, auto nb_t) {
     constexpr int NA = decltype(na_t)::value, NB = decltype(nb_t)::value;
     for (int64_t s = 0; s < nstage; ++s) {
       const int b = (int)(s % TNS), yb = (int)(s & 1);
       mbar_wait(&full[b], (unsigned)((s / TNS) & 1));
       mbar_wait(&ydone[yb], (unsigned)((s >> 1) & 1));
-      const double* Ys = sY + (size_t)yb * 16 * TKS;
+      const double* Ys = sY + (size_t)yb * YMAXC * TKS;
       const double* Abase = i_is_y ? Ys : sP + (size_t)b * np_pad * TKS + (size_t)I * 32 * TKS;
 #pragma unroll
       for (int kk = 0; kk < TKS / 4; ++kk) {
@@ -275,28 +273,23 @@ __global__ void __launch_bounds__(NTHR, 1)
   using I2 = std::integral_constant<int, 2>;
   using I3 = std::integral_constant<int, 3>;
   using I4 = std::integral_constant<int, 4>;
-  if (ncb == 2) {
-    if (na == 4) stage_loop(I4{}, I2{});
-    else if (na == 3) stage_loop(I3{}, I2{});
-    else if (na == 2) stage_loop(I2{}, I2{});
-    else stage_loop(I1{}, I2{});
-  } else {
-    if (na == 4) stage_loop(I4{}, I1{});
-    else if (na == 3) stage_loop(I3{}, I1{});
-    else if (na == 2) stage_loop(I2{}, I1{});
-    else stage_loop(I1{}, I1{});
-  }
+  auto with_na = [&](auto nb_t) {
+    if (na == 4) stage_loop(I4{}, nb_t);
+    else if (na == 3) stage_loop(I3{}, nb_t);
+    else if (na == 2) stage_loop(I2{}, nb_t);
+    else stage_loop(I1{}, nb_t);
+  };
+  if (ncb == 4) with_na(I4{});
+  else if (ncb == 3) with_na(I3{});
+  else if (ncb == 2) with_na(I2{});
+  else with_na(I1{});
   double* dst = p.partial + ((size_t)blockIdx.x * SLOTS + warp * TPW) * 1024;
 #pragma unroll
-  for (int a = 0; a < 4; ++a) {
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const double v0 = c < 2 ? acc[a][c & 1][0] : 0.0, v1 = c < 2 ? acc[a][c & 1][1] : 0.0;
-      *reinterpret_cast<double2*>(dst + (a * 8 + g) * 32 + c * 8 + 2 * tq) = make_double2(v0, v1);
-    }
-  }
+    for (int c = 0; c < 4; ++c)
+      *reinterpret_cast<double2*>(dst + (a * 8 + g) * 32 + c * 8 + 2 * tq) = make_double2(acc[a][c][0], acc[a][c][1]);
 }
-
 
 // ---------------------------------------------------------------- TMA Gram (w == 0)
 // Gram-only pass fed by TMA: 32-row stages (two 16-row 128B-swizzled boxes per segment)

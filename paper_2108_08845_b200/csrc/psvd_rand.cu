@@ -2,6 +2,9 @@
 // per batch): one-sided Jacobi SVD of the projected core, tiny
 // dense products, and the tall sign rule (linalg.py:161, 81-91).
 #include <cfloat>
+#include <cstdio>
+#include <algorithm>
+
 #include "psvd_small.cuh"
 
 namespace psvd {
@@ -45,7 +48,8 @@ jacobi_svd_kernel(const double* __restrict__ Zin, int n, int l, double* __restri
   const int le = l + (l & 1);  // even number of columns (a zero column pads odd l)
   double* Z = SMEM ? sm : ws;
   double* J = SMEM ? sm + (size_t)n * le : sm;
-  double* nrm = J + (size_t)le * le;
+  double* red = J + (size_t)le * le;  // 32 doubles of block_sum scratch
+  double* nrm = red + 32;
   int* order = reinterpret_cast<int*>(nrm + le);
   int* flag = order + le + 1;
   for (int64_t i = tid; i < (int64_t)n * le; i += blockDim.x) {
@@ -53,7 +57,14 @@ jacobi_svd_kernel(const double* __restrict__ Zin, int n, int l, double* __restri
     Z[i] = c < l ? Zin[i] : 0.0;
   }
   for (int i = tid; i < le * le; i += blockDim.x) J[i] = (i % le == i / le) ? 1.0 : 0.0;
-  __syncthreads();
+  // ||Z||_F^2 is invariant under the rotations: pairs whose inner product is below
+  // eps^2 ||Z||_F^2 are at fp64 noise level relative to the matrix (rank-deficient
+  // sketches) and are left alone, so the sweep converges instead of churning noise.
+  double fro = 0.0;
+  for (int64_t i = tid; i < (int64_t)n * le; i += blockDim.x) fro = fma(Z[i], Z[i], fro);
+  fro = block_sum(fro, red);
+  const double cfloor = DBL_EPSILON * DBL_EPSILON * fro;
+  const double ctol = (double)max(n, 2) * DBL_EPSILON;  // orthogonality target (LAPACK-style m*eps)
   const int npair = le / 2;
   for (int sweep = 0; sweep < 40; ++sweep) {
     if (tid == 0) *flag = 0;
@@ -78,10 +89,13 @@ jacobi_svd_kernel(const double* __restrict__ Zin, int n, int l, double* __restri
           b = fma(y, y, b);
           c = fma(x, y, c);
         }
-        a = warp_sum(a);
-        b = warp_sum(b);
-        c = warp_sum(c);
-        if (c != 0.0 && fabs(c) > DBL_EPSILON * sqrt(a * b)) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {  // three interleaved butterflies
+          a += __shfl_xor_sync(0xffffffffu, a, o);
+          b += __shfl_xor_sync(0xffffffffu, b, o);
+          c += __shfl_xor_sync(0xffffffffu, c, o);
+        }
+        if (c != 0.0 && fabs(c) > ctol * sqrt(a * b) && fabs(c) > cfloor) {
           const double zeta = (b - a) / (2.0 * c);
           const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
@@ -104,6 +118,9 @@ jacobi_svd_kernel(const double* __restrict__ Zin, int n, int l, double* __restri
     }
     const int f = *flag;
     __syncthreads();
+#ifdef PSVD_JACOBI_DEBUG
+    if (tid == 0) printf("sweep %d flag %d clock %lld\n", sweep, f, (long long)clock64());
+#endif
     if (f == 0) break;
     if (sweep == 39 && tid == 0) atomicOr(status, PSVD_ST_NOCONVERGE);
   }
@@ -133,14 +150,30 @@ jacobi_svd_kernel(const double* __restrict__ Zin, int n, int l, double* __restri
 
 size_t jacobi_workspace_doubles(int n, int l) { return (size_t)n * (l + 1); }
 
+// SVQB weights from the Jacobi eigen-decomposition of an l x l SPD Gram (S = eigenvalues,
+// descending; T = eigenvectors): T[:, k] *= 1 / sqrt(S_k), or 0 for directions with
+// sqrt(S_k) <= tol * sqrt(S_0) (numerically null, dropped).
+__global__ void svqb_scale_kernel(double* __restrict__ T, const double* __restrict__ S, int l, double tol) {
+  const int k = blockIdx.x;
+  const double s0 = sqrt(fmax(S[0], 0.0)), sk = sqrt(fmax(S[k], 0.0));
+  const double inv = (sk > 0.0 && sk > tol * s0) ? 1.0 / sk : 0.0;
+  for (int i = threadIdx.x; i < l; i += blockDim.x) T[(size_t)k * l + i] *= inv;
+}
+
+void launch_svqb_scale(double* T, const double* S, int l, double tol, cudaStream_t st) {
+  svqb_scale_kernel<<<l, 32, 0, st>>>(T, S, l, tol);
+}
+
 void launch_jacobi_svd(const double* Z, int n, int l, double* S, double* J, double* ws, int* status, cudaStream_t st) {
   const int le = l + (l & 1);
-  const size_t small = (size_t)le * le + le + le + 8;
+  const size_t small = (size_t)le * le + 32 + le + le + 8;
   const size_t limit = 227 * 1024 / sizeof(double);
   if ((size_t)n * le + small <= limit) {
     const size_t smem = ((size_t)n * le + small) * sizeof(double);
     cudaFuncSetAttribute(jacobi_svd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    jacobi_svd_kernel<true><<<1, 1024, smem, st>>>(Z, n, l, S, J, ws, status);
+    // one warp per column pair (fewer idle warps at the round barriers for small l)
+    const int thr = std::min(1024, std::max(64, 32 * (le / 2)));
+    jacobi_svd_kernel<true><<<1, thr, smem, st>>>(Z, n, l, S, J, ws, status);
   } else {
     const size_t smem = small * sizeof(double);
     cudaFuncSetAttribute(jacobi_svd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

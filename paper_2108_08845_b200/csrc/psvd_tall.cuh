@@ -86,13 +86,14 @@ size_t gram_ws_smem_bytes(int np_pad, int ns);
 void launch_gram_ws(const TallParams& p, int grid, cudaStream_t st);
 void launch_tall_reduce(const double* partial, const ReduceMap& map, double* tiles, cudaStream_t st);
 
-// Warp-specialized TMA pass for narrow panels (w <= 16, Gram tiles only against Y):
+// Warp-specialized TMA pass for narrow panels (w <= 32, Gram tiles only against Y):
 // every segment starts on an 8-column boundary of the panel (1024-byte swizzle atoms).
 constexpr int TMA_MAX_OPS = 16;
 constexpr int TMA_NOT_IN_W = -(1 << 30);
 constexpr int TMA_MAX_BLK = 192;  // 8-column blocks of the panel
-constexpr int TMA_GRAM_WARP0 = 4;                 // warps 0..3 form Y
-constexpr int TMA_GRAM_WARPS = NWARP - 1 - TMA_GRAM_WARP0;  // last warp is the TMA producer
+// narrow TMA pass: warps 0 .. 2*ncb-1 form Y (ncb = Y column blocks, w <= 32), the following
+// ones own one Gram tile each, the last warp is the TMA producer
+constexpr int TMA_MAX_Y = 32;
 struct TmaMaps {
   CUtensorMap m[MAX_SEG];
 };
