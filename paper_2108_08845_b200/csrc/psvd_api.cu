@@ -281,6 +281,7 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
     return n_;
   };
   int np = layout(1);
+  int pshift = 0;
   if (tma) {
     std::vector<int> c1(segs.size());
     for (size_t i = 0; i < segs.size(); ++i) c1[i] = p.seg[i].col0;
@@ -289,9 +290,25 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
     for (size_t i = 0; i < segs.size(); ++i) same = same && c1[i] == p.seg[i].col0;
     for (size_t i = 0; i < segs.size(); ++i)
       tma = tma && aligned16(segs[i].ptr) && segs[i].ld % 2 == 0 && segs[i].ncols > 0;
-    if (gram_py && py_lo >= 0 && !same) tma = false;
-    if (tma && tma_pass_smem_bytes(rup(np8, 32), rup(wk, 8) + 8 * (int)segs.size()) > (size_t)SMEM_LIMIT) tma = false;
-    np = tma ? np8 : layout(1);
+    bool use_gaps = true;
+    if (gram_py && py_lo >= 0 && !same) {
+      // P-tiles at fixed logical blocks: keep the contiguous layout, shifted right by pshift so
+      // that every segment after the first starts on an 8-column boundary (the first one's box
+      // starts out of bounds, zero filled)
+      pshift = c1.size() > 1 ? (8 - c1[1] % 8) % 8 : 0;
+      bool ok = c1.size() > 1;
+      for (size_t i = 1; i < c1.size(); ++i) ok = ok && (c1[i] + pshift) % 8 == 0;
+      if (!ok) tma = false;
+      use_gaps = false;
+    }
+    const int pw = (use_gaps ? rup(np8, 32) : rup(np, 32) + pshift) + 8;
+    if (tma && tma_pass_smem_bytes(pw, rup(wk, 8) + 8 * (int)segs.size()) > (size_t)SMEM_LIMIT) tma = false;
+    if (tma && use_gaps) {
+      np = np8;
+    } else {
+      np = layout(1);
+      if (!tma) pshift = 0;
+    }
   }
   if (py_lo < 0) {  // P-tiles over the last segment (its own 32-column block)
     const Seg& l = p.seg[segs.size() - 1];
@@ -369,7 +386,7 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
     if (rc2) return rc2;
     p.partial = (double*)ps.part->ptr;
   }
-  if ((tma || ps.gtma) && tma_pass_prepare(p, ps.maps, ps.x) != 0)
+  if ((tma || ps.gtma) && tma_pass_prepare(p, ps.maps, ps.x, tma ? pshift : 0) != 0)
     return fail(c, PSVD_ECUDA, "TMA descriptor setup failed");
   return PSVD_OK;
 }

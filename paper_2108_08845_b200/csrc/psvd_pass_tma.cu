@@ -55,9 +55,9 @@ PSVD_DEV int swz(int c, int k) { return c * 16 + ((((k >> 1) ^ (c & 7)) << 1) | 
 
 }  // namespace
 
-size_t tma_pass_smem_bytes(int np_pad, int kp_span) {
+size_t tma_pass_smem_bytes(int pwidth, int kp_span) {
   size_t b = 1024;  // alignment slack for the 1024-byte swizzle atoms
-  b += sizeof(double) * (size_t)TNS * np_pad * TKS;  // panel ring
+  b += sizeof(double) * (size_t)TNS * pwidth * TKS;  // panel ring
   b += sizeof(double) * 2 * YMAXC * TKS;             // Y double buffer (<= 32 columns)
   b += sizeof(double) * (size_t)kp_span * WSP;       // W
   b += 64 * sizeof(uint64_t);                        // barriers
@@ -75,13 +75,14 @@ __global__ void __launch_bounds__(NTHR, 1)
   const int64_t chunk = blockIdx.x / p.nslices;
   const int64_t row_begin = chunk * p.rows_per_cta;
   const int64_t row_end = min(p.M, row_begin + p.rows_per_cta);
-  const int np_pad = p.np_pad;
+  const int np_pad = p.np_pad;  // logical panel width (Y block index boundary)
+  const int pw = x.pwidth;       // physical ring width (>= np_pad + pshift)
   const int kspan = x.kp_hi - x.kp_lo;
   const int ncb = p.w_pad >> 3;  // Y column blocks (1..4); warps 0 .. 2*ncb-1 form Y
 
   unsigned char* base = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
   double* sP = reinterpret_cast<double*>(base);
-  double* sY = sP + (size_t)TNS * np_pad * TKS;
+  double* sY = sP + (size_t)TNS * pw * TKS;
   double* sW = sY + 2 * YMAXC * TKS;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sW + (size_t)kspan * WSP);
   uint64_t* full = bars;
@@ -96,8 +97,8 @@ __global__ void __launch_bounds__(NTHR, 1)
 
   // one-time setup: zero the panel columns no TMA box writes (alignment gaps), the Y
   // buffers (columns >= w stay zero), stage W with zero rows for gap columns
-  for (int i = tid; i < TNS * np_pad; i += NTHR) {
-    const int c = i % np_pad;
+  for (int i = tid; i < TNS * pw; i += NTHR) {
+    const int c = i % pw;
     if (!x.written[c >> 3]) {
       double* col = sP + (size_t)i * TKS;
 #pragma unroll
@@ -111,7 +112,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     double v = 0.0;
     if (o < p.w) {
       for (int s = 0; s < p.nseg; ++s) {
-        const int c0 = p.seg[s].col0;
+        const int c0 = p.seg[s].col0 + x.pshift;  // physical start
         if (x.wrow0[s] != TMA_NOT_IN_W && pc >= c0 && pc < c0 + p.seg[s].ncols) {
           const int wr = x.wrow0[s] + (pc - c0);
           if (wr >= 0 && wr < p.wk) v = p.W[(int64_t)o * p.ldw + wr];
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(NTHR, 1)
         const int b = (int)(s % TNS);
         if (s >= TNS) mbar_wait(&empty[b], (unsigned)(((s / TNS) - 1) & 1));
         mbar_expect_tx(&full[b], x.stage_bytes);
-        double* dst = sP + (size_t)b * np_pad * TKS;
+        double* dst = sP + (size_t)b * pw * TKS;
         const int r0 = (int)(row_begin + s * TKS);
         for (int o = 0; o < x.nops; ++o)
           tma_load_2d(dst + (size_t)x.op_pcol[o] * TKS, &maps.m[x.op_seg[o]], r0, x.op_col[o], &full[b]);
@@ -159,7 +160,7 @@ __global__ void __launch_bounds__(NTHR, 1)
     for (int64_t s = 0; s < nstage; ++s) {
       const int b = (int)(s % TNS), yb = (int)(s & 1);
       mbar_wait(&full[b], (unsigned)((s / TNS) & 1));
-      const double* P = sP + (size_t)b * np_pad * TKS;
+      const double* P = sP + (size_t)b * pw * TKS;
       double ya0 = 0.0, ya1 = 0.0, yb0 = 0.0, yb1 = 0.0;
       const int kr = rb * 8 + g;
       const double* wb = sW + (size_t)tq * WSP + cb * 8 + g;
@@ -238,6 +239,7 @@ __global__ void __launch_bounds__(NTHR, 1)
   const int I = wp.ti[0];
   const bool i_is_y = I * 32 >= np_pad;
   const int na = i_is_y ? ncb : min(4, (p.np - I * 32 + 7) / 8);
+  const int acol = I * 32 + x.pshift;  // physical first column of a panel tile
   double acc[4][4][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
@@ -250,13 +252,14 @@ __global__ void __launch_bounds__(NTHR, 1)
       mbar_wait(&full[b], (unsigned)((s / TNS) & 1));
       mbar_wait(&ydone[yb], (unsigned)((s >> 1) & 1));
       const double* Ys = sY + (size_t)yb * YMAXC * TKS;
-      const double* Abase = i_is_y ? Ys : sP + (size_t)b * np_pad * TKS + (size_t)I * 32 * TKS;
+      const double* Abase = sP + (size_t)b * pw * TKS;
 #pragma unroll
       for (int kk = 0; kk < TKS / 4; ++kk) {
         const int k = kk * 4 + tq;
         double fa[NA], fb[NB];
 #pragma unroll
-        for (int q = 0; q < NA; ++q) fa[q] = Abase[swz(q * 8 + g, k)];
+        for (int q = 0; q < NA; ++q)
+          fa[q] = i_is_y ? Ys[swz(q * 8 + g, k)] : Abase[swz(acol + q * 8 + g, k)];
 #pragma unroll
         for (int q = 0; q < NB; ++q) fb[q] = Ys[swz(q * 8 + g, k)];
 #pragma unroll
@@ -447,18 +450,23 @@ static EncodeTiledFn encode_fn() {
 
 bool tma_available() { return encode_fn() != nullptr; }
 
-int tma_pass_prepare(const TallParams& p, TmaMaps& maps, TmaExtra& x) {
+int tma_pass_prepare(const TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return -1;
   memset(&x, 0, sizeof(x));
+  x.pshift = pshift;
   int nops = 0;
   uint32_t bytes = 0;
   int logical = 0;
-  int kp_lo = 1 << 30, kp_hi = 0;
+  int kp_lo = 1 << 30, kp_hi = 0, pend = 0;
   for (int s = 0; s < p.nseg; ++s) {
     const Seg& sg = p.seg[s];
-    if ((sg.col0 & 7) != 0 || (reinterpret_cast<uintptr_t>(sg.ptr) & 15) != 0 || (sg.ld & 1) != 0) return -1;
-    const int bw = std::min(256, (sg.ncols + 7) / 8 * 8);
+    const int P = sg.col0 + pshift;         // physical first column
+    const int lead = P & 7;                 // only the first segment may start off an 8-column boundary
+    if ((lead != 0 && (s != 0 || P != pshift)) || (reinterpret_cast<uintptr_t>(sg.ptr) & 15) != 0 ||
+        (sg.ld & 1) != 0)
+      return -1;
+    const int bw = std::min(256, (sg.ncols + lead + 7) / 8 * 8);
     cuuint64_t dims[2] = {(cuuint64_t)p.M, (cuuint64_t)sg.ncols};
     cuuint64_t strides[1] = {(cuuint64_t)sg.ld * sizeof(double)};
     cuuint32_t box[2] = {(cuuint32_t)TKS, (cuuint32_t)bw};
@@ -467,22 +475,24 @@ int tma_pass_prepare(const TallParams& p, TmaMaps& maps, TmaExtra& x) {
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return -1;
-    for (int c = 0; c < sg.ncols; c += bw) {
+    // boxes start at tensor column -lead (out of bounds -> zero filled) so they land 1024-byte aligned
+    for (int c = -lead; c < sg.ncols; c += bw) {
       if (nops >= TMA_MAX_OPS) return -1;
+      const int dst = P + c;
       x.op_seg[nops] = (short)s;
       x.op_col[nops] = (short)c;
-      x.op_pcol[nops] = (short)(sg.col0 + c);
-      for (int q = (sg.col0 + c) >> 3; q < (sg.col0 + c + bw) >> 3 && q < TMA_MAX_BLK; ++q) x.written[q] = 1;
+      x.op_pcol[nops] = (short)dst;
+      for (int q = dst >> 3; q < (dst + bw) >> 3 && q < TMA_MAX_BLK; ++q) x.written[q] = 1;
       bytes += (uint32_t)(TKS * bw * sizeof(double));
+      pend = std::max(pend, dst + bw);
       ++nops;
     }
-    // W rows: logical column range [logical, logical + ncols) against [wlo, wlo + wk)
     x.wrow0[s] = TMA_NOT_IN_W;
     const int lo = std::max(logical, p.wlo), hi = std::min(logical + sg.ncols, p.wlo + p.wk);
     if (p.w > 0 && lo < hi) {
-      x.wrow0[s] = logical - p.wlo;  // may be negative when the W range starts inside the segment
-      kp_lo = std::min(kp_lo, sg.col0 + (lo - logical));
-      kp_hi = std::max(kp_hi, sg.col0 + (hi - logical));
+      x.wrow0[s] = logical - p.wlo;
+      kp_lo = std::min(kp_lo, P + (lo - logical));
+      kp_hi = std::max(kp_hi, P + (hi - logical));
     }
     logical += sg.ncols;
   }
@@ -492,11 +502,12 @@ int tma_pass_prepare(const TallParams& p, TmaMaps& maps, TmaExtra& x) {
   }
   x.nops = nops;
   x.stage_bytes = bytes;
+  x.pwidth = std::max((p.np_pad + pshift + 7) / 8 * 8, (pend + 7) / 8 * 8);
   return 0;
 }
 
 void launch_pass_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x, int grid, cudaStream_t st) {
-  const size_t smem = tma_pass_smem_bytes(p.np_pad, x.kp_hi - x.kp_lo);
+  const size_t smem = tma_pass_smem_bytes(x.pwidth, x.kp_hi - x.kp_lo);
   cudaFuncSetAttribute(pass_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   pass_tma_kernel<<<grid, NTHR, smem, st>>>(p, maps, x);
 }

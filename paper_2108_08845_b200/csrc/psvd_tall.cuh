@@ -102,12 +102,14 @@ struct TmaExtra {
   short op_seg[TMA_MAX_OPS], op_col[TMA_MAX_OPS], op_pcol[TMA_MAX_OPS];
   int wrow0[MAX_SEG];        // W row of the segment's first column (TMA_NOT_IN_W: outside Y's range)
   int kp_lo, kp_hi;          // Y's k range in physical panel columns
+  int pshift;                // physical column = logical column + pshift (narrow pass)
+  int pwidth;                // physical ring width (columns)
   unsigned stage_bytes;
   unsigned char written[TMA_MAX_BLK];  // 8-column panel blocks covered by a TMA box
 };
 bool tma_available();
-size_t tma_pass_smem_bytes(int np_pad, int kp_span);
-int tma_pass_prepare(const TallParams& p, TmaMaps& maps, TmaExtra& x);
+size_t tma_pass_smem_bytes(int pwidth, int kp_span);
+int tma_pass_prepare(const TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift = 0);
 void launch_pass_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x, int grid, cudaStream_t st);
 // TMA-fed Gram-only pass (w == 0, segments on 8-column boundaries, <= NWARP - 1 tiles per slice)
 constexpr int TMA_GRAM_CONS = NWARP - 1;
