@@ -95,10 +95,12 @@ jacobi_svd_kernel(const double* __restrict__ Zin, int n, int l, double* __restri
           b += __shfl_xor_sync(0xffffffffu, b, o);
           c += __shfl_xor_sync(0xffffffffu, c, o);
         }
-        if (c != 0.0 && fabs(c) > ctol * sqrt(a * b) && fabs(c) > cfloor) {
-          const double zeta = (b - a) / (2.0 * c);
-          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        if (c != 0.0 && c * c > ctol * ctol * (a * b) && fabs(c) > cfloor) {
+          // t = tan(theta) of the Hestenes rotation, smaller root: t = 2c sgn(b - a) / (|b - a| + sqrt((b - a)^2 + 4c^2))
+          // (one sqrt, one division, one rsqrt per pair: the FP64 div/sqrt chains set the round latency)
+          const double d = b - a;
+          const double t = (d >= 0.0 ? 2.0 * c : -2.0 * c) / (fabs(d) + sqrt(fma(d, d, 4.0 * c * c)));
+          const double cs = rsqrt(fma(t, t, 1.0)), sn = cs * t;
           for (int i = lane; i < n; i += 32) {
             const double x = zp[i], y = zq[i];
             zp[i] = cs * x - sn * y;
