@@ -74,6 +74,11 @@ int psvd_set_exchange(psvd_ctx* ctx, psvd_allreduce_fn allreduce, psvd_allgather
  * gated full Householder solver ran. */
 int psvd_last_core_path(psvd_ctx* ctx, int* full);
 
+/* Pass-kernel counters since context creation (diagnostics): out[0] narrow TMA passes,
+ * out[1] TMA-fed Gram passes, out[2] cp.async Gram passes, out[3] general cp.async passes,
+ * out[4] wide-route tall-skinny GEMM updates. */
+int psvd_path_counters(psvd_ctx* ctx, long long* out5);
+
 /* Number of kernels this context has enqueued so far (launch accounting). */
 long long psvd_launch_count(psvd_ctx* ctx);
 

@@ -40,6 +40,7 @@ _SIGS = {
     "psvd_set_drift_tol": (_c_int, [_vp, _c_dbl]),
     "psvd_set_exchange": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_i64]),
     "psvd_last_core_path": (_c_int, [_vp, ctypes.POINTER(_c_int)]),
+    "psvd_path_counters": (_c_int, [_vp, ctypes.POINTER(_c_i64)]),
     "psvd_eig_phase_cycles": (_c_int, [_vp, ctypes.POINTER(ctypes.c_longlong)]),
     "psvd_read_status": (_c_int, [_vp, ctypes.POINTER(_c_int), _c_int, _vp]),
     "psvd_gram": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_int, _vp, _c_i64, _c_int, _vp, _vp]),
@@ -104,6 +105,13 @@ def call(name, ctx, *args):
     rc = getattr(lib(), name)(ctx, *args)
     if rc != PSVD_OK:
         _raise(rc, ctx)
+
+
+def path_counters(ctx):
+    """(narrow TMA, TMA Gram, cp.async Gram, general cp.async, wide route) pass counts."""
+    out = (_c_i64 * 5)()
+    call("psvd_path_counters", ctx, out)
+    return tuple(out)
 
 
 def require_cuda():

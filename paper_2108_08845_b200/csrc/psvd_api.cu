@@ -36,6 +36,7 @@ struct psvd_ctx {
   long long* d_timers = nullptr;  // eig phase clocks (diagnostics)
   int* h_status = nullptr;  // pinned
   long long launches = 0;   // kernels enqueued by this context (bench evidence)
+  long long path_count[5] = {0, 0, 0, 0, 0};  // narrow TMA, TMA Gram, cp.async Gram, general, wide route
   double drift_tol = 1e-8;  // streaming.py:25 ORTHO_DRIFT_TOL (psvd_set_drift_tol overrides, e.g. to force the rescue)
   Buf partial, tiles, gram, eigws, wbuf, utu, tbuf, dvec, colmax;
   Buf ybuf, rsmall, jacws;  // randomized path: sketch Y (M x l), small matrices, Jacobi scratch
@@ -301,13 +302,15 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
       if (!ok) tma = false;
       use_gaps = false;
     }
-    const int pw = (use_gaps ? rup(np8, 32) : rup(np, 32) + pshift) + 8;
-    if (tma && tma_pass_smem_bytes(pw, rup(wk, 8) + 8 * (int)segs.size()) > (size_t)SMEM_LIMIT) tma = false;
+    const int pw = use_gaps ? rup(np8, 32) : rup(np, 32) + 8;
+    if (tma && tma_pass_smem_bytes(pw, rup(wk, 8) + 8 * (int)segs.size(), rup(w, 8)) > (size_t)SMEM_LIMIT) {
+      tma = false;
+      pshift = 0;
+    }
     if (tma && use_gaps) {
       np = np8;
     } else {
       np = layout(1);
-      if (!tma) pshift = 0;
     }
   }
   if (py_lo < 0) {  // P-tiles over the last segment (its own 32-column block)
@@ -392,6 +395,7 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
 }
 
 int run_pass(psvd_ctx* c, Pass& ps, cudaStream_t st) {
+  c->path_count[ps.tma ? 0 : ps.gtma ? 1 : ps.ws ? 2 : 3]++;
   if (ps.tma)
     launch_pass_tma(ps.p, ps.maps, ps.x, ps.grid, st);
   else if (ps.gtma)
@@ -563,6 +567,12 @@ int psvd_set_exchange(psvd_ctx* c, psvd_allreduce_fn allreduce, psvd_allgather_f
   c->ex_user = user;
   c->ex_nranks = allreduce ? nranks : 1;
   c->ex_row_offset = allreduce ? row_offset : 0;
+  return PSVD_OK;
+}
+
+int psvd_path_counters(psvd_ctx* c, long long* out5) {
+  if (!c || !out5) return PSVD_EINVAL;
+  for (int i = 0; i < 5; ++i) out5[i] = c->path_count[i];
   return PSVD_OK;
 }
 
@@ -834,6 +844,7 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
            plan_pass(c, t2, M, pb, n, l, l, T1, l, false, true, true, n) != PSVD_OK;
   }
   if (wide) {
+    c->path_count[4]++;
     if ((rc = ensure(c, c->ybuf2, sizeof(double) * (size_t)ldy * l))) return rc;
     double* Y2 = (double*)c->ybuf2.ptr;
     const size_t part = std::max(tgemm_tn_partial_doubles(M, n, l, c->num_sms), tgemm_tn_partial_doubles(M, l, l, c->num_sms));
@@ -1021,6 +1032,7 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
         first = pa;
       }
       pa.p.partial = (double*)c->partial2.ptr + part_off;
+      c->path_count[pa.gtma ? 1 : pa.ws ? 2 : 3]++;
       if (pa.gtma)
         launch_gram_tma(pa.p, pa.maps, pa.x, pa.grid, lo);
       else if (pa.ws)

@@ -34,7 +34,8 @@ constexpr int TKS = 16;       // rows per stage = one 128-byte swizzled column
 constexpr int TNS = 3;        // ring depth
 constexpr int YMAXC = 32;     // widest Y of the narrow pass (4 column blocks)
 constexpr int PROD_WARP = NWARP - 1;
-constexpr int WSP = YMAXC + 4;  // sW row stride (doubles, = 4 mod 16): 2 wavefronts per B-fragment load
+// sW row stride (doubles, = 4 mod 16: 2 wavefronts per B-fragment load), sized by the Y width
+__host__ __device__ inline int w_stride(int w_pad) { return w_pad <= 16 ? 20 : 36; }
 
 PSVD_DEV uint32_t saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -55,11 +56,11 @@ PSVD_DEV int swz(int c, int k) { return c * 16 + ((((k >> 1) ^ (c & 7)) << 1) | 
 
 }  // namespace
 
-size_t tma_pass_smem_bytes(int pwidth, int kp_span) {
+size_t tma_pass_smem_bytes(int pwidth, int kp_span, int w_pad) {
   size_t b = 1024;  // alignment slack for the 1024-byte swizzle atoms
   b += sizeof(double) * (size_t)TNS * pwidth * TKS;  // panel ring
   b += sizeof(double) * 2 * YMAXC * TKS;             // Y double buffer (<= 32 columns)
-  b += sizeof(double) * (size_t)kp_span * WSP;       // W
+  b += sizeof(double) * (size_t)kp_span * w_stride(w_pad);  // W
   b += 64 * sizeof(uint64_t);                        // barriers
   b += sizeof(double) * 2 * YMAXC * 3;               // argmax scratch
   return b;
@@ -78,6 +79,7 @@ __global__ void __launch_bounds__(NTHR, 1)
   const int np_pad = p.np_pad;  // logical panel width (Y block index boundary)
   const int pw = x.pwidth;       // physical ring width (>= np_pad + pshift)
   const int kspan = x.kp_hi - x.kp_lo;
+  const int WSP = w_stride(p.w_pad);
   const int ncb = p.w_pad >> 3;  // Y column blocks (1..4); warps 0 .. 2*ncb-1 form Y
 
   unsigned char* base = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
@@ -507,7 +509,7 @@ int tma_pass_prepare(const TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift
 }
 
 void launch_pass_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x, int grid, cudaStream_t st) {
-  const size_t smem = tma_pass_smem_bytes(x.pwidth, x.kp_hi - x.kp_lo);
+  const size_t smem = tma_pass_smem_bytes(x.pwidth, x.kp_hi - x.kp_lo, p.w_pad);
   cudaFuncSetAttribute(pass_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   pass_tma_kernel<<<grid, NTHR, smem, st>>>(p, maps, x);
 }

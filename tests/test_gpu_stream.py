@@ -496,3 +496,24 @@ def test_core_solver_paths_both_exercised_and_exact():
     rm, rs, _ = oracle.ref_stream_all(_batches(g, 200), 10, 0.95)
     m, s = _np(st)
     _assert_parity(m, s, rm, rs)
+
+
+def test_config2_shapes_run_on_the_tma_kernels():
+    """Guard against silent fallbacks: at the config-2 shapes (B = 200, K = 10, l = 20) every
+    pass of the deterministic stream and of the randomized update runs on the TMA kernels."""
+    p = _pkg()
+    from paper_2108_08845_b200 import _native as nat
+    dev = torch.device("cuda", 0)
+    c = nat.context(dev)
+    a = torch.from_numpy(np.asfortranarray(oracle.burgers_matrix(1 << 16, 800))).cuda()
+    cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200)
+    before = nat.path_counters(c)
+    p.stream_all([a[:, i:i + 200] for i in range(0, 800, 200)], cfg)
+    d = [x - y for x, y in zip(nat.path_counters(c), before)]
+    assert d[0] >= 4 and d[1] >= 4 and d[2] == 0 and d[3] == 0 and d[4] == 0, d
+    rcfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200,
+                          sketch=p.RandomSketchConfig(target_rank=10, oversampling=10, power_iterations=1, seed=0))
+    before = nat.path_counters(c)
+    p.stream_all([a[:, i:i + 200] for i in range(0, 800, 200)], rcfg)
+    d = [x - y for x, y in zip(nat.path_counters(c), before)]
+    assert d[0] > 0 and d[2] == 0 and d[3] == 0 and d[4] == 0, d
