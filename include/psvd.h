@@ -152,6 +152,21 @@ int psvd_stream_run(psvd_ctx* ctx, int64_t M, const double* U_in, int64_t ldu, c
                     double* U_a, double* U_b, int64_t ldo, double* sigma_hist, int* final_buf,
                     void* const* batch_ready, void* stream);
 
+/* ---- one-shot distributed SVD helpers (APMOS, dsvd.py:80-173) ----
+ * Top-k eigenpairs of a symmetric PSD n x n matrix G (col-major, ld n): V (n x k,
+ * ld ldv) the eigenvectors, s = sqrt(max(lambda, 0)) descending (the right singular
+ * vectors / values of any C with C^T C = G; generate_right_vectors' "gram" route). */
+int psvd_sym_topk(psvd_ctx* ctx, const double* G, int n, int k, double* V, int64_t ldv, double* s, void* stream);
+
+/* X (n x m, ld ldx) = A^T Y for tall A (M x n) and Y (M x m), both column-major with even
+ * leading dimensions: the rows are split over CTAs and summed in a fixed order. */
+int psvd_tn_product(psvd_ctx* ctx, int64_t M, const double* A, int64_t lda, int n, const double* Y, int64_t ldy,
+                    int m, double* X, int64_t ldx, void* stream);
+
+/* Column sign rule of linalg.py:81-91 in place: the largest-|.| entry of each column of
+ * X (rows x cols, ld even) becomes positive (first row wins ties). */
+int psvd_sign_by_peak(psvd_ctx* ctx, double* X, int64_t ld, int64_t rows, int cols, void* stream);
+
 /* ---- randomized streaming update (low_rank_svd of the panel,
  * linalg.py:126-162) ----
  * U_out, sigma_out = low_rank_svd([ff U diag(sigma) | A], target_rank = K,

@@ -23,4 +23,5 @@ from .core import (  # noqa: F401
     ref_stream_all, ref_rand_stream_init, ref_rand_stream_update,
     ref_rand_stream_all, ref_parallel_stream_all, sigma_rel_err,
     sine_angles, mode_angles, aligned_mode_difference, synth_config_matrix,
+    ref_generate_right_vectors, ref_apmos,
 )

@@ -262,6 +262,65 @@ def synth_config_matrix(*args, **kwargs):  # pragma: no cover - see paper_2108_0
 
 
 # --------------------------------------------------------------------------
+# one-shot distributed SVD (dsvd.py:39-173, APMOS)
+# --------------------------------------------------------------------------
+
+def ref_generate_right_vectors(a, local_rank, method="svd"):
+    """Leading right singular vectors / values of a local slice, zero-padded to
+    local_rank columns — dsvd.py:80-124."""
+    a = _check(a, "a_local")
+    n = a.shape[1]
+    if local_rank < 1:
+        raise ValueError(f"local_rank must be >= 1, got {local_rank}")
+    if local_rank > n:
+        raise ValueError(f"local_rank {local_rank} exceeds the snapshot count {n}")
+    if method == "svd":
+        _, s_all, vt = ref_svd(a, want_vt=True)
+        keep = min(local_rank, s_all.size)
+        v, s = vt[:keep].T.copy(), s_all[:keep].copy()
+    else:  # "gram": method of snapshots (dsvd.py:108-118)
+        lam, vec = np.linalg.eigh(a.T @ a)
+        order = np.argsort(-lam, kind="stable")
+        lam = np.clip(lam[order], 0.0, None)
+        vec = vec[:, order]
+        idx = np.argmax(np.abs(vec), axis=0)
+        sg = np.sign(vec[idx, np.arange(vec.shape[1])])
+        sg[sg == 0.0] = 1.0
+        keep = min(local_rank, n)
+        v, s = (vec * sg)[:, :keep], np.sqrt(lam[:keep])
+    if keep < local_rank:
+        v = np.hstack([v, np.zeros((n, local_rank - keep))])
+        s = np.concatenate([s, np.zeros(local_rank - keep)])
+    return v, s
+
+
+def ref_apmos(blocks, local_rank, global_rank, k, use_randomized=False, sketch=None):
+    """apmos over rank-ordered row blocks — dsvd.py:127-173.  The gather of
+    W_i = V_i S_i to the root is the rank-ordered concatenation; the root's
+    factorization (svd_full, or low_rank_svd with sketch = (target_rank,
+    oversampling, power_iterations, seed)) is what every rank receives.
+    Returns (stacked modes, singular values)."""
+    if global_rank > len(blocks) * local_rank:
+        raise ValueError(f"global_rank {global_rank} exceeds the {len(blocks) * local_rank} columns "
+                         f"the exchange can produce")
+    w = np.concatenate([v * s for v, s in (ref_generate_right_vectors(b, local_rank) for b in blocks)], axis=1)
+    if use_randomized:
+        tr, ov, pi, seed = sketch if sketch is not None else (global_rank, 10, 1, 0)
+        u, s, _ = ref_low_rank_svd(w, tr, ov, pi, seed)
+    else:
+        u, s, _ = ref_svd(w, want_vt=False)
+    if s.size < global_rank:
+        raise ValueError(f"stacked exchange matrix only has {s.size} singular values, "
+                         f"global_rank is {global_rank}")
+    x, lam = u[:, :global_rank], s[:global_rank]
+    for j in range(k):
+        if lam[j] == 0.0:
+            raise ZeroDivisionError(f"mode {j} has a zero singular value and cannot be assembled")
+    modes = np.concatenate([_check(b, "a_local") @ x[:, :k] / lam[:k] for b in blocks], axis=0)
+    return modes, lam[:k].copy()
+
+
+# --------------------------------------------------------------------------
 # comparison metrics (harness only; sine-based so angles below 1e-8 resolve,
 # SURVEY F5)
 # --------------------------------------------------------------------------

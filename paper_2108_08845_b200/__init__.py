@@ -6,6 +6,7 @@ randomized sketch configuration, computed by hand-written sm_100a FP64
 kernels (libpsvd.so, include/psvd.h) on state that stays in HBM.
 """
 
+from .oneshot import ApmosConfig, apmos, generate_right_vectors  # noqa: F401
 from .datagen import burgers_device, burgers_matrix, burgers_solution, partition_bounds  # noqa: F401
 from .dsvd import (LocalModes, RankContext, gather_modes, parallel_stream_incorporate,  # noqa: F401
                    parallel_stream_initialize)

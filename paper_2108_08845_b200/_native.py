@@ -41,6 +41,9 @@ _SIGS = {
     "psvd_set_exchange": (_c_int, [_vp, _vp, _vp, _vp, _c_int, _c_i64]),
     "psvd_last_core_path": (_c_int, [_vp, ctypes.POINTER(_c_int)]),
     "psvd_path_counters": (_c_int, [_vp, ctypes.POINTER(_c_i64)]),
+    "psvd_sym_topk": (_c_int, [_vp, _vp, _c_int, _c_int, _vp, _c_i64, _vp, _vp]),
+    "psvd_sign_by_peak": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _vp]),
+    "psvd_tn_product": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _vp, _c_i64, _vp]),
     "psvd_eig_phase_cycles": (_c_int, [_vp, ctypes.POINTER(ctypes.c_longlong)]),
     "psvd_read_status": (_c_int, [_vp, ctypes.POINTER(_c_int), _c_int, _vp]),
     "psvd_gram": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_int, _vp, _c_i64, _c_int, _vp, _vp]),

@@ -616,6 +616,16 @@ int psvd_gram(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const double
   if (Kc > 0 && sigma == nullptr) return fail(c, PSVD_EINVAL, "sigma is null");
   if (G == nullptr) return fail(c, PSVD_EINVAL, "G is null");
   const int n = Kc + B;
+  const int nb32 = (n + 31) / 32;
+  if (Kc == 0 && nb32 * (nb32 + 1) / 2 > MAX_OUT_TILES) {
+    // too many 32x32 tiles for one pass: the tall-skinny TN GEMM (full n x n, split over rows)
+    c->path_count[4]++;
+    if ((rc = ensure(c, c->partial, sizeof(double) * tgemm_tn_partial_doubles(M, n, n, c->num_sms)))) return rc;
+    const GemmSeg ga{A, lda, B};
+    launch_tgemm_tn(M, &ga, 1, A, lda, B, nullptr, G, n, (double*)c->partial.ptr, c->num_sms, st);
+    c->launches += 2;
+    return cuda_check(c, "wide gram");
+  }
   Pass ps;
   if ((rc = plan_pass(c, ps, M, panel(U, ldu, Kc, A, lda, B), 0, 0, 0, nullptr, 0, true, false, false))) return rc;
   if ((rc = run_pass(c, ps, st))) return rc;
@@ -623,6 +633,51 @@ int psvd_gram(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const double
   launch_extract_sym((const double*)c->tiles.ptr, ps.NB, 0, n, (const double*)c->dvec.ptr, G, st);
   c->launches++;
   return cuda_check(c, "extract gram");
+}
+
+int psvd_sym_topk(psvd_ctx* c, const double* G, int n, int k, double* V, int64_t ldv, double* s, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n < 1 || k < 1 || k > n) return fail(c, PSVD_EINVAL, "bad eig shape n=%d k=%d", n, k);
+  if (!G || !V || !s || ldv < n) return fail(c, PSVD_EINVAL, "bad eig arguments");
+  int rc;
+  if ((rc = ensure(c, c->eigws, sizeof(double) * eig_workspace_doubles(n, k)))) return rc;
+  double* ws = (double*)c->eigws.ptr;
+  launch_eig_topk(G, n, k, nullptr, ws /* W unused */, s, ws, c->d_status, nullptr, st, 0.0, 1);
+  cudaMemcpy2DAsync(V, ldv * sizeof(double), ws + (size_t)n * (n + 1) / 2, n * sizeof(double), n * sizeof(double), k,
+                    cudaMemcpyDeviceToDevice, st);
+  c->launches++;
+  return cuda_check(c, "sym topk");
+}
+
+int psvd_tn_product(psvd_ctx* c, int64_t M, const double* A, int64_t lda, int n, const double* Y, int64_t ldy, int m,
+                    double* X, int64_t ldx, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  int rc;
+  if (M < 1 || n < 1 || m < 1 || ldx < n || !X) return fail(c, PSVD_EINVAL, "bad tn_product shape");
+  if ((rc = check_mat(c, "A", A, lda, M, n)) || (rc = check_mat(c, "Y", Y, ldy, M, m))) return rc;
+  if ((rc = ensure(c, c->partial, sizeof(double) * tgemm_tn_partial_doubles(M, n, m, c->num_sms)))) return rc;
+  const GemmSeg ga{A, lda, n};
+  launch_tgemm_tn(M, &ga, 1, Y, ldy, m, nullptr, X, (int)ldx, (double*)c->partial.ptr, c->num_sms,
+                  (cudaStream_t)stream);
+  c->launches += 2;
+  return cuda_check(c, "tn product");
+}
+
+int psvd_sign_by_peak(psvd_ctx* c, double* X, int64_t ld, int64_t rows, int cols, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if ((rc = check_mat(c, "X", X, ld, rows, cols))) return rc;
+  if (cols == 0) return PSVD_OK;
+  const int64_t nch = colmax_rows_chunks(rows);
+  if ((rc = ensure(c, c->colmax, sizeof(double) * (size_t)nch * cols * 2)) ||
+      (rc = ensure(c, c->xpairs, sizeof(double) * (size_t)cols))) return rc;
+  launch_colmax_rows(X, ld, rows, cols, 0, (double*)c->colmax.ptr, st);
+  launch_colmax_sign((const double*)c->colmax.ptr, (int)nch, cols, (double*)c->xpairs.ptr, st);
+  launch_scale_cols(X, ld, rows, cols, (const double*)c->xpairs.ptr, st);
+  c->launches += 3;
+  return cuda_check(c, "sign by peak");
 }
 
 int psvd_core_eig(psvd_ctx* c, const double* G, int n, const double* sigma_in, double ff, int Kc, int K, double* W,

@@ -813,12 +813,12 @@ void launch_eig_topk(const double* G, int n, int K, const double* dscale, double
     const size_t smem = (npk + vec) * sizeof(double);
     cudaFuncSetAttribute(eig_topk_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     eig_topk_kernel<true, false><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers,
-                                                                  rank_tol, 0, gate);
+                                                                  rank_tol, split, gate);
   } else {
     const size_t smem = vec * sizeof(double);
     cudaFuncSetAttribute(eig_topk_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     eig_topk_kernel<false, false><<<1, SMALL_THREADS, smem, st>>>(G, n, K, dscale, W, sigma, ws, status, timers,
-                                                                   rank_tol, 0, gate);
+                                                                   rank_tol, split, gate);
   }
 }
 

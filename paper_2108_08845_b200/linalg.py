@@ -64,10 +64,11 @@ def device_omega(n_cols, config, device):
     return om
 
 
-def randomized_update(U, sigma, A, sketch, ff, device, check=True, total_rows=None):
+def randomized_update(U, sigma, A, sketch, ff, device, check=True, total_rows=None, omega=None):
     """One randomized step: low_rank_svd([ff*U*diag(sigma) | A], sketch) on the
     device (linalg.py:150-162 composed per batch).  U: DevMat or None.
     total_rows: rows of the whole (row-partitioned) panel for the width check.
+    omega: optional device test matrix (n x l, column-major) replacing the Philox draw.
     Returns (DevMat M x K, sigma (K,))."""
     import torch
     from . import _native as nat
@@ -78,7 +79,7 @@ def randomized_update(U, sigma, A, sketch, ff, device, check=True, total_rows=No
     rows = M if total_rows is None else total_rows
     if l > min(rows, n):
         raise ValueError(f"sketch width {l} exceeds min(a.shape) = {min(rows, n)}")
-    om = device_omega(n, sketch, device)
+    om = device_omega(n, sketch, device) if omega is None else omega
     ctx = nat.context(device)
     with torch.cuda.device(device):
         out = nat.DevMat.empty(M, k, device)

@@ -133,6 +133,35 @@ def main():
     save("par_burgers2048_p4", grid=2048, snaps=800, k=10, ff=0.95, batch=200, world=4,
          input_sha=sha(a), modes=modes, sigma=sig)
 
+    # ---- G7: apmos one-shot distributed SVD (dsvd.py:127-173, test_dsvd.py:73-133 shapes) ----
+    from parsvd.dsvd import ApmosConfig, apmos
+    out = {}
+    rng = np.random.Generator(np.random.Philox(42))
+    g = rng.standard_normal((64, 16))
+    out["gauss_a"] = g
+    for world, (r1, r2, k) in ((1, (16, 16, 5)), (4, (16, 16, 5)), (4, (6, 8, 4)), (3, (10, 12, 6))):
+        blocks = row_partition(g, world)
+        cfg_a = ApmosConfig(local_rank=r1, global_rank=r2, k_modes=k)
+        modes, sig = run_simulated(world, lambda ctx: (gather_modes(ctx, apmos(ctx, blocks[ctx.rank], cfg_a)),
+                                                       None))[0][0], None
+        loc = run_simulated(world, lambda ctx: apmos(ctx, blocks[ctx.rank], cfg_a))[0]
+        out[f"gauss_p{world}_r{r1}_{r2}_{k}_modes"] = modes
+        out[f"gauss_p{world}_r{r1}_{r2}_{k}_sigma"] = loc.singular_values
+    c = synthetic_spectrum_matrix(48, 12, 2.0 ** -np.arange(6), seed=64)
+    out["spec_a"] = c
+    blocks = row_partition(c, 3)
+    sk = RandomSketchConfig(target_rank=6, oversampling=6, power_iterations=2, seed=9)
+    cfg_a = ApmosConfig(local_rank=12, global_rank=6, k_modes=3, use_randomized=True, sketch=sk)
+    out["spec_rand_modes"] = run_simulated(3, lambda ctx: gather_modes(ctx, apmos(ctx, blocks[ctx.rank], cfg_a)))[0]
+    out["spec_rand_sigma"] = run_simulated(3, lambda ctx: apmos(ctx, blocks[ctx.rank], cfg_a))[0].singular_values
+    a = burgers_matrix(BurgersConfig(grid_points=2048, n_snapshots=200))
+    out["burgers_sha"] = sha(a)
+    blocks = row_partition(a, 4)
+    cfg_a = ApmosConfig(local_rank=40, global_rank=30, k_modes=10)
+    out["burgers_p4_modes"] = run_simulated(4, lambda ctx: gather_modes(ctx, apmos(ctx, blocks[ctx.rank], cfg_a)))[0]
+    out["burgers_p4_sigma"] = run_simulated(4, lambda ctx: apmos(ctx, blocks[ctx.rank], cfg_a))[0].singular_values
+    save("apmos_cases", **out)
+
     with open(os.path.join(OUT, "PROVENANCE.txt"), "w") as f:
         f.write("generated by tests/golden/make_golden.py from the live reference parsvd "
                 f"{parsvd.__version__} at {REF_SRC}\n")

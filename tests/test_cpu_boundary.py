@@ -79,3 +79,16 @@ def test_product_never_imports_oracle():
             if f.endswith(".py"):
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
+
+
+def test_apmos_config_validation():
+    """ApmosConfig checks of dsvd.py:52-68 (host logic, no GPU)."""
+    import pytest
+    from paper_2108_08845_b200 import ApmosConfig, RandomSketchConfig
+    with pytest.raises(ValueError):
+        ApmosConfig(local_rank=0, global_rank=2, k_modes=1)
+    with pytest.raises(ValueError):
+        ApmosConfig(local_rank=4, global_rank=2, k_modes=3)
+    with pytest.raises(ValueError):
+        ApmosConfig(local_rank=4, global_rank=4, k_modes=2, sketch=RandomSketchConfig(target_rank=2))
+    assert ApmosConfig(local_rank=4, global_rank=4, k_modes=2).use_randomized is False

@@ -1,0 +1,134 @@
+"""APMOS one-shot distributed SVD (dsvd.py:39-173) on the GPU
+against the live reference's golden vectors and the pinned oracle."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _pkg():
+    import paper_2108_08845_b200 as p
+    return p
+
+
+def _blocks(a, world):
+    return [a[lo:hi] for lo, hi in oracle.partition_bounds(a.shape[0], world)]
+
+
+def test_apmos_single_rank_golden(golden):
+    p = _pkg()
+    g = golden("apmos_cases")
+    a = g["gauss_a"]
+    loc = p.apmos(p.RankContext(), a, p.ApmosConfig(local_rank=16, global_rank=16, k_modes=5))
+    m, s = loc.modes.cpu().numpy(), loc.singular_values.cpu().numpy()
+    assert oracle.sigma_rel_err(s, g["gauss_p1_r16_16_5_sigma"]) <= 1e-12
+    assert np.max(oracle.aligned_mode_difference(m, g["gauss_p1_r16_16_5_modes"])) <= 1e-9
+
+
+def test_apmos_burgers_emulated_ranks_match_golden(golden):
+    """The exchange is the rank-ordered concatenation of W_i = V_i S_i: build it from
+    per-block device right vectors exactly as four ranks would, then finish on one GPU."""
+    p = _pkg()
+    from paper_2108_08845_b200 import oneshot as am
+    from paper_2108_08845_b200 import _native as nat
+    g = golden("apmos_cases")
+    a = oracle.burgers_matrix(2048, 200)
+    dev = torch.device("cuda", 0)
+    ws = []
+    for blk in _blocks(a, 4):
+        w, _ = am._right_vectors(nat.as_device_colmajor(blk, dev), 40, dev, None)
+        ws.append(w)
+    W = nat.as_device_colmajor(torch.cat(ws, dim=1), dev)
+    X, lam = am._left_factor(W, 30, dev)
+    lam = lam[:10]
+    modes = np.concatenate([am._recompose(nat.as_device_colmajor(b, dev), X.view[:, :10] / lam, 10, dev).view
+                            .cpu().numpy() for b in _blocks(a, 4)], axis=0)
+    assert oracle.sigma_rel_err(lam.cpu().numpy(), g["burgers_p4_sigma"]) <= 1e-10
+    assert np.max(oracle.mode_angles(modes, g["burgers_p4_modes"])) <= 1e-8
+
+
+def _apmos_worker(rank, world, port, q, case):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2108_08845_b200 as p
+        if case == "gauss":
+            rng = np.random.Generator(np.random.Philox(42))
+            a = rng.standard_normal((64, 16))
+            cfg = p.ApmosConfig(local_rank=6, global_rank=8, k_modes=4)
+        else:
+            a = oracle.burgers_matrix(2048, 200)
+            sk = p.RandomSketchConfig(target_rank=30, oversampling=10, power_iterations=1, seed=3)
+            cfg = p.ApmosConfig(local_rank=40, global_rank=30, k_modes=10, use_randomized=True, sketch=sk)
+        blk = _blocks(a, world)[rank]
+        ctx = p.RankContext()
+        loc = p.apmos(ctx, blk, cfg)
+        full = p.gather_modes(ctx, loc)
+        if rank == 0:
+            q.put((full.cpu().numpy(), loc.singular_values.cpu().numpy()))
+    except Exception as e:
+        q.put(("error", repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case", ["gauss", "burgers_rand"])
+def test_apmos_two_ranks_match_oracle(case):
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_apmos_worker, args=(r, 2, port, q, case)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    m, sig = q.get(timeout=300)
+    for pr in procs:
+        pr.join(timeout=120)
+    assert not (isinstance(m, str) and m == "error"), sig
+    assert all(pr.exitcode == 0 for pr in procs)
+    if case == "gauss":
+        rng = np.random.Generator(np.random.Philox(42))
+        a = rng.standard_normal((64, 16))
+        rm, rs = oracle.ref_apmos(_blocks(a, 2), 6, 8, 4)
+    else:
+        a = oracle.burgers_matrix(2048, 200)
+        rm, rs = oracle.ref_apmos(_blocks(a, 2), 40, 30, 10, use_randomized=True, sketch=(30, 10, 1, 3))
+    assert oracle.sigma_rel_err(sig, rs) <= 1e-10
+    assert np.max(oracle.mode_angles(m, rm)) <= 1e-8
+
+
+def test_generate_right_vectors_both_methods():
+    p = _pkg()
+    rng = np.random.Generator(np.random.Philox(7))
+    a = rng.standard_normal((50, 12))
+    for method in ("svd", "gram"):
+        v, s = p.generate_right_vectors(a, 8, method=method)
+        rv, rs = oracle.ref_generate_right_vectors(a, 8, method=method)
+        assert oracle.sigma_rel_err(s.cpu().numpy(), rs) <= 1e-12
+        assert np.max(np.abs(v.cpu().numpy() - rv)) <= 1e-10  # same column signs as the reference
+    short = rng.standard_normal((5, 12))  # short block: zero-padded past min(rows, cols)
+    v, s = p.generate_right_vectors(short, 8)
+    assert np.all(s.cpu().numpy()[5:] == 0.0) and np.all(v.cpu().numpy()[:, 5:] == 0.0)
+    with pytest.raises(ValueError):
+        p.generate_right_vectors(a, 13)
+
+
+def test_apmos_errors():
+    p = _pkg()
+    from paper_2108_08845_b200.errors import DegenerateModeError
+    with pytest.raises(DegenerateModeError, match="mode 0"):
+        p.apmos(p.RankContext(), np.zeros((8, 6)), p.ApmosConfig(local_rank=3, global_rank=2, k_modes=2))
+    with pytest.raises(ValueError, match="global_rank"):
+        p.apmos(p.RankContext(), np.ones((3, 4)), p.ApmosConfig(local_rank=2, global_rank=5, k_modes=2))

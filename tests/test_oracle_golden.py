@@ -113,3 +113,25 @@ def test_metrics_resolve_tiny_angles():
     v = u + 1e-12 * rng.standard_normal(u.shape)
     ang = oracle.mode_angles(u, -v)
     assert np.all(ang < 1e-10) and np.all(ang > 0)
+
+
+def _blocks(a, world):
+    return [a[lo:hi] for lo, hi in oracle.partition_bounds(a.shape[0], world)]
+
+
+def test_apmos_oracle_matches_reference(golden):
+    g = golden("apmos_cases")
+    a = g["gauss_a"]
+    for world, (r1, r2, k) in ((1, (16, 16, 5)), (4, (16, 16, 5)), (4, (6, 8, 4)), (3, (10, 12, 6))):
+        m, s = oracle.ref_apmos(_blocks(a, world), r1, r2, k)
+        tag = f"gauss_p{world}_r{r1}_{r2}_{k}"
+        assert oracle.sigma_rel_err(s, g[tag + "_sigma"]) <= 1e-12
+        assert np.max(oracle.mode_angles(m, g[tag + "_modes"])) <= 1e-10
+        assert np.max(oracle.aligned_mode_difference(m, g[tag + "_modes"])) <= 1e-10
+    m, s = oracle.ref_apmos(_blocks(g["spec_a"], 3), 12, 6, 3, use_randomized=True, sketch=(6, 6, 2, 9))
+    assert oracle.sigma_rel_err(s, g["spec_rand_sigma"]) <= 1e-12
+    assert np.max(oracle.mode_angles(m, g["spec_rand_modes"])) <= 1e-10
+    b = oracle.burgers_matrix(2048, 200)
+    m, s = oracle.ref_apmos(_blocks(b, 4), 40, 30, 10)
+    assert oracle.sigma_rel_err(s, g["burgers_p4_sigma"]) <= 1e-12
+    assert np.max(oracle.mode_angles(m, g["burgers_p4_modes"])) <= 1e-9
