@@ -10,7 +10,9 @@ from .oneshot import ApmosConfig, apmos, generate_right_vectors  # noqa: F401
 from .datagen import burgers_device, burgers_matrix, burgers_solution, partition_bounds  # noqa: F401
 from .dsvd import (LocalModes, RankContext, gather_modes, parallel_stream_incorporate,  # noqa: F401
                    parallel_stream_initialize)
-from .errors import CapacityError, CollectiveTimeout, ConvergenceError, DegenerateModeError  # noqa: F401
+from .errors import (CapacityError, CollectiveTimeout, ConvergenceError, DegenerateModeError,  # noqa: F401
+                     MatrixFormatError)
+from .io import BatchSource, read_batches, read_matrix, read_matrix_header, read_submatrix, write_matrix  # noqa: F401
 from .linalg import RandomSketchConfig, low_rank_svd  # noqa: F401
 from .streaming import StreamConfig, StreamState, stream_all, stream_incorporate, stream_initialize  # noqa: F401
 

@@ -162,6 +162,12 @@ def main():
     out["burgers_p4_sigma"] = run_simulated(4, lambda ctx: apmos(ctx, blocks[ctx.rank], cfg_a))[0].singular_values
     save("apmos_cases", **out)
 
+    # ---- G8: a PARSVD01 matrix file written by the reference (io.py:27-32) ----
+    from parsvd.io import write_matrix
+    rng = np.random.Generator(np.random.Philox(77))
+    write_matrix(os.path.join(OUT, "sample_37x11.parsvd"), rng.standard_normal((37, 11)))
+    print("wrote sample_37x11.parsvd")
+
     with open(os.path.join(OUT, "PROVENANCE.txt"), "w") as f:
         f.write("generated by tests/golden/make_golden.py from the live reference parsvd "
                 f"{parsvd.__version__} at {REF_SRC}\n")

@@ -517,3 +517,28 @@ def test_config2_shapes_run_on_the_tma_kernels():
     p.stream_all([a[:, i:i + 200] for i in range(0, 800, 200)], rcfg)
     d = [x - y for x, y in zip(nat.path_counters(c), before)]
     assert d[0] > 0 and d[2] == 0 and d[3] == 0 and d[4] == 0, d
+
+
+def test_stream_all_from_parsvd_file_pinned_prefetch(tmp_path):
+    """§8(f) batch ingestion: a PARSVD01 file read by a background thread into pinned
+    column-major batches, uploaded on the copy stream while earlier batches update:
+    bitwise the result of the device-resident stream, and the oracle's."""
+    p = _pkg()
+    a = oracle.burgers_matrix(12000, 800)
+    path = tmp_path / "burgers.parsvd"
+    p.write_matrix(path, a)
+    cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200)
+    s_dev, _ = p.stream_all([torch.from_numpy(np.asfortranarray(a[:, i:i + 200])).cuda() for i in range(0, 800, 200)],
+                            cfg)
+    src = p.BatchSource.from_file(path, 200, pinned=True, prefetch=2)
+    batches = list(src)
+    assert all(b.is_pinned() and b.stride(0) == 1 for b in batches)
+    s_file, _ = p.stream_all(p.BatchSource.from_file(path, 200, pinned=True, prefetch=2), cfg)
+    assert torch.equal(s_file.modes, s_dev.modes) and torch.equal(s_file.singular_values, s_dev.singular_values)
+    rm, rs, _ = oracle.ref_stream_all(_batches(a, 200), 10, 0.95)
+    m, s = _np(s_file)
+    _assert_parity(m, s, rm, rs)
+    # a rank's row block straight from the file
+    lo, hi = p.partition_bounds(12000, 3)[1]
+    part = np.concatenate([b.numpy() for b in p.BatchSource(200, path=path, rows=(lo, hi), pinned=True)], axis=1)
+    assert np.array_equal(part, a[lo:hi])
