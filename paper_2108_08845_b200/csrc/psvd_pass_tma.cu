@@ -21,6 +21,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 
@@ -48,6 +49,16 @@ PSVD_DEV void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uin
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
           "r"(saddr(dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(saddr(bar))
+      : "memory");
+}
+
+// multicast variant: the box lands at the same smem offset in every CTA of ctaMask and
+// signals the mbarrier at the same offset in each of them
+PSVD_DEV void tma_load_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(saddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(saddr(bar)), "h"(mask)
       : "memory");
 }
 
@@ -306,9 +317,14 @@ size_t gram_tma_smem_bytes(int np_pad) {
   return 1024 + sizeof(double) * (size_t)GNS * 2 * np_pad * TKS + 2 * GNS * sizeof(uint64_t) + 64;
 }
 
+// MC: the two slice CTAs of a row chunk form a cluster and share every stage through
+// TMA multicast (each producer loads one 16-row half into both CTAs), so the panel is
+// read from HBM/L2 once instead of once per slice.  Consumers release a ring slot on
+// both CTAs' empty barriers (the producer overwrites it in both).
+template <bool MC>
 __global__ void __launch_bounds__(NTHR, 1)
     gram_tma_kernel(const __grid_constant__ TallParams p, const __grid_constant__ TmaMaps maps, const TmaExtra x) {
-  if (p.gate != nullptr && *p.gate == 0) return;
+  if (p.gate != nullptr && *p.gate == 0) return;  // uniform over the grid (and a cluster)
   extern __shared__ unsigned char smem_raw[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tq = lane & 3;
@@ -321,8 +337,16 @@ __global__ void __launch_bounds__(NTHR, 1)
   double* sP = reinterpret_cast<double*>(base);  // [stage][half][np_pad][16]
   uint64_t* full = reinterpret_cast<uint64_t*>(sP + (size_t)GNS * 2 * np_pad * TKS);
   uint64_t* empty = full + GNS;
+  unsigned crank = 0;
+  if (MC) asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(crank));
   int ncons = 0;
   for (int w = 0; w < PROD_WARP; ++w) ncons += p.plan[slice][w].ntile > 0;
+  int nrel = ncons;  // arrivals that release a ring slot
+  if (MC) {
+    nrel = 0;
+    for (int s2 = 0; s2 < 2; ++s2)
+      for (int w = 0; w < PROD_WARP; ++w) nrel += p.plan[s2][w].ntile > 0;
+  }
   for (int i = tid; i < GNS * 2 * np_pad; i += NTHR) {
     const int c = i % np_pad;
     if (!x.written[c >> 3]) {
@@ -334,12 +358,13 @@ __global__ void __launch_bounds__(NTHR, 1)
   if (tid == 0) {
     for (int b = 0; b < GNS; ++b) {
       mbar_init(&full[b], 1);
-      mbar_init(&empty[b], (unsigned)max(ncons, 1));
+      mbar_init(&empty[b], (unsigned)max(nrel, 1));
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   __syncthreads();
+  if (MC) asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   const int64_t nstage = row_end > row_begin ? (row_end - row_begin + 2 * TKS - 1) / (2 * TKS) : 0;
 
   if (warp == PROD_WARP) {
@@ -347,86 +372,125 @@ __global__ void __launch_bounds__(NTHR, 1)
       for (int64_t s = 0; s < nstage; ++s) {
         const int b = (int)(s % GNS);
         if (s >= GNS) mbar_wait(&empty[b], (unsigned)(((s / GNS) - 1) & 1));
-        mbar_expect_tx(&full[b], 2 * x.stage_bytes);
-        for (int h = 0; h < 2; ++h) {
+        mbar_expect_tx(&full[b], 2 * x.stage_bytes);  // both halves land here (one per producer when MC)
+        for (int h = MC ? (int)crank : 0; h < (MC ? (int)crank + 1 : 2); ++h) {
           double* dst = sP + ((size_t)b * 2 + h) * np_pad * TKS;
           const int r0 = (int)(row_begin + s * 2 * TKS + h * TKS);
-          for (int o = 0; o < x.nops; ++o)
-            tma_load_2d(dst + (size_t)x.op_pcol[o] * TKS, &maps.m[x.op_seg[o]], r0, x.op_col[o], &full[b]);
+          for (int o = 0; o < x.nops; ++o) {
+            if (MC)
+              tma_load_2d_mc(dst + (size_t)x.op_pcol[o] * TKS, &maps.m[x.op_seg[o]], r0, x.op_col[o], &full[b], 0x3);
+            else
+              tma_load_2d(dst + (size_t)x.op_pcol[o] * TKS, &maps.m[x.op_seg[o]], r0, x.op_col[o], &full[b]);
+          }
         }
       }
     }
-    return;
-  }
-  const WarpPlan wp = p.plan[slice][warp];
-  if (wp.ntile == 0) return;
-  double acc[4][4][2];
+  } else if (p.plan[slice][warp].ntile > 0) {
+    const WarpPlan wp = p.plan[slice][warp];
+    double acc[4][4][2];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
-  const int I = wp.ti[0], J = wp.tj[0];
-  const int nva = min(4, (p.np - I * 32 + 7) / 8), nvb = min(4, (p.np - J * 32 + 7) / 8);
-  auto stage_loop = [&](auto na_t, auto nb_t, auto diag_t) {
-    constexpr int NA = decltype(na_t)::value, NB = decltype(nb_t)::value;
-    constexpr bool DIAG = decltype(diag_t)::value;
-    for (int64_t s = 0; s < nstage; ++s) {
-      const int b = (int)(s % GNS);
-      mbar_wait(&full[b], (unsigned)((s / GNS) & 1));
+      for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+    const int I = wp.ti[0], J = wp.tj[0];
+    const int nva = min(4, (p.np - I * 32 + 7) / 8), nvb = min(4, (p.np - J * 32 + 7) / 8);
+    uint32_t peer_empty = 0;
+    if (MC) {
+      const uint32_t loc = saddr(&empty[0]);
+      asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(peer_empty) : "r"(loc), "r"(crank ^ 1u));
+    }
+    auto stage_loop = [&](auto na_t, auto nb_t, auto diag_t) {
+      constexpr int NA = decltype(na_t)::value, NB = decltype(nb_t)::value;
+      constexpr bool DIAG = decltype(diag_t)::value;
+      for (int64_t s = 0; s < nstage; ++s) {
+        const int b = (int)(s % GNS);
+        mbar_wait(&full[b], (unsigned)((s / GNS) & 1));
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const double* H = sP + ((size_t)b * 2 + h) * np_pad * TKS;
-        const double* bI = H + (size_t)I * 32 * TKS;
-        const double* bJ = H + (size_t)J * 32 * TKS;
+        for (int h = 0; h < 2; ++h) {
+          const double* H = sP + ((size_t)b * 2 + h) * np_pad * TKS;
+          const double* bI = H + (size_t)I * 32 * TKS;
+          const double* bJ = H + (size_t)J * 32 * TKS;
 #pragma unroll
-        for (int kk = 0; kk < TKS / 4; ++kk) {
-          const int k = kk * 4 + tq;
-          double fa[NA], fb[NB];
+          for (int kk = 0; kk < TKS / 4; ++kk) {
+            const int k = kk * 4 + tq;
+            double fa[NA], fb[NB];
 #pragma unroll
-          for (int q = 0; q < NA; ++q) fa[q] = bI[swz(q * 8 + g, k)];
+            for (int q = 0; q < NA; ++q) fa[q] = bI[swz(q * 8 + g, k)];
 #pragma unroll
-          for (int q = 0; q < NB; ++q) fb[q] = bJ[swz(q * 8 + g, k)];
+            for (int q = 0; q < NB; ++q) fb[q] = bJ[swz(q * 8 + g, k)];
 #pragma unroll
-          for (int a = 0; a < NA; ++a)
+            for (int a = 0; a < NA; ++a)
 #pragma unroll
-            for (int c = 0; c < NB; ++c)
-              if (!DIAG || c >= a) dmma884(acc[a][c][0], acc[a][c][1], fa[a], fb[c]);
+              for (int c = 0; c < NB; ++c)
+                if (!DIAG || c >= a) dmma884(acc[a][c][0], acc[a][c][1], fa[a], fb[c]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&empty[b]);
+          if (MC) {
+            const uint32_t remote = peer_empty + (uint32_t)(b * sizeof(uint64_t));
+            asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(remote) : "memory");
+          }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[b]);
+    };
+    using F = std::false_type;
+    using T = std::true_type;
+    using I1 = std::integral_constant<int, 1>;
+    using I2 = std::integral_constant<int, 2>;
+    using I3 = std::integral_constant<int, 3>;
+    using I4 = std::integral_constant<int, 4>;
+    if (I != J) {
+      if (nvb == 4) stage_loop(I4{}, I4{}, F{});
+      else if (nvb == 3) stage_loop(I4{}, I3{}, F{});
+      else if (nvb == 2) stage_loop(I4{}, I2{}, F{});
+      else stage_loop(I4{}, I1{}, F{});
+    } else {
+      if (nva == 4) stage_loop(I4{}, I4{}, T{});
+      else if (nva == 3) stage_loop(I3{}, I3{}, T{});
+      else if (nva == 2) stage_loop(I2{}, I2{}, T{});
+      else stage_loop(I1{}, I1{}, T{});
     }
-  };
-  using F = std::false_type;
-  using T = std::true_type;
-  using I1 = std::integral_constant<int, 1>;
-  using I2 = std::integral_constant<int, 2>;
-  using I3 = std::integral_constant<int, 3>;
-  using I4 = std::integral_constant<int, 4>;
-  if (I != J) {
-    if (nvb == 4) stage_loop(I4{}, I4{}, F{});
-    else if (nvb == 3) stage_loop(I4{}, I3{}, F{});
-    else if (nvb == 2) stage_loop(I4{}, I2{}, F{});
-    else stage_loop(I4{}, I1{}, F{});
-    (void)nva;
-  } else {
-    if (nva == 4) stage_loop(I4{}, I4{}, T{});
-    else if (nva == 3) stage_loop(I3{}, I3{}, T{});
-    else if (nva == 2) stage_loop(I2{}, I2{}, T{});
-    else stage_loop(I1{}, I1{}, T{});
+    double* dst = p.partial + ((size_t)blockIdx.x * SLOTS + warp * TPW) * 1024;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<double2*>(dst + (a * 8 + g) * 32 + c * 8 + 2 * tq) =
+            make_double2(acc[a][c][0], acc[a][c][1]);
   }
-  double* dst = p.partial + ((size_t)blockIdx.x * SLOTS + warp * TPW) * 1024;
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      *reinterpret_cast<double2*>(dst + (a * 8 + g) * 32 + c * 8 + 2 * tq) = make_double2(acc[a][c][0], acc[a][c][1]);
+  // neither CTA may exit while its peer can still multicast into it or arrive on its barriers
+  if (MC) {
+    __syncwarp();
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  }
 }
 
 void launch_gram_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x, int grid, cudaStream_t st) {
   const size_t smem = gram_tma_smem_bytes(p.np_pad);
-  cudaFuncSetAttribute(gram_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  gram_tma_kernel<<<grid, NTHR, smem, st>>>(p, maps, x);
+  // Multicast halves the panel traffic of a two-slice Gram but couples the two CTAs' pace
+  // (measured slower at B = 200: 25.8 vs 29.7 TF/s), so it is opt-in (PSVD_GRAM_MULTICAST=1).
+  static const bool mc = getenv("PSVD_GRAM_MULTICAST") != nullptr;
+  if (p.nslices == 2 && grid % 2 == 0 && mc) {
+    cudaFuncSetAttribute(gram_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(NTHR);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, gram_tma_kernel<true>, p, maps, x);
+    return;
+  }
+  cudaFuncSetAttribute(gram_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  gram_tma_kernel<false><<<grid, NTHR, smem, st>>>(p, maps, x);
 }
 
 // ---------------------------------------------------------------- host side
