@@ -839,9 +839,13 @@ static int exchange_sign(psvd_ctx* c, const double* local_pairs, int nchunks, in
 static int svqb(psvd_ctx* c, const double* Gs, int l, double* T, double* sig_scratch, cudaStream_t st) {
   int rc = ensure(c, c->eigws, sizeof(double) * std::max(eig_workspace_doubles(l, l), jacobi_workspace_doubles(l, l)));
   if (rc) return rc;
-  launch_jacobi_svd(Gs, l, l, sig_scratch, T, (double*)c->eigws.ptr, c->d_status, st);
-  launch_svqb_scale(T, sig_scratch, l, 1e-7, st);
-  c->launches += 2;
+  // CholeskyQR weights T = R^-1 first (one short kernel); when the sketch is ill conditioned
+  // (max R_ii / min R_ii > 1e6 or a dropped pivot) the gated Jacobi SVQB overwrites them
+  int* illcond = c->d_status + 3;
+  launch_chol_inv(Gs, l, T, st, illcond);
+  launch_jacobi_svd(Gs, l, l, sig_scratch, T, (double*)c->eigws.ptr, c->d_status, st, illcond);
+  launch_svqb_scale(T, sig_scratch, l, 1e-7, st, illcond);
+  c->launches += 3;
   return cuda_check(c, "svqb");
 }
 

@@ -42,7 +42,8 @@ void launch_small_gemm(const double* A, int lda, int transA, const double* B, in
 template <bool SMEM>
 __global__ void __launch_bounds__(1024, 1)
 jacobi_svd_kernel(const double* __restrict__ Zin, int n, int l, double* __restrict__ S, double* __restrict__ Jout,
-                  double* __restrict__ ws, int* __restrict__ status) {
+                  double* __restrict__ ws, int* __restrict__ status, const int* __restrict__ gate) {
+  if (gate != nullptr && *gate == 0) return;  // the CholeskyQR route was well conditioned
   extern __shared__ double sm[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int le = l + (l & 1);  // even number of columns (a zero column pads odd l)
@@ -155,18 +156,21 @@ size_t jacobi_workspace_doubles(int n, int l) { return (size_t)n * (l + 1); }
 // SVQB weights from the Jacobi eigen-decomposition of an l x l SPD Gram (S = eigenvalues,
 // descending; T = eigenvectors): T[:, k] *= 1 / sqrt(S_k), or 0 for directions with
 // sqrt(S_k) <= tol * sqrt(S_0) (numerically null, dropped).
-__global__ void svqb_scale_kernel(double* __restrict__ T, const double* __restrict__ S, int l, double tol) {
+__global__ void svqb_scale_kernel(double* __restrict__ T, const double* __restrict__ S, int l, double tol,
+                                  const int* __restrict__ gate) {
+  if (gate != nullptr && *gate == 0) return;
   const int k = blockIdx.x;
   const double s0 = sqrt(fmax(S[0], 0.0)), sk = sqrt(fmax(S[k], 0.0));
   const double inv = (sk > 0.0 && sk > tol * s0) ? 1.0 / sk : 0.0;
   for (int i = threadIdx.x; i < l; i += blockDim.x) T[(size_t)k * l + i] *= inv;
 }
 
-void launch_svqb_scale(double* T, const double* S, int l, double tol, cudaStream_t st) {
-  svqb_scale_kernel<<<l, 32, 0, st>>>(T, S, l, tol);
+void launch_svqb_scale(double* T, const double* S, int l, double tol, cudaStream_t st, const int* gate) {
+  svqb_scale_kernel<<<l, 32, 0, st>>>(T, S, l, tol, gate);
 }
 
-void launch_jacobi_svd(const double* Z, int n, int l, double* S, double* J, double* ws, int* status, cudaStream_t st) {
+void launch_jacobi_svd(const double* Z, int n, int l, double* S, double* J, double* ws, int* status, cudaStream_t st,
+                       const int* gate) {
   const int le = l + (l & 1);
   const size_t small = (size_t)le * le + 32 + le + le + 8;
   const size_t limit = 227 * 1024 / sizeof(double);
@@ -175,11 +179,11 @@ void launch_jacobi_svd(const double* Z, int n, int l, double* S, double* J, doub
     cudaFuncSetAttribute(jacobi_svd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // one warp per column pair (fewer idle warps at the round barriers for small l)
     const int thr = std::min(1024, std::max(64, 32 * (le / 2)));
-    jacobi_svd_kernel<true><<<1, thr, smem, st>>>(Z, n, l, S, J, ws, status);
+    jacobi_svd_kernel<true><<<1, thr, smem, st>>>(Z, n, l, S, J, ws, status, gate);
   } else {
     const size_t smem = small * sizeof(double);
     cudaFuncSetAttribute(jacobi_svd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    jacobi_svd_kernel<false><<<1, 1024, smem, st>>>(Z, n, l, S, J, ws, status);
+    jacobi_svd_kernel<false><<<1, 1024, smem, st>>>(Z, n, l, S, J, ws, status, gate);
   }
 }
 
@@ -188,7 +192,8 @@ void launch_jacobi_svd(const double* Z, int n, int l, double* S, double* J, doub
 // orthonormalization pass of a sketch whose Gram is already ~I (CholeskyQR2's
 // refinement step); columns of a numerically null direction (pivot <= tiny)
 // are zeroed, matching the first (SVQB) pass which dropped them.
-__global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restrict__ G, int l, double* __restrict__ T) {
+__global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restrict__ G, int l, double* __restrict__ T,
+                                                           int* __restrict__ illcond) {
   extern __shared__ double sm[];
   double* R = sm;          // l x l col-major, upper used
   double* X = R + l * l;   // inverse
@@ -223,12 +228,23 @@ __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restr
   }
   __syncthreads();
   for (int idx = tid; idx < l * l; idx += nthr) T[idx] = X[idx];
+  if (illcond != nullptr && tid == 0) {
+    // CholeskyQR2 keeps O(eps) orthogonality for cond(Y) < ~1e7: flag anything beyond
+    // cond(Y) ~ max R_ii / min R_ii > 1e6, or a dropped pivot, for the SVQB route
+    double rmax = 0.0, rmin = DBL_MAX;
+    for (int i = 0; i < l; ++i) {
+      const double d = R[(size_t)i * l + i];
+      rmax = fmax(rmax, d);
+      rmin = fmin(rmin, d);
+    }
+    *illcond = !(rmin > 0.0 && rmax <= 1e6 * rmin);
+  }
 }
 
-void launch_chol_inv(const double* G, int l, double* T, cudaStream_t st) {
+void launch_chol_inv(const double* G, int l, double* T, cudaStream_t st, int* illcond) {
   const size_t smem = 2 * (size_t)l * l * sizeof(double);
   cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  chol_inv_kernel<<<1, 1024, smem, st>>>(G, l, T);
+  chol_inv_kernel<<<1, 1024, smem, st>>>(G, l, T, illcond);
 }
 
 // ---------------------------------------------------------------- tall sign rule
