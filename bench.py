@@ -374,18 +374,20 @@ def time_randomized(a, D, M, dev, c, stream, q):
     sk = RandomSketchConfig(target_rank=K, oversampling=10, power_iterations=q, seed=0)
     l = sk.sketch_width
     st = nat._vp(stream.cuda_stream)
+    nb = SNAPS // BATCH
     om = {n: device_omega(n, sk, dev) for n in (BATCH, K + BATCH)}
-    Ub = [nat.DevMat.empty(M, K, dev) for _ in range(2)]
-    sig = [torch.zeros(K, dtype=torch.float64, device=dev) for _ in range(2)]
+    Uo = nat.DevMat.empty(M, K, dev)
+    hist = torch.empty((nb, K), dtype=torch.float64, device=dev)
+    Aptr = (nat._vp * nb)(*[nat._vp(D.data_ptr() + 8 * D.ld * b * BATCH) for b in range(nb)])
+    Ald = (ctypes.c_int64 * nb)(*([D.ld] * nb))
+    Bc = (ctypes.c_int * nb)(*([BATCH] * nb))
+    Om = (nat._vp * nb)(*[nat._vp(om[(0 if b == 0 else K) + BATCH].data_ptr()) for b in range(nb)])
 
     def step():
-        cur = 0
-        for b in range(SNAPS // BATCH):
-            kc = 0 if b == 0 else K
-            nat.call("psvd_rand_update", c, M, nat._vp(Ub[cur].data_ptr()), Ub[cur].ld, nat.ptr(sig[cur]), FF, kc,
-                     nat._vp(D.data_ptr() + 8 * D.ld * b * BATCH), D.ld, BATCH, K, l, q, nat.ptr(om[kc + BATCH]),
-                     nat._vp(Ub[cur ^ 1].data_ptr()), Ub[cur ^ 1].ld, nat.ptr(sig[cur ^ 1]), st)
-            cur ^= 1
+        # the whole stream through psvd_rand_stream_run (pipelined: the next batch's sketch
+        # A Omega[K:] overlaps the small solves; U written once at the end)
+        nat.call("psvd_rand_stream_run", c, M, nat._vp(0), 0, nat._vp(0), 0, nb, Aptr, Ald, Bc, K, l, q, FF, Om,
+                 nat._vp(Uo.data_ptr()), Uo.ld, nat.ptr(hist), None, st)
 
     for _ in range(a.warmup):
         step()

@@ -181,6 +181,19 @@ int psvd_rand_update(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, con
                      int Kc, const double* A, int64_t lda, int B, int K, int l, int q, const double* Omega,
                      double* U_out, int64_t ldo, double* sigma_out, void* stream);
 
+/* Randomized stream over nb device batches (reference: stream_all with the R9 composition,
+ * i.e. low_rank_svd([ff U S | A_b]) per batch, linalg.py:126-162 + streaming.py:119-133),
+ * pipelined: the state between updates stays a sketch basis (U is written once, to U_out), and
+ * the state-independent sketch A_{b+1} Omega[K:] of the next batch runs on a low-priority stream
+ * while the one-CTA small solves of batch b run.  Omega[b]: the (n_b x l) test matrix of batch b
+ * (col-major, ld n_b; n_b = K + B[b] after the first update, B[0] when Kc = 0).  sigma_hist:
+ * nb x K singular values per update.  Requires l <= 32 (returns PSVD_EINVAL otherwise: use
+ * psvd_rand_update per batch) and no exchange hooks (single GPU). */
+int psvd_rand_stream_run(psvd_ctx* ctx, int64_t M, const double* U_in, int64_t ldu, const double* sigma_in, int Kc,
+                         int nb, const double* const* A, const int64_t* lda, const int* B, int K, int l, int q,
+                         double ff, const double* const* Omega, double* U_out, int64_t ldo, double* sigma_hist,
+                         void* const* batch_ready, void* stream);
+
 /* ---- row-parallel helpers ---- */
 
 /* out (n x n) = sum_r parts[r] in rank order (parts: P contiguous n x n blocks);

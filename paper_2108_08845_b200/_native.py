@@ -59,6 +59,9 @@ _SIGS = {
                                  _c_i64, _vp, ctypes.POINTER(_c_int), ctypes.POINTER(_vp), _vp]),
     "psvd_rand_update": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_int, _vp, _c_i64, _c_int, _c_int,
                                   _c_int, _c_int, _vp, _vp, _c_i64, _vp, _vp]),
+    "psvd_rand_stream_run": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_int, _c_int, ctypes.POINTER(_vp),
+                                      ctypes.POINTER(_c_i64), ctypes.POINTER(_c_int), _c_int, _c_int, _c_int,
+                                      _c_dbl, ctypes.POINTER(_vp), _vp, _c_i64, _vp, ctypes.POINTER(_vp), _vp]),
     "psvd_sum_ordered": (_c_int, [_vp, _vp, _c_int, _c_i64, _vp, _vp]),
     "psvd_burgers": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_dbl,
                               _c_dbl, _c_dbl, _vp]),

@@ -50,6 +50,8 @@ struct psvd_ctx {
   int ex_nranks = 1;
   int64_t ex_row_offset = 0;
   Buf partial2, tiles2[2];  // A^T A passes on the low-priority stream (double-buffered tiles)
+  Buf zbuf, rs2;            // pipelined randomized stream: look-ahead sketch Z = A Omega_A, small matrices
+  cudaEvent_t ev_qready = nullptr;  // pipelined randomized stream: the sketch basis of the last update is final
   cudaStream_t s_hi = nullptr, s_lo = nullptr;  // pipelined stream_run: critical chain / look-ahead Grams
   cudaStream_t s_aux = nullptr;                  // concurrent LDL^T of the split core solve
   cudaEvent_t ev_ldlt_fork = nullptr, ev_ldlt_join = nullptr, ev_eig_start = nullptr;
@@ -259,7 +261,8 @@ static int plan_tiles_tma(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int
 // Common pass setup.  segs: panel segments; w/W: optional Y = P[:, wlo:wlo+wk] * W.
 int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, int wlo, int wk, int w,
               const double* W, int64_t ldw, bool gram_pp, bool gram_yy, bool gram_py, int py_cols = -1,
-              int pp_rows = -1, Buf* part = nullptr, Buf* tl = nullptr, int max_ctas = 0, int py_lo = 0) {
+              int pp_rows = -1, Buf* part = nullptr, Buf* tl = nullptr, int max_ctas = 0, int py_lo = 0,
+              bool gaps_ok = false) {
   memset(&ps.p, 0, sizeof(ps.p));
   ps.part = part ? part : &c->partial;
   ps.tl = tl ? tl : &c->tiles;
@@ -292,7 +295,8 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
     for (size_t i = 0; i < segs.size(); ++i)
       tma = tma && aligned16(segs[i].ptr) && segs[i].ld % 2 == 0 && segs[i].ncols > 0;
     bool use_gaps = true;
-    if (gram_py && py_lo >= 0 && !same) {
+    // gaps_ok: the caller extracts by segment (p.seg[i].col0), so the gapped layout is fine
+    if (gram_py && py_lo >= 0 && !same && !gaps_ok) {
       // P-tiles at fixed logical blocks: keep the contiguous layout, shifted right by pshift so
       // that every segment after the first starts on an 8-column boundary (the first one's box
       // starts out of bounds, zero filled)
@@ -520,6 +524,7 @@ int psvd_create(int device, psvd_ctx** out) {
     }
     cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_qready, cudaEventDisableTiming);
   }
   cudaDeviceSynchronize();
   *out = c;
@@ -531,7 +536,8 @@ int psvd_destroy(psvd_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   Buf* bufs[] = {&c->partial, &c->tiles, &c->gram, &c->eigws, &c->wbuf, &c->utu, &c->tbuf, &c->dvec, &c->colmax,
-                 &c->ybuf, &c->ybuf2, &c->xpairs, &c->ssws, &c->rsmall, &c->jacws, &c->partial2, &c->tiles2[0], &c->tiles2[1]};
+                 &c->ybuf, &c->ybuf2, &c->xpairs, &c->ssws, &c->rsmall, &c->jacws, &c->partial2, &c->tiles2[0], &c->tiles2[1],
+                 &c->zbuf, &c->rs2};
   for (Buf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
   if (c->s_hi) cudaStreamDestroy(c->s_hi);
@@ -546,6 +552,7 @@ int psvd_destroy(psvd_ctx* c) {
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->ev_qready) cudaEventDestroy(c->ev_qready);
   cudaFree(c->d_status);
   cudaFree(c->d_timers);
   cudaFreeHost(c->h_status);
@@ -842,7 +849,7 @@ static int svqb(psvd_ctx* c, const double* Gs, int l, double* T, double* sig_scr
   // CholeskyQR weights T = R^-1 first (one short kernel); when the sketch is ill conditioned
   // (max R_ii / min R_ii > 1e6 or a dropped pivot) the gated Jacobi SVQB overwrites them
   int* illcond = c->d_status + 3;
-  launch_chol_inv(Gs, l, T, st, illcond);
+  launch_chol_inv(Gs, l, T, st, illcond, c->d_status);
   launch_jacobi_svd(Gs, l, l, sig_scratch, T, (double*)c->eigws.ptr, c->d_status, st, illcond);
   launch_svqb_scale(T, sig_scratch, l, 1e-7, st, illcond);
   c->launches += 3;
@@ -1211,6 +1218,295 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
     cudaFree(tbuf);
   }
   return cuda_check(c, "stream_run");
+}
+
+// Pipelined randomized stream (SURVEY §8 R9 over a batch list; reference linalg.py:126-162 composed
+// per batch).  The state between updates is the sketch basis Q_b = Y1_b (M x l) plus small weights
+// (U_b = Q_b Wf_b diag(s_b)), so U is materialized once, at the end.  Per update b:
+//   hi:  sign pass over Q_{b-1} (argmax of Q Wf)  ->  G1 = Y^T Y for Y = Q C + Z_b (small)  ->  SVQB
+//        ->  projection pass over [Q_{b-1} | Z_b | A_b]: Y1 = (Q C + Z_b) T1, Y1^T Y1, [Q | A]^T Y1
+//        ->  [power iterations: sketch pass over [Q | A], projection pass]  ->  Cholesky, Jacobi SVD
+//   lo:  Z_{b+1} = A_{b+1} Omega[K:] with Q_b^T Z_{b+1} and Z^T Z (the state-independent half of the
+//        next sketch), started as soon as Q_b is final so it overlaps the one-SM small solves.
+// Same arithmetic as psvd_rand_update per batch up to rounding (U is replaced by Q Wf diag(s)).
+int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, const double* sigma_in, int Kc,
+                         int nb, const double* const* A, const int64_t* lda, const int* B, int K, int l, int q,
+                         double ff, const double* const* Omega, double* U_out, int64_t ldo, double* sigma_hist,
+                         void* const* batch_ready, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  if (nb < 1 || !A || !lda || !B || !Omega || !U_out || !sigma_hist)
+    return fail(c, PSVD_EINVAL, "bad rand_stream_run arguments");
+  if (K < 1 || l < K || q < 0) return fail(c, PSVD_EINVAL, "bad sketch K=%d l=%d q=%d", K, l, q);
+  if (l > TMA_MAX_Y || !tma_available())
+    return fail(c, PSVD_EINVAL, "sketch width %d not supported by the pipelined run (use psvd_rand_update)", l);
+  if (c->ex_allreduce) return fail(c, PSVD_EINVAL, "the pipelined randomized run is single-GPU");
+  if (Kc != 0 && Kc != K) return fail(c, PSVD_EINVAL, "initial state carries %d modes, K=%d", Kc, K);
+  if (Kc > 0 && (!U_in || !sigma_in)) return fail(c, PSVD_EINVAL, "null initial state");
+  int rc;
+  int bmax = 0;
+  for (int b = 0; b < nb; ++b) {
+    if ((rc = check_mat(c, "A", A[b], lda[b], M, B[b]))) return rc;
+    if (B[b] < 1) return fail(c, PSVD_EINVAL, "empty batch");
+    if (!Omega[b]) return fail(c, PSVD_EINVAL, "null Omega");
+    const int n = ((b > 0 || Kc > 0) ? K : 0) + B[b];
+    if (l > std::min<int64_t>(M, n))
+      return fail(c, PSVD_EINVAL, "sketch width %d exceeds min(a.shape) = %lld", l, (long long)std::min<int64_t>(M, n));
+    bmax = std::max(bmax, B[b]);
+  }
+  if (Kc == 0 && B[0] < K) return fail(c, PSVD_EINVAL, "initial batch has %d columns, need at least k_modes=%d", B[0], K);
+  if ((rc = check_mat(c, "U_out", U_out, ldo, M, K))) return rc;
+  if (Kc > 0 && (rc = check_mat(c, "U_in", U_in, ldu, M, K))) return rc;
+  const int64_t ldq = M + (M & 1);
+  if ((rc = ensure(c, c->ybuf, sizeof(double) * (size_t)ldq * l)) ||
+      (rc = ensure(c, c->ybuf2, sizeof(double) * (size_t)ldq * l)) ||
+      (rc = ensure(c, c->zbuf, sizeof(double) * (size_t)ldq * l)))
+    return rc;
+  double* Qb[2] = {(double*)c->ybuf.ptr, (double*)c->ybuf2.ptr};
+  double* Zt = (double*)c->zbuf.ptr;
+  const int nmax = K + bmax;
+  const size_t ll = (size_t)l * l, nl = (size_t)nmax * l;
+  const size_t need = (size_t)l * K + 4 * ll + 2 * ll + 2 * ll + ll + 5 * nl + ll + (size_t)(l + bmax) * l + 2 * l +
+                      2 * (size_t)l * K + K + 2 * (size_t)K * K + K + 64;
+  if ((rc = ensure(c, c->rs2, sizeof(double) * need))) return rc;
+  double* p_ = (double*)c->rs2.ptr;
+  auto take = [&](size_t n_) { double* r = p_; p_ += n_; return r; };
+  double* Etop = take((size_t)l * K);
+  double* Cm = take(ll);
+  double* G1 = take(ll);
+  double* T1 = take(ll);
+  double* Wb = take(2 * ll);
+  double* G2[2] = {take(ll), take(ll)};
+  double* T2 = take(ll);
+  double* X = take(nl);
+  double* Zs = take(nl);
+  double* Z1 = take(nl);
+  double* Qz = take(nl);
+  double* Bt = take(nl);
+  double* Tz = take(ll);
+  double* W0 = take((size_t)(l + bmax) * l);
+  double* S = take(l);
+  double* sscr = take(l);
+  double* J = take(ll);
+  double* Wf[2] = {take((size_t)l * K), take((size_t)l * K)};
+  double* sgn = take(K);
+  double* WfI = take((size_t)K * K);
+  double* QtQ0 = take((size_t)K * K);
+  double* ones = take(K);
+  if ((rc = ensure(c, c->jacws, sizeof(double) * jacobi_workspace_doubles(nmax, l)))) return rc;
+  cudaStream_t user = (cudaStream_t)stream, hi = c->s_hi, lo = c->s_lo;
+  // PSVD_TRACE=1: timeline of the two streams on stderr (diagnostics; %globaltimer stamps)
+  static const bool trace = getenv("PSVD_TRACE") != nullptr;
+  std::vector<std::string> tl;
+  unsigned long long* tbuf = nullptr;
+  if (trace) cudaMallocManaged(&tbuf, 512 * sizeof(unsigned long long));
+  auto mark = [&](const char* what, int b, cudaStream_t s_) {
+    if (!trace || tl.size() >= 512) return;
+    stamp_kernel<<<1, 1, 0, s_>>>(tbuf + tl.size());
+    tl.push_back(std::string(what) + "[" + std::to_string(b) + "]");
+  };
+  mark("start", 0, user);
+  cudaEventRecord(c->ev_fork, user);
+  cudaStreamWaitEvent(hi, c->ev_fork, 0);
+  cudaStreamWaitEvent(lo, c->ev_fork, 0);
+  if (Kc > 0) {  // user state: Q = U_in, Wf = I, signs +1, Q^T Q from one narrow pass
+    launch_rs_ident(WfI, ones, K, hi);
+    c->launches++;
+    Pass pu;
+    if ((rc = plan_pass(c, pu, M, {Seg{U_in, ldu, K, 0}}, 0, K, K, WfI, K, false, true, false))) return rc;
+    if ((rc = run_pass(c, pu, hi))) return rc;
+    launch_extract_sym((const double*)c->tiles.ptr, pu.NB, pu.p.np_pad, K, nullptr, QtQ0, hi);
+    c->launches++;
+    cudaEventRecord(c->ev_qready, hi);
+  }
+  int la_nb[2] = {0, 0}, la_y[2] = {0, 0};
+  static const int nsub_env = getenv("PSVD_LA_NSUB") ? atoi(getenv("PSVD_LA_NSUB")) : 1;
+  const int nsub = (int)std::max<int64_t>(1, std::min<int64_t>(nsub_env, M / 65536));
+  // look-ahead sketch of batch j on the low-priority stream: Z = A_j Omega_j[K:], tiles Q^T Z, Z^T Z
+  auto la = [&](int j) -> int {
+    const bool hq = j > 0 || Kc > 0;
+    const int lq = j > 0 ? l : Kc;
+    const double* Qp = j > 0 ? Qb[(j - 1) & 1] : U_in;
+    const int64_t ldqp = j > 0 ? ldq : ldu;
+    const int nj = (hq ? K : 0) + B[j];
+    if (hq) cudaStreamWaitEvent(lo, c->ev_qready, 0);
+    if (j >= 2) cudaStreamWaitEvent(lo, c->ev_asm[j & 1], 0);  // tiles2[j&1] consumed by update j-2
+    if (batch_ready && batch_ready[j]) cudaStreamWaitEvent(lo, (cudaEvent_t)batch_ready[j], 0);
+    const int64_t rows_sub = (M + nsub - 1) / nsub / 32 * 32 + 32;
+    Pass first;
+    size_t part_off = 0;
+    int nchunks_total = 0;
+    mark("lo:la_begin", j, lo);
+    for (int k = 0; k < nsub; ++k) {
+      const int64_t r0 = (int64_t)k * rows_sub;
+      if (r0 >= M) break;
+      const int64_t mk = std::min(M, r0 + rows_sub) - r0;
+      std::vector<Seg> segs;
+      if (hq) segs.push_back(Seg{Qp + r0, ldqp, lq, 0});
+      segs.push_back(Seg{A[j] + r0, lda[j], B[j], 0});
+      Pass pa;
+      int r = plan_pass(c, pa, mk, segs, hq ? lq : 0, B[j], l, Omega[j] + (hq ? K : 0), nj, false, true, hq,
+                        hq ? lq : -1, -1, &c->partial2, &c->tiles2[j & 1], c->num_sms - 2, 0, true);
+      if (r) return r;
+      const size_t need_p = part_off + (size_t)pa.grid * SLOTS * 1024;
+      if (k == 0) {
+        if ((r = ensure(c, c->partial2, sizeof(double) * need_p * nsub))) return r;
+        first = pa;
+      }
+      pa.p.partial = (double*)c->partial2.ptr + part_off;
+      pa.p.Yout = Zt + r0;
+      pa.p.ldy = ldq;
+      c->path_count[pa.tma ? 0 : 3]++;
+      if (pa.tma)
+        launch_pass_tma(pa.p, pa.maps, pa.x, pa.grid, lo);
+      else
+        launch_tall(pa.p, pa.grid, lo);
+      c->launches++;
+      if ((r = cuda_check(c, "look-ahead sketch"))) return r;
+      part_off += (size_t)pa.grid * SLOTS * 1024;
+      nchunks_total += pa.map.nchunks;
+    }
+    first.map.nchunks = nchunks_total;
+    launch_tall_reduce((const double*)c->partial2.ptr, first.map, (double*)c->tiles2[j & 1].ptr, lo);
+    c->launches++;
+    la_nb[j & 1] = first.NB;
+    la_y[j & 1] = first.p.np_pad;
+    mark("lo:la_end", j, lo);
+    cudaEventRecord(c->ev_aa[j & 1], lo);
+    return cuda_check(c, "look-ahead reduce");
+  };
+  if ((rc = la(0))) return rc;
+  for (int b = 0; b < nb; ++b) {
+    const bool hq = b > 0 || Kc > 0;
+    const int lq = b > 0 ? l : Kc, kq = hq ? K : 0, n = kq + B[b];
+    const double* Qp = b > 0 ? Qb[(b - 1) & 1] : U_in;
+    const int64_t ldqp = b > 0 ? ldq : ldu;
+    const double* Wfp = b > 0 ? Wf[(b - 1) & 1] : WfI;
+    const double* sgp = b > 0 ? sgn : ones;
+    const double* sigp = b > 0 ? sigma_hist + (size_t)(b - 1) * K : sigma_in;
+    const double* QtQ = b > 0 ? G2[(b - 1) & 1] : QtQ0;
+    double* Qn = Qb[b & 1];
+    double* G2c = G2[b & 1];
+    mark("hi:update", b, hi);
+    if (b > 0) {  // tall sign rule of U_{b-1} = Q Wf (linalg.py:161, 81-91): argmax pass, no write
+      Pass ps;
+      if ((rc = plan_pass(c, ps, M, {Seg{Qp, ldqp, l, 0}}, 0, l, K, Wfp, l, false, false, false))) return rc;
+      if ((rc = ensure(c, c->colmax, sizeof(double) * (size_t)ps.map.nchunks * K * 2))) return rc;
+      ps.p.colmax = (double*)c->colmax.ptr;
+      if ((rc = run_pass(c, ps, hi))) return rc;
+      if ((rc = exchange_sign(c, (const double*)c->colmax.ptr, ps.map.nchunks, K, sgn, hi))) return rc;
+    }
+    mark("hi:sign_end", b, hi);
+    cudaStreamWaitEvent(hi, c->ev_aa[b & 1], 0);
+    mark("hi:prep", b, hi);
+    launch_rs_prep(sgp, Wfp, lq, K, sigp, ff, Omega[b], n, QtQ, (const double*)c->tiles2[b & 1].ptr, la_nb[b & 1], 0,
+                   la_y[b & 1], l, hq, Etop, Cm, G1, hi);
+    c->launches++;
+    cudaEventRecord(c->ev_asm[b & 1], hi);
+    if ((rc = svqb(c, G1, l, T1, sscr, hi))) return rc;
+    mark("hi:svqb_end", b, hi);
+    launch_rs_wb(Cm, lq, T1, l, hq, Wb, hi);
+    c->launches++;
+    if (batch_ready && batch_ready[b]) cudaStreamWaitEvent(hi, (cudaEvent_t)batch_ready[b], 0);
+    // projection pass: Y1 = [Q | Z] Wb, Y1^T Y1, [Q | Z | A]^T Y1
+    {
+      std::vector<Seg> segs;
+      if (hq) segs.push_back(Seg{Qp, ldqp, lq, 0});
+      segs.push_back(Seg{Zt, ldq, l, 0});
+      segs.push_back(Seg{A[b], lda[b], B[b], 0});
+      const int wk = (hq ? lq : 0) + l;
+      Pass pb;
+      if ((rc = plan_pass(c, pb, M, segs, 0, wk, l, Wb, wk, false, true, true, -1, -1, nullptr, nullptr, 0, 0, true)))
+        return rc;
+      pb.p.Yout = Qn;
+      pb.p.ldy = ldq;
+      mark("hi:projB", b, hi);
+      if ((rc = run_pass(c, pb, hi))) return rc;
+      mark("hi:projB_end", b, hi);
+      if (q == 0) {
+        cudaEventRecord(c->ev_qready, hi);
+        if (b + 1 < nb && (rc = la(b + 1))) return rc;
+      }
+      launch_rs_post((const double*)c->tiles.ptr, pb.NB, hq ? pb.p.seg[0].col0 : 0, pb.p.seg[hq ? 2 : 1].col0,
+                     pb.p.np_pad, lq, B[b], l, Etop, K, hq, G2c, X, hi);
+      c->launches++;
+    }
+    launch_chol_inv(G2c, l, T2, hi);
+    launch_small_gemm(X, n, 0, T2, l, q > 0 ? Zs : Bt, n, n, l, l, nullptr, hi);
+    c->launches += 2;
+    for (int it = 1; it <= q; ++it) {
+      // power iteration (linalg.py:143-145): Qz = orth(C^T Q) by SVQB + CholeskyQR, next sketch P (D Qz)
+      launch_small_gemm(Zs, n, 1, Zs, n, G1, l, l, n, l, nullptr, hi);
+      c->launches++;
+      if ((rc = svqb(c, G1, l, Tz, sscr, hi))) return rc;
+      launch_small_gemm(Zs, n, 0, Tz, l, Z1, n, n, l, l, nullptr, hi);
+      launch_small_gemm(Z1, n, 1, Z1, n, G1, l, l, n, l, nullptr, hi);
+      launch_chol_inv(G1, l, Tz, hi);
+      launch_small_gemm(Z1, n, 0, Tz, l, Qz, n, n, l, l, nullptr, hi);
+      const int rows = (hq ? lq : 0) + B[b];
+      launch_rs_w0(Etop, lq, K, Qz, n, B[b], l, hq, W0, hi);
+      c->launches += 5;
+      std::vector<Seg> segs;
+      if (hq) segs.push_back(Seg{Qp, ldqp, lq, 0});
+      segs.push_back(Seg{A[b], lda[b], B[b], 0});
+      Pass pA;  // sketch pass: Y = [Q | A] (E Qz), Y^T Y
+      if ((rc = plan_pass(c, pA, M, segs, 0, rows, l, W0, rows, false, true, false))) return rc;
+      pA.p.Yout = Qn;
+      pA.p.ldy = ldq;
+      if ((rc = run_pass(c, pA, hi))) return rc;
+      launch_extract_sym((const double*)c->tiles.ptr, pA.NB, pA.p.np_pad, l, nullptr, G1, hi);
+      c->launches++;
+      if ((rc = svqb(c, G1, l, T1, sscr, hi))) return rc;
+      segs.push_back(Seg{Qn, ldq, l, 0});
+      Pass pB;  // projection pass: Y1 = Y T1 in place, Y1^T Y1, [Q | A]^T Y1
+      if ((rc = plan_pass(c, pB, M, segs, rows, l, l, T1, l, false, true, true, -1, -1, nullptr, nullptr, 0, 0, true)))
+        return rc;
+      pB.p.Yout = Qn;
+      pB.p.ldy = ldq;
+      if ((rc = run_pass(c, pB, hi))) return rc;
+      if (it == q) {
+        cudaEventRecord(c->ev_qready, hi);
+        if (b + 1 < nb && (rc = la(b + 1))) return rc;
+      }
+      launch_rs_post((const double*)c->tiles.ptr, pB.NB, hq ? pB.p.seg[0].col0 : 0, pB.p.seg[hq ? 1 : 0].col0,
+                     pB.p.np_pad, lq, B[b], l, Etop, K, hq, G2c, X, hi);
+      launch_chol_inv(G2c, l, T2, hi);
+      launch_small_gemm(X, n, 0, T2, l, it < q ? Zs : Bt, n, n, l, l, nullptr, hi);
+      c->launches += 3;
+    }
+    // small SVD of B = Q^T C through B^T = Bt (U_B = J); Wf = T2 J[:, :K]
+    mark("hi:jacobi", b, hi);
+    launch_jacobi_svd(Bt, n, l, S, J, (double*)c->jacws.ptr, c->d_status, hi);
+    mark("hi:jacobi_end", b, hi);
+    launch_small_gemm(T2, l, 0, J, l, Wf[b & 1], l, l, l, K, nullptr, hi);
+    cudaMemcpyAsync(sigma_hist + (size_t)b * K, S, sizeof(double) * K, cudaMemcpyDeviceToDevice, hi);
+    c->launches += 2;
+    if ((rc = cuda_check(c, "randomized stream update"))) return rc;
+  }
+  {  // U = Q Wf with the sign rule, written once
+    Pass pc;
+    const double* Ql = Qb[(nb - 1) & 1];
+    if ((rc = plan_pass(c, pc, M, {Seg{Ql, ldq, l, 0}}, 0, l, K, Wf[(nb - 1) & 1], l, false, false, false))) return rc;
+    if ((rc = ensure(c, c->colmax, sizeof(double) * (size_t)pc.map.nchunks * K * 2))) return rc;
+    pc.p.Yout = U_out;
+    pc.p.ldy = ldo;
+    pc.p.colmax = (double*)c->colmax.ptr;
+    if ((rc = run_pass(c, pc, hi))) return rc;
+    if ((rc = exchange_sign(c, (const double*)c->colmax.ptr, pc.map.nchunks, K, sgn, hi))) return rc;
+    launch_scale_cols(U_out, ldo, M, K, sgn, hi);
+    c->launches++;
+  }
+  cudaEventRecord(c->ev_join, lo);
+  cudaStreamWaitEvent(user, c->ev_join, 0);
+  cudaEventRecord(c->ev_join, hi);
+  cudaStreamWaitEvent(user, c->ev_join, 0);
+  if (trace) {
+    mark("end", 0, user);
+    cudaDeviceSynchronize();
+    for (size_t i = 0; i < tl.size(); ++i)
+      fprintf(stderr, "psvd_trace %-18s %9.3f ms\n", tl[i].c_str(), (double)(tbuf[i] - tbuf[0]) * 1e-6);
+    cudaFree(tbuf);
+  }
+  return cuda_check(c, "rand_stream_run");
 }
 
 int psvd_refine_normalize(psvd_ctx* c, int64_t M, double* U, int64_t ldu, int K, double* UtU, double* sigma,

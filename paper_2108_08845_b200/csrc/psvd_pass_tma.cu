@@ -32,7 +32,7 @@ namespace psvd {
 namespace {
 
 constexpr int TKS = 16;       // rows per stage = one 128-byte swizzled column
-constexpr int TNS = 3;        // ring depth
+constexpr int TNS_MAX = 4;    // ring depth: x.ns stages of 16 rows (as many as fit, 3 .. 4)
 constexpr int YMAXC = 32;     // widest Y of the narrow pass (4 column blocks)
 constexpr int PROD_WARP = NWARP - 1;
 // sW row stride (doubles, = 4 mod 16: 2 wavefronts per B-fragment load), sized by the Y width
@@ -67,9 +67,10 @@ PSVD_DEV int swz(int c, int k) { return c * 16 + ((((k >> 1) ^ (c & 7)) << 1) | 
 
 }  // namespace
 
-size_t tma_pass_smem_bytes(int pwidth, int kp_span, int w_pad) {
+size_t tma_pass_smem_bytes(int pwidth, int kp_span, int w_pad, int ns, int ny) {
   size_t b = 1024;  // alignment slack for the 1024-byte swizzle atoms
-  b += sizeof(double) * (size_t)TNS * pwidth * TKS;  // panel ring
+  (void)ny;
+  b += sizeof(double) * (size_t)ns * pwidth * TKS;   // panel ring
   b += sizeof(double) * 2 * YMAXC * TKS;             // Y double buffer (<= 32 columns)
   b += sizeof(double) * (size_t)kp_span * w_stride(w_pad);  // W
   b += 64 * sizeof(uint64_t);                        // barriers
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(NTHR, 1)
 
   unsigned char* base = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
   double* sP = reinterpret_cast<double*>(base);
+  const int TNS = x.ns;
   double* sY = sP + (size_t)TNS * pw * TKS;
   double* sW = sY + 2 * YMAXC * TKS;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sW + (size_t)kspan * WSP);
@@ -178,7 +180,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       const int kr = rb * 8 + g;
       const double* wb = sW + (size_t)tq * WSP + cb * 8 + g;
       int k0 = x.kp_lo;
-      for (; k0 + 8 <= x.kp_hi; k0 += 8) {
+      for (; p.dbg != 1 && k0 + 8 <= x.kp_hi; k0 += 8) {
         const double a0 = P[swz(k0 + tq, kr)], a1 = P[swz(k0 + 4 + tq, kr)];
         const double b0 = wb[(size_t)(k0 - x.kp_lo) * WSP], b1 = wb[(size_t)(k0 + 4 - x.kp_lo) * WSP];
         dmma884(ya0, ya1, a0, b0);
@@ -276,9 +278,11 @@ __global__ void __launch_bounds__(NTHR, 1)
 #pragma unroll
         for (int q = 0; q < NB; ++q) fb[q] = Ys[swz(q * 8 + g, k)];
 #pragma unroll
-        for (int a = 0; a < NA; ++a)
+        if (p.dbg != 1)
 #pragma unroll
-          for (int c = 0; c < NB; ++c) dmma884(acc[a][c][0], acc[a][c][1], fa[a], fb[c]);
+          for (int a = 0; a < NA; ++a)
+#pragma unroll
+            for (int c = 0; c < NB; ++c) dmma884(acc[a][c][0], acc[a][c][1], fa[a], fb[c]);
       }
       mbar_arrive(&yfree[yb]);
       __syncwarp();
@@ -516,7 +520,7 @@ static EncodeTiledFn encode_fn() {
 
 bool tma_available() { return encode_fn() != nullptr; }
 
-int tma_pass_prepare(const TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift) {
+int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return -1;
   memset(&x, 0, sizeof(x));
@@ -569,11 +573,17 @@ int tma_pass_prepare(const TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift
   x.nops = nops;
   x.stage_bytes = bytes;
   x.pwidth = std::max((p.np_pad + pshift + 7) / 8 * 8, (pend + 7) / 8 * 8);
+  // ring depth: as many 16-row stages as shared memory holds (3 .. TNS_MAX)
+  x.ns = 3;
+  while (x.ns < TNS_MAX &&
+         tma_pass_smem_bytes(x.pwidth, x.kp_hi - x.kp_lo, p.w_pad, x.ns + 1, 1) <= (size_t)(227 * 1024))
+    ++x.ns;
+  if (const char* e = getenv("PSVD_TMA_NS")) x.ns = std::max(2, std::min(x.ns, atoi(e)));
   return 0;
 }
 
 void launch_pass_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x, int grid, cudaStream_t st) {
-  const size_t smem = tma_pass_smem_bytes(x.pwidth, x.kp_hi - x.kp_lo, p.w_pad);
+  const size_t smem = tma_pass_smem_bytes(x.pwidth, x.kp_hi - x.kp_lo, p.w_pad, x.ns, 1);
   cudaFuncSetAttribute(pass_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   pass_tma_kernel<<<grid, NTHR, smem, st>>>(p, maps, x);
 }

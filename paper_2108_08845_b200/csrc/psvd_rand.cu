@@ -193,13 +193,20 @@ void launch_jacobi_svd(const double* Z, int n, int l, double* S, double* J, doub
 // refinement step); columns of a numerically null direction (pivot <= tiny)
 // are zeroed, matching the first (SVQB) pass which dropped them.
 __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restrict__ G, int l, double* __restrict__ T,
-                                                           int* __restrict__ illcond) {
+                                                           int* __restrict__ illcond, int* __restrict__ status) {
   extern __shared__ double sm[];
   double* R = sm;          // l x l col-major, upper used
   double* X = R + l * l;   // inverse
   const int tid = threadIdx.x, nthr = blockDim.x;
   double dmax = 0.0;
-  for (int i = 0; i < l; ++i) dmax = fmax(dmax, G[(size_t)i * l + i]);
+  bool finite = true;
+  for (int i = 0; i < l; ++i) {
+    const double g = G[(size_t)i * l + i];
+    finite = finite && isfinite(g);
+    dmax = fmax(dmax, g);
+  }
+  // a non-finite snapshot entry reaches every sketch column (Gaussian Omega): its Gram diagonal
+  if (!finite && status != nullptr && threadIdx.x == 0) atomicOr(status, PSVD_ST_NONFINITE);
   const double tiny = 64.0 * DBL_EPSILON * dmax;
   for (int idx = tid; idx < l * l; idx += nthr) R[idx] = G[idx];
   __syncthreads();
@@ -241,10 +248,10 @@ __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restr
   }
 }
 
-void launch_chol_inv(const double* G, int l, double* T, cudaStream_t st, int* illcond) {
+void launch_chol_inv(const double* G, int l, double* T, cudaStream_t st, int* illcond, int* status) {
   const size_t smem = 2 * (size_t)l * l * sizeof(double);
   cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  chol_inv_kernel<<<1, 1024, smem, st>>>(G, l, T, illcond);
+  chol_inv_kernel<<<1, 1024, smem, st>>>(G, l, T, illcond, status);
 }
 
 // ---------------------------------------------------------------- tall sign rule
@@ -314,5 +321,172 @@ void launch_scale_rows(const double* X, int ldx, int m, int k, const double* d, 
   const int64_t tot = (int64_t)m * k;
   scale_rows_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(X, ldx, m, k, d, Y, ldy);
 }
+
+// ================================================================ pipelined randomized stream glue
+// The pipelined stream (psvd_rand_stream_run) keeps the state of update b-1 as a sketch basis
+// Q = Y1_{b-1} (M x lq, the once-orthonormalized sketch), weights Wf (lq x K), sigma (K) and the
+// column signs s of the sign rule, U_{b-1} = Q Wf diag(s).  The panel of update b,
+// [ff U S | A] = [Q | A] E with E = blockdiag(Wf diag(s ff sigma), I) ((lq + B) x (K + B)),
+// is never formed: every product with it goes through E (reference: linalg.py:126-162 composed
+// per batch, streaming.py:97-98).
+namespace {
+__device__ __forceinline__ double tile_at(const double* __restrict__ tiles, int NB, int gi, int gj) {
+  return tiles[((size_t)(gi >> 5) * NB + (gj >> 5)) * 1024 + (gi & 31) * 32 + (gj & 31)];
+}
+__device__ __forceinline__ double tile_sym(const double* __restrict__ tiles, int NB, int gi, int gj) {
+  return gi <= gj ? tile_at(tiles, NB, gi, gj) : tile_at(tiles, NB, gj, gi);
+}
+}  // namespace
+
+// Etop = Wf diag(s ff sigma) (lq x K); C = Etop Omega[0:K, :] (lq x l);
+// G1 = Y^T Y for Y = Q C + Z:  C^T QtQ C + C^T QtZ + QtZ^T C + ZtZ, where QtZ / ZtZ come from the
+// look-ahead pass tiles (Q at panel columns [q_c0, q_c0 + lq), Z = its Y block at y_c0).
+// have_q == 0 (first batch, no state): G1 = ZtZ.  One CTA.
+__global__ void rs_prep_kernel(const double* __restrict__ sgn, const double* __restrict__ Wf, int lq, int K,
+                               const double* __restrict__ sigma, double ff, const double* __restrict__ Om, int ldom,
+                               const double* __restrict__ QtQ, const double* __restrict__ tiles, int NB, int q_c0,
+                               int y_c0, int l, int have_q, double* __restrict__ Etop, double* __restrict__ C,
+                               double* __restrict__ G1) {
+  extern __shared__ double sm[];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (!have_q) {
+    for (int i = tid; i < l * l; i += nt) {
+      const int r = i % l, cc = i / l;
+      G1[i] = tile_sym(tiles, NB, y_c0 + r, y_c0 + cc);
+    }
+    return;
+  }
+  double* E = sm;              // lq x K
+  double* Cs = E + lq * K;     // lq x l
+  double* QZ = Cs + lq * l;    // lq x l
+  double* H = QZ + lq * l;     // lq x l: QtQ C + QtZ
+  for (int i = tid; i < lq * K; i += nt) {
+    const int k = i / lq;
+    const double e = Wf[i] * (sgn[k] * (ff * sigma[k]));
+    E[i] = e;
+    Etop[i] = e;
+  }
+  for (int i = tid; i < lq * l; i += nt) {
+    const int r = i % lq, cc = i / lq;
+    QZ[i] = tile_at(tiles, NB, q_c0 + r, y_c0 + cc);
+  }
+  __syncthreads();
+  for (int i = tid; i < lq * l; i += nt) {
+    const int r = i % lq, cc = i / lq;
+    double s = 0.0;
+    for (int k = 0; k < K; ++k) s = fma(E[k * lq + r], Om[(size_t)cc * ldom + k], s);
+    Cs[i] = s;
+    C[i] = s;
+  }
+  __syncthreads();
+  for (int i = tid; i < lq * l; i += nt) {
+    const int r = i % lq, cc = i / lq;
+    double s = QZ[i];
+    for (int m = 0; m < lq; ++m) s = fma(QtQ[m * lq + r], Cs[cc * lq + m], s);
+    H[i] = s;
+  }
+  __syncthreads();
+  for (int i = tid; i < l * l; i += nt) {
+    const int r = i % l, cc = i / l;
+    if (r > cc) continue;
+    double s = tile_sym(tiles, NB, y_c0 + r, y_c0 + cc);
+    for (int m = 0; m < lq; ++m) s += Cs[r * lq + m] * H[cc * lq + m] + QZ[m + r * lq] * Cs[cc * lq + m];
+    G1[cc * l + r] = s;
+    G1[r * l + cc] = s;
+  }
+}
+
+void launch_rs_prep(const double* sgn, const double* Wf, int lq, int K, const double* sigma, double ff,
+                    const double* Om, int ldom, const double* QtQ, const double* tiles, int NB, int q_c0, int y_c0,
+                    int l, int have_q, double* Etop, double* C, double* G1, cudaStream_t st) {
+  const size_t smem = sizeof(double) * ((size_t)lq * K + 3 * (size_t)lq * l);
+  rs_prep_kernel<<<1, 256, smem, st>>>(sgn, Wf, lq, K, sigma, ff, Om, ldom, QtQ, tiles, NB, q_c0, y_c0, l, have_q,
+                                       Etop, C, G1);
+}
+
+// Wb ((lq + l) x l) = [C T1; T1] (the weights of Y1 = [Q | Z] Wb = (Q C + Z) T1); have_q == 0: Wb = T1.
+__global__ void rs_wb_kernel(const double* __restrict__ C, int lq, const double* __restrict__ T1, int l, int have_q,
+                             double* __restrict__ Wb) {
+  const int rows = have_q ? lq + l : l;
+  for (int i = threadIdx.x; i < rows * l; i += blockDim.x) {
+    const int r = i % rows, cc = i / rows;
+    double v;
+    if (have_q && r < lq) {
+      v = 0.0;
+      for (int m = 0; m < l; ++m) v = fma(C[m * lq + r], T1[cc * l + m], v);
+    } else {
+      v = T1[cc * l + (have_q ? r - lq : r)];
+    }
+    Wb[i] = v;
+  }
+}
+
+void launch_rs_wb(const double* C, int lq, const double* T1, int l, int have_q, double* Wb, cudaStream_t st) {
+  rs_wb_kernel<<<1, 256, 0, st>>>(C, lq, T1, l, have_q, Wb);
+}
+
+// After a projection pass (Y1 at y_c0, Q at q_c0, A at a_c0):  G2 = Y1^T Y1 (l x l) and
+// X = E^T [Q | A]^T Y1 (n x l, n = K + B with Q, else B): X[k] = sum_i Etop[i, k] (Q^T Y1)[i],
+// X[K + r] = (A^T Y1)[r]  (= D P^T Y1 of the unpipelined update).
+__global__ void rs_post_kernel(const double* __restrict__ tiles, int NB, int q_c0, int a_c0, int y_c0, int lq, int B,
+                               int l, const double* __restrict__ Etop, int K, int have_q, double* __restrict__ G2,
+                               double* __restrict__ X) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int i = tid; i < l * l; i += nt) {
+    const int r = i % l, cc = i / l;
+    G2[i] = tile_sym(tiles, NB, y_c0 + r, y_c0 + cc);
+  }
+  const int kq = have_q ? K : 0, n = kq + B;
+  for (int i = tid; i < n * l; i += nt) {
+    const int r = i % n, cc = i / n;
+    double v;
+    if (r < kq) {
+      v = 0.0;
+      for (int m = 0; m < lq; ++m) v = fma(Etop[r * lq + m], tile_at(tiles, NB, q_c0 + m, y_c0 + cc), v);
+    } else {
+      v = tile_at(tiles, NB, a_c0 + (r - kq), y_c0 + cc);
+    }
+    X[i] = v;
+  }
+}
+
+void launch_rs_post(const double* tiles, int NB, int q_c0, int a_c0, int y_c0, int lq, int B, int l,
+                    const double* Etop, int K, int have_q, double* G2, double* X, cudaStream_t st) {
+  const int n = (have_q ? K : 0) + B;
+  const int tot = std::max(l * l, n * l);
+  rs_post_kernel<<<(tot + 255) / 256, 256, 0, st>>>(tiles, NB, q_c0, a_c0, y_c0, lq, B, l, Etop, K, have_q, G2, X);
+}
+
+// Power-iteration sketch weights W0 = E Qz ((lq + B) x l): [Etop Qz[0:K]; Qz[K:]]; have_q == 0: W0 = Qz.
+__global__ void rs_w0_kernel(const double* __restrict__ Etop, int lq, int K, const double* __restrict__ Qz, int n,
+                             int B, int l, int have_q, double* __restrict__ W0) {
+  const int rows = have_q ? lq + B : B, kq = have_q ? K : 0;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int i = tid; i < rows * l; i += nt) {
+    const int r = i % rows, cc = i / rows;
+    double v;
+    if (have_q && r < lq) {
+      v = 0.0;
+      for (int k = 0; k < K; ++k) v = fma(Etop[k * lq + r], Qz[(size_t)cc * n + k], v);
+    } else {
+      v = Qz[(size_t)cc * n + kq + (r - (have_q ? lq : 0))];
+    }
+    W0[i] = v;
+  }
+}
+
+void launch_rs_w0(const double* Etop, int lq, int K, const double* Qz, int n, int B, int l, int have_q, double* W0,
+                  cudaStream_t st) {
+  const int rows = have_q ? lq + B : B;
+  rs_w0_kernel<<<(rows * l + 255) / 256, 256, 0, st>>>(Etop, lq, K, Qz, n, B, l, have_q, W0);
+}
+
+// identity (K x K) and ones (K): the weights / signs of a user-supplied initial state
+__global__ void rs_ident_kernel(double* __restrict__ I, double* __restrict__ ones, int K) {
+  for (int i = threadIdx.x; i < K * K; i += blockDim.x) I[i] = (i % K == i / K) ? 1.0 : 0.0;
+  for (int i = threadIdx.x; i < K; i += blockDim.x) ones[i] = 1.0;
+}
+
+void launch_rs_ident(double* I, double* ones, int K, cudaStream_t st) { rs_ident_kernel<<<1, 256, 0, st>>>(I, ones, K); }
 
 }  // namespace psvd

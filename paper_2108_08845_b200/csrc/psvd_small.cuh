@@ -77,11 +77,22 @@ void launch_small_gemm(const double* A, int lda, int transA, const double* B, in
 size_t jacobi_workspace_doubles(int n, int l);
 void launch_jacobi_svd(const double* Z, int n, int l, double* S, double* J, double* ws, int* status, cudaStream_t st,
                        const int* gate = nullptr);
-void launch_chol_inv(const double* G, int l, double* T, cudaStream_t st, int* illcond = nullptr);
+void launch_chol_inv(const double* G, int l, double* T, cudaStream_t st, int* illcond = nullptr, int* status = nullptr);
 void launch_colmax_sign(const double* colmax, int nchunks, int K, double* sign, cudaStream_t st);
 void launch_colmax_reduce(const double* colmax, int nchunks, int K, double* out, cudaStream_t st);
 void launch_svqb_scale(double* T, const double* S, int l, double tol, cudaStream_t st, const int* gate = nullptr);
 void launch_scale_cols(double* U, int64_t ld, int64_t M, int K, const double* s, cudaStream_t st);
 void launch_scale_rows(const double* X, int ldx, int m, int k, const double* d, double* Y, int ldy, cudaStream_t st);
+
+// ---- pipelined randomized stream glue (psvd_rand.cu; see psvd_rand_stream_run)
+void launch_rs_prep(const double* sgn, const double* Wf, int lq, int K, const double* sigma, double ff,
+                    const double* Om, int ldom, const double* QtQ, const double* tiles, int NB, int q_c0, int y_c0,
+                    int l, int have_q, double* Etop, double* C, double* G1, cudaStream_t st);
+void launch_rs_wb(const double* C, int lq, const double* T1, int l, int have_q, double* Wb, cudaStream_t st);
+void launch_rs_post(const double* tiles, int NB, int q_c0, int a_c0, int y_c0, int lq, int B, int l,
+                    const double* Etop, int K, int have_q, double* G2, double* X, cudaStream_t st);
+void launch_rs_w0(const double* Etop, int lq, int K, const double* Qz, int n, int B, int l, int have_q, double* W0,
+                  cudaStream_t st);
+void launch_rs_ident(double* I, double* ones, int K, cudaStream_t st);
 
 }  // namespace psvd

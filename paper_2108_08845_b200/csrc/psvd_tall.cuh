@@ -105,11 +105,12 @@ struct TmaExtra {
   int pshift;                // physical column = logical column + pshift (narrow pass)
   int pwidth;                // physical ring width (columns)
   unsigned stage_bytes;
+  int ns;                    // ring depth (stages)
   unsigned char written[TMA_MAX_BLK];  // 8-column panel blocks covered by a TMA box
 };
 bool tma_available();
-size_t tma_pass_smem_bytes(int pwidth, int kp_span, int w_pad);
-int tma_pass_prepare(const TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift = 0);
+size_t tma_pass_smem_bytes(int pwidth, int kp_span, int w_pad, int ns = 3, int ny = 1);
+int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift = 0);
 void launch_pass_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x, int grid, cudaStream_t st);
 // TMA-fed Gram-only pass (w == 0, segments on 8-column boundaries, <= NWARP - 1 tiles per slice)
 constexpr int TMA_GRAM_CONS = NWARP - 1;

@@ -197,15 +197,66 @@ def _run_window(state, mats, config, dev, ready=None):
     return new_state, [hist[i] for i in range(nb)]
 
 
+RAND_STREAM_MAX_WIDTH = 32  # widest sketch of the pipelined randomized run (narrow TMA passes)
+
+
+def _run_rand_window(state, mats, config, dev, ready=None):
+    """Randomized updates over device batches `mats` through the pipelined
+    psvd_rand_stream_run (SURVEY R9 per batch; the next batch's state-independent
+    sketch overlaps the current small solves, U is written once at the end)."""
+    from .linalg import device_omega
+    sk = config.sketch
+    k, l, q = sk.target_rank, sk.sketch_width, sk.power_iterations
+    M = mats[0].rows
+    for m in mats:
+        if m.rows != M:
+            raise ValueError(f"batch rows {m.rows} != mode rows {M}")
+    if state is None and mats[0].cols < k:
+        raise ValueError(f"initial batch has {mats[0].cols} columns, need at least k_modes={k}")
+    for i, m in enumerate(mats):
+        n = (k if (state is not None or i > 0) else 0) + m.cols
+        if l > min(M, n):
+            raise ValueError(f"sketch width {l} exceeds min(a.shape) = {min(M, n)}")
+    ctx = nat.context(dev)
+    nb = len(mats)
+    with torch.cuda.device(dev):
+        if state is not None:
+            U = nat.as_device_colmajor(state.modes, dev, "modes")
+            sig = nat.as_device_vector(state.singular_values, dev, k, "singular_values")
+            kc, uptr, uld, sptr = k, nat._vp(U.data_ptr()), U.ld, nat.ptr(sig)
+        else:
+            U = sig = None
+            kc, uptr, uld, sptr = 0, nat._vp(0), 0, nat._vp(0)
+        out = nat.DevMat.empty(M, k, dev)
+        hist = torch.empty((nb, k), dtype=torch.float64, device=dev)
+        oms = [device_omega((k if (state is not None or i > 0) else 0) + m.cols, sk, dev) for i, m in enumerate(mats)]
+        A = (nat._vp * nb)(*[nat._vp(m.data_ptr()) for m in mats])
+        lda = (ctypes.c_int64 * nb)(*[m.ld for m in mats])
+        B = (ctypes.c_int * nb)(*[m.cols for m in mats])
+        Om = (nat._vp * nb)(*[nat._vp(o.data_ptr()) for o in oms])
+        rd = None
+        if ready is not None and any(e is not None for e in ready):
+            rd = (nat._vp * nb)(*[nat._vp(e.cuda_event if e is not None else 0) for e in ready])
+        nat.call("psvd_rand_stream_run", ctx, M, uptr, uld, sptr, kc, nb, A, lda, B, k, l, q,
+                 float(config.forget_factor), Om, nat._vp(out.data_ptr()), out.ld, nat.ptr(hist), rd,
+                 nat.stream_ptr(dev))
+        if _check_status(ctx, dev, "a_new") & nat.ST_NOCONVERGE:
+            from .errors import ConvergenceError
+            raise ConvergenceError("randomized core SVD did not converge")
+    it0 = -1 if state is None else state.iteration
+    return StreamState(out.view, hist[nb - 1].clone(), it0 + nb), [hist[i] for i in range(nb)]
+
+
 def stream_all(batches, config, device=None):
     """Initialize on the first batch, incorporate the rest (streaming.py:119-133).
     Returns (final_state, history) with the singular values after every step.
     Deterministic streams run in windows of STREAM_WINDOW resident batches
     through the pipelined psvd_stream_run (pinned host batches are uploaded on a
-    side stream, overlapping the updates); randomized ones update per batch."""
+    side stream, overlapping the updates); randomized ones (sketch width <= 32)
+    through the pipelined psvd_rand_stream_run, wider sketches per batch."""
     state = None
     history = []
-    if config.sketch is not None:
+    if config.sketch is not None and config.sketch.sketch_width > RAND_STREAM_MAX_WIDTH:
         for batch in batches:
             if state is None:
                 state = stream_initialize(batch, config, device)
@@ -214,6 +265,7 @@ def stream_all(batches, config, device=None):
             history.append(state.singular_values.clone())
     else:
         dev = None if device is None else torch.device(device)
+        run = _run_window if config.sketch is None else _run_rand_window
         window, ready = [], []
         for batch in batches:
             if dev is None:
@@ -223,11 +275,11 @@ def stream_all(batches, config, device=None):
             window.append(m)
             ready.append(ev)
             if len(window) == STREAM_WINDOW:
-                state, h = _run_window(state, window, config, dev, ready)
+                state, h = run(state, window, config, dev, ready)
                 history.extend(h)
                 window, ready = [], []
         if window:
-            state, h = _run_window(state, window, config, dev, ready)
+            state, h = run(state, window, config, dev, ready)
             history.extend(h)
     if state is None:
         raise ValueError("batch stream is empty")

@@ -342,6 +342,48 @@ def test_randomized_vs_oracle(rows, k, p_, q, ff):
     _assert_parity(m, s, ref_m, ref_s)
 
 
+@pytest.mark.parametrize("q", [0, 1, 2])
+def test_pipelined_randomized_run_matches_per_update_and_oracle(q):
+    """stream_all runs psvd_rand_stream_run (state kept as a sketch basis between updates, the
+    next batch's sketch on the low-priority stream, U written once); stream_incorporate runs
+    psvd_rand_update per batch.  Both against the oracle, per step: 10 batches with a ragged
+    last one, so the second window starts from a materialized state (Kc = K)."""
+    p = _pkg()
+    a = oracle.burgers_matrix(8192, 950) + 1e-3 * np.random.default_rng(4).standard_normal((8192, 950))
+    bs = _batches(a, 100)
+    assert len(bs) == 10 and bs[-1].shape[1] == 50
+    sk = p.RandomSketchConfig(target_rank=10, oversampling=10, power_iterations=q, seed=5)
+    cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=100, sketch=sk)
+    st, hist = p.stream_all(bs, cfg)
+    st2 = p.stream_initialize(bs[0], cfg)
+    for b in bs[1:]:
+        st2 = p.stream_incorporate(st2, b, cfg)
+    ref_m, ref_s, ref_h = oracle.ref_rand_stream_all(bs, 10, 0.95, 10, q, 5)
+    m, s = _np(st)
+    _assert_parity(m, s, ref_m, ref_s)
+    m2, s2 = _np(st2)
+    _assert_parity(m2, s2, ref_m, ref_s)
+    assert len(hist) == len(ref_h)
+    for h, rh in zip(hist, ref_h):
+        assert oracle.sigma_rel_err(h.cpu().numpy(), rh) <= SIG_TOL
+
+
+def test_pipelined_randomized_run_bitwise_and_validation():
+    p = _pkg()
+    a = oracle.burgers_matrix(4096, 800)[:, :400]
+    sk = p.RandomSketchConfig(target_rank=10, oversampling=10, power_iterations=1, seed=0)
+    cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200, sketch=sk)
+    s1, _ = p.stream_all(_batches(a, 200), cfg)
+    s2, _ = p.stream_all(_batches(a, 200), cfg)
+    assert torch.equal(s1.modes, s2.modes) and torch.equal(s1.singular_values, s2.singular_values)
+    bad = a.copy()
+    bad[7, 250] = np.nan
+    with pytest.raises(ValueError):
+        p.stream_all(_batches(bad, 200), cfg)
+    with pytest.raises(ValueError):  # initial batch narrower than k_modes
+        p.stream_all([a[:, :5], a[:, 5:200]], cfg)
+
+
 def test_randomized_validation():
     p = _pkg()
     with pytest.raises(ValueError):
