@@ -87,6 +87,8 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        if os.environ.get("PSVD_NO_CLOCKS"):
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -430,16 +432,30 @@ def e2e(a, p, D, M, dev, world, ctxr):
             m, s = st.modes, st.singular_values
         return m.cpu(), s.cpu()
 
-    one()
+    for _ in range(max(1, getattr(a, "warmup", 3))):  # same warm-up count as the device-timed leg
+        ti = time.perf_counter()
+        one()
+        if os.environ.get("PSVD_E2E_VERBOSE"):
+            torch.cuda.synchronize()
+            print(f"e2e warm-up {(time.perf_counter() - ti) * 1e3:.1f} ms", file=sys.stderr)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    n = max(1, min(a.steps, 3))
+    n = max(3, min(a.steps, 10))
+    verbose = os.environ.get("PSVD_E2E_VERBOSE")
+    import gc
+    gc.collect()
+    gc.disable()  # no collector pauses inside the wall-clock region
     t0 = time.perf_counter()
     for _ in range(n):
+        ti = time.perf_counter()
         out = one()
+        if verbose:
+            torch.cuda.synchronize()
+            print(f"e2e iteration {(time.perf_counter() - ti) * 1e3:.1f} ms", file=sys.stderr)
     torch.cuda.synchronize()
     dt = (time.perf_counter() - t0) / n
+    gc.enable()
     if world > 1:
         tt = torch.tensor([dt], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)

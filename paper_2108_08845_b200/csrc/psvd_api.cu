@@ -238,7 +238,17 @@ static int plan_tiles_tma(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int
   const int nt = (int)tiles.size();
   memset(ps.p.plan, 0, sizeof(ps.p.plan));
   memset(&ps.map, 0, sizeof(ps.map));
-  const int warp0 = 2 * (ps.p.w_pad / 8), nwarps = NWARP - 1 - warp0;
+  // Y warps: 2 row blocks x ncb column blocks; each block's k range is split yks ways (up to 12
+  // Y warps = 3 per SMSP) while the Gram tiles still fit one slice: the Y product is bound by
+  // the per-warp load -> DMMA latency chain, so more warps on it pay
+  const int nyo = 2 * (ps.p.w_pad / 8);
+  static const int yks_max = getenv("PSVD_YKS") ? atoi(getenv("PSVD_YKS")) : 1;
+  int yks = 1;
+  while (yks < yks_max && nyo * (yks + 1) <= 12 && nyo * (yks + 1) + nt <= NWARP - 1 &&
+         (ps.p.wk + 7) / 8 >= 2 * (yks + 1) && yks * nyo <= 10)  // partial slots: (yks - 1) * nyo <= 10
+    ++yks;
+  ps.p.yks = yks;
+  const int warp0 = nyo * yks, nwarps = NWARP - 1 - warp0;
   const int nslices = std::max(1, (nt + nwarps - 1) / nwarps);
   if (nt > MAX_OUT_TILES || nslices > MAX_SLICES) return fail(c, PSVD_EINVAL, "panel too wide (%d tiles)", nt);
   ps.p.nslices = nslices;

@@ -32,8 +32,9 @@ namespace psvd {
 namespace {
 
 constexpr int TKS = 16;       // rows per stage = one 128-byte swizzled column
-constexpr int TNS_MAX = 4;    // ring depth: x.ns stages of 16 rows (as many as fit, 3 .. 4)
+constexpr int TNS_MAX = 8;    // ring depth: x.ns stages of 16 rows (as many as fit, 3 .. 8)
 constexpr int YMAXC = 32;     // widest Y of the narrow pass (4 column blocks)
+constexpr int YB = 2;         // Y ring depth (Y warps run up to YB stages ahead of the Gram warps; 4 measured no faster)
 constexpr int PROD_WARP = NWARP - 1;
 // sW row stride (doubles, = 4 mod 16: 2 wavefronts per B-fragment load), sized by the Y width
 __host__ __device__ inline int w_stride(int w_pad) { return w_pad <= 16 ? 20 : 36; }
@@ -71,10 +72,11 @@ size_t tma_pass_smem_bytes(int pwidth, int kp_span, int w_pad, int ns, int ny) {
   size_t b = 1024;  // alignment slack for the 1024-byte swizzle atoms
   (void)ny;
   b += sizeof(double) * (size_t)ns * pwidth * TKS;   // panel ring
-  b += sizeof(double) * 2 * YMAXC * TKS;             // Y double buffer (<= 32 columns)
+  b += sizeof(double) * YB * YMAXC * TKS;            // Y ring (<= 32 columns)
   b += sizeof(double) * (size_t)kp_span * w_stride(w_pad);  // W
   b += 64 * sizeof(uint64_t);                        // barriers
   b += sizeof(double) * 2 * YMAXC * 3;               // argmax scratch
+  b += sizeof(double) * 2 * 10 * 32 * 2;             // k-split Y partials ((yks - 1) * nyo <= 10)
   return b;
 }
 
@@ -92,22 +94,25 @@ __global__ void __launch_bounds__(NTHR, 1)
   const int pw = x.pwidth;       // physical ring width (>= np_pad + pshift)
   const int kspan = x.kp_hi - x.kp_lo;
   const int WSP = w_stride(p.w_pad);
-  const int ncb = p.w_pad >> 3;  // Y column blocks (1..4); warps 0 .. 2*ncb-1 form Y
+  const int ncb = p.w_pad >> 3;  // Y column blocks (1..4)
+  const int nyo = 2 * ncb;       // Y output blocks (2 row blocks x ncb), owned by warps 0 .. nyo-1
+  const int yks = max(1, p.yks);  // warps per Y block (k split); warps 0 .. nyo*yks-1 form Y
 
   unsigned char* base = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
   double* sP = reinterpret_cast<double*>(base);
   const int TNS = x.ns;
   double* sY = sP + (size_t)TNS * pw * TKS;
-  double* sW = sY + 2 * YMAXC * TKS;
+  double* sW = sY + YB * YMAXC * TKS;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sW + (size_t)kspan * WSP);
   uint64_t* full = bars;
   uint64_t* empty = bars + TNS;
   uint64_t* ydone = bars + 2 * TNS;
-  uint64_t* yfree = ydone + 2;
+  uint64_t* yfree = ydone + YB;
   double* cmx = reinterpret_cast<double*>(bars + 64);  // [2 rb][32 cols][val, abs, row]
 
+  double* ypart = cmx + 2 * YMAXC * 3;  // k-split partials: [2 parity][yks-1][nyo][32 lanes][2]
   int ngram = 0;
-  const int ny = 2 * ncb;
+  const int ny = nyo * yks;
   for (int w = ny; w < PROD_WARP; ++w) ngram += p.plan[slice][w].ntile > 0;
 
   // one-time setup: zero the panel columns no TMA box writes (alignment gaps), the Y
@@ -120,10 +125,17 @@ __global__ void __launch_bounds__(NTHR, 1)
       for (int k = 0; k < TKS; ++k) col[k] = 0.0;
     }
   }
-  for (int i = tid; i < 2 * YMAXC * TKS; i += NTHR) sY[i] = 0.0;
+  for (int i = tid; i < YB * YMAXC * TKS; i += NTHR) sY[i] = 0.0;
   for (int i = tid; i < kspan * WSP; i += NTHR) {
     const int kk = i / WSP, o = i % WSP;
-    const int pc = x.kp_lo + kk;  // physical panel column
+    // rows of each full 8-column step are stored in the Y warps' k order: step half h reads
+    // columns 2h + {0, 1, 4, 5} (see the Y warps); the 4-column tail keeps the natural order
+    int kperm = kk;
+    if (kk < ((kspan >> 3) << 3)) {
+      const int r = kk & 7, h = r >> 2, t = r & 3;
+      kperm = (kk & ~7) + 2 * h + (t & 1) + 4 * (t >> 1);
+    }
+    const int pc = x.kp_lo + kperm;  // physical panel column
     double v = 0.0;
     if (o < p.w) {
       for (int s = 0; s < p.nseg; ++s) {
@@ -141,8 +153,8 @@ __global__ void __launch_bounds__(NTHR, 1)
       mbar_init(&full[b], 1);
       mbar_init(&empty[b], (unsigned)(ny + ngram));
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&ydone[b], 32u * ny);
+    for (int b = 0; b < YB; ++b) {
+      mbar_init(&ydone[b], 32u * nyo);
       mbar_init(&yfree[b], (unsigned)max(32 * ngram, 1));
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -168,31 +180,82 @@ __global__ void __launch_bounds__(NTHR, 1)
 
   if (warp < ny) {
     // ---------------------------------------------------------------- Y warps
-    const int rb = warp & 1, cb = warp >> 1;
+    // warp -> output block blk = (rb, cb) and k part (the k range of a block split yks ways in
+    // 8-column steps, the last part takes the 4-column tail); part 0 owns the block
+    const int blk = warp % nyo, part = warp / nyo;
+    const int rb = blk & 1, cb = blk >> 1;
+    const int n8all = (x.kp_hi - x.kp_lo) >> 3;
+    const int k_lo = x.kp_lo + (n8all * part / yks) * 8;
+    const int k_hi = part == yks - 1 ? x.kp_hi : x.kp_lo + (n8all * (part + 1) / yks) * 8;
     double cm_val[2] = {0.0, 0.0}, cm_abs[2] = {-1.0, -1.0};
     int64_t cm_row[2] = {-1, -1};
     const bool do_y = slice == 0;
     for (int64_t s = 0; s < nstage; ++s) {
-      const int b = (int)(s % TNS), yb = (int)(s & 1);
+      const int b = (int)(s % TNS), yb = (int)(s & (YB - 1));
       mbar_wait(&full[b], (unsigned)((s / TNS) & 1));
       const double* P = sP + (size_t)b * pw * TKS;
-      double ya0 = 0.0, ya1 = 0.0, yb0 = 0.0, yb1 = 0.0;
       const int kr = rb * 8 + g;
-      const double* wb = sW + (size_t)tq * WSP + cb * 8 + g;
-      int k0 = x.kp_lo;
-      for (; p.dbg != 1 && k0 + 8 <= x.kp_hi; k0 += 8) {
-        const double a0 = P[swz(k0 + tq, kr)], a1 = P[swz(k0 + 4 + tq, kr)];
-        const double b0 = wb[(size_t)(k0 - x.kp_lo) * WSP], b1 = wb[(size_t)(k0 + 4 - x.kp_lo) * WSP];
-        dmma884(ya0, ya1, a0, b0);
-        dmma884(yb0, yb1, a1, b1);
+      // kp_lo is a multiple of 8: the swizzle phase of column kp_lo + 8i + tq (+ 4) is tq (+ 4)
+      // for every i, so the fragment addresses advance by 8 columns = 128 doubles per step.
+      // Groups of 4 steps: 16 independent loads issued together, then 8 DMMAs on 4 chains
+      // (the per-warp load -> DMMA latency chain, not the pipes, bounded the one-step loop).
+      // step half h of an 8-column step reads columns k0 + 2h + {0, 1, 4, 5}[tq]: the four columns
+      // of a fragment then fall in both 64-byte halves of the swizzled 128-byte rows (2 wavefronts
+      // per LDS instead of 4); W's staged rows follow the same order
+      const int ph = (tq & 1) + 4 * (tq >> 1);
+      const double* pa = P + (size_t)(k_lo + ph) * TKS + ((((kr >> 1) ^ ph) << 1) | (kr & 1));
+      const double* pb = P + (size_t)(k_lo + ph + 2) * TKS + ((((kr >> 1) ^ (ph + 2)) << 1) | (kr & 1));
+      const double* wa = sW + (size_t)(k_lo - x.kp_lo + tq) * WSP + cb * 8 + g;
+      const double* wbp = wa + (size_t)4 * WSP;
+      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0, c4 = 0.0, c5 = 0.0, c6 = 0.0, c7 = 0.0;
+      const int n8 = p.dbg == 1 ? 0 : (k_hi - k_lo) >> 3;
+      int i = 0;
+#pragma unroll 1
+      for (; i + 4 <= n8; i += 4) {
+        double fa[8], fw[8];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          fa[2 * j] = pa[(size_t)(i + j) * 128];
+          fa[2 * j + 1] = pb[(size_t)(i + j) * 128];
+          fw[2 * j] = wa[(size_t)(8 * (i + j)) * WSP];
+          fw[2 * j + 1] = wbp[(size_t)(8 * (i + j)) * WSP];
+        }
+        dmma884(c0, c1, fa[0], fw[0]);
+        dmma884(c2, c3, fa[1], fw[1]);
+        dmma884(c4, c5, fa[2], fw[2]);
+        dmma884(c6, c7, fa[3], fw[3]);
+        dmma884(c0, c1, fa[4], fw[4]);
+        dmma884(c2, c3, fa[5], fw[5]);
+        dmma884(c4, c5, fa[6], fw[6]);
+        dmma884(c6, c7, fa[7], fw[7]);
       }
-      if (k0 < x.kp_hi) {  // kp span is a multiple of 4
-        dmma884(ya0, ya1, P[swz(k0 + tq, kr)], wb[(size_t)(k0 - x.kp_lo) * WSP]);
+      for (; i < n8; ++i) {
+        dmma884(c0, c1, pa[(size_t)i * 128], wa[(size_t)(8 * i) * WSP]);
+        dmma884(c2, c3, pb[(size_t)i * 128], wbp[(size_t)(8 * i) * WSP]);
       }
+      if (p.dbg != 1 && k_lo + 8 * n8 < k_hi)  // kp span is a multiple of 4; natural order
+        dmma884(c4, c5, P[swz(k_lo + 8 * n8 + tq, kr)], wa[(size_t)(8 * n8) * WSP]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[b]);  // panel slot no longer read by this warp
-      const double y0 = ya0 + yb0, y1 = ya1 + yb1;
-      if (s >= 2 && ngram > 0) mbar_wait(&yfree[yb], (unsigned)(((s >> 1) - 1) & 1));
+      double y0 = (c0 + c4) + (c2 + c6), y1 = (c1 + c5) + (c3 + c7);
+      if (yks > 1) {
+        // partials meet at the block's named barrier (ids 2 .. 2+nyo-1); part 0 adds them in part
+        // order.  Double-buffered by stage parity: a partial for stage s+2 is written only after
+        // the rendezvous of stage s+1, i.e. after part 0 read stage s.
+        double* slot = ypart + ((((size_t)(s & 1) * (yks - 1)) * nyo + blk) * 32 + lane) * 2;
+        const size_t pstride = (size_t)nyo * 32 * 2;
+        if (part > 0) {
+          slot[(part - 1) * pstride] = y0;
+          slot[(part - 1) * pstride + 1] = y1;
+        }
+        asm volatile("bar.sync %0, %1;\n" ::"r"(2 + blk), "r"(32 * yks) : "memory");
+        if (part > 0) continue;
+        for (int q = 1; q < yks; ++q) {
+          y0 += slot[(q - 1) * pstride];
+          y1 += slot[(q - 1) * pstride + 1];
+        }
+      }
+      if (s >= YB && ngram > 0) mbar_wait(&yfree[yb], (unsigned)(((s / YB) - 1) & 1));
       double* Ys = sY + (size_t)yb * YMAXC * TKS;
       const int o0 = cb * 8 + 2 * tq;
       Ys[swz(o0, kr)] = y0;
@@ -210,6 +273,7 @@ __global__ void __launch_bounds__(NTHR, 1)
         }
       }
     }
+    if (part > 0) return;
     if (do_y && p.colmax != nullptr) {
       // combine over g (lanes 4 apart), ties to the smaller row (first occurrence)
 #pragma unroll
@@ -230,7 +294,7 @@ __global__ void __launch_bounds__(NTHR, 1)
           d[0] = cm_val[e]; d[1] = cm_abs[e]; d[2] = (double)cm_row[e];
         }
       }
-      asm volatile("bar.sync 1, %0;\n" ::"r"(32 * ny) : "memory");
+      asm volatile("bar.sync 1, %0;\n" ::"r"(32 * nyo) : "memory");
       if (rb == 0 && g == 0) {
         for (int e = 0; e < 2; ++e) {
           const int o = cb * 8 + 2 * tq + e;
@@ -263,9 +327,9 @@ __global__ void __launch_bounds__(NTHR, 1)
   auto stage_loop = [&](auto na_t, auto nb_t) {
     constexpr int NA = decltype(na_t)::value, NB = decltype(nb_t)::value;
     for (int64_t s = 0; s < nstage; ++s) {
-      const int b = (int)(s % TNS), yb = (int)(s & 1);
+      const int b = (int)(s % TNS), yb = (int)(s & (YB - 1));
       mbar_wait(&full[b], (unsigned)((s / TNS) & 1));
-      mbar_wait(&ydone[yb], (unsigned)((s >> 1) & 1));
+      mbar_wait(&ydone[yb], (unsigned)((s / YB) & 1));
       const double* Ys = sY + (size_t)yb * YMAXC * TKS;
       const double* Abase = sP + (size_t)b * pw * TKS;
 #pragma unroll
@@ -277,7 +341,6 @@ __global__ void __launch_bounds__(NTHR, 1)
           fa[q] = i_is_y ? Ys[swz(q * 8 + g, k)] : Abase[swz(acol + q * 8 + g, k)];
 #pragma unroll
         for (int q = 0; q < NB; ++q) fb[q] = Ys[swz(q * 8 + g, k)];
-#pragma unroll
         if (p.dbg != 1)
 #pragma unroll
           for (int a = 0; a < NA; ++a)

@@ -63,6 +63,7 @@ struct TallParams {
   double* Yout;          // optional global copy of Y (col-major, ld ldy)
   int64_t ldy;
   int nslices;
+  int yks;               // TMA pass: warps per Y output block (k range split yks ways, summed in part order)
   WarpPlan plan[MAX_SLICES][NWARP];
   double* partial;       // [grid][SLOTS][1024]
   double* colmax;        // optional [grid][w][2] = (signed value at max |y|, global row)
