@@ -1012,15 +1012,23 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
   // U = Q U_B[:, :K] = Y1 (T2 J[:, :K])
   launch_small_gemm(T2, l, 0, J, l, Wf, l, l, l, K, nullptr, st);
   c->launches += 2;
-  Pass pc;
-  if ((rc = plan_pass(c, pc, M, {Seg{Y, ldy, l, 0}}, 0, l, K, Wf, l, false, false, false))) return rc;
-  const int nchunks = pc.map.nchunks;
-  if ((rc = ensure(c, c->colmax, sizeof(double) * (size_t)nchunks * K * 2))) return rc;
-  pc.p.Yout = U_out;
-  pc.p.ldy = ldo;
-  pc.p.colmax = (double*)c->colmax.ptr;
-  pc.p.row_offset = c->ex_row_offset;
-  if ((rc = run_pass(c, pc, st))) return rc;
+  int nchunks;
+  if (qw_colmax_supported(l, K)) {
+    nchunks = qw_colmax_chunks(M, c->num_sms);
+    if ((rc = ensure(c, c->colmax, sizeof(double) * (size_t)nchunks * K * 2))) return rc;
+    launch_qw_colmax(Y, ldy, M, l, Wf, K, U_out, ldo, c->ex_row_offset, (double*)c->colmax.ptr, c->num_sms, st);
+    c->launches++;
+  } else {
+    Pass pc;
+    if ((rc = plan_pass(c, pc, M, {Seg{Y, ldy, l, 0}}, 0, l, K, Wf, l, false, false, false))) return rc;
+    nchunks = pc.map.nchunks;
+    if ((rc = ensure(c, c->colmax, sizeof(double) * (size_t)nchunks * K * 2))) return rc;
+    pc.p.Yout = U_out;
+    pc.p.ldy = ldo;
+    pc.p.colmax = (double*)c->colmax.ptr;
+    pc.p.row_offset = c->ex_row_offset;
+    if ((rc = run_pass(c, pc, st))) return rc;
+  }
   if ((rc = exchange_sign(c, (const double*)c->colmax.ptr, nchunks, K, sgn, st))) return rc;
   launch_scale_cols(U_out, ldo, M, K, sgn, st);
   cudaMemcpyAsync(sigma_out, S, sizeof(double) * K, cudaMemcpyDeviceToDevice, st);
@@ -1247,7 +1255,7 @@ int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu
   if (nb < 1 || !A || !lda || !B || !Omega || !U_out || !sigma_hist)
     return fail(c, PSVD_EINVAL, "bad rand_stream_run arguments");
   if (K < 1 || l < K || q < 0) return fail(c, PSVD_EINVAL, "bad sketch K=%d l=%d q=%d", K, l, q);
-  if (l > TMA_MAX_Y || !tma_available())
+  if (l > TMA_MAX_Y || !tma_available() || !qw_colmax_supported(l, K))
     return fail(c, PSVD_EINVAL, "sketch width %d not supported by the pipelined run (use psvd_rand_update)", l);
   if (c->ex_allreduce) return fail(c, PSVD_EINVAL, "the pipelined randomized run is single-GPU");
   if (Kc != 0 && Kc != K) return fail(c, PSVD_EINVAL, "initial state carries %d modes, K=%d", Kc, K);
@@ -1398,12 +1406,11 @@ int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu
     double* G2c = G2[b & 1];
     mark("hi:update", b, hi);
     if (b > 0) {  // tall sign rule of U_{b-1} = Q Wf (linalg.py:161, 81-91): argmax pass, no write
-      Pass ps;
-      if ((rc = plan_pass(c, ps, M, {Seg{Qp, ldqp, l, 0}}, 0, l, K, Wfp, l, false, false, false))) return rc;
-      if ((rc = ensure(c, c->colmax, sizeof(double) * (size_t)ps.map.nchunks * K * 2))) return rc;
-      ps.p.colmax = (double*)c->colmax.ptr;
-      if ((rc = run_pass(c, ps, hi))) return rc;
-      if ((rc = exchange_sign(c, (const double*)c->colmax.ptr, ps.map.nchunks, K, sgn, hi))) return rc;
+      const int nch = qw_colmax_chunks(M, c->num_sms);
+      if ((rc = ensure(c, c->colmax, sizeof(double) * (size_t)nch * K * 2))) return rc;
+      launch_qw_colmax(Qp, ldqp, M, l, Wfp, K, nullptr, 0, c->ex_row_offset, (double*)c->colmax.ptr, c->num_sms, hi);
+      c->launches++;
+      if ((rc = exchange_sign(c, (const double*)c->colmax.ptr, nch, K, sgn, hi))) return rc;
     }
     mark("hi:sign_end", b, hi);
     cudaStreamWaitEvent(hi, c->ev_aa[b & 1], 0);
@@ -1493,17 +1500,14 @@ int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu
     if ((rc = cuda_check(c, "randomized stream update"))) return rc;
   }
   {  // U = Q Wf with the sign rule, written once
-    Pass pc;
     const double* Ql = Qb[(nb - 1) & 1];
-    if ((rc = plan_pass(c, pc, M, {Seg{Ql, ldq, l, 0}}, 0, l, K, Wf[(nb - 1) & 1], l, false, false, false))) return rc;
-    if ((rc = ensure(c, c->colmax, sizeof(double) * (size_t)pc.map.nchunks * K * 2))) return rc;
-    pc.p.Yout = U_out;
-    pc.p.ldy = ldo;
-    pc.p.colmax = (double*)c->colmax.ptr;
-    if ((rc = run_pass(c, pc, hi))) return rc;
-    if ((rc = exchange_sign(c, (const double*)c->colmax.ptr, pc.map.nchunks, K, sgn, hi))) return rc;
+    const int nch = qw_colmax_chunks(M, c->num_sms);
+    if ((rc = ensure(c, c->colmax, sizeof(double) * (size_t)nch * K * 2))) return rc;
+    launch_qw_colmax(Ql, ldq, M, l, Wf[(nb - 1) & 1], K, U_out, ldo, c->ex_row_offset, (double*)c->colmax.ptr,
+                     c->num_sms, hi);
+    if ((rc = exchange_sign(c, (const double*)c->colmax.ptr, nch, K, sgn, hi))) return rc;
     launch_scale_cols(U_out, ldo, M, K, sgn, hi);
-    c->launches++;
+    c->launches += 2;
   }
   cudaEventRecord(c->ev_join, lo);
   cudaStreamWaitEvent(user, c->ev_join, 0);

@@ -489,4 +489,112 @@ __global__ void rs_ident_kernel(double* __restrict__ I, double* __restrict__ one
 
 void launch_rs_ident(double* I, double* ones, int K, cudaStream_t st) { rs_ident_kernel<<<1, 256, 0, st>>>(I, ones, K); }
 
+
+// ---------------------------------------------------------------- U = Q W with the column argmax
+// Narrow recompose for the sign rule of the randomized path (linalg.py:161, 81-91): Q (M x l,
+// l <= 32) times W (l x K, K <= 16), optionally written to U, and per CTA (a contiguous row
+// range, so CTA order = row order) the (signed value at max |u|, global row) of every column,
+// ties to the lowest row.  A plain bandwidth kernel: a handful of FMAs per loaded double, many
+// CTAs per SM (the TMA pass's one-CTA-per-SM ring is latency-bound on panels this narrow).
+constexpr int QW_THREADS = 256;
+constexpr int QW_KMAX = 16;
+
+template <int LM, int KM>
+__global__ void __launch_bounds__(QW_THREADS, 2) qw_colmax_kernel(const double* __restrict__ Q, int64_t ldq, int64_t M,
+                                                                  int l, const double* __restrict__ W, int K,
+                                                                  double* __restrict__ U, int64_t ldu,
+                                                                  int64_t rows_per_cta, int64_t row_offset,
+                                                                  double* __restrict__ colmax) {
+  __shared__ double sW[LM * KM];
+  // per thread and column: |u| max in a register, (row << 1 | negative) of it in shared memory
+  __shared__ long long srow[KM][QW_THREADS];
+  __shared__ double rb[QW_THREADS / 32][KM];
+  __shared__ long long rr[QW_THREADS / 32][KM];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < LM * KM; i += QW_THREADS) {
+    const int j = i / KM, k = i % KM;
+    sW[i] = (j < l && k < K) ? W[(size_t)k * l + j] : 0.0;  // sW[j][k], zero padded
+  }
+#pragma unroll
+  for (int k = 0; k < KM; ++k) srow[k][tid] = -1;
+  __syncthreads();
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta, r1 = min(M, r0 + rows_per_cta);
+  double ba[KM];
+#pragma unroll
+  for (int k = 0; k < KM; ++k) ba[k] = -1.0;
+  for (int64_t r = r0 + tid; r < r1; r += QW_THREADS) {
+    double q[LM];
+#pragma unroll
+    for (int j = 0; j < LM; ++j) q[j] = j < l ? __ldg(Q + (size_t)j * ldq + r) : 0.0;  // l loads in flight
+#pragma unroll
+    for (int k = 0; k < KM; ++k) {
+      double u = 0.0;
+#pragma unroll
+      for (int j = 0; j < LM; ++j) u = fma(q[j], sW[j * KM + k], u);
+      if (k < K) {
+        if (U != nullptr) U[(size_t)k * ldu + r] = u;
+        if (fabs(u) > ba[k]) {
+          ba[k] = fabs(u);
+          srow[k][tid] = (r << 1) | (u < 0.0 ? 1 : 0);
+        }
+      }
+    }
+  }
+  if (colmax == nullptr) return;
+  // warp then block reduction, ties to the smaller row (numpy argmax: first occurrence)
+#pragma unroll
+  for (int k = 0; k < KM; ++k) {
+    double a = ba[k];
+    long long rw = srow[k][tid];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double oa = __shfl_xor_sync(0xffffffffu, a, off);
+      const long long orw = __shfl_xor_sync(0xffffffffu, rw, off);
+      if (oa > a || (oa == a && orw >= 0 && (rw < 0 || (orw >> 1) < (rw >> 1)))) { a = oa; rw = orw; }
+    }
+    if (lane == 0) { rb[warp][k] = a; rr[warp][k] = rw; }
+  }
+  __syncthreads();
+  if (tid < K) {
+    double a = -1.0;
+    long long rw = -1;
+    for (int w = 0; w < QW_THREADS / 32; ++w) {
+      const double oa = rb[w][tid];
+      const long long orw = rr[w][tid];
+      if (oa > a || (oa == a && orw >= 0 && (rw < 0 || (orw >> 1) < (rw >> 1)))) { a = oa; rw = orw; }
+    }
+    double* dst = colmax + ((size_t)blockIdx.x * K + tid) * 2;
+    dst[0] = rw < 0 ? 0.0 : ((rw & 1) ? -a : a);
+    dst[1] = rw < 0 ? -1.0 : (double)(rw >> 1) + (double)row_offset;
+  }
+}
+
+// rows per CTA (multiple of 32) and the CTA count = number of argmax chunks
+int64_t qw_colmax_rows(int64_t M, int num_sms) {
+  const int64_t target = std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * 4, (M + 255) / 256));
+  return ((M + target - 1) / target + 31) / 32 * 32;
+}
+int qw_colmax_chunks(int64_t M, int num_sms) {
+  const int64_t rows = qw_colmax_rows(M, num_sms);
+  return (int)((M + rows - 1) / rows);
+}
+
+bool qw_colmax_supported(int l, int K) { return l >= 1 && l <= 32 && K >= 1 && K <= QW_KMAX; }
+
+void launch_qw_colmax(const double* Q, int64_t ldq, int64_t M, int l, const double* W, int K, double* U, int64_t ldu,
+                      int64_t row_offset, double* colmax, int num_sms, cudaStream_t st) {
+  const int64_t rows = qw_colmax_rows(M, num_sms);
+  const int grid = (int)((M + rows - 1) / rows);
+#define QW_LAUNCH(LM_, KM_) \
+  qw_colmax_kernel<LM_, KM_><<<grid, QW_THREADS, 0, st>>>(Q, ldq, M, l, W, K, U, ldu, rows, row_offset, colmax)
+  if (l <= 16) {
+    if (K <= 8) QW_LAUNCH(16, 8); else QW_LAUNCH(16, 16);
+  } else if (l <= 24) {
+    if (K <= 8) QW_LAUNCH(24, 8); else if (K <= 12) QW_LAUNCH(24, 12); else QW_LAUNCH(24, 16);
+  } else {
+    if (K <= 8) QW_LAUNCH(32, 8); else QW_LAUNCH(32, 16);
+  }
+#undef QW_LAUNCH
+}
+
 }  // namespace psvd

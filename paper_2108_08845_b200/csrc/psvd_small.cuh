@@ -94,5 +94,12 @@ void launch_rs_post(const double* tiles, int NB, int q_c0, int a_c0, int y_c0, i
 void launch_rs_w0(const double* Etop, int lq, int K, const double* Qz, int n, int B, int l, int have_q, double* W0,
                   cudaStream_t st);
 void launch_rs_ident(double* I, double* ones, int K, cudaStream_t st);
+// U = Q W (optional write) with per-CTA column argmax pairs for the sign rule: qw_colmax_chunks
+// CTAs over contiguous row ranges (chunk order = row order).
+int64_t qw_colmax_rows(int64_t M, int num_sms);
+int qw_colmax_chunks(int64_t M, int num_sms);
+bool qw_colmax_supported(int l, int K);
+void launch_qw_colmax(const double* Q, int64_t ldq, int64_t M, int l, const double* W, int K, double* U, int64_t ldu,
+                      int64_t row_offset, double* colmax, int num_sms, cudaStream_t st);
 
 }  // namespace psvd

@@ -198,6 +198,7 @@ def _run_window(state, mats, config, dev, ready=None):
 
 
 RAND_STREAM_MAX_WIDTH = 32  # widest sketch of the pipelined randomized run (narrow TMA passes)
+RAND_STREAM_MAX_K = 16      # most modes of the pipelined run (its U = Q W argmax kernel)
 
 
 def _run_rand_window(state, mats, config, dev, ready=None):
@@ -256,7 +257,8 @@ def stream_all(batches, config, device=None):
     through the pipelined psvd_rand_stream_run, wider sketches per batch."""
     state = None
     history = []
-    if config.sketch is not None and config.sketch.sketch_width > RAND_STREAM_MAX_WIDTH:
+    if config.sketch is not None and (config.sketch.sketch_width > RAND_STREAM_MAX_WIDTH
+                                      or config.k_modes > RAND_STREAM_MAX_K):
         for batch in batches:
             if state is None:
                 state = stream_initialize(batch, config, device)
