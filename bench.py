@@ -75,37 +75,76 @@ def args_():
 # ------------------------------------------------------------------ clocks
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms while running."""
+    """SM clock and clock-event (throttle) reasons sampled DURING the timed region:
+    NVML every 2 ms on a thread (one sample at entry and exit at least), falling back
+    to `nvidia-smi -lms 200` when NVML is unavailable."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, index):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, max_mhz, set of reasons)
         self.proc = None
+        self.nvml = None
+        self._stop = threading.Event()
+
+    def _nvml_sample(self):
+        nv, h = self.nvml
+        try:
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+        reasons = {n for n, b in zip(self.NAMES, bits) if r & b}
+        self.rows.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                          float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)), reasons))
+
+    def _nvml_loop(self):
+        while not self._stop.is_set():
+            try:
+                self._nvml_sample()
+            except Exception:
+                return
+            self._stop.wait(0.002)
 
     def __enter__(self):
         if os.environ.get("PSVD_NO_CLOCKS"):
             return self
         try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nvml = (nv, nv.nvmlDeviceGetHandleByIndex(self.index))
+            self._nvml_sample()
+            self.t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.t.start()
+            return self
+        except Exception:
+            self.nvml = None
+        try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._smi_read, daemon=True)
             self.t.start()
         except Exception:
             self.proc = None
         return self
 
-    def _read(self):
+    def _smi_read(self):
         for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 7:
-                self.rows.append(parts)
+            parts = [q.strip() for q in line.split(",")]
+            if len(parts) == 6 and parts[0].replace(".", "").isdigit():
+                self.rows.append((float(parts[0]), float(parts[1]) if parts[1].replace(".", "").isdigit() else 0.0,
+                                  {n for n, v in zip(self.NAMES, parts[2:]) if v.lower() == "active"}))
 
     def __exit__(self, *a):
+        if self.nvml is not None:
+            self._stop.set()
+            self.t.join(timeout=1)
         if self.proc is not None:
             self.proc.terminate()
             try:
@@ -113,15 +152,21 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
+    def sample_now(self):
+        """One extra sample (call while the timed work is still queued on the GPU)."""
+        if self.nvml is not None:
+            try:
+                self._nvml_sample()
+            except Exception:
+                pass
+
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "samples": len(self.rows), "reasons": reasons}
+        sm = [r[0] for r in self.rows]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in self.rows),
+                "samples": len(self.rows), "source": "nvml" if self.nvml is not None else "nvidia-smi",
+                "reasons": sorted(set().union(*[r[2] for r in self.rows]))}
 
 
 # ------------------------------------------------------------------ CPU reference
@@ -296,6 +341,7 @@ def run_ours(a):
         for _ in range(a.steps):
             step(record=True)
         t1.record(stream)
+        clk.sample_now()  # the queued steps are still running
         barrier()
     launches = nat.lib().psvd_launch_count(c) - launches0
     ms = t0.elapsed_time(t1)

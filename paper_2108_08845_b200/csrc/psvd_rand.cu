@@ -256,44 +256,62 @@ void launch_chol_inv(const double* G, int l, double* T, cudaStream_t st, int* il
 
 // ---------------------------------------------------------------- tall sign rule
 // colmax: [nchunks][K][2] = (signed value at max |u|, global row) per chunk in row
-// order; the first chunk wins ties (lowest row, numpy argmax).  sign = +1 for >= 0.
-__global__ void colmax_sign_kernel(const double* __restrict__ colmax, int nchunks, int K, double* __restrict__ sign) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= K) return;
-  double best = -1.0, val = 0.0;
-  for (int c = 0; c < nchunks; ++c) {
-    const double v = colmax[((size_t)c * K + k) * 2];
-    if (fabs(v) > best) {
-      best = fabs(v);
-      val = v;
+// order; the first chunk wins ties (lowest row, numpy argmax).  One CTA per column: each
+// thread scans a strided subset of the chunks in increasing order, then a tree reduction
+// that prefers the larger |value| and, on ties, the lower chunk index.
+constexpr int CM_THREADS = 256;
+
+__device__ void colmax_best(const double* __restrict__ colmax, int nchunks, int K, int k, double& val, double& row) {
+  __shared__ double sa[CM_THREADS], sv[CM_THREADS], sr[CM_THREADS];
+  __shared__ int sc[CM_THREADS];
+  double best = -1.0, v = 0.0, r = -1.0;
+  int bc = 0x7fffffff;
+  for (int c = threadIdx.x; c < nchunks; c += CM_THREADS) {
+    const double x = colmax[((size_t)c * K + k) * 2];
+    if (fabs(x) > best) {
+      best = fabs(x);
+      v = x;
+      r = colmax[((size_t)c * K + k) * 2 + 1];
+      bc = c;
     }
   }
-  sign[k] = val < 0.0 ? -1.0 : 1.0;  // applied with scale_cols (multiplies by +-1)
+  sa[threadIdx.x] = best; sv[threadIdx.x] = v; sr[threadIdx.x] = r; sc[threadIdx.x] = bc;
+  __syncthreads();
+  for (int o = CM_THREADS / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) {
+      const int j = threadIdx.x + o;
+      if (sa[j] > sa[threadIdx.x] || (sa[j] == sa[threadIdx.x] && sc[j] < sc[threadIdx.x])) {
+        sa[threadIdx.x] = sa[j]; sv[threadIdx.x] = sv[j]; sr[threadIdx.x] = sr[j]; sc[threadIdx.x] = sc[j];
+      }
+    }
+    __syncthreads();
+  }
+  val = sv[0];
+  row = sr[0];
+}
+
+__global__ void colmax_sign_kernel(const double* __restrict__ colmax, int nchunks, int K, double* __restrict__ sign) {
+  double v, r;
+  colmax_best(colmax, nchunks, K, blockIdx.x, v, r);
+  if (threadIdx.x == 0) sign[blockIdx.x] = v < 0.0 ? -1.0 : 1.0;  // applied with scale_cols (multiplies by +-1)
 }
 
 // one (value, row) pair per column from the per-chunk pairs (first chunk wins ties)
 __global__ void colmax_reduce_kernel(const double* __restrict__ colmax, int nchunks, int K, double* __restrict__ out) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= K) return;
-  double best = -1.0, val = 0.0, row = -1.0;
-  for (int c = 0; c < nchunks; ++c) {
-    const double v = colmax[((size_t)c * K + k) * 2];
-    if (fabs(v) > best) {
-      best = fabs(v);
-      val = v;
-      row = colmax[((size_t)c * K + k) * 2 + 1];
-    }
+  double v, r;
+  colmax_best(colmax, nchunks, K, blockIdx.x, v, r);
+  if (threadIdx.x == 0) {
+    out[(size_t)blockIdx.x * 2] = v;
+    out[(size_t)blockIdx.x * 2 + 1] = r;
   }
-  out[(size_t)k * 2] = val;
-  out[(size_t)k * 2 + 1] = row;
 }
 
 void launch_colmax_reduce(const double* colmax, int nchunks, int K, double* out, cudaStream_t st) {
-  colmax_reduce_kernel<<<(K + 127) / 128, 128, 0, st>>>(colmax, nchunks, K, out);
+  colmax_reduce_kernel<<<K, CM_THREADS, 0, st>>>(colmax, nchunks, K, out);
 }
 
 void launch_colmax_sign(const double* colmax, int nchunks, int K, double* sign, cudaStream_t st) {
-  colmax_sign_kernel<<<(K + 127) / 128, 128, 0, st>>>(colmax, nchunks, K, sign);
+  colmax_sign_kernel<<<K, CM_THREADS, 0, st>>>(colmax, nchunks, K, sign);
 }
 
 __global__ void scale_cols_kernel(double* __restrict__ U, int64_t ld, int64_t M, int K, const double* __restrict__ s) {
