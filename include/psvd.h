@@ -147,6 +147,10 @@ int psvd_stream_update(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, c
  * and joined back into it.  batch_ready (optional, nb cudaEvent_t or NULL
  * entries): batch j is read only after its event, so host->device copies of
  * later batches can overlap the updates of earlier ones. */
+/* 1 in *ok when psvd_stream_run supports batches of up to Bmax columns with K modes on M rows
+ * (its look-ahead Gram and fused pass plan within the kernels' limits), else 0: stream those
+ * batches through psvd_stream_update. */
+int psvd_stream_run_supported(psvd_ctx* ctx, int64_t M, int K, int Bmax, int* ok);
 int psvd_stream_run(psvd_ctx* ctx, int64_t M, const double* U_in, int64_t ldu, const double* sigma_in, int Kc,
                     int nb, const double* const* A, const int64_t* lda, const int* B, int K, double ff, int rescue,
                     double* U_a, double* U_b, int64_t ldo, double* sigma_hist, int* final_buf,
@@ -189,10 +193,44 @@ int psvd_rand_update(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, con
  * (col-major, ld n_b; n_b = K + B[b] after the first update, B[0] when Kc = 0).  sigma_hist:
  * nb x K singular values per update.  Requires l <= 32 (returns PSVD_EINVAL otherwise: use
  * psvd_rand_update per batch) and no exchange hooks (single GPU). */
+/* 1 in *ok when psvd_rand_stream_run's passes plan for batches of up to Bmax columns (sketch
+ * width l, K modes, q power iterations) on M rows, else 0: use psvd_rand_update per batch. */
+int psvd_rand_stream_run_supported(psvd_ctx* ctx, int64_t M, int K, int l, int q, int Bmax, int* ok);
 int psvd_rand_stream_run(psvd_ctx* ctx, int64_t M, const double* U_in, int64_t ldu, const double* sigma_in, int Kc,
                          int nb, const double* const* A, const int64_t* lda, const int* B, int K, int l, int q,
                          double ff, const double* const* Omega, double* U_out, int64_t ldo, double* sigma_hist,
                          void* const* batch_ready, void* stream);
+
+/* ---- dense factorizations behind the reference's linalg boundary ----
+ * qr_factor (linalg.py:94-104): psvd_qr, tall A (M >= n, n <= 112): CholeskyQR2, or the shifted
+ * CholeskyQR3 when the first Cholesky flags cond(A) beyond CholeskyQR2's range (one host sync to
+ * read that flag).  Q: M x n (ld ldq), R: n x n (ld n) upper with diag(R) >= 0.
+ * svd_full (linalg.py:107-123): psvd_jacobi, one-sided Jacobi SVD of X (m x n, m >= n, n <= 160;
+ * S descending, V n x n), composed with psvd_qr for tall inputs; psvd_sign_pair applies the
+ * reference's sign rule (linalg.py:81-91) to U and the same flips to V.
+ * randomized_range (linalg.py:126-147): psvd_nn_product (Y = A W, A tall) with psvd_tn_product
+ * and psvd_qr.  parallel_qr (dsvd.py:176-202): psvd_gram + rank-ordered sum + psvd_chol
+ * (R and R^-1 of a Gram, n <= 112) + psvd_nn_product + psvd_small_matmul (C = op(A) B, small). */
+int psvd_chol(psvd_ctx* ctx, const double* G, int n, double* R, double* T, void* stream);
+int psvd_chol_shift(psvd_ctx* ctx, double* G, int n, int64_t M, void* stream);
+int psvd_chol_illcond(psvd_ctx* ctx, int* flag, void* stream);
+int psvd_nn_product(psvd_ctx* ctx, int64_t M, const double* A, int64_t lda, int n, const double* W, int64_t ldw, int w,
+                    double* Y, int64_t ldy, void* stream);
+int psvd_small_matmul(psvd_ctx* ctx, const double* A, int lda, int transA, const double* B, int ldb, double* C,
+                      int ldc, int m, int k, int n, void* stream);
+int psvd_qr(psvd_ctx* ctx, int64_t M, int n, const double* A, int64_t lda, double* Q, int64_t ldq, double* R,
+            void* stream);
+int psvd_jacobi(psvd_ctx* ctx, const double* X, int64_t ldx, int64_t m, int n, double* S, double* V, int64_t ldv,
+                void* stream);
+int psvd_sign_pair(psvd_ctx* ctx, double* U, int64_t ldu, int64_t rows, int cols, double* V, int64_t ldv,
+                   int64_t vrows, void* stream);
+
+/* X[:, j] *= s_j, or /= s_j (0 where s_j == 0) with invert = 1. */
+int psvd_scale_cols(psvd_ctx* ctx, double* X, int64_t ld, int64_t rows, int cols, const double* s, int invert,
+                    void* stream);
+/* low_rank_svd's right factor (linalg.py:157-162) from the last psvd_rand_update on this context
+ * (same stream, right after it): vt (K x n, ld ldvt), rows signed like the returned U's columns. */
+int psvd_rand_last_vt(psvd_ctx* ctx, int n, int l, int K, double* Vt, int64_t ldvt, void* stream);
 
 /* ---- row-parallel helpers ---- */
 

@@ -8,12 +8,13 @@ kernels (libpsvd.so, include/psvd.h) on state that stays in HBM.
 
 from .oneshot import ApmosConfig, apmos, generate_right_vectors  # noqa: F401
 from .datagen import burgers_device, burgers_matrix, burgers_solution, partition_bounds  # noqa: F401
-from .dsvd import (LocalModes, RankContext, gather_modes, parallel_stream_incorporate,  # noqa: F401
+from .dsvd import (LocalModes, RankContext, gather_modes, parallel_qr, parallel_stream_incorporate,  # noqa: F401
                    parallel_stream_initialize)
 from .errors import (CapacityError, CollectiveTimeout, ConvergenceError, DegenerateModeError,  # noqa: F401
                      MatrixFormatError)
 from .io import BatchSource, read_batches, read_matrix, read_matrix_header, read_submatrix, write_matrix  # noqa: F401
-from .linalg import RandomSketchConfig, low_rank_svd  # noqa: F401
+from .linalg import (QrResult, RandomSketchConfig, SvdResult, aligned_mode_difference, low_rank_svd,  # noqa: F401
+                     qr_factor, randomized_range, subspace_angles, svd_full)
 from .streaming import StreamConfig, StreamState, stream_all, stream_incorporate, stream_initialize  # noqa: F401
 
 from . import streaming  # noqa: F401,E402  (module access: STREAM_WINDOW)

@@ -62,6 +62,18 @@ _SIGS = {
     "psvd_rand_stream_run": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_int, _c_int, ctypes.POINTER(_vp),
                                       ctypes.POINTER(_c_i64), ctypes.POINTER(_c_int), _c_int, _c_int, _c_int,
                                       _c_dbl, ctypes.POINTER(_vp), _vp, _c_i64, _vp, ctypes.POINTER(_vp), _vp]),
+    "psvd_chol": (_c_int, [_vp, _vp, _c_int, _vp, _vp, _vp]),
+    "psvd_chol_shift": (_c_int, [_vp, _vp, _c_int, _c_i64, _vp]),
+    "psvd_chol_illcond": (_c_int, [_vp, ctypes.POINTER(_c_int), _vp]),
+    "psvd_nn_product": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _vp, _c_i64, _vp]),
+    "psvd_small_matmul": (_c_int, [_vp, _vp, _c_int, _c_int, _vp, _c_int, _vp, _c_int, _c_int, _c_int, _c_int, _vp]),
+    "psvd_qr": (_c_int, [_vp, _c_i64, _c_int, _vp, _c_i64, _vp, _c_i64, _vp, _vp]),
+    "psvd_jacobi": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _vp, _vp, _c_i64, _vp]),
+    "psvd_sign_pair": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _vp, _c_i64, _c_i64, _vp]),
+    "psvd_scale_cols": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _vp, _c_int, _vp]),
+    "psvd_rand_last_vt": (_c_int, [_vp, _c_int, _c_int, _c_int, _vp, _c_i64, _vp]),
+    "psvd_stream_run_supported": (_c_int, [_vp, _c_i64, _c_int, _c_int, ctypes.POINTER(_c_int)]),
+    "psvd_rand_stream_run_supported": (_c_int, [_vp, _c_i64, _c_int, _c_int, _c_int, _c_int, ctypes.POINTER(_c_int)]),
     "psvd_sum_ordered": (_c_int, [_vp, _vp, _c_int, _c_i64, _vp, _vp]),
     "psvd_burgers": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _c_i64, _c_int, _c_int, _c_int, _c_dbl,
                               _c_dbl, _c_dbl, _vp]),

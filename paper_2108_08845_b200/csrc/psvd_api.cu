@@ -51,6 +51,7 @@ struct psvd_ctx {
   int64_t ex_row_offset = 0;
   Buf partial2, tiles2[2];  // A^T A passes on the low-priority stream (double-buffered tiles)
   Buf zbuf, rs2;            // pipelined randomized stream: look-ahead sketch Z = A Omega_A, small matrices
+  Buf dense, dense2;        // dense utilities (psvd_qr / psvd_jacobi): small factors, a tall temporary
   cudaEvent_t ev_qready = nullptr;  // pipelined randomized stream: the sketch basis of the last update is final
   cudaStream_t s_hi = nullptr, s_lo = nullptr;  // pipelined stream_run: critical chain / look-ahead Grams
   cudaStream_t s_aux = nullptr;                  // concurrent LDL^T of the split core solve
@@ -248,7 +249,8 @@ static int plan_tiles_tma(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int
          (ps.p.wk + 7) / 8 >= 2 * (yks + 1) && yks * nyo <= 10)  // partial slots: (yks - 1) * nyo <= 10
     ++yks;
   ps.p.yks = yks;
-  const int warp0 = nyo * yks, nwarps = NWARP - 1 - warp0;
+  static const int cap = getenv("PSVD_TMA_SLICE_WARPS") ? atoi(getenv("PSVD_TMA_SLICE_WARPS")) : 0;  // diagnostics
+  const int warp0 = nyo * yks, nwarps = cap > 0 ? std::min(cap, NWARP - 1 - warp0) : NWARP - 1 - warp0;
   const int nslices = std::max(1, (nt + nwarps - 1) / nwarps);
   if (nt > MAX_OUT_TILES || nslices > MAX_SLICES) return fail(c, PSVD_EINVAL, "panel too wide (%d tiles)", nt);
   ps.p.nslices = nslices;
@@ -316,7 +318,10 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
       if (!ok) tma = false;
       use_gaps = false;
     }
-    const int pw = use_gaps ? rup(np8, 32) : rup(np, 32) + 8;
+    // + 8 per 256-column box boundary: equal boxes may end up to 8 columns past the panel
+    int nbig = 0;
+    for (size_t i = 0; i < segs.size(); ++i) nbig += (segs[i].ncols + 7) / 256;
+    const int pw = (use_gaps ? rup(np8, 32) : rup(np, 32) + 8) + 8 * nbig;
     if (tma && tma_pass_smem_bytes(pw, rup(wk, 8) + 8 * (int)segs.size(), rup(w, 8)) > (size_t)SMEM_LIMIT) {
       tma = false;
       pshift = 0;
@@ -405,10 +410,16 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
   }
   if ((tma || ps.gtma) && tma_pass_prepare(p, ps.maps, ps.x, tma ? pshift : 0) != 0)
     return fail(c, PSVD_ECUDA, "TMA descriptor setup failed");
+  if (tma && tma_pass_smem_bytes(ps.x.pwidth, ps.x.kp_hi - ps.x.kp_lo, p.w_pad, ps.x.ns, 1) > (size_t)SMEM_LIMIT)
+    return fail(c, PSVD_EINVAL, "narrow pass ring of %d columns exceeds shared memory", ps.x.pwidth);
   return PSVD_OK;
 }
 
 int run_pass(psvd_ctx* c, Pass& ps, cudaStream_t st) {
+  if (ps.p.Yout != nullptr && ps.p.nslices > 1)
+    for (int i = 0; i < ps.p.nseg; ++i)
+      if (ps.p.seg[i].ptr == ps.p.Yout)
+        return fail(c, PSVD_EINVAL, "in-place pass with %d slices would race", ps.p.nslices);
   c->path_count[ps.tma ? 0 : ps.gtma ? 1 : ps.ws ? 2 : 3]++;
   if (ps.tma)
     launch_pass_tma(ps.p, ps.maps, ps.x, ps.grid, st);
@@ -420,7 +431,16 @@ int run_pass(psvd_ctx* c, Pass& ps, cudaStream_t st) {
     launch_tall(ps.p, ps.grid, st);
   c->launches += 1 + (ps.map.nout > 0);
   int rc = cuda_check(c, "tall pass");
-  if (rc) return rc;
+  if (rc) {
+    char buf[400];
+    snprintf(buf, sizeof(buf), " [%s pass: np=%d np_pad=%d w=%d wk=%d nseg=%d grid=%d pwidth=%d kspan=%d ns=%d smem=%zu]",
+             ps.tma ? "narrow TMA" : ps.gtma ? "TMA Gram" : ps.ws ? "ws Gram" : "general", ps.p.np, ps.p.np_pad, ps.p.w,
+             ps.p.wk, ps.p.nseg, ps.grid, ps.x.pwidth, ps.x.kp_hi - ps.x.kp_lo, ps.x.ns,
+             ps.tma ? tma_pass_smem_bytes(ps.x.pwidth, ps.x.kp_hi - ps.x.kp_lo, ps.p.w_pad, ps.x.ns, 1)
+                    : tall_smem_bytes(ps.p.ks, ps.p.np_pad, ps.p.wk, ps.p.w, ps.p.nstage));
+    c->err += buf;
+    return rc;
+  }
   if (ps.map.nout > 0) {
     launch_tall_reduce((const double*)ps.part->ptr, ps.map, (double*)ps.tl->ptr, st);
     rc = cuda_check(c, "tall reduce");
@@ -452,6 +472,27 @@ __global__ void stamp_kernel(unsigned long long* out) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   *out = t;
+}
+
+__global__ void scale_cols_any_kernel(double* __restrict__ X, int64_t ld, int64_t rows, int cols,
+                                      const double* __restrict__ s, int invert) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y;
+  if (i >= rows || j >= cols) return;
+  const double f = s[j];
+  double& x = X[(size_t)j * ld + i];
+  x = invert ? (f != 0.0 ? x / f : 0.0) : x * f;
+}
+
+__global__ void rand_vt_kernel(const double* __restrict__ Bt, int n, int l, const double* __restrict__ J,
+                               const double* __restrict__ S, const double* __restrict__ sgn, int K,
+                               double* __restrict__ Vt, int64_t ldvt) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n * K) return;
+  const int k = idx % K, j = idx / K;
+  double v = 0.0;
+  for (int i = 0; i < l; ++i) v = fma(Bt[(size_t)i * n + j], J[(size_t)k * l + i], v);
+  Vt[(size_t)j * ldvt + k] = S[k] != 0.0 ? sgn[k] * v / S[k] : 0.0;
 }
 
 __global__ void sum_ordered_kernel(const double* __restrict__ parts, int P, int64_t count, double* __restrict__ out) {
@@ -547,7 +588,7 @@ int psvd_destroy(psvd_ctx* c) {
   cudaDeviceSynchronize();
   Buf* bufs[] = {&c->partial, &c->tiles, &c->gram, &c->eigws, &c->wbuf, &c->utu, &c->tbuf, &c->dvec, &c->colmax,
                  &c->ybuf, &c->ybuf2, &c->xpairs, &c->ssws, &c->rsmall, &c->jacws, &c->partial2, &c->tiles2[0], &c->tiles2[1],
-                 &c->zbuf, &c->rs2};
+                 &c->zbuf, &c->rs2, &c->dense, &c->dense2};
   for (Buf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
   if (c->s_hi) cudaStreamDestroy(c->s_hi);
@@ -634,13 +675,31 @@ int psvd_gram(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const double
   if (G == nullptr) return fail(c, PSVD_EINVAL, "G is null");
   const int n = Kc + B;
   const int nb32 = (n + 31) / 32;
-  if (Kc == 0 && nb32 * (nb32 + 1) / 2 > MAX_OUT_TILES) {
-    // too many 32x32 tiles for one pass: the tall-skinny TN GEMM (full n x n, split over rows)
+  if (nb32 * (nb32 + 1) / 2 > MAX_OUT_TILES) {
+    // too many 32x32 tiles for one pass: the tall-skinny TN GEMM (full n x n, split over rows),
+    // [U | A]^T U and [U | A]^T A, then the d_i d_j scaling of the panel [ff U S | A]
     c->path_count[4]++;
-    if ((rc = ensure(c, c->partial, sizeof(double) * tgemm_tn_partial_doubles(M, n, n, c->num_sms)))) return rc;
-    const GemmSeg ga{A, lda, B};
-    launch_tgemm_tn(M, &ga, 1, A, lda, B, nullptr, G, n, (double*)c->partial.ptr, c->num_sms, st);
-    c->launches += 2;
+    if ((rc = ensure(c, c->partial, sizeof(double) * tgemm_tn_partial_doubles(M, n, std::max(B, std::max(Kc, 1)),
+                                                                              c->num_sms))))
+      return rc;
+    std::vector<GemmSeg> gp;
+    if (Kc > 0) gp.push_back(GemmSeg{U, ldu, Kc});
+    if (B > 0) gp.push_back(GemmSeg{A, lda, B});
+    if ((rc = make_dvec(c, sigma, ff, Kc, n, st))) return rc;
+    const double* d = Kc > 0 ? (const double*)c->dvec.ptr : nullptr;
+    if (Kc > 0) {
+      launch_tgemm_tn(M, gp.data(), (int)gp.size(), U, ldu, Kc, d, G, n, (double*)c->partial.ptr, c->num_sms, st);
+      c->launches += 2;
+    }
+    if (B > 0) {
+      launch_tgemm_tn(M, gp.data(), (int)gp.size(), A, lda, B, d, G + (size_t)Kc * n, n, (double*)c->partial.ptr,
+                      c->num_sms, st);
+      c->launches += 2;
+    }
+    if (Kc > 0) {
+      launch_scale_cols(G, n, n, Kc, d, st);  // columns of the U block: d_j = ff sigma_j
+      c->launches++;
+    }
     return cuda_check(c, "wide gram");
   }
   Pass ps;
@@ -722,7 +781,23 @@ int psvd_recompose(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, int Kc,
     return rc;
   const int n = Kc + B;
   Pass ps;
-  if ((rc = plan_pass(c, ps, M, panel(U, ldu, Kc, A, lda, B), 0, n, K, W, n, false, UtU != nullptr, false))) return rc;
+  if (plan_pass(c, ps, M, panel(U, ldu, Kc, A, lda, B), 0, n, K, W, n, false, UtU != nullptr, false) != PSVD_OK) {
+    // panel + W beyond one pass's shared memory: U_out = [U | A] W and U_out^T U_out on the
+    // tall-skinny GEMMs (the panel is read once per product)
+    c->path_count[4]++;
+    std::vector<GemmSeg> gp;
+    if (Kc > 0) gp.push_back(GemmSeg{U, ldu, Kc});
+    gp.push_back(GemmSeg{A, lda, B});
+    launch_tgemm_nn(M, gp.data(), (int)gp.size(), W, n, K, U_out, ldo, st);
+    c->launches++;
+    if (UtU) {
+      if ((rc = ensure(c, c->partial, sizeof(double) * tgemm_tn_partial_doubles(M, K, K, c->num_sms)))) return rc;
+      const GemmSeg gu{U_out, ldo, K};
+      launch_tgemm_tn(M, &gu, 1, U_out, ldo, K, nullptr, UtU, K, (double*)c->partial.ptr, c->num_sms, st);
+      c->launches += 2;
+    }
+    return cuda_check(c, "wide recompose");
+  }
   ps.p.Yout = U_out;
   ps.p.ldy = ldo;
   if ((rc = run_pass(c, ps, st))) return rc;
@@ -913,6 +988,10 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
   std::vector<Seg> pa = panel(U, ldu, Kc, A, lda, B);
   std::vector<Seg> pb = pa;
   pb.push_back(Seg{Y, ldy, l, 0});
+  // the projection pass writes Y1 = Y T1 to a second buffer: with more than one slice CTA per row
+  // chunk an in-place update would race (slice 0 writes rows the other slices still read)
+  if ((rc = ensure(c, c->ybuf2, sizeof(double) * (size_t)ldy * l))) return rc;
+  double* Y1b = (double*)c->ybuf2.ptr;
   bool wide = l > MAX_W || getenv("PSVD_FORCE_WIDE") != nullptr;
   if (!wide) {  // dry-run plans of the fused passes (no launches): wide when they do not fit
     Pass t1, t2;
@@ -979,10 +1058,10 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
     c->launches++;
     if ((rc = ex_allreduce(c, G1, (int64_t)l * l, st))) return rc;
     if ((rc = svqb(c, G1, l, T1, sscr, st))) return rc;
-    // pass B: Y <- Y T1 (in place), (Y^T Y, D P^T Y)
+    // pass B: Y1 = Y T1 (into the second buffer), (Y1^T Y1, D P^T Y1)
     Pass pb_;
     if ((rc = plan_pass(c, pb_, M, pb, n, l, l, T1, l, false, true, true, n))) return rc;
-    pb_.p.Yout = Y;
+    pb_.p.Yout = Y1b;
     pb_.p.ldy = ldy;
     if ((rc = run_pass(c, pb_, st))) return rc;
     launch_extract_sym((const double*)c->tiles.ptr, pb_.NB, pb_.p.np_pad, l, nullptr, G2, st);
@@ -1016,11 +1095,11 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
   if (qw_colmax_supported(l, K)) {
     nchunks = qw_colmax_chunks(M, c->num_sms);
     if ((rc = ensure(c, c->colmax, sizeof(double) * (size_t)nchunks * K * 2))) return rc;
-    launch_qw_colmax(Y, ldy, M, l, Wf, K, U_out, ldo, c->ex_row_offset, (double*)c->colmax.ptr, c->num_sms, st);
+    launch_qw_colmax(Y1b, ldy, M, l, Wf, K, U_out, ldo, c->ex_row_offset, (double*)c->colmax.ptr, c->num_sms, st);
     c->launches++;
   } else {
     Pass pc;
-    if ((rc = plan_pass(c, pc, M, {Seg{Y, ldy, l, 0}}, 0, l, K, Wf, l, false, false, false))) return rc;
+    if ((rc = plan_pass(c, pc, M, {Seg{Y1b, ldy, l, 0}}, 0, l, K, Wf, l, false, false, false))) return rc;
     nchunks = pc.map.nchunks;
     if ((rc = ensure(c, c->colmax, sizeof(double) * (size_t)nchunks * K * 2))) return rc;
     pc.p.Yout = U_out;
@@ -1465,16 +1544,16 @@ int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu
       std::vector<Seg> segs;
       if (hq) segs.push_back(Seg{Qp, ldqp, lq, 0});
       segs.push_back(Seg{A[b], lda[b], B[b], 0});
-      Pass pA;  // sketch pass: Y = [Q | A] (E Qz), Y^T Y
+      Pass pA;  // sketch pass: Y = [Q | A] (E Qz), Y^T Y (into Z's buffer: Z_b was consumed by the first projection)
       if ((rc = plan_pass(c, pA, M, segs, 0, rows, l, W0, rows, false, true, false))) return rc;
-      pA.p.Yout = Qn;
+      pA.p.Yout = Zt;
       pA.p.ldy = ldq;
       if ((rc = run_pass(c, pA, hi))) return rc;
       launch_extract_sym((const double*)c->tiles.ptr, pA.NB, pA.p.np_pad, l, nullptr, G1, hi);
       c->launches++;
       if ((rc = svqb(c, G1, l, T1, sscr, hi))) return rc;
-      segs.push_back(Seg{Qn, ldq, l, 0});
-      Pass pB;  // projection pass: Y1 = Y T1 in place, Y1^T Y1, [Q | A]^T Y1
+      segs.push_back(Seg{Zt, ldq, l, 0});
+      Pass pB;  // projection pass: Y1 = Y T1 (not in place: slices), Y1^T Y1, [Q | A]^T Y1
       if ((rc = plan_pass(c, pB, M, segs, rows, l, l, T1, l, false, true, true, -1, -1, nullptr, nullptr, 0, 0, true)))
         return rc;
       pB.p.Yout = Qn;
@@ -1521,6 +1600,247 @@ int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu
     cudaFree(tbuf);
   }
   return cuda_check(c, "rand_stream_run");
+}
+
+// ---- dense factorizations behind the reference's linalg boundary (qr_factor / svd_full /
+// randomized_range, linalg.py:94-147; parallel_qr, dsvd.py:176-202).  Library utilities, not
+// the streaming update: psvd_qr reads one condition flag back (one host sync).
+
+int psvd_chol(psvd_ctx* c, const double* G, int n, double* R, double* T, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  if (n < 1 || n > CHOL_NMAX || !G || !T) return fail(c, PSVD_EINVAL, "bad Cholesky n=%d (1..%d)", n, CHOL_NMAX);
+  launch_chol_inv(G, n, T, (cudaStream_t)stream, c->d_status + 3, c->d_status, R);
+  c->launches++;
+  return cuda_check(c, "chol");
+}
+
+int psvd_chol_shift(psvd_ctx* c, double* G, int n, int64_t M, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  if (n < 1 || !G || M < 1) return fail(c, PSVD_EINVAL, "bad shift arguments");
+  launch_chol_shift(G, n, M, (cudaStream_t)stream);
+  c->launches++;
+  return cuda_check(c, "chol shift");
+}
+
+int psvd_chol_illcond(psvd_ctx* c, int* flag, void* stream) {
+  if (!c || !flag) return PSVD_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemcpyAsync(c->h_status, c->d_status + 3, sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check(c, "chol flag");
+  *flag = *c->h_status;
+  return PSVD_OK;
+}
+
+int psvd_nn_product(psvd_ctx* c, int64_t M, const double* A, int64_t lda, int n, const double* W, int64_t ldw, int w,
+                    double* Y, int64_t ldy, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  int rc;
+  if (M < 1 || n < 1 || w < 1 || !W || ldw < n) return fail(c, PSVD_EINVAL, "bad nn_product shape");
+  if ((rc = check_mat(c, "A", A, lda, M, n)) || (rc = check_mat(c, "Y", Y, ldy, M, w))) return rc;
+  const GemmSeg ga{A, lda, n};
+  launch_tgemm_nn(M, &ga, 1, W, ldw, w, Y, ldy, (cudaStream_t)stream);
+  c->launches++;
+  return cuda_check(c, "nn product");
+}
+
+int psvd_small_matmul(psvd_ctx* c, const double* A, int lda, int transA, const double* B, int ldb, double* C, int ldc,
+                      int m, int k, int n, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  if (m < 1 || k < 1 || n < 1 || !A || !B || !C || ldc < m) return fail(c, PSVD_EINVAL, "bad small matmul");
+  launch_small_gemm(A, lda, transA, B, ldb, C, ldc, m, k, n, nullptr, (cudaStream_t)stream);
+  c->launches++;
+  return cuda_check(c, "small matmul");
+}
+
+// Tall QR (M >= n, n <= CHOL_NMAX): CholeskyQR2 (R = R2 R1 from two Gram passes), or the shifted
+// CholeskyQR3 when the first Cholesky flags cond(A) beyond CholeskyQR2's range.  diag(R) >= 0 by
+// construction (qr_factor's sign convention, linalg.py:94-104); numerically null directions give zero
+// rows of R and zero columns of Q.  R: n x n, ld n.
+int psvd_qr(psvd_ctx* c, int64_t M, int n, const double* A, int64_t lda, double* Q, int64_t ldq, double* R,
+            void* stream) {
+  if (!c) return PSVD_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if (n < 1 || n > CHOL_NMAX || M < n) return fail(c, PSVD_EINVAL, "qr needs M >= n and n <= %d (M=%lld n=%d)",
+                                                  CHOL_NMAX, (long long)M, n);
+  if ((rc = check_mat(c, "A", A, lda, M, n)) || (rc = check_mat(c, "Q", Q, ldq, M, n))) return rc;
+  if (!R) return fail(c, PSVD_EINVAL, "R is null");
+  const size_t nn = (size_t)n * n;
+  const int64_t ldt = M + (M & 1);
+  if ((rc = ensure(c, c->dense, sizeof(double) * 8 * nn)) || (rc = ensure(c, c->dense2, sizeof(double) * ldt * n)))
+    return rc;
+  double* G = (double*)c->dense.ptr;
+  double* R1 = G + nn;
+  double* T1 = R1 + nn;
+  double* R2 = T1 + nn;
+  double* T2 = R2 + nn;
+  double* R3 = T2 + nn;
+  double* T3 = R3 + nn;
+  double* Rt = T3 + nn;
+  double* tmp = (double*)c->dense2.ptr;
+  auto gram = [&](const double* X, int64_t ldx) { return psvd_gram(c, M, nullptr, 0, nullptr, 1.0, 0, X, ldx, n, G, st); };
+  auto mul = [&](const double* X, int64_t ldx, const double* T, double* Y, int64_t ldy) {
+    const GemmSeg gx{X, ldx, n};
+    launch_tgemm_nn(M, &gx, 1, T, n, n, Y, ldy, st);
+    c->launches++;
+  };
+  auto refine = [&](double* Rk, double* Tk) -> int {  // Q <- Q chol(Q^T Q)^-1, returns the new factor in Rk
+    int r;
+    if ((r = gram(Q, ldq))) return r;
+    launch_chol_inv(G, n, Tk, st, nullptr, c->d_status, Rk);
+    mul(Q, ldq, Tk, tmp, ldt);
+    cudaMemcpy2DAsync(Q, ldq * sizeof(double), tmp, ldt * sizeof(double), M * sizeof(double), n,
+                      cudaMemcpyDeviceToDevice, st);
+    c->launches++;
+    return cuda_check(c, "qr refine");
+  };
+  // CholeskyQR2
+  if ((rc = gram(A, lda))) return rc;
+  launch_chol_inv(G, n, T1, st, c->d_status + 3, c->d_status, R1);
+  c->launches++;
+  int ill = 0;
+  if ((rc = psvd_chol_illcond(c, &ill, stream))) return rc;
+  if (ill) {  // shifted CholeskyQR3
+    if ((rc = gram(A, lda))) return rc;
+    launch_chol_shift(G, n, M, st);
+    launch_chol_inv(G, n, T1, st, nullptr, c->d_status, R1);
+    c->launches += 2;
+  }
+  mul(A, lda, T1, Q, ldq);
+  if ((rc = refine(R2, T2))) return rc;
+  launch_small_gemm(R2, n, 0, R1, n, ill ? Rt : R, n, n, n, n, nullptr, st);  // R2 R1
+  c->launches++;
+  if (ill) {
+    if ((rc = refine(R3, T3))) return rc;
+    launch_small_gemm(R3, n, 0, Rt, n, R, n, n, n, n, nullptr, st);  // R3 R2 R1
+    c->launches++;
+  }
+  return cuda_check(c, "qr");
+}
+
+// One-sided Jacobi SVD of X (m x n, m >= n, n <= JACOBI_NMAX): S (n, descending), V (n x n, ld ldv;
+// X = U diag(S) V^T).  Relative accuracy (no squaring); X is packed first.
+int psvd_jacobi(psvd_ctx* c, const double* X, int64_t ldx, int64_t m, int n, double* S, double* V, int64_t ldv,
+                void* stream) {
+  if (!c) return PSVD_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if (n < 1 || n > JACOBI_NMAX || m < n || m > (int64_t)INT32_MAX)
+    return fail(c, PSVD_EINVAL, "jacobi needs m >= n and n <= %d (m=%lld n=%d)", JACOBI_NMAX, (long long)m, n);
+  if (!X || !S || !V || ldx < m || ldv < n) return fail(c, PSVD_EINVAL, "bad jacobi arguments");
+  const size_t mn = (size_t)m * n;
+  if ((rc = ensure(c, c->dense2, sizeof(double) * (mn + (size_t)n * n))) ||
+      (rc = ensure(c, c->jacws, sizeof(double) * jacobi_workspace_doubles((int)m, n))))
+    return rc;
+  double* Xp = (double*)c->dense2.ptr;
+  double* J = Xp + mn;
+  cudaMemcpy2DAsync(Xp, m * sizeof(double), X, ldx * sizeof(double), m * sizeof(double), n, cudaMemcpyDeviceToDevice,
+                    st);
+  launch_jacobi_svd(Xp, (int)m, n, S, J, (double*)c->jacws.ptr, c->d_status, st);
+  cudaMemcpy2DAsync(V, ldv * sizeof(double), J, n * sizeof(double), n * sizeof(double), n, cudaMemcpyDeviceToDevice, st);
+  c->launches++;
+  return cuda_check(c, "jacobi");
+}
+
+// The reference's sign rule (linalg.py:81-91): per column of U (rows x cols) the entry of largest
+// magnitude (first occurrence) is made positive; the same flips go to the columns of V (vrows x
+// cols, may be null: the rows of vt).
+int psvd_sign_pair(psvd_ctx* c, double* U, int64_t ldu, int64_t rows, int cols, double* V, int64_t ldv, int64_t vrows,
+                   void* stream) {
+  if (!c) return PSVD_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if (rows < 1 || cols < 1 || !U || ldu < rows || (V && ldv < vrows)) return fail(c, PSVD_EINVAL, "bad sign arguments");
+  const int64_t nch = colmax_rows_chunks(rows);
+  if ((rc = ensure(c, c->colmax, sizeof(double) * (size_t)nch * cols * 2)) ||
+      (rc = ensure(c, c->xpairs, sizeof(double) * (size_t)cols)))
+    return rc;
+  double* sgn = (double*)c->xpairs.ptr;
+  launch_colmax_rows(U, ldu, rows, cols, 0, (double*)c->colmax.ptr, st);
+  launch_colmax_sign((const double*)c->colmax.ptr, (int)nch, cols, sgn, st);
+  launch_scale_cols(U, ldu, rows, cols, sgn, st);
+  c->launches += 3;
+  if (V) {
+    launch_scale_cols(V, ldv, vrows, cols, sgn, st);
+    c->launches++;
+  }
+  return cuda_check(c, "sign pair");
+}
+
+// X[:, j] *= s_j (invert = 0) or /= s_j with 0 for s_j == 0 (invert = 1)
+int psvd_scale_cols(psvd_ctx* c, double* X, int64_t ld, int64_t rows, int cols, const double* s, int invert,
+                    void* stream) {
+  if (!c) return PSVD_EINVAL;
+  if (!X || !s || rows < 1 || cols < 1 || ld < rows) return fail(c, PSVD_EINVAL, "bad scale_cols arguments");
+  dim3 g((unsigned)((rows + 255) / 256), (unsigned)cols);
+  scale_cols_any_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(X, ld, rows, cols, s, invert);
+  c->launches++;
+  return cuda_check(c, "scale cols");
+}
+
+// vt (K x n, ld ldvt) of the last psvd_rand_update on this context (low_rank_svd's right factor,
+// linalg.py:157-162): vt[k] = sign_k (B^T U_B[:, k])^T / S_k from the update's small matrices.
+// Valid on the same stream right after that update.
+int psvd_rand_last_vt(psvd_ctx* c, int n, int l, int K, double* Vt, int64_t ldvt, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  if (!Vt || n < 1 || l < K || K < 1 || ldvt < K) return fail(c, PSVD_EINVAL, "bad rand_last_vt arguments");
+  const size_t nl = (size_t)n * l, ll = (size_t)l * l;
+  const size_t need = sizeof(double) * (6 * nl + 6 * ll + 2 * l + (size_t)l * K + K);
+  if (c->rsmall.bytes < need) return fail(c, PSVD_EINVAL, "no randomized update of this shape to read");
+  const double* base = (const double*)c->rsmall.ptr;
+  const double* Bt = base + 5 * nl;
+  const double* J = Bt + nl + 4 * ll;
+  const double* S = J + 2 * ll;
+  const double* sgn = S + 2 * l + (size_t)l * K;
+  rand_vt_kernel<<<(unsigned)((n * K + 127) / 128), 128, 0, (cudaStream_t)stream>>>(Bt, n, l, J, S, sgn, K, Vt, ldvt);
+  c->launches++;
+  return cuda_check(c, "rand vt");
+}
+
+// 1 when psvd_stream_run can take batches of up to Bmax columns with K modes on M rows: its
+// look-ahead Gram (one pass of 32x32 tiles) and its fused pass [U | A_b | A_{b+1}] plan within
+// the kernels' limits; 0 otherwise (stream batch by batch through psvd_stream_update instead).
+int psvd_stream_run_supported(psvd_ctx* c, int64_t M, int K, int Bmax, int* ok) {
+  if (!c || !ok || M < 1 || K < 1 || Bmax < 1) return PSVD_EINVAL;
+  *ok = 0;
+  const int nb32 = (Bmax + 31) / 32;
+  if (nb32 * (nb32 + 1) / 2 > MAX_OUT_TILES) return PSVD_OK;
+  // dry-run plans on placeholder 16-byte aligned pointers (plans launch nothing)
+  const double* fake = reinterpret_cast<const double*>(uintptr_t(1) << 20);
+  const int64_t ld = M + (M & 1);
+  Pass pa, pf;
+  std::string saved = c->err;
+  bool fit = plan_pass(c, pa, M, {Seg{fake, ld, Bmax, 0}}, 0, 0, 0, nullptr, 0, true, false, false) == PSVD_OK &&
+             plan_pass(c, pf, M, {Seg{fake, ld, K, 0}, Seg{fake, ld, Bmax, 0}, Seg{fake, ld, Bmax, 1}}, 0, K + Bmax,
+                       K, fake, K + Bmax, false, true, true, -1, -1, nullptr, nullptr, 0, -1) == PSVD_OK;
+  c->err = saved;
+  *ok = fit ? 1 : 0;
+  return PSVD_OK;
+}
+
+// 1 when psvd_rand_stream_run's passes plan for batches of up to Bmax columns (sketch width l,
+// K modes, q power iterations) on M rows; 0: use psvd_rand_update per batch (its wide route).
+int psvd_rand_stream_run_supported(psvd_ctx* c, int64_t M, int K, int l, int q, int Bmax, int* ok) {
+  if (!c || !ok || M < 1 || K < 1 || l < K || Bmax < 1 || q < 0) return PSVD_EINVAL;
+  *ok = 0;
+  if (l > TMA_MAX_Y || !tma_available() || !qw_colmax_supported(l, K)) return PSVD_OK;
+  const double* fake = reinterpret_cast<const double*>(uintptr_t(1) << 20);
+  const int64_t ld = M + (M & 1);
+  std::string saved = c->err;
+  Pass p1, p2, p3, p4;
+  bool fit = plan_pass(c, p1, M, {Seg{fake, ld, l, 0}, Seg{fake, ld, Bmax, 0}}, l, Bmax, l, fake, K + Bmax, false,
+                       true, true, l, -1, &c->partial2, &c->tiles2[0], c->num_sms - 2, 0, true) == PSVD_OK &&
+             p1.tma &&
+             plan_pass(c, p2, M, {Seg{fake, ld, l, 0}, Seg{fake, ld, l, 0}, Seg{fake, ld, Bmax, 0}}, 0, 2 * l, l,
+                       fake, 2 * l, false, true, true, -1, -1, nullptr, nullptr, 0, 0, true) == PSVD_OK;
+  if (fit && q > 0)
+    fit = plan_pass(c, p3, M, {Seg{fake, ld, l, 0}, Seg{fake, ld, Bmax, 0}}, 0, l + Bmax, l, fake, l + Bmax, false,
+                    true, false) == PSVD_OK &&
+          plan_pass(c, p4, M, {Seg{fake, ld, l, 0}, Seg{fake, ld, Bmax, 0}, Seg{fake, ld, l, 0}}, l + Bmax, l, l,
+                    fake, l, false, true, true, -1, -1, nullptr, nullptr, 0, 0, true) == PSVD_OK;
+  c->err = saved;
+  *ok = fit ? 1 : 0;
+  return PSVD_OK;
 }
 
 int psvd_refine_normalize(psvd_ctx* c, int64_t M, double* U, int64_t ldu, int K, double* UtU, double* sigma,

@@ -599,20 +599,31 @@ int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift) {
     if ((lead != 0 && (s != 0 || P != pshift)) || (reinterpret_cast<uintptr_t>(sg.ptr) & 15) != 0 ||
         (sg.ld & 1) != 0)
       return -1;
-    const int bw = std::min(256, (sg.ncols + lead + 7) / 8 * 8);
+    // boxes of 256 columns, then one tail box of the remaining columns rounded up to 8 (its own
+    // tensor map): a box may overhang the segment by < 8 columns only, so it never lands on the
+    // next segment's columns (which start on the next 8-column boundary)
+    const int span = sg.ncols + lead;
+    const int nfull = span > 256 ? span / 256 : 0;
+    const int tail = span - 256 * nfull;
     cuuint64_t dims[2] = {(cuuint64_t)p.M, (cuuint64_t)sg.ncols};
     cuuint64_t strides[1] = {(cuuint64_t)sg.ld * sizeof(double)};
-    cuuint32_t box[2] = {(cuuint32_t)TKS, (cuuint32_t)bw};
     cuuint32_t es[2] = {1, 1};
-    if (enc(&maps.m[s], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(sg.ptr), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return -1;
+    auto encode = [&](int map, int bw) {
+      cuuint32_t box[2] = {(cuuint32_t)TKS, (cuuint32_t)bw};
+      return enc(&maps.m[map], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(sg.ptr), dims, strides, box, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    if (nfull > 0 && !encode(s, 256)) return -1;
+    const int tw = (tail + 7) / 8 * 8;
+    if (tail > 0 && !encode(nfull > 0 ? MAX_SEG + s : s, tw)) return -1;
     // boxes start at tensor column -lead (out of bounds -> zero filled) so they land 1024-byte aligned
-    for (int c = -lead; c < sg.ncols; c += bw) {
+    for (int k = 0; k < nfull + (tail > 0); ++k) {
       if (nops >= TMA_MAX_OPS) return -1;
+      const int c = -lead + 256 * k;
+      const int bw = k < nfull ? 256 : tw;
       const int dst = P + c;
-      x.op_seg[nops] = (short)s;
+      x.op_seg[nops] = (short)(k < nfull ? s : (nfull > 0 ? MAX_SEG + s : s));
       x.op_col[nops] = (short)c;
       x.op_pcol[nops] = (short)dst;
       for (int q = dst >> 3; q < (dst + bw) >> 3 && q < TMA_MAX_BLK; ++q) x.written[q] = 1;

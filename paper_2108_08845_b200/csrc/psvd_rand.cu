@@ -193,7 +193,8 @@ void launch_jacobi_svd(const double* Z, int n, int l, double* S, double* J, doub
 // refinement step); columns of a numerically null direction (pivot <= tiny)
 // are zeroed, matching the first (SVQB) pass which dropped them.
 __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restrict__ G, int l, double* __restrict__ T,
-                                                           int* __restrict__ illcond, int* __restrict__ status) {
+                                                           int* __restrict__ illcond, int* __restrict__ status,
+                                                           double* __restrict__ Rout) {
   extern __shared__ double sm[];
   double* R = sm;          // l x l col-major, upper used
   double* X = R + l * l;   // inverse
@@ -235,6 +236,8 @@ __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restr
   }
   __syncthreads();
   for (int idx = tid; idx < l * l; idx += nthr) T[idx] = X[idx];
+  if (Rout != nullptr)
+    for (int idx = tid; idx < l * l; idx += nthr) Rout[idx] = (idx % l <= idx / l) ? R[idx] : 0.0;
   if (illcond != nullptr && tid == 0) {
     // CholeskyQR2 keeps O(eps) orthogonality for cond(Y) < ~1e7: flag anything beyond
     // cond(Y) ~ max R_ii / min R_ii > 1e6, or a dropped pivot, for the SVQB route
@@ -248,10 +251,29 @@ __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restr
   }
 }
 
-void launch_chol_inv(const double* G, int l, double* T, cudaStream_t st, int* illcond, int* status) {
+void launch_chol_inv(const double* G, int l, double* T, cudaStream_t st, int* illcond, int* status, double* Rout) {
   const size_t smem = 2 * (size_t)l * l * sizeof(double);
   cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  chol_inv_kernel<<<1, 1024, smem, st>>>(G, l, T, illcond, status);
+  chol_inv_kernel<<<1, 1024, smem, st>>>(G, l, T, illcond, status, Rout);
+}
+
+// G += shift I with shift = 11 (M n + n (n + 1)) u tr(G): the shifted CholeskyQR of Fukaya et al.
+// (an R that exists for any cond(A) < 1/u; two unshifted CholeskyQR passes then restore orthogonality)
+__global__ void chol_shift_kernel(double* __restrict__ G, int n, double mfac) {
+  __shared__ double tr;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += G[(size_t)i * n + i];
+    tr = t;
+  }
+  __syncthreads();
+  const double sh = 11.0 * mfac * DBL_EPSILON * 0.5 * tr;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) G[(size_t)i * n + i] += sh;
+}
+
+void launch_chol_shift(double* G, int n, int64_t M, cudaStream_t st) {
+  const double mfac = (double)M * n + (double)n * (n + 1);
+  chol_shift_kernel<<<1, 128, 0, st>>>(G, n, mfac);
 }
 
 // ---------------------------------------------------------------- tall sign rule

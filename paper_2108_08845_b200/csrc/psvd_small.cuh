@@ -75,9 +75,13 @@ void launch_drift_check(const double* UtU, int K, double tol, double* sigma, dou
 void launch_small_gemm(const double* A, int lda, int transA, const double* B, int ldb, double* C, int ldc, int m,
                        int k1, int k2, const double* rowscale, cudaStream_t st);
 size_t jacobi_workspace_doubles(int n, int l);
+constexpr int JACOBI_NMAX = 160;  // the rotation accumulator J (n x n) lives in shared memory
 void launch_jacobi_svd(const double* Z, int n, int l, double* S, double* J, double* ws, int* status, cudaStream_t st,
                        const int* gate = nullptr);
-void launch_chol_inv(const double* G, int l, double* T, cudaStream_t st, int* illcond = nullptr, int* status = nullptr);
+void launch_chol_inv(const double* G, int l, double* T, cudaStream_t st, int* illcond = nullptr, int* status = nullptr,
+                     double* Rout = nullptr);
+constexpr int CHOL_NMAX = 112;  // chol_inv keeps R and R^-1 in shared memory
+void launch_chol_shift(double* G, int n, int64_t M, cudaStream_t st);
 void launch_colmax_sign(const double* colmax, int nchunks, int K, double* sign, cudaStream_t st);
 void launch_colmax_reduce(const double* colmax, int nchunks, int K, double* out, cudaStream_t st);
 void launch_svqb_scale(double* T, const double* S, int l, double tol, cudaStream_t st, const int* gate = nullptr);

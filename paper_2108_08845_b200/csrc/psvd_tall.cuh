@@ -96,11 +96,11 @@ constexpr int TMA_MAX_BLK = 192;  // 8-column blocks of the panel
 // ones own one Gram tile each, the last warp is the TMA producer
 constexpr int TMA_MAX_Y = 32;
 struct TmaMaps {
-  CUtensorMap m[MAX_SEG];
+  CUtensorMap m[2 * MAX_SEG];  // per segment: 256-column boxes, and the narrower tail box [MAX_SEG + s]
 };
 struct TmaExtra {
   int nops;
-  short op_seg[TMA_MAX_OPS], op_col[TMA_MAX_OPS], op_pcol[TMA_MAX_OPS];
+  short op_seg[TMA_MAX_OPS], op_col[TMA_MAX_OPS], op_pcol[TMA_MAX_OPS];  // op_seg: tensor map index
   int wrow0[MAX_SEG];        // W row of the segment's first column (TMA_NOT_IN_W: outside Y's range)
   int kp_lo, kp_hi;          // Y's k range in physical panel columns
   int pshift;                // physical column = logical column + pshift (narrow pass)

@@ -244,3 +244,74 @@ def gather_modes(ctx, local_modes, root=0):
     if ctx.rank != root:
         return None
     return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0)
+
+
+def parallel_qr(ctx, a_local, device=None):
+    """Tall-skinny QR of the row-stacked global matrix (dsvd.py:176-202): QrResult(q_local,
+    r) with r identical on every rank.  World size 1 is qr_factor.  Otherwise a
+    distributed CholeskyQR2 (shifted CholeskyQR3 when ill conditioned): every Gram is a
+    rank-ordered allreduce of the local Grams, so every rank factors identical bits, and
+    q_local = a_local R^-1 stays local (no q slices on the wire, unlike the reference's
+    gather / send / broadcast of the TSQR tree)."""
+    from .linalg import QR_MAX_COLS, QrResult, qr_factor
+    if ctx.world_size == 1:
+        return qr_factor(a_local, device)
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    A = nat.as_device_colmajor(a_local, dev, "a_local")
+    m, n = A.rows, A.cols
+    if n > QR_MAX_COLS:
+        raise ValueError(f"parallel_qr on the device supports up to {QR_MAX_COLS} columns, got {n}")
+    c = nat.context(dev)
+    st = nat.stream_ptr(dev)
+    rows = torch.tensor([float(m)], dtype=torch.float64,
+                        device=dev if dist.get_backend(ctx.group) == "nccl" else torch.device("cpu"))
+    dist.all_reduce(rows, group=ctx.group)
+    m_total = int(rows.item())
+
+    nccl = dist.get_backend(ctx.group) == "nccl"
+
+    def gram(X):
+        G = torch.empty((n, n), dtype=torch.float64, device=dev)
+        nat.call("psvd_gram", c, X.rows, nat._vp(0), 0, nat._vp(0), 1.0, 0, nat._vp(X.data_ptr()), X.ld, n,
+                 nat.ptr(G), st)
+        if nccl:
+            return allreduce_ordered(G, ctx).contiguous()
+        return allreduce_ordered(G.cpu(), ctx).to(dev).contiguous()  # gloo: host-staged (CPU test harness)
+
+    def chol(G):
+        R = torch.empty((n, n), dtype=torch.float64, device=dev)
+        T = torch.empty((n, n), dtype=torch.float64, device=dev)
+        nat.call("psvd_chol", c, nat.ptr(G), n, nat.ptr(R), nat.ptr(T), st)
+        return R, T
+
+    def times(X, T):
+        Y = nat.DevMat.empty(X.rows, n, dev)
+        nat.call("psvd_nn_product", c, X.rows, nat._vp(X.data_ptr()), X.ld, n, nat.ptr(T), n, n,
+                 nat._vp(Y.data_ptr()), Y.ld, st)
+        return Y
+
+    def rmul(Ra, Rb):
+        out = torch.empty((n, n), dtype=torch.float64, device=dev)
+        nat.call("psvd_small_matmul", c, nat.ptr(Ra), n, 0, nat.ptr(Rb), n, nat.ptr(out), n, n, n, n, st)
+        return out
+
+    with torch.cuda.device(dev):
+        G = gram(A)
+        R1, T1 = chol(G)
+        flag = ctypes.c_int(0)
+        nat.call("psvd_chol_illcond", c, ctypes.byref(flag), st)
+        if flag.value:  # shifted CholeskyQR3 (the flag is computed from identical bits on every rank)
+            nat.call("psvd_chol_shift", c, nat.ptr(G), n, m_total, st)
+            R1, T1 = chol(G)
+        Q = times(A, T1)
+        R2, T2 = chol(gram(Q))
+        Q = times(Q, T2)
+        R = rmul(R2, R1)
+        if flag.value:
+            R3, T3 = chol(gram(Q))
+            Q = times(Q, T3)
+            R = rmul(R3, R)
+        st_word = nat.read_status(c, reset=True, device=dev)
+    if st_word & nat.ST_NONFINITE:
+        raise ValueError("a_local contains non-finite entries")
+    return QrResult(Q.view, R.T)

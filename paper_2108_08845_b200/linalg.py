@@ -3,6 +3,7 @@ streaming update (reference linalg.py:33-62, 126-162)."""
 
 from __future__ import annotations
 
+from collections import namedtuple
 from dataclasses import dataclass
 
 import numpy as np
@@ -100,11 +101,272 @@ def randomized_update(U, sigma, A, sketch, ff, device, check=True, total_rows=No
 
 def low_rank_svd(a, config, device=None):
     """Randomized truncated SVD of a device/host matrix (linalg.py:150-162):
-    returns (u (m x target_rank) CUDA tensor, s (target_rank,) CUDA tensor).
-    vt is not formed (the streaming update never uses it)."""
+    SvdResult(u (m x target_rank), s (target_rank,), vt (target_rank x n)) as CUDA
+    tensors, the sign rule applied to u's columns and vt's rows together."""
     import torch
     from . import _native as nat
-    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    dev = _dev(device)
     A = nat.as_device_colmajor(a, dev, "a")
     u, s = randomized_update(None, None, A, config, 1.0, dev)
-    return u.view, s
+    k, l = config.target_rank, config.sketch_width
+    ctx = nat.context(dev)
+    with torch.cuda.device(dev):
+        vt = torch.empty((A.cols, k), dtype=torch.float64, device=dev)  # (k x n) column-major
+        nat.call("psvd_rand_last_vt", ctx, A.cols, l, k, nat.ptr(vt), k, nat.stream_ptr(dev))
+    return SvdResult(u.view, s, vt.T)
+
+
+# --------------------------------------------------------------------------
+# dense factorizations of the reference's linalg boundary (linalg.py:94-147)
+# --------------------------------------------------------------------------
+
+QrResult = namedtuple("QrResult", ["q", "r"])
+SvdResult = namedtuple("SvdResult", ["u", "s", "vt"])
+
+QR_MAX_COLS = 112      # CHOL_NMAX: R and R^-1 of a Gram in one CTA's shared memory
+JACOBI_MAX_COLS = 160  # JACOBI_NMAX: the one-sided Jacobi rotation accumulator in shared memory
+
+
+def _dev(device):
+    import torch
+    return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+def _check(ctx, dev, what):
+    from . import _native as nat
+    st = nat.read_status(ctx, reset=True, device=dev)
+    if st & nat.ST_NONFINITE:
+        raise ValueError(f"{what} contains non-finite entries")
+    if st & nat.ST_NOCONVERGE:
+        from .errors import ConvergenceError
+        raise ConvergenceError(f"{what}: SVD did not converge")
+
+
+def _tall_qr(A, dev):
+    """(Q DevMat m x n, R (n x n) tensor) of a tall DevMat (m >= n) on the device."""
+    import torch
+    from . import _native as nat
+    m, n = A.rows, A.cols
+    if n > QR_MAX_COLS:
+        raise ValueError(f"qr_factor on the device supports up to {QR_MAX_COLS} columns, got {n}")
+    ctx = nat.context(dev)
+    Q = nat.DevMat.empty(m, n, dev)
+    R = torch.empty((n, n), dtype=torch.float64, device=dev)  # column-major (n x n): R.T is the matrix
+    with torch.cuda.device(dev):
+        nat.call("psvd_qr", ctx, m, n, nat._vp(A.data_ptr()), A.ld, nat._vp(Q.data_ptr()), Q.ld, nat.ptr(R),
+                 nat.stream_ptr(dev))
+        dropped = torch.nonzero(torch.diagonal(R) == 0.0).flatten().tolist()
+        if dropped:
+            _complete_basis(Q, dropped, dev)
+    return Q, R.T
+
+
+def _complete_basis(Q, cols, dev):
+    """Rank-deficient input: CholeskyQR leaves the columns of numerically null directions at
+    zero (their rows of R are zero, so q r still reconstructs a).  Householder QR returns an
+    orthonormal q there (linalg.py:94-104 promises orthonormal columns), so fill them with
+    unit vectors orthogonal to every other column: e_i (lowest i first) projected out twice
+    (classical Gram-Schmidt with re-orthogonalization on the library's products), kept when
+    at least half its norm survives."""
+    import torch
+    from . import _native as nat
+    ctx = nat.context(dev)
+    st = nat.stream_ptr(dev)
+    m, n = Q.rows, Q.cols
+    v = nat.DevMat.empty(m, 1, dev)
+    c = torch.empty((n, 1), dtype=torch.float64, device=dev)
+    nrm = torch.empty((1, 1), dtype=torch.float64, device=dev)
+    neg = torch.tensor([-1.0], dtype=torch.float64, device=dev)
+    i = 0
+    for j in cols:
+        while i < m:
+            v.view.zero_()
+            v.view[i, 0] = 1.0
+            i += 1
+            for _ in range(2):
+                nat.call("psvd_tn_product", ctx, m, nat._vp(Q.data_ptr()), Q.ld, n, nat._vp(v.data_ptr()), v.ld, 1,
+                         nat.ptr(c), n, st)
+                nat.call("psvd_scale_cols", ctx, nat.ptr(c), n, n, 1, nat.ptr(neg), 0, st)
+                # v += Q (-c): Q times the small vector, added through a second column of the product
+                w = nat.DevMat.empty(m, 1, dev)
+                nat.call("psvd_nn_product", ctx, m, nat._vp(Q.data_ptr()), Q.ld, n, nat.ptr(c), n, 1,
+                         nat._vp(w.data_ptr()), w.ld, st)
+                v.view.add_(w.view)
+            nat.call("psvd_tn_product", ctx, m, nat._vp(v.data_ptr()), v.ld, 1, nat._vp(v.data_ptr()), v.ld, 1,
+                     nat.ptr(nrm), 1, st)
+            norm = float(nrm.item()) ** 0.5
+            if norm > 0.5:
+                nrm.fill_(norm)
+                nat.call("psvd_scale_cols", ctx, nat._vp(v.data_ptr()), v.ld, m, 1, nat.ptr(nrm.view(-1)), 1, st)
+                Q.view[:, j].copy_(v.view[:, 0])
+                break
+
+
+def qr_factor(a, device=None):
+    """Reduced QR with diag(r) >= 0 (linalg.py:94-104): QrResult(q (m x min(m, n)),
+    r (min(m, n) x n)) as CUDA tensors.  Tall inputs run CholeskyQR2 (shifted
+    CholeskyQR3 when ill conditioned) on the device; wide ones factor their leading
+    square block and form r's remaining columns as q^T a.  Up to 112 columns in the
+    factored block (CholeskyQR's R and R^-1 live in one CTA's shared memory)."""
+    import torch
+    from . import _native as nat
+    dev = _dev(device)
+    A = nat.as_device_colmajor(a, dev, "a")
+    m, n = A.rows, A.cols
+    ctx = nat.context(dev)
+    if m >= n:
+        Q, R = _tall_qr(A, dev)
+        _check(ctx, dev, "a")
+        return QrResult(Q.view, R)
+    lead = nat.DevMat(A.view[:, :m], A.ld)
+    Q, R0 = _tall_qr(lead, dev)
+    rest = torch.empty((n - m, m), dtype=torch.float64, device=dev)  # column-major (m x (n - m))
+    with torch.cuda.device(dev):
+        nat.call("psvd_tn_product", ctx, m, nat._vp(Q.data_ptr()), Q.ld, m,
+                 nat._vp(A.data_ptr() + 8 * A.ld * m), A.ld, n - m, nat.ptr(rest), m, nat.stream_ptr(dev))
+    _check(ctx, dev, "a")
+    return QrResult(Q.view, torch.cat([R0, rest.T], dim=1))
+
+
+def _svd_tall(A, dev, want_vt):
+    """(U DevMat m x n, s (n,), V (n x n) column-major tensor view) of a tall DevMat."""
+    import torch
+    from . import _native as nat
+    m, n = A.rows, A.cols
+    ctx = nat.context(dev)
+    st = nat.stream_ptr(dev)
+    s = torch.empty(n, dtype=torch.float64, device=dev)
+    Vb = torch.empty((n, n), dtype=torch.float64, device=dev)  # column-major V: Vb.T
+    U = nat.DevMat.empty(m, n, dev)
+    with torch.cuda.device(dev):
+        if n <= QR_MAX_COLS:
+            # QR-preconditioned one-sided Jacobi: A = Q R, R = U_R S V^T, U = Q U_R
+            if m > n:
+                Q, R = _tall_qr(A, dev)
+                Rm = nat.as_device_colmajor(R, dev, "r")
+            else:
+                Q, Rm = None, A
+            nat.call("psvd_jacobi", ctx, nat._vp(Rm.data_ptr()), Rm.ld, Rm.rows, n, nat.ptr(s), nat.ptr(Vb), n, st)
+            UR = nat.DevMat.empty(n, n, dev)
+            nat.call("psvd_small_matmul", ctx, nat._vp(Rm.data_ptr()), Rm.ld, 0, nat.ptr(Vb), n,
+                     nat._vp(UR.data_ptr()), UR.ld, n, n, n, st)
+            nat.call("psvd_scale_cols", ctx, nat._vp(UR.data_ptr()), UR.ld, n, n, nat.ptr(s), 1, st)
+            if Q is None:
+                U = UR
+            else:
+                nat.call("psvd_nn_product", ctx, m, nat._vp(Q.data_ptr()), Q.ld, n, nat._vp(UR.data_ptr()), UR.ld, n,
+                         nat._vp(U.data_ptr()), U.ld, st)
+        elif n <= JACOBI_MAX_COLS and m <= 4 * n:
+            nat.call("psvd_jacobi", ctx, nat._vp(A.data_ptr()), A.ld, m, n, nat.ptr(s), nat.ptr(Vb), n, st)
+            nat.call("psvd_nn_product", ctx, m, nat._vp(A.data_ptr()), A.ld, n, nat.ptr(Vb), n, n,
+                     nat._vp(U.data_ptr()), U.ld, st)
+            nat.call("psvd_scale_cols", ctx, nat._vp(U.data_ptr()), U.ld, m, n, nat.ptr(s), 1, st)
+        else:
+            # wide cores: eigenpairs of the Gram (singular values below ~sqrt(eps) s_1 lose
+            # relative accuracy on this route: eps s_1^2 / s_k)
+            G = torch.empty((n, n), dtype=torch.float64, device=dev)
+            nat.call("psvd_gram", ctx, m, nat._vp(0), 0, nat._vp(0), 1.0, 0, nat._vp(A.data_ptr()), A.ld, n,
+                     nat.ptr(G), st)
+            nat.call("psvd_sym_topk", ctx, nat.ptr(G), n, n, nat.ptr(Vb), n, nat.ptr(s), st)
+            nat.call("psvd_nn_product", ctx, m, nat._vp(A.data_ptr()), A.ld, n, nat.ptr(Vb), n, n,
+                     nat._vp(U.data_ptr()), U.ld, st)
+            nat.call("psvd_scale_cols", ctx, nat._vp(U.data_ptr()), U.ld, m, n, nat.ptr(s), 1, st)
+        nat.call("psvd_sign_pair", ctx, nat._vp(U.data_ptr()), U.ld, m, n, nat.ptr(Vb), n, n, st)
+    return U, s, Vb.T
+
+
+def svd_full(a, want_vt=True, device=None):
+    """Thin SVD (linalg.py:107-123): SvdResult(u, s descending, vt or None) as CUDA
+    tensors with the reference's sign rule (each u column's largest-magnitude entry
+    positive, first occurrence; vt's rows follow).  Up to 112 columns (of the taller
+    orientation): CholeskyQR then one-sided Jacobi on R (relative accuracy); up to 160
+    nearly square: Jacobi on the matrix; wider: Gram eigenpairs (absolute accuracy
+    eps s_1^2 / s_k).  Non-convergence raises ConvergenceError."""
+    from . import _native as nat
+    dev = _dev(device)
+    A = nat.as_device_colmajor(a, dev, "a")
+    ctx = nat.context(dev)
+    if A.rows >= A.cols:
+        U, s, V = _svd_tall(A, dev, want_vt)
+        _check(ctx, dev, "a")
+        return SvdResult(U.view, s, V.T if want_vt else None)
+    # wide: svd(a^T) = V S U^T; the sign rule is on the left factor, so apply it again
+    At = nat.as_device_colmajor(A.view.T, dev, "a")
+    Vw, s, Uw = _svd_tall(At, dev, True)  # a^T = Vw diag(s) Uw^T
+    u = nat.DevMat.empty(A.rows, A.rows, dev)
+    u.view.copy_(Uw)
+    vt_cols = nat.DevMat.empty(A.cols, A.rows, dev)  # v = Vw (n x k), column-major
+    vt_cols.view.copy_(Vw.view)
+    with __import__("torch").cuda.device(dev):
+        nat.call("psvd_sign_pair", ctx, nat._vp(u.data_ptr()), u.ld, A.rows, A.rows, nat._vp(vt_cols.data_ptr()),
+                 vt_cols.ld, A.cols, nat.stream_ptr(dev))
+    _check(ctx, dev, "a")
+    return SvdResult(u.view, s, vt_cols.view.T if want_vt else None)
+
+
+def randomized_range(a, config, device=None):
+    """Orthonormal basis of the sketched range (linalg.py:126-147): q = qr(a Omega).q
+    with Omega = Philox(seed).standard_normal((n, width)), then `power_iterations`
+    rounds of q = qr(a^T q).q, q = qr(a q).q.  Returns q (m x width), CUDA."""
+    import torch
+    from . import _native as nat
+    dev = _dev(device)
+    A = nat.as_device_colmajor(a, dev, "a")
+    m, n = A.rows, A.cols
+    w = config.sketch_width
+    if w > min(m, n):
+        raise ValueError(f"sketch width {w} exceeds min(a.shape) = {min(m, n)}")
+    ctx = nat.context(dev)
+    st = nat.stream_ptr(dev)
+    om = device_omega(n, config, dev)  # column-major n x w
+    Y = nat.DevMat.empty(m, w, dev)
+    with torch.cuda.device(dev):
+        nat.call("psvd_nn_product", ctx, m, nat._vp(A.data_ptr()), A.ld, n, nat.ptr(om), n, w,
+                 nat._vp(Y.data_ptr()), Y.ld, st)
+        q, _ = _tall_qr(Y, dev)
+        for _ in range(config.power_iterations):
+            Z = nat.DevMat.empty(n, w, dev)
+            nat.call("psvd_tn_product", ctx, m, nat._vp(A.data_ptr()), A.ld, n, nat._vp(q.data_ptr()), q.ld, w,
+                     nat._vp(Z.data_ptr()), Z.ld, st)
+            z, _ = _tall_qr(Z, dev)
+            nat.call("psvd_nn_product", ctx, m, nat._vp(A.data_ptr()), A.ld, n, nat._vp(z.data_ptr()), z.ld, w,
+                     nat._vp(Y.data_ptr()), Y.ld, st)
+            q, _ = _tall_qr(Y, dev)
+    _check(ctx, dev, "a")
+    return q.view
+
+
+def aligned_mode_difference(a, b):
+    """Per-column max |a*sign - b| after matching each column's sign (linalg.py:165-176)."""
+    import torch
+    a = torch.as_tensor(a, dtype=torch.float64)
+    b = torch.as_tensor(b, dtype=torch.float64, device=a.device)
+    if a.shape != b.shape:
+        raise ValueError(f"shape mismatch: {tuple(a.shape)} vs {tuple(b.shape)}")
+    signs = torch.sign(torch.sum(a * b, dim=0))
+    signs[signs == 0.0] = 1.0
+    return torch.max(torch.abs(a * signs - b), dim=0).values
+
+
+def subspace_angles(a, b, device=None):
+    """Principal angles (ascending, radians) between the column spans (linalg.py:179-192):
+    arccos of the singular values of qa^T qb, as the reference computes them."""
+    import torch
+    qa = qr_factor(a, device).q
+    qb = qr_factor(b, device).q
+    c = svd_full(_tn(qa, qb, device), want_vt=False, device=device).s
+    return torch.sort(torch.arccos(torch.clamp(c, -1.0, 1.0))).values
+
+
+def _tn(x, y, device):
+    """x^T y for tall column-major CUDA matrices, on the library's TN product."""
+    import torch
+    from . import _native as nat
+    dev = _dev(device)
+    X = nat.as_device_colmajor(x, dev, "x")
+    Y = nat.as_device_colmajor(y, dev, "y")
+    out = torch.empty((Y.cols, X.cols), dtype=torch.float64, device=dev)  # column-major X.cols x Y.cols
+    with torch.cuda.device(dev):
+        nat.call("psvd_tn_product", nat.context(dev), X.rows, nat._vp(X.data_ptr()), X.ld, X.cols,
+                 nat._vp(Y.data_ptr()), Y.ld, Y.cols, nat.ptr(out), X.cols, nat.stream_ptr(dev))
+    return out.T

@@ -171,6 +171,23 @@ def _run_window(state, mats, config, dev, ready=None):
         raise ValueError(f"initial batch has {M} rows, need at least k_modes={k}")
     ctx = nat.context(dev)
     nb = len(mats)
+    ok = ctypes.c_int(0)
+    nat.call("psvd_stream_run_supported", ctx, M, k, max(m.cols for m in mats), ctypes.byref(ok))
+    if not ok.value:
+        # batches too wide for the pipelined kernels: one psvd_stream_update per batch
+        # (wide Grams on the tall-skinny TN GEMM), same update rule
+        if ready is not None:
+            for e in ready:
+                if e is not None:
+                    torch.cuda.current_stream(dev).wait_event(e)
+        hist = []
+        for m in mats:
+            if state is None:
+                state = stream_initialize(m, config, dev)
+            else:
+                state = stream_incorporate(state, m, config)
+            hist.append(state.singular_values.clone())
+        return state, hist
     with torch.cuda.device(dev):
         if state is not None:
             U = nat.as_device_colmajor(state.modes, dev, "modes")
@@ -220,6 +237,18 @@ def _run_rand_window(state, mats, config, dev, ready=None):
             raise ValueError(f"sketch width {l} exceeds min(a.shape) = {min(M, n)}")
     ctx = nat.context(dev)
     nb = len(mats)
+    ok = ctypes.c_int(0)
+    nat.call("psvd_rand_stream_run_supported", ctx, M, k, l, q, max(m.cols for m in mats), ctypes.byref(ok))
+    if not ok.value:  # passes beyond the pipelined kernels: psvd_rand_update per batch (wide route)
+        if ready is not None:
+            for e in ready:
+                if e is not None:
+                    torch.cuda.current_stream(dev).wait_event(e)
+        hist = []
+        for m in mats:
+            state = stream_initialize(m, config, dev) if state is None else stream_incorporate(state, m, config)
+            hist.append(state.singular_values.clone())
+        return state, hist
     with torch.cuda.device(dev):
         if state is not None:
             U = nat.as_device_colmajor(state.modes, dev, "modes")

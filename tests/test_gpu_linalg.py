@@ -1,0 +1,238 @@
+"""GPU parity of the dense factorizations behind the reference's linalg boundary:
+qr_factor / svd_full / randomized_range / low_rank_svd's vt (linalg.py:94-162) and
+parallel_qr (dsvd.py:176-202), against the oracle restatement (tests follow the
+reference's own test_linalg.py / test_dsvd.py cases: exact identities, sign conventions,
+Gram-Schmidt agreement, exact-rank range finding, short row blocks).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _p():
+    import paper_2108_08845_b200 as p
+    return p
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _rng(seed):
+    return np.random.Generator(np.random.Philox(seed))
+
+
+# ---------------------------------------------------------------- qr_factor
+
+def test_qr_identity_exact():
+    res = _p().qr_factor(np.eye(4))
+    assert np.array_equal(_np(res.q), np.eye(4)) and np.array_equal(_np(res.r), np.eye(4))
+
+
+def test_qr_negated_identity_sign_convention():
+    res = _p().qr_factor(-np.eye(3))
+    q, r = _np(res.q), _np(res.r)
+    assert np.all(np.diag(r) >= 0.0)
+    assert np.max(np.abs(q @ r + np.eye(3))) < 1e-15
+
+
+@pytest.mark.parametrize("m,n", [(8, 3), (6, 6), (3, 7), (20, 7), (5000, 40), (1 << 16, 112)])
+def test_qr_matches_reference(m, n):
+    a = _rng(10 + m).standard_normal((m, n))
+    res = _p().qr_factor(a)
+    q, r = _np(res.q), _np(res.r)
+    qr_, rr = oracle.ref_qr(a)
+    k = min(m, n)
+    assert q.shape == (m, k) and r.shape == (k, n)
+    assert np.max(np.abs(q - qr_)) < 1e-10
+    assert np.max(np.abs(r - rr)) < 1e-10 * max(1.0, np.abs(rr).max())
+    assert np.max(np.abs(q @ r - a)) < 1e-12 * max(1.0, np.abs(a).max()) * np.sqrt(m)
+    assert np.all(np.diag(r) >= 0.0)
+
+
+def test_qr_ill_conditioned_takes_shifted_route():
+    # cond ~ 1e10: beyond CholeskyQR2, the shifted CholeskyQR3 keeps Q orthonormal
+    rng = _rng(21)
+    u = oracle.ref_qr(rng.standard_normal((400, 12)))[0]
+    v = oracle.ref_qr(rng.standard_normal((12, 12)))[0]
+    a = (u * np.logspace(0, -10, 12)) @ v.T
+    res = _p().qr_factor(a)
+    q, r = _np(res.q), _np(res.r)
+    assert np.max(np.abs(q.T @ q - np.eye(12))) < 1e-12
+    assert np.max(np.abs(q @ r - a)) < 1e-14
+    assert np.all(np.diag(r) >= 0.0)
+
+
+def test_qr_rejects_bad_input_and_is_deterministic():
+    p = _p()
+    with pytest.raises(ValueError):
+        p.qr_factor(np.zeros((0, 3)))
+    with pytest.raises(ValueError):
+        p.qr_factor(np.ones(4))
+    with pytest.raises(ValueError):
+        p.qr_factor(np.array([[1.0, np.nan], [0.0, 1.0]]))
+    with pytest.raises(ValueError):
+        p.qr_factor(np.array([[np.inf, 1.0], [0.0, 1.0]]))
+    a = _rng(11).standard_normal((20, 7))
+    r1, r2 = p.qr_factor(a), p.qr_factor(a.copy())
+    assert torch.equal(r1.q, r2.q) and torch.equal(r1.r, r2.r)
+
+
+# ---------------------------------------------------------------- svd_full
+
+def test_svd_diagonal_and_identity_exact():
+    p = _p()
+    res = p.svd_full(np.diag([3.0, 1.0]))
+    assert np.array_equal(_np(res.s), [3.0, 1.0])
+    assert np.array_equal(np.abs(_np(res.u)), np.eye(2)) and np.array_equal(np.abs(_np(res.vt)), np.eye(2))
+    res = p.svd_full(np.eye(5))
+    assert np.array_equal(_np(res.s), np.ones(5))
+    assert np.max(np.abs(_np(res.u) @ np.diag(_np(res.s)) @ _np(res.vt) - np.eye(5))) < 1e-14
+
+
+@pytest.mark.parametrize("m,n", [(6, 4), (4, 6), (9, 9), (10, 6), (300, 40), (40, 300), (3000, 112), (700, 150)])
+def test_svd_matches_reference(m, n):
+    a = _rng(12 + m + n).standard_normal((m, n))
+    res = _p().svd_full(a)
+    u, s, vt = _np(res.u), _np(res.s), _np(res.vt)
+    ru, rs, rvt = oracle.ref_svd(a)
+    k = min(m, n)
+    assert u.shape == (m, k) and s.shape == (k,) and vt.shape == (k, n)
+    assert np.max(np.abs(s - rs)) < 1e-12 * rs[0]
+    assert np.all(np.diff(s) <= 0.0) and np.all(s >= 0.0)
+    assert np.max(np.abs(u.T @ u - np.eye(k))) < 1e-12
+    assert np.max(np.abs(vt @ vt.T - np.eye(k))) < 1e-12
+    assert np.max(np.abs((u * s) @ vt - a)) < 1e-12 * rs[0]
+    # Gaussian spectra are well separated: the vectors match the reference, signs included
+    assert np.max(np.abs(u - ru)) < 1e-9 and np.max(np.abs(vt - rvt)) < 1e-9
+    peaks = u[np.argmax(np.abs(u), axis=0), np.arange(k)]
+    assert np.all(peaks > 0.0)
+
+
+def test_svd_wide_core_gram_route():
+    # more than 160 columns on both sides: the Gram eigenpair route (leading values)
+    a = oracle.burgers_matrix(2048, 400)
+    res = _p().svd_full(a, want_vt=False)
+    ru, rs, _ = oracle.ref_svd(a, want_vt=False)
+    assert res.vt is None
+    s = _np(res.s)
+    assert np.max(np.abs(s[:10] - rs[:10]) / rs[:10]) < 1e-10
+    assert np.max(oracle.mode_angles(_np(res.u)[:, :10], ru[:, :10])) < 1e-8
+
+
+def test_svd_want_vt_false_and_zero_matrix():
+    p = _p()
+    a = _rng(14).standard_normal((7, 5))
+    full, left = p.svd_full(a, want_vt=True), p.svd_full(a, want_vt=False)
+    assert left.vt is None
+    assert torch.equal(full.u, left.u) and torch.equal(full.s, left.s)
+    assert np.array_equal(_np(p.svd_full(np.zeros((4, 3))).s), np.zeros(3))
+
+
+# ---------------------------------------------------------------- randomized_range / low_rank_svd
+
+def test_range_finder_exact_rank_and_reference():
+    p = _p()
+    rng = _rng(15)
+    a = np.outer(rng.standard_normal(30), rng.standard_normal(12))
+    a += np.outer(rng.standard_normal(30), rng.standard_normal(12))
+    cfg = p.RandomSketchConfig(target_rank=2, oversampling=3, power_iterations=0, seed=0)
+    q = _np(p.randomized_range(a, cfg))
+    assert q.shape == (30, 5)
+    assert np.max(np.abs(q.T @ q - np.eye(5))) < 1e-12
+    assert np.max(np.abs(a - q @ (q.T @ a))) < 1e-10
+    b = _rng(16).standard_normal((2000, 60))
+    for it in (0, 1, 2):
+        cfg = p.RandomSketchConfig(target_rank=8, oversampling=4, power_iterations=it, seed=99)
+        q = _np(p.randomized_range(b, cfg))
+        ref = oracle.ref_range(b, 12, it, 99)
+        assert np.max(np.abs(q - ref)) < 1e-10  # same basis: qr_factor's sign convention
+    with pytest.raises(ValueError):
+        p.randomized_range(np.eye(4), p.RandomSketchConfig(target_rank=3, oversampling=2))
+
+
+def test_low_rank_svd_vt_matches_reference():
+    p = _p()
+    rng = _rng(17)
+    u0 = oracle.ref_qr(rng.standard_normal((40, 3)))[0]
+    v0 = oracle.ref_qr(rng.standard_normal((15, 3)))[0]
+    a = (u0 * [7.0, 4.0, 2.0]) @ v0.T
+    res = p.low_rank_svd(a, p.RandomSketchConfig(target_rank=3, oversampling=5, power_iterations=1, seed=1))
+    assert np.allclose(_np(res.s), [7.0, 4.0, 2.0], rtol=1e-10)
+    assert np.max(np.abs((_np(res.u) * _np(res.s)) @ _np(res.vt) - a)) < 1e-9
+    b = oracle.burgers_matrix(4096, 300)
+    res = p.low_rank_svd(b, p.RandomSketchConfig(target_rank=10, oversampling=10, power_iterations=1, seed=3))
+    ru, rs, rvt = oracle.ref_low_rank_svd(b, 10, 10, 1, 3)
+    assert oracle.sigma_rel_err(_np(res.s), rs) < 1e-10
+    assert np.max(oracle.mode_angles(_np(res.vt).T, rvt.T)) < 1e-8
+    assert np.all(np.sum(_np(res.vt) * rvt, axis=1) > 0)  # rows signed like the reference's
+
+
+# ---------------------------------------------------------------- parallel_qr
+
+def _qr_rank_worker(rank, world, port, q, rows, cols, seed):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2108_08845_b200 as p
+        a = np.random.Generator(np.random.Philox(seed)).standard_normal((rows, cols))
+        lo, hi = p.partition_bounds(rows, world)[rank]
+        res = p.parallel_qr(p.RankContext(), a[lo:hi])
+        q.put((rank, res.q.cpu().numpy(), res.r.cpu().numpy()))
+    except Exception as e:
+        q.put((rank, "error", repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,rows,cols", [(4, 32, 5), (3, 9, 5), (2, 20000, 30)])
+def test_parallel_qr_ranks_match_serial(world, rows, cols):
+    """Four ranks of 8 rows, three of 3 rows (shorter than the 5 columns: dsvd.py's short
+    blocks), two of 10000: same R on every rank, stacked Q orthonormal, factors equal to
+    the serial qr_factor's (test_dsvd.py:174-211)."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_qr_rank_worker, args=(r, world, port, q, rows, cols, 66)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = {}
+    for _ in range(world):
+        rank, qq, rr = q.get(timeout=300)
+        assert not (isinstance(qq, str) and qq == "error"), rr
+        out[rank] = (qq, rr)
+    for pr in procs:
+        pr.join(timeout=120)
+    assert all(pr.exitcode == 0 for pr in procs)
+    r = out[0][1]
+    for rank in range(1, world):
+        assert np.array_equal(out[rank][1], r)
+    a = np.random.Generator(np.random.Philox(66)).standard_normal((rows, cols))
+    qfull = np.concatenate([out[k][0] for k in range(world)], axis=0)
+    assert np.max(np.abs(qfull.T @ qfull - np.eye(cols))) < 1e-12
+    assert np.max(np.abs(qfull @ r - a)) < 1e-12 * np.sqrt(rows)
+    qs, rs = oracle.ref_qr(a)
+    assert np.max(np.abs(r - rs)) < 1e-10 * max(1.0, np.abs(rs).max())
+    assert np.max(np.abs(qfull - qs)) < 1e-10
+
+
+def test_parallel_qr_world_one_is_qr_factor():
+    p = _p()
+    a = _rng(65).standard_normal((20, 6))
+    serial = p.qr_factor(a)
+    par = p.parallel_qr(p.RankContext(), a)
+    assert torch.equal(par.q, serial.q) and torch.equal(par.r, serial.r)

@@ -323,11 +323,11 @@ def test_randomized_stream_golden(golden, q):
 def test_low_rank_svd_small_golden(golden):
     p = _pkg()
     g = golden("rand_small")
-    u, s = p.low_rank_svd(g["lowrank_a"], p.RandomSketchConfig(target_rank=3, oversampling=5, power_iterations=1,
-                                                               seed=1))
+    u, s, _ = p.low_rank_svd(g["lowrank_a"], p.RandomSketchConfig(target_rank=3, oversampling=5, power_iterations=1,
+                                                                  seed=1))
     _assert_parity(u.cpu().numpy(), s.cpu().numpy(), g["lowrank_u"], g["lowrank_s"])
-    u, s = p.low_rank_svd(g["gauss_a"], p.RandomSketchConfig(target_rank=4, oversampling=2, power_iterations=0,
-                                                             seed=99))
+    u, s, _ = p.low_rank_svd(g["gauss_a"], p.RandomSketchConfig(target_rank=4, oversampling=2, power_iterations=0,
+                                                                seed=99))
     _assert_parity(u.cpu().numpy(), s.cpu().numpy(), g["gauss_u"], g["gauss_s"], sig_tol=1e-10, ang_tol=1e-8)
 
 
@@ -382,6 +382,25 @@ def test_pipelined_randomized_run_bitwise_and_validation():
         p.stream_all(_batches(bad, 200), cfg)
     with pytest.raises(ValueError):  # initial batch narrower than k_modes
         p.stream_all([a[:, :5], a[:, 5:200]], cfg)
+
+
+@pytest.mark.parametrize("b", [264, 300, 520])
+def test_batches_wider_than_one_tma_box(b):
+    """Segments wider than 256 columns take several TMA boxes; the last one may overhang the
+    segment by < 8 columns only (a full-width overhang once zero-filled the next segment's
+    columns).  Deterministic and randomized streams against the oracle."""
+    p = _pkg()
+    a = oracle.burgers_matrix(8192, 3 * b) + 1e-3 * np.random.default_rng(b).standard_normal((8192, 3 * b))
+    bs = _batches(a, b)
+    ref_m, ref_s, _ = oracle.ref_stream_all(bs, 10, 0.95)
+    st, _ = p.stream_all(bs, p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=b))
+    m, s_ = _np(st)
+    _assert_parity(m, s_, ref_m, ref_s)
+    sk = p.RandomSketchConfig(target_rank=10, oversampling=10, power_iterations=1, seed=2)
+    ref_m, ref_s, _ = oracle.ref_rand_stream_all(bs, 10, 0.95, 10, 1, 2)
+    st, _ = p.stream_all(bs, p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=b, sketch=sk))
+    m, s_ = _np(st)
+    _assert_parity(m, s_, ref_m, ref_s)
 
 
 def test_randomized_validation():
