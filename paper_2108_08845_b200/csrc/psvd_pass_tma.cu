@@ -37,7 +37,8 @@ constexpr int YMAXC = 32;     // widest Y of the narrow pass (4 column blocks)
 constexpr int YB = 2;         // Y ring depth (Y warps run up to YB stages ahead of the Gram warps; 4 measured no faster)
 constexpr int PROD_WARP = NWARP - 1;
 // sW row stride (doubles, = 4 mod 16: 2 wavefronts per B-fragment load), sized by the Y width
-__host__ __device__ inline int w_stride(int w_pad) { return w_pad <= 16 ? 20 : 36; }
+// (stride mod 16 = 4 or 12: the four W rows of a fragment load tile the 32 banks twice)
+__host__ __device__ inline int w_stride(int w_pad) { return w_pad <= 16 ? 20 : (w_pad <= 24 ? 28 : 36); }
 
 PSVD_DEV uint32_t saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -165,14 +166,24 @@ __global__ void __launch_bounds__(NTHR, 1)
 
   if (warp == PROD_WARP) {
     if (lane == 0) {
-      for (int64_t s = 0; s < nstage; ++s) {
-        const int b = (int)(s % TNS);
-        if (s >= TNS) mbar_wait(&empty[b], (unsigned)(((s / TNS) - 1) & 1));
-        mbar_expect_tx(&full[b], x.stage_bytes);
-        double* dst = sP + (size_t)b * pw * TKS;
-        const int r0 = (int)(row_begin + s * TKS);
+      // stages are issued in groups of x.grp consecutive ones, box by box, so each column's
+      // grp x 128 contiguous bytes reach DRAM back to back (a lone 128-byte piece per column
+      // and stage is a poor DRAM access: tools/colmajor_bw.cu measured 16-row chunks at ~60%
+      // of the 64-row rate)
+      const int G = x.grp;
+      for (int64_t s0 = 0; s0 < nstage; s0 += G) {
+        const int64_t s1 = min(nstage, s0 + G);
+        for (int64_t s = s0; s < s1; ++s) {
+          const int b = (int)(s % TNS);
+          if (s >= TNS) mbar_wait(&empty[b], (unsigned)(((s / TNS) - 1) & 1));
+          mbar_expect_tx(&full[b], x.stage_bytes);
+        }
         for (int o = 0; o < x.nops; ++o)
-          tma_load_2d(dst + (size_t)x.op_pcol[o] * TKS, &maps.m[x.op_seg[o]], r0, x.op_col[o], &full[b]);
+          for (int64_t s = s0; s < s1; ++s) {
+            const int b = (int)(s % TNS);
+            tma_load_2d(sP + (size_t)b * pw * TKS + (size_t)x.op_pcol[o] * TKS, &maps.m[x.op_seg[o]],
+                        (int)(row_begin + s * TKS), x.op_col[o], &full[b]);
+          }
       }
     }
     return;
@@ -653,6 +664,9 @@ int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift) {
          tma_pass_smem_bytes(x.pwidth, x.kp_hi - x.kp_lo, p.w_pad, x.ns + 1, 1) <= (size_t)(227 * 1024))
     ++x.ns;
   if (const char* e = getenv("PSVD_TMA_NS")) x.ns = std::max(2, std::min(x.ns, atoi(e)));
+  // issue groups: half the ring (two groups in flight), at most 4 stages = 64 rows
+  x.grp = 1;  // grouped issue (consecutive stages box by box) measured no faster: off by default
+  if (const char* e = getenv("PSVD_TMA_GROUP")) x.grp = std::max(1, std::min(x.ns, atoi(e)));
   return 0;
 }
 

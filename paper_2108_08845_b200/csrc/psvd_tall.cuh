@@ -107,6 +107,7 @@ struct TmaExtra {
   int pwidth;                // physical ring width (columns)
   unsigned stage_bytes;
   int ns;                    // ring depth (stages)
+  int grp;                   // stages issued together (consecutive rows of every column back to back)
   unsigned char written[TMA_MAX_BLK];  // 8-column panel blocks covered by a TMA box
 };
 bool tma_available();

@@ -236,3 +236,30 @@ def test_parallel_qr_world_one_is_qr_factor():
     serial = p.qr_factor(a)
     par = p.parallel_qr(p.RankContext(), a)
     assert torch.equal(par.q, serial.q) and torch.equal(par.r, serial.r)
+
+
+def test_kernel_invariants_1000_matrices():
+    """test_acceptance.py:226-261 on the device: 1000 seeded matrices, every dimension up to 32;
+    QR and SVD post-conditions and agreement with the Gram-eigenvalue route."""
+    import time
+    p = _p()
+    t0 = time.perf_counter()
+    worst = 0.0
+    for seed in range(1000):
+        rng = np.random.Generator(np.random.Philox(seed))
+        rows, cols = (int(x) for x in rng.integers(1, 33, size=2))
+        a = rng.standard_normal((rows, cols))
+        qr = p.qr_factor(a)
+        q, r = _np(qr.q), _np(qr.r)
+        assert np.max(np.abs(q.T @ q - np.eye(min(rows, cols)))) <= 1e-13 * max(rows, cols)
+        assert np.max(np.abs(q @ r - a)) <= 1e-12 * (1 + np.max(np.abs(a)))
+        assert np.all(np.diag(r) >= 0)
+        res = p.svd_full(a)
+        u, s, vt = _np(res.u), _np(res.s), _np(res.vt)
+        assert np.all(s >= 0) and np.all(np.diff(s) <= 0)
+        assert np.max(np.abs((u * s) @ vt - a)) <= 1e-12 * (1 + s[0])
+        gram = a.T @ a if cols <= rows else a @ a.T
+        ref = np.sqrt(np.clip(np.linalg.eigvalsh(gram)[::-1], 0.0, None))
+        worst = max(worst, float(np.max(np.abs(ref - s)) / (1 + s[0])))
+    assert worst <= 1e-9
+    assert time.perf_counter() - t0 < 120.0
