@@ -239,18 +239,15 @@ static int plan_tiles_tma(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int
   const int nt = (int)tiles.size();
   memset(ps.p.plan, 0, sizeof(ps.p.plan));
   memset(&ps.map, 0, sizeof(ps.map));
-  // Y warps: 2 row blocks x ncb column blocks; each block's k range is split yks ways (up to 12
-  // Y warps = 3 per SMSP) while the Gram tiles still fit one slice: the Y product is bound by
-  // the per-warp load -> DMMA latency chain, so more warps on it pay
+  // Y warps: 2 row blocks x ncb column blocks; with 32-row stages (M a multiple of 16) a second
+  // set of warps takes the second 16-row half when the Gram tiles still fit one slice (3 Y warps
+  // per SMSP instead of 1.5: the Y product is bound by each warp's load -> DMMA chains)
   const int nyo = 2 * (ps.p.w_pad / 8);
-  static const int yks_max = getenv("PSVD_YKS") ? atoi(getenv("PSVD_YKS")) : 1;
-  int yks = 1;
-  while (yks < yks_max && nyo * (yks + 1) <= 12 && nyo * (yks + 1) + nt <= NWARP - 1 &&
-         (ps.p.wk + 7) / 8 >= 2 * (yks + 1) && yks * nyo <= 10)  // partial slots: (yks - 1) * nyo <= 10
-    ++yks;
-  ps.p.yks = yks;
+  static const bool no_yh = getenv("PSVD_NO_YH") != nullptr;
+  const int yh = (!no_yh && ps.p.M % 16 == 0 && 2 * nyo + nt <= NWARP - 1) ? 2 : 1;
+  ps.p.yh = yh;
   static const int cap = getenv("PSVD_TMA_SLICE_WARPS") ? atoi(getenv("PSVD_TMA_SLICE_WARPS")) : 0;  // diagnostics
-  const int warp0 = nyo * yks, nwarps = cap > 0 ? std::min(cap, NWARP - 1 - warp0) : NWARP - 1 - warp0;
+  const int warp0 = nyo * yh, nwarps = cap > 0 ? std::min(cap, NWARP - 1 - warp0) : NWARP - 1 - warp0;
   const int nslices = std::max(1, (nt + nwarps - 1) / nwarps);
   if (nt > MAX_OUT_TILES || nslices > MAX_SLICES) return fail(c, PSVD_EINVAL, "panel too wide (%d tiles)", nt);
   ps.p.nslices = nslices;
@@ -408,9 +405,9 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
     if (rc2) return rc2;
     p.partial = (double*)ps.part->ptr;
   }
-  if ((tma || ps.gtma) && tma_pass_prepare(p, ps.maps, ps.x, tma ? pshift : 0) != 0)
+  if ((tma || ps.gtma) && tma_pass_prepare(p, ps.maps, ps.x, tma ? pshift : 0, tma) != 0)
     return fail(c, PSVD_ECUDA, "TMA descriptor setup failed");
-  if (tma && tma_pass_smem_bytes(ps.x.pwidth, ps.x.kp_hi - ps.x.kp_lo, p.w_pad, ps.x.ns, 1) > (size_t)SMEM_LIMIT)
+  if (tma && tma_pass_smem_bytes(ps.x.pwidth, ps.x.kp_hi - ps.x.kp_lo, p.w_pad, ps.x.ns, ps.x.rb) > (size_t)SMEM_LIMIT)
     return fail(c, PSVD_EINVAL, "narrow pass ring of %d columns exceeds shared memory", ps.x.pwidth);
   return PSVD_OK;
 }
@@ -436,7 +433,7 @@ int run_pass(psvd_ctx* c, Pass& ps, cudaStream_t st) {
     snprintf(buf, sizeof(buf), " [%s pass: np=%d np_pad=%d w=%d wk=%d nseg=%d grid=%d pwidth=%d kspan=%d ns=%d smem=%zu]",
              ps.tma ? "narrow TMA" : ps.gtma ? "TMA Gram" : ps.ws ? "ws Gram" : "general", ps.p.np, ps.p.np_pad, ps.p.w,
              ps.p.wk, ps.p.nseg, ps.grid, ps.x.pwidth, ps.x.kp_hi - ps.x.kp_lo, ps.x.ns,
-             ps.tma ? tma_pass_smem_bytes(ps.x.pwidth, ps.x.kp_hi - ps.x.kp_lo, ps.p.w_pad, ps.x.ns, 1)
+             ps.tma ? tma_pass_smem_bytes(ps.x.pwidth, ps.x.kp_hi - ps.x.kp_lo, ps.p.w_pad, ps.x.ns, ps.x.rb)
                     : tall_smem_bytes(ps.p.ks, ps.p.np_pad, ps.p.wk, ps.p.w, ps.p.nstage));
     c->err += buf;
     return rc;

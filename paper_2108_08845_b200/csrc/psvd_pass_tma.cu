@@ -67,23 +67,40 @@ PSVD_DEV void tma_load_2d_mc(void* dst, const CUtensorMap* map, int c0, int c1, 
 // element (column c, stage row k) of a 128B-swizzled 16-row stage, in doubles
 PSVD_DEV int swz(int c, int k) { return c * 16 + ((((k >> 1) ^ (c & 7)) << 1) | (k & 1)); }
 
+// RB row blocks of 16 per stage: column c's rows are RB consecutive 128-byte units (the layout a
+// 3-D TMA box {16 rows, RB row blocks, columns} lands in), unit u = c RB + (k >> 4) swizzled by u & 7
+template <int RB>
+PSVD_DEV int swzr(int c, int k) {
+  const int u = c * RB + (k >> 4);
+  return u * 16 + (((((k & 15) >> 1) ^ (u & 7)) << 1) | (k & 1));
+}
+
+PSVD_DEV void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::
+          "r"(saddr(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(saddr(bar))
+      : "memory");
+}
+
 }  // namespace
 
-size_t tma_pass_smem_bytes(int pwidth, int kp_span, int w_pad, int ns, int ny) {
+size_t tma_pass_smem_bytes(int pwidth, int kp_span, int w_pad, int ns, int rb) {
   size_t b = 1024;  // alignment slack for the 1024-byte swizzle atoms
-  (void)ny;
-  b += sizeof(double) * (size_t)ns * pwidth * TKS;   // panel ring
-  b += sizeof(double) * YB * YMAXC * TKS;            // Y ring (<= 32 columns)
+  const int sr = TKS * std::max(1, rb);
+  b += sizeof(double) * (size_t)ns * pwidth * sr;    // panel ring
+  b += sizeof(double) * YB * YMAXC * sr;             // Y ring (<= 32 columns)
   b += sizeof(double) * (size_t)kp_span * w_stride(w_pad);  // W
   b += 64 * sizeof(uint64_t);                        // barriers
-  b += sizeof(double) * 2 * YMAXC * 3;               // argmax scratch
-  b += sizeof(double) * 2 * 10 * 32 * 2;             // k-split Y partials ((yks - 1) * nyo <= 10)
+  b += sizeof(double) * 4 * YMAXC * 3;               // argmax scratch
   return b;
 }
 
+template <int RB>
 __global__ void __launch_bounds__(NTHR, 1)
     pass_tma_kernel(const __grid_constant__ TallParams p, const __grid_constant__ TmaMaps maps, const TmaExtra x) {
   if (p.gate != nullptr && *p.gate == 0) return;  // gated pass (drift rescue) not needed
+  constexpr int SR = TKS * RB;  // rows per stage
   extern __shared__ unsigned char smem_raw[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tq = lane & 3;
@@ -96,14 +113,15 @@ __global__ void __launch_bounds__(NTHR, 1)
   const int kspan = x.kp_hi - x.kp_lo;
   const int WSP = w_stride(p.w_pad);
   const int ncb = p.w_pad >> 3;  // Y column blocks (1..4)
-  const int nyo = 2 * ncb;       // Y output blocks (2 row blocks x ncb), owned by warps 0 .. nyo-1
-  const int yks = max(1, p.yks);  // warps per Y block (k split); warps 0 .. nyo*yks-1 form Y
+  const int nyo = 2 * ncb;       // Y output blocks (2 row blocks of 8 x ncb) per 16-row block
+  // 32-row stages: the two 16-row halves of a block go to one warp (yh = 1) or to two (yh = 2)
+  const int yh = (RB == 2 && p.yh == 2) ? 2 : 1;
 
   unsigned char* base = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
   double* sP = reinterpret_cast<double*>(base);
   const int TNS = x.ns;
-  double* sY = sP + (size_t)TNS * pw * TKS;
-  double* sW = sY + YB * YMAXC * TKS;
+  double* sY = sP + (size_t)TNS * pw * SR;
+  double* sW = sY + YB * YMAXC * SR;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sW + (size_t)kspan * WSP);
   uint64_t* full = bars;
   uint64_t* empty = bars + TNS;
@@ -111,9 +129,8 @@ __global__ void __launch_bounds__(NTHR, 1)
   uint64_t* yfree = ydone + YB;
   double* cmx = reinterpret_cast<double*>(bars + 64);  // [2 rb][32 cols][val, abs, row]
 
-  double* ypart = cmx + 2 * YMAXC * 3;  // k-split partials: [2 parity][yks-1][nyo][32 lanes][2]
   int ngram = 0;
-  const int ny = nyo * yks;
+  const int ny = nyo * yh;  // Y warps 0 .. ny-1
   for (int w = ny; w < PROD_WARP; ++w) ngram += p.plan[slice][w].ntile > 0;
 
   // one-time setup: zero the panel columns no TMA box writes (alignment gaps), the Y
@@ -121,18 +138,18 @@ __global__ void __launch_bounds__(NTHR, 1)
   for (int i = tid; i < TNS * pw; i += NTHR) {
     const int c = i % pw;
     if (!x.written[c >> 3]) {
-      double* col = sP + (size_t)i * TKS;
+      double* col = sP + (size_t)i * SR;
 #pragma unroll
-      for (int k = 0; k < TKS; ++k) col[k] = 0.0;
+      for (int k = 0; k < SR; ++k) col[k] = 0.0;
     }
   }
-  for (int i = tid; i < YB * YMAXC * TKS; i += NTHR) sY[i] = 0.0;
+  for (int i = tid; i < YB * YMAXC * SR; i += NTHR) sY[i] = 0.0;
   for (int i = tid; i < kspan * WSP; i += NTHR) {
     const int kk = i / WSP, o = i % WSP;
     // rows of each full 8-column step are stored in the Y warps' k order: step half h reads
     // columns 2h + {0, 1, 4, 5} (see the Y warps); the 4-column tail keeps the natural order
     int kperm = kk;
-    if (kk < ((kspan >> 3) << 3)) {
+    if (RB == 1 && kk < ((kspan >> 3) << 3)) {
       const int r = kk & 7, h = r >> 2, t = r & 3;
       kperm = (kk & ~7) + 2 * h + (t & 1) + 4 * (t >> 1);
     }
@@ -155,14 +172,14 @@ __global__ void __launch_bounds__(NTHR, 1)
       mbar_init(&empty[b], (unsigned)(ny + ngram));
     }
     for (int b = 0; b < YB; ++b) {
-      mbar_init(&ydone[b], 32u * nyo);
+      mbar_init(&ydone[b], 32u * ny);
       mbar_init(&yfree[b], (unsigned)max(32 * ngram, 1));
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // zero fills before the first TMA writes
   __syncthreads();
-  const int64_t nstage = row_end > row_begin ? (row_end - row_begin + TKS - 1) / TKS : 0;
+  const int64_t nstage = row_end > row_begin ? (row_end - row_begin + SR - 1) / SR : 0;
 
   if (warp == PROD_WARP) {
     if (lane == 0) {
@@ -176,13 +193,18 @@ __global__ void __launch_bounds__(NTHR, 1)
         for (int64_t s = s0; s < s1; ++s) {
           const int b = (int)(s % TNS);
           if (s >= TNS) mbar_wait(&empty[b], (unsigned)(((s / TNS) - 1) & 1));
-          mbar_expect_tx(&full[b], x.stage_bytes);
+          mbar_expect_tx(&full[b], p.dbg == 2 ? 0u : x.stage_bytes);  // dbg 2: no loads (compute-only timing)
         }
+        if (p.dbg == 2) continue;
         for (int o = 0; o < x.nops; ++o)
           for (int64_t s = s0; s < s1; ++s) {
             const int b = (int)(s % TNS);
-            tma_load_2d(sP + (size_t)b * pw * TKS + (size_t)x.op_pcol[o] * TKS, &maps.m[x.op_seg[o]],
-                        (int)(row_begin + s * TKS), x.op_col[o], &full[b]);
+            double* dst = sP + (size_t)b * pw * SR + (size_t)x.op_pcol[o] * SR;
+            const int r0 = (int)(row_begin + s * SR);
+            if (RB == 1)
+              tma_load_2d(dst, &maps.m[x.op_seg[o]], r0, x.op_col[o], &full[b]);
+            else  // rows r0 .. r0 + SR - 1 of every column: SR * 8 contiguous bytes per column
+              tma_load_3d(dst, &maps.m[x.op_seg[o]], 0, r0 / TKS, x.op_col[o], &full[b]);
           }
       }
     }
@@ -191,100 +213,109 @@ __global__ void __launch_bounds__(NTHR, 1)
 
   if (warp < ny) {
     // ---------------------------------------------------------------- Y warps
-    // warp -> output block blk = (rb, cb) and k part (the k range of a block split yks ways in
-    // 8-column steps, the last part takes the 4-column tail); part 0 owns the block
-    const int blk = warp % nyo, part = warp / nyo;
+    // warp -> output block blk = (rb, cb) of every 16-row block h it owns (all of a stage's
+    // halves when yh == 1, half hp when yh == 2), over the whole k range
+    const int blk = warp % nyo, hp = warp / nyo;
     const int rb = blk & 1, cb = blk >> 1;
-    const int n8all = (x.kp_hi - x.kp_lo) >> 3;
-    const int k_lo = x.kp_lo + (n8all * part / yks) * 8;
-    const int k_hi = part == yks - 1 ? x.kp_hi : x.kp_lo + (n8all * (part + 1) / yks) * 8;
+    const int h_lo = yh == 2 ? hp : 0, h_hi = yh == 2 ? hp + 1 : RB;
+    const int k_lo = x.kp_lo, k_hi = x.kp_hi;
     double cm_val[2] = {0.0, 0.0}, cm_abs[2] = {-1.0, -1.0};
     int64_t cm_row[2] = {-1, -1};
     const bool do_y = slice == 0;
     for (int64_t s = 0; s < nstage; ++s) {
       const int b = (int)(s % TNS), yb = (int)(s & (YB - 1));
       mbar_wait(&full[b], (unsigned)((s / TNS) & 1));
-      const double* P = sP + (size_t)b * pw * TKS;
+      const double* P = sP + (size_t)b * pw * SR;
       const int kr = rb * 8 + g;
-      // kp_lo is a multiple of 8: the swizzle phase of column kp_lo + 8i + tq (+ 4) is tq (+ 4)
-      // for every i, so the fragment addresses advance by 8 columns = 128 doubles per step.
-      // Groups of 4 steps: 16 independent loads issued together, then 8 DMMAs on 4 chains
-      // (the per-warp load -> DMMA latency chain, not the pipes, bounded the one-step loop).
-      // step half h of an 8-column step reads columns k0 + 2h + {0, 1, 4, 5}[tq]: the four columns
-      // of a fragment then fall in both 64-byte halves of the swizzled 128-byte rows (2 wavefronts
-      // per LDS instead of 4); W's staged rows follow the same order
-      const int ph = (tq & 1) + 4 * (tq >> 1);
-      const double* pa = P + (size_t)(k_lo + ph) * TKS + ((((kr >> 1) ^ ph) << 1) | (kr & 1));
-      const double* pb = P + (size_t)(k_lo + ph + 2) * TKS + ((((kr >> 1) ^ (ph + 2)) << 1) | (kr & 1));
-      const double* wa = sW + (size_t)(k_lo - x.kp_lo + tq) * WSP + cb * 8 + g;
-      const double* wbp = wa + (size_t)4 * WSP;
-      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0, c4 = 0.0, c5 = 0.0, c6 = 0.0, c7 = 0.0;
-      const int n8 = p.dbg == 1 ? 0 : (k_hi - k_lo) >> 3;
-      int i = 0;
-#pragma unroll 1
-      for (; i + 4 <= n8; i += 4) {
-        double fa[8], fw[8];
+      double y0h[RB], y1h[RB];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          fa[2 * j] = pa[(size_t)(i + j) * 128];
-          fa[2 * j + 1] = pb[(size_t)(i + j) * 128];
-          fw[2 * j] = wa[(size_t)(8 * (i + j)) * WSP];
-          fw[2 * j + 1] = wbp[(size_t)(8 * (i + j)) * WSP];
+      for (int h = 0; h < RB; ++h) {
+        y0h[h] = y1h[h] = 0.0;
+        if (h < h_lo || h >= h_hi) continue;
+        // RB == 1: kp_lo is a multiple of 8, so the swizzle phase of a column is fixed per lane and
+        // the fragment addresses advance by 8 columns per step.  Step half h of an 8-column step
+        // reads columns k0 + 2h + {0, 1, 4, 5}[tq] (the four columns of a fragment then fall in
+        // both 64-byte halves of the swizzled rows: 2 wavefronts per LDS); W's rows follow.
+        // RB == 2: the unit phase is (2 c + h) & 7, already spread by the natural order k0 + tq.
+        // Groups of 4 steps: 16 independent loads, then 8 DMMAs on 4 chains (the per-warp
+        // load -> DMMA latency chain bounded the one-step loop).
+        int colA, colB, phA, phB;
+        if (RB == 1) {
+          colA = (tq & 1) + 4 * (tq >> 1);
+          colB = colA + 2;
+          phA = colA;
+          phB = colB;
+        } else {
+          colA = tq;
+          colB = tq + 4;
+          phA = (RB * tq + h) & 7;
+          phB = phA;
         }
-        dmma884(c0, c1, fa[0], fw[0]);
-        dmma884(c2, c3, fa[1], fw[1]);
-        dmma884(c4, c5, fa[2], fw[2]);
-        dmma884(c6, c7, fa[3], fw[3]);
-        dmma884(c0, c1, fa[4], fw[4]);
-        dmma884(c2, c3, fa[5], fw[5]);
-        dmma884(c4, c5, fa[6], fw[6]);
-        dmma884(c6, c7, fa[7], fw[7]);
+        const double* pa = P + (size_t)(RB * (k_lo + colA) + h) * 16 + ((((kr >> 1) ^ phA) << 1) | (kr & 1));
+        const double* pb = P + (size_t)(RB * (k_lo + colB) + h) * 16 + ((((kr >> 1) ^ phB) << 1) | (kr & 1));
+        constexpr int STEP = 128 * RB;  // doubles per 8 columns
+        const double* wa = sW + (size_t)(k_lo - x.kp_lo + tq) * WSP + cb * 8 + g;
+        const double* wbp = wa + (size_t)4 * WSP;
+        double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0, c4 = 0.0, c5 = 0.0, c6 = 0.0, c7 = 0.0;
+        const int n8 = p.dbg == 1 ? 0 : (k_hi - k_lo) >> 3;
+        int i = 0;
+#pragma unroll 1
+        for (; i + 4 <= n8; i += 4) {
+          double fa[8], fw[8];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            fa[2 * j] = pa[(size_t)(i + j) * STEP];
+            fa[2 * j + 1] = pb[(size_t)(i + j) * STEP];
+            fw[2 * j] = wa[(size_t)(8 * (i + j)) * WSP];
+            fw[2 * j + 1] = wbp[(size_t)(8 * (i + j)) * WSP];
+          }
+          dmma884(c0, c1, fa[0], fw[0]);
+          dmma884(c2, c3, fa[1], fw[1]);
+          dmma884(c4, c5, fa[2], fw[2]);
+          dmma884(c6, c7, fa[3], fw[3]);
+          dmma884(c0, c1, fa[4], fw[4]);
+          dmma884(c2, c3, fa[5], fw[5]);
+          dmma884(c4, c5, fa[6], fw[6]);
+          dmma884(c6, c7, fa[7], fw[7]);
+        }
+        for (; i < n8; ++i) {
+          dmma884(c0, c1, pa[(size_t)i * STEP], wa[(size_t)(8 * i) * WSP]);
+          dmma884(c2, c3, pb[(size_t)i * STEP], wbp[(size_t)(8 * i) * WSP]);
+        }
+        if (p.dbg != 1 && k_lo + 8 * n8 < k_hi)  // kp span is a multiple of 4; natural order
+          dmma884(c4, c5, P[swzr<RB>(k_lo + 8 * n8 + tq, kr + 16 * h)], wa[(size_t)(8 * n8) * WSP]);
+        y0h[h] = (c0 + c4) + (c2 + c6);
+        y1h[h] = (c1 + c5) + (c3 + c7);
       }
-      for (; i < n8; ++i) {
-        dmma884(c0, c1, pa[(size_t)i * 128], wa[(size_t)(8 * i) * WSP]);
-        dmma884(c2, c3, pb[(size_t)i * 128], wbp[(size_t)(8 * i) * WSP]);
-      }
-      if (p.dbg != 1 && k_lo + 8 * n8 < k_hi)  // kp span is a multiple of 4; natural order
-        dmma884(c4, c5, P[swz(k_lo + 8 * n8 + tq, kr)], wa[(size_t)(8 * n8) * WSP]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[b]);  // panel slot no longer read by this warp
-      double y0 = (c0 + c4) + (c2 + c6), y1 = (c1 + c5) + (c3 + c7);
-      if (yks > 1) {
-        // partials meet at the block's named barrier (ids 2 .. 2+nyo-1); part 0 adds them in part
-        // order.  Double-buffered by stage parity: a partial for stage s+2 is written only after
-        // the rendezvous of stage s+1, i.e. after part 0 read stage s.
-        double* slot = ypart + ((((size_t)(s & 1) * (yks - 1)) * nyo + blk) * 32 + lane) * 2;
-        const size_t pstride = (size_t)nyo * 32 * 2;
-        if (part > 0) {
-          slot[(part - 1) * pstride] = y0;
-          slot[(part - 1) * pstride + 1] = y1;
-        }
-        asm volatile("bar.sync %0, %1;\n" ::"r"(2 + blk), "r"(32 * yks) : "memory");
-        if (part > 0) continue;
-        for (int q = 1; q < yks; ++q) {
-          y0 += slot[(q - 1) * pstride];
-          y1 += slot[(q - 1) * pstride + 1];
-        }
-      }
       if (s >= YB && ngram > 0) mbar_wait(&yfree[yb], (unsigned)(((s / YB) - 1) & 1));
-      double* Ys = sY + (size_t)yb * YMAXC * TKS;
+      double* Ys = sY + (size_t)yb * YMAXC * SR;
       const int o0 = cb * 8 + 2 * tq;
-      Ys[swz(o0, kr)] = y0;
-      Ys[swz(o0 + 1, kr)] = y1;
+#pragma unroll
+      for (int h = 0; h < RB; ++h) {
+        if (h < h_lo || h >= h_hi) continue;
+        Ys[swzr<RB>(o0, kr + 16 * h)] = y0h[h];
+        Ys[swzr<RB>(o0 + 1, kr + 16 * h)] = y1h[h];
+      }
       mbar_arrive(&ydone[yb]);
-      const int64_t r = row_begin + s * TKS + kr;
-      if (do_y && r < row_end) {
-        if (p.Yout != nullptr) {
-          if (o0 < p.w) p.Yout[(int64_t)o0 * p.ldy + r] = y0;
-          if (o0 + 1 < p.w) p.Yout[(int64_t)(o0 + 1) * p.ldy + r] = y1;
-        }
-        if (p.colmax != nullptr) {
-          if (fabs(y0) > cm_abs[0]) { cm_abs[0] = fabs(y0); cm_val[0] = y0; cm_row[0] = r; }
-          if (fabs(y1) > cm_abs[1]) { cm_abs[1] = fabs(y1); cm_val[1] = y1; cm_row[1] = r; }
+#pragma unroll
+      for (int h = 0; h < RB; ++h) {
+        if (h < h_lo || h >= h_hi) continue;
+        const int64_t r = row_begin + s * SR + 16 * h + kr;
+        const double y0 = y0h[h], y1 = y1h[h];
+        if (do_y && r < row_end) {
+          if (p.Yout != nullptr) {
+            if (o0 < p.w) p.Yout[(int64_t)o0 * p.ldy + r] = y0;
+            if (o0 + 1 < p.w) p.Yout[(int64_t)(o0 + 1) * p.ldy + r] = y1;
+          }
+          if (p.colmax != nullptr) {
+            if (fabs(y0) > cm_abs[0]) { cm_abs[0] = fabs(y0); cm_val[0] = y0; cm_row[0] = r; }
+            if (fabs(y1) > cm_abs[1]) { cm_abs[1] = fabs(y1); cm_val[1] = y1; cm_row[1] = r; }
+          }
         }
       }
     }
-    if (part > 0) return;
     if (do_y && p.colmax != nullptr) {
       // combine over g (lanes 4 apart), ties to the smaller row (first occurrence)
 #pragma unroll
@@ -301,19 +332,20 @@ __global__ void __launch_bounds__(NTHR, 1)
       }
       if (g == 0) {
         for (int e = 0; e < 2; ++e) {
-          double* d = cmx + ((size_t)rb * YMAXC + cb * 8 + 2 * tq + e) * 3;
+          double* d = cmx + ((size_t)(rb + 2 * hp) * YMAXC + cb * 8 + 2 * tq + e) * 3;
           d[0] = cm_val[e]; d[1] = cm_abs[e]; d[2] = (double)cm_row[e];
         }
       }
-      asm volatile("bar.sync 1, %0;\n" ::"r"(32 * nyo) : "memory");
-      if (rb == 0 && g == 0) {
+      asm volatile("bar.sync 1, %0;\n" ::"r"(32 * ny) : "memory");
+      if (rb == 0 && hp == 0 && g == 0) {
         for (int e = 0; e < 2; ++e) {
           const int o = cb * 8 + 2 * tq + e;
           if (o >= p.w) continue;
-          const double* d0 = cmx + (size_t)o * 3;
-          const double* d1 = cmx + ((size_t)YMAXC + o) * 3;
-          const bool take1 = d1[1] > d0[1] || (d1[1] == d0[1] && d1[2] >= 0 && (d0[2] < 0 || d1[2] < d0[2]));
-          const double* d = take1 ? d1 : d0;
+          const double* d = cmx + (size_t)o * 3;
+          for (int q = 1; q < 2 * yh; ++q) {  // ties: the smaller row (first occurrence)
+            const double* d1 = cmx + ((size_t)q * YMAXC + o) * 3;
+            if (d1[1] > d[1] || (d1[1] == d[1] && d1[2] >= 0 && (d[2] < 0 || d1[2] < d[2]))) d = d1;
+          }
           double* dst = p.colmax + ((size_t)chunk * p.w + o) * 2;
           dst[0] = d[0];
           dst[1] = d[2] + (double)p.row_offset;
@@ -341,17 +373,17 @@ __global__ void __launch_bounds__(NTHR, 1)
       const int b = (int)(s % TNS), yb = (int)(s & (YB - 1));
       mbar_wait(&full[b], (unsigned)((s / TNS) & 1));
       mbar_wait(&ydone[yb], (unsigned)((s / YB) & 1));
-      const double* Ys = sY + (size_t)yb * YMAXC * TKS;
-      const double* Abase = sP + (size_t)b * pw * TKS;
+      const double* Ys = sY + (size_t)yb * YMAXC * SR;
+      const double* Abase = sP + (size_t)b * pw * SR;
 #pragma unroll
-      for (int kk = 0; kk < TKS / 4; ++kk) {
+      for (int kk = 0; kk < SR / 4; ++kk) {
         const int k = kk * 4 + tq;
         double fa[NA], fb[NB];
 #pragma unroll
         for (int q = 0; q < NA; ++q)
-          fa[q] = i_is_y ? Ys[swz(q * 8 + g, k)] : Abase[swz(acol + q * 8 + g, k)];
+          fa[q] = i_is_y ? Ys[swzr<RB>(q * 8 + g, k)] : Abase[swzr<RB>(acol + q * 8 + g, k)];
 #pragma unroll
-        for (int q = 0; q < NB; ++q) fb[q] = Ys[swz(q * 8 + g, k)];
+        for (int q = 0; q < NB; ++q) fb[q] = Ys[swzr<RB>(q * 8 + g, k)];
         if (p.dbg != 1)
 #pragma unroll
           for (int a = 0; a < NA; ++a)
@@ -594,7 +626,7 @@ static EncodeTiledFn encode_fn() {
 
 bool tma_available() { return encode_fn() != nullptr; }
 
-int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift) {
+int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift, bool narrow) {
   EncodeTiledFn enc = encode_fn();
   if (!enc) return -1;
   memset(&x, 0, sizeof(x));
@@ -637,6 +669,7 @@ int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift) {
       x.op_seg[nops] = (short)(k < nfull ? s : (nfull > 0 ? MAX_SEG + s : s));
       x.op_col[nops] = (short)c;
       x.op_pcol[nops] = (short)dst;
+      x.op_bw[nops] = (short)bw;
       for (int q = dst >> 3; q < (dst + bw) >> 3 && q < TMA_MAX_BLK; ++q) x.written[q] = 1;
       bytes += (uint32_t)(TKS * bw * sizeof(double));
       pend = std::max(pend, dst + bw);
@@ -658,10 +691,34 @@ int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift) {
   x.nops = nops;
   x.stage_bytes = bytes;
   x.pwidth = std::max((p.np_pad + pshift + 7) / 8 * 8, (pend + 7) / 8 * 8);
-  // ring depth: as many 16-row stages as shared memory holds (3 .. TNS_MAX)
-  x.ns = 3;
+  // 32-row stages (narrow passes, M a multiple of 16, a 2-deep ring fits): one 3-D box per
+  // column block brings 256 contiguous bytes of every column per request -- 16-row boxes (128
+  // bytes per column) cap TMA streaming at ~4.6 TB/s, 32-row ones reach ~6.9
+  // (tools/tma_stream_bw.cu)
+  static const bool no_rb2 = getenv("PSVD_TMA_RB1") != nullptr;
+  x.rb = 1;
+  if (narrow && !no_rb2 && p.M % TKS == 0 &&
+      tma_pass_smem_bytes(x.pwidth, x.kp_hi - x.kp_lo, p.w_pad, 2, 2) <= (size_t)(227 * 1024)) {
+    x.rb = 2;
+    for (int o = 0; o < nops; ++o) {
+      const int m = x.op_seg[o], sidx = m % MAX_SEG;
+      const Seg& sg = p.seg[sidx];
+      cuuint64_t dims[3] = {(cuuint64_t)TKS, (cuuint64_t)(p.M / TKS), (cuuint64_t)sg.ncols};
+      cuuint64_t strides[2] = {(cuuint64_t)TKS * sizeof(double), (cuuint64_t)sg.ld * sizeof(double)};
+      cuuint32_t box[3] = {(cuuint32_t)TKS, 2, (cuuint32_t)x.op_bw[o]};
+      cuuint32_t es[3] = {1, 1, 1};
+      if (enc(&maps.m[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(sg.ptr), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return -1;
+    }
+    x.stage_bytes = 2 * bytes;
+  }
+  if (x.rb != 2) p.yh = 1;  // 16-row stages: the second half-warps of the plan stay idle
+  // ring depth: as many stages as shared memory holds (3 .. TNS_MAX; 2 .. for 32-row stages)
+  x.ns = x.rb == 2 ? 2 : 3;
   while (x.ns < TNS_MAX &&
-         tma_pass_smem_bytes(x.pwidth, x.kp_hi - x.kp_lo, p.w_pad, x.ns + 1, 1) <= (size_t)(227 * 1024))
+         tma_pass_smem_bytes(x.pwidth, x.kp_hi - x.kp_lo, p.w_pad, x.ns + 1, x.rb) <= (size_t)(227 * 1024))
     ++x.ns;
   if (const char* e = getenv("PSVD_TMA_NS")) x.ns = std::max(2, std::min(x.ns, atoi(e)));
   // issue groups: half the ring (two groups in flight), at most 4 stages = 64 rows
@@ -671,9 +728,14 @@ int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift) {
 }
 
 void launch_pass_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x, int grid, cudaStream_t st) {
-  const size_t smem = tma_pass_smem_bytes(x.pwidth, x.kp_hi - x.kp_lo, p.w_pad, x.ns, 1);
-  cudaFuncSetAttribute(pass_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  pass_tma_kernel<<<grid, NTHR, smem, st>>>(p, maps, x);
+  const size_t smem = tma_pass_smem_bytes(x.pwidth, x.kp_hi - x.kp_lo, p.w_pad, x.ns, x.rb);
+  if (x.rb == 2) {
+    cudaFuncSetAttribute(pass_tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    pass_tma_kernel<2><<<grid, NTHR, smem, st>>>(p, maps, x);
+  } else {
+    cudaFuncSetAttribute(pass_tma_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    pass_tma_kernel<1><<<grid, NTHR, smem, st>>>(p, maps, x);
+  }
 }
 
 }  // namespace psvd

@@ -63,7 +63,7 @@ struct TallParams {
   double* Yout;          // optional global copy of Y (col-major, ld ldy)
   int64_t ldy;
   int nslices;
-  int yks;               // TMA pass: warps per Y output block (k range split yks ways, summed in part order)
+  int yh;                // narrow TMA pass with 32-row stages: 2 = one Y warp per 16-row half of a block
   WarpPlan plan[MAX_SLICES][NWARP];
   double* partial;       // [grid][SLOTS][1024]
   double* colmax;        // optional [grid][w][2] = (signed value at max |y|, global row)
@@ -101,6 +101,7 @@ struct TmaMaps {
 struct TmaExtra {
   int nops;
   short op_seg[TMA_MAX_OPS], op_col[TMA_MAX_OPS], op_pcol[TMA_MAX_OPS];  // op_seg: tensor map index
+  short op_bw[TMA_MAX_OPS];  // box width (columns)
   int wrow0[MAX_SEG];        // W row of the segment's first column (TMA_NOT_IN_W: outside Y's range)
   int kp_lo, kp_hi;          // Y's k range in physical panel columns
   int pshift;                // physical column = logical column + pshift (narrow pass)
@@ -108,11 +109,12 @@ struct TmaExtra {
   unsigned stage_bytes;
   int ns;                    // ring depth (stages)
   int grp;                   // stages issued together (consecutive rows of every column back to back)
+  int rb;                    // 16-row blocks per stage of the narrow pass (1: 2-D boxes; 2: 3-D boxes)
   unsigned char written[TMA_MAX_BLK];  // 8-column panel blocks covered by a TMA box
 };
 bool tma_available();
 size_t tma_pass_smem_bytes(int pwidth, int kp_span, int w_pad, int ns = 3, int ny = 1);
-int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift = 0);
+int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift = 0, bool narrow = false);
 void launch_pass_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x, int grid, cudaStream_t st);
 // TMA-fed Gram-only pass (w == 0, segments on 8-column boundaries, <= NWARP - 1 tiles per slice)
 constexpr int TMA_GRAM_CONS = NWARP - 1;
