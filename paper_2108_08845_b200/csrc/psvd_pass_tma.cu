@@ -191,14 +191,14 @@ __global__ void __launch_bounds__(NTHR, 1)
       for (int64_t s0 = 0; s0 < nstage; s0 += G) {
         const int64_t s1 = min(nstage, s0 + G);
         for (int64_t s = s0; s < s1; ++s) {
-          const int b = (int)(s % TNS);
-          if (s >= TNS) mbar_wait(&empty[b], (unsigned)(((s / TNS) - 1) & 1));
+          const int si = (int)s, b = si % TNS;
+          if (si >= TNS) mbar_wait(&empty[b], (unsigned)(((si / TNS) - 1) & 1));
           mbar_expect_tx(&full[b], p.dbg == 2 ? 0u : x.stage_bytes);  // dbg 2: no loads (compute-only timing)
         }
         if (p.dbg == 2) continue;
         for (int o = 0; o < x.nops; ++o)
           for (int64_t s = s0; s < s1; ++s) {
-            const int b = (int)(s % TNS);
+            const int b = (int)s % TNS;
             double* dst = sP + (size_t)b * pw * SR + (size_t)x.op_pcol[o] * SR;
             const int r0 = (int)(row_begin + s * SR);
             if (RB == 1)
@@ -222,9 +222,12 @@ __global__ void __launch_bounds__(NTHR, 1)
     double cm_val[2] = {0.0, 0.0}, cm_abs[2] = {-1.0, -1.0};
     int64_t cm_row[2] = {-1, -1};
     const bool do_y = slice == 0;
-    for (int64_t s = 0; s < nstage; ++s) {
-      const int b = (int)(s % TNS), yb = (int)(s & (YB - 1));
-      mbar_wait(&full[b], (unsigned)((s / TNS) & 1));
+    // ring position (b, phase) advanced per stage: no 64-bit divisions in the stage loop
+    int b = 0;
+    unsigned ph = 0;
+    for (int64_t s = 0; s < nstage; ++s, (++b == TNS ? (b = 0, ph ^= 1u) : 0u)) {
+      const int yb = (int)(s & (YB - 1));
+      mbar_wait(&full[b], ph);
       const double* P = sP + (size_t)b * pw * SR;
       const int kr = rb * 8 + g;
       double y0h[RB], y1h[RB];
@@ -289,7 +292,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[b]);  // panel slot no longer read by this warp
-      if (s >= YB && ngram > 0) mbar_wait(&yfree[yb], (unsigned)(((s / YB) - 1) & 1));
+      if (s >= YB && ngram > 0) mbar_wait(&yfree[yb], (unsigned)((((int)s / YB) - 1) & 1));
       double* Ys = sY + (size_t)yb * YMAXC * SR;
       const int o0 = cb * 8 + 2 * tq;
 #pragma unroll
@@ -369,10 +372,12 @@ __global__ void __launch_bounds__(NTHR, 1)
     for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
   auto stage_loop = [&](auto na_t, auto nb_t) {
     constexpr int NA = decltype(na_t)::value, NB = decltype(nb_t)::value;
-    for (int64_t s = 0; s < nstage; ++s) {
-      const int b = (int)(s % TNS), yb = (int)(s & (YB - 1));
-      mbar_wait(&full[b], (unsigned)((s / TNS) & 1));
-      mbar_wait(&ydone[yb], (unsigned)((s / YB) & 1));
+    int b = 0;
+    unsigned ph = 0;
+    for (int64_t s = 0; s < nstage; ++s, (++b == TNS ? (b = 0, ph ^= 1u) : 0u)) {
+      const int yb = (int)(s & (YB - 1));
+      mbar_wait(&full[b], ph);
+      mbar_wait(&ydone[yb], (unsigned)(((int)s / YB) & 1));
       const double* Ys = sY + (size_t)yb * YMAXC * SR;
       const double* Abase = sP + (size_t)b * pw * SR;
 #pragma unroll
