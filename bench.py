@@ -261,13 +261,7 @@ def run_ours(a):
         return nat._vp(D.data_ptr() + 8 * ld * j)
 
     Ubuf = [nat.DevMat.empty(M, K, dev) for _ in range(2)]
-    sig = [torch.zeros(K, dtype=torch.float64, device=dev) for _ in range(2)]
-    nmax = K + BATCH
-    G = torch.empty((nmax, nmax), dtype=torch.float64, device=dev)
-    W = torch.empty((K, nmax), dtype=torch.float64, device=dev)
-    gram_ev = []
     Gloc = {n: torch.empty((n, n), dtype=torch.float64, device=dev) for n in (BATCH, K + BATCH)}
-    utu = torch.empty((K, K), dtype=torch.float64, device=dev)
 
     nb = SNAPS // BATCH
     Aptr = (nat._vp * nb)(*[col_ptr(b * BATCH) for b in range(nb)])
@@ -276,37 +270,21 @@ def run_ours(a):
     hist = torch.empty((nb, K), dtype=torch.float64, device=dev)
     fin = ctypes.c_int(0)
 
+    ex = None
+    if world > 1:
+        # the pipelined stream with the library's exchange hooks (dsvd._Exchange): per update a
+        # rank-ordered NCCL sum of the streaming Gram and of U^T U on the library's stream
+        from paper_2108_08845_b200.dsvd import _Exchange
+        ex = _Exchange(ctxr, dev)
+        nat.call("psvd_set_exchange", c, ctypes.cast(ex.ar, nat._vp), ctypes.cast(ex.ag, nat._vp), None, world, lo)
+
     def step(record=False):
-        if world == 1:
-            # whole stream through psvd_stream_run (look-ahead A^T A on a second stream)
-            nat.call("psvd_stream_run", c, M, nat._vp(0), 0, nat._vp(0), 0, nb, Aptr, Ald, Bc, K, FF, 1,
-                     nat._vp(Ubuf[0].data_ptr()), nat._vp(Ubuf[1].data_ptr()), Ubuf[0].ld, nat.ptr(hist),
-                     ctypes.byref(fin), None, st)
-            return Ubuf[fin.value], hist[nb - 1]
-        cur = 0
-        for b in range(nb):
-            kc = 0 if b == 0 else K
-            n = kc + BATCH
-            Uin, Uout = Ubuf[cur], Ubuf[cur ^ 1]
-            Gl = Gloc[n]
-            if record:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-            nat.call("psvd_gram", c, M, nat._vp(Uin.data_ptr()), Uin.ld, nat.ptr(sig[cur]), FF, kc,
-                     col_ptr(b * BATCH), ld, BATCH, nat.ptr(Gl), st)
-            if record:
-                e1.record(stream)
-                gram_ev.append((e0, e1, M * n * (n + 1)))
-            Gs = allreduce_ordered(Gl, ctxr)
-            nat.call("psvd_core_eig", c, nat.ptr(Gs), n, nat.ptr(sig[cur]), FF, kc, K, nat.ptr(W),
-                     nat.ptr(sig[cur ^ 1]), st)
-            nat.call("psvd_recompose", c, M, nat._vp(Uin.data_ptr()), Uin.ld, kc, col_ptr(b * BATCH), ld,
-                     BATCH, nat.ptr(W), K, nat._vp(Uout.data_ptr()), Uout.ld, nat.ptr(utu), st)
-            u2 = allreduce_ordered(utu, ctxr)
-            nat.call("psvd_refine_normalize", c, M, nat._vp(Uout.data_ptr()), Uout.ld, K, nat.ptr(u2),
-                     nat.ptr(sig[cur ^ 1]), st)
-            cur ^= 1
-        return Ubuf[cur], sig[cur]
+        # whole stream through psvd_stream_run (look-ahead A^T A on a second stream); no drift
+        # rescue when row-partitioned (dsvd.py:220-242 has none)
+        nat.call("psvd_stream_run", c, M, nat._vp(0), 0, nat._vp(0), 0, nb, Aptr, Ald, Bc, K, FF, int(world == 1),
+                 nat._vp(Ubuf[0].data_ptr()), nat._vp(Ubuf[1].data_ptr()), Ubuf[0].ld, nat.ptr(hist),
+                 ctypes.byref(fin), None, st)
+        return Ubuf[fin.value], hist[nb - 1]
 
     def gram_probe():
         """The dominant kernel on its own: the batch Gram A^T A (M x B, the look-ahead pass of
@@ -344,6 +322,8 @@ def run_ours(a):
         clk.sample_now()  # the queued steps are still running
         barrier()
     launches = nat.lib().psvd_launch_count(c) - launches0
+    if ex is not None:
+        nat.call("psvd_set_exchange", c, None, None, None, 1, 0)
     ms = t0.elapsed_time(t1)
     if world > 1:
         tt = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -353,12 +333,10 @@ def run_ours(a):
     snap_bytes = 8.0 * a.rows * SNAPS  # whole job, all ranks
     value = snap_bytes / (ms_step * 1e-3) / 1e9
 
-    if gram_ev:
-        gram_ms = [e0.elapsed_time(e1) for e0, e1, _ in gram_ev]
-        gram_flops = [f for _, _, f in gram_ev]
-    else:  # N = 1 runs the pipelined stream; time the Gram kernel alone after the timed region
-        gms, gfl = gram_probe()
-        gram_ms, gram_flops = [gms] * (a.steps * (SNAPS // BATCH)), [gfl] * (a.steps * (SNAPS // BATCH))
+    # the pipelined stream interleaves kernels on two streams: time the Gram kernel alone after
+    # the timed region (the look-ahead A^T A launch of the stream, same shape)
+    gms, gfl = gram_probe()
+    gram_ms, gram_flops = [gms] * (a.steps * (SNAPS // BATCH)), [gfl] * (a.steps * (SNAPS // BATCH))
     g_ach = sum(gram_flops) / (sum(gram_ms) * 1e-3) / 1e12
     alg_bytes_step = sum(8.0 * M * (2 * BATCH + 3 * (0 if b == 0 else K)) for b in range(SNAPS // BATCH))
     hbm_ach = alg_bytes_step / (ms_step * 1e-3) / 1e9  # per GPU
@@ -471,10 +449,8 @@ def e2e(a, p, D, M, dev, world, ctxr):
             # stream_all: pinned batches upload on a side stream, overlapping the pipelined updates
             st, _ = p.stream_all(batches, cfg, device=dev)
             return st.to_host()
-        else:
-            st = p.parallel_stream_initialize(ctxr, batches[0].to(dev), cfg)
-            for bt in batches[1:]:
-                st = p.parallel_stream_incorporate(ctxr, st, bt.to(dev), cfg)
+        else:  # row-partitioned pipelined stream (exchange hooks on NCCL)
+            st, _ = p.parallel_stream_all(ctxr, batches, cfg, device=dev)
             m, s = st.modes, st.singular_values
         return m.cpu(), s.cpu()
 
@@ -509,7 +485,7 @@ def e2e(a, p, D, M, dev, world, ctxr):
     return {"value": round(8.0 * a.rows * SNAPS / dt / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": int(8 * M * SNAPS), "d2h_bytes_per_step": int(out[0].numel() * 8 + out[1].numel() * 8),
             "ms_per_step": round(dt * 1e3, 2), "steps": n,
-            "path": "public API stream_all (N=1) / parallel_stream_* (N>1) from pinned host batches"}
+            "path": "public API stream_all (N=1) / parallel_stream_all (N>1) from pinned host batches"}
 
 
 def main():

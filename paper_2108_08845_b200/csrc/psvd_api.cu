@@ -1238,12 +1238,18 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
       launch_assemble_gram((const double*)c->tiles.ptr, nbua, (const double*)c->tiles2[b & 1].ptr, nbaa[b & 1], kc,
                            B[b], (const double*)c->dvec.ptr, G, hi);
     } else {
+      // row-partitioned (exchange hooks): U^T U is already the global, normalized Gram; the other
+      // blocks are local.  Only the first rank keeps the U^T U block, so the rank-ordered sum
+      // below reproduces it exactly
+      const double uu_w = (c->ex_allreduce && c->ex_row_offset != 0) ? 0.0 : 1.0;
       const double* tb = (const double*)c->tbuf.ptr;
       launch_assemble_gram_fused((const double*)c->tiles.ptr, nbua, fused_a0, fused_y, UtU, tb + (size_t)K * K,
                                  prev_resc ? c->d_gate : nullptr, tb, (const double*)c->tiles2[b & 1].ptr,
-                                 nbaa[b & 1], K, B[b], (const double*)c->dvec.ptr, G, hi);
+                                 nbaa[b & 1], K, B[b], (const double*)c->dvec.ptr, G, hi, uu_w);
     }
     c->launches++;
+    // row-partitioned: the streaming Gram is the rank-ordered sum of the local ones
+    if ((rc = ex_allreduce(c, G, (int64_t)n * n, hi))) return rc;
     cudaEventRecord(c->ev_asm[b & 1], hi);
     double* sig_b = sigma_hist + (size_t)b * K;
     if ((rc = core_solve(c, G, n, K, (const double*)c->dvec.ptr, W, sig_b, hi, nullptr))) return rc;
@@ -1284,11 +1290,13 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
       }
       launch_extract_sym((const double*)c->tiles.ptr, pf.NB, pf.p.np_pad, K, nullptr, UtU, hi);
       c->launches++;
+      if ((rc = ex_allreduce(c, UtU, (int64_t)K * K, hi))) return rc;  // global U^T U
       nbua = pf.NB;
       fused_a0 = a0;
       fused_y = pf.p.np_pad / 32;
     } else {
       if ((rc = psvd_recompose(c, M, Uprev, ldprev, kc, A[b], lda[b], B[b], W, K, Uout, ldo, UtU, hi))) return rc;
+      if ((rc = ex_allreduce(c, UtU, (int64_t)K * K, hi))) return rc;
     }
     if ((rc = refine_normalize(c, M, Uout, ldo, K, UtU, sig_b, hi))) return rc;
     if (resc && (rc = psvd_drift_rescue(c, M, Uout, ldo, K, UtU, sig_b, c->drift_tol, hi))) return rc;

@@ -89,7 +89,7 @@ __global__ void assemble_gram_fused_kernel(const double* __restrict__ tf, int nb
                                            const double* __restrict__ UU, const double* __restrict__ scale,
                                            const int* __restrict__ gate, const double* __restrict__ T,
                                            const double* __restrict__ taa, int nbaa, int K, int B,
-                                           const double* __restrict__ d, double* __restrict__ G) {
+                                           const double* __restrict__ d, double* __restrict__ G, double uu_w) {
   const int n = K + B;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)n * n) return;
@@ -108,7 +108,7 @@ __global__ void assemble_gram_fused_kernel(const double* __restrict__ tf, int nb
         v += T[(size_t)i * K + a] * s;
       }
     }
-    v *= d[i] * d[j];
+    v *= d[i] * d[j] * uu_w;  // uu_w: 0 on all but the first rank when the local Grams are summed
   } else if (i < K) {
     const int col = j - K;
     auto ua = [&](int k) {
@@ -130,10 +130,10 @@ __global__ void assemble_gram_fused_kernel(const double* __restrict__ tf, int nb
 
 void launch_assemble_gram_fused(const double* tf, int nbf, int a0, int yb, const double* UU, const double* scale,
                                 const int* gate, const double* T, const double* taa, int nbaa, int K, int B,
-                                const double* d, double* G, cudaStream_t st) {
+                                const double* d, double* G, cudaStream_t st, double uu_w) {
   const int64_t tot = (int64_t)(K + B) * (K + B);
   assemble_gram_fused_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(tf, nbf, a0, yb, UU, scale, gate, T, taa,
-                                                                             nbaa, K, B, d, G);
+                                                                             nbaa, K, B, d, G, uu_w);
 }
 
 void launch_extract_rect(const double* tiles, int NB, int r0, int nr, int c0, int nc, const double* d,

@@ -21,7 +21,7 @@ void launch_assemble_gram(const double* tua, int nbua, const double* taa, int nb
                           double* G, cudaStream_t st);
 void launch_assemble_gram_fused(const double* tf, int nbf, int a0, int yb, const double* UU, const double* scale,
                                 const int* gate, const double* T, const double* taa, int nbaa, int K, int B,
-                                const double* d, double* G, cudaStream_t st);
+                                const double* d, double* G, cudaStream_t st, double uu_w = 1.0);
 // Extract the rectangular block rows [r0, r0+nr) x cols [c0, c0+nc) (r-block <= c-block),
 // scaled by row factors d (length nr, may be null).  col-major, ld nr.
 void launch_extract_rect(const double* tiles, int NB, int r0, int nr, int c0, int nc, const double* d,

@@ -62,6 +62,8 @@ def allreduce_ordered(t, ctx):
     if ctx.world_size == 1:
         return t
     t = t.contiguous()
+    if t.device.type == "cuda" and dist.get_backend(ctx.group) != "nccl":
+        return allreduce_ordered(t.cpu(), ctx).to(t.device)  # gloo: host-staged (test harness)
     if t.device.type == "cuda":
         parts = torch.empty((ctx.world_size,) + tuple(t.shape), dtype=t.dtype, device=t.device)
         dist.all_gather_into_tensor(parts, t, group=ctx.group)
@@ -223,6 +225,65 @@ def parallel_stream_incorporate(ctx, state, a_new_local, config):
     else:
         out, sig = _parallel_update(ctx, U, sigma, A, k, config.forget_factor, dev)
     return LocalModes(out.view, sig)
+
+
+def parallel_stream_all(ctx, batches_local, config, device=None):
+    """Row-partitioned stream over this rank's batches (B200 extension: the reference drives
+    parallel_stream_initialize / parallel_stream_incorporate batch by batch, cli.py:262-276;
+    same update rule, dsvd.py:205-242, no drift rescue).  Deterministic configs run in windows
+    through the pipelined psvd_stream_run with the exchange hooks: per update a rank-ordered
+    sum of the streaming Gram (first rank contributes the already-global U^T U block) and of
+    U^T U, so every rank factors identical bits; the next batch's A^T A still overlaps the
+    replicated core solve.  Randomized configs update batch by batch.  Returns
+    (LocalModes, history of singular values)."""
+    from .streaming import STREAM_WINDOW, _run_window
+    batches_local = list(batches_local)
+    if not batches_local:
+        raise ValueError("batch stream is empty")
+    dev = torch.device(device) if device is not None else _device(batches_local[0])
+    k = config.k_modes
+    if config.sketch is not None:
+        st = parallel_stream_initialize(ctx, batches_local[0], config)
+        hist = [st.singular_values.clone()]
+        for b in batches_local[1:]:
+            st = parallel_stream_incorporate(ctx, st, b, config)
+            hist.append(st.singular_values.clone())
+        return st, hist
+    mats = [nat.as_device_colmajor(b, dev, "a_local") for b in batches_local]
+    M = mats[0].rows
+    c = nat.context(dev)
+    ok = ctypes.c_int(0)
+    nat.call("psvd_stream_run_supported", c, M, k, max(m.cols for m in mats), ctypes.byref(ok))
+    flag = torch.tensor([float(ok.value)], dtype=torch.float64,
+                        device=dev if (ctx.world_size > 1 and dist.get_backend(ctx.group) == "nccl") else "cpu")
+    if ctx.world_size > 1:  # every rank takes the same route
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=ctx.group)
+    if not flag.item():
+        st = parallel_stream_initialize(ctx, mats[0], config)
+        hist = [st.singular_values.clone()]
+        for m in mats[1:]:
+            st = parallel_stream_incorporate(ctx, st, m, config)
+            hist.append(st.singular_values.clone())
+        return st, hist
+    off, _ = _row_offset(ctx, M, dev)
+    ex = None
+    if ctx.world_size > 1:
+        ex = _Exchange(ctx, dev)
+        nat.call("psvd_set_exchange", c, ctypes.cast(ex.ar, nat._vp), ctypes.cast(ex.ag, nat._vp), None,
+                 ctx.world_size, off)
+    state, hist = None, []
+    try:
+        for w0 in range(0, len(mats), STREAM_WINDOW):
+            state, h = _run_window(state, mats[w0:w0 + STREAM_WINDOW], config, dev, rescue=False, ok=True)
+            hist.extend(h)
+    except (RuntimeError, ValueError):
+        if ex is not None and ex.error is not None:
+            raise ex.error
+        raise
+    finally:
+        if ex is not None:
+            nat.call("psvd_set_exchange", c, None, None, None, 1, 0)
+    return LocalModes(state.modes, state.singular_values), hist
 
 
 def gather_modes(ctx, local_modes, root=0):

@@ -156,7 +156,7 @@ def stream_incorporate(state, a_new, config):
 STREAM_WINDOW = 8  # batches resident on the device per pipelined run
 
 
-def _run_window(state, mats, config, dev, ready=None):
+def _run_window(state, mats, config, dev, ready=None, rescue=True, ok=None):
     """Deterministic updates over device batches `mats` with look-ahead
     (psvd_stream_run): the next batch's A^T A overlaps the current core solve.
     `ready`: per-batch upload events (or None) the device work waits on."""
@@ -171,9 +171,11 @@ def _run_window(state, mats, config, dev, ready=None):
         raise ValueError(f"initial batch has {M} rows, need at least k_modes={k}")
     ctx = nat.context(dev)
     nb = len(mats)
-    ok = ctypes.c_int(0)
-    nat.call("psvd_stream_run_supported", ctx, M, k, max(m.cols for m in mats), ctypes.byref(ok))
-    if not ok.value:
+    if ok is None:
+        ok = ctypes.c_int(0)
+        nat.call("psvd_stream_run_supported", ctx, M, k, max(m.cols for m in mats), ctypes.byref(ok))
+        ok = ok.value
+    if not ok:
         # batches too wide for the pipelined kernels: one psvd_stream_update per batch
         # (wide Grams on the tall-skinny TN GEMM), same update rule
         if ready is not None:
@@ -205,7 +207,8 @@ def _run_window(state, mats, config, dev, ready=None):
         rd = None
         if ready is not None and any(e is not None for e in ready):
             rd = (nat._vp * nb)(*[nat._vp(e.cuda_event if e is not None else 0) for e in ready])
-        nat.call("psvd_stream_run", ctx, M, uptr, uld, sptr, kc, nb, A, lda, B, k, float(config.forget_factor), 1,
+        nat.call("psvd_stream_run", ctx, M, uptr, uld, sptr, kc, nb, A, lda, B, k, float(config.forget_factor),
+                 int(bool(rescue)),
                  nat._vp(outs[0].data_ptr()), nat._vp(outs[1].data_ptr()), outs[0].ld, nat.ptr(hist),
                  ctypes.byref(fin), rd, nat.stream_ptr(dev))
         _check_status(ctx, dev, "a_new")

@@ -520,6 +520,69 @@ def test_parallel_randomized_two_ranks_match_serial_oracle():
     _assert_parity(m, s_, rm, rs)
 
 
+def _det_run_rank_worker(rank, world, port, q, rows, cols, b):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2108_08845_b200 as p
+        a = oracle.burgers_matrix(rows, cols) + 1e-4 * np.random.default_rng(9).standard_normal((rows, cols))
+        lo, hi = p.partition_bounds(rows, world)[rank]
+        cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=b)
+        ctx = p.RankContext()
+        loc = [a[lo:hi, c0:c0 + b] for c0 in range(0, cols, b)]
+        st, hist = p.parallel_stream_all(ctx, loc, cfg)
+        st2 = p.parallel_stream_initialize(ctx, loc[0], cfg)
+        for m in loc[1:]:
+            st2 = p.parallel_stream_incorporate(ctx, st2, m, cfg)
+        full, full2 = p.gather_modes(ctx, st), p.gather_modes(ctx, st2)
+        q.put((rank, st.singular_values.cpu().numpy(), [h.cpu().numpy() for h in hist],
+               None if full is None else full.cpu().numpy(), None if full2 is None else full2.cpu().numpy(),
+               st2.singular_values.cpu().numpy()))
+    except Exception as e:
+        q.put((rank, "error", repr(e), None, None, None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,rows,cols,b", [(2, 6001, 600, 200), (3, 8192, 1000, 100)])
+def test_parallel_pipelined_stream_ranks_match_serial(world, rows, cols, b):
+    """Row-partitioned pipelined stream (psvd_stream_run with the exchange hooks; two or three
+    processes sharing this GPU, gloo through the host): identical singular values on every rank,
+    the gathered modes match the serial oracle on the whole matrix and the per-update parallel
+    path; 10 batches of 100 span two windows."""
+    import socket
+    import torch.multiprocessing as mp
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_det_run_rank_worker, args=(r, world, port, q, rows, cols, b)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = {}
+    for _ in range(world):
+        rank, sig, hist, full, full2, sig2 = q.get(timeout=300)
+        assert not (isinstance(sig, str) and sig == "error"), hist
+        out[rank] = (sig, hist, full, full2, sig2)
+    for pr in procs:
+        pr.join(timeout=120)
+    assert all(pr.exitcode == 0 for pr in procs)
+    for r in range(1, world):
+        assert np.array_equal(out[r][0], out[0][0])  # replicated core solve on identical bits
+    a = oracle.burgers_matrix(rows, cols) + 1e-4 * np.random.default_rng(9).standard_normal((rows, cols))
+    rm, rs, rh = oracle.ref_stream_all(_batches(a, b), 10, 0.95)
+    _assert_parity(out[0][2], out[0][0], rm, rs)
+    _assert_parity(out[0][3], out[0][4], rm, rs)
+    for h, r_ in zip(out[0][1], rh):
+        assert oracle.sigma_rel_err(h, r_) <= SIG_TOL
+
+
 def test_parallel_randomized_single_rank_is_serial():
     p = _pkg()
     a = oracle.burgers_matrix(4096, 400)
