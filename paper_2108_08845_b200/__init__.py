@@ -7,7 +7,8 @@ kernels (libpsvd.so, include/psvd.h) on state that stays in HBM.
 """
 
 from .oneshot import ApmosConfig, apmos, generate_right_vectors  # noqa: F401
-from .datagen import burgers_device, burgers_matrix, burgers_solution, partition_bounds  # noqa: F401
+from .datagen import (DEFAULT_MATRIX_CAP, BurgersConfig, burgers_device, burgers_matrix, burgers_solution,  # noqa: F401
+                      partition_bounds, row_partition, synthetic_spectrum_matrix)
 from .dsvd import (LocalModes, RankContext, gather_modes, parallel_qr, parallel_stream_all,  # noqa: F401
                    parallel_stream_incorporate, parallel_stream_initialize)
 from .errors import (CapacityError, CollectiveTimeout, ConvergenceError, DegenerateModeError,  # noqa: F401

@@ -8,21 +8,77 @@ few ulp: CUDA's exp/log1p vs glibc's).  partition_bounds is datagen.py:118-136.
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 import torch
 
 from . import _native as nat
+from .errors import CapacityError
+
+# datagen.py:15-17: allocation cap of the host generator
+DEFAULT_MATRIX_CAP = 1 << 30
 
 
-def burgers_solution(x, t, reynolds=1000.0):
+@dataclass(frozen=True)
+class BurgersConfig:
+    """Domain and discretization of the analytical Burgers dataset (datagen.py:21-46)."""
+
+    length: float = 1.0
+    t_final: float = 2.0
+    reynolds: float = 1000.0
+    grid_points: int = 16384
+    n_snapshots: int = 800
+
+    def __post_init__(self):
+        if not self.length > 0.0:
+            raise ValueError(f"length must be positive, got {self.length}")
+        if not self.t_final > 0.0:
+            raise ValueError(f"t_final must be positive, got {self.t_final}")
+        if not self.reynolds > 0.0:
+            raise ValueError(f"reynolds must be positive, got {self.reynolds}")
+        if self.grid_points < 2:
+            raise ValueError(f"grid_points must be >= 2, got {self.grid_points}")
+        if self.n_snapshots < 1:
+            raise ValueError(f"n_snapshots must be >= 1, got {self.n_snapshots}")
+
+
+def burgers_solution(x, t, config=None, reynolds=1000.0):
+    """u(x, t) of viscous Burgers in log space (datagen.py:49-73).  `config` may be a
+    BurgersConfig (the reference's signature: domain checks, its Reynolds number) or a
+    float Reynolds number; scalars in give a float out."""
+    if isinstance(config, BurgersConfig):
+        re = config.reynolds
+        xa, ta = np.asarray(x, dtype=np.float64), np.asarray(t, dtype=np.float64)
+        if xa.size and (np.min(xa) < 0.0 or np.max(xa) > config.length):
+            raise ValueError(f"x outside [0, {config.length}]")
+        if ta.size and (np.min(ta) < 0.0 or np.max(ta) > config.t_final):
+            raise ValueError(f"t outside [0, {config.t_final}]")
+    else:
+        re = float(config) if config is not None else reynolds
     x = np.asarray(x, dtype=np.float64)
     t = np.asarray(t, dtype=np.float64)
-    expo = 0.5 * (np.log1p(t) - reynolds / 8.0) + reynolds * x * x / (4.0 * (t + 1.0))
-    return (x / (t + 1.0)) * np.exp(-np.logaddexp(0.0, expo))
+    expo = 0.5 * (np.log1p(t) - re / 8.0) + re * x * x / (4.0 * (t + 1.0))
+    u = (x / (t + 1.0)) * np.exp(-np.logaddexp(0.0, expo))
+    return float(u) if u.ndim == 0 else u
 
 
-def burgers_matrix(grid_points, n_snapshots, length=1.0, t_final=2.0, reynolds=1000.0, rows=None, cols=None):
-    """u(x_i, t_j) on inclusive linspace grids; optional row / column slices."""
+def burgers_matrix(grid_points=None, n_snapshots=None, length=1.0, t_final=2.0, reynolds=1000.0, rows=None,
+                   cols=None, max_bytes=None):
+    """u(x_i, t_j) on inclusive linspace grids.  Reference form (datagen.py:76-90):
+    burgers_matrix(BurgersConfig(...), max_bytes=DEFAULT_MATRIX_CAP), CapacityError past the cap.
+    Extended form: burgers_matrix(grid_points, n_snapshots, ...) with optional row / column
+    slices (half-open ranges) for per-rank blocks of matrices too large to build whole."""
+    if grid_points is None or isinstance(grid_points, BurgersConfig):
+        cfg = grid_points if grid_points is not None else BurgersConfig()
+        cap = DEFAULT_MATRIX_CAP if max_bytes is None else max_bytes
+        if n_snapshots is not None and max_bytes is None:
+            cap = n_snapshots  # positional max_bytes, as the reference's second parameter
+        need = 8 * cfg.grid_points * cfg.n_snapshots
+        if need > cap:
+            raise CapacityError(f"snapshot matrix needs {need} bytes, cap is {cap}")
+        grid_points, n_snapshots = cfg.grid_points, cfg.n_snapshots
+        length, t_final, reynolds = cfg.length, cfg.t_final, cfg.reynolds
     x = np.linspace(0.0, length, grid_points)
     t = np.linspace(0.0, t_final, n_snapshots)
     if rows is not None:
@@ -30,6 +86,40 @@ def burgers_matrix(grid_points, n_snapshots, length=1.0, t_final=2.0, reynolds=1
     if cols is not None:
         t = t[cols[0]:cols[1]]
     return burgers_solution(x[:, None], t[None, :], reynolds)
+
+
+def synthetic_spectrum_matrix(rows, cols, singular_values, seed=0):
+    """Dense matrix with exactly the given leading singular values (datagen.py:93-115):
+    Philox(seed) Gaussian factors orthonormalized by QR (diag(R) >= 0, as qr_factor),
+    (u * sigma) @ v^T.  Host input generation, byte-identical to the reference's."""
+    sv = np.asarray(singular_values, dtype=np.float64)
+    if sv.ndim != 1 or sv.size < 1:
+        raise ValueError("singular_values must be a non-empty 1-D sequence")
+    if sv.size > min(rows, cols):
+        raise ValueError(f"{sv.size} singular values do not fit a {rows}x{cols} matrix")
+    if np.any(sv < 0.0):
+        raise ValueError("singular values must be non-negative")
+    if np.any(np.diff(sv) > 0.0):
+        raise ValueError("singular values must be non-increasing")
+    rng = np.random.Generator(np.random.Philox(seed))
+
+    def orth(m):
+        q, r = np.linalg.qr(m, mode="reduced")
+        d = np.sign(np.diag(r))
+        d[d == 0.0] = 1.0
+        return q * d
+
+    u = orth(rng.standard_normal((rows, sv.size)))
+    v = orth(rng.standard_normal((cols, sv.size)))
+    return (u * sv) @ v.T
+
+
+def row_partition(a, world_size):
+    """Per-rank row blocks (copies, in rank order) of a host matrix (datagen.py:139-142)."""
+    a = np.asarray(a, dtype=np.float64)
+    if a.ndim != 2 or min(a.shape) < 1:
+        raise ValueError(f"a must be a non-empty 2-D matrix, got shape {a.shape}")
+    return [a[lo:hi].copy() for lo, hi in partition_bounds(a.shape[0], world_size)]
 
 
 def burgers_device(grid_points, n_snapshots, rows=None, cols=None, length=1.0, t_final=2.0,

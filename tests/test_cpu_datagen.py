@@ -1,6 +1,9 @@
 """Builder-defined synthetic configs 3-5: seeded, column slices reproduce
 the full matrix's bytes (so batches can be generated alone), prescribed spectra."""
 import numpy as np
+import pytest
+
+import oracle
 
 from paper_2108_08845_b200 import datagen as dg
 
@@ -30,3 +33,58 @@ def test_column_noise_is_per_column():
     a = dg._column_noise(100, 3, 7, 5)
     b = dg._column_noise(100, 0, 10, 5)
     assert np.array_equal(a, b[:, 3:7])
+
+
+def test_reference_signatures_of_the_generators():
+    """datagen.py:21-142 signatures: BurgersConfig, burgers_matrix(config, max_bytes) with the
+    CapacityError cap, burgers_solution(x, t, config), synthetic_spectrum_matrix, row_partition."""
+    import paper_2108_08845_b200 as p
+    with pytest.raises(ValueError):
+        p.BurgersConfig(grid_points=1)
+    with pytest.raises(ValueError):
+        p.BurgersConfig(reynolds=0.0)
+    cfg = p.BurgersConfig(grid_points=4096, n_snapshots=800)
+    a = p.burgers_matrix(cfg)
+    assert np.array_equal(a, p.burgers_matrix(4096, 800))
+    assert np.array_equal(a, oracle.burgers_matrix(4096, 800))
+    with pytest.raises(p.CapacityError):
+        p.burgers_matrix(p.BurgersConfig(grid_points=1 << 20, n_snapshots=800))
+    with pytest.raises(p.CapacityError):
+        p.burgers_matrix(cfg, 1000)
+    assert isinstance(p.burgers_solution(0.5, 1.0, cfg), float)
+    with pytest.raises(ValueError):
+        p.burgers_solution(1.5, 1.0, cfg)
+    sv = [5.0, 3.0, 1.0]
+    m = p.synthetic_spectrum_matrix(40, 12, sv, seed=3)
+    assert np.allclose(np.linalg.svd(m, compute_uv=False)[:3], sv, rtol=1e-13)
+    assert np.array_equal(m, p.synthetic_spectrum_matrix(40, 12, sv, seed=3))
+    with pytest.raises(ValueError):
+        p.synthetic_spectrum_matrix(4, 4, [1.0, 2.0])
+    blocks = p.row_partition(np.arange(20.0).reshape(10, 2), 3)
+    assert [b.shape[0] for b in blocks] == [4, 3, 3]
+    assert np.array_equal(np.concatenate(blocks), np.arange(20.0).reshape(10, 2))
+
+
+# parsvd/__init__.py:16-35, the reference's public names, and where each lives here
+REFERENCE_PUBLIC = {
+    "StreamConfig", "StreamState", "stream_all", "stream_incorporate", "stream_initialize",
+    "ApmosConfig", "LocalModes", "apmos", "gather_modes", "generate_right_vectors", "parallel_qr",
+    "parallel_stream_incorporate", "parallel_stream_initialize",
+    "QrResult", "RandomSketchConfig", "SvdResult", "aligned_mode_difference", "low_rank_svd", "qr_factor",
+    "randomized_range", "subspace_angles", "svd_full",
+    "BurgersConfig", "burgers_matrix", "burgers_solution", "partition_bounds", "row_partition",
+    "synthetic_spectrum_matrix",
+    "BatchSource", "read_batches", "read_matrix", "read_matrix_header", "read_submatrix", "write_matrix",
+    "CapacityError", "CollectiveTimeout", "ConvergenceError", "DegenerateModeError", "MatrixFormatError",
+}
+# out of scope by SURVEY §8(f) / DESIGN §7: the TCP / simulated transports of comm.py, the CSV/SVG
+# emitters of io.py, and the errors only those raise
+OUT_OF_SCOPE = {"CommStats", "RankContext_tcp", "SimTransport", "TcpTransport", "broadcast", "decode_matrix",
+                "encode_matrix", "gather", "recv", "run_simulated", "send", "tcp_context_from_env",
+                "write_mode_svg", "write_modes_csv", "write_singular_values_csv", "ConfigError", "ProtocolError"}
+
+
+def test_public_api_covers_the_reference_hot_path_names():
+    import paper_2108_08845_b200 as p
+    missing = sorted(n for n in REFERENCE_PUBLIC if not hasattr(p, n))
+    assert not missing, missing
