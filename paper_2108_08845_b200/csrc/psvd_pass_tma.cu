@@ -37,8 +37,11 @@ constexpr int YMAXC = 32;     // widest Y of the narrow pass (4 column blocks)
 constexpr int YB = 2;         // Y ring depth (Y warps run up to YB stages ahead of the Gram warps; 4 measured no faster)
 constexpr int PROD_WARP = NWARP - 1;
 // sW row stride (doubles, = 4 mod 16: 2 wavefronts per B-fragment load), sized by the Y width
-// (stride mod 16 = 4 or 12: the four W rows of a fragment load tile the 32 banks twice)
-__host__ __device__ inline int w_stride(int w_pad) { return w_pad <= 16 ? 20 : (w_pad <= 24 ? 28 : 36); }
+// W row stride in doubles: the four W rows of a fragment load must tile the 16 double-banks
+// exactly twice (stride = 8 mod 16: w_pad 8 or 24 itself; 4 or 12 mod 16: 20 and 36 for 16 and 32)
+__host__ __device__ inline int w_stride(int w_pad) {
+  return (w_pad & 15) == 8 ? w_pad : (w_pad <= 16 ? 20 : 36);
+}
 
 PSVD_DEV uint32_t saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 
@@ -89,7 +92,7 @@ size_t tma_pass_smem_bytes(int pwidth, int kp_span, int w_pad, int ns, int rb) {
   size_t b = 1024;  // alignment slack for the 1024-byte swizzle atoms
   const int sr = TKS * std::max(1, rb);
   b += sizeof(double) * (size_t)ns * pwidth * sr;    // panel ring
-  b += sizeof(double) * YB * YMAXC * sr;             // Y ring (<= 32 columns)
+  b += sizeof(double) * YB * std::max(w_pad, 8) * sr;  // Y ring (w_pad <= 32 columns)
   b += sizeof(double) * (size_t)kp_span * w_stride(w_pad);  // W
   b += 64 * sizeof(uint64_t);                        // barriers
   b += sizeof(double) * 4 * YMAXC * 3;               // argmax scratch
@@ -121,7 +124,8 @@ __global__ void __launch_bounds__(NTHR, 1)
   double* sP = reinterpret_cast<double*>(base);
   const int TNS = x.ns;
   double* sY = sP + (size_t)TNS * pw * SR;
-  double* sW = sY + YB * YMAXC * SR;
+  const int YC = max(p.w_pad, 8);  // Y ring columns
+  double* sW = sY + YB * YC * SR;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sW + (size_t)kspan * WSP);
   uint64_t* full = bars;
   uint64_t* empty = bars + TNS;
@@ -143,7 +147,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       for (int k = 0; k < SR; ++k) col[k] = 0.0;
     }
   }
-  for (int i = tid; i < YB * YMAXC * SR; i += NTHR) sY[i] = 0.0;
+  for (int i = tid; i < YB * YC * SR; i += NTHR) sY[i] = 0.0;
   for (int i = tid; i < kspan * WSP; i += NTHR) {
     const int kk = i / WSP, o = i % WSP;
     // rows of each full 8-column step are stored in the Y warps' k order: step half h reads
@@ -293,7 +297,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[b]);  // panel slot no longer read by this warp
       if (s >= YB && ngram > 0) mbar_wait(&yfree[yb], (unsigned)((((int)s / YB) - 1) & 1));
-      double* Ys = sY + (size_t)yb * YMAXC * SR;
+      double* Ys = sY + (size_t)yb * YC * SR;
       const int o0 = cb * 8 + 2 * tq;
 #pragma unroll
       for (int h = 0; h < RB; ++h) {
@@ -378,7 +382,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       const int yb = (int)(s & (YB - 1));
       mbar_wait(&full[b], ph);
       mbar_wait(&ydone[yb], (unsigned)(((int)s / YB) & 1));
-      const double* Ys = sY + (size_t)yb * YMAXC * SR;
+      const double* Ys = sY + (size_t)yb * YC * SR;
       const double* Abase = sP + (size_t)b * pw * SR;
 #pragma unroll
       for (int kk = 0; kk < SR / 4; ++kk) {
