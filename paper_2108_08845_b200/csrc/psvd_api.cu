@@ -246,8 +246,20 @@ static int plan_tiles_tma(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int
   static const bool no_yh = getenv("PSVD_NO_YH") != nullptr;
   const int yh = (!no_yh && ps.p.M % 16 == 0 && 2 * nyo + nt <= NWARP - 1) ? 2 : 1;
   ps.p.yh = yh;
+  // register-resident W (32-row stages): column block x k part warps, most parts that fit
+  const int ncb = ps.p.w_pad / 8;
+  static const int kp_max = getenv("PSVD_YKP") ? atoi(getenv("PSVD_YKP")) : 4;
+  const int kspan_est = rup(ps.p.wk, 8) + 8 * ps.p.nseg;  // physical k span, gaps included
+  int ykp = 1;
+  if (ps.p.M % 16 == 0)
+    for (int kp = std::min(kp_max, 4); kp >= 2; --kp)
+      if (ncb * kp + nt <= NWARP - 1 && ncb * kp >= nyo && (kspan_est / 4 + kp - 1) / kp <= 16) {
+        ykp = kp;
+        break;
+      }
+  ps.p.ykp = ykp;
   static const int cap = getenv("PSVD_TMA_SLICE_WARPS") ? atoi(getenv("PSVD_TMA_SLICE_WARPS")) : 0;  // diagnostics
-  const int warp0 = nyo * yh, nwarps = cap > 0 ? std::min(cap, NWARP - 1 - warp0) : NWARP - 1 - warp0;
+  const int warp0 = ykp > 1 ? ncb * ykp : nyo * yh, nwarps = cap > 0 ? std::min(cap, NWARP - 1 - warp0) : NWARP - 1 - warp0;
   const int nslices = std::max(1, (nt + nwarps - 1) / nwarps);
   if (nt > MAX_OUT_TILES || nslices > MAX_SLICES) return fail(c, PSVD_EINVAL, "panel too wide (%d tiles)", nt);
   ps.p.nslices = nslices;

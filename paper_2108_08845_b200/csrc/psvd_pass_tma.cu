@@ -34,6 +34,7 @@ namespace {
 constexpr int TKS = 16;       // rows per stage = one 128-byte swizzled column
 constexpr int TNS_MAX = 8;    // ring depth: x.ns stages of 16 rows (as many as fit, 3 .. 8)
 constexpr int YMAXC = 32;     // widest Y of the narrow pass (4 column blocks)
+constexpr int YKP_WR = 16;    // W fragments held in registers per Y warp (k steps of 4 columns)
 constexpr int YB = 2;         // Y ring depth (Y warps run up to YB stages ahead of the Gram warps; 4 measured no faster)
 constexpr int PROD_WARP = NWARP - 1;
 // sW row stride (doubles, = 4 mod 16: 2 wavefronts per B-fragment load), sized by the Y width
@@ -119,6 +120,10 @@ __global__ void __launch_bounds__(NTHR, 1)
   const int nyo = 2 * ncb;       // Y output blocks (2 row blocks of 8 x ncb) per 16-row block
   // 32-row stages: the two 16-row halves of a block go to one warp (yh = 1) or to two (yh = 2)
   const int yh = (RB == 2 && p.yh == 2) ? 2 : 1;
+  // 32-row stages, register-resident W: Y warp (cb, kp) holds the W fragments of its k part and
+  // forms all 32 rows of column block cb over that part; the ykp partials meet in the Y tile in
+  // part order through a chain of mbarriers
+  const int ykp = (RB == 2 && p.ykp > 1) ? p.ykp : 1;
 
   unsigned char* base = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
   double* sP = reinterpret_cast<double*>(base);
@@ -133,8 +138,9 @@ __global__ void __launch_bounds__(NTHR, 1)
   uint64_t* yfree = ydone + YB;
   double* cmx = reinterpret_cast<double*>(bars + 64);  // [2 rb][32 cols][val, abs, row]
 
+  uint64_t* chain = bars + 24;  // [YB][4 cb][3 links] (ykp > 1)
   int ngram = 0;
-  const int ny = nyo * yh;  // Y warps 0 .. ny-1
+  const int ny = ykp > 1 ? ncb * ykp : nyo * yh;  // Y warps 0 .. ny-1
   for (int w = ny; w < PROD_WARP; ++w) ngram += p.plan[slice][w].ntile > 0;
 
   // one-time setup: zero the panel columns no TMA box writes (alignment gaps), the Y
@@ -176,9 +182,11 @@ __global__ void __launch_bounds__(NTHR, 1)
       mbar_init(&empty[b], (unsigned)(ny + ngram));
     }
     for (int b = 0; b < YB; ++b) {
-      mbar_init(&ydone[b], 32u * ny);
+      mbar_init(&ydone[b], 32u * (ykp > 1 ? ncb : ny));
       mbar_init(&yfree[b], (unsigned)max(32 * ngram, 1));
     }
+    if (ykp > 1)
+      for (int i = 0; i < YB * 4 * 3; ++i) mbar_init(&chain[i], 32u);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // zero fills before the first TMA writes
@@ -210,6 +218,109 @@ __global__ void __launch_bounds__(NTHR, 1)
             else  // rows r0 .. r0 + SR - 1 of every column: SR * 8 contiguous bytes per column
               tma_load_3d(dst, &maps.m[x.op_seg[o]], 0, r0 / TKS, x.op_col[o], &full[b]);
           }
+      }
+    }
+    return;
+  }
+
+  if (RB == 2 && ykp > 1 && warp < ny) {
+    // ---------------------------------------------------------------- Y warps, W in registers
+    const int cb = warp % ncb, kp = warp / ncb;
+    const int n4 = kspan >> 2;  // k steps of 4 columns (kp span is a multiple of 4)
+    const int j0 = n4 * kp / ykp, nj = n4 * (kp + 1) / ykp - j0;  // nj <= YKP_WR (host-checked)
+    double wr[YKP_WR];
+#pragma unroll
+    for (int j = 0; j < YKP_WR; ++j)
+      wr[j] = j < nj ? sW[(size_t)(4 * (j0 + j) + tq) * WSP + cb * 8 + g] : 0.0;
+    const bool last = kp == ykp - 1;
+    const bool do_y = slice == 0 && last;
+    double cm_val[2] = {0.0, 0.0}, cm_abs[2] = {-1.0, -1.0};
+    int64_t cm_row[2] = {-1, -1};
+    int b = 0;
+    unsigned ph = 0;
+    for (int64_t s = 0; s < nstage; ++s, (++b == TNS ? (b = 0, ph ^= 1u) : 0u)) {
+      const int yb = (int)(s & (YB - 1));
+      const unsigned yph = (unsigned)(((int)s / YB) & 1);
+      mbar_wait(&full[b], ph);
+      const double* P = sP + (size_t)b * pw * SR;
+      // 4 row blocks of 8 (q = 2 h + rb), 4 independent accumulator chains; column c of step j is
+      // unit 2c + h, phase (2 (k0 + tq) + h) & 7: conflict-free across tq
+      double acc[4][2];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
+      const int cbase = x.kp_lo + 4 * j0 + tq;
+#pragma unroll
+      for (int j = 0; j < YKP_WR; ++j) {
+        if (j < nj && p.dbg != 1) {
+          const int c = cbase + 4 * j;
+          double a[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) a[q] = P[swzr<2>(c, (q >> 1) * 16 + (q & 1) * 8 + g)];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dmma884(acc[q][0], acc[q][1], a[q], wr[j]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[b]);  // panel slot no longer read by this warp
+      double* Ys = sY + (size_t)yb * YC * SR;
+      const int o0 = cb * 8 + 2 * tq;
+      if (kp == 0) {
+        if (s >= YB && ngram > 0) mbar_wait(&yfree[yb], yph ^ 1u);
+      } else {
+        mbar_wait(&chain[(yb * 4 + cb) * 3 + kp - 1], yph);  // the partial sum of parts 0 .. kp-1
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = (q >> 1) * 16 + (q & 1) * 8 + g;
+          acc[q][0] = Ys[swzr<2>(o0, r)] + acc[q][0];
+          acc[q][1] = Ys[swzr<2>(o0 + 1, r)] + acc[q][1];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = (q >> 1) * 16 + (q & 1) * 8 + g;
+        Ys[swzr<2>(o0, r)] = acc[q][0];
+        Ys[swzr<2>(o0 + 1, r)] = acc[q][1];
+      }
+      if (!last) {
+        mbar_arrive(&chain[(yb * 4 + cb) * 3 + kp]);
+        continue;
+      }
+      mbar_arrive(&ydone[yb]);
+      if (do_y) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // q = 2 h + rb: rows 8 q + g, increasing (first occurrence kept)
+          const int64_t row = row_begin + s * SR + 8 * q + g;
+          const double y0 = acc[q][0], y1 = acc[q][1];
+          if (row >= row_end) continue;
+          if (p.Yout != nullptr) {
+            if (o0 < p.w) p.Yout[(int64_t)o0 * p.ldy + row] = y0;
+            if (o0 + 1 < p.w) p.Yout[(int64_t)(o0 + 1) * p.ldy + row] = y1;
+          }
+          if (p.colmax != nullptr) {
+            if (fabs(y0) > cm_abs[0]) { cm_abs[0] = fabs(y0); cm_val[0] = y0; cm_row[0] = row; }
+            if (fabs(y1) > cm_abs[1]) { cm_abs[1] = fabs(y1); cm_val[1] = y1; cm_row[1] = row; }
+          }
+        }
+      }
+    }
+    if (do_y && p.colmax != nullptr) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+#pragma unroll
+        for (int off = 4; off < 32; off <<= 1) {
+          const double oa = __shfl_xor_sync(0xffffffffu, cm_abs[e], off);
+          const double ov = __shfl_xor_sync(0xffffffffu, cm_val[e], off);
+          const long long orow = __shfl_xor_sync(0xffffffffu, (long long)cm_row[e], off);
+          if (oa > cm_abs[e] || (oa == cm_abs[e] && orow >= 0 && (cm_row[e] < 0 || orow < cm_row[e]))) {
+            cm_abs[e] = oa; cm_val[e] = ov; cm_row[e] = orow;
+          }
+        }
+        const int o = cb * 8 + 2 * tq + e;
+        if (g == 0 && o < p.w) {
+          double* dst = p.colmax + ((size_t)chunk * p.w + o) * 2;
+          dst[0] = cm_val[e];
+          dst[1] = (double)cm_row[e] + (double)p.row_offset;
+        }
       }
     }
     return;
@@ -724,6 +835,10 @@ int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift, bool
     x.stage_bytes = 2 * bytes;
   }
   if (x.rb != 2) p.yh = 1;  // 16-row stages: the second half-warps of the plan stay idle
+  if (p.ykp > 1 && (x.rb != 2 || ((x.kp_hi - x.kp_lo) / 4 + p.ykp - 1) / p.ykp > YKP_WR)) {
+    p.ykp = 1;  // the plan's Y warps 0 .. 2 ncb - 1 then run the fragment-reloading path
+    p.yh = 1;
+  }
   // ring depth: as many stages as shared memory holds (3 .. TNS_MAX; 2 .. for 32-row stages)
   x.ns = x.rb == 2 ? 2 : 3;
   while (x.ns < TNS_MAX &&
