@@ -226,8 +226,9 @@ __global__ void __launch_bounds__(NTHR, 1)
   if (RB == 2 && ykp > 1 && warp < ny) {
     // ---------------------------------------------------------------- Y warps, W in registers
     const int cb = warp % ncb, kp = warp / ncb;
-    const int n4 = kspan >> 2;  // k steps of 4 columns (kp span is a multiple of 4)
-    const int j0 = n4 * kp / ykp, nj = n4 * (kp + 1) / ykp - j0;  // nj <= YKP_WR (host-checked)
+    // k steps of 4 columns of this part: sized on the host so that every SMSP carries the same
+    // DMMA count per stage, its Gram tiles included (nj <= YKP_WR)
+    const int j0 = p.ykj0[warp], nj = p.yknj[warp];
     double wr[YKP_WR];
 #pragma unroll
     for (int j = 0; j < YKP_WR; ++j)
@@ -838,6 +839,49 @@ int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift, bool
   if (p.ykp > 1 && (x.rb != 2 || ((x.kp_hi - x.kp_lo) / 4 + p.ykp - 1) / p.ykp > YKP_WR)) {
     p.ykp = 1;  // the plan's Y warps 0 .. 2 ncb - 1 then run the fragment-reloading path
     p.yh = 1;
+  }
+  if (p.ykp > 1) {
+    // split each column block's k steps over its ykp parts in proportion to what the parts'
+    // SMSPs (warp w issues on SMSP w % 4) have left after their Gram tiles: a Y step is 4
+    // DMMAs per stage (4 row blocks), a Gram tile na x nb DMMAs per 4 rows
+    const int n4 = (x.kp_hi - x.kp_lo) / 4, ncb = p.w_pad / 8, ny = ncb * p.ykp;
+    double gload[4] = {0.0, 0.0, 0.0, 0.0};  // Gram DMMAs per 32-row stage per SMSP (slice 0 stands for all)
+    for (int w = ny; w < NWARP - 1; ++w) {
+      const WarpPlan& wp = p.plan[0][w];
+      if (wp.ntile == 0) continue;
+      const int I = wp.ti[0];
+      const int na = I * 32 >= p.np_pad ? ncb : std::min(4, (p.np - I * 32 + 7) / 8);
+      gload[w % 4] += (double)na * ncb * (2 * TKS / 4);
+    }
+    int ywarps[4] = {0, 0, 0, 0};
+    for (int v = 0; v < ny; ++v) ywarps[v % 4]++;
+    const double share = (gload[0] + gload[1] + gload[2] + gload[3] + 4.0 * n4 * ncb) / 4.0;
+    for (int cb = 0; cb < ncb; ++cb) {
+      // part kp's weight: what its SMSP has left of the even share after the Gram tiles, split
+      // over the Y warps issuing there (a Y step is 4 DMMAs per stage)
+      double wgt[4], sum = 0.0;
+      for (int kp = 0; kp < p.ykp; ++kp) {
+        const int q = (cb + ncb * kp) % 4;
+        wgt[kp] = std::max(1.0, (share - gload[q]) / std::max(1, ywarps[q]));
+        sum += wgt[kp];
+      }
+      int j = 0;
+      for (int kp = 0; kp < p.ykp; ++kp) {
+        const int w = cb + ncb * kp;
+        int nj = kp == p.ykp - 1 ? n4 - j : (int)(n4 * wgt[kp] / sum + 0.5);
+        nj = std::max(0, std::min(nj, std::min(YKP_WR, n4 - j)));
+        p.ykj0[w] = (unsigned char)j;
+        p.yknj[w] = (unsigned char)nj;
+        j += nj;
+      }
+      if (j != n4 || p.yknj[cb + ncb * (p.ykp - 1)] > YKP_WR) {  // fall back to the even split
+        for (int kp = 0; kp < p.ykp; ++kp) {
+          const int w = cb + ncb * kp;
+          p.ykj0[w] = (unsigned char)(n4 * kp / p.ykp);
+          p.yknj[w] = (unsigned char)(n4 * (kp + 1) / p.ykp - n4 * kp / p.ykp);
+        }
+      }
+    }
   }
   // ring depth: as many stages as shared memory holds (3 .. TNS_MAX; 2 .. for 32-row stages)
   x.ns = x.rb == 2 ? 2 : 3;

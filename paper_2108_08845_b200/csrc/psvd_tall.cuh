@@ -65,6 +65,7 @@ struct TallParams {
   int nslices;
   int yh;                // narrow TMA pass with 32-row stages: 2 = one Y warp per 16-row half of a block
   int ykp;               // narrow TMA pass with 32-row stages: > 1 = W in registers, k split into ykp parts
+  unsigned char ykj0[NWARP], yknj[NWARP];  // per Y warp: first k step and step count of its part
   WarpPlan plan[MAX_SLICES][NWARP];
   double* partial;       // [grid][SLOTS][1024]
   double* colmax;        // optional [grid][w][2] = (signed value at max |y|, global row)
