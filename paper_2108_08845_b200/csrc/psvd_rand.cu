@@ -4,6 +4,7 @@
 #include <cfloat>
 #include <cstdio>
 #include <algorithm>
+#include <cstdlib>
 
 #include "psvd_small.cuh"
 
@@ -251,7 +252,70 @@ __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restr
   }
 }
 
+// The same factorization for l <= 32 on one warp (lane j owns column j of R and of R^-1; row-major
+// shared copies with a 33-double stride): same operations in the same order as chol_inv_kernel,
+// without its 3 CTA barriers per column and single-thread columns of the inverse.
+__global__ void __launch_bounds__(32, 1) chol_inv_warp_kernel(const double* __restrict__ G, int l,
+                                                               double* __restrict__ T, int* __restrict__ illcond,
+                                                               int* __restrict__ status, double* __restrict__ Rout) {
+  __shared__ double R[32 * 33];
+  __shared__ double X[32 * 33];
+  const int lane = threadIdx.x;
+  const bool mine = lane < l;
+  double dmax = 0.0;
+  bool finite = true;
+  for (int i = 0; i < l; ++i) {  // identical scan order to chol_inv_kernel's
+    const double g = G[(size_t)i * l + i];
+    finite = finite && isfinite(g);
+    dmax = fmax(dmax, g);
+  }
+  if (!finite && status != nullptr && lane == 0) atomicOr(status, PSVD_ST_NONFINITE);
+  const double tiny = 64.0 * DBL_EPSILON * dmax;
+  if (mine)
+    for (int i = 0; i < l; ++i) R[i * 33 + lane] = G[(size_t)lane * l + i];  // R[i][j] = G(i, j)
+  __syncwarp();
+  for (int k = 0; k < l; ++k) {
+    const double piv = R[k * 33 + k];
+    const bool ok = piv > tiny;
+    const double rk = ok ? sqrt(piv) : 0.0;
+    __syncwarp();
+    if (mine && lane >= k) R[k * 33 + lane] = ok ? (lane == k ? rk : R[k * 33 + lane] / rk) : 0.0;
+    __syncwarp();
+    if (mine) {
+      const double rkj = R[k * 33 + lane];
+      for (int i = k + 1; i <= lane; ++i) R[i * 33 + lane] -= R[k * 33 + i] * rkj;
+    }
+    __syncwarp();
+  }
+  if (mine) {
+    const int j = lane;
+    for (int i = l - 1; i >= 0; --i) {
+      double v = (i == j) ? 1.0 : 0.0;
+      for (int q = i + 1; q <= j; ++q) v -= R[i * 33 + q] * X[q * 33 + j];
+      const double d = R[i * 33 + i];
+      X[i * 33 + j] = (i <= j && d != 0.0) ? v / d : 0.0;
+    }
+    for (int i = 0; i < l; ++i) T[(size_t)j * l + i] = X[i * 33 + j];
+    if (Rout != nullptr)
+      for (int i = 0; i < l; ++i) Rout[(size_t)j * l + i] = i <= j ? R[i * 33 + j] : 0.0;
+  }
+  if (illcond != nullptr && lane == 0) {
+    double rmax = 0.0, rmin = DBL_MAX;
+    for (int i = 0; i < l; ++i) {
+      const double d = R[i * 33 + i];
+      rmax = fmax(rmax, d);
+      rmin = fmin(rmin, d);
+    }
+    *illcond = !(rmin > 0.0 && rmax <= 1e6 * rmin);
+  }
+}
+
 void launch_chol_inv(const double* G, int l, double* T, cudaStream_t st, int* illcond, int* status, double* Rout) {
+  static const bool no_warp = getenv("PSVD_NO_WARP_CHOL") != nullptr;
+  if (l <= 32 && !no_warp) {
+    chol_inv_warp_kernel<<<1, 32, 0, st>>>(G, l, T, illcond, status, Rout);
+    return;
+  }
   const size_t smem = 2 * (size_t)l * l * sizeof(double);
   cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   chol_inv_kernel<<<1, 1024, smem, st>>>(G, l, T, illcond, status, Rout);
