@@ -13,7 +13,9 @@ from .dsvd import (LocalModes, RankContext, gather_modes, parallel_qr, parallel_
                    parallel_stream_incorporate, parallel_stream_initialize)
 from .errors import (CapacityError, CollectiveTimeout, ConvergenceError, DegenerateModeError,  # noqa: F401
                      MatrixFormatError)
-from .io import BatchSource, read_batches, read_matrix, read_matrix_header, read_submatrix, write_matrix  # noqa: F401
+from .io import (BatchSource, read_batches, read_matrix, read_matrix_header, read_modes_csv,  # noqa: F401
+                 read_singular_values_csv, read_submatrix, write_history_csv, write_matrix, write_mode_svg,
+                 write_modes_csv, write_singular_values_csv)
 from .linalg import (QrResult, RandomSketchConfig, SvdResult, aligned_mode_difference, low_rank_svd,  # noqa: F401
                      qr_factor, randomized_range, subspace_angles, svd_full)
 from .streaming import StreamConfig, StreamState, stream_all, stream_incorporate, stream_initialize  # noqa: F401

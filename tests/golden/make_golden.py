@@ -168,12 +168,35 @@ def main():
     write_matrix(os.path.join(OUT, "sample_37x11.parsvd"), rng.standard_normal((37, 11)))
     print("wrote sample_37x11.parsvd")
 
+    outputs()
+
     with open(os.path.join(OUT, "PROVENANCE.txt"), "w") as f:
         f.write("generated by tests/golden/make_golden.py from the live reference parsvd "
                 f"{parsvd.__version__} at {REF_SRC}\n")
         f.write(f"numpy {np.__version__}; BLAS pinned to 1 thread (threadpoolctl)\n")
 
 
+def outputs():
+    """G9: the reference's text emitters (io.py:156-270) on seeded inputs: sigma / modes /
+    history CSV (17 significant digits) and the mode SVG, byte for byte."""
+    sys.path.insert(0, REF_SRC)
+    from parsvd.io import write_history_csv, write_mode_svg, write_modes_csv, write_singular_values_csv
+    rng = np.random.Generator(np.random.Philox(78))
+    grid = np.linspace(0.0, 1.0, 33)
+    modes = rng.standard_normal((33, 4))
+    sigma = np.sort(np.abs(rng.standard_normal(6)))[::-1] * 1e3
+    hist = np.abs(rng.standard_normal((5, 3)))
+    write_singular_values_csv(os.path.join(OUT, "out_sigma.csv"), sigma)
+    write_modes_csv(os.path.join(OUT, "out_modes.csv"), grid, modes)
+    write_history_csv(os.path.join(OUT, "out_history.csv"), hist)
+    write_mode_svg(os.path.join(OUT, "out_modes.svg"), grid, modes[:, :3])
+    write_mode_svg(os.path.join(OUT, "out_flat.svg"), np.arange(5.0), np.ones((5, 2)))
+    print("wrote out_sigma.csv out_modes.csv out_history.csv out_modes.svg out_flat.svg")
+
+
 if __name__ == "__main__":
     with threadpool_limits(1):
-        main()
+        if len(sys.argv) > 1 and sys.argv[1] == "--outputs-only":
+            outputs()
+        else:
+            main()

@@ -75,13 +75,13 @@ REFERENCE_PUBLIC = {
     "BurgersConfig", "burgers_matrix", "burgers_solution", "partition_bounds", "row_partition",
     "synthetic_spectrum_matrix",
     "BatchSource", "read_batches", "read_matrix", "read_matrix_header", "read_submatrix", "write_matrix",
+    "write_mode_svg", "write_modes_csv", "write_singular_values_csv",
     "CapacityError", "CollectiveTimeout", "ConvergenceError", "DegenerateModeError", "MatrixFormatError",
 }
-# out of scope by SURVEY §8(f) / DESIGN §7: the TCP / simulated transports of comm.py, the CSV/SVG
-# emitters of io.py, and the errors only those raise
-OUT_OF_SCOPE = {"CommStats", "RankContext_tcp", "SimTransport", "TcpTransport", "broadcast", "decode_matrix",
-                "encode_matrix", "gather", "recv", "run_simulated", "send", "tcp_context_from_env",
-                "write_mode_svg", "write_modes_csv", "write_singular_values_csv", "ConfigError", "ProtocolError"}
+# out of scope by SURVEY §8(f) / DESIGN §7: the TCP / simulated transports of comm.py and the errors
+# only those raise (torch.distributed is the transport here)
+OUT_OF_SCOPE = {"CommStats", "SimTransport", "TcpTransport", "broadcast", "decode_matrix", "encode_matrix", "gather",
+                "recv", "run_simulated", "send", "tcp_context_from_env", "ConfigError", "ProtocolError"}
 
 
 def test_public_api_covers_the_reference_hot_path_names():

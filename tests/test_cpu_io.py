@@ -58,3 +58,34 @@ def test_format_errors(tmp_path):
         pio.read_submatrix(p, 0, 37, 0, 11)
     with pytest.raises(ValueError):
         pio.write_matrix(tmp_path / "nan", np.array([[np.nan]]))
+
+
+def test_text_emitters_match_reference_bytes(tmp_path):
+    """io.py:156-270: sigma / modes / history CSV and the mode SVG, byte for byte against files
+    the live reference wrote (tests/golden/make_golden.py outputs()), and their readers."""
+    g = os.path.join(os.path.dirname(__file__), "golden")
+    rng = np.random.Generator(np.random.Philox(78))
+    grid = np.linspace(0.0, 1.0, 33)
+    modes = rng.standard_normal((33, 4))
+    sigma = np.sort(np.abs(rng.standard_normal(6)))[::-1] * 1e3
+    hist = np.abs(rng.standard_normal((5, 3)))
+    cases = [("out_sigma.csv", lambda p: pio.write_singular_values_csv(p, sigma)),
+             ("out_modes.csv", lambda p: pio.write_modes_csv(p, grid, modes)),
+             ("out_history.csv", lambda p: pio.write_history_csv(p, hist)),
+             ("out_modes.svg", lambda p: pio.write_mode_svg(p, grid, modes[:, :3])),
+             ("out_flat.svg", lambda p: pio.write_mode_svg(p, np.arange(5.0), np.ones((5, 2))))]
+    for name, write in cases:
+        out = tmp_path / name
+        write(out)
+        assert out.read_bytes() == open(os.path.join(g, name), "rb").read(), name
+    assert np.array_equal(pio.read_singular_values_csv(os.path.join(g, "out_sigma.csv")), sigma)
+    gb, mb = pio.read_modes_csv(os.path.join(g, "out_modes.csv"))
+    assert np.array_equal(gb, grid) and np.array_equal(mb, modes)
+    with pytest.raises(ValueError):
+        pio.write_modes_csv(tmp_path / "x.csv", np.zeros(3), np.zeros((4, 2)))
+    junk = tmp_path / "junk.csv"
+    junk.write_text("time,value\n0,1\n")
+    with pytest.raises(MatrixFormatError):
+        pio.read_singular_values_csv(junk)
+    with pytest.raises(MatrixFormatError):
+        pio.read_modes_csv(junk)
