@@ -368,6 +368,27 @@ def test_pipelined_randomized_run_matches_per_update_and_oracle(q):
         assert oracle.sigma_rel_err(h.cpu().numpy(), rh) <= SIG_TOL
 
 
+@pytest.mark.parametrize("rows,b,k,p_,q", [(37, 12, 3, 2, 1), (1000, 20, 10, 0, 0), (4097, 64, 16, 16, 2),
+                                          (65536, 200, 1, 1, 1), (24576, 100, 12, 20, 0)])
+def test_pipelined_randomized_run_edge_shapes(rows, b, k, p_, q):
+    """The pipelined randomized run at its edges: tiny and odd row counts (16-row TMA stages),
+    no oversampling, the widest sketch (l = 32), K = 1, rows a multiple of 16 (32-row stages,
+    register-resident W): against the oracle per step."""
+    p = _pkg()
+    a = np.random.default_rng(rows + b).standard_normal((rows, 4 * b)) * np.linspace(2.0, 0.1, 4 * b)
+    bs = _batches(a, b)
+    sk = p.RandomSketchConfig(target_rank=k, oversampling=p_, power_iterations=q, seed=11)
+    st, hist = p.stream_all(bs, p.StreamConfig(k_modes=k, forget_factor=0.9, batch_columns=b, sketch=sk))
+    rm, rs, rh = oracle.ref_rand_stream_all(bs, k, 0.9, p_, q, 11)
+    m, s_ = _np(st)
+    for h, r_ in zip(hist, rh):
+        assert oracle.sigma_rel_err(h.cpu().numpy(), r_) <= SIG_TOL
+    gaps = np.minimum(np.abs(np.diff(np.r_[np.inf, rs])), np.abs(np.diff(np.r_[rs, 0.0]))) / rs
+    sep = gaps > 1e-3  # sine angles are only defined for separated modes
+    assert oracle.sigma_rel_err(s_, rs) <= SIG_TOL
+    assert np.max(oracle.mode_angles(m[:, sep], rm[:, sep]), initial=0.0) <= ANG_TOL
+
+
 def test_pipelined_randomized_run_bitwise_and_validation():
     p = _pkg()
     a = oracle.burgers_matrix(4096, 800)[:, :400]
