@@ -2,14 +2,17 @@
 
 import os
 import subprocess
+import tempfile
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libpsvd.so")
-SOURCES = ["psvd_tall.cu", "psvd_pass_tma.cu", "psvd_gemm.cu", "psvd_small.cu", "psvd_subspace.cu", "psvd_rand.cu", "psvd_api.cu"]
+SOURCES = ["psvd_tall.cu", "psvd_pass_tma.cu", "psvd_gemm.cu", "psvd_small.cu", "psvd_subspace.cu", "psvd_rand.cu",
+           "psvd_api.cu", "psvd_stream.cu", "psvd_rand_api.cu", "psvd_dense.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared"]
+              "-Xcompiler", "-fPIC"]
 
 
 def nvcc():
@@ -31,10 +34,22 @@ def build(force=False, verbose=False):
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
     tmp = LIB + ".tmp"
-    cmd = [nvcc()] + NVCC_FLAGS + [os.path.join(CSRC, s) for s in SOURCES] + ["-o", tmp]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.run(cmd, check=True, cwd=CSRC)
+    with tempfile.TemporaryDirectory(prefix="psvd_build_") as obj:
+        # one nvcc per translation unit, in parallel; then one link
+        cmds = [[nvcc()] + NVCC_FLAGS + ["-c", os.path.join(CSRC, s), "-o", os.path.join(obj, s + ".o")]
+                for s in SOURCES]
+        link = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a"] + \
+            [c[-1] for c in cmds] + ["-o", tmp]
+
+        def run(cmd):
+            if verbose:
+                print(" ".join(cmd), flush=True)
+            subprocess.run(cmd, check=True, cwd=CSRC)
+
+        with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+            for f in [ex.submit(run, c) for c in cmds]:
+                f.result()
+        run(link)
     os.replace(tmp, LIB)
     return LIB
 
