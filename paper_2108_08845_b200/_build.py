@@ -29,15 +29,17 @@ def needs_build():
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_build():
+def build(force=False, verbose=False, defines=(), variant=None):
+    """defines: extra -D flags; variant: build lib/libpsvd.<variant>.so instead (A/B timing)."""
+    out = LIB if variant is None else os.path.join(LIBDIR, "libpsvd." + variant + ".so")
+    if variant is None and not force and not needs_build():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
-    tmp = LIB + ".tmp"
+    tmp = out + ".tmp"
     with tempfile.TemporaryDirectory(prefix="psvd_build_") as obj:
         # one nvcc per translation unit, in parallel; then one link
-        cmds = [[nvcc()] + NVCC_FLAGS + ["-c", os.path.join(CSRC, s), "-o", os.path.join(obj, s + ".o")]
-                for s in SOURCES]
+        cmds = [[nvcc()] + NVCC_FLAGS + ["-D" + d for d in defines] +
+                ["-c", os.path.join(CSRC, s), "-o", os.path.join(obj, s + ".o")] for s in SOURCES]
         link = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a"] + \
             [c[-1] for c in cmds] + ["-o", tmp]
 
@@ -50,9 +52,14 @@ def build(force=False, verbose=False):
             for f in [ex.submit(run, c) for c in cmds]:
                 f.result()
         run(link)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose=True))
+    import sys
+    # python -m paper_2108_08845_b200._build [VARIANT NAME=VALUE ...]
+    if len(sys.argv) > 1:
+        print(build(verbose=True, variant=sys.argv[1], defines=sys.argv[2:]))
+    else:
+        print(build(force=True, verbose=True))

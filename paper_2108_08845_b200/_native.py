@@ -20,6 +20,8 @@ from .errors import ConvergenceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libpsvd.so")
+if os.environ.get("PSVD_LIB_VARIANT"):  # diagnostics: an in-tree build variant (tools/, A/B timing)
+    LIB_PATH = os.path.join(_HERE, "lib", "libpsvd." + os.environ["PSVD_LIB_VARIANT"] + ".so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "psvd.h")
 
 PSVD_OK, PSVD_EINVAL, PSVD_ENOCONV, PSVD_ECUDA = 0, 1, 2, 3

@@ -171,7 +171,8 @@ int plan_tiles_balanced(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, 
 }
 
 // TMA pass: tiles on the Gram warps (after the 2*ncb Y warps), one tile each, no k-split.
-int plan_tiles_tma(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& tiles) {
+int plan_tiles_tma(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& tiles,
+                   const std::vector<unsigned char>& sub) {
   const int nt = (int)tiles.size();
   memset(ps.p.plan, 0, sizeof(ps.p.plan));
   memset(&ps.map, 0, sizeof(ps.map));
@@ -201,14 +202,63 @@ int plan_tiles_tma(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>
   ps.p.nslices = nslices;
   ps.map.nout = nt;
   const int per = (nt + nslices - 1) / nslices;
+  // warp of each tile: in order, or (one slice, register-W Y warps) longest-first onto the SMSP
+  // (warp % 4) with the least Gram work so far -- the Y parts' k split then evens the SMSPs out
+  std::vector<int> warp_of(nt);
+  for (int o = 0; o < nt; ++o) warp_of[o] = warp0 + o % per;
+  static const bool no_lpt = getenv("PSVD_TMA_NO_LPT") != nullptr;  // diagnostics: tiles in order
+  if (nslices == 1 && ykp > 1 && !no_lpt) {
+    const int NBp = ps.p.np_pad / 32;
+    std::vector<int> cost(nt), order(nt);
+    for (int o = 0; o < nt; ++o) {
+      const int I = tiles[o].first;
+      const int na = I >= NBp ? ncb : sub[o] ? (sub[o] >> 4) : std::min(4, (ps.p.np - I * 32 + 7) / 8);
+      cost[o] = na * ncb;
+      order[o] = o;
+    }
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    int load[4] = {0, 0, 0, 0};
+    std::vector<char> used(NWARP, 0);
+    for (int o : order) {
+      int best = -1;
+      for (int w = warp0; w < warp0 + nwarps; ++w)
+        if (!used[w] && (best < 0 || load[w % 4] < load[best % 4])) best = w;
+      used[best] = 1;
+      load[best % 4] += cost[o];
+      warp_of[o] = best;
+    }
+    // pairwise swaps across SMSPs while they lower the busiest SMSP (then the spread)
+    auto score = [&](const int* L) {
+      int mx = 0, sq = 0;
+      for (int q = 0; q < 4; ++q) mx = std::max(mx, L[q]), sq += L[q] * L[q];
+      return std::make_pair(mx, sq);
+    };
+    for (bool improved = true; improved;) {
+      improved = false;
+      for (int a = 0; a < nt && !improved; ++a)
+        for (int b = a + 1; b < nt && !improved; ++b) {
+          const int qa = warp_of[a] % 4, qb = warp_of[b] % 4;
+          if (qa == qb || cost[a] == cost[b]) continue;
+          int L[4] = {load[0], load[1], load[2], load[3]};
+          L[qa] += cost[b] - cost[a];
+          L[qb] += cost[a] - cost[b];
+          if (score(L) < score(load)) {
+            std::swap(warp_of[a], warp_of[b]);
+            for (int q = 0; q < 4; ++q) load[q] = L[q];
+            improved = true;
+          }
+        }
+    }
+  }
   for (int o = 0; o < nt; ++o) {
-    const int sl = o / per, w = warp0 + o % per;
+    const int sl = o / per, w = warp_of[o];
     WarpPlan& wp = ps.p.plan[sl][w];
     wp.ksplit = 1;
     wp.kpart = 0;
     wp.ti[0] = (signed char)tiles[o].first;
     wp.tj[0] = (signed char)tiles[o].second;
     wp.ntile = 1;
+    wp.sub = sub[o];
     ps.map.src[o][ps.map.nsrc[o]++] = (unsigned char)(sl * SLOTS + w * TPW);
     ps.map.out_id[o] = (short)(tiles[o].first * ps.NB + tiles[o].second);
   }
@@ -327,7 +377,29 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
   }
   ps.tma = tma;
   if (tma) p.narrow = 1;
-  int rc = tma ? plan_tiles_tma(c, ps, tiles)
+  // narrow TMA pass: P-tiles compute only the 8-column sub-blocks that hold wanted rows, the
+  // columns of segments not flagged "no P^T Y" (col0 == 2 on input) inside [py_lo block, py_cols)
+  std::vector<unsigned char> sub(tiles.size(), 0);
+  if (tma && gram_py) {
+    std::vector<char> want((size_t)np_pad / 8, 0);
+    const int lo = py_lo * 32, hi = py_cols < 0 ? np_pad : std::min(np_pad, py_cols);
+    for (size_t i = 0; i < segs.size(); ++i) {
+      if (segs[i].col0 == 2) continue;
+      const int c0 = std::max(lo, p.seg[i].col0), c1 = std::min(hi, p.seg[i].col0 + p.seg[i].ncols);
+      for (int sb = c0 / 8; sb * 8 < c1; ++sb) want[sb] = 1;
+    }
+    for (size_t o = 0; o < tiles.size(); ++o) {
+      if (tiles[o].first >= NBp) continue;
+      int a0 = -1, a1 = -1;
+      for (int a = 0; a < 4; ++a)
+        if (want[(size_t)tiles[o].first * 4 + a]) {
+          if (a0 < 0) a0 = a;
+          a1 = a;
+        }
+      if (a0 >= 0) sub[o] = (unsigned char)(a0 | ((a1 - a0 + 1) << 4));
+    }
+  }
+  int rc = tma ? plan_tiles_tma(c, ps, tiles, sub)
                : ps.gtma ? plan_tiles_balanced(c, ps, tiles, np, TMA_GRAM_CONS)
                : ps.ws ? plan_tiles_balanced(c, ps, tiles, np) : plan_tiles(c, ps, tiles, w == 0);
   {

@@ -21,6 +21,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -33,7 +34,10 @@ namespace {
 
 constexpr int TKS = 16;       // rows per stage = one 128-byte swizzled column
 constexpr int TNS_MAX = 8;    // ring depth: x.ns stages of 16 rows (as many as fit, 3 .. 8)
-constexpr int YMAXC = 32;     // widest Y of the narrow pass (4 column blocks)
+constexpr int YMAXC = 32;
+#ifndef PSVD_PRE_MAX
+#define PSVD_PRE_MAX 42  // Gram warps of the narrow pass: register budget (doubles) of the early release
+#endif     // widest Y of the narrow pass (4 column blocks)
 constexpr int YKP_WR = 16;    // W fragments held in registers per Y warp (k steps of 4 columns)
 constexpr int YB = 2;         // Y ring depth (Y warps run up to YB stages ahead of the Gram warps; 4 measured no faster)
 constexpr int PROD_WARP = NWARP - 1;
@@ -479,8 +483,10 @@ __global__ void __launch_bounds__(NTHR, 1)
   if (wp.ntile == 0) return;
   const int I = wp.ti[0];
   const bool i_is_y = I * 32 >= np_pad;
-  const int na = i_is_y ? ncb : min(4, (p.np - I * 32 + 7) / 8);
-  const int acol = I * 32 + x.pshift;  // physical first column of a panel tile
+  // P-tile: the wanted 8-column sub-blocks a0 .. a0 + na - 1 (plan_pass trims unwanted rows)
+  const int a0 = (!i_is_y && wp.sub != 0) ? (wp.sub & 15) : 0;
+  const int na = i_is_y ? ncb : wp.sub != 0 ? (wp.sub >> 4) : min(4, (p.np - I * 32 + 7) / 8);
+  const int acol = I * 32 + x.pshift + a0 * 8;  // physical first column of a panel tile
   double acc[4][4][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
@@ -534,8 +540,14 @@ __global__ void __launch_bounds__(NTHR, 1)
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int c = 0; c < 4; ++c)
-      *reinterpret_cast<double2*>(dst + (a * 8 + g) * 32 + c * 8 + 2 * tq) = make_double2(acc[a][c][0], acc[a][c][1]);
+    for (int c = 0; c < 4; ++c) {
+      // accumulator a holds sub-block a0 + a: rows outside the computed range are zero
+      double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+      for (int s = 0; s < 4; ++s)
+        if (s + a0 == a) v0 = acc[s][c][0], v1 = acc[s][c][1];
+      *reinterpret_cast<double2*>(dst + (a * 8 + g) * 32 + c * 8 + 2 * tq) = make_double2(v0, v1);
+    }
 }
 
 // ---------------------------------------------------------------- TMA Gram (w == 0)
@@ -850,7 +862,7 @@ int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift, bool
       const WarpPlan& wp = p.plan[0][w];
       if (wp.ntile == 0) continue;
       const int I = wp.ti[0];
-      const int na = I * 32 >= p.np_pad ? ncb : std::min(4, (p.np - I * 32 + 7) / 8);
+      const int na = I * 32 >= p.np_pad ? ncb : wp.sub != 0 ? (wp.sub >> 4) : std::min(4, (p.np - I * 32 + 7) / 8);
       gload[w % 4] += (double)na * ncb * (2 * TKS / 4);
     }
     int ywarps[4] = {0, 0, 0, 0};
@@ -897,6 +909,18 @@ int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift, bool
 
 void launch_pass_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x, int grid, cudaStream_t st) {
   const size_t smem = tma_pass_smem_bytes(x.pwidth, x.kp_hi - x.kp_lo, p.w_pad, x.ns, x.rb);
+  static int verbose = getenv("PSVD_PASS_VERBOSE") ? atoi(getenv("PSVD_PASS_VERBOSE")) : 0;
+  if (verbose > 0) {  // diagnostics: the geometry of the first launches
+    --verbose;
+    fprintf(stderr, "pass_tma: grid=%d M=%lld np=%d np_pad=%d w=%d wk=%d pwidth=%d kspan=%d ns=%d rb=%d ykp=%d yh=%d "
+            "nslices=%d smem=%zu tiles:", grid, (long long)p.M, p.np, p.np_pad, p.w, p.wk, x.pwidth, x.kp_hi - x.kp_lo,
+            x.ns, x.rb, p.ykp, p.yh, p.nslices, smem);
+    for (int w = 0; w < NWARP; ++w)
+      if (p.plan[0][w].ntile) fprintf(stderr, " w%d(%d,%d,sub%02x)", w, p.plan[0][w].ti[0], p.plan[0][w].tj[0], p.plan[0][w].sub);
+    if (p.ykp > 1)
+      for (int w = 0; w < (p.w_pad / 8) * p.ykp; ++w) fprintf(stderr, " y%d[%d+%d]", w, p.ykj0[w], p.yknj[w]);
+    fprintf(stderr, "\n");
+  }
   if (x.rb == 2) {
     cudaFuncSetAttribute(pass_tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     pass_tma_kernel<2><<<grid, NTHR, smem, st>>>(p, maps, x);

@@ -429,7 +429,7 @@ int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu
     {
       std::vector<Seg> segs;
       if (hq) segs.push_back(Seg{Qp, ldqp, lq, 0});
-      segs.push_back(Seg{Zt, ldq, l, 0});
+      segs.push_back(Seg{Zt, ldq, l, 2});  // Z^T Y1 is not needed: no P^T Y rows for Z
       segs.push_back(Seg{A[b], lda[b], B[b], 0});
       const int wk = (hq ? lq : 0) + l;
       Pass pb;
@@ -474,7 +474,7 @@ int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu
       launch_extract_sym((const double*)c->tiles.ptr, pA.NB, pA.p.np_pad, l, nullptr, G1, hi);
       c->launches++;
       if ((rc = svqb(c, G1, l, T1, sscr, hi))) return rc;
-      segs.push_back(Seg{Zt, ldq, l, 0});
+      segs.push_back(Seg{Zt, ldq, l, 2});  // (no Z^T Y1 rows)
       Pass pB;  // projection pass: Y1 = Y T1 (not in place: slices), Y1^T Y1, [Q | A]^T Y1
       if ((rc = plan_pass(c, pB, M, segs, rows, l, l, T1, l, false, true, true, -1, -1, nullptr, nullptr, 0, 0, true)))
         return rc;

@@ -39,12 +39,14 @@ struct Seg {
   const double* ptr;
   int64_t ld;
   int ncols;
-  int col0;  // first column in the panel space (plan_pass fills it; pass 1 on input = align to 32)
+  int col0;  // first column in the panel space (plan_pass fills it). On input: 1 = start on a
+             // 32-column block, 2 = no P^T Y rows wanted for this segment (narrow TMA pass)
 };
 
 struct WarpPlan {
   signed char ti[2], tj[2];  // 32-column block indices into [P | Y]
-  unsigned char ntile, kpart, ksplit, pad_;
+  unsigned char ntile, kpart, ksplit;
+  unsigned char sub;  // narrow TMA pass, P-tile: first wanted 8-column sub-block | count << 4 (0: all)
 };
 
 struct TallParams {
