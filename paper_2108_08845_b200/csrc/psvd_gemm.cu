@@ -133,11 +133,16 @@ __global__ void __launch_bounds__(GT) tgemm_nn_kernel(int64_t M, ColTable P, int
 constexpr int TR = 32;          // rows per stage of tgemm_tn
 constexpr int TSTR = TR + 4;    // = 4 mod 16
 constexpr int TO = 64;          // output tile edge
+#ifndef TN_CTAS_PER_SM
+#define TN_CTAS_PER_SM 3        // split-K CTAs per SM (3 fit by shared memory)
+#endif
 
 // partial[(chunk * ntk + kt) * ntn + nt][64 x 64] (row-major 64x64, row = P column)
 __global__ void __launch_bounds__(GT) tgemm_tn_kernel(int64_t M, int64_t rows_per_chunk, ColTable P, int K,
                                                       const double* __restrict__ Y, int64_t ldy, int N, int ntk,
-                                                      int ntn, double* __restrict__ partial) {
+                                                      int ntn, int sym, double* __restrict__ partial) {
+  // sym: P == Y (a Gram): tiles below the diagonal are not computed (the reduce mirrors them)
+  if (sym && (int)(blockIdx.x % (ntk * ntn)) / ntn > (int)(blockIdx.x % (ntk * ntn)) % ntn) return;
   extern __shared__ __align__(16) double gsm[];
   double (*sA)[TO * TSTR] = reinterpret_cast<double (*)[TO * TSTR]>(gsm);
   double (*sB)[TO * TSTR] = reinterpret_cast<double (*)[TO * TSTR]>(gsm + 2 * TO * TSTR);
@@ -217,15 +222,23 @@ __global__ void __launch_bounds__(GT) tgemm_tn_kernel(int64_t M, int64_t rows_pe
 
 // X[m + n*ldx] = d[m] * sum_chunks partial(chunk, m, n), chunks in order
 __global__ void tgemm_tn_reduce_kernel(const double* __restrict__ partial, int nchunks, int K, int N, int ntk,
-                                       int ntn, const double* __restrict__ d, double* __restrict__ X, int ldx) {
+                                       int ntn, int sym, const double* __restrict__ d, double* __restrict__ X,
+                                       int ldx) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)K * N) return;
-  const int m = (int)(idx % K), n = (int)(idx / K);
+  int m = (int)(idx % K), n = (int)(idx / K);
+  const int mo = m;
+  if (sym && m / TO > n / TO) {  // below-diagonal tile of a Gram: its mirror (same sums, same order)
+    const int t = m;
+    m = n;
+    n = t;
+  }
   const int kt = m / TO, nt = n / TO;
   const size_t off = (size_t)(m % TO) * TO + (n % TO);
   double s = 0.0;
   for (int c = 0; c < nchunks; ++c) s += partial[((size_t)c * ntk * ntn + kt * ntn + nt) * TO * TO + off];
-  X[(int64_t)n * ldx + m] = d != nullptr ? d[m] * s : s;
+  const int no = (int)(idx / K);
+  X[(int64_t)no * ldx + mo] = d != nullptr ? d[mo] * s : s;
 }
 
 // per-chunk (value at max |u|, global row) of each column; ties -> first row
@@ -297,7 +310,7 @@ void launch_tgemm_nn(int64_t M, const GemmSeg* segs, int nseg, const double* W, 
 
 size_t tgemm_tn_partial_doubles(int64_t M, int K, int N, int num_sms) {
   const int ntk = (K + TO - 1) / TO, ntn = (N + TO - 1) / TO;
-  const int64_t want = std::max<int64_t>(1, (int64_t)2 * num_sms / (ntk * ntn));
+  const int64_t want = std::max<int64_t>(1, (int64_t)TN_CTAS_PER_SM * num_sms / (ntk * ntn));
   const int64_t nchunks = std::min<int64_t>(want, (M + TR - 1) / TR);
   return (size_t)std::max<int64_t>(nchunks, 1) * ntk * ntn * TO * TO;
 }
@@ -307,16 +320,17 @@ void launch_tgemm_tn(int64_t M, const GemmSeg* segs, int nseg, const double* Y, 
   const ColTable t = make_table(segs, nseg);
   const int K = t.c0[nseg];
   const int ntk = (K + TO - 1) / TO, ntn = (N + TO - 1) / TO;
-  const int64_t want = std::max<int64_t>(1, (int64_t)2 * num_sms / (ntk * ntn));
+  const int64_t want = std::max<int64_t>(1, (int64_t)TN_CTAS_PER_SM * num_sms / (ntk * ntn));
   int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(want, (M + TR - 1) / TR));
   const int64_t rows = ((M + nchunks - 1) / nchunks + TR - 1) / TR * TR;
   nchunks = (M + rows - 1) / rows;
   const size_t sm = sizeof(double) * 4 * TO * TSTR + 8 * (size_t)K + 16;
   cudaFuncSetAttribute(tgemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  tgemm_tn_kernel<<<(unsigned)(nchunks * ntk * ntn), GT, sm, st>>>(M, rows, t, K, Y, ldy, N, ntk, ntn, partial);
+  const int sym = (nseg == 1 && segs[0].ptr == Y && segs[0].ld == ldy && K == N) ? 1 : 0;
+  tgemm_tn_kernel<<<(unsigned)(nchunks * ntk * ntn), GT, sm, st>>>(M, rows, t, K, Y, ldy, N, ntk, ntn, sym, partial);
   const int64_t tot = (int64_t)K * N;
-  tgemm_tn_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(partial, (int)nchunks, K, N, ntk, ntn, d, X,
-                                                                        ldx);
+  tgemm_tn_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(partial, (int)nchunks, K, N, ntk, ntn, sym, d,
+                                                                        X, ldx);
 }
 
 int64_t colmax_rows_chunks(int64_t M) { return std::max<int64_t>(1, std::min<int64_t>(256, (M + 4095) / 4096)); }

@@ -200,19 +200,20 @@ __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restr
   double* R = sm;          // l x l col-major, upper used
   double* X = R + l * l;   // inverse
   const int tid = threadIdx.x, nthr = blockDim.x;
+  for (int idx = tid; idx < l * l; idx += nthr) R[idx] = G[idx];
+  __syncthreads();
   double dmax = 0.0;
   bool finite = true;
-  for (int i = 0; i < l; ++i) {
-    const double g = G[(size_t)i * l + i];
+  for (int i = 0; i < l; ++i) {  // the diagonal from the shared copy (same scan order)
+    const double g = R[(size_t)i * l + i];
     finite = finite && isfinite(g);
     dmax = fmax(dmax, g);
   }
   // a non-finite snapshot entry reaches every sketch column (Gaussian Omega): its Gram diagonal
   if (!finite && status != nullptr && threadIdx.x == 0) atomicOr(status, PSVD_ST_NONFINITE);
   const double tiny = 64.0 * DBL_EPSILON * dmax;
-  for (int idx = tid; idx < l * l; idx += nthr) R[idx] = G[idx];
-  __syncthreads();
-  // right-looking Cholesky on the upper triangle: R[k][j] for j >= k
+  const int lane = tid & 31, warp = tid >> 5, nwarp = nthr >> 5;
+  // right-looking Cholesky on the upper triangle: R[k][j] for j >= k (column j of R at R + j l)
   for (int k = 0; k < l; ++k) {
     const double piv = R[(size_t)k * l + k];
     const bool ok = piv > tiny;
@@ -220,19 +221,40 @@ __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restr
     __syncthreads();
     for (int j = k + tid; j < l; j += nthr) R[(size_t)j * l + k] = ok ? (j == k ? rk : R[(size_t)j * l + k] / rk) : 0.0;
     __syncthreads();
-    for (int idx = tid; idx < l * l; idx += nthr) {
-      const int i = idx % l, j = idx / l;
-      if (i > k && j >= i) R[(size_t)j * l + i] -= R[(size_t)i * l + k] * R[(size_t)j * l + k];
+    // trailing update: warp per column j, lanes over rows i in (k, j]
+    for (int j = k + 1 + warp; j < l; j += nwarp) {
+      const double rkj = R[(size_t)j * l + k];
+      for (int i = k + 1 + lane; i <= j; i += 32) R[(size_t)j * l + i] -= R[(size_t)i * l + k] * rkj;
     }
     __syncthreads();
   }
-  // X = R^{-1} (upper): column j by back substitution, zero rows for zero pivots
-  for (int j = tid; j < l; j += nthr) {
-    for (int i = l - 1; i >= 0; --i) {
-      double s = (i == j) ? 1.0 : 0.0;
-      for (int q = i + 1; q <= j; ++q) s -= R[(size_t)q * l + i] * X[(size_t)j * l + q];
-      const double d = R[(size_t)i * l + i];
-      X[(size_t)j * l + i] = (i <= j && d != 0.0) ? s / d : 0.0;
+  // X = R^{-1} (upper), warp per column j: column-oriented back substitution, the right-hand
+  // side b (= e_j) held by the lanes (row i in lane i % 32, slot i / 32); zero rows for zero pivots
+  constexpr int SLOTS_MAX = (CHOL_NMAX + 31) / 32;
+  for (int j = warp; j < l; j += nwarp) {
+    double b[SLOTS_MAX];
+#pragma unroll
+    for (int t = 0; t < SLOTS_MAX; ++t) b[t] = (t * 32 + lane == j) ? 1.0 : 0.0;
+#pragma unroll
+    for (int t = SLOTS_MAX - 1; t >= 0; --t) {
+      if (t * 32 > j) continue;
+      for (int r = 31; r >= 0; --r) {
+        const int q = t * 32 + r;
+        if (q > j) continue;
+        const double d = R[(size_t)q * l + q];
+        const double xq = d != 0.0 ? __shfl_sync(0xffffffffu, b[t], r) / d : 0.0;
+        if (lane == r) b[t] = xq;
+#pragma unroll
+        for (int u = 0; u <= t; ++u) {
+          const int i = u * 32 + lane;
+          if (i < q) b[u] -= R[(size_t)q * l + i] * xq;
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < SLOTS_MAX; ++t) {
+      const int i = t * 32 + lane;
+      if (i < l) X[(size_t)j * l + i] = i <= j ? b[t] : 0.0;
     }
   }
   __syncthreads();

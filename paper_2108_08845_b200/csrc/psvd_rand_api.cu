@@ -159,7 +159,27 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
         c->launches += 5;
       }
     }
-    launch_jacobi_svd(Bt, n, l, S, J, (double*)c->jacws.ptr, c->d_status, st);
+    if (n >= 2 * l && l <= CHOL_NMAX) {
+      // small SVD of B through a QR of B^T (CholeskyQR2, n x l) and one-sided Jacobi on R (l x l):
+      // B^T J = Q (R J) gives the same J and column norms, and rotating columns of length l
+      // instead of n costs n / l times less; an ill-conditioned B^T (max R_ii / min R_ii > 1e6)
+      // takes the gated Jacobi on B^T itself
+      int* illcond = c->d_status + 3;
+      double* R1 = Tz;
+      double* R2 = Z;
+      double* Rq = Qz;
+      launch_small_gemm(Bt, n, 1, Bt, n, G1, l, l, n, l, nullptr, st);    // B B^T
+      launch_chol_inv(G1, l, T1, st, illcond, c->d_status, R1);
+      launch_small_gemm(Bt, n, 0, T1, l, Z1, n, n, l, l, nullptr, st);    // Q1 = B^T R1^-1
+      launch_small_gemm(Z1, n, 1, Z1, n, G2, l, l, n, l, nullptr, st);
+      launch_chol_inv(G2, l, X, st, nullptr, nullptr, R2);
+      launch_small_gemm(R2, l, 0, R1, l, Rq, l, l, l, l, nullptr, st);    // R = R2 R1
+      launch_jacobi_svd(Rq, l, l, S, J, (double*)c->jacws.ptr, c->d_status, st);
+      launch_jacobi_svd(Bt, n, l, S, J, (double*)c->jacws.ptr, c->d_status, st, illcond);
+      c->launches += 8;
+    } else {
+      launch_jacobi_svd(Bt, n, l, S, J, (double*)c->jacws.ptr, c->d_status, st);
+    }
     launch_small_gemm(T2, l, 0, J, l, Wf, l, l, l, K, nullptr, st);
     launch_tgemm_nn(M, &gy2, 1, Wf, l, K, U_out, ldo, st);  // U = Y1 (T2 U_B[:, :K])
     const int64_t nch = colmax_rows_chunks(M);

@@ -476,6 +476,32 @@ def test_config4_weak_randomized_wide():
     _config_parity(dg.weak_scaling_matrix(1 << 13, 1024), K=100, B=512, ff=0.95, sketch=10)
 
 
+def test_wide_randomized_rank_deficient_core():
+    """Wide route (l = 50 > 32) on a numerically rank-30 stream: the core SVD's CholeskyQR of B^T
+    flags the ill-conditioned factor and the gated Jacobi on B^T itself runs; the modes above the
+    noise floor match the oracle (the well-conditioned QR-then-Jacobi route is covered by the
+    config 3 / 4 cases)."""
+    p = _pkg()
+    rng = np.random.default_rng(5)
+    M, S, r = 6000, 600, 30
+    U = np.linalg.qr(rng.standard_normal((M, r)))[0]
+    V = np.linalg.qr(rng.standard_normal((S, r)))[0]
+    a = np.asfortranarray((U * 0.8 ** np.arange(r)) @ V.T + 1e-13 * rng.standard_normal((M, S)))
+    batches = _batches(a, 200)
+    K = 40
+    cfg = p.StreamConfig(k_modes=K, forget_factor=0.95, batch_columns=200,
+                         sketch=p.RandomSketchConfig(target_rank=K, oversampling=10, power_iterations=1, seed=0))
+    st, hist = p.stream_all(batches, cfg)
+    rm, rs, rh = oracle.ref_rand_stream_all(batches, K, 0.95, 10, 1, 0)
+    m, s = _np(st)
+    assert oracle.sigma_rel_err(s[:r], rs[:r]) <= SIG_TOL
+    assert np.all(s[r:] < 1e-9 * s[0])
+    mask = _gap_mask(rs[:r])
+    ang = oracle.mode_angles(m[:, :r], rm[:, :r])
+    assert mask.sum() >= r // 2
+    assert np.max(ang[mask]) <= ANG_TOL, ang
+
+
 def test_wide_randomized_route_matches_fused(monkeypatch):
     """The tall-skinny GEMM route (forced) and the fused passes agree to rounding."""
     p = _pkg()
