@@ -269,8 +269,8 @@ __global__ void __launch_bounds__(NTHR, 1)
       if (lane == 0) mbar_arrive(&empty[b]);  // panel slot no longer read by this warp
       double* Ys = sY + (size_t)yb * YC * SR;
       const int o0 = cb * 8 + 2 * tq;
-      if (kp == 0) {
-        if (s >= YB && ngram > 0) mbar_wait(&yfree[yb], yph ^ 1u);
+      if (kp == 0 || p.dbg == 3) {  // dbg 3 (timing only, wrong Y): parts do not wait for each other
+        if ((kp == 0 || last) && s >= YB && ngram > 0) mbar_wait(&yfree[yb], yph ^ 1u);
       } else {
         mbar_wait(&chain[(yb * 4 + cb) * 3 + kp - 1], yph);  // the partial sum of parts 0 .. kp-1
 #pragma unroll
@@ -920,6 +920,16 @@ void launch_pass_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x
     if (p.ykp > 1)
       for (int w = 0; w < (p.w_pad / 8) * p.ykp; ++w) fprintf(stderr, " y%d[%d+%d]", w, p.ykj0[w], p.yknj[w]);
     fprintf(stderr, "\n");
+  }
+  static const bool drop_gram = getenv("PSVD_DBG_DROP_GRAM") != nullptr;  // timing diagnostics only: wrong tiles
+  if (drop_gram && x.rb == 2) {
+    TallParams q = p;
+    const int ny = p.ykp > 1 ? (p.w_pad / 8) * p.ykp : 0;
+    for (int sl = 0; sl < MAX_SLICES; ++sl)
+      for (int w = ny; w < NWARP; ++w) q.plan[sl][w].ntile = 0;
+    cudaFuncSetAttribute(pass_tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    pass_tma_kernel<2><<<grid, NTHR, smem, st>>>(q, maps, x);
+    return;
   }
   if (x.rb == 2) {
     cudaFuncSetAttribute(pass_tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -4,5 +4,5 @@
 if [ "$1" == "-" ]; then shift; set -- "" "$@"; else set -- "" "PSVD_TMA_NS=2" "PSVD_GRAM_DBG=1" "$@"; fi
 for v in "$@"; do
   echo "== ${v:-default}"
-  env $v python tools/rand_trace.py 0 2>&1 >/dev/null | python tools/trace_passes.py
+  env $v timeout 120 python tools/rand_trace.py 0 2>&1 >/dev/null | python tools/trace_passes.py
 done
