@@ -19,6 +19,7 @@ from .io import (BatchSource, read_batches, read_matrix, read_matrix_header, rea
 from .linalg import (QrResult, RandomSketchConfig, SvdResult, aligned_mode_difference, low_rank_svd,  # noqa: F401
                      qr_factor, randomized_range, subspace_angles, svd_full)
 from .streaming import StreamConfig, StreamState, stream_all, stream_incorporate, stream_initialize  # noqa: F401
+from .classes import Parsvd_Base, Parsvd_Parallel, Parsvd_Serial  # noqa: F401
 
 from . import streaming  # noqa: F401,E402  (module access: STREAM_WINDOW)
 

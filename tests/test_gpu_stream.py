@@ -585,11 +585,20 @@ def _det_run_rank_worker(rank, world, port, q, rows, cols, b):
         for m in loc[1:]:
             st2 = p.parallel_stream_incorporate(ctx, st2, m, cfg)
         full, full2 = p.gather_modes(ctx, st), p.gather_modes(ctx, st2)
+        # the paper's class surface over the same calls (modes gathered at the root every step)
+        obj = p.Parsvd_Parallel(10, 0.95, ctx=ctx).initialize(loc[0])
+        for m in loc[1:]:
+            obj.incorporate_data(m)
+        same = (np.array_equal(obj.singular_values.cpu().numpy(), st2.singular_values.cpu().numpy()) and
+                np.array_equal(obj.ulocal.cpu().numpy(), st2.modes.cpu().numpy()) and
+                (obj.modes is None) == (full2 is None) and
+                (full2 is None or np.array_equal(obj.modes.cpu().numpy(), full2.cpu().numpy())) and
+                obj.iteration == len(loc) - 1)
         q.put((rank, st.singular_values.cpu().numpy(), [h.cpu().numpy() for h in hist],
                None if full is None else full.cpu().numpy(), None if full2 is None else full2.cpu().numpy(),
-               st2.singular_values.cpu().numpy()))
+               st2.singular_values.cpu().numpy(), same))
     except Exception as e:
-        q.put((rank, "error", repr(e), None, None, None))
+        q.put((rank, "error", repr(e), None, None, None, False))
         raise
     finally:
         dist.destroy_process_group()
@@ -614,8 +623,9 @@ def test_parallel_pipelined_stream_ranks_match_serial(world, rows, cols, b):
         pr.start()
     out = {}
     for _ in range(world):
-        rank, sig, hist, full, full2, sig2 = q.get(timeout=300)
+        rank, sig, hist, full, full2, sig2, same = q.get(timeout=300)
         assert not (isinstance(sig, str) and sig == "error"), hist
+        assert same  # Parsvd_Parallel == parallel_stream_initialize / incorporate, bitwise
         out[rank] = (sig, hist, full, full2, sig2)
     for pr in procs:
         pr.join(timeout=120)
@@ -628,6 +638,29 @@ def test_parallel_pipelined_stream_ranks_match_serial(world, rows, cols, b):
     _assert_parity(out[0][3], out[0][4], rm, rs)
     for h, r_ in zip(out[0][1], rh):
         assert oracle.sigma_rel_err(h, r_) <= SIG_TOL
+
+
+@pytest.mark.parametrize("low_rank", [False, True])
+def test_parsvd_serial_class_matches_function_api_and_oracle(low_rank):
+    """PyParSVD's class surface (listing 1): Parsvd_Serial(K, ff).initialize(A0) then
+    incorporate_data(A) per batch is the function API bitwise, and the reference by the oracle."""
+    p = _pkg()
+    a = oracle.burgers_matrix(4096, 800)
+    bs = _batches(a, 200)
+    obj = p.Parsvd_Serial(10, 0.95, low_rank=low_rank).initialize(bs[0])
+    st = p.stream_initialize(bs[0], obj.config)
+    for b in bs[1:]:
+        obj.incorporate_data(b)
+        st = p.stream_incorporate(st, b, obj.config)
+    assert obj.iteration == 3
+    assert np.array_equal(obj.singular_values.cpu().numpy(), st.singular_values.cpu().numpy())
+    assert np.array_equal(obj.modes.cpu().numpy(), st.modes.cpu().numpy())
+    if low_rank:
+        rm, rs, _ = oracle.ref_rand_stream_all(bs, 10, 0.95, 10, 1, 0)
+    else:
+        rm, rs, _ = oracle.ref_stream_all(bs, 10, 0.95)
+    m, s_ = _np(obj.state)
+    _assert_parity(m, s_, rm, rs)
 
 
 def test_parallel_randomized_single_rank_is_serial():
