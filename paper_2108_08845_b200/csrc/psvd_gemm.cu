@@ -10,6 +10,7 @@
 //              order by tgemm_tn_reduce (bitwise reproducible), optionally row-scaled by d.
 //   colmax_rows: per-chunk (value at max |u|, global row) of each column, first occurrence.
 #include <algorithm>
+#include <cstdlib>
 
 #include "psvd_gemm.cuh"
 
@@ -25,7 +26,7 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem, int src_
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(src_bytes));
 }
 constexpr int BM = 64, BK = 32;   // rows per CTA, K chunk
-constexpr int PSTR = BM + 4;      // smem stride of a P column chunk (= 4 mod 16)
+
 constexpr int WSTR = BK + 4;      // smem stride of a W column chunk
 
 struct ColTable {
@@ -46,39 +47,43 @@ __device__ __forceinline__ void build_cols(const ColTable& t, int K, const doubl
   }
 }
 
-size_t nn_smem(int NB, int K) { return sizeof(double) * (2 * BK * PSTR + 2 * (size_t)NB * WSTR) + 8 * (size_t)K + 16; }
+size_t nn_smem(int NB, int K, int BMT = BM) {
+  return sizeof(double) * (2 * BK * (size_t)(BMT + 4) + 2 * (size_t)NB * WSTR) + 8 * (size_t)K + 16;
+}
 
-template <int NB>  // output columns per CTA (64 or 128)
+template <int NB, int BMT = BM>  // output columns per CTA (64 or 128); rows per CTA (64 or 128)
 __global__ void __launch_bounds__(GT) tgemm_nn_kernel(int64_t M, ColTable P, int K, const double* __restrict__ W,
                                                       int64_t ldw, int N, double* __restrict__ C, int64_t ldc) {
   constexpr int CBW = NB / 8 / 2;  // column blocks per warp (warp pair shares the row blocks)
+  constexpr int RBW = BMT / 32;    // row blocks per warp (4 warps over the rows)
+  constexpr int PS = BMT + 4;      // smem stride of a P column chunk (= 4 mod 16)
   extern __shared__ __align__(16) double gsm[];
-  double (*sP)[BK * PSTR] = reinterpret_cast<double (*)[BK * PSTR]>(gsm);
-  double (*sW)[NB * WSTR] = reinterpret_cast<double (*)[NB * WSTR]>(gsm + 2 * BK * PSTR);
-  const double** cols = reinterpret_cast<const double**>(gsm + 2 * BK * PSTR + 2 * NB * WSTR);
+  double (*sP)[BK * PS] = reinterpret_cast<double (*)[BK * PS]>(gsm);
+  double (*sW)[NB * WSTR] = reinterpret_cast<double (*)[NB * WSTR]>(gsm + 2 * BK * PS);
+  const double** cols = reinterpret_cast<const double**>(gsm + 2 * BK * PS + 2 * NB * WSTR);
   build_cols(P, K, cols);
   __syncthreads();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, tq = lane & 3;
-  const int64_t r0 = (int64_t)blockIdx.x * BM;
+  const int64_t r0 = (int64_t)blockIdx.x * BMT;
   const int n0 = blockIdx.y * NB;
-  const int rbase = (warp & 3) * 2;           // row blocks rbase, rbase + 1
+  const int rbase = (warp & 3) * RBW;         // row blocks rbase .. rbase + RBW - 1
   const int cbase = (warp >> 2) * CBW;        // column blocks cbase .. cbase + CBW - 1
-  double acc[2][CBW][2];
+  double acc[RBW][CBW][2];
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < RBW; ++a)
 #pragma unroll
     for (int b = 0; b < CBW; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
   const int nchunk = (K + BK - 1) / BK;
   auto load = [&](int ch, int buf) {
     const int k0 = ch * BK;
-    // P: BK columns x 64 rows = 32 x 32 16-byte pieces
-    for (int q = tid; q < BK * (BM / 2); q += GT) {
-      const int kk = q / (BM / 2), pc = q % (BM / 2);
+    // P: BK columns x BMT rows in 16-byte pieces
+    for (int q = tid; q < BK * (BMT / 2); q += GT) {
+      const int kk = q / (BMT / 2), pc = q % (BMT / 2);
       const int k = k0 + kk;
       const int64_t r = r0 + 2 * pc;
-      double* dst = &sP[buf][kk * PSTR + 2 * pc];
+      double* dst = &sP[buf][kk * PS + 2 * pc];
       const int64_t valid = M - r;
       const int bytes = (k < K) ? (valid >= 2 ? 16 : (valid == 1 ? 8 : 0)) : 0;
       const double* src = (bytes > 0) ? cols[k] + r : P.ptr[0];
@@ -105,20 +110,20 @@ __global__ void __launch_bounds__(GT) tgemm_nn_kernel(int64_t M, ColTable P, int
 #pragma unroll
     for (int ks = 0; ks < BK / 4; ++ks) {
       const int k = ks * 4 + tq;
-      double fa[2], fb[CBW];
+      double fa[RBW], fb[CBW];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) fa[a] = p[k * PSTR + (rbase + a) * 8 + g];
+      for (int a = 0; a < RBW; ++a) fa[a] = p[k * PS + (rbase + a) * 8 + g];
 #pragma unroll
       for (int b = 0; b < CBW; ++b) fb[b] = w[((cbase + b) * 8 + g) * WSTR + k];
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
+      for (int a = 0; a < RBW; ++a)
 #pragma unroll
         for (int b = 0; b < CBW; ++b) dmma884(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int a = 0; a < 2; ++a) {
+  for (int a = 0; a < RBW; ++a) {
     const int64_t r = r0 + (rbase + a) * 8 + g;
     if (r >= M) continue;
 #pragma unroll
@@ -297,7 +302,13 @@ void launch_tgemm_nn(int64_t M, const GemmSeg* segs, int nseg, const double* W, 
   const ColTable t = make_table(segs, nseg);
   const int K = t.c0[nseg];
   const unsigned gx = (unsigned)((M + BM - 1) / BM);
-  if (N <= 64) {
+  static const int bm128 = getenv("PSVD_NN_BM64") ? 0 : 1;  // A/B switch: 64-row CTAs
+  if (N <= 64 && bm128) {
+    // 128-row CTAs: 4 row blocks x 4 column blocks per warp, 8 fragment loads per 16 DMMAs
+    const size_t sm = nn_smem(64, K, 128);
+    cudaFuncSetAttribute(tgemm_nn_kernel<64, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    tgemm_nn_kernel<64, 128><<<dim3((unsigned)((M + 127) / 128), 1), GT, sm, st>>>(M, t, K, W, ldw, N, C, ldc);
+  } else if (N <= 64) {
     const size_t sm = nn_smem(64, K);
     cudaFuncSetAttribute(tgemm_nn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     tgemm_nn_kernel<64><<<dim3(gx, 1), GT, sm, st>>>(M, t, K, W, ldw, N, C, ldc);
