@@ -244,10 +244,18 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # PSVD_BENCH_SHARED_GPU=1 (flow check only, not a measurement): every rank on GPU 0 with gloo
+    # through the host, so the N > 1 path runs on a one-GPU box
+    shared = os.environ.get("PSVD_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     ctxr = RankContext()
     lo, hi = p.partition_bounds(a.rows, world)[rank]
     M = hi - lo
@@ -326,9 +334,7 @@ def run_ours(a):
         nat.call("psvd_set_exchange", c, None, None, None, 1, 0)
     ms = t0.elapsed_time(t1)
     if world > 1:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
+        ms = max_over_ranks(ms, dev)
     ms_step = ms / a.steps
     snap_bytes = 8.0 * a.rows * SNAPS  # whole job, all ranks
     value = snap_bytes / (ms_step * 1e-3) / 1e9
@@ -431,6 +437,16 @@ def time_randomized(a, D, M, dev, c, stream, q):
             "sketch": f"K={K} p=10 q={q} seed=0", "hbm_frac": round(alg / (ms * 1e-3) / 1e9 / HBM_PEAK[0], 4)}
 
 
+def max_over_ranks(x, dev):
+    """Max of a host scalar over ranks (on the device under NCCL, through the host under gloo)."""
+    import torch
+    import torch.distributed as dist
+    on_dev = dist.get_backend() == "nccl"
+    tt = torch.tensor([x], dtype=torch.float64, device=dev if on_dev else "cpu")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    return float(tt.item())
+
+
 def e2e(a, p, D, M, dev, world, ctxr):
     """Same metric through the public API (stream_all at N = 1, parallel_stream_* at
     N > 1) with the snapshot batches in pinned host memory: every step copies its
@@ -479,9 +495,7 @@ def e2e(a, p, D, M, dev, world, ctxr):
     dt = (time.perf_counter() - t0) / n
     gc.enable()
     if world > 1:
-        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        dt = float(tt.item())
+        dt = max_over_ranks(dt, dev)
     return {"value": round(8.0 * a.rows * SNAPS / dt / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": int(8 * M * SNAPS), "d2h_bytes_per_step": int(out[0].numel() * 8 + out[1].numel() * 8),
             "ms_per_step": round(dt * 1e3, 2), "steps": n,
