@@ -4,7 +4,7 @@
 // lambda_10 < 1e-7) has its top K eigenvectors inside the span of G^m Q0 after m = 2
 // applications.  So before the one-CTA Householder eigensolver (O(n^3) latency-bound
 // steps) we try:
-//   ss_iterate:  Q0 = orth([e_0..e_{K-1} | pseudo-random]) (n x 32), Q <- orth(G Q) twice,
+//   ss_iterate:  X0 = [e_0..e_{K-1} | pseudo-random] (n x 32), Q <- orth(G Q) twice from Q = X0,
 //                W = G Q, H = Q^T W (32 x 32).  G Q on DMMA with G streamed from L2,
 //                orth = Householder QR in shared memory (one CTA).
 //   eig_topk(H): Ritz values / vectors (the existing solver at n = 32).
@@ -121,15 +121,16 @@ __global__ void __launch_bounds__(SS_THREADS, 1)
   double* Qs = ssm;
   double* Ys = Qs + (size_t)SP * ldq;
   double* stau = Ys + (size_t)SP * ldq;
-  // X0 = [e_0 .. e_{K-1} | pseudo-random], rows >= n zero
+  // X0 = [e_0 .. e_{K-1} | pseudo-random], rows >= n zero.  No QR of X0: span(G^m X0) does not
+  // depend on the basis of span(X0), and X0 is well conditioned (unit vectors next to random
+  // columns), so the first product takes X0 as it is
   for (int i = threadIdx.x; i < SP * ldq; i += blockDim.x) {
     const int c = i / ldq, r = i % ldq;
     double v = 0.0;
     if (r < n) v = (c < K) ? (r == c ? 1.0 : 0.0) : prand_ss(7919u * c + 17u, r);
-    Ys[i] = v;
+    Qs[i] = v;
   }
   __syncthreads();
-  house_qr(Ys, n, ldq, Qs, stau);
   for (int it = 0; it < iters; ++it) {
     gq_product(G, n, Qs, ldq, Ys);
     __syncthreads();
