@@ -61,56 +61,64 @@ __device__ void gq_product(const double* __restrict__ G, int n, const double* Qs
   }
 }
 
+// Householder reflector of column j of Y (rows j .. n-1), by one warp: v = Y[j+1:, j] scaled in
+// place (v_j = 1 implied), tau into *tau_out; Y[j, j] keeps alpha (R is not needed).
+__device__ __forceinline__ void house_reflector(double* v, int j, int n, double* tau_out) {
+  const int lane = threadIdx.x & 31;
+  double part = 0.0;
+  for (int i = j + 1 + lane; i < n; i += 32) part = fma(v[i], v[i], part);
+  const double xn2 = warp_sum(part);
+  const double alpha = v[j];
+  double tau = 0.0, scl = 0.0;
+  if (xn2 != 0.0) {
+    const double beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
+    tau = (beta - alpha) / beta;
+    scl = 1.0 / (alpha - beta);
+  }
+  for (int i = j + 1 + lane; i < n; i += 32) v[i] *= scl;
+  if (lane == 0) *tau_out = tau;
+}
+
+// y <- H_j y = y - tau v (v^T y) on rows j .. n-1, by one warp (v_j = 1 implied)
+__device__ __forceinline__ void house_apply(const double* v, double tau, int j, int n, double* y) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int i = j + 1 + lane; i < n; i += 32) s = fma(v[i], y[i], s);
+  s = (warp_sum(s) + y[j]) * tau;
+  __syncwarp();
+  if (lane == 0) y[j] -= s;
+  for (int i = j + 1 + lane; i < n; i += 32) y[i] = fma(-s, v[i], y[i]);
+  __syncwarp();
+}
+
 // Householder QR of Y (n x SP in smem, ld ldq); Q (explicit, n x SP) into Qs.  Y is destroyed.
+// One CTA barrier per column: the warp that updates column j + 1 (warp 0) forms its reflector
+// right away while the other warps update theirs.  Q column c = H_0 ... H_c e_c (the reflectors
+// after c leave e_c alone), one warp per column, no barriers.
 __device__ void house_qr(double* Ys, int n, int ldq, double* Qs, double* stau) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  for (int j = 0; j < SP; ++j) {
-    double* v = Ys + (size_t)j * ldq;
-    if (warp == 0) {
-      double part = 0.0;
-      for (int i = j + 1 + lane; i < n; i += 32) part = fma(v[i], v[i], part);
-      const double xn2 = warp_sum(part);
-      const double alpha = v[j];
-      double tau = 0.0, scl = 0.0;
-      if (xn2 != 0.0) {
-        const double beta = -copysign(sqrt(alpha * alpha + xn2), alpha);
-        tau = (beta - alpha) / beta;
-        scl = 1.0 / (alpha - beta);
-      }
-      for (int i = j + 1 + lane; i < n; i += 32) v[i] *= scl;
-      if (lane == 0) stau[j] = tau;
-    }
-    __syncthreads();
+  if (warp == 0) house_reflector(Ys, 0, n, &stau[0]);
+  __syncthreads();
+  for (int j = 0; j < SP - 1; ++j) {
+    const double* v = Ys + (size_t)j * ldq;
     const double tau = stau[j];
     for (int c = j + 1 + warp; c < SP; c += nwarps) {
       double* y = Ys + (size_t)c * ldq;
-      double s = 0.0;
-      for (int i = j + 1 + lane; i < n; i += 32) s = fma(v[i], y[i], s);
-      s = (warp_sum(s) + y[j]) * tau;
-      if (lane == 0) y[j] -= s;
-      for (int i = j + 1 + lane; i < n; i += 32) y[i] = fma(-s, v[i], y[i]);
+      house_apply(v, tau, j, n, y);
+      if (c == j + 1) house_reflector(y, j + 1, n, &stau[j + 1]);  // warp 0: the next reflector
     }
     __syncthreads();
   }
-  // Q = H_0 ... H_{SP-1} [I; 0]
-  for (int i = threadIdx.x; i < SP * ldq; i += blockDim.x) {
-    const int c = i / ldq, r = i % ldq;
-    Qs[i] = (r == c) ? 1.0 : 0.0;
-  }
-  __syncthreads();
-  for (int j = SP - 1; j >= 0; --j) {
-    const double* v = Ys + (size_t)j * ldq;
-    const double tau = stau[j];
-    for (int c = j + warp; c < SP; c += nwarps) {
+  // columns c and SP - 1 - c on one warp (equal work: c + 1 + SP - c reflector applications)
+  for (int w = warp; w < SP / 2; w += nwarps)
+    for (int h = 0; h < 2; ++h) {
+      const int c = h ? SP - 1 - w : w;
       double* q = Qs + (size_t)c * ldq;
-      double s = 0.0;
-      for (int i = j + 1 + lane; i < n; i += 32) s = fma(v[i], q[i], s);
-      s = (warp_sum(s) + q[j]) * tau;
-      if (lane == 0) q[j] -= s;
-      for (int i = j + 1 + lane; i < n; i += 32) q[i] = fma(-s, v[i], q[i]);
+      for (int i = lane; i < ldq; i += 32) q[i] = (i == c) ? 1.0 : 0.0;
+      __syncwarp();
+      for (int j = c; j >= 0; --j) house_apply(Ys + (size_t)j * ldq, stau[j], j, n, q);
     }
-    __syncthreads();
-  }
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(SS_THREADS, 1)
