@@ -369,11 +369,13 @@ def test_pipelined_randomized_run_matches_per_update_and_oracle(q):
 
 
 @pytest.mark.parametrize("rows,b,k,p_,q", [(37, 12, 3, 2, 1), (1000, 20, 10, 0, 0), (4097, 64, 16, 16, 2),
-                                          (65536, 200, 1, 1, 1), (24576, 100, 12, 20, 0)])
+                                          (65536, 200, 1, 1, 1), (24576, 100, 12, 20, 0),
+                                          (16384, 197, 7, 6, 0), (32768, 130, 11, 9, 1)])
 def test_pipelined_randomized_run_edge_shapes(rows, b, k, p_, q):
     """The pipelined randomized run at its edges: tiny and odd row counts (16-row TMA stages),
     no oversampling, the widest sketch (l = 32), K = 1, rows a multiple of 16 (32-row stages,
-    register-resident W): against the oracle per step."""
+    register-resident W), odd batch widths and sketch widths off the 8-column grid (trimmed P-tile
+    sub-blocks, SMSP-balanced tile placement): against the oracle per step."""
     p = _pkg()
     a = np.random.default_rng(rows + b).standard_normal((rows, 4 * b)) * np.linspace(2.0, 0.1, 4 * b)
     bs = _batches(a, b)
