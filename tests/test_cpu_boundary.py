@@ -92,3 +92,36 @@ def test_apmos_config_validation():
     with pytest.raises(ValueError):
         ApmosConfig(local_rank=4, global_rank=4, k_modes=2, sketch=RandomSketchConfig(target_rank=2))
     assert ApmosConfig(local_rank=4, global_rank=4, k_modes=2).use_randomized is False
+
+
+def _kind_c(param):
+    """Category of a C parameter declaration from include/psvd.h."""
+    t = param.strip()
+    if "*" in t or t.split()[0].endswith("_fn"):
+        return "ptr"
+    base = " ".join(t.split()[:-1]).replace("const ", "")
+    return {"int": "i32", "int64_t": "i64", "long long": "i64", "double": "f64"}[base]
+
+
+def _kind_ctypes(tp):
+    if tp in (ctypes.c_int, ctypes.c_int32):
+        return "i32"
+    if tp in (ctypes.c_int64, ctypes.c_longlong):
+        return "i64"
+    if tp is ctypes.c_double:
+        return "f64"
+    return "ptr"
+
+
+def test_ctypes_signatures_match_the_header():
+    """Every ctypes argtypes list has the header's arity and argument kinds (32 / 64-bit integer,
+    double, pointer): a drifted signature would pass wrong bits through the ABI silently."""
+    import re
+    hdr = open(os.path.join(os.path.dirname(nat.LIB_PATH), "..", "..", "include", "psvd.h")).read()
+    protos = re.findall(r"^(?:int|long long|const char\s*\*)\s+(psvd_\w+)\s*\(([^;]*?)\)\s*;", hdr, re.M | re.S)
+    assert len(protos) == len(nat._SIGS)
+    for name, params in protos:
+        params = " ".join(params.split())
+        want = [] if params in ("", "void") else [_kind_c(x) for x in params.split(",")]
+        got = [_kind_ctypes(t) for t in nat._SIGS[name][1]]
+        assert got == want, (name, got, want)
