@@ -1,23 +1,25 @@
-// Warp-specialized TMA pass for narrow panels (see psvd_tall.cuh, "narrow").
+// Warp-specialized TMA pass for narrow panels (see psvd_tall.cuh, "narrow"): Y = P W for a Y of
+// <= 32 columns and the Gram tiles P^T Y, Y^T Y in one read of the panel P = [seg_0 | seg_1 | ...].
 //
-// One CTA per SM streams its row chunk of the panel P = [seg_0 | seg_1 | ...] in
-// 16-row stages.  Each stage is one 2-D TMA box per segment (16 rows x <= 256
-// columns, 128-byte swizzle: column c of a stage is 128 contiguous bytes whose
-// 16-byte chunks are XOR-ed with c & 7), landing in an NS-deep ring signalled by
-// mbarriers (complete_tx).  Warp roles:
+// One CTA per SM streams its row chunk in stages landing in an NS-deep ring signalled by mbarriers
+// (complete_tx).  With M a multiple of 16 and two stages fitting, a stage is 32 rows brought by 3-D
+// TMA boxes {16 rows, 2, <= 256 columns} (256 contiguous bytes of every column per request); else 16
+// rows from 2-D boxes.  128-byte swizzle: the 16-byte chunks of a column are XOR-ed with its unit
+// index (swzr).  Warp roles:
 //
-//   warp 15      producer: one lane issues the stage's TMA boxes once the ring
-//                slot is released;
-//   warps 0..3   Y = P[:, W rows] * W on DMMA, one 8x8 output block each
-//                (row block rb, column block cb), two accumulator chains; Y goes
-//                to a double-buffered swizzled smem tile, to global (slice 0) and
-//                into the per-column argmax of |y|;
-//   warps 4..14  Gram tiles (I, Y) of [P | Y]: A^T Y and Y^T Y, one 32x16 tile each,
-//                compile-time block shape (no per-DMMA predicates).
+//   last warp    producer: one lane issues the stage's TMA boxes once the ring slot is released;
+//   Y warps      32-row stages: W held in registers, each (8-column block, k part) warp forms all 32
+//                rows of its block over its k part, the parts' partial sums meet in the Y tile in
+//                part order through an mbarrier chain; the k split is weighted per SMSP by the Gram
+//                work placed there.  16-row stages: fragment-reloading Y warps (one 8x8 output block
+//                each).  The last part writes Y to global (slice 0) and folds the per-column argmax
+//                of |y|;
+//   Gram warps   one tile (I, Y) of [P | Y] each, compile-time sub-block shape, sub-blocks nobody
+//                reads trimmed at plan time, tiles placed longest-first onto the least-loaded SMSP.
 //
-// No CTA-wide barrier inside the stage loop: full / empty (panel ring), ydone /
-// yfree (Y double buffer) mbarriers only.  Results are bitwise identical run to
-// run (fixed per-warp accumulation order, fixed-order tall_reduce afterwards).
+// No CTA-wide barrier inside the stage loop: full / empty (panel ring), ydone / yfree (Y double
+// buffer) and chain mbarriers only.  Results are bitwise identical run to run (fixed per-warp
+// accumulation order, fixed-order tall_reduce afterwards).
 #include <cuda.h>
 
 #include <algorithm>
@@ -32,12 +34,9 @@ namespace psvd {
 
 namespace {
 
-constexpr int TKS = 16;       // rows per stage = one 128-byte swizzled column
-constexpr int TNS_MAX = 8;    // ring depth: x.ns stages of 16 rows (as many as fit, 3 .. 8)
-constexpr int YMAXC = 32;
-#ifndef PSVD_PRE_MAX
-#define PSVD_PRE_MAX 42  // Gram warps of the narrow pass: register budget (doubles) of the early release
-#endif     // widest Y of the narrow pass (4 column blocks)
+constexpr int TKS = 16;       // rows per 128-byte swizzled column piece (a stage is TKS or 2 TKS rows)
+constexpr int TNS_MAX = 8;    // ring depth: x.ns stages, as many as fit (3 .. 8 of 16 rows, 2 .. 8 of 32)
+constexpr int YMAXC = 32;     // widest Y of the narrow pass (4 column blocks)
 constexpr int YKP_WR = 16;    // W fragments held in registers per Y warp (k steps of 4 columns)
 constexpr int YB = 2;         // Y ring depth (Y warps run up to YB stages ahead of the Gram warps; 4 measured no faster)
 constexpr int PROD_WARP = NWARP - 1;
