@@ -2,9 +2,10 @@
 // (randomized update at configs 3/4: n = K + B up to ~1000, sketch width l up to 128).
 //
 //   tgemm_nn:  C (M x N) = [P_0 | P_1 | ...] (M x K) * W (K x N)        (sketch Y = C Omega,
-//              Y <- Y T, U = Y W_f).  CTA = 64 rows x 64/128 output columns, K in 32-column
-//              chunks through a cp.async double buffer, 8 warps x (2 row blocks x NB/2 column
-//              blocks) of 8x8 DMMA tiles.  Each output element is written once (no in-place).
+//              Y <- Y T, U = Y W_f).  CTA = 128 rows x 64 output columns (N <= 64) or 64 rows x
+//              128, K in 32-column chunks through a cp.async double buffer, 8 warps x (4 or 2 row
+//              blocks x NB/16 column blocks) of 8x8 DMMA tiles.  Each output element is written once.
+//              The sym case of tgemm_tn (P == Y) skips the tiles below the diagonal.
 //   tgemm_tn:  X (K x N) = P^T Y with the M rows split over CTAs (split-K): CTA = (row chunk,
 //              64 x 64 output tile), 32-row stages; per-chunk partial tiles are summed in a fixed
 //              order by tgemm_tn_reduce (bitwise reproducible), optionally row-scaled by d.
