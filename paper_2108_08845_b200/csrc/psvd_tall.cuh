@@ -54,7 +54,7 @@ struct TallParams {
   int64_t rows_per_cta;  // multiple of 32
   int ks;                // rows per stage (32 or 16)
   int nstage;            // cp.async pipeline depth (2 or 3)
-  int narrow;            // every Gram tile's column block is the Y block (<= 32 columns)
+  int narrow;            // every Gram tile ends in the Y block (Y <= 16 columns; <= 32 on the TMA pass)
   int dbg;               // diagnostics (PSVD_GRAM_DBG): 1 = skip DMMA, 2 = skip global loads
   int nseg;
   Seg seg[MAX_SEG];
