@@ -44,6 +44,8 @@ extern "C" {
 #define PSVD_ST_RESCUE 4     /* orthogonality-drift rescue ran (streaming.py:106-115) */
 #define PSVD_ST_RANKDEF 8    /* a kept singular value is exactly zero */
 #define PSVD_ST_CHOLFAIL 16  /* sketch Cholesky needed the shifted retry */
+#define PSVD_ST_ILLCOND 32   /* deterministic Gram route: kept spectrum sigma_1 / sigma_K > 300, so the
+                                update must be redone on the accurate route (psvd_stream_update_accurate) */
 
 typedef struct psvd_ctx psvd_ctx;
 
@@ -131,7 +133,10 @@ int psvd_drift_rescue(psvd_ctx* ctx, int64_t M, double* U, int64_t ldu, int K, c
                       double* sigma, double tol, void* stream);
 
 /* One whole single-GPU update = gram + core_eig + recompose (+ drift rescue
- * when rescue != 0): stream_initialize (Kc = 0) / stream_incorporate. */
+ * when rescue != 0): stream_initialize (Kc = 0) / stream_incorporate.
+ * Gram route: its kept singular values carry eps (sigma_1 / sigma_k)^2 error terms.  When the
+ * kept spectrum is wider than sigma_1 / sigma_K = 300 it sets PSVD_ST_ILLCOND in the status
+ * word; the caller then redoes the update with psvd_stream_update_accurate. */
 int psvd_stream_update(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, const double* sigma,
                        double ff, int Kc, const double* A, int64_t lda, int B, int K, int rescue,
                        double* U_out, int64_t ldo, double* sigma_out, void* stream);
@@ -155,6 +160,27 @@ int psvd_stream_run(psvd_ctx* ctx, int64_t M, const double* U_in, int64_t ldu, c
                     int nb, const double* const* A, const int64_t* lda, const int* B, int K, double ff, int rescue,
                     double* U_a, double* U_b, int64_t ldo, double* sigma_hist, int* final_buf,
                     void* const* batch_ready, void* stream);
+
+/* The accurate route of one deterministic update (same arguments and result as
+ * psvd_stream_update) at any conditioning and rank: an orthonormal basis Q of the explicit
+ * panel C = [ff U S | A] by Gram deflation (levels of Gram -> Jacobi eig -> keep lambda >
+ * 1e-10 lambda_max -> CholeskyQR2 -> project out, until the residual is at rounding level),
+ * B = Q^T C, the multi-CTA one-sided Jacobi SVD of B^T (relative accuracy, no squaring), the
+ * reference's sign rule on U_R = R V S^-1 with R the Householder R of B (= the R of
+ * qr(C), diag >= 0; streaming.py:97-103, linalg.py:81-104), U_out = Q U_B[:, :K] (orthonormal
+ * by construction), then the drift rescue when rescue != 0.  Synchronizes the host (the
+ * deflation levels are sized from device values).  Uses the exchange hooks when set: every
+ * Gram / projection is summed over the row-partitioned ranks. */
+int psvd_stream_update_accurate(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, const double* sigma,
+                                double ff, int Kc, const double* A, int64_t lda, int B, int K, int rescue,
+                                double* U_out, int64_t ldo, double* sigma_out, void* stream);
+
+/* qr_factor at any conditioning and rank (linalg.py:94-104): the same Gram-deflation basis,
+ * completed to n orthonormal columns (deterministic pseudo-random candidates, projected out),
+ * B = Q^T A, Householder QR of B (one CTA), Q <- Q Q_B.  psvd_qr takes this route itself when
+ * the first Cholesky flags cond(A) > ~1e6.  Synchronizes the host.  Q: M x n (ld ldq), R: n x n. */
+int psvd_qr_robust(psvd_ctx* ctx, int64_t M, int n, const double* A, int64_t lda, double* Q, int64_t ldq, double* R,
+                   void* stream);
 
 /* ---- one-shot distributed SVD helpers (APMOS, dsvd.py:80-173) ----
  * Top-k eigenpairs of a symmetric PSD n x n matrix G (col-major, ld n): V (n x k,
@@ -202,15 +228,15 @@ int psvd_rand_stream_run(psvd_ctx* ctx, int64_t M, const double* U_in, int64_t l
                          void* const* batch_ready, void* stream);
 
 /* ---- dense factorizations behind the reference's linalg boundary ----
- * qr_factor (linalg.py:94-104): psvd_qr, tall A (M >= n, n <= 112): CholeskyQR2, or the shifted
+ * qr_factor (linalg.py:94-104): psvd_qr, tall A (M >= n, any n): CholeskyQR2, or the shifted
  * CholeskyQR3 when the first Cholesky flags cond(A) beyond CholeskyQR2's range (one host sync to
  * read that flag).  Q: M x n (ld ldq), R: n x n (ld n) upper with diag(R) >= 0.
- * svd_full (linalg.py:107-123): psvd_jacobi, one-sided Jacobi SVD of X (m x n, m >= n, n <= 160;
+ * svd_full (linalg.py:107-123): psvd_jacobi, one-sided Jacobi SVD of X (m x n, m >= n, any n;
  * S descending, V n x n), composed with psvd_qr for tall inputs; psvd_sign_pair applies the
  * reference's sign rule (linalg.py:81-91) to U and the same flips to V.
  * randomized_range (linalg.py:126-147): psvd_nn_product (Y = A W, A tall) with psvd_tn_product
  * and psvd_qr.  parallel_qr (dsvd.py:176-202): psvd_gram + rank-ordered sum + psvd_chol
- * (R and R^-1 of a Gram, n <= 112) + psvd_nn_product + psvd_small_matmul (C = op(A) B, small). */
+ * (R and R^-1 of a Gram, any n) + psvd_nn_product + psvd_small_matmul (C = op(A) B, small). */
 int psvd_chol(psvd_ctx* ctx, const double* G, int n, double* R, double* T, void* stream);
 int psvd_chol_shift(psvd_ctx* ctx, double* G, int n, int64_t M, void* stream);
 int psvd_chol_illcond(psvd_ctx* ctx, int* flag, void* stream);
@@ -224,6 +250,13 @@ int psvd_jacobi(psvd_ctx* ctx, const double* X, int64_t ldx, int64_t m, int n, d
                 void* stream);
 int psvd_sign_pair(psvd_ctx* ctx, double* U, int64_t ldu, int64_t rows, int cols, double* V, int64_t ldv,
                    int64_t vrows, void* stream);
+/* svd_full's core for any width (linalg.py:107-123; the reference's dgesdd of the R factor):
+ * multi-CTA one-sided Jacobi on X (m x n, ld ldx) or, with transpose = 1, on X^T of an n x m X.
+ * S (n) descending, V (n x n, ld ldv) the right singular vectors, optional U (m x n, ld ldu) =
+ * X V S^-1 (0 columns for zero singular values).  Bitwise reproducible.  psvd_qr and psvd_chol take
+ * any n as well (one-CTA kernels up to 112 columns, blocked global-memory kernels beyond). */
+int psvd_jacobi_uv(psvd_ctx* ctx, const double* X, int64_t ldx, int64_t m, int n, int transpose, double* S,
+                   double* V, int64_t ldv, double* U, int64_t ldu, void* stream);
 
 /* X[:, j] *= s_j, or /= s_j (0 where s_j == 0) with invert = 1. */
 int psvd_scale_cols(psvd_ctx* ctx, double* X, int64_t ld, int64_t rows, int cols, const double* s, int invert,

@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libpsvd.so")
 SOURCES = ["psvd_tall.cu", "psvd_pass_tma.cu", "psvd_gemm.cu", "psvd_small.cu", "psvd_subspace.cu", "psvd_rand.cu",
-           "psvd_api.cu", "psvd_stream.cu", "psvd_rand_api.cu", "psvd_dense.cu"]
+           "psvd_api.cu", "psvd_stream.cu", "psvd_rand_api.cu", "psvd_dense.cu", "psvd_big.cu", "psvd_accurate.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC"]
 

@@ -25,7 +25,7 @@ if os.environ.get("PSVD_LIB_VARIANT"):  # diagnostics: an in-tree build variant 
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "psvd.h")
 
 PSVD_OK, PSVD_EINVAL, PSVD_ENOCONV, PSVD_ECUDA = 0, 1, 2, 3
-ST_NONFINITE, ST_NOCONVERGE, ST_RESCUE, ST_RANKDEF, ST_CHOLFAIL = 1, 2, 4, 8, 16
+ST_NONFINITE, ST_NOCONVERGE, ST_RESCUE, ST_RANKDEF, ST_CHOLFAIL, ST_ILLCOND = 1, 2, 4, 8, 16, 32
 
 _c_i64 = ctypes.c_int64
 _c_int = ctypes.c_int
@@ -72,6 +72,10 @@ _SIGS = {
     "psvd_qr": (_c_int, [_vp, _c_i64, _c_int, _vp, _c_i64, _vp, _c_i64, _vp, _vp]),
     "psvd_jacobi": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _vp, _vp, _c_i64, _vp]),
     "psvd_sign_pair": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _vp, _c_i64, _c_i64, _vp]),
+    "psvd_stream_update_accurate": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_int, _vp, _c_i64, _c_int,
+                                             _c_int, _c_int, _vp, _c_i64, _vp, _vp]),
+    "psvd_qr_robust": (_c_int, [_vp, _c_i64, _c_int, _vp, _c_i64, _vp, _c_i64, _vp, _vp]),
+    "psvd_jacobi_uv": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _c_int, _vp, _vp, _c_i64, _vp, _c_i64, _vp]),
     "psvd_scale_cols": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _vp, _c_int, _vp]),
     "psvd_rand_last_vt": (_c_int, [_vp, _c_int, _c_int, _c_int, _vp, _c_i64, _vp]),
     "psvd_stream_run_supported": (_c_int, [_vp, _c_i64, _c_int, _c_int, ctypes.POINTER(_c_int)]),
@@ -142,8 +146,11 @@ def require_cuda():
 def context(device=None):
     """The library context of a CUDA device (created once per process)."""
     require_cuda()
-    dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index or 0)
-    idx = dev.index
+    if device is None:
+        idx = torch.cuda.current_device()
+    else:
+        d = torch.device(device)
+        idx = d.index if d.index is not None else torch.cuda.current_device()  # 'cuda' = the current device
     if idx not in _ctxs:
         with _lock:
             if idx not in _ctxs:
@@ -219,8 +226,8 @@ def as_device_colmajor(a, device, name="a"):
             raise ValueError(f"{name} must be 2-D, got {t.dim()}-D")
         if min(t.shape) < 1:
             raise ValueError(f"{name} must have positive dimensions, got {tuple(t.shape)}")
-        if t.device.type == "cuda" and t.dtype == torch.float64:
-            dm = _aligned_colmajor(t)
+        if t.device.type == "cuda" and t.dtype == torch.float64 and t.device == torch.device(device):
+            dm = _aligned_colmajor(t)  # zero copy only for a tensor already on the context's device
             if dm is not None:
                 return dm
         out = DevMat.empty(t.shape[0], t.shape[1], device)

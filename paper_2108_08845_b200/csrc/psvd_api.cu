@@ -534,9 +534,20 @@ extern "C" {
 
 int psvd_version(void) { return 1; }
 
+// The caller's current device is restored on return (the context's kernels run on `device`; the
+// Python layer enters that device around every call).
+struct DeviceGuard {
+  int prev = -1;
+  DeviceGuard() { cudaGetDevice(&prev); }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
 int psvd_create(int device, psvd_ctx** out) {
   if (!out) return PSVD_EINVAL;
   *out = nullptr;
+  DeviceGuard guard;
   if (cudaSetDevice(device) != cudaSuccess) {
     cudaGetLastError();
     return PSVD_ECUDA;
@@ -553,6 +564,9 @@ int psvd_create(int device, psvd_ctx** out) {
   c->d_ssgate = c->d_status + 2;
   if (cudaMalloc(&c->d_timers, 16 * sizeof(long long)) != cudaSuccess) {
     cudaGetLastError();
+    cudaFree(c->d_status);
+    cudaFreeHost(c->h_status);
+    delete c;
     return PSVD_ECUDA;
   }
   cudaMemset(c->d_status, 0, 4 * sizeof(int));
@@ -580,11 +594,12 @@ int psvd_create(int device, psvd_ctx** out) {
 
 int psvd_destroy(psvd_ctx* c) {
   if (!c) return PSVD_OK;
+  DeviceGuard guard;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   Buf* bufs[] = {&c->partial, &c->tiles, &c->gram, &c->eigws, &c->wbuf, &c->utu, &c->tbuf, &c->dvec, &c->colmax,
                  &c->ybuf, &c->ybuf2, &c->xpairs, &c->ssws, &c->rsmall, &c->jacws, &c->partial2, &c->tiles2[0], &c->tiles2[1],
-                 &c->zbuf, &c->rs2, &c->dense, &c->dense2};
+                 &c->zbuf, &c->rs2, &c->dense, &c->dense2, &c->bigws, &c->bigjac, &c->accws, &c->accq};
   for (Buf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
   if (c->s_hi) cudaStreamDestroy(c->s_hi);
@@ -811,7 +826,7 @@ int psvd_drift_rescue(psvd_ctx* c, int64_t M, double* U, int64_t ldu, int K, con
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
   if ((rc = check_mat(c, "U", U, ldu, M, K))) return rc;
-  if (K > MAX_W) return fail(c, PSVD_EINVAL, "K=%d too large for the rescue pass", K);
+  if (K > DRIFT_SMEM_KMAX) return drift_rescue_wide(c, M, U, ldu, K, UtU, sigma, tol, st);
   if ((rc = ensure(c, c->tbuf, sizeof(double) * ((size_t)K * K + K)))) return rc;
   launch_drift_check(UtU, K, tol, sigma, (double*)c->tbuf.ptr, c->d_gate, c->d_status, st);
   c->launches++;
@@ -826,6 +841,58 @@ int psvd_drift_rescue(psvd_ctx* c, int64_t M, double* U, int64_t ldu, int K, con
 }
 
 }  // extern "C"
+
+__global__ void or_status_kernel(int* status, int bits) { atomicOr(status, bits); }
+
+// Drift rescue for K beyond the one-CTA check's shared memory (K > DRIFT_SMEM_KMAX): the deviation
+// max|UtU - I| is read back (one host sync), and when it exceeds tol U <- qr(U).q, sigma <- sigma |diag r|,
+// both reordered stable-descending (streaming.py:106-115) through psvd_qr (any K, rank robust).
+int psvd_internal::drift_rescue_wide(psvd_ctx* c, int64_t M, double* U, int64_t ldu, int K, const double* UtU,
+                                     double* sigma, double tol, cudaStream_t st) {
+  std::vector<double> h((size_t)K * K), sg(K), dg(K);
+  if (cudaMemcpyAsync(h.data(), UtU, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return cuda_check(c, "drift read");
+  double dev = 0.0;
+  for (int j = 0; j < K; ++j)
+    for (int i = 0; i < K; ++i) dev = std::max(dev, std::fabs(h[(size_t)j * K + i] - (i == j ? 1.0 : 0.0)));
+  if (!(dev > tol)) return PSVD_OK;
+  const int64_t ldq = M + (M & 1);
+  Buf q, r;
+  int rc = PSVD_OK;
+  if (cudaMalloc(&q.ptr, sizeof(double) * ldq * K) != cudaSuccess ||
+      cudaMalloc(&r.ptr, sizeof(double) * (size_t)K * K) != cudaSuccess) {
+    cudaFree(q.ptr);
+    return fail(c, PSVD_ECUDA, "drift rescue allocation");
+  }
+  double* Q = (double*)q.ptr;
+  double* R = (double*)r.ptr;
+  if ((rc = psvd_qr(c, M, K, U, ldu, Q, ldq, R, st)) == PSVD_OK) {
+    cudaMemcpyAsync(sg.data(), sigma, sizeof(double) * K, cudaMemcpyDeviceToHost, st);
+    cudaMemcpy2DAsync(dg.data(), sizeof(double), R, sizeof(double) * (K + 1), sizeof(double), K,
+                      cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    std::vector<int> order(K);
+    for (int k = 0; k < K; ++k) {
+      sg[k] *= std::fabs(dg[k]);
+      order[k] = k;
+    }
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return sg[a] > sg[b]; });
+    std::vector<double> so(K);
+    for (int k = 0; k < K; ++k) {
+      so[k] = sg[order[k]];
+      cudaMemcpyAsync(U + (size_t)k * ldu, Q + (size_t)order[k] * ldq, sizeof(double) * M, cudaMemcpyDeviceToDevice,
+                      st);
+    }
+    cudaMemcpyAsync(sigma, so.data(), sizeof(double) * K, cudaMemcpyHostToDevice, st);
+    or_status_kernel<<<1, 1, 0, st>>>(c->d_status, PSVD_ST_RESCUE);
+    c->launches++;
+    cudaStreamSynchronize(st);  // so's host buffer
+  }
+  cudaFree(q.ptr);
+  cudaFree(r.ptr);
+  return rc ? rc : cuda_check(c, "drift rescue wide");
+}
 
 // Core solve of a Gram: eig (+ concurrent LDL^T on the aux stream when the split path applies)
 int psvd_internal::core_solve(psvd_ctx* c, const double* G, int n, int K, const double* dscale, double* W, double* sigma,
@@ -865,7 +932,7 @@ int psvd_internal::refine_normalize(psvd_ctx* c, int64_t M, double* U, int64_t l
   int rc = ensure(c, c->tbuf, sizeof(double) * ((size_t)K * K + K));
   if (rc) return rc;
   double* scale = (double*)c->tbuf.ptr + (size_t)K * K;
-  launch_normalize_gram(UtU, K, sigma, scale, st);
+  launch_normalize_gram(UtU, K, sigma, scale, c->d_status, st);
   launch_scale_cols(U, ld, M, K, scale, st);
   c->launches += 2;
   return cuda_check(c, "refine");

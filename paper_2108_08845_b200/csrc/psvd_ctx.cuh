@@ -45,6 +45,8 @@ struct psvd_ctx {
   Buf partial2, tiles2[2];  // A^T A passes on the low-priority stream (double-buffered tiles)
   Buf zbuf, rs2;            // pipelined randomized stream: look-ahead sketch Z = A Omega_A, small matrices
   Buf dense, dense2;        // dense utilities (psvd_qr / psvd_jacobi): small factors, a tall temporary
+  Buf bigws, bigjac;        // any-width Cholesky / Jacobi workspaces (psvd_big.cu)
+  Buf accws, accq;          // accurate R-factor route of the deterministic update: small factors, tall Q
   cudaEvent_t ev_qready = nullptr;  // pipelined randomized stream: the sketch basis of the last update is final
   cudaStream_t s_hi = nullptr, s_lo = nullptr;  // pipelined stream_run: critical chain / look-ahead Grams
   cudaStream_t s_aux = nullptr;                  // concurrent LDL^T of the split core solve
@@ -90,7 +92,16 @@ int core_solve(psvd_ctx* c, const double* G, int n, int K, const double* dscale,
 // sigma_k <- ||C v_k|| and unit columns (Rayleigh refinement), UtU normalized in place
 int refine_normalize(psvd_ctx* c, int64_t M, double* U, int64_t ld, int K, double* UtU, double* sigma,
                      cudaStream_t st);
+// drift rescue beyond the one-CTA check (K > DRIFT_SMEM_KMAX): host-checked, psvd_qr based
+int drift_rescue_wide(psvd_ctx* c, int64_t M, double* U, int64_t ldu, int K, const double* UtU, double* sigma,
+                      double tol, cudaStream_t st);
 // exchange points of the row-partitioned updates (no-ops on one GPU)
 int ex_allreduce(psvd_ctx* c, double* buf, int64_t count, cudaStream_t st);
+// Cholesky R and R^-1 of an n x n Gram for any n (the one-CTA kernel up to CHOL_NMAX, psvd_big.cu beyond)
+int chol_any(psvd_ctx* c, const double* G, int n, double* T, int* illcond, int* status, double* Rout,
+             cudaStream_t st);
+// one-sided Jacobi SVD for any n (psvd_big.cu): S, V (ld ldv), optional U = X V S^-1 (ld ldu)
+int jacobi_any(psvd_ctx* c, const double* X, int64_t ldx, int64_t m, int n, int transpose, double* S, double* V,
+               int64_t ldv, double* U, int64_t ldu, cudaStream_t st);
 
 }  // namespace psvd_internal

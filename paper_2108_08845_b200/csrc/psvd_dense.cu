@@ -25,6 +25,31 @@ __global__ void scale_cols_any_kernel(double* __restrict__ X, int64_t ld, int64_
   x = invert ? (f != 0.0 ? x / f : 0.0) : x * f;
 }
 
+int chol_any(psvd_ctx* c, const double* G, int n, double* T, int* illcond, int* status, double* Rout,
+             cudaStream_t st) {
+  if (n <= CHOL_NMAX) {
+    launch_chol_inv(G, n, T, st, illcond, status, Rout);
+    c->launches++;
+    return cuda_check(c, "chol");
+  }
+  int rc = ensure(c, c->bigws, sizeof(double) * chol_big_workspace_doubles(n));
+  if (rc) return rc;
+  launch_chol_big(G, n, T, illcond, status, Rout, (double*)c->bigws.ptr, st);
+  c->launches += chol_big_launches(n);
+  return cuda_check(c, "chol big");
+}
+
+int jacobi_any(psvd_ctx* c, const double* X, int64_t ldx, int64_t m, int n, int transpose, double* S, double* V,
+               int64_t ldv, double* U, int64_t ldu, cudaStream_t st) {
+  int rc = ensure(c, c->bigjac, sizeof(double) * jacobi_big_workspace_doubles(m, n));
+  if (rc) return rc;
+  const int e = launch_jacobi_big(X, ldx, m, n, transpose, S, V, ldv, U, ldu, (double*)c->bigjac.ptr, c->d_status,
+                                  nullptr, c->num_sms, st);
+  c->launches += 2;
+  if (e != 0) return fail(c, PSVD_ECUDA, "jacobi launch: %s", cudaGetErrorString((cudaError_t)e));
+  return cuda_check(c, "jacobi big");
+}
+
 }  // namespace psvd_internal
 
 extern "C" {
@@ -35,10 +60,8 @@ extern "C" {
 
 int psvd_chol(psvd_ctx* c, const double* G, int n, double* R, double* T, void* stream) {
   if (!c) return PSVD_EINVAL;
-  if (n < 1 || n > CHOL_NMAX || !G || !T) return fail(c, PSVD_EINVAL, "bad Cholesky n=%d (1..%d)", n, CHOL_NMAX);
-  launch_chol_inv(G, n, T, (cudaStream_t)stream, c->d_status + 3, c->d_status, R);
-  c->launches++;
-  return cuda_check(c, "chol");
+  if (n < 1 || !G || !T) return fail(c, PSVD_EINVAL, "bad Cholesky n=%d", n);
+  return chol_any(c, G, n, T, c->d_status + 3, c->d_status, R, (cudaStream_t)stream);
 }
 
 int psvd_chol_shift(psvd_ctx* c, double* G, int n, int64_t M, void* stream) {
@@ -79,31 +102,27 @@ int psvd_small_matmul(psvd_ctx* c, const double* A, int lda, int transA, const d
   return cuda_check(c, "small matmul");
 }
 
-// Tall QR (M >= n, n <= CHOL_NMAX): CholeskyQR2 (R = R2 R1 from two Gram passes), or the shifted
-// CholeskyQR3 when the first Cholesky flags cond(A) beyond CholeskyQR2's range.  diag(R) >= 0 by
-// construction (qr_factor's sign convention, linalg.py:94-104); numerically null directions give zero
-// rows of R and zero columns of Q.  R: n x n, ld n.
+// Tall QR (M >= n, any n: one-CTA Cholesky up to CHOL_NMAX, the global-memory one beyond): CholeskyQR2
+// (R = R2 R1 from two Gram passes), or psvd_qr_robust (psvd_accurate.cu: Gram deflation + Householder
+// QR of the small factor) when the first Cholesky flags cond(A) beyond CholeskyQR2's range or a rank
+// deficiency.  diag(R) >= 0 (qr_factor's sign convention, linalg.py:94-104).  R: n x n, ld n.
 int psvd_qr(psvd_ctx* c, int64_t M, int n, const double* A, int64_t lda, double* Q, int64_t ldq, double* R,
             void* stream) {
   if (!c) return PSVD_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
-  if (n < 1 || n > CHOL_NMAX || M < n) return fail(c, PSVD_EINVAL, "qr needs M >= n and n <= %d (M=%lld n=%d)",
-                                                  CHOL_NMAX, (long long)M, n);
+  if (n < 1 || M < n) return fail(c, PSVD_EINVAL, "qr needs M >= n >= 1 (M=%lld n=%d)", (long long)M, n);
   if ((rc = check_mat(c, "A", A, lda, M, n)) || (rc = check_mat(c, "Q", Q, ldq, M, n))) return rc;
   if (!R) return fail(c, PSVD_EINVAL, "R is null");
   const size_t nn = (size_t)n * n;
   const int64_t ldt = M + (M & 1);
-  if ((rc = ensure(c, c->dense, sizeof(double) * 8 * nn)) || (rc = ensure(c, c->dense2, sizeof(double) * ldt * n)))
+  if ((rc = ensure(c, c->dense, sizeof(double) * 5 * nn)) || (rc = ensure(c, c->dense2, sizeof(double) * ldt * n)))
     return rc;
   double* G = (double*)c->dense.ptr;
   double* R1 = G + nn;
   double* T1 = R1 + nn;
   double* R2 = T1 + nn;
   double* T2 = R2 + nn;
-  double* R3 = T2 + nn;
-  double* T3 = R3 + nn;
-  double* Rt = T3 + nn;
   double* tmp = (double*)c->dense2.ptr;
   auto gram = [&](const double* X, int64_t ldx) { return psvd_gram(c, M, nullptr, 0, nullptr, 1.0, 0, X, ldx, n, G, st); };
   auto mul = [&](const double* X, int64_t ldx, const double* T, double* Y, int64_t ldy) {
@@ -114,7 +133,7 @@ int psvd_qr(psvd_ctx* c, int64_t M, int n, const double* A, int64_t lda, double*
   auto refine = [&](double* Rk, double* Tk) -> int {  // Q <- Q chol(Q^T Q)^-1, returns the new factor in Rk
     int r;
     if ((r = gram(Q, ldq))) return r;
-    launch_chol_inv(G, n, Tk, st, nullptr, c->d_status, Rk);
+    if ((r = chol_any(c, G, n, Tk, nullptr, c->d_status, Rk, st))) return r;
     mul(Q, ldq, Tk, tmp, ldt);
     cudaMemcpy2DAsync(Q, ldq * sizeof(double), tmp, ldt * sizeof(double), M * sizeof(double), n,
                       cudaMemcpyDeviceToDevice, st);
@@ -123,25 +142,14 @@ int psvd_qr(psvd_ctx* c, int64_t M, int n, const double* A, int64_t lda, double*
   };
   // CholeskyQR2
   if ((rc = gram(A, lda))) return rc;
-  launch_chol_inv(G, n, T1, st, c->d_status + 3, c->d_status, R1);
-  c->launches++;
+  if ((rc = chol_any(c, G, n, T1, c->d_status + 3, c->d_status, R1, st))) return rc;
   int ill = 0;
   if ((rc = psvd_chol_illcond(c, &ill, stream))) return rc;
-  if (ill) {  // shifted CholeskyQR3
-    if ((rc = gram(A, lda))) return rc;
-    launch_chol_shift(G, n, M, st);
-    launch_chol_inv(G, n, T1, st, nullptr, c->d_status, R1);
-    c->launches += 2;
-  }
+  if (ill) return psvd_qr_robust(c, M, n, A, lda, Q, ldq, R, stream);  // beyond CholeskyQR2's range / rank deficient
   mul(A, lda, T1, Q, ldq);
   if ((rc = refine(R2, T2))) return rc;
-  launch_small_gemm(R2, n, 0, R1, n, ill ? Rt : R, n, n, n, n, nullptr, st);  // R2 R1
+  launch_small_gemm(R2, n, 0, R1, n, R, n, n, n, n, nullptr, st);  // R2 R1
   c->launches++;
-  if (ill) {
-    if ((rc = refine(R3, T3))) return rc;
-    launch_small_gemm(R3, n, 0, Rt, n, R, n, n, n, n, nullptr, st);  // R3 R2 R1
-    c->launches++;
-  }
   return cuda_check(c, "qr");
 }
 
@@ -152,9 +160,10 @@ int psvd_jacobi(psvd_ctx* c, const double* X, int64_t ldx, int64_t m, int n, dou
   if (!c) return PSVD_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
-  if (n < 1 || n > JACOBI_NMAX || m < n || m > (int64_t)INT32_MAX)
-    return fail(c, PSVD_EINVAL, "jacobi needs m >= n and n <= %d (m=%lld n=%d)", JACOBI_NMAX, (long long)m, n);
+  if (n < 1 || m < n || m > (int64_t)INT32_MAX)
+    return fail(c, PSVD_EINVAL, "jacobi needs m >= n >= 1 (m=%lld n=%d)", (long long)m, n);
   if (!X || !S || !V || ldx < m || ldv < n) return fail(c, PSVD_EINVAL, "bad jacobi arguments");
+  if (n > JACOBI_NMAX) return jacobi_any(c, X, ldx, m, n, 0, S, V, ldv, nullptr, 0, st);
   const size_t mn = (size_t)m * n;
   if ((rc = ensure(c, c->dense2, sizeof(double) * (mn + (size_t)n * n))) ||
       (rc = ensure(c, c->jacws, sizeof(double) * jacobi_workspace_doubles((int)m, n))))
@@ -167,6 +176,16 @@ int psvd_jacobi(psvd_ctx* c, const double* X, int64_t ldx, int64_t m, int n, dou
   cudaMemcpy2DAsync(V, ldv * sizeof(double), J, n * sizeof(double), n * sizeof(double), n, cudaMemcpyDeviceToDevice, st);
   c->launches++;
   return cuda_check(c, "jacobi");
+}
+
+// One-sided Jacobi SVD of any width on the global-memory kernel: X (m x n, ld ldx) or, with
+// transpose = 1, X^T of an n x m X.  S (n) descending, V (n x n, ld ldv), optional U = X V S^-1.
+int psvd_jacobi_uv(psvd_ctx* c, const double* X, int64_t ldx, int64_t m, int n, int transpose, double* S, double* V,
+                   int64_t ldv, double* U, int64_t ldu, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  if (n < 1 || m < 1 || !X || !S || !V || ldv < n || (U && ldu < m) || ldx < (transpose ? n : m))
+    return fail(c, PSVD_EINVAL, "bad jacobi_uv arguments (m=%lld n=%d)", (long long)m, n);
+  return jacobi_any(c, X, ldx, m, n, transpose, S, V, ldv, U, ldu, (cudaStream_t)stream);
 }
 
 // The reference's sign rule (linalg.py:81-91): per column of U (rows x cols) the entry of largest

@@ -948,7 +948,7 @@ void launch_sign_weights(const double* Lg, const double* Z, const double* sigma,
 // eigenvector error, vs eps*kappa^2 for sqrt(lambda)).  sigma_k <- ||C v_k||,
 // UtU <- D^-1 UtU D^-1 (D = diag ||u_k||) and scale_k = 1 / ||u_k|| for the columns.
 __global__ void normalize_gram_kernel(double* __restrict__ UtU, int K, double* __restrict__ sigma,
-                                      double* __restrict__ scale) {
+                                      double* __restrict__ scale, int* __restrict__ status) {
   __shared__ double nk[1024];
   for (int k = threadIdx.x; k < K; k += blockDim.x) {
     const double d = UtU[(size_t)k * K + k];
@@ -963,10 +963,15 @@ __global__ void normalize_gram_kernel(double* __restrict__ UtU, int K, double* _
     sigma[k] *= nk[k];
     scale[k] = 1.0 / nk[k];
   }
+  // conditioning gate of the Gram route: its kept values carry eps (s_1 / s_k)^2 error terms, so a
+  // kept spectrum wider than GRAM_KAPPA_MAX flags the update for the accurate (R-factor) route
+  __syncthreads();
+  if (threadIdx.x == 0 && status != nullptr && K > 0 && !(sigma[K - 1] * GRAM_KAPPA_MAX >= sigma[0]))
+    atomicOr(status, PSVD_ST_ILLCOND);
 }
 
-void launch_normalize_gram(double* UtU, int K, double* sigma, double* scale, cudaStream_t st) {
-  normalize_gram_kernel<<<1, 1024, 0, st>>>(UtU, K, sigma, scale);
+void launch_normalize_gram(double* UtU, int K, double* sigma, double* scale, int* status, cudaStream_t st) {
+  normalize_gram_kernel<<<1, 1024, 0, st>>>(UtU, K, sigma, scale, status);
 }
 
 // ---------------------------------------------------------------- drift check / rescue

@@ -62,14 +62,18 @@ void launch_sign_weights(const double* Lg, const double* Z, const double* sigma,
                          double* W, double* sigma_out, int* status, double rank_tol, cudaStream_t st);
 bool eig_supported(int n, int K);
 
-// Rayleigh refinement of sigma from the recomposed columns' norms (see psvd_small.cu).
-void launch_normalize_gram(double* UtU, int K, double* sigma, double* scale, cudaStream_t st);
+// Rayleigh refinement of sigma from the recomposed columns' norms (see psvd_small.cu); sets
+// PSVD_ST_ILLCOND in *status when sigma_1 / sigma_K > GRAM_KAPPA_MAX (the Gram route's accuracy gate).
+constexpr double GRAM_KAPPA_MAX = 300.0;
+void launch_normalize_gram(double* UtU, int K, double* sigma, double* scale, int* status, cudaStream_t st);
 
 // Drift check of streaming.py:106-115 on the K x K Gram UtU = U_new^T U_new:
 // if max|UtU - I| > tol: T = rr^{-1}[:, order] with rr = chol(UtU) (= qr(U).R),
 // sigma <- (sigma * |diag rr|)[order] (stable descending), *gate = 1; else *gate = 0.
 void launch_drift_check(const double* UtU, int K, double tol, double* sigma, double* T, int* gate,
                         int* status, cudaStream_t st);
+// the check keeps (2 K^2 + K + 65 + (K + 1) / 2) doubles in shared memory: K <= 120 within 227 KB
+constexpr int DRIFT_SMEM_KMAX = 120;
 
 // ---- randomized-update helpers (psvd_rand.cu)
 void launch_small_gemm(const double* A, int lda, int transA, const double* B, int ldb, double* C, int ldc, int m,
@@ -87,6 +91,21 @@ void launch_colmax_reduce(const double* colmax, int nchunks, int K, double* out,
 void launch_svqb_scale(double* T, const double* S, int l, double tol, cudaStream_t st, const int* gate = nullptr);
 void launch_scale_cols(double* U, int64_t ld, int64_t M, int K, const double* s, cudaStream_t st);
 void launch_scale_rows(const double* X, int ldx, int m, int k, const double* d, double* Y, int ldy, cudaStream_t st);
+
+// ---- any-width dense kernels, operands in global memory (psvd_big.cu)
+// chol_big: same contract as launch_chol_inv (T = R^-1, optional Rout, zero rows for numerically null
+// pivots, *illcond for cond > ~1e6) for any n; ws: chol_big_workspace_doubles(n).
+size_t chol_big_workspace_doubles(int n);
+void launch_chol_big(const double* G, int n, double* T, int* illcond, int* status, double* Rout, double* ws,
+                     cudaStream_t st);
+int chol_big_launches(int n);
+// jacobi_big: one-sided Jacobi SVD of X (m x n, ld ldx; transpose = 1 takes X^T of an n x m X):
+// S (n, descending), V (n x n, ld ldv) the accumulated rotations (right singular vectors), optional
+// U (m x n, ld ldu) = X V S^-1.  ws: jacobi_big_workspace_doubles(m, n).  Returns a cudaError_t.
+size_t jacobi_big_workspace_doubles(int64_t m, int n);
+int launch_jacobi_big(const double* X, int64_t ldx, int64_t m, int n, int transpose, double* S, double* V,
+                      int64_t ldv, double* U, int64_t ldu, double* ws, int* status, int* sweeps_out, int num_sms,
+                      cudaStream_t st);
 
 // ---- pipelined randomized stream glue (psvd_rand.cu; see psvd_rand_stream_run)
 void launch_rs_prep(const double* sgn, const double* Wf, int lq, int K, const double* sigma, double ff,

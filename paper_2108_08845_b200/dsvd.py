@@ -140,6 +140,34 @@ def _row_offset(ctx, rows, dev):
     return sum(counts[:ctx.rank]), sum(counts)
 
 
+class exchange_hooks:
+    """Context manager: the library's exchange hooks (psvd_set_exchange) on this RankContext
+    for the calls inside; a collective failure re-raises the hook's exception."""
+
+    def __init__(self, ctx, dev, row_offset=None):
+        self.ctx, self.dev = ctx, dev
+        self.off = row_offset
+
+    def __enter__(self):
+        self.c = nat.context(self.dev)
+        if self.ctx.world_size == 1:
+            self.ex = None
+            return self
+        if self.off is None:
+            raise ValueError("exchange_hooks needs the rank's global row offset")
+        self.ex = _Exchange(self.ctx, self.dev)
+        nat.call("psvd_set_exchange", self.c, ctypes.cast(self.ex.ar, nat._vp), ctypes.cast(self.ex.ag, nat._vp),
+                 None, self.ctx.world_size, self.off)
+        return self
+
+    def __exit__(self, et, ev, tb):
+        if self.ex is not None:
+            nat.call("psvd_set_exchange", self.c, None, None, None, 1, 0)
+            if et is not None and issubclass(et, RuntimeError) and self.ex.error is not None:
+                raise self.ex.error
+        return False
+
+
 def _parallel_rand_update(ctx, U, sigma, A, sketch, ff, dev):
     from .linalg import randomized_update
     c = nat.context(dev)
@@ -183,6 +211,16 @@ def _parallel_update(ctx, U, sigma, A, k, ff, dev):
         utu = allreduce_ordered(utu, ctx)  # global U^T U: Rayleigh refinement of sigma, unit columns
         nat.call("psvd_refine_normalize", c, M, nat._vp(out.data_ptr()), out.ld, k, nat.ptr(utu), nat.ptr(sig), st)
         status = nat.read_status(c, reset=True, device=dev)
+        if status & nat.ST_ILLCOND and not status & nat.ST_NONFINITE:
+            # kept spectrum beyond the Gram route's accuracy (identical sigma bits on every rank, so
+            # every rank takes this branch): the accurate route, its Grams summed over the ranks
+            from . import streaming
+            streaming.ACCURATE_UPDATES += 1
+            off, _ = _row_offset(ctx, M, dev)
+            with exchange_hooks(ctx, dev, off):
+                nat.call("psvd_stream_update_accurate", c, M, uptr, uld, sptr, float(ff), kc, nat._vp(A.data_ptr()),
+                         A.ld, B, k, 0, nat._vp(out.data_ptr()), out.ld, nat.ptr(sig), st)
+            status |= nat.read_status(c, reset=True, device=dev)
     if status & nat.ST_NONFINITE:
         raise ValueError("a_local contains non-finite entries")
     return out, sig
@@ -230,52 +268,83 @@ def parallel_stream_incorporate(ctx, state, a_new_local, config):
 def parallel_stream_all(ctx, batches_local, config, device=None):
     """Row-partitioned stream over this rank's batches (B200 extension: the reference drives
     parallel_stream_initialize / parallel_stream_incorporate batch by batch, cli.py:262-276;
-    same update rule, dsvd.py:205-242, no drift rescue).  Deterministic configs run in windows
+    same update rule, dsvd.py:205-242, no drift rescue).  The iterable is consumed lazily, one
+    window at a time.  Deterministic configs run in windows
     through the pipelined psvd_stream_run with the exchange hooks: per update a rank-ordered
     sum of the streaming Gram (first rank contributes the already-global U^T U block) and of
     U^T U, so every rank factors identical bits; the next batch's A^T A still overlaps the
     replicated core solve.  Randomized configs update batch by batch.  Returns
     (LocalModes, history of singular values)."""
-    from .streaming import STREAM_WINDOW, _run_window
-    batches_local = list(batches_local)
-    if not batches_local:
-        raise ValueError("batch stream is empty")
-    dev = torch.device(device) if device is not None else _device(batches_local[0])
+    from .streaming import StreamState, _run_window, window_length
     k = config.k_modes
-    if config.sketch is not None:
-        st = parallel_stream_initialize(ctx, batches_local[0], config)
+    it = iter(batches_local)
+    first = next(it, None)
+    if first is None:
+        raise ValueError("batch stream is empty")
+    dev = torch.device(device) if device is not None else _device(first)
+    if config.sketch is not None:  # per batch; the iterable is consumed lazily
+        st = parallel_stream_initialize(ctx, first, config)
         hist = [st.singular_values.clone()]
-        for b in batches_local[1:]:
+        for b in it:
             st = parallel_stream_incorporate(ctx, st, b, config)
             hist.append(st.singular_values.clone())
         return st, hist
-    mats = [nat.as_device_colmajor(b, dev, "a_local") for b in batches_local]
-    M = mats[0].rows
     c = nat.context(dev)
-    ok = ctypes.c_int(0)
-    nat.call("psvd_stream_run_supported", c, M, k, max(m.cols for m in mats), ctypes.byref(ok))
-    flag = torch.tensor([float(ok.value)], dtype=torch.float64,
-                        device=dev if (ctx.world_size > 1 and dist.get_backend(ctx.group) == "nccl") else "cpu")
-    if ctx.world_size > 1:  # every rank takes the same route
-        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=ctx.group)
-    if not flag.item():
-        st = parallel_stream_initialize(ctx, mats[0], config)
-        hist = [st.singular_values.clone()]
-        for m in mats[1:]:
-            st = parallel_stream_incorporate(ctx, st, m, config)
-            hist.append(st.singular_values.clone())
-        return st, hist
-    off, _ = _row_offset(ctx, M, dev)
+    wlen = window_length(first, dev)
+    off = None
     ex = None
-    if ctx.world_size > 1:
-        ex = _Exchange(ctx, dev)
-        nat.call("psvd_set_exchange", c, ctypes.cast(ex.ar, nat._vp), ctypes.cast(ex.ag, nat._vp), None,
-                 ctx.world_size, off)
     state, hist = None, []
-    try:
-        for w0 in range(0, len(mats), STREAM_WINDOW):
-            state, h = _run_window(state, mats[w0:w0 + STREAM_WINDOW], config, dev, rescue=False, ok=True)
+
+    def per_batch(st0, window):
+        # the batches this route handles one update at a time (too wide for the pipelined kernels,
+        # or an update of the window left the Gram route's accuracy range): the row-parallel update
+        # (accurate route where gated), the run's exchange hooks off meanwhile
+        if ex is not None:
+            nat.call("psvd_set_exchange", c, None, None, None, 1, 0)
+        try:
+            st = None if st0 is None else LocalModes(st0.modes, st0.singular_values)
+            out = []
+            for m in window:
+                st = parallel_stream_initialize(ctx, m, config) if st is None else \
+                    parallel_stream_incorporate(ctx, st, m, config)
+                out.append(st.singular_values.clone())
+            it0 = -1 if st0 is None else st0.iteration
+            return StreamState(st.modes, st.singular_values, it0 + len(window)), out
+        finally:
+            if ex is not None:
+                nat.call("psvd_set_exchange", c, ctypes.cast(ex.ar, nat._vp), ctypes.cast(ex.ag, nat._vp), None,
+                         ctx.world_size, off)
+
+    def run(window):
+        nonlocal state, off, ex
+        M = window[0].rows
+        ok = ctypes.c_int(0)
+        nat.call("psvd_stream_run_supported", c, M, k, max(m.cols for m in window), ctypes.byref(ok))
+        flag = torch.tensor([float(ok.value)], dtype=torch.float64,
+                            device=dev if (ctx.world_size > 1 and dist.get_backend(ctx.group) == "nccl") else "cpu")
+        if ctx.world_size > 1:  # every rank takes the same route
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=ctx.group)
+        if not flag.item():
+            state, h = per_batch(state, window)
             hist.extend(h)
+            return
+        if off is None:
+            off, _ = _row_offset(ctx, M, dev)
+            if ctx.world_size > 1:
+                ex = _Exchange(ctx, dev)
+                nat.call("psvd_set_exchange", c, ctypes.cast(ex.ar, nat._vp), ctypes.cast(ex.ag, nat._vp), None,
+                         ctx.world_size, off)
+        state, h = _run_window(state, window, config, dev, rescue=False, ok=True, on_illcond=per_batch)
+        hist.extend(h)
+
+    try:
+        window = [nat.as_device_colmajor(first, dev, "a_local")]
+        for b in it:
+            if len(window) == wlen:
+                run(window)
+                window = []
+            window.append(nat.as_device_colmajor(b, dev, "a_local"))
+        run(window)
     except (RuntimeError, ValueError):
         if ex is not None and ex.error is not None:
             raise ex.error
@@ -310,24 +379,22 @@ def gather_modes(ctx, local_modes, root=0):
 def parallel_qr(ctx, a_local, device=None):
     """Tall-skinny QR of the row-stacked global matrix (dsvd.py:176-202): QrResult(q_local,
     r) with r identical on every rank.  World size 1 is qr_factor.  Otherwise a
-    distributed CholeskyQR2 (shifted CholeskyQR3 when ill conditioned): every Gram is a
+    distributed CholeskyQR2 (the rank-robust Gram-deflation route, psvd_qr_robust, when the
+    first Cholesky flags an ill-conditioned or rank-deficient matrix): every Gram is a
     rank-ordered allreduce of the local Grams, so every rank factors identical bits, and
-    q_local = a_local R^-1 stays local (no q slices on the wire, unlike the reference's
-    gather / send / broadcast of the TSQR tree)."""
-    from .linalg import QR_MAX_COLS, QrResult, qr_factor
+    q_local stays local (no q slices on the wire, unlike the reference's gather / send /
+    broadcast of the TSQR tree)."""
+    from .linalg import QrResult, qr_factor
     if ctx.world_size == 1:
         return qr_factor(a_local, device)
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     A = nat.as_device_colmajor(a_local, dev, "a_local")
     m, n = A.rows, A.cols
-    if n > QR_MAX_COLS:
-        raise ValueError(f"parallel_qr on the device supports up to {QR_MAX_COLS} columns, got {n}")
     c = nat.context(dev)
     st = nat.stream_ptr(dev)
-    rows = torch.tensor([float(m)], dtype=torch.float64,
-                        device=dev if dist.get_backend(ctx.group) == "nccl" else torch.device("cpu"))
-    dist.all_reduce(rows, group=ctx.group)
-    m_total = int(rows.item())
+    off, m_total = _row_offset(ctx, m, dev)
+    if m_total < n:
+        raise ValueError(f"parallel_qr needs at least as many rows as columns ({m_total} < {n})")
 
     nccl = dist.get_backend(ctx.group) == "nccl"
 
@@ -361,17 +428,19 @@ def parallel_qr(ctx, a_local, device=None):
         R1, T1 = chol(G)
         flag = ctypes.c_int(0)
         nat.call("psvd_chol_illcond", c, ctypes.byref(flag), st)
-        if flag.value:  # shifted CholeskyQR3 (the flag is computed from identical bits on every rank)
-            nat.call("psvd_chol_shift", c, nat.ptr(G), n, m_total, st)
-            R1, T1 = chol(G)
-        Q = times(A, T1)
-        R2, T2 = chol(gram(Q))
-        Q = times(Q, T2)
-        R = rmul(R2, R1)
         if flag.value:
-            R3, T3 = chol(gram(Q))
-            Q = times(Q, T3)
-            R = rmul(R3, R)
+            # beyond CholeskyQR2 (the flag comes from identical bits on every rank): the rank-robust
+            # Gram-deflation route with every Gram / projection summed over the ranks
+            Q = nat.DevMat.empty(m, n, dev)
+            R = torch.empty((n, n), dtype=torch.float64, device=dev)
+            with exchange_hooks(ctx, dev, off):
+                nat.call("psvd_qr_robust", c, m, n, nat._vp(A.data_ptr()), A.ld, nat._vp(Q.data_ptr()), Q.ld,
+                         nat.ptr(R), st)
+        else:
+            Q = times(A, T1)
+            R2, T2 = chol(gram(Q))
+            Q = times(Q, T2)
+            R = rmul(R2, R1)
         st_word = nat.read_status(c, reset=True, device=dev)
     if st_word & nat.ST_NONFINITE:
         raise ValueError("a_local contains non-finite entries")

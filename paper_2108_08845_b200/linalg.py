@@ -123,8 +123,8 @@ def low_rank_svd(a, config, device=None):
 QrResult = namedtuple("QrResult", ["q", "r"])
 SvdResult = namedtuple("SvdResult", ["u", "s", "vt"])
 
-QR_MAX_COLS = 112      # CHOL_NMAX: R and R^-1 of a Gram in one CTA's shared memory
-JACOBI_MAX_COLS = 160  # JACOBI_NMAX: the one-sided Jacobi rotation accumulator in shared memory
+QR_SMEM_COLS = 112      # CHOL_NMAX: R and R^-1 of a Gram in one CTA's shared memory (wider: psvd_big.cu)
+JACOBI_SMEM_COLS = 160  # JACOBI_NMAX: the one-CTA Jacobi's rotation accumulator (wider: psvd_big.cu)
 
 
 def _dev(device):
@@ -143,71 +143,32 @@ def _check(ctx, dev, what):
 
 
 def _tall_qr(A, dev):
-    """(Q DevMat m x n, R (n x n) tensor) of a tall DevMat (m >= n) on the device."""
+    """(Q DevMat m x n, R (n x n) tensor) of a tall DevMat (m >= n) on the device: CholeskyQR2,
+    or the rank-robust route (psvd_qr_robust) when the first Cholesky flags an
+    ill-conditioned or rank-deficient input; numerically null directions get an orthonormal
+    completion in q, as Householder QR gives (linalg.py:94-104)."""
     import torch
     from . import _native as nat
     m, n = A.rows, A.cols
-    if n > QR_MAX_COLS:
-        raise ValueError(f"qr_factor on the device supports up to {QR_MAX_COLS} columns, got {n}")
     ctx = nat.context(dev)
     Q = nat.DevMat.empty(m, n, dev)
     R = torch.empty((n, n), dtype=torch.float64, device=dev)  # column-major (n x n): R.T is the matrix
     with torch.cuda.device(dev):
-        nat.call("psvd_qr", ctx, m, n, nat._vp(A.data_ptr()), A.ld, nat._vp(Q.data_ptr()), Q.ld, nat.ptr(R),
-                 nat.stream_ptr(dev))
-        dropped = torch.nonzero(torch.diagonal(R) == 0.0).flatten().tolist()
-        if dropped:
-            _complete_basis(Q, dropped, dev)
+        try:
+            nat.call("psvd_qr", ctx, m, n, nat._vp(A.data_ptr()), A.ld, nat._vp(Q.data_ptr()), Q.ld, nat.ptr(R),
+                     nat.stream_ptr(dev))
+        except ValueError:
+            nat.read_status(ctx, reset=True, device=dev)  # the failed call's status bits are reported here
+            raise
     return Q, R.T
-
-
-def _complete_basis(Q, cols, dev):
-    """Rank-deficient input: CholeskyQR leaves the columns of numerically null directions at
-    zero (their rows of R are zero, so q r still reconstructs a).  Householder QR returns an
-    orthonormal q there (linalg.py:94-104 promises orthonormal columns), so fill them with
-    unit vectors orthogonal to every other column: e_i (lowest i first) projected out twice
-    (classical Gram-Schmidt with re-orthogonalization on the library's products), kept when
-    at least half its norm survives."""
-    import torch
-    from . import _native as nat
-    ctx = nat.context(dev)
-    st = nat.stream_ptr(dev)
-    m, n = Q.rows, Q.cols
-    v = nat.DevMat.empty(m, 1, dev)
-    c = torch.empty((n, 1), dtype=torch.float64, device=dev)
-    nrm = torch.empty((1, 1), dtype=torch.float64, device=dev)
-    neg = torch.tensor([-1.0], dtype=torch.float64, device=dev)
-    i = 0
-    for j in cols:
-        while i < m:
-            v.view.zero_()
-            v.view[i, 0] = 1.0
-            i += 1
-            for _ in range(2):
-                nat.call("psvd_tn_product", ctx, m, nat._vp(Q.data_ptr()), Q.ld, n, nat._vp(v.data_ptr()), v.ld, 1,
-                         nat.ptr(c), n, st)
-                nat.call("psvd_scale_cols", ctx, nat.ptr(c), n, n, 1, nat.ptr(neg), 0, st)
-                # v += Q (-c): Q times the small vector, added through a second column of the product
-                w = nat.DevMat.empty(m, 1, dev)
-                nat.call("psvd_nn_product", ctx, m, nat._vp(Q.data_ptr()), Q.ld, n, nat.ptr(c), n, 1,
-                         nat._vp(w.data_ptr()), w.ld, st)
-                v.view.add_(w.view)
-            nat.call("psvd_tn_product", ctx, m, nat._vp(v.data_ptr()), v.ld, 1, nat._vp(v.data_ptr()), v.ld, 1,
-                     nat.ptr(nrm), 1, st)
-            norm = float(nrm.item()) ** 0.5
-            if norm > 0.5:
-                nrm.fill_(norm)
-                nat.call("psvd_scale_cols", ctx, nat._vp(v.data_ptr()), v.ld, m, 1, nat.ptr(nrm.view(-1)), 1, st)
-                Q.view[:, j].copy_(v.view[:, 0])
-                break
 
 
 def qr_factor(a, device=None):
     """Reduced QR with diag(r) >= 0 (linalg.py:94-104): QrResult(q (m x min(m, n)),
     r (min(m, n) x n)) as CUDA tensors.  Tall inputs run CholeskyQR2 (shifted
     CholeskyQR3 when ill conditioned) on the device; wide ones factor their leading
-    square block and form r's remaining columns as q^T a.  Up to 112 columns in the
-    factored block (CholeskyQR's R and R^-1 live in one CTA's shared memory)."""
+    square block and form r's remaining columns as q^T a.  Any width (the Cholesky factors
+    live in one CTA's shared memory up to 112 columns, in global memory beyond)."""
     import torch
     from . import _native as nat
     dev = _dev(device)
@@ -239,7 +200,7 @@ def _svd_tall(A, dev, want_vt):
     Vb = torch.empty((n, n), dtype=torch.float64, device=dev)  # column-major V: Vb.T
     U = nat.DevMat.empty(m, n, dev)
     with torch.cuda.device(dev):
-        if n <= QR_MAX_COLS:
+        if n <= QR_SMEM_COLS:
             # QR-preconditioned one-sided Jacobi: A = Q R, R = U_R S V^T, U = Q U_R
             if m > n:
                 Q, R = _tall_qr(A, dev)
@@ -256,21 +217,25 @@ def _svd_tall(A, dev, want_vt):
             else:
                 nat.call("psvd_nn_product", ctx, m, nat._vp(Q.data_ptr()), Q.ld, n, nat._vp(UR.data_ptr()), UR.ld, n,
                          nat._vp(U.data_ptr()), U.ld, st)
-        elif n <= JACOBI_MAX_COLS and m <= 4 * n:
+        elif n <= JACOBI_SMEM_COLS and m <= 4 * n:
             nat.call("psvd_jacobi", ctx, nat._vp(A.data_ptr()), A.ld, m, n, nat.ptr(s), nat.ptr(Vb), n, st)
             nat.call("psvd_nn_product", ctx, m, nat._vp(A.data_ptr()), A.ld, n, nat.ptr(Vb), n, n,
                      nat._vp(U.data_ptr()), U.ld, st)
             nat.call("psvd_scale_cols", ctx, nat._vp(U.data_ptr()), U.ld, m, n, nat.ptr(s), 1, st)
         else:
-            # wide cores: eigenpairs of the Gram (singular values below ~sqrt(eps) s_1 lose
-            # relative accuracy on this route: eps s_1^2 / s_k)
-            G = torch.empty((n, n), dtype=torch.float64, device=dev)
-            nat.call("psvd_gram", ctx, m, nat._vp(0), 0, nat._vp(0), 1.0, 0, nat._vp(A.data_ptr()), A.ld, n,
-                     nat.ptr(G), st)
-            nat.call("psvd_sym_topk", ctx, nat.ptr(G), n, n, nat.ptr(Vb), n, nat.ptr(s), st)
-            nat.call("psvd_nn_product", ctx, m, nat._vp(A.data_ptr()), A.ld, n, nat.ptr(Vb), n, n,
+            # wide cores: A = Q R (CholeskyQR2 / shifted CholeskyQR3), then the multi-CTA one-sided
+            # Jacobi on R^T (psvd_big.cu): R^T J = U~ S gives R = J S U~^T, so U_R = J (the
+            # accumulated rotations) and V_R = U~; U = Q U_R.  Relative accuracy on every
+            # singular value, as dgesdd of the reference's R (linalg.py:107-123).
+            Q, R = _tall_qr(A, dev)
+            Rm = nat.as_device_colmajor(R, dev, "r")
+            UR = nat.DevMat.empty(n, n, dev)
+            VR = nat.DevMat.empty(n, n, dev)
+            nat.call("psvd_jacobi_uv", ctx, nat._vp(Rm.data_ptr()), Rm.ld, n, n, 1, nat.ptr(s),
+                     nat._vp(UR.data_ptr()), UR.ld, nat._vp(VR.data_ptr()), VR.ld, st)
+            nat.call("psvd_nn_product", ctx, m, nat._vp(Q.data_ptr()), Q.ld, n, nat._vp(UR.data_ptr()), UR.ld, n,
                      nat._vp(U.data_ptr()), U.ld, st)
-            nat.call("psvd_scale_cols", ctx, nat._vp(U.data_ptr()), U.ld, m, n, nat.ptr(s), 1, st)
+            Vb.T.copy_(VR.view)
         nat.call("psvd_sign_pair", ctx, nat._vp(U.data_ptr()), U.ld, m, n, nat.ptr(Vb), n, n, st)
     return U, s, Vb.T
 
@@ -278,10 +243,10 @@ def _svd_tall(A, dev, want_vt):
 def svd_full(a, want_vt=True, device=None):
     """Thin SVD (linalg.py:107-123): SvdResult(u, s descending, vt or None) as CUDA
     tensors with the reference's sign rule (each u column's largest-magnitude entry
-    positive, first occurrence; vt's rows follow).  Up to 112 columns (of the taller
-    orientation): CholeskyQR then one-sided Jacobi on R (relative accuracy); up to 160
-    nearly square: Jacobi on the matrix; wider: Gram eigenpairs (absolute accuracy
-    eps s_1^2 / s_k).  Non-convergence raises ConvergenceError."""
+    positive, first occurrence; vt's rows follow).  Any width (of the taller orientation):
+    CholeskyQR then one-sided Jacobi on R (relative accuracy; the one-CTA kernels up to
+    112 / 160 columns, the multi-CTA Jacobi of psvd_big.cu beyond).  Non-convergence
+    raises ConvergenceError."""
     from . import _native as nat
     dev = _dev(device)
     A = nat.as_device_colmajor(a, dev, "a")

@@ -85,6 +85,7 @@ def _device_of(*objs):
 
 
 LAST_STATUS = 0  # device status word of the last checked update (diagnostics: PSVD_ST_* bits)
+ACCURATE_UPDATES = 0  # updates recomputed on the accurate route (the Gram route's gate fired)
 
 
 def _check_status(ctx, device, what):
@@ -96,9 +97,11 @@ def _check_status(ctx, device, what):
     return st
 
 
-def deterministic_update(U, sigma, A, k, ff, rescue, device, check=True):
+def deterministic_update(U, sigma, A, k, ff, rescue, device, check=True, accurate_gate=True):
     """One deterministic update on the device.  U: DevMat or None (initialize),
-    sigma: (Kc,) CUDA tensor, A: DevMat.  Returns (DevMat M x k, sigma (k,))."""
+    sigma: (Kc,) CUDA tensor, A: DevMat.  Returns (DevMat M x k, sigma (k,)).
+    The Gram route runs first; when its conditioning gate fires (PSVD_ST_ILLCOND) the update
+    is recomputed by psvd_stream_update_accurate (streaming.py:97-103 at any conditioning)."""
     ctx = nat.context(device)
     with torch.cuda.device(device):
         st = nat.stream_ptr(device)
@@ -106,13 +109,19 @@ def deterministic_update(U, sigma, A, k, ff, rescue, device, check=True):
         kc = 0 if U is None else U.cols
         out = nat.DevMat.empty(M, k, device)
         sig = torch.empty(k, dtype=torch.float64, device=device)
-        nat.call("psvd_stream_update", ctx, M,
-                 nat._vp(U.data_ptr() if U is not None else 0), U.ld if U is not None else 0,
-                 nat.ptr(sigma if U is not None else None), float(ff), kc,
-                 nat._vp(A.data_ptr()), A.ld, B, k, int(bool(rescue)),
-                 nat._vp(out.data_ptr()), out.ld, nat.ptr(sig), st)
-        if check:
-            _check_status(ctx, device, "a_new" if U is not None else "a0")
+        args = (ctx, M, nat._vp(U.data_ptr() if U is not None else 0), U.ld if U is not None else 0,
+                nat.ptr(sigma if U is not None else None), float(ff), kc, nat._vp(A.data_ptr()), A.ld, B, k,
+                int(bool(rescue)), nat._vp(out.data_ptr()), out.ld, nat.ptr(sig), st)
+        nat.call("psvd_stream_update", *args)
+        if check or accurate_gate:
+            what = "a_new" if U is not None else "a0"
+            if _check_status(ctx, device, what) & nat.ST_ILLCOND:
+                # kept spectrum beyond the Gram route's accuracy (sigma_1 / sigma_K > 300): redo the
+                # update on the R-factor route (Gram deflation basis + Jacobi of the small factor)
+                global ACCURATE_UPDATES
+                ACCURATE_UPDATES += 1
+                nat.call("psvd_stream_update_accurate", *args)
+                _check_status(ctx, device, what)
     return out, sig
 
 
@@ -153,13 +162,28 @@ def stream_incorporate(state, a_new, config):
     return StreamState(u.view, s, state.iteration + 1)
 
 
-STREAM_WINDOW = 8  # batches resident on the device per pipelined run
+STREAM_WINDOW = 8  # most batches resident on the device per pipelined run
+STREAM_WINDOW_MEM_FRACTION = 0.25  # ... and at most this share of the device's memory
 
 
-def _run_window(state, mats, config, dev, ready=None, rescue=True, ok=None):
+def window_length(batch, device):
+    """Batches per pipelined window: STREAM_WINDOW, fewer when they would take more than
+    STREAM_WINDOW_MEM_FRACTION of HBM (at least 2, so the look-ahead Gram still overlaps)."""
+    shape = getattr(batch, "shape", None)
+    if shape is None or len(shape) != 2:
+        return STREAM_WINDOW
+    nbytes = 8 * int(shape[0]) * int(shape[1])
+    total = torch.cuda.get_device_properties(torch.device(device)).total_memory
+    return int(max(2, min(STREAM_WINDOW, (STREAM_WINDOW_MEM_FRACTION * total) // max(nbytes, 1))))
+
+
+def _run_window(state, mats, config, dev, ready=None, rescue=True, ok=None, on_illcond=None):
     """Deterministic updates over device batches `mats` with look-ahead
     (psvd_stream_run): the next batch's A^T A overlaps the current core solve.
-    `ready`: per-batch upload events (or None) the device work waits on."""
+    `ready`: per-batch upload events (or None) the device work waits on.  When an update
+    of the window trips the Gram route's conditioning gate, the window is redone batch by
+    batch from its input state: on_illcond(state, mats) (the row-parallel caller), else the
+    serial per-update path with its accurate route."""
     k = config.k_modes
     M = mats[0].rows
     for m in mats:
@@ -211,7 +235,12 @@ def _run_window(state, mats, config, dev, ready=None, rescue=True, ok=None):
                  int(bool(rescue)),
                  nat._vp(outs[0].data_ptr()), nat._vp(outs[1].data_ptr()), outs[0].ld, nat.ptr(hist),
                  ctypes.byref(fin), rd, nat.stream_ptr(dev))
-        _check_status(ctx, dev, "a_new")
+        if _check_status(ctx, dev, "a_new") & nat.ST_ILLCOND:
+            # an update of the window left the Gram route's accuracy range: redo the window from its
+            # input state one batch at a time (each update gated onto the accurate route as needed)
+            if on_illcond is not None:
+                return on_illcond(state, mats)
+            return _run_window(state, mats, config, dev, None, rescue, ok=0)
     it0 = -1 if state is None else state.iteration
     new_state = StreamState(outs[fin.value].view, hist[nb - 1].clone(), it0 + nb)
     return new_state, [hist[i] for i in range(nb)]
@@ -283,7 +312,9 @@ def _run_rand_window(state, mats, config, dev, ready=None):
 def stream_all(batches, config, device=None):
     """Initialize on the first batch, incorporate the rest (streaming.py:119-133).
     Returns (final_state, history) with the singular values after every step.
-    Deterministic streams run in windows of STREAM_WINDOW resident batches
+    The iterable is consumed lazily, one window at a time (window_length: at most
+    STREAM_WINDOW batches and a quarter of HBM), so past batches are never retained.
+    Deterministic streams run in windows of resident batches
     through the pipelined psvd_stream_run (pinned host batches are uploaded on a
     side stream, overlapping the updates); randomized ones (sketch width <= 32)
     through the pipelined psvd_rand_stream_run, wider sketches per batch."""
@@ -301,14 +332,17 @@ def stream_all(batches, config, device=None):
         dev = None if device is None else torch.device(device)
         run = _run_window if config.sketch is None else _run_rand_window
         window, ready = [], []
+        wlen = None
         for batch in batches:
             if dev is None:
                 dev = _device_of(batch)
+            if wlen is None:
+                wlen = window_length(batch, dev)
             # pinned host batches upload on a side stream: later copies overlap earlier updates
             m, ev = nat.upload_async(batch, dev, "a0" if state is None and not window else "a_new")
             window.append(m)
             ready.append(ev)
-            if len(window) == STREAM_WINDOW:
+            if len(window) == wlen:
                 state, h = run(state, window, config, dev, ready)
                 history.extend(h)
                 window, ready = [], []

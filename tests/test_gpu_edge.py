@@ -1,0 +1,196 @@
+"""GPU ports of the reference's own streaming edge cases (VERDICT r1 "do this" #9).
+
+Each test restates a case of /root/reference/pkg/tests/test_streaming.py or test_dsvd.py on the
+device path and checks it two ways: the reference test's own property (exactness, invariance,
+truncation profile), and parity with the pinned oracle on the same bytes at the north-star bar
+(sigma relative error <= 1e-10, sine-based mode angles <= 1e-8, the reference's signs).
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+SIG_TOL = 1e-10
+ANG_TOL = 1e-8
+
+
+def _p():
+    import paper_2108_08845_b200 as p
+    return p
+
+
+def _batches(a, w):
+    return [a[:, i:i + w] for i in range(0, a.shape[1], w)]
+
+
+def _constructed(rows=60, cols=36, seed=11):
+    """test_streaming.py:14-18: a clear gap after the fifth value and a tiny tail."""
+    sv = np.concatenate([1.25 ** -np.arange(5), 1e-8 * 0.5 ** np.arange(12)])
+    return _p().synthetic_spectrum_matrix(rows, cols, sv, seed=seed)
+
+
+def _parity(state, ref_m, ref_s, sel=None):
+    m, s = state.numpy()
+    assert oracle.sigma_rel_err(s, ref_s) <= SIG_TOL, (s, ref_s)
+    ang = oracle.mode_angles(m, ref_m)
+    sel = np.ones(ang.size, dtype=bool) if sel is None else sel
+    assert np.max(ang[sel]) <= ANG_TOL, ang
+    assert np.all(np.sum(m * ref_m, axis=0)[sel] > 0)
+    return m, s
+
+
+@pytest.mark.parametrize("width", [36, 12, 9, 7, 5])
+def test_partition_invariance(width):
+    """test_streaming.py:66-76: K = 5, ff = 1 over batch widths 36 / 12 / 9 / 7 / 5 lands on the
+    direct SVD (1e-6 / 1e-5, the reference's bars) — and on the reference's own stream to 1e-10."""
+    p = _p()
+    a = _constructed()
+    ru, rs, _ = oracle.ref_svd(a)
+    cfg = p.StreamConfig(k_modes=5, forget_factor=1.0, batch_columns=width)
+    st, hist = p.stream_all(_batches(a, width), cfg)
+    m, s = st.numpy()
+    assert np.max(np.abs(s - rs[:5]) / rs[:5]) < 1e-6
+    assert np.max(oracle.aligned_mode_difference(m, ru[:, :5])) < 1e-5
+    assert st.iteration == len(hist) - 1 == -(-36 // width) - 1
+    ref_m, ref_s, _ = oracle.ref_stream_all(_batches(a, width), 5, 1.0)
+    _parity(st, ref_m, ref_s)
+
+
+def test_incorporate_batch_in_current_span():
+    """test_streaming.py:89-106: a batch inside span(modes) leaves the subspace unchanged and the
+    new values are exactly svd([diag(s) | coefficients]) (rtol 1e-12)."""
+    p = _p()
+    rng = np.random.Generator(np.random.Philox(41))
+    a0 = rng.standard_normal((25, 6))
+    cfg = p.StreamConfig(k_modes=4, forget_factor=1.0, batch_columns=6)
+    st = p.stream_initialize(a0, cfg)
+    m0, s0 = st.numpy()
+    coeff = rng.standard_normal((4, 3))
+    batch = m0 @ coeff
+    new = p.stream_incorporate(st, batch, cfg)
+    m1, s1 = new.numpy()
+    assert np.max(oracle.sine_angles(m1, m0)) < 1e-12  # sine-based: resolves far below arccos's 2e-8
+    expect = np.linalg.svd(np.concatenate([np.diag(s0), coeff], axis=1), compute_uv=False)[:4]
+    assert np.allclose(s1, expect, rtol=1e-12, atol=0)
+    assert new.iteration == 1
+    ref_m, ref_s = oracle.ref_stream_update(m0, s0, batch, 4, 1.0)
+    _parity(new, ref_m, ref_s)
+
+
+def test_exact_when_k_covers_rank():
+    """test_streaming.py:79-86: rank-3 data, K = 3, ff = 1: streaming loses nothing."""
+    p = _p()
+    a = p.synthetic_spectrum_matrix(40, 24, [4.0, 2.0, 1.0], seed=12)
+    st, _ = p.stream_all(_batches(a, 6), p.StreamConfig(k_modes=3, forget_factor=1.0, batch_columns=6))
+    m, s = st.numpy()
+    assert np.allclose(s, [4.0, 2.0, 1.0], rtol=1e-12, atol=0)
+    ru, _, _ = oracle.ref_svd(a)
+    assert np.max(oracle.aligned_mode_difference(m, ru[:, :3])) < 1e-12
+
+
+@pytest.mark.parametrize("kind", ["zero", "rank1", "repeat"])
+def test_degenerate_batch_mid_stream(kind):
+    """A zero batch, a rank-one batch and a repeat of an earlier batch in the middle of a stream:
+    the reference's update handles them through Householder QR; here the Gram route (or its
+    accurate route) must agree with it."""
+    p = _p()
+    rng = np.random.Generator(np.random.Philox(50))
+    a = oracle.burgers_matrix(3000, 400)[:, :300] + 1e-3 * rng.standard_normal((3000, 300))
+    bs = _batches(a, 60)
+    if kind == "zero":
+        mid = np.zeros((3000, 60))
+    elif kind == "rank1":
+        mid = np.outer(rng.standard_normal(3000), rng.standard_normal(60))
+    else:
+        mid = bs[1].copy()
+    stream = bs[:3] + [mid] + bs[3:]
+    cfg = p.StreamConfig(k_modes=8, forget_factor=0.95, batch_columns=60)
+    st, hist = p.stream_all(stream, cfg)
+    ref_m, ref_s, ref_h = oracle.ref_stream_all(stream, 8, 0.95)
+    _parity(st, ref_m, ref_s)
+    for h, rh in zip(hist, ref_h):
+        assert oracle.sigma_rel_err(h.cpu().numpy(), rh) <= SIG_TOL
+    if kind == "zero":  # ff = 0.95 only rescales: sigma after the zero batch = 0.95 sigma before
+        assert np.allclose(hist[3].cpu().numpy(), 0.95 * hist[2].cpu().numpy(), rtol=1e-13, atol=0)
+
+
+def test_modes_stay_orthonormal_over_many_updates():
+    """test_streaming.py:119-129: 50 updates of Gaussian batches keep U^T U = I and sigma sorted."""
+    p = _p()
+    rng = np.random.Generator(np.random.Philox(42))
+    cfg = p.StreamConfig(k_modes=6, forget_factor=0.95, batch_columns=8)
+    batches = [rng.standard_normal((64, 8)) for _ in range(51)]
+    st = p.stream_initialize(batches[0], cfg)
+    for b in batches[1:]:
+        st = p.stream_incorporate(st, b, cfg)
+    m, s = st.numpy()
+    assert np.max(np.abs(m.T @ m - np.eye(6))) < 1e-12
+    assert np.all(np.diff(s) <= 0.0) and np.all(s >= 0.0)
+    assert st.iteration == 50
+    ref_m, ref_s, _ = oracle.ref_stream_all(batches, 6, 0.95)
+    assert oracle.sigma_rel_err(s, ref_s) <= SIG_TOL
+
+
+def test_burgers_truncation_profile():
+    """test_dsvd.py:253-285 on the serial device path: on Burgers 2048 x 800 a K = 5 state lands
+    in (1e-6, 2e-2) of the top five direct values, a K = 50 state within 1e-6.  K = 50 keeps
+    values down to ~1e-13 sigma_1, so its updates take the accurate route; against the
+    reference's own K = 50 stream every value above 1e-5 sigma_1 agrees to 1e-10 and all to
+    1e-13 sigma_1 absolute (both sides are backward stable: O(eps sigma_1) absolute)."""
+    p = _p()
+    a = oracle.burgers_matrix(2048, 800)
+    _, ds, _ = oracle.ref_svd(a, want_vt=False)
+    n0 = p.streaming.ACCURATE_UPDATES
+    out = {}
+    for k in (5, 50):
+        st, _ = p.stream_all(_batches(a, 200), p.StreamConfig(k_modes=k, forget_factor=1.0, batch_columns=200))
+        out[k] = st.numpy()
+    err_narrow = np.max(np.abs(out[5][1] - ds[:5]) / ds[:5])
+    assert 1e-6 < err_narrow < 2e-2
+    assert np.max(np.abs(out[50][1][:5] - ds[:5]) / ds[:5]) < 1e-6
+    assert p.streaming.ACCURATE_UPDATES > n0
+    ref_m, ref_s, _ = oracle.ref_stream_all(_batches(a, 200), 50, 1.0)
+    m, s = out[50]
+    big = ref_s >= 1e-5 * ref_s[0]
+    assert np.max(np.abs(s[big] - ref_s[big]) / ref_s[big]) <= SIG_TOL
+    assert np.max(np.abs(s - ref_s)) <= 1e-13 * ref_s[0]
+    gap = np.minimum(np.abs(np.diff(ref_s, prepend=np.inf)), np.abs(np.diff(ref_s, append=-np.inf))) / ref_s
+    sel = big & (gap > 1e-3)
+    ang = oracle.mode_angles(m, ref_m)
+    assert np.max(ang[sel]) <= ANG_TOL
+    assert np.all(np.sum(m * ref_m, axis=0)[sel] > 0)
+    ref5_m, ref5_s, _ = oracle.ref_stream_all(_batches(a, 200), 5, 1.0)
+    assert oracle.sigma_rel_err(out[5][1], ref5_s) <= SIG_TOL
+
+
+@pytest.mark.parametrize("k", [125, 150])
+def test_wide_k_drift_check(k):
+    """k_modes beyond the one-CTA drift check (K > 120) — the check and rescue run on
+    the wide path (host-checked, psvd_qr based) instead of failing the launch; forced rescue
+    reproduces the unforced result."""
+    p = _p()
+    from paper_2108_08845_b200 import _native as nat
+    import torch
+    rng = np.random.Generator(np.random.Philox(60))
+    a = rng.standard_normal((2000, 3 * k)) * np.logspace(0, -1, 3 * k)
+    bs = _batches(a, k)
+    cfg = p.StreamConfig(k_modes=k, forget_factor=0.95, batch_columns=k)
+    st, _ = p.stream_all(bs, cfg)
+    ref_m, ref_s, _ = oracle.ref_stream_all(bs, k, 0.95)
+    m, s = st.numpy()
+    assert oracle.sigma_rel_err(s, ref_s) <= SIG_TOL
+    ctx = nat.context(torch.device("cuda", 0))
+    nat.call("psvd_set_drift_tol", ctx, -1.0)
+    try:
+        st2 = p.stream_incorporate(p.stream_initialize(bs[0], cfg), bs[1], cfg)
+        assert p.streaming.LAST_STATUS & nat.ST_RESCUE
+    finally:
+        nat.call("psvd_set_drift_tol", ctx, 1e-8)
+    st1 = p.stream_incorporate(p.stream_initialize(bs[0], cfg), bs[1], cfg)
+    m1, s1 = st1.numpy()
+    m2, s2 = st2.numpy()
+    assert oracle.sigma_rel_err(s2, s1) <= 1e-12
+    assert np.max(np.abs(m2.T @ m2 - np.eye(k))) < 1e-12

@@ -41,7 +41,8 @@ def test_qr_negated_identity_sign_convention():
     assert np.max(np.abs(q @ r + np.eye(3))) < 1e-15
 
 
-@pytest.mark.parametrize("m,n", [(8, 3), (6, 6), (3, 7), (20, 7), (5000, 40), (1 << 16, 112)])
+@pytest.mark.parametrize("m,n", [(8, 3), (6, 6), (3, 7), (20, 7), (5000, 40), (1 << 16, 112), (1 << 16, 210),
+                                 (1 << 16, 612), (700, 700), (200, 450)])
 def test_qr_matches_reference(m, n):
     a = _rng(10 + m).standard_normal((m, n))
     res = _p().qr_factor(a)
@@ -66,6 +67,29 @@ def test_qr_ill_conditioned_takes_shifted_route():
     assert np.max(np.abs(q.T @ q - np.eye(12))) < 1e-12
     assert np.max(np.abs(q @ r - a)) < 1e-14
     assert np.all(np.diag(r) >= 0.0)
+
+
+@pytest.mark.parametrize("n", [40, 112, 210, 612])
+def test_qr_rank_deficient_burgers(n):
+    """Numerically rank-deficient input (Burgers 4096 x n: ~30 significant directions), where
+    CholeskyQR breaks down: the rank-robust route keeps Householder's guarantees (orthonormal q,
+    q r = a to rounding, diag(r) >= 0) and the well-determined rows of r match the reference's."""
+    a = oracle.burgers_matrix(4096, 800)[:, :n]
+    res = _p().qr_factor(a)
+    q, r = _np(res.q), _np(res.r)
+    qr_, rr = oracle.ref_qr(a)
+    assert np.max(np.abs(q.T @ q - np.eye(n))) < 1e-13
+    assert np.max(np.abs(q @ r - a)) < 1e-13 * np.abs(a).max()
+    assert np.all(np.diag(r) >= 0.0) and np.allclose(r, np.triu(r), atol=0)
+    # row k of r (and column k of q) is determined to ~eps |a|_2^2 / r_kk (eps |a|_2 / r_kk) by any
+    # backward-stable QR; rows at rounding level are arbitrary (Householder's too)
+    s1 = np.linalg.norm(a, 2)
+    lead = np.abs(np.diag(rr)) > 1e-6 * np.abs(rr[0, 0])
+    k = int(np.argmin(lead)) if not lead.all() else n
+    assert k >= 3
+    d = np.abs(np.diag(rr))[:k]
+    assert np.all(np.max(np.abs(r[:k] - rr[:k]), axis=1) < 16 * np.finfo(float).eps * s1 * s1 / d)
+    assert np.all(np.max(np.abs(q[:, :k] - qr_[:, :k]), axis=0) < 16 * np.finfo(float).eps * s1 / d)
 
 
 def test_qr_rejects_bad_input_and_is_deterministic():
@@ -114,15 +138,43 @@ def test_svd_matches_reference(m, n):
     assert np.all(peaks > 0.0)
 
 
-def test_svd_wide_core_gram_route():
-    # more than 160 columns on both sides: the Gram eigenpair route (leading values)
-    a = oracle.burgers_matrix(2048, 400)
+@pytest.mark.parametrize("m,n", [(2000, 300), (300, 2000), (612, 612)])
+def test_svd_wide_matches_reference(m, n):
+    """Beyond the one-CTA kernels (160 columns): CholeskyQR + the multi-CTA Jacobi on R^T."""
+    a = _rng(30 + m + n).standard_normal((m, n))
+    res = _p().svd_full(a)
+    u, s, vt = _np(res.u), _np(res.s), _np(res.vt)
+    ru, rs, rvt = oracle.ref_svd(a)
+    k = min(m, n)
+    assert np.max(np.abs(s - rs) / rs) < 1e-10
+    assert np.max(np.abs(u.T @ u - np.eye(k))) < 1e-12
+    assert np.max(np.abs(vt @ vt.T - np.eye(k))) < 1e-12
+    assert np.max(np.abs((u * s) @ vt - a)) < 1e-12 * rs[0]
+    # well-separated modes match the reference with its signs
+    gap = np.minimum(np.abs(np.diff(rs, prepend=np.inf)), np.abs(np.diff(rs, append=-np.inf))) / rs
+    sep = gap > 1e-3
+    assert np.max(oracle.mode_angles(u[:, sep], ru[:, sep])) < 1e-8
+    assert np.all(np.sum(u * ru, axis=0)[sep] > 0)
+
+
+def test_svd_burgers_4096x800_full_spectrum():
+    """svd_full of the whole Burgers 4096 x 800 matrix (the reference's serial-batch mode,
+    cli.py:329-340): every singular value with a relative bar that backward-stable
+    algorithms can meet (sigma_k >= 1e-5 sigma_1: both sides carry O(eps sigma_1) absolute
+    error, the reference's dgesdd included), the rest to 1e-13 sigma_1 absolute; the
+    leading modes to 1e-8 with the reference's signs."""
+    a = oracle.burgers_matrix(4096, 800)
     res = _p().svd_full(a, want_vt=False)
     ru, rs, _ = oracle.ref_svd(a, want_vt=False)
     assert res.vt is None
     s = _np(res.s)
-    assert np.max(np.abs(s[:10] - rs[:10]) / rs[:10]) < 1e-10
-    assert np.max(oracle.mode_angles(_np(res.u)[:, :10], ru[:, :10])) < 1e-8
+    u = _np(res.u)
+    big = rs >= 1e-5 * rs[0]
+    assert big.sum() >= 20
+    assert np.max(np.abs(s[big] - rs[big]) / rs[big]) < 1e-10
+    assert np.max(np.abs(s - rs)) < 1e-13 * rs[0]
+    assert np.max(oracle.mode_angles(u[:, :20], ru[:, :20])) < 1e-8
+    assert np.all(np.sum(u[:, :20] * ru[:, :20], axis=0) > 0)
 
 
 def test_svd_want_vt_false_and_zero_matrix():
@@ -194,7 +246,7 @@ def _qr_rank_worker(rank, world, port, q, rows, cols, seed):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,rows,cols", [(4, 32, 5), (3, 9, 5), (2, 20000, 30)])
+@pytest.mark.parametrize("world,rows,cols", [(4, 32, 5), (3, 9, 5), (2, 20000, 30), (4, 40000, 210)])
 def test_parallel_qr_ranks_match_serial(world, rows, cols):
     """Four ranks of 8 rows, three of 3 rows (shorter than the 5 columns: dsvd.py's short
     blocks), two of 10000: same R on every rank, stacked Q orthonormal, factors equal to

@@ -31,13 +31,25 @@ def _np(state):
     return state.numpy()
 
 
-def _assert_parity(modes, sigma, ref_modes, ref_sigma, sig_tol=SIG_TOL, ang_tol=ANG_TOL, signs=True):
+def _separated(sigma, rel_gap=1e-3):
+    """Modes whose relative gap to both neighbours is at least rel_gap: the ones the north star's
+    angle bar applies to (a mode inside a cluster is not determined by its singular value)."""
+    s = np.asarray(sigma, dtype=np.float64)
+    gap = np.full(s.size, np.inf)
+    d = np.abs(np.diff(s))
+    gap[:-1] = np.minimum(gap[:-1], d)
+    gap[1:] = np.minimum(gap[1:], d)
+    return gap >= rel_gap * np.maximum(s, 1e-300)
+
+
+def _assert_parity(modes, sigma, ref_modes, ref_sigma, sig_tol=SIG_TOL, ang_tol=ANG_TOL, signs=True, sep=None):
     assert modes.shape == ref_modes.shape
     assert oracle.sigma_rel_err(sigma, ref_sigma) <= sig_tol, (sigma, ref_sigma)
     ang = oracle.mode_angles(modes, ref_modes)
-    assert np.max(ang) <= ang_tol, ang
+    sel = np.ones(ang.size, dtype=bool) if sep is None else sep
+    assert np.max(ang[sel]) <= ang_tol, ang
     if signs:  # the reference's sign convention is reproduced, not just the subspace
-        assert np.all(np.sum(modes * ref_modes, axis=0) > 0)
+        assert np.all(np.sum(modes * ref_modes, axis=0)[sel] > 0)
 
 
 def test_config1_burgers_golden(golden):
@@ -74,7 +86,7 @@ def test_edge_cases_golden(golden):
     cfg = p.StreamConfig(k_modes=5, forget_factor=1.0, batch_columns=7)
     st, _ = p.stream_all(_batches(g["constructed_a"], 7), cfg)
     m, s = _np(st)
-    _assert_parity(m, s, g["constructed_w7_modes"], g["constructed_w7_sigma"], sig_tol=1e-10, ang_tol=1e-7)
+    _assert_parity(m, s, g["constructed_w7_modes"], g["constructed_w7_sigma"])
     st, _ = p.stream_all(_batches(g["rank3_a"], 6), p.StreamConfig(k_modes=3, forget_factor=1.0, batch_columns=6))
     m, s = _np(st)
     _assert_parity(m, s, g["rank3_modes"], g["rank3_sigma"])
@@ -118,7 +130,7 @@ def test_drift_rescue_golden(golden):
     gram = m.T @ m
     assert np.max(np.abs(gram - np.eye(3))) < 1e-12
     assert np.all(np.diff(s) <= 0.0)
-    _assert_parity(m, s, g["rescue_modes"], g["rescue_sigma"], sig_tol=1e-9, ang_tol=1e-7)
+    _assert_parity(m, s, g["rescue_modes"], g["rescue_sigma"])
 
 
 @pytest.mark.parametrize("rows,ff,k,b", [(65536, 0.95, 10, 200), (10007, 0.9, 8, 64), (4097, 1.0, 12, 100)])
@@ -142,7 +154,8 @@ def test_shapes_vs_oracle(rows, cols, k, b):
     ref_m, ref_s, _ = oracle.ref_stream_all(_batches(a, b), k, 0.95)
     st, _ = p.stream_all(_batches(a, b), p.StreamConfig(k_modes=k, forget_factor=0.95, batch_columns=b))
     m, s = _np(st)
-    _assert_parity(m, s, ref_m, ref_s, sig_tol=1e-9, ang_tol=1e-7, signs=False)
+    # the north-star bar with the reference's signs, over the modes a Gaussian spectrum separates
+    _assert_parity(m, s, ref_m, ref_s, sep=_separated(ref_s))
 
 
 def test_deterministic_bitwise():
@@ -640,6 +653,104 @@ def test_parallel_pipelined_stream_ranks_match_serial(world, rows, cols, b):
     _assert_parity(out[0][3], out[0][4], rm, rs)
     for h, r_ in zip(out[0][1], rh):
         assert oracle.sigma_rel_err(h, r_) <= SIG_TOL
+
+
+def _illcond_matrix(rows=6000, cols=320, span=1e-6, rank=40, seed=7):
+    """synthetic_spectrum_matrix (datagen.py:93-115) with `rank` values log-spaced over `span`:
+    a K = 40 stream whose kept spectrum is far beyond the Gram route's accuracy (eps kappa^2)."""
+    import paper_2108_08845_b200 as p
+    return p.synthetic_spectrum_matrix(rows, cols, np.logspace(0, np.log10(span), rank), seed=seed)
+
+
+@pytest.mark.parametrize("ff,bw,span", [(1.0, 80, 1e-6), (0.95, 64, 1e-6), (0.95, 100, 1e-5)])
+def test_ill_conditioned_stream_takes_accurate_route(ff, bw, span):
+    """VERDICT r1 weak #2 / ADVICE: a K = 40 stream with sigma_1 / sigma_K up to 1e6.  The Gram
+    route's gate (sigma_1 / sigma_K > 300) reroutes every update to the R-factor route, which
+    meets the 1e-10 / 1e-8 bar against the reference with its signs, both through the pipelined
+    stream_all (window redone per batch) and per update."""
+    p = _pkg()
+    a = _illcond_matrix(span=span)
+    ref_m, ref_s, ref_h = oracle.ref_stream_all(_batches(a, bw), 40, ff)
+    cfg = p.StreamConfig(k_modes=40, forget_factor=ff, batch_columns=bw)
+    n0 = p.streaming.ACCURATE_UPDATES
+    st, hist = p.stream_all(_batches(a, bw), cfg)
+    assert p.streaming.ACCURATE_UPDATES - n0 >= len(_batches(a, bw))
+    m, s = _np(st)
+    _assert_parity(m, s, ref_m, ref_s)
+    for h, rh in zip(hist, ref_h):
+        assert oracle.sigma_rel_err(h.cpu().numpy(), rh) <= SIG_TOL
+    assert np.max(np.abs(m.T @ m - np.eye(40))) < 1e-12
+    # per update (stream_initialize / stream_incorporate) gives the same answer
+    bs = _batches(a, bw)
+    st2 = p.stream_initialize(bs[0], cfg)
+    for b in bs[1:]:
+        st2 = p.stream_incorporate(st2, b, cfg)
+    m2, s2 = _np(st2)
+    _assert_parity(m2, s2, ref_m, ref_s)
+
+
+def test_gram_route_stays_on_when_well_conditioned():
+    """The gate costs nothing on the benchmark's own data: Burgers K = 10 (sigma_1 / sigma_K ~ 25)
+    never reroutes."""
+    p = _pkg()
+    a = oracle.burgers_matrix(8192, 800)
+    n0 = p.streaming.ACCURATE_UPDATES
+    p.stream_all(_batches(a, 200), p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200))
+    assert p.streaming.ACCURATE_UPDATES == n0
+
+
+def _illcond_rank_worker(rank, world, port, q):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2108_08845_b200 as p
+        a = _illcond_matrix(rows=5001, cols=240)
+        lo, hi = p.partition_bounds(a.shape[0], world)[rank]
+        cfg = p.StreamConfig(k_modes=40, forget_factor=0.95, batch_columns=80)
+        ctx = p.RankContext()
+        loc = [a[lo:hi, c0:c0 + 80] for c0 in range(0, a.shape[1], 80)]
+        st, hist = p.parallel_stream_all(ctx, loc, cfg)
+        full = p.gather_modes(ctx, st)
+        q.put((rank, st.singular_values.cpu().numpy(), None if full is None else full.cpu().numpy(),
+               p.streaming.ACCURATE_UPDATES))
+    except Exception as e:
+        q.put((rank, "error", repr(e), 0))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_parallel_ill_conditioned_stream_accurate_route():
+    """The accurate route row-partitioned (two processes sharing this GPU, gloo): every Gram and
+    projection of the deflation basis is summed over the ranks through the exchange hooks, the
+    small factorizations are replicated on identical bits."""
+    import socket
+    import torch.multiprocessing as mp
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_illcond_rank_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = {}
+    for _ in range(2):
+        rank, sig, full, nacc = q.get(timeout=300)
+        assert not (isinstance(sig, str) and sig == "error"), full
+        out[rank] = (sig, full, nacc)
+    for pr in procs:
+        pr.join(timeout=120)
+    assert all(pr.exitcode == 0 for pr in procs)
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][2] >= 3
+    a = _illcond_matrix(rows=5001, cols=240)
+    rm, rs, _ = oracle.ref_stream_all(_batches(a, 80), 40, 0.95)
+    _assert_parity(out[0][1], out[0][0], rm, rs)
 
 
 @pytest.mark.parametrize("low_rank", [False, True])
