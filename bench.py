@@ -280,11 +280,11 @@ def run_ours(a):
 
     ex = None
     if world > 1:
-        # the pipelined stream with the library's exchange hooks (dsvd._Exchange): per update a
-        # rank-ordered NCCL sum of the streaming Gram and of U^T U on the library's stream
-        from paper_2108_08845_b200.dsvd import _Exchange
-        ex = _Exchange(ctxr, dev)
-        nat.call("psvd_set_exchange", c, ctypes.cast(ex.ar, nat._vp), ctypes.cast(ex.ag, nat._vp), None, world, lo)
+        # the pipelined stream with the library's exchange (dsvd.exchange_hooks): on NCCL the library
+        # issues its own in-stream ncclAllGather + rank-ordered sum of the streaming Gram and of U^T U
+        # per update (gloo in the shared-GPU flow check: torch.distributed callbacks)
+        from paper_2108_08845_b200.dsvd import exchange_hooks
+        ex = exchange_hooks(ctxr, dev, lo).__enter__()
 
     def step(record=False):
         # whole stream through psvd_stream_run (look-ahead A^T A on a second stream); no drift
@@ -331,7 +331,7 @@ def run_ours(a):
         barrier()
     launches = nat.lib().psvd_launch_count(c) - launches0
     if ex is not None:
-        nat.call("psvd_set_exchange", c, None, None, None, 1, 0)
+        ex.suspend()
     ms = t0.elapsed_time(t1)
     if world > 1:
         ms = max_over_ranks(ms, dev)

@@ -71,6 +71,21 @@ typedef int (*psvd_allgather_fn)(void* user, const double* send, int64_t count, 
 int psvd_set_exchange(psvd_ctx* ctx, psvd_allreduce_fn allreduce, psvd_allgather_fn allgather, void* user,
                       int nranks, int64_t row_offset);
 
+/* NCCL data plane of the same exchange points (no Python in the loop): the caller creates one
+ * communicator per context from a unique id it distributes (psvd_nccl_unique_id on one rank, then a
+ * broadcast, then psvd_nccl_init on every rank; libnccl.so.2 is loaded at run time) and enables it
+ * around row-partitioned calls.  Each exchange is then an in-stream ncclAllGather on the library's
+ * stream plus a rank-ordered sum, bitwise identical on every rank (replaces the reference's
+ * gather / send / broadcast, dsvd.py:176-202).  Mutually exclusive with psvd_set_exchange. */
+int psvd_nccl_available(int* ok);
+int psvd_nccl_unique_id(psvd_ctx* ctx, unsigned char* id128);
+int psvd_nccl_init(psvd_ctx* ctx, int nranks, int rank, const unsigned char* id128);
+int psvd_nccl_enable(psvd_ctx* ctx, int on, int64_t row_offset);
+int psvd_nccl_destroy(psvd_ctx* ctx);
+/* Exchange accounting since context creation (the reference's CommStats, comm.py:74-88):
+ * out[0] collectives issued at the exchange points, out[1] bytes received from other ranks. */
+int psvd_exchange_stats(psvd_ctx* ctx, long long* out2);
+
 /* Which core solver produced the last split-mode core solve (diagnostics, syncs the
  * device): *full = 0 when the subspace-iteration fast path converged, 1 when the
  * gated full Householder solver ran. */

@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libpsvd.so")
 SOURCES = ["psvd_tall.cu", "psvd_pass_tma.cu", "psvd_gemm.cu", "psvd_small.cu", "psvd_subspace.cu", "psvd_rand.cu",
-           "psvd_api.cu", "psvd_stream.cu", "psvd_rand_api.cu", "psvd_dense.cu", "psvd_big.cu", "psvd_accurate.cu"]
+           "psvd_api.cu", "psvd_stream.cu", "psvd_rand_api.cu", "psvd_dense.cu", "psvd_big.cu", "psvd_accurate.cu", "psvd_nccl.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC"]
 
@@ -41,7 +41,7 @@ def build(force=False, verbose=False, defines=(), variant=None):
         cmds = [[nvcc()] + NVCC_FLAGS + ["-D" + d for d in defines] +
                 ["-c", os.path.join(CSRC, s), "-o", os.path.join(obj, s + ".o")] for s in SOURCES]
         link = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a"] + \
-            [c[-1] for c in cmds] + ["-o", tmp]
+            [c[-1] for c in cmds] + ["-ldl", "-o", tmp]
 
         def run(cmd):
             if verbose:

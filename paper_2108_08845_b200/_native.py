@@ -75,6 +75,12 @@ _SIGS = {
     "psvd_stream_update_accurate": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_int, _vp, _c_i64, _c_int,
                                              _c_int, _c_int, _vp, _c_i64, _vp, _vp]),
     "psvd_qr_robust": (_c_int, [_vp, _c_i64, _c_int, _vp, _c_i64, _vp, _c_i64, _vp, _vp]),
+    "psvd_nccl_available": (_c_int, [ctypes.POINTER(_c_int)]),
+    "psvd_nccl_unique_id": (_c_int, [_vp, ctypes.c_char_p]),
+    "psvd_nccl_init": (_c_int, [_vp, _c_int, _c_int, ctypes.c_char_p]),
+    "psvd_nccl_enable": (_c_int, [_vp, _c_int, _c_i64]),
+    "psvd_nccl_destroy": (_c_int, [_vp]),
+    "psvd_exchange_stats": (_c_int, [_vp, ctypes.POINTER(ctypes.c_longlong)]),
     "psvd_jacobi_uv": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _c_int, _vp, _vp, _c_i64, _vp, _c_i64, _vp]),
     "psvd_scale_cols": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _vp, _c_int, _vp]),
     "psvd_rand_last_vt": (_c_int, [_vp, _c_int, _c_int, _c_int, _vp, _c_i64, _vp]),

@@ -356,7 +356,7 @@ int psvd_qr_robust(psvd_ctx* c, int64_t M, int n, const double* A, int64_t lda, 
   cudaStream_t st = (cudaStream_t)stream;
   int rc;
   // a row-partitioned rank (exchange hooks set) may hold fewer rows than columns
-  if (n < 1 || M < 1 || (c->ex_allreduce == nullptr && M < n))
+  if (n < 1 || M < 1 || (!ex_active(c) && M < n))
     return fail(c, PSVD_EINVAL, "qr needs M >= n >= 1 (M=%lld n=%d)", (long long)M, n);
   if ((rc = check_mat(c, "A", A, lda, M, n)) || (rc = check_mat(c, "Q", Q, ldq, M, n))) return rc;
   if (!R) return fail(c, PSVD_EINVAL, "R is null");

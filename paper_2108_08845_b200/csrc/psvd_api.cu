@@ -599,7 +599,9 @@ int psvd_destroy(psvd_ctx* c) {
   cudaDeviceSynchronize();
   Buf* bufs[] = {&c->partial, &c->tiles, &c->gram, &c->eigws, &c->wbuf, &c->utu, &c->tbuf, &c->dvec, &c->colmax,
                  &c->ybuf, &c->ybuf2, &c->xpairs, &c->ssws, &c->rsmall, &c->jacws, &c->partial2, &c->tiles2[0], &c->tiles2[1],
-                 &c->zbuf, &c->rs2, &c->dense, &c->dense2, &c->bigws, &c->bigjac, &c->accws, &c->accq};
+                 &c->zbuf, &c->rs2, &c->dense, &c->dense2, &c->bigws, &c->bigjac, &c->accws, &c->accq,
+                 &c->nccl_parts};
+  psvd_nccl_destroy(c);
   for (Buf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
   if (c->s_hi) cudaStreamDestroy(c->s_hi);
@@ -631,6 +633,7 @@ int psvd_set_exchange(psvd_ctx* c, psvd_allreduce_fn allreduce, psvd_allgather_f
   if (!c) return PSVD_EINVAL;
   if ((allreduce == nullptr) != (allgather == nullptr) || nranks < 1 || row_offset < 0)
     return fail(c, PSVD_EINVAL, "bad exchange hooks");
+  if (allreduce && c->nccl_on) return fail(c, PSVD_EINVAL, "the NCCL exchange is enabled (psvd_nccl_enable)");
   c->ex_allreduce = allreduce;
   c->ex_allgather = allgather;
   c->ex_user = user;
@@ -940,7 +943,10 @@ int psvd_internal::refine_normalize(psvd_ctx* c, int64_t M, double* U, int64_t l
 
 // exchange points of the row-partitioned randomized update (no-ops on one GPU)
 int psvd_internal::ex_allreduce(psvd_ctx* c, double* buf, int64_t count, cudaStream_t st) {
+  if (c->nccl_on) return nccl_allreduce_ordered(c, buf, count, st);
   if (!c->ex_allreduce) return PSVD_OK;
+  c->ex_calls++;
+  c->ex_bytes += 8 * count * (c->ex_nranks - 1);
   if (c->ex_allreduce(c->ex_user, buf, count, (void*)st) != 0) return fail(c, PSVD_ECUDA, "allreduce hook failed");
   return PSVD_OK;
 }

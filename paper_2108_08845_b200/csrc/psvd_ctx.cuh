@@ -47,6 +47,11 @@ struct psvd_ctx {
   Buf dense, dense2;        // dense utilities (psvd_qr / psvd_jacobi): small factors, a tall temporary
   Buf bigws, bigjac;        // any-width Cholesky / Jacobi workspaces (psvd_big.cu)
   Buf accws, accq;          // accurate R-factor route of the deterministic update: small factors, tall Q
+  void* nccl_comm = nullptr;  // NCCL data plane of the exchange points (psvd_nccl.cu)
+  bool nccl_on = false;
+  int nccl_nranks = 1, nccl_rank = 0;
+  Buf nccl_parts;             // allgather landing buffer of the rank-ordered sums
+  long long ex_calls = 0, ex_bytes = 0;  // collectives issued / bytes received at the exchange points
   cudaEvent_t ev_qready = nullptr;  // pipelined randomized stream: the sketch basis of the last update is final
   cudaStream_t s_hi = nullptr, s_lo = nullptr;  // pipelined stream_run: critical chain / look-ahead Grams
   cudaStream_t s_aux = nullptr;                  // concurrent LDL^T of the split core solve
@@ -95,8 +100,12 @@ int refine_normalize(psvd_ctx* c, int64_t M, double* U, int64_t ld, int K, doubl
 // drift rescue beyond the one-CTA check (K > DRIFT_SMEM_KMAX): host-checked, psvd_qr based
 int drift_rescue_wide(psvd_ctx* c, int64_t M, double* U, int64_t ldu, int K, const double* UtU, double* sigma,
                       double tol, cudaStream_t st);
-// exchange points of the row-partitioned updates (no-ops on one GPU)
+// exchange points of the row-partitioned updates (no-ops on one GPU): NCCL in-stream when a
+// communicator is enabled, else the caller's hooks
 int ex_allreduce(psvd_ctx* c, double* buf, int64_t count, cudaStream_t st);
+bool ex_active(const psvd_ctx* c);  // a row-partitioned exchange is set (NCCL or hooks)
+int nccl_allgather(psvd_ctx* c, const double* send, int64_t count, double* recv, cudaStream_t st);
+int nccl_allreduce_ordered(psvd_ctx* c, double* buf, int64_t count, cudaStream_t st);
 // Cholesky R and R^-1 of an n x n Gram for any n (the one-CTA kernel up to CHOL_NMAX, psvd_big.cu beyond)
 int chol_any(psvd_ctx* c, const double* G, int n, double* T, int* illcond, int* status, double* Rout,
              cudaStream_t st);

@@ -29,7 +29,7 @@ __global__ void rand_vt_kernel(const double* __restrict__ Bt, int n, int l, cons
 
 // sign rule over ranks: local per-chunk pairs -> one pair per column -> allgather -> sign
 int exchange_sign(psvd_ctx* c, const double* local_pairs, int nchunks, int K, double* sgn, cudaStream_t st) {
-  if (!c->ex_allgather) {
+  if (!ex_active(c)) {
     launch_colmax_sign(local_pairs, nchunks, K, sgn, st);
     c->launches++;
     return PSVD_OK;
@@ -39,8 +39,14 @@ int exchange_sign(psvd_ctx* c, const double* local_pairs, int nchunks, int K, do
   double* mine = (double*)c->xpairs.ptr;
   double* all = mine + (size_t)K * 2;
   launch_colmax_reduce(local_pairs, nchunks, K, mine, st);
-  if (c->ex_allgather(c->ex_user, mine, (int64_t)K * 2, all, (void*)st) != 0)
-    return fail(c, PSVD_ECUDA, "allgather hook failed");
+  if (c->nccl_on) {
+    if ((rc = nccl_allgather(c, mine, (int64_t)K * 2, all, st))) return rc;
+  } else {
+    c->ex_calls++;
+    c->ex_bytes += 16 * (int64_t)K * (c->ex_nranks - 1);
+    if (c->ex_allgather(c->ex_user, mine, (int64_t)K * 2, all, (void*)st) != 0)
+      return fail(c, PSVD_ECUDA, "allgather hook failed");
+  }
   launch_colmax_sign(all, c->ex_nranks, K, sgn, st);  // rank order = global row order: first rank wins ties
   c->launches += 2;
   return PSVD_OK;
@@ -278,7 +284,7 @@ int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu
   if (K < 1 || l < K || q < 0) return fail(c, PSVD_EINVAL, "bad sketch K=%d l=%d q=%d", K, l, q);
   if (l > TMA_MAX_Y || !tma_available() || !qw_colmax_supported(l, K))
     return fail(c, PSVD_EINVAL, "sketch width %d not supported by the pipelined run (use psvd_rand_update)", l);
-  if (c->ex_allreduce) return fail(c, PSVD_EINVAL, "the pipelined randomized run is single-GPU");
+  if (ex_active(c)) return fail(c, PSVD_EINVAL, "the pipelined randomized run is single-GPU");
   if (Kc != 0 && Kc != K) return fail(c, PSVD_EINVAL, "initial state carries %d modes, K=%d", Kc, K);
   if (Kc > 0 && (!U_in || !sigma_in)) return fail(c, PSVD_EINVAL, "null initial state");
   int rc;

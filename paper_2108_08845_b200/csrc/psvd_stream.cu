@@ -144,7 +144,7 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
       // row-partitioned (exchange hooks): U^T U is already the global, normalized Gram; the other
       // blocks are local.  Only the first rank keeps the U^T U block, so the rank-ordered sum
       // below reproduces it exactly
-      const double uu_w = (c->ex_allreduce && c->ex_row_offset != 0) ? 0.0 : 1.0;
+      const double uu_w = (ex_active(c) && c->ex_row_offset != 0) ? 0.0 : 1.0;
       const double* tb = (const double*)c->tbuf.ptr;
       launch_assemble_gram_fused((const double*)c->tiles.ptr, nbua, fused_a0, fused_y, UtU, tb + (size_t)K * K,
                                  prev_resc ? c->d_gate : nullptr, tb, (const double*)c->tiles2[b & 1].ptr,

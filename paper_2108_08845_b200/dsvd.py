@@ -26,6 +26,7 @@ replicated host draw, so every rank runs the identical small factorizations.
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 
 import torch
@@ -140,52 +141,108 @@ def _row_offset(ctx, rows, dev):
     return sum(counts[:ctx.rank]), sum(counts)
 
 
+_NCCL_COMMS = {}  # device index -> the process group whose communicator the library context holds
+
+
+def _nccl_exchange(ctx):
+    """The library's own NCCL data plane for this group: NCCL process groups, unless
+    PSVD_EXCHANGE=python asks for the torch.distributed callbacks (diagnostics)."""
+    if ctx.world_size == 1 or dist.get_backend(ctx.group) != "nccl":
+        return False
+    if os.environ.get("PSVD_EXCHANGE", "nccl") == "python":
+        return False
+    ok = ctypes.c_int(0)
+    nat.lib().psvd_nccl_available(ctypes.byref(ok))
+    return bool(ok.value)
+
+
+def _ensure_nccl_comm(ctx, dev):
+    """One NCCL communicator per library context, created from a unique id rank 0 draws and
+    broadcasts over the process group (psvd_nccl_unique_id / psvd_nccl_init)."""
+    key = dev.index
+    if _NCCL_COMMS.get(key) is ctx.group and key in _NCCL_COMMS:
+        return
+    c = nat.context(dev)
+    idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if ctx.rank == 0:
+        buf = ctypes.create_string_buffer(128)
+        nat.call("psvd_nccl_unique_id", c, buf)
+        idt.copy_(torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8))
+    src = dist.get_global_rank(ctx.group, 0) if ctx.group is not None else 0
+    dist.broadcast(idt, src=src, group=ctx.group)
+    raw = bytes(idt.cpu().numpy().tobytes())
+    with torch.cuda.device(dev):
+        nat.call("psvd_nccl_init", c, ctx.world_size, ctx.rank, raw)
+    _NCCL_COMMS[key] = ctx.group
+
+
 class exchange_hooks:
-    """Context manager: the library's exchange hooks (psvd_set_exchange) on this RankContext
-    for the calls inside; a collective failure re-raises the hook's exception."""
+    """Context manager: the library's row-partitioned exchange for the calls inside.  On NCCL
+    process groups the library issues its own in-stream ncclAllGather + rank-ordered sum
+    (psvd_nccl_enable: no Python in the loop); on gloo (CPU / shared-GPU test harness) it calls
+    back into torch.distributed (psvd_set_exchange).  suspend() / resume() bracket calls that
+    must run without it."""
 
     def __init__(self, ctx, dev, row_offset=None):
         self.ctx, self.dev = ctx, dev
         self.off = row_offset
+        self.ex = None
+        self.nccl = False
+
+    def resume(self):
+        if self.ctx.world_size == 1:
+            return
+        if self.nccl:
+            nat.call("psvd_nccl_enable", self.c, 1, self.off)
+        else:
+            nat.call("psvd_set_exchange", self.c, ctypes.cast(self.ex.ar, nat._vp), ctypes.cast(self.ex.ag, nat._vp),
+                     None, self.ctx.world_size, self.off)
+
+    def suspend(self):
+        if self.ctx.world_size == 1:
+            return
+        if self.nccl:
+            nat.call("psvd_nccl_enable", self.c, 0, 0)
+        else:
+            nat.call("psvd_set_exchange", self.c, None, None, None, 1, 0)
 
     def __enter__(self):
         self.c = nat.context(self.dev)
         if self.ctx.world_size == 1:
-            self.ex = None
             return self
         if self.off is None:
             raise ValueError("exchange_hooks needs the rank's global row offset")
-        self.ex = _Exchange(self.ctx, self.dev)
-        nat.call("psvd_set_exchange", self.c, ctypes.cast(self.ex.ar, nat._vp), ctypes.cast(self.ex.ag, nat._vp),
-                 None, self.ctx.world_size, self.off)
+        self.nccl = _nccl_exchange(self.ctx)
+        if self.nccl:
+            _ensure_nccl_comm(self.ctx, self.dev)
+        else:
+            self.ex = _Exchange(self.ctx, self.dev)
+        self.resume()
         return self
 
     def __exit__(self, et, ev, tb):
-        if self.ex is not None:
-            nat.call("psvd_set_exchange", self.c, None, None, None, 1, 0)
-            if et is not None and issubclass(et, RuntimeError) and self.ex.error is not None:
+        if self.ctx.world_size > 1:
+            self.suspend()
+            if et is not None and issubclass(et, RuntimeError) and self.ex is not None and self.ex.error is not None:
                 raise self.ex.error
         return False
 
 
+def exchange_stats(device=None):
+    """(collectives issued, bytes received) at the library's exchange points since context
+    creation — the reference's CommStats counters (comm.py:74-88)."""
+    out = (ctypes.c_longlong * 2)()
+    nat.call("psvd_exchange_stats", nat.context(device), out)
+    return int(out[0]), int(out[1])
+
+
 def _parallel_rand_update(ctx, U, sigma, A, sketch, ff, dev):
     from .linalg import randomized_update
-    c = nat.context(dev)
     off, total = _row_offset(ctx, A.rows, dev)
     if ctx.world_size == 1:
         return randomized_update(U, sigma, A, sketch, ff, dev)
-    ex = _Exchange(ctx, dev)
-    nat.call("psvd_set_exchange", c, ctypes.cast(ex.ar, nat._vp), ctypes.cast(ex.ag, nat._vp), None,
-             ctx.world_size, off)
-    try:
-        out = randomized_update(U, sigma, A, sketch, ff, dev, total_rows=total)
-    except RuntimeError:
-        if ex.error is not None:
-            raise ex.error
-        raise
-    finally:
-        nat.call("psvd_set_exchange", c, None, None, None, 1, 0)
-    return out
+    with exchange_hooks(ctx, dev, off):
+        return randomized_update(U, sigma, A, sketch, ff, dev, total_rows=total)
 
 
 def _parallel_update(ctx, U, sigma, A, k, ff, dev):
@@ -292,7 +349,7 @@ def parallel_stream_all(ctx, batches_local, config, device=None):
     c = nat.context(dev)
     wlen = window_length(first, dev)
     off = None
-    ex = None
+    ex = None  # exchange_hooks, entered at the first pipelined window
     state, hist = None, []
 
     def per_batch(st0, window):
@@ -300,7 +357,7 @@ def parallel_stream_all(ctx, batches_local, config, device=None):
         # or an update of the window left the Gram route's accuracy range): the row-parallel update
         # (accurate route where gated), the run's exchange hooks off meanwhile
         if ex is not None:
-            nat.call("psvd_set_exchange", c, None, None, None, 1, 0)
+            ex.suspend()
         try:
             st = None if st0 is None else LocalModes(st0.modes, st0.singular_values)
             out = []
@@ -312,8 +369,7 @@ def parallel_stream_all(ctx, batches_local, config, device=None):
             return StreamState(st.modes, st.singular_values, it0 + len(window)), out
         finally:
             if ex is not None:
-                nat.call("psvd_set_exchange", c, ctypes.cast(ex.ar, nat._vp), ctypes.cast(ex.ag, nat._vp), None,
-                         ctx.world_size, off)
+                ex.resume()
 
     def run(window):
         nonlocal state, off, ex
@@ -331,9 +387,7 @@ def parallel_stream_all(ctx, batches_local, config, device=None):
         if off is None:
             off, _ = _row_offset(ctx, M, dev)
             if ctx.world_size > 1:
-                ex = _Exchange(ctx, dev)
-                nat.call("psvd_set_exchange", c, ctypes.cast(ex.ar, nat._vp), ctypes.cast(ex.ag, nat._vp), None,
-                         ctx.world_size, off)
+                ex = exchange_hooks(ctx, dev, off).__enter__()
         state, h = _run_window(state, window, config, dev, rescue=False, ok=True, on_illcond=per_batch)
         hist.extend(h)
 
@@ -346,34 +400,38 @@ def parallel_stream_all(ctx, batches_local, config, device=None):
             window.append(nat.as_device_colmajor(b, dev, "a_local"))
         run(window)
     except (RuntimeError, ValueError):
-        if ex is not None and ex.error is not None:
-            raise ex.error
+        if ex is not None and ex.ex is not None and ex.ex.error is not None:
+            raise ex.ex.error
         raise
     finally:
         if ex is not None:
-            nat.call("psvd_set_exchange", c, None, None, None, 1, 0)
+            ex.suspend()
     return LocalModes(state.modes, state.singular_values), hist
 
 
 def gather_modes(ctx, local_modes, root=0):
     """Stack per-rank mode blocks at the root in rank order (dsvd.py:245-251).
-    Returns the (total_rows, K) tensor at the root and None elsewhere."""
+    Returns the (total_rows, K) tensor at the root and None elsewhere: one gather to the
+    root (NCCL on device buffers; staged through the host on gloo), not an allgather."""
     m = local_modes.modes
     if ctx.world_size == 1:
         return m.contiguous()
     dev = m.device
-    rows = torch.tensor([m.shape[0]], dtype=torch.int64, device=dev)
+    stage = dist.get_backend(ctx.group) != "nccl"
+    rows = torch.tensor([m.shape[0]], dtype=torch.int64, device="cpu" if stage else dev)
     all_rows = [torch.zeros_like(rows) for _ in range(ctx.world_size)]
     dist.all_gather(all_rows, rows, group=ctx.group)
     counts = [int(r.item()) for r in all_rows]
     mx = max(counts)
-    pad = torch.zeros((mx, m.shape[1]), dtype=m.dtype, device=dev)
+    pad = torch.zeros((mx, m.shape[1]), dtype=m.dtype, device="cpu" if stage else dev)
     pad[: m.shape[0]] = m
-    parts = [torch.empty_like(pad) for _ in range(ctx.world_size)]
-    dist.all_gather(parts, pad, group=ctx.group)
+    dst = dist.get_global_rank(ctx.group, root) if ctx.group is not None else root
     if ctx.rank != root:
+        dist.gather(pad, None, dst=dst, group=ctx.group)
         return None
-    return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0)
+    parts = [torch.empty_like(pad) for _ in range(ctx.world_size)]
+    dist.gather(pad, parts, dst=dst, group=ctx.group)
+    return torch.cat([p[:c] for p, c in zip(parts, counts)], dim=0).to(dev)
 
 
 def parallel_qr(ctx, a_local, device=None):

@@ -859,3 +859,49 @@ def test_stream_all_from_parsvd_file_pinned_prefetch(tmp_path):
     lo, hi = p.partition_bounds(12000, 3)[1]
     part = np.concatenate([b.numpy() for b in p.BatchSource(200, path=path, rows=(lo, hi), pinned=True)], axis=1)
     assert np.array_equal(part, a[lo:hi])
+
+
+def test_library_nccl_exchange_world_one_is_bitwise_serial():
+    """The library's own NCCL data plane (psvd_nccl_*: dlopen'ed libnccl, in-stream ncclAllGather +
+    rank-ordered sum at every exchange point, no Python in the loop), on a one-rank communicator:
+    the pipelined deterministic stream, the randomized update and the accurate route all run
+    through it and reproduce the single-GPU results bit for bit; the exchange counters
+    (CommStats analogue) advance."""
+    import ctypes
+    from paper_2108_08845_b200 import _native as nat
+    from paper_2108_08845_b200.dsvd import exchange_stats
+    p = _pkg()
+    dev = torch.device("cuda", 0)
+    c = nat.context(dev)
+    ok = ctypes.c_int(0)
+    nat.lib().psvd_nccl_available(ctypes.byref(ok))
+    assert ok.value == 1
+    a = oracle.burgers_matrix(6000, 800)[:, :600]
+    det = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200)
+    rnd = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200,
+                         sketch=p.RandomSketchConfig(target_rank=10, oversampling=10, power_iterations=1, seed=0))
+    ill = _illcond_matrix(rows=3000, cols=160)
+    icfg = p.StreamConfig(k_modes=40, forget_factor=0.95, batch_columns=80)
+
+    def runs():
+        s1, _ = p.stream_all(_batches(a, 200), det)
+        s2 = p.stream_incorporate(p.stream_initialize(a[:, :200], rnd), a[:, 200:400], rnd)
+        s3 = p.stream_incorporate(p.stream_initialize(ill[:, :80], icfg), ill[:, 80:], icfg)
+        return s1, s2, s3
+
+    base = runs()
+    buf = ctypes.create_string_buffer(128)
+    nat.call("psvd_nccl_unique_id", c, buf)
+    with torch.cuda.device(dev):
+        nat.call("psvd_nccl_init", c, 1, 0, buf.raw)
+    calls0, _ = exchange_stats(dev)
+    nat.call("psvd_nccl_enable", c, 1, 0)
+    try:
+        viann = runs()
+    finally:
+        nat.call("psvd_nccl_enable", c, 0, 0)
+        nat.call("psvd_nccl_destroy", c)
+    calls1, _ = exchange_stats(dev)
+    assert calls1 > calls0
+    for x, y in zip(base, viann):
+        assert torch.equal(x.modes, y.modes) and torch.equal(x.singular_values, y.singular_values)
