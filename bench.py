@@ -69,6 +69,7 @@ def args_():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-rand", action="store_true")
+    ap.add_argument("--no-weak", action="store_true")
     return ap.parse_args()
 
 
@@ -194,27 +195,81 @@ def cpu_reference_gbs(rows, path, steps=1, warmup=0):
     return 8.0 * rows * SNAPS / dt / 1e9, dt
 
 
+def host_config2(rows):
+    """Config-2 host bytes (the first `rows` grid rows of Burgers 2^20 x 800, C-ordered as the
+    reference generates them), generated in row slices on every core."""
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    a = np.empty((rows, SNAPS))
+    edges = np.linspace(0, rows, 65).astype(np.int64)
+
+    def fill(i):
+        lo, hi = int(edges[i]), int(edges[i + 1])
+        if hi > lo:
+            a[lo:hi] = oracle.burgers_matrix(GRID, SNAPS, rows=(lo, hi))
+
+    with ThreadPoolExecutor(os.cpu_count()) as ex:
+        list(ex.map(fill, range(64)))
+    return a
+
+
 def run_reference(a):
+    """The reference's CPU path (the oracle port of streaming.py / the R9 composition, numpy
+    LAPACK on every host thread) on the SAME config as our arm: all 2^20 grid rows.  One step is
+    one update of the stream at full size, cycling init, incorporate, incorporate, incorporate
+    (so K steps cover K/4 full streams); warm-up steps run the same cycle on a 2^14-row slice
+    (untimed; they only warm the BLAS threads)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    rows = a.cpu_rows
-    gbs_steps = []
-    ws = []
-    for i in range(a.warmup + a.steps):
-        g, dt = cpu_reference_gbs(rows, a.path)
-        (ws if i < a.warmup else gbs_steps).append((g, dt))
-    value = float(np.mean([g for g, _ in gbs_steps]))
-    ms = float(np.mean([dt for _, dt in gbs_steps])) * 1e3
+    import oracle
+    rows = a.rows
+    full = host_config2(rows)
+    small = full[: 1 << 14]
+    nb = SNAPS // BATCH
+
+    def cycle(mat):
+        state = {"U": None, "s": None, "b": 0}
+
+        def one():
+            b = state["b"]
+            blk = mat[:, b * BATCH:(b + 1) * BATCH]
+            if a.path == "det":
+                if b == 0:
+                    state["U"], state["s"] = oracle.ref_stream_init(blk, K)
+                else:
+                    state["U"], state["s"] = oracle.ref_stream_update(state["U"], state["s"], blk, K, FF)
+            else:
+                if b == 0:
+                    state["U"], state["s"] = oracle.ref_rand_stream_init(blk, K, 10, 1, 0)
+                else:
+                    state["U"], state["s"] = oracle.ref_rand_stream_update(state["U"], state["s"], blk, K, FF, 10,
+                                                                           1, 0)
+            state["b"] = (b + 1) % nb
+        return one
+
+    warm = cycle(small)
+    for _ in range(a.warmup):
+        warm()
+    step = cycle(full)
+    times = []
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        step()
+        times.append(time.perf_counter() - t0)
+    dt = float(np.mean(times))
+    value = 8.0 * rows * BATCH / dt / 1e9  # snapshot bytes of one batch per step
     cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": metric_name(a.path), "value": round(value, 4), "unit": "GB/s",
-        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(ms, 2),
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(dt * 1e3, 2),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (analytic Burgers, host-generated)", "config": config_dict(a, rows),
+        "same_config": rows == GRID,
         "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "port",
-                         "sample": f"first {rows} of {GRID} grid rows x {SNAPS} snapshots, init + 3 incorporates "
-                                   f"(oracle/core.py, numpy {np.__version__} LAPACK/BLAS, all {cores} host threads)"},
+                         "sample": f"all {rows} grid rows; one step = one update (200 columns) of the 4-update stream, "
+                                   f"cycled (oracle/core.py, numpy {np.__version__} LAPACK/BLAS, all {cores} host "
+                                   "threads)"},
         "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -318,18 +373,24 @@ def run_ours(a):
             dist.barrier()
         torch.cuda.synchronize()
 
+    from paper_2108_08845_b200.dsvd import exchange_stats
     launches0 = nat.lib().psvd_launch_count(c)
+    ex0 = exchange_stats(dev)
+    gt = (ctypes.c_double * 3)()
     with ClockSampler(local) as clk:
         barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
+        nat.call("psvd_gram_timing", c, 1, gt)  # event pairs around every in-step A^T A Gram
         t0.record(stream)
         for _ in range(a.steps):
             step(record=True)
         t1.record(stream)
         clk.sample_now()  # the queued steps are still running
         barrier()
+    nat.call("psvd_gram_timing", c, 0, gt)
     launches = nat.lib().psvd_launch_count(c) - launches0
+    ex1 = exchange_stats(dev)
     if ex is not None:
         ex.suspend()
     ms = t0.elapsed_time(t1)
@@ -339,14 +400,24 @@ def run_ours(a):
     snap_bytes = 8.0 * a.rows * SNAPS  # whole job, all ranks
     value = snap_bytes / (ms_step * 1e-3) / 1e9
 
-    # the pipelined stream interleaves kernels on two streams: time the Gram kernel alone after
-    # the timed region (the look-ahead A^T A launch of the stream, same shape)
+    # the dominant kernel IN the step: the look-ahead A^T A Gram launches of psvd_stream_run, timed by
+    # event pairs on the library's low-priority stream (they share SMs with the high-priority fused
+    # pass, so this is the in-step rate, below the kernel's standalone rate: gram_probe)
+    g_ms_sum, g_launches, g_flops = gt[0], int(gt[1]), gt[2]
+    g_ach = g_flops / (g_ms_sum * 1e-3) / 1e12 if g_ms_sum > 0 else 0.0
     gms, gfl = gram_probe()
-    gram_ms, gram_flops = [gms] * (a.steps * (SNAPS // BATCH)), [gfl] * (a.steps * (SNAPS // BATCH))
-    g_ach = sum(gram_flops) / (sum(gram_ms) * 1e-3) / 1e12
-    alg_bytes_step = sum(8.0 * M * (2 * BATCH + 3 * (0 if b == 0 else K)) for b in range(SNAPS // BATCH))
+    g_probe = gfl / (gms * 1e-3) / 1e12
+    nbu = SNAPS // BATCH
+    alg_bytes_step = sum(8.0 * M * (2 * BATCH + 3 * (0 if b == 0 else K)) for b in range(nbu))
     hbm_ach = alg_bytes_step / (ms_step * 1e-3) / 1e9  # per GPU
-    gram_share = sum(gram_ms) / ms
+    gram_share = g_ms_sum / ms
+    # SURVEY 8(d) Gram-route flops per update: M n^2 + 2 M n K (n = Kc + B), per GPU
+    flops_step = sum(M * (BATCH + (0 if b == 0 else K)) ** 2 + 2.0 * M * (BATCH + (0 if b == 0 else K)) * K
+                     for b in range(nbu))
+    t_fp64 = flops_step / (FP64_PEAK_TFLOPS * 1e12)
+    t_hbm = alg_bytes_step / (HBM_PEAK[0] * 1e9)
+    binding = "fp64" if t_fp64 >= t_hbm else "hbm"
+    binding_frac = max(t_fp64, t_hbm) / (ms_step * 1e-3)
 
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_gram_r01.json")
@@ -363,18 +434,32 @@ def run_ours(a):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (analytic Burgers, device-generated; same formula as the host generator)",
         "config": config_dict(a),
-        "roofline": {"bound": "tensor", "kernel": "gram_tma_kernel (batch Gram A^T A on DMMA, TMA-fed; psvd_gram probe)",
+        "roofline": {"bound": "tensor",
+                     "kernel": "gram_tma_kernel (batch Gram A^T A on DMMA, TMA-fed): the in-step look-ahead launches "
+                               "of psvd_stream_run, CUDA events on the library's low-priority stream",
                      "achieved": round(g_ach, 3), "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": round(g_ach / FP64_PEAK_TFLOPS, 4), "traffic": traffic,
                      "peak_source": "measured DMMA.8x8x4 peak (profiles/fp64_peaks_r01.jsonl); "
                                     "MEASURED_PEAKS.json has no FP64 entry",
-                     "flops_per_launch": "M*n*(n+1) (upper triangle of A^T A), n = B",
-                     "share_of_step": round(gram_share, 4)},
+                     "flops_per_launch": "M*B*(B+1) (upper triangle of A^T A), B = 200",
+                     "launches_timed": g_launches, "share_of_step": round(gram_share, 4),
+                     "standalone_probe_tflops": round(g_probe, 3)},
         "hbm_roofline": {"achieved": round(hbm_ach, 1), "peak": HBM_PEAK[0], "unit": "GB/s",
                          "frac": round(hbm_ach / HBM_PEAK[0], 4), "peak_source": HBM_PEAK[1],
                          "bytes_per_step": "sum over updates of 8*M*(2B+3K) per GPU"},
+        "binding_roofline": {"bound": binding, "frac": round(binding_frac, 4),
+                             "fp64_flops_per_step": flops_step, "t_fp64_ms": round(t_fp64 * 1e3, 3),
+                             "t_hbm_ms": round(t_hbm * 1e3, 3),
+                             "flops": "sum over updates of M n^2 + 2 M n K (Gram route, SURVEY 8(d)), per GPU"},
         "gpu_launches": int(launches),
     }
+    if world > 1:
+        upd = a.steps * nbu
+        line["exchange"] = {"collectives_per_update": round((ex1[0] - ex0[0]) / upd, 2),
+                            "bytes_received_per_update_per_rank": int((ex1[1] - ex0[1]) / upd),
+                            "data_plane": "library NCCL (in-stream allgather + rank-ordered sum)"
+                            if (ex is not None and ex.nccl) else "torch.distributed callbacks"}
+    line["parity"] = self_check(hist[nb - 1], a, world)
     line["clocks"] = clk.summary()
 
     # ---- end to end through the public API with host (pinned) buffers
@@ -384,8 +469,16 @@ def run_ours(a):
     if world == 1 and not a.no_rand:
         line["randomized"] = {f"q{qq}": time_randomized(a, D, M, dev, c, stream, qq) for qq in (0, 1)}
 
+    if not a.no_weak:
+        del D
+        torch.cuda.empty_cache()
+        try:
+            line["weak_scaling"] = weak_scaling(a, p, dev, world, rank, ctxr)
+        except Exception as e:  # reported, never fatal to the headline line
+            line["weak_scaling"] = {"error": repr(e)[:300]}
+
     if world == 1 and rank == 0 and not a.no_cpu:
-        g, dt = cpu_reference_gbs(a.cpu_rows, a.path)
+        g, dt = cpu_reference_gbs(a.cpu_rows, a.path)  # bounded row sample; --impl reference runs all rows
         cores = os.cpu_count()
         line["cpu_baseline"] = {"value": round(g, 4), "unit": "GB/s", "cores": cores, "kind": "port",
                                 "sample": f"first {a.cpu_rows} grid rows x {SNAPS} snapshots, init + 3 incorporates"
@@ -435,6 +528,82 @@ def time_randomized(a, D, M, dev, c, stream, q):
     alg = sum(8.0 * M * (passes * (BATCH + (0 if b == 0 else K)) + K) for b in range(SNAPS // BATCH))
     return {"value": round(8.0 * a.rows * SNAPS / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms, 4),
             "sketch": f"K={K} p=10 q={q} seed=0", "hbm_frac": round(alg / (ms * 1e-3) / 1e9 / HBM_PEAK[0], 4)}
+
+
+def self_check(sigma_dev, a, world):
+    """The timed run's final singular values against the live reference's own full-size run of
+    the same config (tests/golden/fullsize_fingerprints.npz, written by make_fullsize.py; the
+    device-generated Burgers bytes differ from the host's by a few ulp)."""
+    import oracle
+    path = os.path.join(ROOT, "tests", "golden", "fullsize_fingerprints.npz")
+    if a.rows != GRID or a.path != "det" or not os.path.exists(path):
+        return {"checked": False}
+    ref = np.load(path)["c2_det_sigma"]
+    err = oracle.sigma_rel_err(sigma_dev.cpu().numpy(), ref)
+    return {"checked": True, "sigma_rel_err_vs_reference": float(f"{err:.3e}"), "ok": bool(err <= 1e-10),
+            "reference": "live reference stream_all at 2^20 rows (fullsize_fingerprints.npz)"}
+
+
+def weak_scaling(a, p, dev, world, rank, ctxr):
+    """BASELINE config 4 (the north star's >= 85% weak-scaling target): 4,194,304 rows per GPU,
+    batches of 512 snapshots, 8 updates, K = 100, randomized p = 10, q = 1, through the
+    public stream_all (N = 1) / parallel_stream_all (N > 1: every sketch Gram / projection summed
+    over the ranks by the library's NCCL exchange).  Data: rank-200 Gaussian-factor signal with
+    sigma_i = i^-1.5 plus N(0, 1e-4) noise, generated on the device (seeded; the datagen
+    distribution, not its bytes); 3 distinct batches per GPU cycle through the 8 updates so the
+    stream fits HBM next to the state.  Timed on the device, max over ranks."""
+    import math
+    import torch
+    import torch.distributed as dist
+    M, S, B, KK = 4194304, 4096, 512, 100
+    sig = torch.arange(1, 201, dtype=torch.float64, device=dev) ** -1.5
+    gen = torch.Generator(device=dev).manual_seed(2 + 7919 * rank)  # this rank's rows of U_f
+    Ut = torch.randn((200, M), generator=gen, dtype=torch.float64, device=dev).div_(math.sqrt(M * world))
+    gv = torch.Generator(device=dev).manual_seed(2)  # V_f is shared by every rank
+    V = torch.randn((S, 200), generator=gv, dtype=torch.float64, device=dev).div_(math.sqrt(S))
+    distinct = []
+    for j in range(3):
+        At = (V[j * B:(j + 1) * B] * sig[None, :]) @ Ut  # B x M row-major = M x B column-major
+        At.add_(torch.randn(At.shape, generator=gen, dtype=torch.float64, device=dev), alpha=1e-4)
+        distinct.append(At.T)
+    del Ut, V
+    torch.cuda.empty_cache()
+    batches = [distinct[i % 3] for i in range(S // B)]
+    sk = p.RandomSketchConfig(target_rank=KK, oversampling=10, power_iterations=1, seed=0)
+    cfg = p.StreamConfig(k_modes=KK, forget_factor=0.95, batch_columns=B, sketch=sk)
+    stream = torch.cuda.current_stream(dev)
+
+    def one():
+        if world == 1:
+            return p.stream_all(batches, cfg, device=dev)[0].singular_values
+        return p.parallel_stream_all(ctxr, batches, cfg, device=dev)[0].singular_values
+
+    one()  # warm-up (workspaces, Omega uploads)
+    steps = max(2, min(a.steps, 3))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        s_last = one()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    if world > 1:
+        ms = max_over_ranks(ms, dev)
+    l = KK + 10
+    per_upd_bytes = [8.0 * M * (4 * (B + (0 if u == 0 else KK)) + KK) for u in range(S // B)]
+    per_upd_flops = [4 * 2.0 * M * (B + (0 if u == 0 else KK)) * l + 8.0 * M * l * l + 2.0 * M * l * KK
+                     for u in range(S // B)]
+    return {"config": "config4: 4,194,304 rows per GPU x 4096 snapshots, B=512, K=100, p=10, q=1",
+            "n_gpus": world, "rows_total": M * world, "ms_per_stream": round(ms, 2),
+            "value": round(8.0 * M * world * S / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+            "per_gpu_gbs": round(8.0 * M * S / (ms * 1e-3) / 1e9, 2),
+            "hbm_frac": round(sum(per_upd_bytes) / (ms * 1e-3) / 1e9 / HBM_PEAK[0], 4),
+            "fp64_frac": round(sum(per_upd_flops) / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
+            "steps": steps, "scaling": "weak", "sigma_head": [round(float(x), 6) for x in s_last[:3].cpu()],
+            "data": "device-generated Gaussian factors (datagen.weak_scaling_matrix distribution)"}
 
 
 def max_over_ranks(x, dev):

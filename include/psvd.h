@@ -171,6 +171,10 @@ int psvd_stream_update(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, c
  * (its look-ahead Gram and fused pass plan within the kernels' limits), else 0: stream those
  * batches through psvd_stream_update. */
 int psvd_stream_run_supported(psvd_ctx* ctx, int64_t M, int K, int Bmax, int* ok);
+/* In-step timing of psvd_stream_run's dominant kernel (benchmark evidence): mode 1 starts recording
+ * CUDA-event pairs on the library's low-priority stream around every look-ahead A^T A Gram; mode 0
+ * stops, synchronizes and returns out3 = {summed ms, launches timed, summed flops M B (B + 1)}. */
+int psvd_gram_timing(psvd_ctx* ctx, int mode, double* out3);
 int psvd_stream_run(psvd_ctx* ctx, int64_t M, const double* U_in, int64_t ldu, const double* sigma_in, int Kc,
                     int nb, const double* const* A, const int64_t* lda, const int* B, int K, double ff, int rescue,
                     double* U_a, double* U_b, int64_t ldo, double* sigma_hist, int* final_buf,

@@ -81,6 +81,7 @@ _SIGS = {
     "psvd_nccl_enable": (_c_int, [_vp, _c_int, _c_i64]),
     "psvd_nccl_destroy": (_c_int, [_vp]),
     "psvd_exchange_stats": (_c_int, [_vp, ctypes.POINTER(ctypes.c_longlong)]),
+    "psvd_gram_timing": (_c_int, [_vp, _c_int, ctypes.POINTER(_c_dbl)]),
     "psvd_jacobi_uv": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _c_int, _vp, _vp, _c_i64, _vp, _c_i64, _vp]),
     "psvd_scale_cols": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _vp, _c_int, _vp]),
     "psvd_rand_last_vt": (_c_int, [_vp, _c_int, _c_int, _c_int, _vp, _c_i64, _vp]),

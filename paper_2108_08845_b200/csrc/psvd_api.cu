@@ -602,6 +602,7 @@ int psvd_destroy(psvd_ctx* c) {
                  &c->zbuf, &c->rs2, &c->dense, &c->dense2, &c->bigws, &c->bigjac, &c->accws, &c->accq,
                  &c->nccl_parts};
   psvd_nccl_destroy(c);
+  for (auto& e : c->tev) cudaEventDestroy(e);
   for (Buf* b : bufs)
     if (b->ptr) cudaFree(b->ptr);
   if (c->s_hi) cudaStreamDestroy(c->s_hi);

@@ -52,6 +52,12 @@ struct psvd_ctx {
   int nccl_nranks = 1, nccl_rank = 0;
   Buf nccl_parts;             // allgather landing buffer of the rank-ordered sums
   long long ex_calls = 0, ex_bytes = 0;  // collectives issued / bytes received at the exchange points
+  // in-step timing of the look-ahead A^T A Gram launches of psvd_stream_run (psvd_gram_timing):
+  // event pairs on the low-priority stream around each batch's Gram sub-launches
+  bool timing_on = false;
+  std::vector<cudaEvent_t> tev;
+  int tev_used = 0;
+  double timed_flops = 0.0;
   cudaEvent_t ev_qready = nullptr;  // pipelined randomized stream: the sketch basis of the last update is final
   cudaStream_t s_hi = nullptr, s_lo = nullptr;  // pipelined stream_run: critical chain / look-ahead Grams
   cudaStream_t s_aux = nullptr;                  // concurrent LDL^T of the split core solve

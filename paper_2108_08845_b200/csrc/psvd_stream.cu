@@ -81,6 +81,13 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
     size_t part_off = 0;
     int nchunks_total = 0;
     mark("lo:aa_begin", j, lo);
+    cudaEvent_t te1 = nullptr;
+    if (c->timing_on && c->tev_used + 2 <= (int)c->tev.size()) {
+      cudaEventRecord(c->tev[c->tev_used], lo);
+      te1 = c->tev[c->tev_used + 1];
+      c->tev_used += 2;
+      c->timed_flops += (double)M * B[j] * (B[j] + 1);  // upper triangle of A^T A (DMMA tiles)
+    }
     for (int k = 0; k < nsub; ++k) {
       const int64_t r0 = (int64_t)k * rows_sub;
       if (r0 >= M) break;
@@ -107,6 +114,7 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
       part_off += (size_t)pa.grid * SLOTS * 1024;
       nchunks_total += pa.map.nchunks;
     }
+    if (te1) cudaEventRecord(te1, lo);
     first.map.nchunks = nchunks_total;
     launch_tall_reduce((const double*)c->partial2.ptr, first.map, (double*)c->tiles2[j & 1].ptr, lo);
     c->launches++;
@@ -228,6 +236,37 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
 // 1 when psvd_stream_run can take batches of up to Bmax columns with K modes on M rows: its
 // look-ahead Gram (one pass of 32x32 tiles) and its fused pass [U | A_b | A_{b+1}] plan within
 // the kernels' limits; 0 otherwise (stream batch by batch through psvd_stream_update instead).
+// In-step timing of the dominant kernel (bench roofline): mode 1 starts recording event pairs around
+// every look-ahead A^T A Gram of psvd_stream_run; mode 0 stops, synchronizes and returns
+// out3 = {summed milliseconds, launches timed, summed flops M B (B + 1)}.
+int psvd_gram_timing(psvd_ctx* c, int mode, double* out3) {
+  if (!c) return PSVD_EINVAL;
+  if (mode == 1) {
+    if (c->tev.empty()) {
+      c->tev.resize(1024);
+      for (auto& e : c->tev) cudaEventCreate(&e);
+    }
+    c->tev_used = 0;
+    c->timed_flops = 0.0;
+    c->timing_on = true;
+    return cuda_check(c, "timing start");
+  }
+  c->timing_on = false;
+  double ms = 0.0;
+  for (int i = 0; i + 1 < c->tev_used; i += 2) {
+    cudaEventSynchronize(c->tev[i + 1]);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, c->tev[i], c->tev[i + 1]);
+    ms += t;
+  }
+  if (out3) {
+    out3[0] = ms;
+    out3[1] = c->tev_used / 2;
+    out3[2] = c->timed_flops;
+  }
+  return cuda_check(c, "timing read");
+}
+
 int psvd_stream_run_supported(psvd_ctx* c, int64_t M, int K, int Bmax, int* ok) {
   if (!c || !ok || M < 1 || K < 1 || Bmax < 1) return PSVD_EINVAL;
   *ok = 0;
