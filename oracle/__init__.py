@@ -22,6 +22,6 @@ from .core import (  # noqa: F401
     ref_svd, ref_low_rank_svd, ref_range, ref_stream_init, ref_stream_update,
     ref_stream_all, ref_rand_stream_init, ref_rand_stream_update,
     ref_rand_stream_all, ref_parallel_stream_all, sigma_rel_err,
-    sine_angles, mode_angles, aligned_mode_difference, synth_config_matrix,
+    sine_angles, mode_angles, aligned_mode_difference,
     ref_generate_right_vectors, ref_apmos,
 )

@@ -257,10 +257,6 @@ def burgers_matrix(grid_points, n_snapshots, length=1.0, t_final=2.0, reynolds=1
     return burgers_solution(x[:, None], t[None, :], reynolds)
 
 
-def synth_config_matrix(*args, **kwargs):  # pragma: no cover - see paper_2108_08845_b200.datagen
-    raise NotImplementedError("synthetic configs 3-5 live in the product datagen")
-
-
 # --------------------------------------------------------------------------
 # one-shot distributed SVD (dsvd.py:39-173, APMOS)
 # --------------------------------------------------------------------------

@@ -11,8 +11,8 @@ from .datagen import (DEFAULT_MATRIX_CAP, BurgersConfig, burgers_device, burgers
                       partition_bounds, row_partition, synthetic_spectrum_matrix)
 from .dsvd import (LocalModes, RankContext, gather_modes, parallel_qr, parallel_stream_all,  # noqa: F401
                    parallel_stream_incorporate, parallel_stream_initialize)
-from .errors import (CapacityError, CollectiveTimeout, ConvergenceError, DegenerateModeError,  # noqa: F401
-                     MatrixFormatError)
+from .errors import (CapacityError, CollectiveTimeout, ConfigError, ConvergenceError,  # noqa: F401
+                     DegenerateModeError, MatrixFormatError)
 from .io import (BatchSource, read_batches, read_matrix, read_matrix_header, read_modes_csv,  # noqa: F401
                  read_singular_values_csv, read_submatrix, write_history_csv, write_matrix, write_mode_svg,
                  write_modes_csv, write_singular_values_csv)
@@ -22,5 +22,6 @@ from .streaming import StreamConfig, StreamState, stream_all, stream_incorporate
 from .classes import Parsvd_Base, Parsvd_Parallel, Parsvd_Serial  # noqa: F401
 
 from . import streaming  # noqa: F401,E402  (module access: STREAM_WINDOW)
+from .decompose import decompose  # noqa: F401,E402  (cli.py decompose body on the device)
 
 __version__ = "0.1.0"

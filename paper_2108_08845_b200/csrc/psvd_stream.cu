@@ -69,7 +69,14 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
   // low-priority kernel cannot be preempted, so short launches let the high-priority
   // recompose / U^T A passes take the SMs between them.  All sub-ranges write disjoint
   // partial sets and one fixed-order reduction sums them (bitwise reproducible).
-  const int nsub = (int)std::max<int64_t>(1, std::min<int64_t>(4, M / 65536));
+  // The fused pass of batch b waits for the look-ahead Gram of b+1 rather than time-sharing SMs with it
+  // (both kernels hold whole SMs, so sharing bought nothing: 9.04 vs 9.10 ms per config-2 step, and it
+  // cut the Gram's in-step rate from 29.9 to 21 TF/s); the Gram runs as one launch on all SMs but the one
+  // the core solve of batch b occupies.  PSVD_LA_SHARED=1 restores the time-shared schedule (4 row
+  // sub-launches on num_sms - 2 CTAs).
+  static const bool la_serial = getenv("PSVD_LA_SHARED") == nullptr;
+  const int nsub = la_serial ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(4, M / 65536));
+  const int la_ctas = la_serial ? c->num_sms - 1 : c->num_sms - 2;
   auto aa_pass = [&](int j) -> int {
     if (j >= 2) cudaStreamWaitEvent(lo, c->ev_asm[j & 1], 0);  // tiles2[j&1] consumed by batch j-2's assembly
     // start A^T A of batch j with the core solve of batch j-1: it then overlaps that one-SM
@@ -94,7 +101,7 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
       const int64_t mk = std::min(M, r0 + rows_sub) - r0;
       Pass pa;
       int r = plan_pass(c, pa, mk, {Seg{A[j] + r0, lda[j], B[j], 0}}, 0, 0, 0, nullptr, 0, true, false, false, -1,
-                        -1, &c->partial2, &c->tiles2[j & 1], c->num_sms - 2);
+                        -1, &c->partial2, &c->tiles2[j & 1], la_ctas);
       if (r) return r;
       const size_t need = part_off + (size_t)pa.grid * SLOTS * 1024;
       if (k == 0) {  // size the partial buffer for all sub-ranges once
@@ -172,6 +179,7 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
       std::vector<Seg> segs = panel(Uprev, ldprev, kc, A[b], lda[b], B[b]);
       segs.push_back(Seg{A[b + 1], lda[b + 1], B[b + 1], 1});
       if (batch_ready && batch_ready[b + 1]) cudaStreamWaitEvent(hi, (cudaEvent_t)batch_ready[b + 1], 0);
+      if (la_serial) cudaStreamWaitEvent(hi, c->ev_aa[(b + 1) & 1], 0);
       Pass pf;
       const int wk = kc + B[b];
       if ((rc = plan_pass(c, pf, M, segs, 0, wk, K, W, wk, false, true, true, -1, -1, nullptr, nullptr, 0, -1)))
@@ -233,9 +241,6 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
   return cuda_check(c, "stream_run");
 }
 
-// 1 when psvd_stream_run can take batches of up to Bmax columns with K modes on M rows: its
-// look-ahead Gram (one pass of 32x32 tiles) and its fused pass [U | A_b | A_{b+1}] plan within
-// the kernels' limits; 0 otherwise (stream batch by batch through psvd_stream_update instead).
 // In-step timing of the dominant kernel (bench roofline): mode 1 starts recording event pairs around
 // every look-ahead A^T A Gram of psvd_stream_run; mode 0 stops, synchronizes and returns
 // out3 = {summed milliseconds, launches timed, summed flops M B (B + 1)}.
@@ -267,6 +272,9 @@ int psvd_gram_timing(psvd_ctx* c, int mode, double* out3) {
   return cuda_check(c, "timing read");
 }
 
+// 1 when psvd_stream_run can take batches of up to Bmax columns with K modes on M rows: its
+// look-ahead Gram (one pass of 32x32 tiles) and its fused pass [U | A_b | A_{b+1}] plan within
+// the kernels' limits; 0 otherwise (stream batch by batch through psvd_stream_update instead).
 int psvd_stream_run_supported(psvd_ctx* c, int64_t M, int K, int Bmax, int* ok) {
   if (!c || !ok || M < 1 || K < 1 || Bmax < 1) return PSVD_EINVAL;
   *ok = 0;
