@@ -277,6 +277,11 @@ int psvd_sign_pair(psvd_ctx* ctx, double* U, int64_t ldu, int64_t rows, int cols
 int psvd_jacobi_uv(psvd_ctx* ctx, const double* X, int64_t ldx, int64_t m, int n, int transpose, double* S,
                    double* V, int64_t ldv, double* U, int64_t ldu, void* stream);
 
+/* Y (rows x cols, column-major, ld ldy) from a row-major X (row stride ldx): C-ordered input
+ * (the reference's burgers_matrix returns C order) enters the library's column-major layout. */
+int psvd_transpose(psvd_ctx* ctx, const double* X, int64_t ldx, int64_t rows, int64_t cols, double* Y, int64_t ldy,
+                   void* stream);
+
 /* X[:, j] *= s_j, or /= s_j (0 where s_j == 0) with invert = 1. */
 int psvd_scale_cols(psvd_ctx* ctx, double* X, int64_t ld, int64_t rows, int cols, const double* s, int invert,
                     void* stream);

@@ -81,6 +81,7 @@ _SIGS = {
     "psvd_nccl_enable": (_c_int, [_vp, _c_int, _c_i64]),
     "psvd_nccl_destroy": (_c_int, [_vp]),
     "psvd_exchange_stats": (_c_int, [_vp, ctypes.POINTER(ctypes.c_longlong)]),
+    "psvd_transpose": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _vp]),
     "psvd_gram_timing": (_c_int, [_vp, _c_int, ctypes.POINTER(_c_dbl)]),
     "psvd_jacobi_uv": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _c_int, _vp, _vp, _c_i64, _vp, _c_i64, _vp]),
     "psvd_scale_cols": (_c_int, [_vp, _vp, _c_i64, _c_i64, _c_int, _vp, _c_int, _vp]),
@@ -238,7 +239,11 @@ def as_device_colmajor(a, device, name="a"):
             if dm is not None:
                 return dm
         out = DevMat.empty(t.shape[0], t.shape[1], device)
-        if t.device.type == "cpu":
+        if t.dtype == torch.float64 and t.dim() == 2 and t.stride(1) == 1 and t.stride(0) >= t.shape[1]:
+            # row-major fp64 (C order): bytes to the device as they are, transposed by the library
+            src = t if t.device == torch.device(device) else t.to(device, non_blocking=t.is_pinned())
+            _transpose_into(src, out, device)
+        elif t.device.type == "cpu":
             # one H2D copy straight into the column-major buffer (async from pinned memory)
             out.view.copy_(t.to(torch.float64), non_blocking=t.is_pinned())
         else:
@@ -254,10 +259,18 @@ def as_device_colmajor(a, device, name="a"):
     if arr.flags.f_contiguous:
         out.view.T.copy_(torch.from_numpy(arr.T))
     else:
-        # row-major host data: upload as-is, transpose on the device
+        # row-major host data (C order): one H2D copy of its bytes, transposed by the library's kernel
         host = torch.from_numpy(np.ascontiguousarray(arr))
-        out.view.copy_(host.to(device))
+        _transpose_into(host.to(device), out, device)
     return out
+
+
+def _transpose_into(src, out, device):
+    """out (DevMat, column-major) <- src (row-major fp64 CUDA tensor) by psvd_transpose."""
+    with torch.cuda.device(device):
+        call("psvd_transpose", context(device), _vp(src.data_ptr()), src.stride(0), src.shape[0], src.shape[1],
+             _vp(out.data_ptr()), out.ld, stream_ptr(device))
+    src.record_stream(torch.cuda.current_stream(device))
 
 
 def to_host_colmajor(t, pinned=True):

@@ -15,6 +15,24 @@ using namespace psvd_internal;
 
 namespace psvd_internal {
 
+// Y (rows x cols, column-major, ld ldy) = the row-major X (rows x cols, row stride ldx): 32 x 32 tiles
+// through shared memory (padded against bank conflicts), coalesced on both sides.
+__global__ void __launch_bounds__(256) transpose_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows,
+                                                       int64_t cols, double* __restrict__ Y, int64_t ldy) {
+  __shared__ double t[32][33];
+  const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int k = ty; k < 32; k += 8) {
+    const int64_t r = r0 + k, c = c0 + tx;
+    t[k][tx] = (r < rows && c < cols) ? X[r * ldx + c] : 0.0;
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int64_t c = c0 + k, r = r0 + tx;
+    if (r < rows && c < cols) Y[c * ldy + r] = t[tx][k];
+  }
+}
+
 __global__ void scale_cols_any_kernel(double* __restrict__ X, int64_t ld, int64_t rows, int cols,
                                       const double* __restrict__ s, int invert) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -211,6 +229,19 @@ int psvd_sign_pair(psvd_ctx* c, double* U, int64_t ldu, int64_t rows, int cols, 
     c->launches++;
   }
   return cuda_check(c, "sign pair");
+}
+
+// Column-major copy of a row-major device matrix (C-ordered numpy / torch input, as the reference's
+// burgers_matrix returns): X rows x cols with row stride ldx -> Y column-major, ld ldy (even).
+int psvd_transpose(psvd_ctx* c, const double* X, int64_t ldx, int64_t rows, int64_t cols, double* Y, int64_t ldy,
+                   void* stream) {
+  if (!c) return PSVD_EINVAL;
+  if (!X || !Y || rows < 1 || cols < 1 || ldx < cols || ldy < rows) return fail(c, PSVD_EINVAL, "bad transpose");
+  dim3 g((unsigned)((rows + 31) / 32), (unsigned)((cols + 31) / 32));
+  if (g.y > 65535u) return fail(c, PSVD_EINVAL, "transpose: too many columns for one launch");
+  transpose_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(X, ldx, rows, cols, Y, ldy);
+  c->launches++;
+  return cuda_check(c, "transpose");
 }
 
 // X[:, j] *= s_j (invert = 0) or /= s_j with 0 for s_j == 0 (invert = 1)

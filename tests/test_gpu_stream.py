@@ -531,7 +531,13 @@ def test_wide_randomized_route_matches_fused(monkeypatch):
     _assert_parity(m2, g2, m1, g1, sig_tol=1e-13, ang_tol=1e-11)
 
 
-def _rand_rank_worker(rank, world, port, q):
+def _wide_matrix():
+    """A config-3-like field at reduced rows: the wide randomized route (K = 50, l = 60)."""
+    from paper_2108_08845_b200.datagen import weather_matrix
+    return weather_matrix(n_snapshots=768, nlat=91, nlon=180)
+
+
+def _rand_rank_worker(rank, world, port, q, wide=False):
     import os
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -539,14 +545,15 @@ def _rand_rank_worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2108_08845_b200 as p
-        a = oracle.burgers_matrix(6001, 600)
+        a = _wide_matrix() if wide else oracle.burgers_matrix(6001, 600)
+        k, b = (50, 256) if wide else (10, 200)
         lo, hi = p.partition_bounds(a.shape[0], world)[rank]
-        cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200,
-                             sketch=p.RandomSketchConfig(target_rank=10, oversampling=10, power_iterations=1, seed=0))
+        cfg = p.StreamConfig(k_modes=k, forget_factor=0.95, batch_columns=b,
+                             sketch=p.RandomSketchConfig(target_rank=k, oversampling=10, power_iterations=1, seed=0))
         ctx = p.RankContext()
-        st = p.parallel_stream_initialize(ctx, a[lo:hi, :200], cfg)
-        for c0 in (200, 400):
-            st = p.parallel_stream_incorporate(ctx, st, a[lo:hi, c0:c0 + 200], cfg)
+        st = p.parallel_stream_initialize(ctx, a[lo:hi, :b], cfg)
+        for c0 in range(b, a.shape[1], b):
+            st = p.parallel_stream_incorporate(ctx, st, a[lo:hi, c0:c0 + b], cfg)
         full = p.gather_modes(ctx, st)
         if rank == 0:
             q.put((full.cpu().numpy(), st.singular_values.cpu().numpy()))
@@ -557,10 +564,12 @@ def _rand_rank_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_parallel_randomized_two_ranks_match_serial_oracle():
+@pytest.mark.parametrize("wide", [False, True])
+def test_parallel_randomized_two_ranks_match_serial_oracle(wide):
     """Row-partitioned randomized stream (§8(e)): two ranks (two processes sharing this
     GPU, gloo host-staged exchange through the library's collective hooks) reproduce
-    the serial R9 composition on the whole matrix."""
+    the serial R9 composition on the whole matrix; narrow (l = 20, fused passes) and wide
+    (l = 60, the tall-skinny GEMM route the config-4 weak-scaling leg runs)."""
     import socket
     import torch.multiprocessing as mp
     s = socket.socket()
@@ -569,7 +578,7 @@ def test_parallel_randomized_two_ranks_match_serial_oracle():
     s.close()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_rand_rank_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rand_rank_worker, args=(r, 2, port, q, wide)) for r in range(2)]
     for pr in procs:
         pr.start()
     m, s_ = q.get(timeout=300)
@@ -577,9 +586,14 @@ def test_parallel_randomized_two_ranks_match_serial_oracle():
         pr.join(timeout=120)
     assert not (isinstance(m, str) and m == "error"), s_
     assert all(pr.exitcode == 0 for pr in procs)
-    a = oracle.burgers_matrix(6001, 600)
-    rm, rs, _ = oracle.ref_rand_stream_all(_batches(a, 200), 10, 0.95, 10, 1, 0)
-    _assert_parity(m, s_, rm, rs)
+    if wide:
+        a = _wide_matrix()
+        rm, rs, _ = oracle.ref_rand_stream_all(_batches(a, 256), 50, 0.95, 10, 1, 0)
+        _assert_parity(m, s_, rm, rs, sep=_separated(rs))
+    else:
+        a = oracle.burgers_matrix(6001, 600)
+        rm, rs, _ = oracle.ref_rand_stream_all(_batches(a, 200), 10, 0.95, 10, 1, 0)
+        _assert_parity(m, s_, rm, rs)
 
 
 def _det_run_rank_worker(rank, world, port, q, rows, cols, b):
