@@ -929,7 +929,139 @@ sign_weights_kernel(const double* __restrict__ Lg, const double* __restrict__ Z,
   }
 }
 
+// The same factor, blocked: chol(G + delta I) over 32-column panels held in shared memory as dense
+// (n - 32p) x 32 column-major blocks (202 KB at n = 210).  Per panel: warp 0 factors the 32 x 32
+// diagonal block (lane-owned rows, syncwarp only), every thread solves one row below it (forward
+// substitution against the block), and the warps apply the rank-32 trailing update as 8 x 8 DMMA
+// tiles of the lower triangle: 3 CTA barriers per panel instead of one per column (ldlt_pack_kernel:
+// ~367 us at n = 210, one barrier per column and n^3 / 6 shared-memory FMAs).  Zero / negative pivots
+// give zero columns, as ldlt_pack_kernel's.
+constexpr int CP = 8;  // panel width (8: one DMMA k-step pair per trailing tile, a short pivot chain per panel)
+
+__host__ __device__ inline int cp_panels(int n) { return (n + CP - 1) / CP; }
+__host__ __device__ inline size_t cp_doubles(int n) {
+  size_t t = 0;
+  for (int p = 0; p < cp_panels(n); ++p) t += (size_t)(n - CP * p) * CP;
+  return t;
+}
+
+__global__ void __launch_bounds__(EIG_FAST_THREADS, 1)
+chol_panels_kernel(const double* __restrict__ G, int n, double* __restrict__ Lout) {
+  extern __shared__ double sm[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nthr = blockDim.x, nwarps = nthr >> 5;
+  const int P = cp_panels(n);
+  __shared__ int pb[64];  // panel base offsets (n <= 512)
+  __shared__ double red[32];
+  if (tid == 0) {
+    int off = 0;
+    for (int p = 0; p < P; ++p) {
+      pb[p] = off;
+      off += (n - CP * p) * CP;
+    }
+  }
+  double dmax = 0.0;
+  for (int i = tid; i < n; i += nthr) dmax = fmax(dmax, G[(size_t)i * n + i]);
+  dmax = warp_max(dmax);
+  if (lane == 0) red[warp] = dmax;
+  __syncthreads();
+  double gmax = 0.0;
+  for (int w = 0; w < nwarps; ++w) gmax = fmax(gmax, red[w]);
+  const double delta = 10.0 * (double)n * DBL_EPSILON * gmax;  // ldlt_pack_kernel's shift
+  // element (r, c), r >= c: panel p = c / 32, column j = c % 32, row r - 32 p of the (n - 32 p) rows
+  auto at = [&](int r, int c) -> double& {
+    const int p = c / CP;
+    return sm[pb[p] + (c - CP * p) * (n - CP * p) + (r - CP * p)];
+  };
+  for (int j = warp; j < n; j += nwarps) {  // column j: coalesced reads, one panel lookup
+    const int pj = j / CP;
+    double* col = sm + pb[pj] + (j - CP * pj) * (n - CP * pj) - CP * pj;  // col[r] = element (r, j)
+    for (int i = j + lane; i < n; i += 32) col[i] = G[(size_t)j * n + i] + (i == j ? delta : 0.0);
+  }
+  __syncthreads();
+  for (int p = 0; p < P; ++p) {
+    const int c0 = CP * p, w = min(CP, n - c0), nr = n - c0;
+    double* Pp = sm + pb[p];  // nr x CP, column j at Pp + j nr, local row i
+    if (warp == 0) {
+      // the CP x CP diagonal block in registers, lane i = local row i (padded with the identity past w):
+      // straight-line code, shuffles only
+      double row[CP];
+#pragma unroll
+      for (int j = 0; j < CP; ++j)
+        row[j] = (lane < w && j < w) ? (j <= lane ? Pp[j * nr + lane] : 0.0) : (j == lane ? 1.0 : 0.0);
+#pragma unroll
+      for (int k = 0; k < CP; ++k) {
+        const double d = __shfl_sync(0xffffffffu, row[k], k);
+        const bool ok = d > 0.0;
+        const double lkk = ok ? sqrt(d) : 0.0;
+        const double inv = ok ? 1.0 / lkk : 0.0;
+        const double lik = lane == k ? lkk : (lane > k ? row[k] * inv : 0.0);
+        row[k] = lik;
+#pragma unroll
+        for (int j = k + 1; j < CP; ++j) {
+          const double ljk = __shfl_sync(0xffffffffu, lik, j);  // L(j, k), held by lane j
+          row[j] = lane >= j ? fma(-lik, ljk, row[j]) : row[j];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < CP; ++j)
+        if (lane < w && j <= lane && j < w) Pp[j * nr + lane] = row[j];
+    }
+    __syncthreads();
+    // rows below the block: l_i = a_i L_d^-T, one thread per row, forward substitution in place
+    for (int i = w + tid; i < nr; i += nthr) {
+      for (int k = 0; k < w; ++k) {
+        const double lkk = Pp[k * nr + k];
+        double v = Pp[k * nr + i];
+        for (int j = 0; j < k; ++j) v = fma(-Pp[j * nr + i], Pp[j * nr + k], v);
+        Pp[k * nr + i] = lkk > 0.0 ? v / lkk : 0.0;
+      }
+    }
+    __syncthreads();
+    // trailing update on 8 x 8 DMMA tiles: A(r, c) -= sum_k L(r, k) L(c, k), r >= c >= c0 + w
+    const int t0 = c0 + w;
+    if (t0 < n) {
+      const int nb = (n - t0 + 7) / 8;
+      const int ntiles = nb * (nb + 1) / 2;
+      const int g = lane >> 2, tq = lane & 3;
+      for (int t = warp; t < ntiles; t += nwarps) {
+        int bi = 0, rem = t;  // tile t -> (bi >= bj), row-major over the lower triangle
+        while (rem > bi) { rem -= bi + 1; ++bi; }
+        const int bj = rem;
+        const int r0 = t0 + 8 * bi, cc0 = t0 + 8 * bj;
+        double d0 = 0.0, d1 = 0.0;
+        const int ra = r0 + g, cb = cc0 + g;
+        for (int k0 = 0; k0 < w; k0 += 4) {
+          const int k = k0 + tq;
+          const double a = (ra < n && k < w) ? Pp[k * nr + (ra - c0)] : 0.0;
+          const double b = (cb < n && k < w) ? Pp[k * nr + (cb - c0)] : 0.0;
+          dmma884(d0, d1, a, b);
+        }
+        // d{0,1} = D[g][2 tq + {0,1}]: rows r0 + g, columns cc0 + 2 tq (+1)
+        const int r = r0 + g;
+        const int ca = cc0 + 2 * tq;
+        if (r < n && ca < n && r >= ca) at(r, ca) -= d0;
+        if (r < n && ca + 1 < n && r >= ca + 1) at(r, ca + 1) -= d1;
+      }
+    }
+    __syncthreads();
+  }
+  // packed lower output (ldlt_pack's layout: column c at pidx(n, c, c))
+  for (int j = warp; j < n; j += nwarps) {
+    const int pj = j / CP;
+    const double* col = sm + pb[pj] + (j - CP * pj) * (n - CP * pj) - CP * pj;
+    double* out = Lout + pidx(n, j, j) - j;
+    for (int i = j + lane; i < n; i += 32) out[i] = col[i];
+  }
+}
+
 void launch_ldlt_pack(const double* G, int n, double* Lout, cudaStream_t st) {
+  static const bool old = getenv("PSVD_OLD_LDLT") != nullptr;  // A/B: the unblocked kernel
+  const size_t blocked = cp_doubles(n) * sizeof(double);
+  if (!old && blocked <= 227 * 1024 && cp_panels(n) <= 64) {
+    cudaFuncSetAttribute(chol_panels_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)blocked);
+    chol_panels_kernel<<<1, EIG_FAST_THREADS, blocked, st>>>(G, n, Lout);
+    return;
+  }
   const size_t smem = ((size_t)n * (n + 1) / 2 + (n + 1) / 2 + 1 + 32) * sizeof(double);
   cudaFuncSetAttribute(ldlt_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   ldlt_pack_kernel<<<1, EIG_FAST_THREADS, smem, st>>>(G, n, Lout);
