@@ -214,8 +214,13 @@ class exchange_hooks:
             raise ValueError("exchange_hooks needs the rank's global row offset")
         self.nccl = _nccl_exchange(self.ctx)
         if self.nccl:
-            _ensure_nccl_comm(self.ctx, self.dev)
-        else:
+            try:
+                _ensure_nccl_comm(self.ctx, self.dev)
+            except RuntimeError as e:  # no usable libnccl in this process: the torch.distributed callbacks
+                import warnings
+                warnings.warn(f"library NCCL exchange unavailable ({e}); using torch.distributed callbacks")
+                self.nccl = False
+        if not self.nccl:
             self.ex = _Exchange(self.ctx, self.dev)
         self.resume()
         return self
