@@ -57,14 +57,21 @@ class RankContext:
             self.rank, self.world_size = 0, 1
 
 
-def allreduce_ordered(t, ctx):
+_PY_EXCHANGE = [0, 0]  # collectives / bytes received by allreduce_ordered (the Python-level exchange)
+
+
+def allreduce_ordered(t, ctx, count=True):
     """Sum of `t` over ranks, added in rank order so every rank holds the same
-    bits (an allgather + fixed-order sum)."""
+    bits (an allgather + fixed-order sum).  count=False for the library's
+    hooks, which the library counts itself."""
     if ctx.world_size == 1:
         return t
+    if count:
+        _PY_EXCHANGE[0] += 1
+        _PY_EXCHANGE[1] += 8 * t.numel() * (ctx.world_size - 1)
     t = t.contiguous()
     if t.device.type == "cuda" and dist.get_backend(ctx.group) != "nccl":
-        return allreduce_ordered(t.cpu(), ctx).to(t.device)  # gloo: host-staged (test harness)
+        return allreduce_ordered(t.cpu(), ctx, count=False).to(t.device)  # gloo: host-staged (test harness)
     if t.device.type == "cuda":
         parts = torch.empty((ctx.world_size,) + tuple(t.shape), dtype=t.dtype, device=t.device)
         dist.all_gather_into_tensor(parts, t, group=ctx.group)
@@ -104,9 +111,9 @@ class _Exchange:
             t = nat.wrap_device(ptr, count, self.dev)
             with torch.cuda.stream(self._stream(stream)):
                 if self._device_collectives():
-                    t.copy_(allreduce_ordered(t, self.ctx))
+                    t.copy_(allreduce_ordered(t, self.ctx, count=False))
                 else:  # gloo: stage through the host (blocking copies keep the stream order)
-                    t.copy_(allreduce_ordered(t.cpu(), self.ctx).to(self.dev))
+                    t.copy_(allreduce_ordered(t.cpu(), self.ctx, count=False).to(self.dev))
             return 0
         except Exception as e:  # noqa: BLE001 - reported through the return code
             self.error = e
@@ -234,11 +241,12 @@ class exchange_hooks:
 
 
 def exchange_stats(device=None):
-    """(collectives issued, bytes received) at the library's exchange points since context
-    creation — the reference's CommStats counters (comm.py:74-88)."""
+    """(collectives issued, bytes received) at the exchange points since context creation: the
+    library's (NCCL data plane / hooks) plus the Python-level rank-ordered sums of the per-update
+    row-parallel path — the reference's CommStats counters (comm.py:74-88)."""
     out = (ctypes.c_longlong * 2)()
     nat.call("psvd_exchange_stats", nat.context(device), out)
-    return int(out[0]), int(out[1])
+    return int(out[0]) + _PY_EXCHANGE[0], int(out[1]) + _PY_EXCHANGE[1]
 
 
 def _parallel_rand_update(ctx, U, sigma, A, sketch, ff, dev):
