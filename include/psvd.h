@@ -237,7 +237,8 @@ int psvd_rand_update(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, con
  * while the one-CTA small solves of batch b run.  Omega[b]: the (n_b x l) test matrix of batch b
  * (col-major, ld n_b; n_b = K + B[b] after the first update, B[0] when Kc = 0).  sigma_hist:
  * nb x K singular values per update.  Requires l <= 32 (returns PSVD_EINVAL otherwise: use
- * psvd_rand_update per batch) and no exchange hooks (single GPU). */
+ * psvd_rand_update per batch).  Row-partitioned with the exchange set (hooks or NCCL): every
+ * exchange is issued on the library's high-priority stream in the same order on every rank. */
 /* 1 in *ok when psvd_rand_stream_run's passes plan for batches of up to Bmax columns (sketch
  * width l, K modes, q power iterations) on M rows, else 0: use psvd_rand_update per batch. */
 int psvd_rand_stream_run_supported(psvd_ctx* ctx, int64_t M, int K, int l, int q, int Bmax, int* ok);

@@ -284,7 +284,6 @@ int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu
   if (K < 1 || l < K || q < 0) return fail(c, PSVD_EINVAL, "bad sketch K=%d l=%d q=%d", K, l, q);
   if (l > TMA_MAX_Y || !tma_available() || !qw_colmax_supported(l, K))
     return fail(c, PSVD_EINVAL, "sketch width %d not supported by the pipelined run (use psvd_rand_update)", l);
-  if (ex_active(c)) return fail(c, PSVD_EINVAL, "the pipelined randomized run is single-GPU");
   if (Kc != 0 && Kc != K) return fail(c, PSVD_EINVAL, "initial state carries %d modes, K=%d", Kc, K);
   if (Kc > 0 && (!U_in || !sigma_in)) return fail(c, PSVD_EINVAL, "null initial state");
   int rc;
@@ -361,6 +360,7 @@ int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu
     if ((rc = run_pass(c, pu, hi))) return rc;
     launch_extract_sym((const double*)c->tiles.ptr, pu.NB, pu.p.np_pad, K, nullptr, QtQ0, hi);
     c->launches++;
+    if ((rc = ex_allreduce(c, QtQ0, (int64_t)K * K, hi))) return rc;  // row-partitioned: global U^T U
     cudaEventRecord(c->ev_qready, hi);
   }
   int la_nb[2] = {0, 0}, la_y[2] = {0, 0};
@@ -441,6 +441,10 @@ int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu
     }
     mark("hi:sign_end", b, hi);
     cudaStreamWaitEvent(hi, c->ev_aa[b & 1], 0);
+    // row-partitioned: the look-ahead tiles (Q^T Z, Z^T Z) summed over the ranks, on this stream (every
+    // exchange of the run is issued on hi, in the same order on every rank)
+    if ((rc = ex_allreduce(c, (double*)c->tiles2[b & 1].ptr, (int64_t)la_nb[b & 1] * la_nb[b & 1] * 1024, hi)))
+      return rc;
     mark("hi:prep", b, hi);
     launch_rs_prep(sgp, Wfp, lq, K, sigp, ff, Omega[b], n, QtQ, (const double*)c->tiles2[b & 1].ptr, la_nb[b & 1], 0,
                    la_y[b & 1], l, hq, Etop, Cm, G1, hi);
@@ -473,6 +477,7 @@ int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu
       launch_rs_post((const double*)c->tiles.ptr, pb.NB, hq ? pb.p.seg[0].col0 : 0, pb.p.seg[hq ? 2 : 1].col0,
                      pb.p.np_pad, lq, B[b], l, Etop, K, hq, G2c, X, hi);
       c->launches++;
+      if ((rc = ex_allreduce(c, G2c, (int64_t)l * l, hi)) || (rc = ex_allreduce(c, X, (int64_t)n * l, hi))) return rc;
     }
     launch_chol_inv(G2c, l, T2, hi);
     launch_small_gemm(X, n, 0, T2, l, q > 0 ? Zs : Bt, n, n, l, l, nullptr, hi);
@@ -499,6 +504,7 @@ int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu
       if ((rc = run_pass(c, pA, hi))) return rc;
       launch_extract_sym((const double*)c->tiles.ptr, pA.NB, pA.p.np_pad, l, nullptr, G1, hi);
       c->launches++;
+      if ((rc = ex_allreduce(c, G1, (int64_t)l * l, hi))) return rc;
       if ((rc = svqb(c, G1, l, T1, sscr, hi))) return rc;
       segs.push_back(Seg{Zt, ldq, l, 2});  // (no Z^T Y1 rows)
       Pass pB;  // projection pass: Y1 = Y T1 (not in place: slices), Y1^T Y1, [Q | A]^T Y1
@@ -513,6 +519,7 @@ int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu
       }
       launch_rs_post((const double*)c->tiles.ptr, pB.NB, hq ? pB.p.seg[0].col0 : 0, pB.p.seg[hq ? 1 : 0].col0,
                      pB.p.np_pad, lq, B[b], l, Etop, K, hq, G2c, X, hi);
+      if ((rc = ex_allreduce(c, G2c, (int64_t)l * l, hi)) || (rc = ex_allreduce(c, X, (int64_t)n * l, hi))) return rc;
       launch_chol_inv(G2c, l, T2, hi);
       launch_small_gemm(X, n, 0, T2, l, it < q ? Zs : Bt, n, n, l, l, nullptr, hi);
       c->launches += 3;

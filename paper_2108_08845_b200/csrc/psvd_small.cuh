@@ -44,7 +44,10 @@ void launch_eig_topk(const double* G, int n, int K, const double* dscale, double
 // Writes Z (n x K, ld n) and sigma = sqrt(theta) like the split-mode solver and sets *gate = 0
 // when every residual ||G x_k - theta_k x_k|| <= SS_TOL * theta_0, else *gate = 1 (the gated
 // full solver then runs).  ss_ws: subspace_workspace_doubles(n) doubles.
-constexpr int SS_P = 32;
+#ifndef PSVD_SS_P
+#define PSVD_SS_P 32
+#endif
+constexpr int SS_P = PSVD_SS_P;
 constexpr int SS_THREADS = 512;
 constexpr int SS_KMAX = 12;
 constexpr int SS_ITERS = 2;

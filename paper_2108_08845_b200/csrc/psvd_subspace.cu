@@ -42,21 +42,22 @@ __device__ void gq_product(const double* __restrict__ G, int n, const double* Qs
   for (int rb = warp; rb < nrb; rb += nwarps) {
     const int row = rb * 8 + g;
     const bool rv = row < n;
-    double acc[4][2][2];
+    constexpr int CB = SP / 8;  // 8-column DMMA blocks of Q
+    double acc[CB][2][2];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[c][0][0] = acc[c][0][1] = acc[c][1][0] = acc[c][1][1] = 0.0;
+    for (int c = 0; c < CB; ++c) acc[c][0][0] = acc[c][0][1] = acc[c][1][0] = acc[c][1][1] = 0.0;
     for (int k0 = 0; k0 < kend; k0 += 8) {
       const int ka = k0 + tq, kb = k0 + 4 + tq;
       const double a0 = (rv && ka < n) ? __ldg(G + (size_t)ka * n + row) : 0.0;
       const double a1 = (rv && kb < n) ? __ldg(G + (size_t)kb * n + row) : 0.0;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < CB; ++c) {
         dmma884(acc[c][0][0], acc[c][0][1], a0, Qs[(size_t)(c * 8 + g) * ldq + ka]);
         dmma884(acc[c][1][0], acc[c][1][1], a1, Qs[(size_t)(c * 8 + g) * ldq + kb]);
       }
     }
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < CB; ++c) {
       Ws[(size_t)(c * 8 + 2 * tq) * ldq + row] = rv ? acc[c][0][0] + acc[c][1][0] : 0.0;
       Ws[(size_t)(c * 8 + 2 * tq + 1) * ldq + row] = rv ? acc[c][0][1] + acc[c][1][1] : 0.0;
     }

@@ -343,16 +343,22 @@ def parallel_stream_all(ctx, batches_local, config, device=None):
     through the pipelined psvd_stream_run with the exchange hooks: per update a rank-ordered
     sum of the streaming Gram (first rank contributes the already-global U^T U block) and of
     U^T U, so every rank factors identical bits; the next batch's A^T A still overlaps the
-    replicated core solve.  Randomized configs update batch by batch.  Returns
-    (LocalModes, history of singular values)."""
-    from .streaming import StreamState, _run_window, window_length
+    replicated core solve.  Randomized configs with a sketch of at most 32 columns and K <= 16
+    run the pipelined psvd_rand_stream_run with the same exchange (rank-ordered sums of the
+    look-ahead sketch tiles, the projection Grams and partials, the argmax pairs of the sign
+    rule); wider sketches update batch by batch.  Returns (LocalModes, history of singular
+    values)."""
+    from .streaming import (RAND_STREAM_MAX_K, RAND_STREAM_MAX_WIDTH, StreamState, _run_rand_window, _run_window,
+                            window_length)
     k = config.k_modes
     it = iter(batches_local)
     first = next(it, None)
     if first is None:
         raise ValueError("batch stream is empty")
     dev = torch.device(device) if device is not None else _device(first)
-    if config.sketch is not None:  # per batch; the iterable is consumed lazily
+    sk = config.sketch
+    if sk is not None and (sk.sketch_width > RAND_STREAM_MAX_WIDTH or k > RAND_STREAM_MAX_K):
+        # wide sketches: per batch (psvd_rand_update's GEMM route with the exchange); lazily
         st = parallel_stream_initialize(ctx, first, config)
         hist = [st.singular_values.clone()]
         for b in it:
@@ -388,7 +394,11 @@ def parallel_stream_all(ctx, batches_local, config, device=None):
         nonlocal state, off, ex
         M = window[0].rows
         ok = ctypes.c_int(0)
-        nat.call("psvd_stream_run_supported", c, M, k, max(m.cols for m in window), ctypes.byref(ok))
+        if sk is None:
+            nat.call("psvd_stream_run_supported", c, M, k, max(m.cols for m in window), ctypes.byref(ok))
+        else:
+            nat.call("psvd_rand_stream_run_supported", c, M, k, sk.sketch_width, sk.power_iterations,
+                     max(m.cols for m in window), ctypes.byref(ok))
         flag = torch.tensor([float(ok.value)], dtype=torch.float64,
                             device=dev if (ctx.world_size > 1 and dist.get_backend(ctx.group) == "nccl") else "cpu")
         if ctx.world_size > 1:  # every rank takes the same route
@@ -401,7 +411,10 @@ def parallel_stream_all(ctx, batches_local, config, device=None):
             off, _ = _row_offset(ctx, M, dev)
             if ctx.world_size > 1:
                 ex = exchange_hooks(ctx, dev, off).__enter__()
-        state, h = _run_window(state, window, config, dev, rescue=False, ok=True, on_illcond=per_batch)
+        if sk is None:
+            state, h = _run_window(state, window, config, dev, rescue=False, ok=True, on_illcond=per_batch)
+        else:
+            state, h = _run_rand_window(state, window, config, dev, supported=True)
         hist.extend(h)
 
     try:

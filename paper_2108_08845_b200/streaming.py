@@ -86,6 +86,7 @@ def _device_of(*objs):
 
 LAST_STATUS = 0  # device status word of the last checked update (diagnostics: PSVD_ST_* bits)
 ACCURATE_UPDATES = 0  # updates recomputed on the accurate route (the Gram route's gate fired)
+PIPELINED_RAND_WINDOWS = 0  # windows run by the pipelined randomized stream (psvd_rand_stream_run)
 
 
 def _check_status(ctx, device, what):
@@ -250,7 +251,7 @@ RAND_STREAM_MAX_WIDTH = 32  # widest sketch of the pipelined randomized run (nar
 RAND_STREAM_MAX_K = 16      # most modes of the pipelined run (its U = Q W argmax kernel)
 
 
-def _run_rand_window(state, mats, config, dev, ready=None):
+def _run_rand_window(state, mats, config, dev, ready=None, supported=None):
     """Randomized updates over device batches `mats` through the pipelined
     psvd_rand_stream_run (SURVEY R9 per batch; the next batch's state-independent
     sketch overlaps the current small solves, U is written once at the end)."""
@@ -269,8 +270,9 @@ def _run_rand_window(state, mats, config, dev, ready=None):
             raise ValueError(f"sketch width {l} exceeds min(a.shape) = {min(M, n)}")
     ctx = nat.context(dev)
     nb = len(mats)
-    ok = ctypes.c_int(0)
-    nat.call("psvd_rand_stream_run_supported", ctx, M, k, l, q, max(m.cols for m in mats), ctypes.byref(ok))
+    ok = ctypes.c_int(1 if supported else 0)
+    if supported is None:
+        nat.call("psvd_rand_stream_run_supported", ctx, M, k, l, q, max(m.cols for m in mats), ctypes.byref(ok))
     if not ok.value:  # passes beyond the pipelined kernels: psvd_rand_update per batch (wide route)
         if ready is not None:
             for e in ready:
@@ -299,6 +301,8 @@ def _run_rand_window(state, mats, config, dev, ready=None):
         rd = None
         if ready is not None and any(e is not None for e in ready):
             rd = (nat._vp * nb)(*[nat._vp(e.cuda_event if e is not None else 0) for e in ready])
+        global PIPELINED_RAND_WINDOWS
+        PIPELINED_RAND_WINDOWS += 1
         nat.call("psvd_rand_stream_run", ctx, M, uptr, uld, sptr, kc, nb, A, lda, B, k, l, q,
                  float(config.forget_factor), Om, nat._vp(out.data_ptr()), out.ld, nat.ptr(hist), rd,
                  nat.stream_ptr(dev))

@@ -596,6 +596,78 @@ def test_parallel_randomized_two_ranks_match_serial_oracle(wide):
         _assert_parity(m, s_, rm, rs)
 
 
+def _rand_run_rank_worker(rank, world, port, q, qit):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2108_08845_b200 as p
+        p.streaming.STREAM_WINDOW = 2  # 4 batches = two windows: the second starts from a materialized state
+        a = oracle.burgers_matrix(6001, 800)
+        lo, hi = p.partition_bounds(a.shape[0], world)[rank]
+        cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200,
+                             sketch=p.RandomSketchConfig(target_rank=10, oversampling=10, power_iterations=qit, seed=0))
+        ctx = p.RankContext()
+        n0 = p.streaming.PIPELINED_RAND_WINDOWS
+        st, hist = p.parallel_stream_all(ctx, [a[lo:hi, c0:c0 + 200] for c0 in range(0, 800, 200)], cfg)
+        full = p.gather_modes(ctx, st)
+        q.put((rank, st.singular_values.cpu().numpy(), [h.cpu().numpy() for h in hist],
+               None if full is None else full.cpu().numpy(), p.streaming.PIPELINED_RAND_WINDOWS - n0))
+    except Exception as e:
+        q.put((rank, "error", repr(e), None, 0))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("qit", [0, 1])
+def test_parallel_pipelined_randomized_stream_ranks_match_serial(qit):
+    """VERDICT r1 missing #5: the pipelined randomized stream row-partitioned (psvd_rand_stream_run with
+    the exchange: the look-ahead sketch tiles, the projection Grams / partials and the sign rule's
+    argmax pairs summed / gathered over the ranks; two processes sharing this GPU, gloo): identical
+    singular values on both ranks, two windows, equal to the single-GPU pipelined run and to the
+    serial R9 oracle at the bar."""
+    import socket
+    import torch.multiprocessing as mp
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_rand_run_rank_worker, args=(r, 2, port, q, qit)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = {}
+    for _ in range(2):
+        rank, sig, hist, full, nwin = q.get(timeout=300)
+        assert not (isinstance(sig, str) and sig == "error"), hist
+        out[rank] = (sig, hist, full, nwin)
+    for pr in procs:
+        pr.join(timeout=120)
+    assert all(pr.exitcode == 0 for pr in procs)
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][3] == 2  # the pipelined run, in two windows
+    p = _pkg()
+    a = oracle.burgers_matrix(6001, 800)
+    cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200,
+                         sketch=p.RandomSketchConfig(target_rank=10, oversampling=10, power_iterations=qit, seed=0))
+    old = p.streaming.STREAM_WINDOW
+    try:
+        p.streaming.STREAM_WINDOW = 2
+        st, _ = p.stream_all(_batches(a, 200), cfg)
+    finally:
+        p.streaming.STREAM_WINDOW = old
+    m1, s1 = _np(st)
+    _assert_parity(out[0][2], out[0][0], m1, s1, sig_tol=1e-13, ang_tol=1e-11)
+    rm, rs, rh = oracle.ref_rand_stream_all(_batches(a, 200), 10, 0.95, 10, qit, 0)
+    _assert_parity(out[0][2], out[0][0], rm, rs)
+    for h, r_ in zip(out[0][1], rh):
+        assert oracle.sigma_rel_err(h, r_) <= SIG_TOL
+
+
 def _det_run_rank_worker(rank, world, port, q, rows, cols, b):
     import os
     import torch.distributed as dist
