@@ -203,7 +203,7 @@ size_t hh_qr_workspace_doubles(int m, int n) { return (size_t)m * n + std::min(m
 // The accurate factorization workspace: small matrices in accws, four tall M x n buffers in accq.
 struct AccWs {
   double *G, *lam, *V, *Z, *Wt, *T, *scal, *trace;
-  double *X, *X2, *Q, *Y, *Y2;  // tall M x n buffers (ld)
+  double *X, *X2, *Q, *Y2;  // tall M x n buffers (ld): residual (ping-pong), basis, temporary
   int64_t ld;
 };
 
@@ -212,7 +212,7 @@ static int acc_workspace(psvd_ctx* c, int64_t M, int n, AccWs& w) {
   int rc = ensure(c, c->accws, sizeof(double) * (6 * nn + 4 * (size_t)n + 64));
   if (rc) return rc;
   const int64_t ld = M + (M & 1);
-  if ((rc = ensure(c, c->accq, sizeof(double) * 5 * (size_t)ld * n))) return rc;
+  if ((rc = ensure(c, c->accq, sizeof(double) * 4 * (size_t)ld * n))) return rc;
   double* s = (double*)c->accws.ptr;
   w.G = s;
   w.V = w.G + nn;
@@ -227,8 +227,7 @@ static int acc_workspace(psvd_ctx* c, int64_t M, int n, AccWs& w) {
   w.X = t;
   w.X2 = t + (size_t)ld * n;
   w.Q = t + 2 * (size_t)ld * n;
-  w.Y = t + 3 * (size_t)ld * n;
-  w.Y2 = t + 4 * (size_t)ld * n;
+  w.Y2 = t + 3 * (size_t)ld * n;
   return PSVD_OK;
 }
 
@@ -306,7 +305,10 @@ int range_basis(psvd_ctx* c, int64_t M, int n, AccWs& w, int* r_out, cudaStream_
     if (k == 0) break;
     for (int i = 0; i < k; ++i) scal[i] = 1.0 / std::sqrt(lam[i]);
     cudaMemcpyAsync(w.scal, scal.data(), sizeof(double) * k, cudaMemcpyHostToDevice, st);
-    double* Y = w.Y;
+    // the new block is built in place in the basis (columns r .. r + k); its two-pass projections and
+    // CholeskyQR2 ping-pong with Y2 an even number of times, so it ends where it started
+    double* Qk = w.Q + (size_t)r * w.ld;
+    double* Y = Qk;
     double* Yt = w.Y2;
     const GemmSeg gx{X, w.ld, n};
     launch_tgemm_nn(M, &gx, 1, w.V, n, k, Y, w.ld, st);  // Y = X V_k Lambda_k^-1/2
@@ -314,9 +316,7 @@ int range_basis(psvd_ctx* c, int64_t M, int n, AccWs& w, int* r_out, cudaStream_
     c->launches += 2;
     if ((rc = project_out(c, M, w.Q, w.ld, r, Y, Yt, w.ld, k, w, st))) return rc;
     if ((rc = cqr2(c, M, Y, Yt, w.ld, k, w, st))) return rc;
-    double* Qk = w.Q + (size_t)r * w.ld;
-    cudaMemcpy2DAsync(Qk, w.ld * sizeof(double), Y, w.ld * sizeof(double), M * sizeof(double), k,
-                      cudaMemcpyDeviceToDevice, st);
+    if (Y != Qk) return fail(c, PSVD_ECUDA, "range basis: block not back in place");
     if ((rc = project_out(c, M, Qk, w.ld, k, X, Xt, w.ld, n, w, st))) return rc;  // X <- X - Qk (Qk^T X)
     r += k;
   }
@@ -328,7 +328,8 @@ int range_basis(psvd_ctx* c, int64_t M, int n, AccWs& w, int* r_out, cudaStream_
 int complete_basis(psvd_ctx* c, int64_t M, int r, int ncols, AccWs& w, cudaStream_t st) {
   const int k = ncols - r;
   if (k <= 0) return PSVD_OK;
-  double* Y = w.Y;
+  double* Qk = w.Q + (size_t)r * w.ld;  // built in place (an even number of ping-pongs with Y2)
+  double* Y = Qk;
   double* tmp = w.Y2;
   candidates_kernel<<<(unsigned)std::min<int64_t>(4096, (M * k + 255) / 256), 256, 0, st>>>(
       Y, w.ld, M, k, c->ex_row_offset, 0x5eed5eedULL + (unsigned long long)r);
@@ -338,8 +339,7 @@ int complete_basis(psvd_ctx* c, int64_t M, int r, int ncols, AccWs& w, cudaStrea
   if ((rc = cqr2(c, M, Y, tmp, w.ld, k, w, st))) return rc;
   if ((rc = project_out(c, M, w.Q, w.ld, r, Y, tmp, w.ld, k, w, st))) return rc;
   if ((rc = cqr2(c, M, Y, tmp, w.ld, k, w, st))) return rc;
-  cudaMemcpy2DAsync(w.Q + (size_t)r * w.ld, w.ld * sizeof(double), Y, w.ld * sizeof(double), M * sizeof(double), k,
-                    cudaMemcpyDeviceToDevice, st);
+  if (Y != Qk) return fail(c, PSVD_ECUDA, "complete basis: block not back in place");
   return cuda_check(c, "complete basis");
 }
 
