@@ -313,6 +313,11 @@ void launch_tgemm_nn(int64_t M, const GemmSeg* segs, int nseg, const double* W, 
     const size_t sm = nn_smem(64, K);
     cudaFuncSetAttribute(tgemm_nn_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     tgemm_nn_kernel<64><<<dim3(gx, 1), GT, sm, st>>>(M, t, K, W, ldw, N, C, ldc);
+  } else if (N <= 112) {
+    // 14 column blocks (the l = K + p = 110 sketch of config 4 pads to 112 instead of 128)
+    const size_t sm = nn_smem(112, K);
+    cudaFuncSetAttribute(tgemm_nn_kernel<112>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    tgemm_nn_kernel<112><<<dim3(gx, 1), GT, sm, st>>>(M, t, K, W, ldw, N, C, ldc);
   } else {
     const size_t sm = nn_smem(128, K);
     cudaFuncSetAttribute(tgemm_nn_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
