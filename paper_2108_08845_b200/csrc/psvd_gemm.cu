@@ -143,16 +143,20 @@ constexpr int TO = 64;          // output tile edge
 #define TN_CTAS_PER_SM 3        // split-K CTAs per SM (3 fit by shared memory)
 #endif
 
-// partial[(chunk * ntk + kt) * ntn + nt][64 x 64] (row-major 64x64, row = P column)
+// partial[(chunk * ntk + kt) * ntn + nt][64 x TON] (row-major, row = P column).  TON = 64, or 112 for
+// 64 < N <= 112 (config 4's l = 110 sketch: one column tile, so P is read once per row chunk and the tile
+// pads to 112 instead of 128)
+template <int TON>
 __global__ void __launch_bounds__(GT) tgemm_tn_kernel(int64_t M, int64_t rows_per_chunk, ColTable P, int K,
                                                       const double* __restrict__ Y, int64_t ldy, int N, int ntk,
                                                       int ntn, int sym, double* __restrict__ partial) {
   // sym: P == Y (a Gram): tiles below the diagonal are not computed (the reduce mirrors them)
   if (sym && (int)(blockIdx.x % (ntk * ntn)) / ntn > (int)(blockIdx.x % (ntk * ntn)) % ntn) return;
+  constexpr int BW = TON / 16;  // 8-column blocks per warp (two warp groups over the TON columns)
   extern __shared__ __align__(16) double gsm[];
   double (*sA)[TO * TSTR] = reinterpret_cast<double (*)[TO * TSTR]>(gsm);
-  double (*sB)[TO * TSTR] = reinterpret_cast<double (*)[TO * TSTR]>(gsm + 2 * TO * TSTR);
-  const double** cols = reinterpret_cast<const double**>(gsm + 4 * TO * TSTR);
+  double (*sB)[TON * TSTR] = reinterpret_cast<double (*)[TON * TSTR]>(gsm + 2 * TO * TSTR);
+  const double** cols = reinterpret_cast<const double**>(gsm + 2 * TO * TSTR + 2 * TON * TSTR);
   build_cols(P, K, cols);
   __syncthreads();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -161,19 +165,19 @@ __global__ void __launch_bounds__(GT) tgemm_tn_kernel(int64_t M, int64_t rows_pe
   const int64_t chunk = blockIdx.x / (ntk * ntn);
   const int kt = tile / ntn, nt = tile % ntn;
   const int64_t rb = chunk * rows_per_chunk, re = (M < rb + rows_per_chunk) ? M : rb + rows_per_chunk;
-  const int m0 = kt * TO, n0 = nt * TO;
-  const int abase = (warp & 3) * 2, bbase = (warp >> 2) * 4;
-  double acc[2][4][2];
+  const int m0 = kt * TO, n0 = nt * TON;
+  const int abase = (warp & 3) * 2, bbase = (warp >> 2) * BW;
+  double acc[2][BW][2];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int b = 0; b < BW; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
   const int64_t nst = re > rb ? (re - rb + TR - 1) / TR : 0;
   auto load = [&](int64_t s, int buf) {
     const int64_t r0 = rb + s * TR;
-    for (int q = tid; q < 2 * TO * (TR / 2); q += GT) {
-      const int which = q / (TO * (TR / 2));
-      const int qq = q % (TO * (TR / 2));
+    for (int q = tid; q < (TO + TON) * (TR / 2); q += GT) {
+      const int which = q >= TO * (TR / 2);
+      const int qq = which ? q - TO * (TR / 2) : q;
       const int cc = qq / (TR / 2), pc = qq % (TR / 2);
       const int64_t r = r0 + 2 * pc;
       const int64_t valid = re - r;
@@ -205,30 +209,30 @@ __global__ void __launch_bounds__(GT) tgemm_tn_kernel(int64_t M, int64_t rows_pe
 #pragma unroll
     for (int ks = 0; ks < TR / 4; ++ks) {
       const int k = ks * 4 + tq;
-      double fa[2], fb[4];
+      double fa[2], fb[BW];
 #pragma unroll
       for (int a = 0; a < 2; ++a) fa[a] = A[((abase + a) * 8 + g) * TSTR + k];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) fb[b] = B[((bbase + b) * 8 + g) * TSTR + k];
+      for (int b = 0; b < BW; ++b) fb[b] = B[((bbase + b) * 8 + g) * TSTR + k];
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) dmma884(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
+        for (int b = 0; b < BW; ++b) dmma884(acc[a][b][0], acc[a][b][1], fa[a], fb[b]);
     }
     __syncthreads();
   }
-  double* dst = partial + (size_t)blockIdx.x * TO * TO;
+  double* dst = partial + (size_t)blockIdx.x * TO * TON;
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
-      *reinterpret_cast<double2*>(dst + ((abase + a) * 8 + g) * TO + (bbase + b) * 8 + 2 * tq) =
+    for (int b = 0; b < BW; ++b)
+      *reinterpret_cast<double2*>(dst + ((abase + a) * 8 + g) * TON + (bbase + b) * 8 + 2 * tq) =
           make_double2(acc[a][b][0], acc[a][b][1]);
 }
 
 // X[m + n*ldx] = d[m] * sum_chunks partial(chunk, m, n), chunks in order
 __global__ void tgemm_tn_reduce_kernel(const double* __restrict__ partial, int nchunks, int K, int N, int ntk,
-                                       int ntn, int sym, const double* __restrict__ d, double* __restrict__ X,
+                                       int ntn, int ton, int sym, const double* __restrict__ d, double* __restrict__ X,
                                        int ldx) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (int64_t)K * N) return;
@@ -239,10 +243,10 @@ __global__ void tgemm_tn_reduce_kernel(const double* __restrict__ partial, int n
     m = n;
     n = t;
   }
-  const int kt = m / TO, nt = n / TO;
-  const size_t off = (size_t)(m % TO) * TO + (n % TO);
+  const int kt = m / TO, nt = n / ton;  // sym tiles are square (ton == TO)
+  const size_t off = (size_t)(m % TO) * ton + (n % ton);
   double s = 0.0;
-  for (int c = 0; c < nchunks; ++c) s += partial[((size_t)c * ntk * ntn + kt * ntn + nt) * TO * TO + off];
+  for (int c = 0; c < nchunks; ++c) s += partial[((size_t)c * ntk * ntn + kt * ntn + nt) * TO * ton + off];
   const int no = (int)(idx / K);
   X[(int64_t)no * ldx + mo] = d != nullptr ? d[mo] * s : s;
 }
@@ -325,29 +329,43 @@ void launch_tgemm_nn(int64_t M, const GemmSeg* segs, int nseg, const double* W, 
   }
 }
 
-size_t tgemm_tn_partial_doubles(int64_t M, int K, int N, int num_sms) {
-  const int ntk = (K + TO - 1) / TO, ntn = (N + TO - 1) / TO;
+static int tn_width(int N, bool sym) { return (!sym && N > 64 && N <= 112) ? 112 : TO; }
+
+static size_t tn_partial(int64_t M, int K, int N, int ton, int num_sms) {
+  const int ntk = (K + TO - 1) / TO, ntn = (N + ton - 1) / ton;
   const int64_t want = std::max<int64_t>(1, (int64_t)TN_CTAS_PER_SM * num_sms / (ntk * ntn));
   const int64_t nchunks = std::min<int64_t>(want, (M + TR - 1) / TR);
-  return (size_t)std::max<int64_t>(nchunks, 1) * ntk * ntn * TO * TO;
+  return (size_t)std::max<int64_t>(nchunks, 1) * ntk * ntn * TO * ton;
+}
+
+size_t tgemm_tn_partial_doubles(int64_t M, int K, int N, int num_sms) {
+  // sized for either tile width (the launch picks it from N and whether the product is a Gram)
+  return std::max(tn_partial(M, K, N, TO, num_sms), tn_partial(M, K, N, tn_width(N, false), num_sms));
 }
 
 void launch_tgemm_tn(int64_t M, const GemmSeg* segs, int nseg, const double* Y, int64_t ldy, int N,
                      const double* d, double* X, int ldx, double* partial, int num_sms, cudaStream_t st) {
   const ColTable t = make_table(segs, nseg);
   const int K = t.c0[nseg];
-  const int ntk = (K + TO - 1) / TO, ntn = (N + TO - 1) / TO;
+  const int sym = (nseg == 1 && segs[0].ptr == Y && segs[0].ld == ldy && K == N) ? 1 : 0;
+  const int ton = tn_width(N, sym);
+  const int ntk = (K + TO - 1) / TO, ntn = (N + ton - 1) / ton;
   const int64_t want = std::max<int64_t>(1, (int64_t)TN_CTAS_PER_SM * num_sms / (ntk * ntn));
   int64_t nchunks = std::max<int64_t>(1, std::min<int64_t>(want, (M + TR - 1) / TR));
   const int64_t rows = ((M + nchunks - 1) / nchunks + TR - 1) / TR * TR;
   nchunks = (M + rows - 1) / rows;
-  const size_t sm = sizeof(double) * 4 * TO * TSTR + 8 * (size_t)K + 16;
-  cudaFuncSetAttribute(tgemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  const int sym = (nseg == 1 && segs[0].ptr == Y && segs[0].ld == ldy && K == N) ? 1 : 0;
-  tgemm_tn_kernel<<<(unsigned)(nchunks * ntk * ntn), GT, sm, st>>>(M, rows, t, K, Y, ldy, N, ntk, ntn, sym, partial);
+  const size_t sm = sizeof(double) * 2 * (TO + ton) * TSTR + 8 * (size_t)K + 16;
+  const unsigned grid = (unsigned)(nchunks * ntk * ntn);
+  if (ton == 112) {
+    cudaFuncSetAttribute(tgemm_tn_kernel<112>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    tgemm_tn_kernel<112><<<grid, GT, sm, st>>>(M, rows, t, K, Y, ldy, N, ntk, ntn, sym, partial);
+  } else {
+    cudaFuncSetAttribute(tgemm_tn_kernel<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    tgemm_tn_kernel<TO><<<grid, GT, sm, st>>>(M, rows, t, K, Y, ldy, N, ntk, ntn, sym, partial);
+  }
   const int64_t tot = (int64_t)K * N;
-  tgemm_tn_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(partial, (int)nchunks, K, N, ntk, ntn, sym, d,
-                                                                        X, ldx);
+  tgemm_tn_reduce_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(partial, (int)nchunks, K, N, ntk, ntn, ton,
+                                                                        sym, d, X, ldx);
 }
 
 int64_t colmax_rows_chunks(int64_t M) { return std::max<int64_t>(1, std::min<int64_t>(256, (M + 4095) / 4096)); }
