@@ -27,6 +27,18 @@ __global__ void rand_vt_kernel(const double* __restrict__ Bt, int n, int l, cons
   Vt[(size_t)j * ldvt + k] = S[k] != 0.0 ? sgn[k] * v / S[k] : 0.0;
 }
 
+// G (w x w, ld w) = Y^T Y of a tall M x w panel on the Gram pass (upper 32 x 32 tiles, fixed-order reduce);
+// unlike psvd_gram it leaves the context's panel scaling (dvec) alone
+int narrow_gram(psvd_ctx* c, int64_t M, const double* Y, int64_t ldy, int w, double* G, cudaStream_t st) {
+  Pass ps;
+  int rc = plan_pass(c, ps, M, {Seg{Y, ldy, w, 0}}, 0, 0, 0, nullptr, 0, true, false, false);
+  if (rc) return rc;
+  if ((rc = run_pass(c, ps, st))) return rc;
+  launch_extract_sym((const double*)c->tiles.ptr, ps.NB, 0, w, nullptr, G, st);
+  c->launches++;
+  return cuda_check(c, "narrow gram");
+}
+
 // sign rule over ranks: local per-chunk pairs -> one pair per column -> allgather -> sign
 int exchange_sign(psvd_ctx* c, const double* local_pairs, int nchunks, int K, double* sgn, cudaStream_t st) {
   if (!ex_active(c)) {
@@ -141,14 +153,20 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
     const GemmSeg gy{Y, ldy, l}, gy2{Y2, ldy, l};
     for (int it = 0; it <= q; ++it) {
       launch_tgemm_nn(M, gp.data(), (int)gp.size(), W0, n, l, Y, ldy, st);           // Y = P W0
-      launch_tgemm_tn(M, &gy, 1, Y, ldy, l, nullptr, G1, l, pbuf, c->num_sms, st);    // G1 = Y^T Y
-      c->launches += 3;
+      c->launches++;
+      // G1 = Y^T Y on the Gram pass (upper 32 x 32 tiles, TMA-fed, unread sub-blocks trimmed): about half
+      // the DMMA work of the 64 x 64 tiles of the general TN product
+      if ((rc = narrow_gram(c, M, Y, ldy, l, G1, st))) return rc;
       if ((rc = ex_allreduce(c, G1, (int64_t)l * l, st))) return rc;
       if ((rc = svqb(c, G1, l, T1, sscr, st))) return rc;
       launch_tgemm_nn(M, &gy, 1, T1, l, l, Y2, ldy, st);                              // Y1 = Y T1
-      launch_tgemm_tn(M, &gy2, 1, Y2, ldy, l, nullptr, G2, l, pbuf, c->num_sms, st);  // G2 = Y1^T Y1
+      c->launches++;
+      if ((rc = narrow_gram(c, M, Y2, ldy, l, G2, st))) return rc;  // G2 = Y1^T Y1
+      // (the Gram pass may have grown the shared partial-tile workspace: take its current address)
+      if ((rc = ensure(c, c->partial, sizeof(double) * part))) return rc;
+      pbuf = (double*)c->partial.ptr;
       launch_tgemm_tn(M, gp.data(), (int)gp.size(), Y2, ldy, l, d, X, n, pbuf, c->num_sms, st);  // X = D P^T Y1
-      c->launches += 5;
+      c->launches += 2;
       if ((rc = ex_allreduce(c, G2, (int64_t)l * l, st)) || (rc = ex_allreduce(c, X, (int64_t)n * l, st))) return rc;
       launch_chol_inv(G2, l, T2, st);
       launch_small_gemm(X, n, 0, T2, l, (it < q) ? Z : Bt, n, n, l, l, nullptr, st);
