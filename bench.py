@@ -70,6 +70,7 @@ def args_():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-rand", action="store_true")
     ap.add_argument("--no-weak", action="store_true")
+    ap.add_argument("--weak-rows", type=int, default=4194304, help="rows per GPU of the weak-scaling leg (config 4)")
     return ap.parse_args()
 
 
@@ -555,7 +556,7 @@ def weak_scaling(a, p, dev, world, rank, ctxr):
     import math
     import torch
     import torch.distributed as dist
-    M, S, B, KK = 4194304, 4096, 512, 100
+    M, S, B, KK = a.weak_rows, 4096, 512, 100
     sig = torch.arange(1, 201, dtype=torch.float64, device=dev) ** -1.5
     gen = torch.Generator(device=dev).manual_seed(2 + 7919 * rank)  # this rank's rows of U_f
     Ut = torch.randn((200, M), generator=gen, dtype=torch.float64, device=dev).div_(math.sqrt(M * world))
@@ -596,7 +597,7 @@ def weak_scaling(a, p, dev, world, rank, ctxr):
     per_upd_bytes = [8.0 * M * (4 * (B + (0 if u == 0 else KK)) + KK) for u in range(S // B)]
     per_upd_flops = [4 * 2.0 * M * (B + (0 if u == 0 else KK)) * l + 8.0 * M * l * l + 2.0 * M * l * KK
                      for u in range(S // B)]
-    return {"config": "config4: 4,194,304 rows per GPU x 4096 snapshots, B=512, K=100, p=10, q=1",
+    return {"config": f"config4: {M:,} rows per GPU x 4096 snapshots, B=512, K=100, p=10, q=1",
             "n_gpus": world, "rows_total": M * world, "ms_per_stream": round(ms, 2),
             "value": round(8.0 * M * world * S / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
             "per_gpu_gbs": round(8.0 * M * S / (ms * 1e-3) / 1e9, 2),
