@@ -23,8 +23,9 @@ __device__ __forceinline__ void mbar_expect(unsigned long long* b, unsigned byte
 }
 
 template <int DIM>
-__global__ void __launch_bounds__(64) tma_stream(const __grid_constant__ CUtensorMap map, long long M, int C, int R,
-                                                 int ns, long long rows_per_cta) {
+__global__ void __launch_bounds__(64) tma_stream(const __grid_constant__ CUtensorMap map,
+                                                 const __grid_constant__ CUtensorMap pmap, long long M, int C, int R,
+                                                 int ns, long long rows_per_cta, int pf_rows) {
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* base = sm + ((1024 - (saddr(sm) & 1023)) & 1023);
   const unsigned stage = (unsigned)R * C * 8;
@@ -43,6 +44,14 @@ __global__ void __launch_bounds__(64) tma_stream(const __grid_constant__ CUtenso
       if (s >= ns) mbar_wait(&empty[b], (unsigned)(((s / ns) - 1) & 1));
       mbar_expect(&full[b], stage);
       const int row = (int)(r0 + s * R);
+      // optional L2 prefetch of pf_rows-row blocks (3-D box) one block ahead: longer contiguous DRAM runs per column
+      if (pf_rows > 0 && ((s * R) % pf_rows) == 0) {
+        const long long prow = row + pf_rows;
+        if (prow < r1)
+          asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(&pmap), "r"(0),
+                       "r"((int)(prow / 16)), "r"(0)
+                       : "memory");
+      }
       if (DIM == 2) {
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
@@ -69,8 +78,23 @@ int main() {
   const long long M = 1 << 20;
   const int C = 200;
   double* A; cudaMalloc(&A, (size_t)M * C * 8); cudaMemset(A, 0, (size_t)M * C * 8);
+  CUtensorMap pmaps[3];
+  const int pfs[3] = {0, 128, 256};
+  for (int i = 1; i < 3; ++i) {
+    cuuint64_t dims[3] = {16, (cuuint64_t)(M / 16), (cuuint64_t)C};
+    cuuint64_t str[2] = {128, (cuuint64_t)M * 8};
+    cuuint32_t box[3] = {16, (cuuint32_t)(pfs[i] / 16), (cuuint32_t)C};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult e = cuTensorMapEncodeTiled(&pmaps[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, A, dims, str, box, es,
+                                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (e != CUDA_SUCCESS) printf("pmap encode failed %d\n", (int)e);
+  }
+  pmaps[0] = pmaps[1];
+  for (int pfi = 0; pfi < 3; ++pfi)
   for (int dim : {2, 3}) {
     for (int R : {16, 32, 64}) {
+      if (pfi > 0 && !(dim == 2 || R == 32)) continue;
       if (dim == 2 && R != 16) continue;
       CUtensorMap map;
       CUresult e;
@@ -100,15 +124,16 @@ int main() {
         auto kern = dim == 2 ? tma_stream<2> : tma_stream<3>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         const long long rows = ((M + sms - 1) / sms + R - 1) / R * R;
-        kern<<<sms, 64, smem>>>(map, M, C, R, ns, rows);
+        const int pf = pfs[pfi];
+        kern<<<sms, 64, smem>>>(map, pmaps[pfi], M, C, R, ns, rows, pf);
         cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
         cudaEventRecord(e0);
-        for (int i = 0; i < 5; ++i) kern<<<sms, 64, smem>>>(map, M, C, R, ns, rows);
+        for (int i = 0; i < 5; ++i) kern<<<sms, 64, smem>>>(map, pmaps[pfi], M, C, R, ns, rows, pf);
         cudaEventRecord(e1); cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1);
         cudaError_t err = cudaGetLastError();
-        printf("{\"test\": \"tma_stream\", \"dim\": %d, \"rows_per_stage\": %d, \"cols\": %d, \"stages\": %d, \"gbs\": %.1f, \"err\": \"%s\"}\n",
-               dim, R, C, ns, 5.0 * M * C * 8 / (ms * 1e-3) / 1e9, cudaGetErrorString(err));
+        printf("{\"test\": \"tma_stream\", \"dim\": %d, \"rows_per_stage\": %d, \"cols\": %d, \"stages\": %d, \"pf_rows\": %d, \"gbs\": %.1f, \"err\": \"%s\"}\n",
+               dim, R, C, ns, pf, 5.0 * M * C * 8 / (ms * 1e-3) / 1e9, cudaGetErrorString(err));
       }
     }
   }
