@@ -8,6 +8,14 @@ q = 0 and q = 1 (p = 10, seed 0, the host Philox Omega of linalg.py:141-142).
 Config 3 (weather field, 1,038,240 x 1024, B = 256, K = 50, p = 10, q = 1) at
 its full row count on the wide randomized route.
 
+Configs 4 and 5 do not fit the host oracle (~50 GB for config 5), so at
+their full per-GPU size they get device self-checks (device-generated factor data):
+the exact identity of the last update, C^T U = V S with V orthonormal, for
+C = [ff U_prev diag(sigma_prev) | A_last] (any rank-K SVD of C, deterministic or
+randomized, satisfies it), checked by cuBLAS; and for config 5 the pipelined Gram
+route against the accurate route (Householder-R basis + Jacobi, psvd_accurate.cu)
+on the same stream.
+
 Bars (north_star): sigma relative error <= 1e-10 at every step, per-mode
 sine-based angles <= 1e-8 for well-separated modes, the reference's column
 signs.  The oracle run on this box is itself pinned at full size by
@@ -18,6 +26,7 @@ The serial oracle may use every host core (SURVEY F4 is about simulated ranks),
 so these tests lift the session's one-thread BLAS pin.
 """
 
+import math
 import os
 import time
 from concurrent.futures import ThreadPoolExecutor
@@ -165,3 +174,110 @@ def test_config3_randomized_fullsize(golden):
     fp = _fp(golden)
     assert oracle.sigma_rel_err(ref_s, fp["c3_q1_sigma"]) <= SIG_TOL
     assert oracle.sigma_rel_err(sigma, fp["c3_q1_sigma"]) <= SIG_TOL
+
+
+def _factor_batches(M, B, sigma, noise, seed, count):
+    """`count` device batches (M x B column-major views) of U diag(sigma) V^T + noise with
+    Gaussian factors (the config 4 / 5 distributions of SURVEY 8(d), device-generated)."""
+    import torch
+    dev = torch.device("cuda", 0)
+    sig = torch.as_tensor(sigma, dtype=torch.float64, device=dev)
+    gen = torch.Generator(device=dev).manual_seed(seed)
+    ut = torch.randn((sig.numel(), M), generator=gen, dtype=torch.float64, device=dev).div_(math.sqrt(M))
+    out = []
+    for _ in range(count):
+        vb = torch.randn((B, sig.numel()), generator=gen, dtype=torch.float64, device=dev)
+        vb.mul_(sig / math.sqrt(B * count))
+        at = vb @ ut                                   # B x M row-major = M x B column-major
+        at.add_(torch.randn(at.shape, generator=gen, dtype=torch.float64, device=dev), alpha=noise)
+        out.append(at.T)
+    del ut
+    torch.cuda.empty_cache()
+    return out
+
+
+def _last_update_identity(prev, new, a_last, ff):
+    """C^T U = V S for C = [ff U_prev diag(s_prev) | A_last]: returns (max |W^T W - I| for
+    W = C^T U diag(1/s), max |U^T U - I|), both computed on the device by cuBLAS."""
+    import torch
+    U, s = new.modes, new.singular_values
+    z = torch.cat([(ff * prev.singular_values)[:, None] * (prev.modes.T @ U), a_last.T @ U])
+    w = z / s[None, :]
+    eye = torch.eye(U.shape[1], dtype=torch.float64, device=U.device)
+    return float((w.T @ w - eye).abs().max()), float((U.T @ U - eye).abs().max())
+
+
+def _accurate_stream(batches, k, ff):
+    """The stream on the accurate route only: psvd_stream_update_accurate per batch."""
+    import torch
+    from paper_2108_08845_b200 import _native as nat
+    dev = batches[0].device
+    ctx = nat.context(dev)
+    U, sig = None, None
+    for a in batches:
+        A = nat.as_device_colmajor(a, dev, "a")
+        out = nat.DevMat.empty(A.rows, k, dev)
+        s = torch.empty(k, dtype=torch.float64, device=dev)
+        nat.call("psvd_stream_update_accurate", ctx, A.rows, nat._vp(U.data_ptr() if U is not None else 0),
+                 U.ld if U is not None else 0, nat.ptr(sig if U is not None else None), float(ff),
+                 0 if U is None else U.cols, nat._vp(A.data_ptr()), A.ld, A.cols, k, 1, nat._vp(out.data_ptr()),
+                 out.ld, nat.ptr(s), nat.stream_ptr(dev))
+        assert not (nat.read_status(ctx, reset=True, device=dev) & nat.ST_NONFINITE)
+        U, sig = out, s
+    return U.t, sig
+
+
+def test_config5_fullsize_self_check():
+    """Config 5 at its full 8,388,608 rows (B = 128, K = 64, ff = 1, deterministic): the last
+    update's identity, and the Gram route (the bench's path) against the accurate route."""
+    import torch
+    p = _pkg()
+    M, B, K = 8388608, 128, 64
+    sigma = 1.0 / (1.0 + 0.01 * np.arange(512))
+    batches = _factor_batches(M, B, sigma, 1e-6, seed=3, count=4)
+    cfg = p.StreamConfig(k_modes=K, forget_factor=1.0, batch_columns=B)
+    prev, _ = p.stream_all(batches[:-1], cfg)
+    new = p.stream_incorporate(prev, batches[-1], cfg)
+    assert p.streaming.ACCURATE_UPDATES == 0           # kappa ~ 1.6: the gate stays off
+    werr, oerr = _last_update_identity(prev, new, batches[-1], 1.0)
+    assert werr <= 1e-10 and oerr <= 1e-12, (werr, oerr)
+    ua, sa = _accurate_stream(batches, K, 1.0)
+    s, ref = new.singular_values.cpu().numpy(), sa.cpu().numpy()
+    assert oracle.sigma_rel_err(s, ref) <= SIG_TOL
+    # sine-based angles on the device: the whole K-subspace (gap sigma_K / sigma_K+1), and
+    # per mode for the separated ones; the routes apply the same sign rule
+    um = new.modes
+    res = ua - um @ (um.T @ ua)                        # M x K residual, entries ~ the sines
+    sub = math.sqrt(max(0.0, float(torch.linalg.eigvalsh(res.T @ res).max())))
+    assert sub <= ANG_TOL, sub
+    c = (um * ua).sum(0)
+    ang = torch.linalg.vector_norm(ua - um * c[None, :], dim=0).cpu().numpy()
+    sep = _well_separated(ref)
+    assert np.max(ang[sep]) <= ANG_TOL, ang
+    assert bool((c > 0).all())
+    print(f"config5 full size: identity {werr:.1e}, orthonormality {oerr:.1e}, Gram vs accurate route sigma "
+          f"{oracle.sigma_rel_err(s, ref):.1e}, subspace {sub:.1e}, modes {np.max(ang[sep]):.1e} "
+          f"({int(sep.sum())}/{K} separated)")
+    del batches
+    torch.cuda.empty_cache()
+
+
+def test_config4_fullsize_self_check():
+    """Config 4 at its full 4,194,304 rows per GPU (B = 512, K = 100, p = 10, q = 1: the wide
+    randomized route) -- the last update's identity and orthonormality."""
+    import torch
+    p = _pkg()
+    M, B, K = 4194304, 512, 100
+    sigma = np.arange(1, 201, dtype=np.float64) ** -1.5
+    batches = _factor_batches(M, B, sigma, 1e-4, seed=2, count=3)
+    sk = p.RandomSketchConfig(target_rank=K, oversampling=10, power_iterations=1, seed=0)
+    cfg = p.StreamConfig(k_modes=K, forget_factor=0.95, batch_columns=B, sketch=sk)
+    prev, _ = p.stream_all(batches[:-1], cfg)
+    new = p.stream_incorporate(prev, batches[-1], cfg)
+    werr, oerr = _last_update_identity(prev, new, batches[-1], 0.95)
+    s = new.singular_values.cpu().numpy()
+    assert np.all(np.diff(s) <= 0) and s[-1] > 0
+    assert werr <= 1e-9 and oerr <= 1e-12, (werr, oerr)
+    print(f"config4 full size: identity {werr:.1e}, orthonormality {oerr:.1e}, sigma_1/sigma_K {s[0] / s[-1]:.1e}")
+    del batches
+    torch.cuda.empty_cache()
