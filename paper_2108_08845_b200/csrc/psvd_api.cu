@@ -579,6 +579,7 @@ int psvd_create(int device, psvd_ctx** out) {
     cudaEventCreateWithFlags(&c->ev_ldlt_fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_ldlt_join, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_eig_start, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_fdone, cudaEventDisableTiming);
     for (int i = 0; i < 2; ++i) {
       cudaEventCreateWithFlags(&c->ev_aa[i], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&c->ev_asm[i], cudaEventDisableTiming);
@@ -611,6 +612,7 @@ int psvd_destroy(psvd_ctx* c) {
   if (c->ev_ldlt_fork) cudaEventDestroy(c->ev_ldlt_fork);
   if (c->ev_ldlt_join) cudaEventDestroy(c->ev_ldlt_join);
   if (c->ev_eig_start) cudaEventDestroy(c->ev_eig_start);
+  if (c->ev_fdone) cudaEventDestroy(c->ev_fdone);
   for (int i = 0; i < 2; ++i) {
     if (c->ev_aa[i]) cudaEventDestroy(c->ev_aa[i]);
     if (c->ev_asm[i]) cudaEventDestroy(c->ev_asm[i]);

@@ -62,6 +62,7 @@ struct psvd_ctx {
   cudaStream_t s_hi = nullptr, s_lo = nullptr;  // pipelined stream_run: critical chain / look-ahead Grams
   cudaStream_t s_aux = nullptr;                  // concurrent LDL^T of the split core solve
   cudaEvent_t ev_ldlt_fork = nullptr, ev_ldlt_join = nullptr, ev_eig_start = nullptr;
+  cudaEvent_t ev_fdone = nullptr;  // psvd_stream_run: the fused pass kernel of an update has left the SMs
   cudaEvent_t ev_aa[2] = {nullptr, nullptr}, ev_asm[2] = {nullptr, nullptr}, ev_fork = nullptr, ev_join = nullptr;
 };
 

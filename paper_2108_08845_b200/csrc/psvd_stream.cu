@@ -13,6 +13,30 @@
 using namespace psvd;
 using namespace psvd_internal;
 
+namespace {
+
+// Deferred normalization (psvd_stream_run): the previous update's U is left as the fused pass wrote
+// it, U_raw, and U = U_raw diag(scale) T (T the drift rescue's transform when its gate fired, else
+// I).  The panel product [U | A] W then equals [U_raw | A] W' with the top K rows of W replaced by
+// diag(scale) T W_top: one CTA, fixed summation order.
+__global__ void fold_w_kernel(double* W, int64_t ldw, int K, const double* scale, const double* T, const int* gate) {
+  extern __shared__ double wt[];  // K x K, col-major
+  const bool rot = gate != nullptr && *gate != 0;
+  for (int i = threadIdx.x; i < K * K; i += blockDim.x) wt[i] = W[(int64_t)(i / K) * ldw + i % K];
+  __syncthreads();
+  for (int i = threadIdx.x; i < K * K; i += blockDim.x) {
+    const int r = i % K, col = i / K;
+    double v = wt[i];
+    if (rot) {
+      v = 0.0;
+      for (int l = 0; l < K; ++l) v += T[(int64_t)l * K + r] * wt[col * K + l];
+    }
+    W[(int64_t)col * ldw + r] = scale[r] * v;
+  }
+}
+
+}  // namespace
+
 extern "C" {
 
 // Whole stream with look-ahead: the A^T A Gram of batch b+1 runs on a
@@ -75,13 +99,25 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
   // the core solve of batch b occupies.  PSVD_LA_SHARED=1 restores the time-shared schedule (4 row
   // sub-launches on num_sms - 2 CTAs).
   static const bool la_serial = getenv("PSVD_LA_SHARED") == nullptr;
+  // Between an update's fused pass and the next look-ahead Gram only one-CTA kernels remain when the
+  // column normalization (and a fired drift rescue) of U is folded into the next update's W instead of
+  // rewriting U (fold_w_kernel): the Gram then starts as soon as the fused pass leaves the SMs and the
+  // one-CTA tail runs on the SM it leaves free.  PSVD_NO_DEFER_NORM=1: normalize U in place.
+  static const bool defer_env = getenv("PSVD_NO_DEFER_NORM") == nullptr;
+  const bool defer = defer_env && la_serial && K <= DRIFT_SMEM_KMAX;
   const int nsub = la_serial ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(4, M / 65536));
   const int la_ctas = la_serial ? c->num_sms - 1 : c->num_sms - 2;
   auto aa_pass = [&](int j) -> int {
     if (j >= 2) cudaStreamWaitEvent(lo, c->ev_asm[j & 1], 0);  // tiles2[j&1] consumed by batch j-2's assembly
     // start A^T A of batch j with the core solve of batch j-1: it then overlaps that one-SM
-    // solve (the longer of the two) instead of competing with the recompose pass for SMs
-    if (j >= 1) cudaStreamWaitEvent(lo, c->ev_eig_start, 0);
+    // solve (the longer of the two) instead of competing with the recompose pass for SMs.  With the
+    // deferred normalization it only waits for the fused pass of batch j-2 to leave the SMs: the
+    // one-CTA tail of that update (extract, Rayleigh refinement, drift check) and the assembly of
+    // batch j-1 then run on the SM the Gram leaves free
+    if (j >= 2 && defer)
+      cudaStreamWaitEvent(lo, c->ev_fdone, 0);
+    else if (j >= 1)
+      cudaStreamWaitEvent(lo, c->ev_eig_start, 0);
     if (batch_ready && batch_ready[j]) cudaStreamWaitEvent(lo, (cudaEvent_t)batch_ready[j], 0);
     const int64_t rows_sub = (M + nsub - 1) / nsub / 32 * 32 + 32;
     Pass first;
@@ -135,6 +171,9 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
   int64_t ldprev = Kc > 0 ? ldu : 0;
   const double* sprev = Kc > 0 ? sigma_in : nullptr;
   int cur = 0;
+  bool prev_raw = false;  // Uprev = U_raw of the previous update (scale and T in c->tbuf)
+  double* const tb_T = (double*)c->tbuf.ptr;
+  double* const tb_scale = tb_T + (size_t)K * K;
   if (Kc > 0) {  // U^T [U | A_0] for the initial state
     if (batch_ready && batch_ready[0]) cudaStreamWaitEvent(hi, (cudaEvent_t)batch_ready[0], 0);
     Pass pu;
@@ -174,6 +213,11 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
     mark("hi:eig_end", b, hi);
     double* Uout = bufs[cur];
     const bool resc = rescue && kc > 0;
+    if (prev_raw) {
+      fold_w_kernel<<<1, 256, sizeof(double) * K * K, hi>>>(W, kc + B[b], K, tb_scale, tb_T,
+                                                            prev_resc ? c->d_gate : nullptr);
+      c->launches++;
+    }
     if (b + 1 < nb) {
       // fused: U_b = [U_{b-1} | A_b] W, with U_b^T U_b and U_b^T A_{b+1} from the same pass
       std::vector<Seg> segs = panel(Uprev, ldprev, kc, A[b], lda[b], B[b]);
@@ -188,6 +232,7 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
       pf.p.Yout = Uout;
       pf.p.ldy = ldo;
       if ((rc = run_pass(c, pf, hi))) return rc;
+      cudaEventRecord(c->ev_fdone, hi);
       if (getenv("PSVD_DUMP_FUSED")) {  // diagnostics: tiles + Y of the fused pass
         cudaStreamSynchronize(hi);
         std::vector<double> h((size_t)pf.NB * pf.NB * 1024), y((size_t)M * K);
@@ -217,8 +262,21 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
       if ((rc = psvd_recompose(c, M, Uprev, ldprev, kc, A[b], lda[b], B[b], W, K, Uout, ldo, UtU, hi))) return rc;
       if ((rc = ex_allreduce(c, UtU, (int64_t)K * K, hi))) return rc;
     }
-    if ((rc = refine_normalize(c, M, Uout, ldo, K, UtU, sig_b, hi))) return rc;
-    if (resc && (rc = psvd_drift_rescue(c, M, Uout, ldo, K, UtU, sig_b, c->drift_tol, hi))) return rc;
+    if (defer && b + 1 < nb) {
+      // Rayleigh refinement and the drift check without touching U: both fold into the next W
+      launch_normalize_gram(UtU, K, sig_b, tb_scale, c->d_status, hi);
+      c->launches++;
+      if (resc) {
+        launch_drift_check(UtU, K, c->drift_tol, sig_b, tb_T, c->d_gate, c->d_status, hi);
+        c->launches++;
+      }
+      if ((rc = cuda_check(c, "deferred refine"))) return rc;
+      prev_raw = true;
+    } else {
+      if ((rc = refine_normalize(c, M, Uout, ldo, K, UtU, sig_b, hi))) return rc;
+      if (resc && (rc = psvd_drift_rescue(c, M, Uout, ldo, K, UtU, sig_b, c->drift_tol, hi))) return rc;
+      prev_raw = false;
+    }
     prev_resc = resc;
     mark("hi:recompose_end", b, hi);
     Uprev = Uout;
