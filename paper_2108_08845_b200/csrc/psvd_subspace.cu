@@ -46,7 +46,8 @@ __device__ void gq_product(const double* __restrict__ G, int n, const double* Qs
     double acc[CB][2][2];
 #pragma unroll
     for (int c = 0; c < CB; ++c) acc[c][0][0] = acc[c][0][1] = acc[c][1][0] = acc[c][1][1] = 0.0;
-    for (int k0 = 0; k0 < kend; k0 += 8) {
+#pragma unroll 4
+    for (int k0 = 0; k0 < kend; k0 += 8) {  // unrolled: several k steps' loads of G (L2) in flight
       const int ka = k0 + tq, kb = k0 + 4 + tq;
       const double a0 = (rv && ka < n) ? __ldg(G + (size_t)ka * n + row) : 0.0;
       const double a1 = (rv && kb < n) ? __ldg(G + (size_t)kb * n + row) : 0.0;
@@ -64,12 +65,23 @@ __device__ void gq_product(const double* __restrict__ G, int n, const double* Qs
   }
 }
 
+// Rows per lane of the fixed-trip loops below (n <= EIG_FAST_NMAX): every load of a column segment
+// is issued before the first use, instead of one shared-memory round trip per loop iteration
+constexpr int HR = (EIG_FAST_NMAX + 31) / 32;
+
 // Householder reflector of column j of Y (rows j .. n-1), by one warp: v = Y[j+1:, j] scaled in
 // place (v_j = 1 implied), tau into *tau_out; Y[j, j] keeps alpha (R is not needed).
 __device__ __forceinline__ void house_reflector(double* v, int j, int n, double* tau_out) {
   const int lane = threadIdx.x & 31;
+  double x[HR];
+#pragma unroll
+  for (int t = 0; t < HR; ++t) {
+    const int i = j + 1 + lane + 32 * t;
+    x[t] = i < n ? v[i] : 0.0;
+  }
   double part = 0.0;
-  for (int i = j + 1 + lane; i < n; i += 32) part = fma(v[i], v[i], part);
+#pragma unroll
+  for (int t = 0; t < HR; ++t) part = fma(x[t], x[t], part);
   const double xn2 = warp_sum(part);
   const double alpha = v[j];
   double tau = 0.0, scl = 0.0;
@@ -78,19 +90,35 @@ __device__ __forceinline__ void house_reflector(double* v, int j, int n, double*
     tau = (beta - alpha) / beta;
     scl = 1.0 / (alpha - beta);
   }
-  for (int i = j + 1 + lane; i < n; i += 32) v[i] *= scl;
+#pragma unroll
+  for (int t = 0; t < HR; ++t) {
+    const int i = j + 1 + lane + 32 * t;
+    if (i < n) v[i] = x[t] * scl;
+  }
   if (lane == 0) *tau_out = tau;
 }
 
 // y <- H_j y = y - tau v (v^T y) on rows j .. n-1, by one warp (v_j = 1 implied)
 __device__ __forceinline__ void house_apply(const double* v, double tau, int j, int n, double* y) {
   const int lane = threadIdx.x & 31;
+  double vv[HR], yy[HR];
+#pragma unroll
+  for (int t = 0; t < HR; ++t) {
+    const int i = j + 1 + lane + 32 * t;
+    vv[t] = i < n ? v[i] : 0.0;
+    yy[t] = i < n ? y[i] : 0.0;
+  }
   double s = 0.0;
-  for (int i = j + 1 + lane; i < n; i += 32) s = fma(v[i], y[i], s);
+#pragma unroll
+  for (int t = 0; t < HR; ++t) s = fma(vv[t], yy[t], s);
   s = (warp_sum(s) + y[j]) * tau;
   __syncwarp();
   if (lane == 0) y[j] -= s;
-  for (int i = j + 1 + lane; i < n; i += 32) y[i] = fma(-s, v[i], y[i]);
+#pragma unroll
+  for (int t = 0; t < HR; ++t) {
+    const int i = j + 1 + lane + 32 * t;
+    if (i < n) y[i] = fma(-s, vv[t], yy[t]);
+  }
   __syncwarp();
 }
 
