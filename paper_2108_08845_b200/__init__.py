@@ -12,7 +12,7 @@ from .datagen import (DEFAULT_MATRIX_CAP, BurgersConfig, burgers_device, burgers
 from .dsvd import (LocalModes, RankContext, gather_modes, parallel_qr, parallel_stream_all,  # noqa: F401
                    parallel_stream_incorporate, parallel_stream_initialize)
 from .errors import (CapacityError, CollectiveTimeout, ConfigError, ConvergenceError,  # noqa: F401
-                     DegenerateModeError, MatrixFormatError)
+                     DegenerateModeError, MatrixFormatError, ProtocolError)
 from .io import (BatchSource, read_batches, read_matrix, read_matrix_header, read_modes_csv,  # noqa: F401
                  read_singular_values_csv, read_submatrix, write_history_csv, write_matrix, write_mode_svg,
                  write_modes_csv, write_singular_values_csv)

@@ -33,6 +33,7 @@ import torch
 import torch.distributed as dist
 
 from . import _native as nat
+from .errors import ProtocolError
 
 
 @dataclass(frozen=True)
@@ -136,15 +137,19 @@ class _Exchange:
             return 1
 
 
-def _row_offset(ctx, rows, dev):
-    """Global index of this rank's first row (prefix sum of the local row counts)."""
+def _row_offset(ctx, rows, dev, cols=-1):
+    """Global index of this rank's first row (prefix sum of the local row counts).  With `cols`,
+    the ranks' column counts travel in the same allgather and must agree (ProtocolError)."""
     if ctx.world_size == 1:
         return 0, rows
-    t = torch.tensor([rows], dtype=torch.int64,
+    t = torch.tensor([rows, cols], dtype=torch.int64,
                      device=dev if dist.get_backend(ctx.group) == "nccl" else "cpu")
     parts = [torch.zeros_like(t) for _ in range(ctx.world_size)]
     dist.all_gather(parts, t, group=ctx.group)
-    counts = [int(x.item()) for x in parts]
+    counts = [int(x[0].item()) for x in parts]
+    widths = sorted({int(x[1].item()) for x in parts})
+    if len(widths) > 1:
+        raise ProtocolError(f"ranks disagree on the local panel width: {widths}")
     return sum(counts[:ctx.rank]), sum(counts)
 
 
@@ -251,7 +256,7 @@ def exchange_stats(device=None):
 
 def _parallel_rand_update(ctx, U, sigma, A, sketch, ff, dev):
     from .linalg import randomized_update
-    off, total = _row_offset(ctx, A.rows, dev)
+    off, total = _row_offset(ctx, A.rows, dev, A.cols)
     if ctx.world_size == 1:
         return randomized_update(U, sigma, A, sketch, ff, dev)
     with exchange_hooks(ctx, dev, off):
@@ -444,10 +449,13 @@ def gather_modes(ctx, local_modes, root=0):
         return m.contiguous()
     dev = m.device
     stage = dist.get_backend(ctx.group) != "nccl"
-    rows = torch.tensor([m.shape[0]], dtype=torch.int64, device="cpu" if stage else dev)
+    rows = torch.tensor([m.shape[0], m.shape[1]], dtype=torch.int64, device="cpu" if stage else dev)
     all_rows = [torch.zeros_like(rows) for _ in range(ctx.world_size)]
     dist.all_gather(all_rows, rows, group=ctx.group)
-    counts = [int(r.item()) for r in all_rows]
+    counts = [int(r[0].item()) for r in all_rows]
+    widths = sorted({int(r[1].item()) for r in all_rows})
+    if len(widths) > 1:
+        raise ProtocolError(f"ranks hold different numbers of modes: {widths}")
     mx = max(counts)
     pad = torch.zeros((mx, m.shape[1]), dtype=m.dtype, device="cpu" if stage else dev)
     pad[: m.shape[0]] = m
@@ -476,7 +484,7 @@ def parallel_qr(ctx, a_local, device=None):
     m, n = A.rows, A.cols
     c = nat.context(dev)
     st = nat.stream_ptr(dev)
-    off, m_total = _row_offset(ctx, m, dev)
+    off, m_total = _row_offset(ctx, m, dev, n)
     if m_total < n:
         raise ValueError(f"parallel_qr needs at least as many rows as columns ({m_total} < {n})")
 

@@ -60,6 +60,13 @@ def _worker(rank, world, port, q):
                    tuple(full.shape)))
         else:
             assert full is None
+        # ranks that disagree on an exchanged shape raise the reference's ProtocolError on every rank
+        from paper_2108_08845_b200.errors import ProtocolError
+        bad = LocalModes(torch.zeros((4, 3 + rank), dtype=torch.float64), torch.ones(3 + rank, dtype=torch.float64))
+        with pytest.raises(ProtocolError):
+            gather_modes(ctx, bad)
+        with pytest.raises(ProtocolError):
+            _row_offset(ctx, 10, "cpu", 5 + rank)
     finally:
         dist.destroy_process_group()
 
