@@ -268,8 +268,10 @@ int plan_tiles_tma(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>
 // Common pass setup.  segs: panel segments; w/W: optional Y = P[:, wlo:wlo+wk] * W.
 int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, int wlo, int wk, int w,
               const double* W, int64_t ldw, bool gram_pp, bool gram_yy, bool gram_py, int py_cols,
-              int pp_rows, Buf* part, Buf* tl, int max_ctas, int py_lo, bool gaps_ok) {
+              int pp_rows, Buf* part, Buf* tl, int max_ctas, int py_lo, bool gaps_ok,
+              const std::vector<std::pair<int, int>>* skip_pp) {
   memset(&ps.p, 0, sizeof(ps.p));
+  ps.fsplit = false;
   ps.part = part ? part : &c->partial;
   ps.tl = tl ? tl : &c->tiles;
   TallParams& p = ps.p;
@@ -356,7 +358,11 @@ int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, in
   std::vector<std::pair<int, int>> tiles;
   if (gram_pp)
     for (int I = 0; I < (pp_rows < 0 ? NBp : std::min(NBp, (pp_rows + 31) / 32)); ++I)
-      for (int J = I; J < NBp; ++J) tiles.push_back({I, J});
+      for (int J = I; J < NBp; ++J) {
+        // tiles another pass computes (the split-ring fused pass takes some off the look-ahead Gram)
+        if (skip_pp && std::find(skip_pp->begin(), skip_pp->end(), std::make_pair(I, J)) != skip_pp->end()) continue;
+        tiles.push_back({I, J});
+      }
   if (gram_py)
     for (int I = py_lo; I < (py_cols < 0 ? NBp : (py_cols + 31) / 32); ++I)
       for (int J = 0; J < NBy; ++J) tiles.push_back({I, NBp + J});
@@ -462,6 +468,30 @@ int run_pass(psvd_ctx* c, Pass& ps, cudaStream_t st) {
     rc = cuda_check(c, "tall reduce");
   }
   return rc;
+}
+
+bool try_fused_split(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& off, int off_nb) {
+  ps.fsplit = false;
+  static const bool disabled = getenv("PSVD_NO_FSPLIT") != nullptr;
+  if (disabled || !ps.tma || c->num_sms < 1) return false;
+  int offs[FS_MAX_OFF][2];
+  int noff = 0;
+  for (const auto& t : off)
+    if (noff < FS_MAX_OFF) offs[noff][0] = t.first, offs[noff][1] = t.second, ++noff;
+  if (fused_split_prepare(ps.p, ps.x, ps.map, ps.NB, offs, noff, ps.fs, ps.maps3, ps.offmap, off_nb) != 0) return false;
+  ps.fsplit = true;
+  return true;
+}
+
+int run_fused_split(psvd_ctx* c, Pass& ps, cudaStream_t st, double* off_tiles) {
+  c->path_count[0]++;
+  launch_fused_split(ps.p, ps.maps3, ps.x, ps.fs, ps.grid, st);
+  c->launches += 1 + (ps.map.nout > 0) + (ps.offmap.nout > 0);
+  int rc = cuda_check(c, "split-ring fused pass");
+  if (rc) return rc;
+  launch_tall_reduce((const double*)ps.part->ptr, ps.map, (double*)ps.tl->ptr, st);
+  if (ps.offmap.nout > 0) launch_tall_reduce((const double*)ps.part->ptr, ps.offmap, off_tiles, st);
+  return cuda_check(c, "split-ring reduce");
 }
 
 __global__ void make_dvec_kernel(const double* __restrict__ sigma, double ff, int Kc, int n, double* d) {

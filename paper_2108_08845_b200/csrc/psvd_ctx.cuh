@@ -4,6 +4,7 @@
 #pragma once
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/psvd.h"
@@ -79,6 +80,10 @@ struct Pass {
   TmaExtra x;
   Buf* part = nullptr;  // partial-tile workspace of the stream this pass runs on
   Buf* tl = nullptr;    // reduced tiles
+  bool fsplit = false;  // split-ring fused pass (fused_split_kernel) instead of the narrow TMA pass
+  FusedSplit fs;
+  TmaMaps maps3;        // its 3-D tensor maps
+  ReduceMap offmap;     // its offloaded Gram tiles (reduced into the look-ahead Gram's tile array)
 };
 
 namespace psvd_internal {
@@ -93,8 +98,13 @@ int check_mat(psvd_ctx* c, const char* name, const double* p, int64_t ld, int64_
 int plan_pass(psvd_ctx* c, Pass& ps, int64_t M, const std::vector<Seg>& segs, int wlo, int wk, int w,
               const double* W, int64_t ldw, bool gram_pp, bool gram_yy, bool gram_py, int py_cols = -1,
               int pp_rows = -1, Buf* part = nullptr, Buf* tl = nullptr, int max_ctas = 0, int py_lo = 0,
-              bool gaps_ok = false);
+              bool gaps_ok = false, const std::vector<std::pair<int, int>>* skip_pp = nullptr);
 int run_pass(psvd_ctx* c, Pass& ps, cudaStream_t st);
+// Split-ring variant of a planned fused pass [U | A_b | A_next] (psvd_tall.cuh: FusedSplit): sets ps.fsplit
+// when it qualifies; off = 32-column block pairs of A_next^T A_next to compute in the pass (off_nb tile
+// columns in the look-ahead Gram's tile array).  run_fused_split launches it and both reductions.
+bool try_fused_split(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& off, int off_nb);
+int run_fused_split(psvd_ctx* c, Pass& ps, cudaStream_t st, double* off_tiles);
 int make_dvec(psvd_ctx* c, const double* sigma, double ff, int Kc, int n, cudaStream_t st);
 std::vector<Seg> panel(const double* U, int64_t ldu, int Kc, const double* A, int64_t lda, int B);
 void launch_stamp(unsigned long long* out, cudaStream_t st);  // device clock into *out (trace marks)

@@ -27,6 +27,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
+#include <vector>
 
 #include "psvd_tall.cuh"
 
@@ -735,6 +736,341 @@ void launch_gram_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x
   gram_tma_kernel<false><<<grid, NTHR, smem, st>>>(p, maps, x);
 }
 
+// ---------------------------------------------------------------- split-ring fused pass
+// The deterministic stream's fused pass over [U | A_b | A_next] (psvd_tall.cuh: FusedSplit).  A
+// 32-row stage of the whole panel does not fit shared memory twice, which left that pass on 16-row
+// stages (128 contiguous bytes per column and request, ~4.5 TB/s).  Here a stage is split by column
+// group: group A = [U | A_b] (read by the Y warps only) and group B = A_next (read by the tile warps
+// only), each group in its own two-slot ring of 3-D boxes {16 rows, 2, columns} (256 contiguous
+// bytes per column).  W lives in the Y warps' registers (FS_NKP k parts per column block, partial
+// sums met in the Y tile in part order, as in pass_tma_kernel), staged once through ring memory.
+// Tile warps: A_next^T Y over up to 8 sub-blocks of 8 columns each, Y^T Y, and offloaded 32 x 32
+// tiles of A_next^T A_next that the look-ahead Gram then skips.
+namespace {
+
+PSVD_DEV bool mbar_test(uint64_t* bar, unsigned parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(saddr(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+}  // namespace
+
+size_t fused_split_smem_bytes(const FusedSplit& fs) {
+  return 1024 + sizeof(double) * 2 * (size_t)(fs.pwA + fs.pwB) * 32 + sizeof(double) * 2 * 8 * (size_t)fs.ncb * 32 +
+         64 * sizeof(uint64_t);
+}
+
+template <int NCB>
+__global__ void __launch_bounds__(NTHR, 1)
+    fused_split_kernel(const __grid_constant__ TallParams p, const __grid_constant__ TmaMaps maps,
+                       const __grid_constant__ TmaExtra x, const __grid_constant__ FusedSplit fs) {
+  constexpr int SR = 32, YC = 8 * NCB;
+  extern __shared__ unsigned char smem_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int64_t row_begin = (int64_t)blockIdx.x * p.rows_per_cta;
+  const int64_t row_end = min(p.M, row_begin + p.rows_per_cta);
+  unsigned char* base = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
+  const size_t szA = (size_t)fs.pwA * SR, szB = (size_t)fs.pwB * SR;  // doubles per slot
+  double* ring = reinterpret_cast<double*>(base);                     // [A0 | B0 | A1 | B1]
+  double* sY = ring + 2 * (szA + szB);                                // [2][YC columns][32 rows], swzr<2>
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sY + 2 * YC * SR);
+  uint64_t *fullA = bars, *emptyA = bars + 2, *fullB = bars + 4, *emptyB = bars + 6, *ydone = bars + 8,
+           *yfree = bars + 10, *chain = bars + 12;  // chain[(yb * 2 + cb) * 3 + link]
+  const int WSP = w_stride(YC);
+  double* sW = ring;  // W staged through slot A0 before the first box lands there
+
+  for (int i = tid; i < fs.n4 * 4 * WSP; i += NTHR) {
+    const int pc = i / WSP, o = i % WSP;  // physical panel column (kp_lo == 0), Y column
+    double v = 0.0;
+    if (o < p.w) {
+      for (int s = 0; s < p.nseg; ++s) {
+        const int c0 = p.seg[s].col0;
+        if (x.wrow0[s] != TMA_NOT_IN_W && pc >= c0 && pc < c0 + p.seg[s].ncols) {
+          const int wr = x.wrow0[s] + (pc - c0);
+          if (wr >= 0 && wr < p.wk) v = p.W[(int64_t)o * p.ldw + wr];
+        }
+      }
+    }
+    sW[i] = v;
+  }
+  for (int i = tid; i < 2 * YC * SR; i += NTHR) sY[i] = 0.0;
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&fullA[b], 1);
+      mbar_init(&fullB[b], 1);
+      mbar_init(&emptyA[b], (unsigned)(NCB * FS_NKP));
+      mbar_init(&emptyB[b], (unsigned)max(fs.npy + fs.noff, 1));
+      mbar_init(&ydone[b], 32u * NCB);
+      mbar_init(&yfree[b], (unsigned)max(32 * fs.npy, 1));
+    }
+    for (int i = 0; i < 2 * 2 * 3; ++i) mbar_init(&chain[i], 32u);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int role = fs.role[warp];
+  double wr[FS_WR];
+  if (role == FS_Y) {
+    const int cb = fs.ycb[warp], j0 = fs.yj0[warp], nj = fs.ynj[warp];
+#pragma unroll
+    for (int j = 0; j < FS_WR; ++j) wr[j] = j < nj ? sW[(size_t)(4 * (j0 + j) + tq) * WSP + cb * 8 + g] : 0.0;
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic accesses of the ring before the boxes
+  __syncthreads();
+  const int64_t nstage = row_end > row_begin ? (row_end - row_begin + SR - 1) / SR : 0;
+
+  if (role == FS_PROD) {
+    if (lane == 0) {
+      // one lane feeds both rings: whichever group's slot is free gets its next stage
+      int64_t a = 0, b = 0;
+      while (a < nstage || b < nstage) {
+        if (a < nstage) {
+          const int pi = (int)(a & 1);
+          if (a < 2 || mbar_test(&emptyA[pi], (unsigned)(((a >> 1) - 1) & 1))) {
+            mbar_expect_tx(&fullA[pi], fs.bytesA);
+            double* dst = ring + (size_t)pi * (szA + szB);
+            const int r16 = (int)((row_begin + a * SR) / TKS);
+            for (int o = 0; o < fs.nopsA; ++o)
+              tma_load_3d(dst + (size_t)fs.opd[o] * SR, &maps.m[fs.opm[o]], 0, r16, fs.opc[o], &fullA[pi]);
+            ++a;
+          }
+        }
+        if (b < nstage) {
+          const int pi = (int)(b & 1);
+          if (b < 2 || mbar_test(&emptyB[pi], (unsigned)(((b >> 1) - 1) & 1))) {
+            mbar_expect_tx(&fullB[pi], fs.bytesB);
+            double* dst = ring + (size_t)pi * (szA + szB) + szA;
+            const int r16 = (int)((row_begin + b * SR) / TKS);
+            for (int o = fs.nopsA; o < fs.nopsA + fs.nopsB; ++o)
+              tma_load_3d(dst + (size_t)fs.opd[o] * SR, &maps.m[fs.opm[o]], 0, r16, fs.opc[o], &fullB[pi]);
+            ++b;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  if (role == FS_Y) {
+    const int cb = fs.ycb[warp], kp = fs.ykp[warp], j0 = fs.yj0[warp], nj = fs.ynj[warp];
+    const bool last = kp == FS_NKP - 1;
+    const int o0 = cb * 8 + 2 * tq;
+    for (int64_t s = 0; s < nstage; ++s) {
+      const int pi = (int)(s & 1);
+      const unsigned ph = (unsigned)((s >> 1) & 1);
+      mbar_wait(&fullA[pi], ph);
+      const double* P = ring + (size_t)pi * (szA + szB);
+      double acc[4][2];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
+      const int cbase = 4 * j0 + tq;
+#pragma unroll
+      for (int j = 0; j < FS_WR; ++j) {
+        if (j < nj) {
+          const int c = cbase + 4 * j;
+          double a[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) a[q] = P[swzr<2>(c, (q >> 1) * 16 + (q & 1) * 8 + g)];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) dmma884(acc[q][0], acc[q][1], a[q], wr[j]);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&emptyA[pi]);
+      double* Ys = sY + (size_t)pi * YC * SR;
+      if (kp == 0) {
+        if (s >= 2 && fs.npy > 0) mbar_wait(&yfree[pi], ph ^ 1u);  // the tile warps are done with Y of stage s - 2
+      } else {
+        mbar_wait(&chain[(pi * 2 + cb) * 3 + kp - 1], ph);  // the partial sum of parts 0 .. kp - 1
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int r = (q >> 1) * 16 + (q & 1) * 8 + g;
+          acc[q][0] = Ys[swzr<2>(o0, r)] + acc[q][0];
+          acc[q][1] = Ys[swzr<2>(o0 + 1, r)] + acc[q][1];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int r = (q >> 1) * 16 + (q & 1) * 8 + g;
+        Ys[swzr<2>(o0, r)] = acc[q][0];
+        Ys[swzr<2>(o0 + 1, r)] = acc[q][1];
+      }
+      if (!last) {
+        mbar_arrive(&chain[(pi * 2 + cb) * 3 + kp]);
+        continue;
+      }
+      mbar_arrive(&ydone[pi]);
+      if (p.Yout != nullptr) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t row = row_begin + s * SR + 8 * q + g;
+          if (row >= row_end) continue;
+          if (o0 < p.w) p.Yout[(int64_t)o0 * p.ldy + row] = acc[q][0];
+          if (o0 + 1 < p.w) p.Yout[(int64_t)(o0 + 1) * p.ldy + row] = acc[q][1];
+        }
+      }
+    }
+    return;
+  }
+
+  if (role == FS_PY) {
+    const int sb0 = fs.py_sb0[warp];
+    auto run = [&](auto na_t, auto yy_t) {
+      constexpr int NA = decltype(na_t)::value;
+      constexpr bool YY = decltype(yy_t)::value;
+      constexpr int NAX = NA > 0 ? NA : 1;
+      double acc[NAX][NCB][2], accy[NCB][NCB][2];
+#pragma unroll
+      for (int a = 0; a < NAX; ++a)
+#pragma unroll
+        for (int c = 0; c < NCB; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+#pragma unroll
+      for (int a = 0; a < NCB; ++a)
+#pragma unroll
+        for (int c = 0; c < NCB; ++c) accy[a][c][0] = accy[a][c][1] = 0.0;
+      for (int64_t s = 0; s < nstage; ++s) {
+        const int pi = (int)(s & 1);
+        const unsigned ph = (unsigned)((s >> 1) & 1);
+        mbar_wait(&fullB[pi], ph);
+        mbar_wait(&ydone[pi], ph);
+        const double* Bp = ring + (size_t)pi * (szA + szB) + szA;
+        const double* Ys = sY + (size_t)pi * YC * SR;
+#pragma unroll
+        for (int kk = 0; kk < SR / 4; ++kk) {
+          const int k = kk * 4 + tq;
+          double fa[NAX], fb[NCB];
+#pragma unroll
+          for (int c = 0; c < NCB; ++c) fb[c] = Ys[swzr<2>(c * 8 + g, k)];
+          if (NA > 0) {
+#pragma unroll
+            for (int a = 0; a < NAX; ++a) fa[a] = Bp[swzr<2>((sb0 + a) * 8 + g, k)];
+#pragma unroll
+            for (int a = 0; a < NAX; ++a)
+#pragma unroll
+              for (int c = 0; c < NCB; ++c) dmma884(acc[a][c][0], acc[a][c][1], fa[a], fb[c]);
+          }
+          if (YY) {
+#pragma unroll
+            for (int a = 0; a < NCB; ++a)
+#pragma unroll
+              for (int c = 0; c < NCB; ++c) dmma884(accy[a][c][0], accy[a][c][1], fb[a], fb[c]);
+          }
+        }
+        mbar_arrive(&yfree[pi]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyB[pi]);
+      }
+      // full 32 x 32 slots (the fixed-order reduce sums every element): zeros where nothing was computed
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        if (t * 4 >= NA) continue;
+        double* dst = p.partial + ((size_t)blockIdx.x * SLOTS + fs.py_slot[warp][t]) * 1024;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double v0 = 0.0, v1 = 0.0;
+            if (t * 4 + a < NA && c < NCB) v0 = acc[(t * 4 + a) % NAX][c % NCB][0], v1 = acc[(t * 4 + a) % NAX][c % NCB][1];
+            *reinterpret_cast<double2*>(dst + (a * 8 + g) * 32 + c * 8 + 2 * tq) = make_double2(v0, v1);
+          }
+      }
+      if (YY) {
+        double* dst = p.partial + ((size_t)blockIdx.x * SLOTS + fs.yy_slot) * 1024;
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            double v0 = 0.0, v1 = 0.0;
+            if (a < NCB && c < NCB) v0 = accy[a % NCB][c % NCB][0], v1 = accy[a % NCB][c % NCB][1];
+            *reinterpret_cast<double2*>(dst + (a * 8 + g) * 32 + c * 8 + 2 * tq) = make_double2(v0, v1);
+          }
+      }
+    };
+    using F = std::false_type;
+    using T = std::true_type;
+    const int na = fs.py_na[warp];
+    if (fs.py_yy[warp]) {
+      switch (na) {
+        case 0: run(std::integral_constant<int, 0>{}, T{}); break;
+        case 1: run(std::integral_constant<int, 1>{}, T{}); break;
+        case 2: run(std::integral_constant<int, 2>{}, T{}); break;
+        case 3: run(std::integral_constant<int, 3>{}, T{}); break;
+        default: run(std::integral_constant<int, 4>{}, T{}); break;
+      }
+    } else {
+      switch (na) {
+        case 1: run(std::integral_constant<int, 1>{}, F{}); break;
+        case 2: run(std::integral_constant<int, 2>{}, F{}); break;
+        case 3: run(std::integral_constant<int, 3>{}, F{}); break;
+        case 4: run(std::integral_constant<int, 4>{}, F{}); break;
+        case 5: run(std::integral_constant<int, 5>{}, F{}); break;
+        case 6: run(std::integral_constant<int, 6>{}, F{}); break;
+        case 7: run(std::integral_constant<int, 7>{}, F{}); break;
+        default: run(std::integral_constant<int, 8>{}, F{}); break;
+      }
+    }
+    return;
+  }
+
+  if (role == FS_OFF) {
+    const int I = fs.off_i[warp], J = fs.off_j[warp];
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+    auto run = [&](auto diag_t) {
+      constexpr bool DIAG = decltype(diag_t)::value;
+      for (int64_t s = 0; s < nstage; ++s) {
+        const int pi = (int)(s & 1);
+        mbar_wait(&fullB[pi], (unsigned)((s >> 1) & 1));
+        const double* Bp = ring + (size_t)pi * (szA + szB) + szA;
+#pragma unroll
+        for (int kk = 0; kk < SR / 4; ++kk) {
+          const int k = kk * 4 + tq;
+          double fa[4], fb[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) fa[q] = Bp[swzr<2>(I * 32 + q * 8 + g, k)];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) fb[q] = DIAG ? fa[q] : Bp[swzr<2>(J * 32 + q * 8 + g, k)];
+#pragma unroll
+          for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (!DIAG || c >= a) dmma884(acc[a][c][0], acc[a][c][1], fa[a], fb[c]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyB[pi]);
+      }
+    };
+    if (I == J) run(std::true_type{});
+    else run(std::false_type{});
+    double* dst = p.partial + ((size_t)blockIdx.x * SLOTS + fs.off_slot[warp]) * 1024;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<double2*>(dst + (a * 8 + g) * 32 + c * 8 + 2 * tq) = make_double2(acc[a][c][0], acc[a][c][1]);
+  }
+}
+
+void launch_fused_split(const TallParams& p, const TmaMaps& maps3, const TmaExtra& x, const FusedSplit& fs, int grid,
+                        cudaStream_t st) {
+  const size_t smem = fused_split_smem_bytes(fs);
+  if (fs.ncb == 2) {
+    cudaFuncSetAttribute(fused_split_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    fused_split_kernel<2><<<grid, NTHR, smem, st>>>(p, maps3, x, fs);
+  } else {
+    cudaFuncSetAttribute(fused_split_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    fused_split_kernel<1><<<grid, NTHR, smem, st>>>(p, maps3, x, fs);
+  }
+}
+
 // ---------------------------------------------------------------- host side
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -903,6 +1239,208 @@ int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift, bool
   // issue groups: half the ring (two groups in flight), at most 4 stages = 64 rows
   x.grp = 1;  // grouped issue (consecutive stages box by box) measured no faster: off by default
   if (const char* e = getenv("PSVD_TMA_GROUP")) x.grp = std::max(1, std::min(x.ns, atoi(e)));
+  return 0;
+}
+
+// Split-ring fused pass: qualifies a planned narrow TMA pass (p, x: tma_pass_prepare's box list; map: its
+// reduce map with NB tile columns) and builds the warp roles, the k split and the 3-D tensor maps.
+// off[i] = {I, J}: 32-column block pairs of the last segment's Gram to compute here (full blocks
+// only, I <= J), reduced by offmap into a tile array with off_nb tile columns.  Returns 0 when the
+// pass runs on fused_split_kernel, -1 when it has to stay on pass_tma_kernel.
+int fused_split_prepare(const TallParams& p, const TmaExtra& x, const ReduceMap& map, int NB, const int (*off)[2],
+                        int noff, FusedSplit& fs, TmaMaps& maps3, ReduceMap& offmap, int off_nb) {
+  EncodeTiledFn enc = encode_fn();
+  memset(&fs, 0, sizeof(fs));
+  memset(&offmap, 0, sizeof(offmap));
+  if (!enc || p.nseg < 2 || p.nslices != 1 || x.pshift != 0 || p.w < 1 || x.kp_lo != 0 || p.M % TKS != 0 ||
+      (p.w_pad != 8 && p.w_pad != 16) || p.colmax != nullptr || p.gate != nullptr || p.dbg != 0 || p.wlo != 0)
+    return -1;
+  const int last = p.nseg - 1;
+  if (x.wrow0[last] != TMA_NOT_IN_W) return -1;
+  for (int s = 0; s < last; ++s)
+    if (x.wrow0[s] == TMA_NOT_IN_W || (p.seg[s].col0 & 7) != 0) return -1;
+  const int colB = p.seg[last].col0;
+  const int endA = p.seg[last - 1].col0 + p.seg[last - 1].ncols;
+  fs.pwA = (endA + 7) / 8 * 8;
+  fs.pwB = (p.seg[last].ncols + 7) / 8 * 8;
+  fs.ncb = p.w_pad / 8;
+  if ((colB & 31) != 0 || colB < fs.pwA || x.kp_hi > fs.pwA || p.seg[last].ncols > 256) return -1;
+  fs.n4 = x.kp_hi / 4;
+  if (fs.n4 < FS_NKP || fs.n4 > FS_NKP * FS_WR) return -1;
+  if (fused_split_smem_bytes(fs) > (size_t)(227 * 1024)) return -1;
+  // boxes: group A first, then group B; every 8-column block of both slots must be covered
+  std::vector<char> covA(fs.pwA / 8, 0), covB(fs.pwB / 8, 0);
+  int n = 0;
+  for (int pass = 0; pass < 2; ++pass)
+    for (int o = 0; o < x.nops; ++o) {
+      const int m = x.op_seg[o], sidx = m % MAX_SEG;
+      if ((sidx == last) != (pass == 1)) continue;
+      const int dst = x.op_pcol[o] - (pass == 1 ? colB : 0), bw = x.op_bw[o];
+      if (dst < 0 || (dst & 7) != 0 || x.op_col[o] < 0 || dst + bw > (pass == 1 ? fs.pwB : fs.pwA)) return -1;
+      fs.opm[n] = (short)m;
+      fs.opc[n] = x.op_col[o];
+      fs.opd[n] = (short)dst;
+      for (int q = dst / 8; q < (dst + bw) / 8; ++q) (pass == 1 ? covB : covA)[q] = 1;
+      (pass == 1 ? fs.bytesB : fs.bytesA) += (unsigned)(2 * TKS * bw * sizeof(double));
+      (pass == 1 ? fs.nopsB : fs.nopsA)++;
+      const Seg& sg = p.seg[sidx];
+      cuuint64_t dims[3] = {(cuuint64_t)TKS, (cuuint64_t)(p.M / TKS), (cuuint64_t)sg.ncols};
+      cuuint64_t strides[2] = {(cuuint64_t)TKS * sizeof(double), (cuuint64_t)sg.ld * sizeof(double)};
+      cuuint32_t box[3] = {(cuuint32_t)TKS, 2, (cuuint32_t)bw};
+      cuuint32_t es[3] = {1, 1, 1};
+      if (enc(&maps3.m[m], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(sg.ptr), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return -1;
+      ++n;
+    }
+  for (char c : covA) if (!c) return -1;
+  for (char c : covB) if (!c) return -1;
+  // output slots of the planned tiles: (colB / 32 + t, Y block) and (Y block, Y block)
+  const int yblk = p.np_pad / 32;
+  auto slot_of = [&](int I, int J) {
+    for (int o = 0; o < map.nout; ++o)
+      if (map.out_id[o] == I * NB + J && map.nsrc[o] == 1 && map.src[o][0] < SLOTS) return (int)map.src[o][0];
+    return -1;
+  };
+  std::vector<char> used(SLOTS, 0);
+  for (int o = 0; o < map.nout; ++o)
+    for (int i = 0; i < map.nsrc[o]; ++i)
+      if (map.src[o][i] < SLOTS) used[map.src[o][i]] = 1;
+  const int nsbB = fs.pwB / 8, ntB = (nsbB + 3) / 4;
+  if (map.nout != ntB + 1) return -1;
+  const int yy_slot = slot_of(yblk, yblk);
+  if (yy_slot < 0) return -1;
+  fs.yy_slot = (unsigned char)yy_slot;
+  // fixed items: P^T Y warps of up to 8 sub-blocks, Y^T Y on the lightest of them when it has <= 4
+  // sub-blocks (else a warp of its own), offloaded tiles, the producer
+  struct Item { int kind, cost, a, b; };
+  std::vector<Item> items;
+  const int npyw = (nsbB + 7) / 8;
+  for (int i = 0; i < npyw; ++i) {
+    const int na = std::min(8, nsbB - 8 * i);
+    items.push_back({FS_PY, na * fs.ncb * 8, 8 * i, na});
+  }
+  bool yy_own = items.back().b > 4;
+  if (yy_own) items.push_back({FS_PY, fs.ncb * fs.ncb * 8, 0, 0});
+  else items.back().cost += fs.ncb * fs.ncb * 8;
+  const int yy_item = (int)items.size() - 1;
+  const int nfullB = p.seg[last].ncols / 32;
+  int noff_ok = 0;
+  for (int i = 0; i < noff && noff_ok < FS_MAX_OFF; ++i) {
+    const int I = off[i][0], J = off[i][1];
+    if (I < 0 || I > J || J >= nfullB) continue;
+    items.push_back({FS_OFF, (I == J ? 10 : 16) * 8, I, J});
+    ++noff_ok;
+  }
+  items.push_back({FS_PROD, 0, 0, 0});
+  const int nyw = fs.ncb * FS_NKP;
+  if ((int)items.size() + nyw > NWARP) return -1;
+  // longest first onto the least-loaded SMSP (warp w issues on SMSP w % 4) with a free slot
+  std::vector<int> order(items.size());
+  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return items[a].cost > items[b].cost; });
+  int load[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
+  int free_slot = 0;
+  for (int it : order) {
+    int q = -1;
+    for (int c = 0; c < 4; ++c)
+      if (cnt[c] < 4 && (q < 0 || load[c] < load[q] || (load[c] == load[q] && cnt[c] < cnt[q]))) q = c;
+    const int w = q + 4 * cnt[q];
+    cnt[q]++;
+    load[q] += items[it].cost;
+    const Item& im = items[it];
+    fs.role[w] = (unsigned char)im.kind;
+    if (im.kind == FS_PY) {
+      fs.py_sb0[w] = (unsigned char)im.a;
+      fs.py_na[w] = (unsigned char)im.b;
+      fs.py_yy[w] = (unsigned char)(it == yy_item);
+      for (int t = 0; t < 2 && 4 * t < im.b; ++t) {
+        const int sl = slot_of(colB / 32 + im.a / 4 + t, yblk);
+        if (sl < 0) return -1;
+        fs.py_slot[w][t] = (unsigned char)sl;
+      }
+      fs.npy++;
+    } else if (im.kind == FS_OFF) {
+      while (free_slot < SLOTS && used[free_slot]) ++free_slot;
+      if (free_slot >= SLOTS) return -1;
+      used[free_slot] = 1;
+      fs.off_i[w] = (unsigned char)im.a;
+      fs.off_j[w] = (unsigned char)im.b;
+      fs.off_slot[w] = (unsigned char)free_slot;
+      const int o = offmap.nout++;
+      offmap.out_id[o] = (short)(im.a * off_nb + im.b);
+      offmap.nsrc[o] = 1;
+      offmap.src[o][0] = (unsigned char)free_slot;
+      fs.noff++;
+    }
+  }
+  // Y warps take the remaining slots; column blocks alternate so that each gets FS_NKP parts
+  std::vector<int> yw;
+  for (int i = 0; i < 4; ++i)
+    for (int q = 0; q < 4; ++q)
+      if (i >= cnt[q] && (int)yw.size() < nyw) yw.push_back(q + 4 * i);
+  if ((int)yw.size() != nyw) return -1;
+  std::sort(yw.begin(), yw.end(), [](int a, int b) { return a % 4 != b % 4 ? a % 4 < b % 4 : a < b; });
+  int ywarps[4] = {0, 0, 0, 0};
+  for (int w : yw) ywarps[w % 4]++;
+  const double target = (load[0] + load[1] + load[2] + load[3] + 4.0 * fs.n4 * fs.ncb) / 4.0;
+  std::vector<int> kpn(fs.ncb, 0);
+  std::vector<std::vector<int>> wcb(fs.ncb);
+  for (size_t i = 0; i < yw.size(); ++i) wcb[i % fs.ncb].push_back(yw[i]);
+  for (int cb = 0; cb < fs.ncb; ++cb) {
+    // a part's weight: what its SMSP has left of the even share, split over the Y warps issuing there
+    std::vector<double> wgt(FS_NKP);
+    double sum = 0.0;
+    for (int kp = 0; kp < FS_NKP; ++kp) {
+      const int q = wcb[cb][kp] % 4;
+      wgt[kp] = std::max(4.0, (target - load[q]) / std::max(1, ywarps[q]));
+      sum += wgt[kp];
+    }
+    std::vector<int> nj(FS_NKP);
+    int tot = 0;
+    for (int kp = 0; kp < FS_NKP; ++kp) {
+      nj[kp] = std::max(1, std::min(FS_WR, (int)(fs.n4 * wgt[kp] / sum + 0.5)));
+      tot += nj[kp];
+    }
+    for (int guard = 0; tot != fs.n4 && guard < 1000; ++guard) {  // fix the rounding, heaviest weights first
+      int best = -1;
+      for (int kp = 0; kp < FS_NKP; ++kp) {
+        if (tot < fs.n4 && nj[kp] >= FS_WR) continue;
+        if (tot > fs.n4 && nj[kp] <= 1) continue;
+        if (best < 0 || (tot < fs.n4 ? wgt[kp] / nj[kp] > wgt[best] / nj[best] : wgt[kp] / nj[kp] < wgt[best] / nj[best]))
+          best = kp;
+      }
+      if (best < 0) return -1;
+      nj[best] += tot < fs.n4 ? 1 : -1;
+      tot += tot < fs.n4 ? 1 : -1;
+    }
+    if (tot != fs.n4) return -1;
+    int j = 0;
+    for (int kp = 0; kp < FS_NKP; ++kp) {
+      const int w = wcb[cb][kp];
+      fs.role[w] = FS_Y;
+      fs.ycb[w] = (unsigned char)cb;
+      fs.ykp[w] = (unsigned char)kp;
+      fs.yj0[w] = (unsigned char)j;
+      fs.ynj[w] = (unsigned char)nj[kp];
+      j += nj[kp];
+    }
+  }
+  offmap.nchunks = map.nchunks;
+  offmap.nslices = 1;
+  static const bool verbose = getenv("PSVD_PASS_VERBOSE") != nullptr;
+  if (verbose) {
+    fprintf(stderr, "fused_split: pwA=%d pwB=%d n4=%d ncb=%d npy=%d noff=%d smem=%zu roles:", fs.pwA, fs.pwB, fs.n4, fs.ncb,
+            fs.npy, fs.noff, fused_split_smem_bytes(fs));
+    for (int w = 0; w < NWARP; ++w) {
+      if (fs.role[w] == FS_Y) fprintf(stderr, " w%d:Y(cb%d,kp%d,%d+%d)", w, fs.ycb[w], fs.ykp[w], fs.yj0[w], fs.ynj[w]);
+      else if (fs.role[w] == FS_PY) fprintf(stderr, " w%d:PY(sb%d+%d%s)", w, fs.py_sb0[w], fs.py_na[w], fs.py_yy[w] ? ",yy" : "");
+      else if (fs.role[w] == FS_OFF) fprintf(stderr, " w%d:OFF(%d,%d)", w, fs.off_i[w], fs.off_j[w]);
+      else if (fs.role[w] == FS_PROD) fprintf(stderr, " w%d:PROD", w);
+    }
+    fprintf(stderr, "\n");
+  }
   return 0;
 }
 

@@ -107,6 +107,31 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
   const bool defer = defer_env && la_serial && K <= DRIFT_SMEM_KMAX;
   const int nsub = la_serial ? 1 : (int)std::max<int64_t>(1, std::min<int64_t>(4, M / 65536));
   const int la_ctas = la_serial ? c->num_sms - 1 : c->num_sms - 2;
+  // Fused passes planned up front: the ones that qualify run on the split-ring kernel (32-row 3-D boxes,
+  // psvd_tall.cuh: FusedSplit), which also computes a few 32 x 32 tiles of the next batch's A^T A; the
+  // look-ahead Gram of that batch then skips them (skip_pp[j]).  PSVD_NO_FSPLIT=1: the narrow TMA pass for
+  // all of them; PSVD_FS_NOFF=n: tiles taken off the Gram (default 3).
+  static const int fs_noff = getenv("PSVD_FS_NOFF") ? std::max(0, std::min(FS_MAX_OFF, atoi(getenv("PSVD_FS_NOFF")))) : 3;
+  std::vector<Pass> fpass(nb > 1 ? nb - 1 : 0);
+  std::vector<std::vector<std::pair<int, int>>> skip_pp(nb);
+  for (int b = 0; b + 1 < nb; ++b) {
+    const int kc = (b == 0) ? Kc : K;
+    const double* up = b == 0 ? (Kc > 0 ? U_in : nullptr) : bufs[(b - 1) & 1];
+    const int64_t ldp = b == 0 ? (Kc > 0 ? ldu : 0) : ldo;
+    std::vector<Seg> segs = panel(up, ldp, kc, A[b], lda[b], B[b]);
+    segs.push_back(Seg{A[b + 1], lda[b + 1], B[b + 1], 1});
+    const int wk = kc + B[b];
+    static const int fused_ctas = getenv("PSVD_FUSED_CTAS") ? atoi(getenv("PSVD_FUSED_CTAS")) : 0;
+    if ((rc = plan_pass(c, fpass[b], M, segs, 0, wk, K, W, wk, false, true, true, -1, -1, nullptr, nullptr, fused_ctas, -1)))
+      return rc;
+    // full off-diagonal blocks (0,1), (2,3), ... of A_{b+1}^T A_{b+1}
+    std::vector<std::pair<int, int>> off;
+    const int nfull = B[b + 1] / 32;
+    for (int t = 0; 2 * t + 1 < nfull && (int)off.size() < fs_noff; ++t) off.push_back({2 * t, 2 * t + 1});
+    if (la_serial && try_fused_split(c, fpass[b], off, (B[b + 1] + 31) / 32))
+      for (int o = 0; o < fpass[b].offmap.nout; ++o)
+        skip_pp[b + 1].push_back({fpass[b].offmap.out_id[o] / ((B[b + 1] + 31) / 32), fpass[b].offmap.out_id[o] % ((B[b + 1] + 31) / 32)});
+  }
   auto aa_pass = [&](int j) -> int {
     if (j >= 2) cudaStreamWaitEvent(lo, c->ev_asm[j & 1], 0);  // tiles2[j&1] consumed by batch j-2's assembly
     // start A^T A of batch j with the core solve of batch j-1: it then overlaps that one-SM
@@ -129,7 +154,8 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
       cudaEventRecord(c->tev[c->tev_used], lo);
       te1 = c->tev[c->tev_used + 1];
       c->tev_used += 2;
-      c->timed_flops += (double)M * B[j] * (B[j] + 1);  // upper triangle of A^T A (DMMA tiles)
+      // upper triangle of A^T A (DMMA tiles), less the 32 x 32 tiles the split-ring fused pass computes
+      c->timed_flops += (double)M * B[j] * (B[j] + 1) - 2048.0 * M * skip_pp[j].size();
     }
     for (int k = 0; k < nsub; ++k) {
       const int64_t r0 = (int64_t)k * rows_sub;
@@ -137,7 +163,7 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
       const int64_t mk = std::min(M, r0 + rows_sub) - r0;
       Pass pa;
       int r = plan_pass(c, pa, mk, {Seg{A[j] + r0, lda[j], B[j], 0}}, 0, 0, 0, nullptr, 0, true, false, false, -1,
-                        -1, &c->partial2, &c->tiles2[j & 1], la_ctas);
+                        -1, &c->partial2, &c->tiles2[j & 1], la_ctas, 0, false, skip_pp[j].empty() ? nullptr : &skip_pp[j]);
       if (r) return r;
       const size_t need = part_off + (size_t)pa.grid * SLOTS * 1024;
       if (k == 0) {  // size the partial buffer for all sub-ranges once
@@ -220,18 +246,19 @@ int psvd_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu, con
     }
     if (b + 1 < nb) {
       // fused: U_b = [U_{b-1} | A_b] W, with U_b^T U_b and U_b^T A_{b+1} from the same pass
-      std::vector<Seg> segs = panel(Uprev, ldprev, kc, A[b], lda[b], B[b]);
-      segs.push_back(Seg{A[b + 1], lda[b + 1], B[b + 1], 1});
       if (batch_ready && batch_ready[b + 1]) cudaStreamWaitEvent(hi, (cudaEvent_t)batch_ready[b + 1], 0);
       if (la_serial) cudaStreamWaitEvent(hi, c->ev_aa[(b + 1) & 1], 0);
-      Pass pf;
+      Pass& pf = fpass[b];
       const int wk = kc + B[b];
-      if ((rc = plan_pass(c, pf, M, segs, 0, wk, K, W, wk, false, true, true, -1, -1, nullptr, nullptr, 0, -1)))
-        return rc;
+      pf.p.partial = (double*)pf.part->ptr;  // the workspace may have grown since the plan
       const int a0 = pf.p.seg[pf.p.nseg - 1].col0 / 32;
       pf.p.Yout = Uout;
       pf.p.ldy = ldo;
-      if ((rc = run_pass(c, pf, hi))) return rc;
+      if (pf.fsplit) {
+        if ((rc = run_fused_split(c, pf, hi, (double*)c->tiles2[(b + 1) & 1].ptr))) return rc;
+      } else if ((rc = run_pass(c, pf, hi))) {
+        return rc;
+      }
       cudaEventRecord(c->ev_fdone, hi);
       if (getenv("PSVD_DUMP_FUSED")) {  // diagnostics: tiles + Y of the fused pass
         cudaStreamSynchronize(hi);

@@ -120,6 +120,37 @@ bool tma_available();
 size_t tma_pass_smem_bytes(int pwidth, int kp_span, int w_pad, int ns = 3, int ny = 1);
 int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift = 0, bool narrow = false);
 void launch_pass_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x, int grid, cudaStream_t st);
+// Split-ring fused pass of the pipelined deterministic stream (fused_split_kernel): the panel
+// [U | A_b | A_next] streamed as 32-row stages of two column groups (A = [U | A_b], B = A_next),
+// each in its own two-slot ring of 3-D TMA boxes; Y = [U | A_b] W with W in registers, the tiles
+// A_next^T Y and Y^T Y, and up to FS_MAX_OFF offloaded 32 x 32 tiles of A_next^T A_next (work
+// taken off the look-ahead Gram: the pass is HBM-bound, its DMMA pipe has room).
+constexpr int FS_WR = 20;      // W fragments (k steps of 4 columns) a Y warp holds in registers
+constexpr int FS_NKP = 4;      // k parts per Y column block
+constexpr int FS_MAX_OFF = 3;  // offloaded Gram tiles
+enum { FS_IDLE = 0, FS_Y = 1, FS_PY = 2, FS_OFF = 3, FS_PROD = 4 };
+struct FusedSplit {
+  int pwA, pwB;                  // slot widths in columns (multiples of 8)
+  int nopsA, nopsB;              // TMA boxes per stage of each group (group A's come first)
+  short opm[TMA_MAX_OPS], opc[TMA_MAX_OPS], opd[TMA_MAX_OPS];  // tensor map, tensor column, slot column
+  unsigned bytesA, bytesB;       // bytes per stage of each group
+  int ncb;                       // Y column blocks (1 or 2)
+  int n4;                        // k steps of 4 physical panel columns
+  int npy, noff;                 // warps with P^T Y tiles / offloaded Gram tiles
+  unsigned char role[NWARP];
+  unsigned char ycb[NWARP], ykp[NWARP], yj0[NWARP], ynj[NWARP];     // Y warps: column block, part, k steps
+  unsigned char py_sb0[NWARP], py_na[NWARP], py_yy[NWARP];         // P^T Y warps: 8-column sub-blocks of slot B
+  unsigned char py_slot[NWARP][2], yy_slot;                        // partial-tile slots (32-column tiles)
+  unsigned char off_i[NWARP], off_j[NWARP], off_slot[NWARP];       // offloaded tile (I, J) of A_next^T A_next
+};
+size_t fused_split_smem_bytes(const FusedSplit& fs);
+void launch_fused_split(const TallParams& p, const TmaMaps& maps3, const TmaExtra& x, const FusedSplit& fs, int grid,
+                        cudaStream_t st);
+// builds fs and the 3-D tensor maps from a planned narrow TMA pass (p, x, its reduce map); off: wanted
+// offloaded tiles (block pairs of the last segment); returns 0 when the pass qualifies
+int fused_split_prepare(const TallParams& p, const TmaExtra& x, const ReduceMap& map, int NB, const int (*off)[2],
+                        int noff, FusedSplit& fs, TmaMaps& maps3, ReduceMap& offmap, int off_nb);
+
 // TMA-fed Gram-only pass (w == 0, segments on 8-column boundaries, <= NWARP - 1 tiles per slice)
 constexpr int TMA_GRAM_CONS = NWARP - 1;
 size_t gram_tma_smem_bytes(int np_pad);
