@@ -52,6 +52,8 @@ _SIGS = {
     "psvd_core_eig": (_c_int, [_vp, _vp, _c_int, _vp, _c_dbl, _c_int, _c_int, _vp, _vp, _vp]),
     "psvd_recompose": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _vp, _c_int, _vp,
                                 _c_i64, _vp, _vp]),
+    "psvd_fused_pass": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _vp, _c_i64, _c_int, _vp, _c_int,
+                                 _vp, _c_i64, _vp, _vp, _c_int, _c_int, _vp, _vp]),
     "psvd_refine_normalize": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _vp, _vp, _vp]),
     "psvd_drift_rescue": (_c_int, [_vp, _c_i64, _vp, _c_i64, _c_int, _vp, _vp, _c_dbl, _vp]),
     "psvd_stream_update": (_c_int, [_vp, _c_i64, _vp, _c_i64, _vp, _c_dbl, _c_int, _vp, _c_i64, _c_int,

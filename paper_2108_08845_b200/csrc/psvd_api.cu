@@ -474,6 +474,8 @@ bool try_fused_split(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int
   ps.fsplit = false;
   static const bool disabled = getenv("PSVD_NO_FSPLIT") != nullptr;
   if (disabled || !ps.tma || c->num_sms < 1) return false;
+  static const int fs_dbg = getenv("PSVD_FS_DBG") ? atoi(getenv("PSVD_FS_DBG")) : 0;  // timing diagnostics (wrong results)
+  if (fs_dbg) ps.p.dbg = fs_dbg;
   int offs[FS_MAX_OFF][2];
   int noff = 0;
   for (const auto& t : off)
@@ -854,6 +856,39 @@ int psvd_recompose(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, int Kc,
     rc = cuda_check(c, "extract UtU");
   }
   return rc;
+}
+
+int psvd_fused_pass(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, int Kc, const double* A, int64_t lda, int B,
+                    const double* A_next, int64_t ldan, int Bn, const double* W, int K, double* U_out, int64_t ldo,
+                    double* UtU, double* AtU, int mode, int noff, double* off_tiles, void* stream) {
+  if (!c) return PSVD_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc;
+  if (M < 1 || K < 1 || B < 1 || Bn < 1 || Kc < 0 || !W || !UtU || !AtU) return fail(c, PSVD_EINVAL, "bad fused_pass arguments");
+  if ((rc = check_mat(c, "U", U, ldu, M, Kc)) || (rc = check_mat(c, "A", A, lda, M, B)) ||
+      (rc = check_mat(c, "A_next", A_next, ldan, M, Bn)) || (rc = check_mat(c, "U_out", U_out, ldo, M, K)))
+    return rc;
+  std::vector<Seg> segs = panel(U, ldu, Kc, A, lda, B);
+  segs.push_back(Seg{A_next, ldan, Bn, 1});
+  const int wk = Kc + B;
+  Pass pf;
+  if ((rc = plan_pass(c, pf, M, segs, 0, wk, K, W, wk, false, true, true, -1, -1, nullptr, nullptr, 0, -1))) return rc;
+  pf.p.Yout = U_out;
+  pf.p.ldy = ldo;
+  const int off_nb = (Bn + 31) / 32;
+  if (mode == 1) {
+    std::vector<std::pair<int, int>> off;
+    for (int t = 0; 2 * t + 1 < Bn / 32 && t < noff && off_tiles; ++t) off.push_back({2 * t, 2 * t + 1});
+    if (!try_fused_split(c, pf, off, off_nb)) return fail(c, PSVD_EINVAL, "the pass does not qualify for the split-ring kernel");
+    if ((rc = run_fused_split(c, pf, st, off_tiles))) return rc;
+  } else if ((rc = run_pass(c, pf, st))) {
+    return rc;
+  }
+  const int a0 = pf.p.seg[pf.p.nseg - 1].col0 / 32;
+  launch_extract_sym((const double*)c->tiles.ptr, pf.NB, pf.p.np_pad, K, nullptr, UtU, st);
+  launch_extract_rect((const double*)c->tiles.ptr, pf.NB, a0 * 32, Bn, pf.p.np_pad, K, nullptr, AtU, st);
+  c->launches += 2;
+  return cuda_check(c, "fused pass extract");
 }
 
 int psvd_drift_rescue(psvd_ctx* c, int64_t M, double* U, int64_t ldu, int K, const double* UtU, double* sigma,

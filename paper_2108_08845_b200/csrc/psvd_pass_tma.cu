@@ -104,7 +104,7 @@ size_t tma_pass_smem_bytes(int pwidth, int kp_span, int w_pad, int ns, int rb) {
   return b;
 }
 
-template <int RB>
+template <int RB, bool AOFF = false>
 __global__ void __launch_bounds__(NTHR, 1)
     pass_tma_kernel(const __grid_constant__ TallParams p, const __grid_constant__ TmaMaps maps, const TmaExtra x) {
   if (p.gate != nullptr && *p.gate == 0) return;  // gated pass (drift rescue) not needed
@@ -239,6 +239,15 @@ __global__ void __launch_bounds__(NTHR, 1)
       wr[j] = j < nj ? sW[(size_t)(4 * (j0 + j) + tq) * WSP + cb * 8 + g] : 0.0;
     const bool last = kp == ykp - 1;
     const bool do_y = slice == 0 && last;
+    // element (column kp_lo + 4 (j0 + j) + tq, row 16 h + rr) of a stage is unit u = 2 kp_lo + 8 (j0 + j)
+    // + 2 tq + h with u & 7 = 2 tq + h whatever j (kp_lo is a multiple of 8): swzr<2> = a per-lane offset
+    // + 128 j, no address arithmetic per load
+    int aoff[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int h = q >> 1, rr = (q & 1) * 8 + g;
+      aoff[q] = (2 * (x.kp_lo + 4 * j0 + tq) + h) * 16 + ((((rr >> 1) ^ (2 * tq + h)) << 1) | (rr & 1));
+    }
     double cm_val[2] = {0.0, 0.0}, cm_abs[2] = {-1.0, -1.0};
     int64_t cm_row[2] = {-1, -1};
     int b = 0;
@@ -254,13 +263,17 @@ __global__ void __launch_bounds__(NTHR, 1)
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
       const int cbase = x.kp_lo + 4 * j0 + tq;
+      // AOFF: precomputed per-lane offsets, no address arithmetic per load.  Measured faster for one or
+      // two Y column blocks (the recompose: 0.43 -> 0.38 ms) and slower for three (the randomized passes'
+      // 12 Y warps: 0.53 -> 0.63 ms), so the launch picks the instantiation by Y width
 #pragma unroll
       for (int j = 0; j < YKP_WR; ++j) {
         if (j < nj && p.dbg != 1) {
           const int c = cbase + 4 * j;
           double a[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) a[q] = P[swzr<2>(c, (q >> 1) * 16 + (q & 1) * 8 + g)];
+          for (int q = 0; q < 4; ++q)
+            a[q] = AOFF ? P[aoff[q] + 128 * j] : P[swzr<2>(c, (q >> 1) * 16 + (q & 1) * 8 + g)];
 #pragma unroll
           for (int q = 0; q < 4; ++q) dmma884(acc[q][0], acc[q][1], a[q], wr[j]);
         }
@@ -760,8 +773,10 @@ PSVD_DEV bool mbar_test(uint64_t* bar, unsigned parity) {
 
 }  // namespace
 
+constexpr int FS_YB = 2;  // Y ring depth: the Y warps run up to FS_YB stages ahead of the tile warps
+
 size_t fused_split_smem_bytes(const FusedSplit& fs) {
-  return 1024 + sizeof(double) * 2 * (size_t)(fs.pwA + fs.pwB) * 32 + sizeof(double) * 2 * 8 * (size_t)fs.ncb * 32 +
+  return 1024 + sizeof(double) * 2 * (size_t)(fs.pwA + fs.pwB) * 32 + sizeof(double) * FS_YB * 8 * (size_t)fs.ncb * 32 +
          64 * sizeof(uint64_t);
 }
 
@@ -778,10 +793,10 @@ __global__ void __launch_bounds__(NTHR, 1)
   unsigned char* base = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
   const size_t szA = (size_t)fs.pwA * SR, szB = (size_t)fs.pwB * SR;  // doubles per slot
   double* ring = reinterpret_cast<double*>(base);                     // [A0 | B0 | A1 | B1]
-  double* sY = ring + 2 * (szA + szB);                                // [2][YC columns][32 rows], swzr<2>
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sY + 2 * YC * SR);
+  double* sY = ring + 2 * (szA + szB);                                // [FS_YB][YC columns][32 rows], swzr<2>
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sY + FS_YB * YC * SR);
   uint64_t *fullA = bars, *emptyA = bars + 2, *fullB = bars + 4, *emptyB = bars + 6, *ydone = bars + 8,
-           *yfree = bars + 10, *chain = bars + 12;  // chain[(yb * 2 + cb) * 3 + link]
+           *yfree = bars + 8 + FS_YB, *chain = bars + 8 + 2 * FS_YB;  // chain[(yb * 2 + cb) * 3 + link]
   const int WSP = w_stride(YC);
   double* sW = ring;  // W staged through slot A0 before the first box lands there
 
@@ -799,17 +814,19 @@ __global__ void __launch_bounds__(NTHR, 1)
     }
     sW[i] = v;
   }
-  for (int i = tid; i < 2 * YC * SR; i += NTHR) sY[i] = 0.0;
+  for (int i = tid; i < FS_YB * YC * SR; i += NTHR) sY[i] = 0.0;
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
       mbar_init(&fullA[b], 1);
       mbar_init(&fullB[b], 1);
       mbar_init(&emptyA[b], (unsigned)(NCB * FS_NKP));
       mbar_init(&emptyB[b], (unsigned)max(fs.npy + fs.noff, 1));
+    }
+    for (int b = 0; b < FS_YB; ++b) {
       mbar_init(&ydone[b], 32u * NCB);
       mbar_init(&yfree[b], (unsigned)max(32 * fs.npy, 1));
     }
-    for (int i = 0; i < 2 * 2 * 3; ++i) mbar_init(&chain[i], 32u);
+    for (int i = 0; i < FS_YB * 2 * 3; ++i) mbar_init(&chain[i], 32u);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -832,10 +849,10 @@ __global__ void __launch_bounds__(NTHR, 1)
         if (a < nstage) {
           const int pi = (int)(a & 1);
           if (a < 2 || mbar_test(&emptyA[pi], (unsigned)(((a >> 1) - 1) & 1))) {
-            mbar_expect_tx(&fullA[pi], fs.bytesA);
+            mbar_expect_tx(&fullA[pi], p.dbg == 2 ? 0u : fs.bytesA);  // dbg 2: no loads (compute-only timing)
             double* dst = ring + (size_t)pi * (szA + szB);
             const int r16 = (int)((row_begin + a * SR) / TKS);
-            for (int o = 0; o < fs.nopsA; ++o)
+            for (int o = 0; o < (p.dbg == 2 ? 0 : fs.nopsA); ++o)
               tma_load_3d(dst + (size_t)fs.opd[o] * SR, &maps.m[fs.opm[o]], 0, r16, fs.opc[o], &fullA[pi]);
             ++a;
           }
@@ -843,10 +860,10 @@ __global__ void __launch_bounds__(NTHR, 1)
         if (b < nstage) {
           const int pi = (int)(b & 1);
           if (b < 2 || mbar_test(&emptyB[pi], (unsigned)(((b >> 1) - 1) & 1))) {
-            mbar_expect_tx(&fullB[pi], fs.bytesB);
+            mbar_expect_tx(&fullB[pi], p.dbg == 2 ? 0u : fs.bytesB);
             double* dst = ring + (size_t)pi * (szA + szB) + szA;
             const int r16 = (int)((row_begin + b * SR) / TKS);
-            for (int o = fs.nopsA; o < fs.nopsA + fs.nopsB; ++o)
+            for (int o = fs.nopsA; o < (p.dbg == 2 ? 0 : fs.nopsA + fs.nopsB); ++o)
               tma_load_3d(dst + (size_t)fs.opd[o] * SR, &maps.m[fs.opm[o]], 0, r16, fs.opc[o], &fullB[pi]);
             ++b;
           }
@@ -860,60 +877,81 @@ __global__ void __launch_bounds__(NTHR, 1)
     const int cb = fs.ycb[warp], kp = fs.ykp[warp], j0 = fs.yj0[warp], nj = fs.ynj[warp];
     const bool last = kp == FS_NKP - 1;
     const int o0 = cb * 8 + 2 * tq;
-    for (int64_t s = 0; s < nstage; ++s) {
-      const int pi = (int)(s & 1);
-      const unsigned ph = (unsigned)((s >> 1) & 1);
-      mbar_wait(&fullA[pi], ph);
-      const double* P = ring + (size_t)pi * (szA + szB);
-      double acc[4][2];
+    // element (column 4 (j0 + j) + tq, row 16 h + rr) of a stage is unit u = 8 (j0 + j) + 2 tq + h with
+    // u & 7 = 2 tq + h whatever j: swzr<2> = a per-lane offset + 128 j, no address arithmetic per load
+    int aoff[4], yoff[4][2];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
-      const int cbase = 4 * j0 + tq;
+    for (int q = 0; q < 4; ++q) {
+      const int h = q >> 1, rr = (q & 1) * 8 + g;
+      aoff[q] = (8 * j0 + 2 * tq + h) * 16 + ((((rr >> 1) ^ (2 * tq + h)) << 1) | (rr & 1));
+      yoff[q][0] = swzr<2>(o0, 16 * h + rr);
+      yoff[q][1] = swzr<2>(o0 + 1, 16 * h + rr);
+    }
+    // the step count of a part is a compile-time constant of its stage loop: no branch per step and the
+    // fragment loads of later steps issue under the DMMAs of earlier ones
+    const bool y0_ok = p.Yout != nullptr && o0 < p.w, y1_ok = p.Yout != nullptr && o0 + 1 < p.w;
+    double* const yo0 = p.Yout + (int64_t)o0 * p.ldy + row_begin + g;
+    double* const yo1 = yo0 + p.ldy;
+    auto yrun = [&](auto nj_t) {
+      constexpr int NJ = decltype(nj_t)::value;
+      for (int64_t s = 0; s < nstage; ++s) {
+        const int pi = (int)(s & 1);
+        const unsigned ph = (unsigned)((s >> 1) & 1);
+        mbar_wait(&fullA[pi], ph);
+        const double* P = ring + (size_t)pi * (szA + szB);
+        const double* pq[4] = {P + aoff[0], P + aoff[1], P + aoff[2], P + aoff[3]};
+        double acc[4][2];
 #pragma unroll
-      for (int j = 0; j < FS_WR; ++j) {
-        if (j < nj) {
-          const int c = cbase + 4 * j;
+        for (int q = 0; q < 4; ++q) acc[q][0] = acc[q][1] = 0.0;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
           double a[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) a[q] = P[swzr<2>(c, (q >> 1) * 16 + (q & 1) * 8 + g)];
+          for (int q = 0; q < 4; ++q) a[q] = pq[q][128 * j];
 #pragma unroll
           for (int q = 0; q < 4; ++q) dmma884(acc[q][0], acc[q][1], a[q], wr[j]);
         }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&emptyA[pi]);
-      double* Ys = sY + (size_t)pi * YC * SR;
-      if (kp == 0) {
-        if (s >= 2 && fs.npy > 0) mbar_wait(&yfree[pi], ph ^ 1u);  // the tile warps are done with Y of stage s - 2
-      } else {
-        mbar_wait(&chain[(pi * 2 + cb) * 3 + kp - 1], ph);  // the partial sum of parts 0 .. kp - 1
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyA[pi]);
+        const int yb = (int)(s % FS_YB);
+        const unsigned yph = (unsigned)((s / FS_YB) & 1);
+        double* Ys = sY + (size_t)yb * YC * SR;
+        if (kp == 0) {
+          if (s >= FS_YB && fs.npy > 0) mbar_wait(&yfree[yb], yph ^ 1u);  // the tile warps are done with Y of stage s - FS_YB
+        } else {
+          mbar_wait(&chain[(yb * 2 + cb) * 3 + kp - 1], yph);  // the partial sum of parts 0 .. kp - 1
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            acc[q][0] = Ys[yoff[q][0]] + acc[q][0];
+            acc[q][1] = Ys[yoff[q][1]] + acc[q][1];
+          }
+        }
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int r = (q >> 1) * 16 + (q & 1) * 8 + g;
-          acc[q][0] = Ys[swzr<2>(o0, r)] + acc[q][0];
-          acc[q][1] = Ys[swzr<2>(o0 + 1, r)] + acc[q][1];
+          Ys[yoff[q][0]] = acc[q][0];
+          Ys[yoff[q][1]] = acc[q][1];
         }
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int r = (q >> 1) * 16 + (q & 1) * 8 + g;
-        Ys[swzr<2>(o0, r)] = acc[q][0];
-        Ys[swzr<2>(o0 + 1, r)] = acc[q][1];
-      }
-      if (!last) {
-        mbar_arrive(&chain[(pi * 2 + cb) * 3 + kp]);
-        continue;
-      }
-      mbar_arrive(&ydone[pi]);
-      if (p.Yout != nullptr) {
+        if (!last) {
+          mbar_arrive(&chain[(yb * 2 + cb) * 3 + kp]);
+          continue;
+        }
+        mbar_arrive(&ydone[yb]);
+        const int64_t r0 = s * SR;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int64_t row = row_begin + s * SR + 8 * q + g;
-          if (row >= row_end) continue;
-          if (o0 < p.w) p.Yout[(int64_t)o0 * p.ldy + row] = acc[q][0];
-          if (o0 + 1 < p.w) p.Yout[(int64_t)(o0 + 1) * p.ldy + row] = acc[q][1];
+          if (row_begin + r0 + 8 * q + g >= row_end) continue;
+          if (y0_ok) yo0[r0 + 8 * q] = acc[q][0];
+          if (y1_ok) yo1[r0 + 8 * q] = acc[q][1];
         }
       }
+    };
+    switch (nj) {
+#define PSVD_FS_NJ(N) case N: yrun(std::integral_constant<int, N>{}); break;
+      PSVD_FS_NJ(1) PSVD_FS_NJ(2) PSVD_FS_NJ(3) PSVD_FS_NJ(4) PSVD_FS_NJ(5) PSVD_FS_NJ(6) PSVD_FS_NJ(7)
+      PSVD_FS_NJ(8) PSVD_FS_NJ(9) PSVD_FS_NJ(10) PSVD_FS_NJ(11) PSVD_FS_NJ(12) PSVD_FS_NJ(13) PSVD_FS_NJ(14)
+      PSVD_FS_NJ(15) PSVD_FS_NJ(16) PSVD_FS_NJ(17) PSVD_FS_NJ(18) PSVD_FS_NJ(19)
+#undef PSVD_FS_NJ
+      default: yrun(std::integral_constant<int, FS_WR>{}); break;
     }
     return;
   }
@@ -936,10 +974,11 @@ __global__ void __launch_bounds__(NTHR, 1)
       for (int64_t s = 0; s < nstage; ++s) {
         const int pi = (int)(s & 1);
         const unsigned ph = (unsigned)((s >> 1) & 1);
+        const int yb = (int)(s % FS_YB);
         mbar_wait(&fullB[pi], ph);
-        mbar_wait(&ydone[pi], ph);
+        mbar_wait(&ydone[yb], (unsigned)((s / FS_YB) & 1));
         const double* Bp = ring + (size_t)pi * (szA + szB) + szA;
-        const double* Ys = sY + (size_t)pi * YC * SR;
+        const double* Ys = sY + (size_t)yb * YC * SR;
 #pragma unroll
         for (int kk = 0; kk < SR / 4; ++kk) {
           const int k = kk * 4 + tq;
@@ -961,7 +1000,7 @@ __global__ void __launch_bounds__(NTHR, 1)
               for (int c = 0; c < NCB; ++c) dmma884(accy[a][c][0], accy[a][c][1], fb[a], fb[c]);
           }
         }
-        mbar_arrive(&yfree[pi]);
+        mbar_arrive(&yfree[yb]);
         __syncwarp();
         if (lane == 0) mbar_arrive(&emptyB[pi]);
       }
@@ -1253,7 +1292,7 @@ int fused_split_prepare(const TallParams& p, const TmaExtra& x, const ReduceMap&
   memset(&fs, 0, sizeof(fs));
   memset(&offmap, 0, sizeof(offmap));
   if (!enc || p.nseg < 2 || p.nslices != 1 || x.pshift != 0 || p.w < 1 || x.kp_lo != 0 || p.M % TKS != 0 ||
-      (p.w_pad != 8 && p.w_pad != 16) || p.colmax != nullptr || p.gate != nullptr || p.dbg != 0 || p.wlo != 0)
+      (p.w_pad != 8 && p.w_pad != 16) || p.colmax != nullptr || p.gate != nullptr || (p.dbg != 0 && p.dbg != 2) || p.wlo != 0)
     return -1;
   const int last = p.nseg - 1;
   if (x.wrow0[last] != TMA_NOT_IN_W) return -1;
@@ -1468,7 +1507,10 @@ void launch_pass_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x
     pass_tma_kernel<2><<<grid, NTHR, smem, st>>>(q, maps, x);
     return;
   }
-  if (x.rb == 2) {
+  if (x.rb == 2 && p.w_pad <= 16) {
+    cudaFuncSetAttribute(pass_tma_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    pass_tma_kernel<2, true><<<grid, NTHR, smem, st>>>(p, maps, x);
+  } else if (x.rb == 2) {
     cudaFuncSetAttribute(pass_tma_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     pass_tma_kernel<2><<<grid, NTHR, smem, st>>>(p, maps, x);
   } else {
