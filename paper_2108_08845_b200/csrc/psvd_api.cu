@@ -849,7 +849,12 @@ int psvd_recompose(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, int Kc,
   }
   ps.p.Yout = U_out;
   ps.p.ldy = ldo;
-  if ((rc = run_pass(c, ps, st))) return rc;
+  // the split-ring kernel with group A alone (32-row 3-D boxes, W in registers) when the pass qualifies
+  if (UtU != nullptr && try_fused_split(c, ps, {}, 1)) {
+    if ((rc = run_fused_split(c, ps, st, nullptr))) return rc;
+  } else if ((rc = run_pass(c, ps, st))) {
+    return rc;
+  }
   if (UtU) {
     launch_extract_sym((const double*)c->tiles.ptr, ps.NB, ps.p.np_pad, K, nullptr, UtU, st);
     c->launches++;

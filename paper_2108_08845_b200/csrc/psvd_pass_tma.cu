@@ -650,6 +650,11 @@ __global__ void __launch_bounds__(NTHR, 1)
       for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
     const int I = wp.ti[0], J = wp.tj[0];
     const int nva = min(4, (p.np - I * 32 + 7) / 8), nvb = min(4, (p.np - J * 32 + 7) / 8);
+    // element (column 8 q + g, row 4 kk + tq) of a 16-row half is swz = 128 q + goff[kk] (the swizzle phase
+    // of a column is g whatever q): per-lane offsets, no address arithmetic per load
+    int goff[TKS / 4];
+#pragma unroll
+    for (int kk = 0; kk < TKS / 4; ++kk) goff[kk] = swz(g, kk * 4 + tq);
     uint32_t peer_empty = 0;
     if (MC) {
       const uint32_t loc = saddr(&empty[0]);
@@ -668,12 +673,11 @@ __global__ void __launch_bounds__(NTHR, 1)
           const double* bJ = H + (size_t)J * 32 * TKS;
 #pragma unroll
           for (int kk = 0; kk < TKS / 4; ++kk) {
-            const int k = kk * 4 + tq;
             double fa[NA], fb[NB];
 #pragma unroll
-            for (int q = 0; q < NA; ++q) fa[q] = bI[swz(q * 8 + g, k)];
+            for (int q = 0; q < NA; ++q) fa[q] = bI[goff[kk] + 128 * q];
 #pragma unroll
-            for (int q = 0; q < NB; ++q) fb[q] = bJ[swz(q * 8 + g, k)];
+            for (int q = 0; q < NB; ++q) fb[q] = bJ[goff[kk] + 128 * q];
 #pragma unroll
             for (int a = 0; a < NA; ++a)
 #pragma unroll
@@ -820,7 +824,7 @@ __global__ void __launch_bounds__(NTHR, 1)
       mbar_init(&fullA[b], 1);
       mbar_init(&fullB[b], 1);
       mbar_init(&emptyA[b], (unsigned)(NCB * FS_NKP));
-      mbar_init(&emptyB[b], (unsigned)max(fs.npy + fs.noff, 1));
+      mbar_init(&emptyB[b], (unsigned)max(fs.nB, 1));
     }
     for (int b = 0; b < FS_YB; ++b) {
       mbar_init(&ydone[b], 32u * NCB);
@@ -840,6 +844,11 @@ __global__ void __launch_bounds__(NTHR, 1)
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic accesses of the ring before the boxes
   __syncthreads();
   const int64_t nstage = row_end > row_begin ? (row_end - row_begin + SR - 1) / SR : 0;
+  // tile warps: element (column 8 b + g, row 4 kk + tq) of a 32-row stage is swzr<2> = 256 b + eoff[kk]:
+  // unit 16 b + 2 g + (kk >> 2), phase (2 g + (kk >> 2)) & 7 -- per-lane offsets, no arithmetic per load
+  int eoff[SR / 4];
+#pragma unroll
+  for (int kk = 0; kk < SR / 4; ++kk) eoff[kk] = swzr<2>(g, kk * 4 + tq);
 
   if (role == FS_PROD) {
     if (lane == 0) {
@@ -857,6 +866,7 @@ __global__ void __launch_bounds__(NTHR, 1)
             ++a;
           }
         }
+        if (fs.nopsB == 0) b = nstage;  // no group B (a recompose)
         if (b < nstage) {
           const int pi = (int)(b & 1);
           if (b < 2 || mbar_test(&emptyB[pi], (unsigned)(((b >> 1) - 1) & 1))) {
@@ -975,19 +985,18 @@ __global__ void __launch_bounds__(NTHR, 1)
         const int pi = (int)(s & 1);
         const unsigned ph = (unsigned)((s >> 1) & 1);
         const int yb = (int)(s % FS_YB);
-        mbar_wait(&fullB[pi], ph);
+        if (NA > 0) mbar_wait(&fullB[pi], ph);
         mbar_wait(&ydone[yb], (unsigned)((s / FS_YB) & 1));
-        const double* Bp = ring + (size_t)pi * (szA + szB) + szA;
+        const double* Bp = ring + (size_t)pi * (szA + szB) + szA + 256 * sb0;
         const double* Ys = sY + (size_t)yb * YC * SR;
 #pragma unroll
         for (int kk = 0; kk < SR / 4; ++kk) {
-          const int k = kk * 4 + tq;
           double fa[NAX], fb[NCB];
 #pragma unroll
-          for (int c = 0; c < NCB; ++c) fb[c] = Ys[swzr<2>(c * 8 + g, k)];
+          for (int c = 0; c < NCB; ++c) fb[c] = Ys[eoff[kk] + 256 * c];
           if (NA > 0) {
 #pragma unroll
-            for (int a = 0; a < NAX; ++a) fa[a] = Bp[swzr<2>((sb0 + a) * 8 + g, k)];
+            for (int a = 0; a < NAX; ++a) fa[a] = Bp[eoff[kk] + 256 * a];
 #pragma unroll
             for (int a = 0; a < NAX; ++a)
 #pragma unroll
@@ -1002,7 +1011,7 @@ __global__ void __launch_bounds__(NTHR, 1)
         }
         mbar_arrive(&yfree[yb]);
         __syncwarp();
-        if (lane == 0) mbar_arrive(&emptyB[pi]);
+        if (NA > 0 && lane == 0) mbar_arrive(&emptyB[pi]);
       }
       // full 32 x 32 slots (the fixed-order reduce sums every element): zeros where nothing was computed
 #pragma unroll
@@ -1069,14 +1078,15 @@ __global__ void __launch_bounds__(NTHR, 1)
         const int pi = (int)(s & 1);
         mbar_wait(&fullB[pi], (unsigned)((s >> 1) & 1));
         const double* Bp = ring + (size_t)pi * (szA + szB) + szA;
+        const double* bI = Bp + 1024 * I;
+        const double* bJ = Bp + 1024 * J;
 #pragma unroll
         for (int kk = 0; kk < SR / 4; ++kk) {
-          const int k = kk * 4 + tq;
           double fa[4], fb[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) fa[q] = Bp[swzr<2>(I * 32 + q * 8 + g, k)];
+          for (int q = 0; q < 4; ++q) fa[q] = bI[eoff[kk] + 256 * q];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) fb[q] = DIAG ? fa[q] : Bp[swzr<2>(J * 32 + q * 8 + g, k)];
+          for (int q = 0; q < 4; ++q) fb[q] = DIAG ? fa[q] : bJ[eoff[kk] + 256 * q];
 #pragma unroll
           for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -1291,19 +1301,22 @@ int fused_split_prepare(const TallParams& p, const TmaExtra& x, const ReduceMap&
   EncodeTiledFn enc = encode_fn();
   memset(&fs, 0, sizeof(fs));
   memset(&offmap, 0, sizeof(offmap));
-  if (!enc || p.nseg < 2 || p.nslices != 1 || x.pshift != 0 || p.w < 1 || x.kp_lo != 0 || p.M % TKS != 0 ||
+  if (!enc || p.nseg < 1 || p.nslices != 1 || x.pshift != 0 || p.w < 1 || x.kp_lo != 0 || p.M % TKS != 0 ||
       (p.w_pad != 8 && p.w_pad != 16) || p.colmax != nullptr || p.gate != nullptr || (p.dbg != 0 && p.dbg != 2) || p.wlo != 0)
     return -1;
-  const int last = p.nseg - 1;
-  if (x.wrow0[last] != TMA_NOT_IN_W) return -1;
+  // the last segment is group B unless W covers it too (a recompose: group A only, Y^T Y the one tile)
+  const bool hasB = x.wrow0[p.nseg - 1] == TMA_NOT_IN_W;
+  const int last = hasB ? p.nseg - 1 : p.nseg;
+  if (last < 1) return -1;
   for (int s = 0; s < last; ++s)
     if (x.wrow0[s] == TMA_NOT_IN_W || (p.seg[s].col0 & 7) != 0) return -1;
-  const int colB = p.seg[last].col0;
+  const int colB = hasB ? p.seg[last].col0 : 0;
   const int endA = p.seg[last - 1].col0 + p.seg[last - 1].ncols;
   fs.pwA = (endA + 7) / 8 * 8;
-  fs.pwB = (p.seg[last].ncols + 7) / 8 * 8;
+  fs.pwB = hasB ? (p.seg[last].ncols + 7) / 8 * 8 : 0;
   fs.ncb = p.w_pad / 8;
-  if ((colB & 31) != 0 || colB < fs.pwA || x.kp_hi > fs.pwA || p.seg[last].ncols > 256) return -1;
+  if (hasB && ((colB & 31) != 0 || colB < fs.pwA || p.seg[last].ncols > 256)) return -1;
+  if (x.kp_hi > fs.pwA) return -1;
   fs.n4 = x.kp_hi / 4;
   if (fs.n4 < FS_NKP || fs.n4 > FS_NKP * FS_WR) return -1;
   if (fused_split_smem_bytes(fs) > (size_t)(227 * 1024)) return -1;
@@ -1313,7 +1326,7 @@ int fused_split_prepare(const TallParams& p, const TmaExtra& x, const ReduceMap&
   for (int pass = 0; pass < 2; ++pass)
     for (int o = 0; o < x.nops; ++o) {
       const int m = x.op_seg[o], sidx = m % MAX_SEG;
-      if ((sidx == last) != (pass == 1)) continue;
+      if ((hasB && sidx == last) != (pass == 1)) continue;
       const int dst = x.op_pcol[o] - (pass == 1 ? colB : 0), bw = x.op_bw[o];
       if (dst < 0 || (dst & 7) != 0 || x.op_col[o] < 0 || dst + bw > (pass == 1 ? fs.pwB : fs.pwA)) return -1;
       fs.opm[n] = (short)m;
@@ -1347,7 +1360,7 @@ int fused_split_prepare(const TallParams& p, const TmaExtra& x, const ReduceMap&
     for (int i = 0; i < map.nsrc[o]; ++i)
       if (map.src[o][i] < SLOTS) used[map.src[o][i]] = 1;
   const int nsbB = fs.pwB / 8, ntB = (nsbB + 3) / 4;
-  if (map.nout != ntB + 1) return -1;
+  if (map.nout != ntB + 1) return -1;  // the planned tiles: A_next^T Y blocks and Y^T Y, nothing else
   const int yy_slot = slot_of(yblk, yblk);
   if (yy_slot < 0) return -1;
   fs.yy_slot = (unsigned char)yy_slot;
@@ -1360,11 +1373,11 @@ int fused_split_prepare(const TallParams& p, const TmaExtra& x, const ReduceMap&
     const int na = std::min(8, nsbB - 8 * i);
     items.push_back({FS_PY, na * fs.ncb * 8, 8 * i, na});
   }
-  bool yy_own = items.back().b > 4;
+  bool yy_own = items.empty() || items.back().b > 4;
   if (yy_own) items.push_back({FS_PY, fs.ncb * fs.ncb * 8, 0, 0});
   else items.back().cost += fs.ncb * fs.ncb * 8;
   const int yy_item = (int)items.size() - 1;
-  const int nfullB = p.seg[last].ncols / 32;
+  const int nfullB = hasB ? p.seg[last].ncols / 32 : 0;
   int noff_ok = 0;
   for (int i = 0; i < noff && noff_ok < FS_MAX_OFF; ++i) {
     const int I = off[i][0], J = off[i][1];
@@ -1466,6 +1479,7 @@ int fused_split_prepare(const TallParams& p, const TmaExtra& x, const ReduceMap&
       j += nj[kp];
     }
   }
+  for (int w = 0; w < NWARP; ++w) fs.nB += fs.role[w] == FS_OFF || (fs.role[w] == FS_PY && fs.py_na[w] > 0);
   offmap.nchunks = map.nchunks;
   offmap.nslices = 1;
   static const bool verbose = getenv("PSVD_PASS_VERBOSE") != nullptr;

@@ -136,7 +136,8 @@ struct FusedSplit {
   unsigned bytesA, bytesB;       // bytes per stage of each group
   int ncb;                       // Y column blocks (1 or 2)
   int n4;                        // k steps of 4 physical panel columns
-  int npy, noff;                 // warps with P^T Y tiles / offloaded Gram tiles
+  int npy, noff;                 // warps with P^T Y (or Y^T Y) tiles / offloaded Gram tiles
+  int nB;                        // warps that read group B (release its ring slots)
   unsigned char role[NWARP];
   unsigned char ycb[NWARP], ykp[NWARP], yj0[NWARP], ynj[NWARP];     // Y warps: column block, part, k steps
   unsigned char py_sb0[NWARP], py_na[NWARP], py_yy[NWARP];         // P^T Y warps: 8-column sub-blocks of slot B
