@@ -442,6 +442,10 @@ int run_pass(psvd_ctx* c, Pass& ps, cudaStream_t st) {
     for (int i = 0; i < ps.p.nseg; ++i)
       if (ps.p.seg[i].ptr == ps.p.Yout)
         return fail(c, PSVD_EINVAL, "in-place pass with %d slices would race", ps.p.nslices);
+  // narrow TMA passes go to the split-ring kernel when they qualify (32-row 3-D boxes, W in registers;
+  // psvd_tall.cuh: FusedSplit); passes planned with offloaded tiles are launched by their owners
+  if (ps.tma && !ps.fsplit) try_fused_split(c, ps, {}, 1);
+  if (ps.fsplit && ps.offmap.nout == 0) return run_fused_split(c, ps, st, nullptr);
   c->path_count[ps.tma ? 0 : ps.gtma ? 1 : ps.ws ? 2 : 3]++;
   if (ps.tma)
     launch_pass_tma(ps.p, ps.maps, ps.x, ps.grid, st);
@@ -472,7 +476,7 @@ int run_pass(psvd_ctx* c, Pass& ps, cudaStream_t st) {
 
 bool try_fused_split(psvd_ctx* c, Pass& ps, const std::vector<std::pair<int, int>>& off, int off_nb) {
   ps.fsplit = false;
-  static const bool disabled = getenv("PSVD_NO_FSPLIT") != nullptr;
+  static const bool disabled = getenv("PSVD_NO_FSPLIT") != nullptr;  // A/B switch: narrow TMA pass everywhere
   if (disabled || !ps.tma || c->num_sms < 1) return false;
   static const int fs_dbg = getenv("PSVD_FS_DBG") ? atoi(getenv("PSVD_FS_DBG")) : 0;  // timing diagnostics (wrong results)
   if (fs_dbg) ps.p.dbg = fs_dbg;
@@ -849,12 +853,7 @@ int psvd_recompose(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, int Kc,
   }
   ps.p.Yout = U_out;
   ps.p.ldy = ldo;
-  // the split-ring kernel with group A alone (32-row 3-D boxes, W in registers) when the pass qualifies
-  if (UtU != nullptr && try_fused_split(c, ps, {}, 1)) {
-    if ((rc = run_fused_split(c, ps, st, nullptr))) return rc;
-  } else if ((rc = run_pass(c, ps, st))) {
-    return rc;
-  }
+  if ((rc = run_pass(c, ps, st))) return rc;  // the split-ring kernel with group A alone when the pass qualifies
   if (UtU) {
     launch_extract_sym((const double*)c->tiles.ptr, ps.NB, ps.p.np_pad, K, nullptr, UtU, st);
     c->launches++;
@@ -886,8 +885,13 @@ int psvd_fused_pass(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, int Kc
     for (int t = 0; 2 * t + 1 < Bn / 32 && t < noff && off_tiles; ++t) off.push_back({2 * t, 2 * t + 1});
     if (!try_fused_split(c, pf, off, off_nb)) return fail(c, PSVD_EINVAL, "the pass does not qualify for the split-ring kernel");
     if ((rc = run_fused_split(c, pf, st, off_tiles))) return rc;
-  } else if ((rc = run_pass(c, pf, st))) {
-    return rc;
+  } else {  // mode 0: the narrow TMA pass itself (run_pass would pick the split-ring kernel)
+    if (!pf.tma) return fail(c, PSVD_EINVAL, "the pass does not plan as a narrow TMA pass");
+    c->path_count[0]++;
+    launch_pass_tma(pf.p, pf.maps, pf.x, pf.grid, st);
+    c->launches += 2;
+    if ((rc = cuda_check(c, "narrow fused pass"))) return rc;
+    launch_tall_reduce((const double*)pf.part->ptr, pf.map, (double*)pf.tl->ptr, st);
   }
   const int a0 = pf.p.seg[pf.p.nseg - 1].col0 / 32;
   launch_extract_sym((const double*)c->tiles.ptr, pf.NB, pf.p.np_pad, K, nullptr, UtU, st);

@@ -780,7 +780,7 @@ PSVD_DEV bool mbar_test(uint64_t* bar, unsigned parity) {
 constexpr int FS_YB = 2;  // Y ring depth: the Y warps run up to FS_YB stages ahead of the tile warps
 
 size_t fused_split_smem_bytes(const FusedSplit& fs) {
-  return 1024 + sizeof(double) * 2 * (size_t)(fs.pwA + fs.pwB) * 32 + sizeof(double) * FS_YB * 8 * (size_t)fs.ncb * 32 +
+  return 1024 + sizeof(double) * (size_t)fs.ns * (fs.pwA + fs.pwB) * 32 + sizeof(double) * FS_YB * 8 * (size_t)fs.ncb * 32 +
          64 * sizeof(uint64_t);
 }
 
@@ -796,16 +796,17 @@ __global__ void __launch_bounds__(NTHR, 1)
   const int64_t row_end = min(p.M, row_begin + p.rows_per_cta);
   unsigned char* base = smem_raw + ((1024 - (saddr(smem_raw) & 1023)) & 1023);
   const size_t szA = (size_t)fs.pwA * SR, szB = (size_t)fs.pwB * SR;  // doubles per slot
-  double* ring = reinterpret_cast<double*>(base);                     // [A0 | B0 | A1 | B1]
-  double* sY = ring + 2 * (szA + szB);                                // [FS_YB][YC columns][32 rows], swzr<2>
+  const int NS = fs.ns;                                               // slots per ring (2 .. FS_NS_MAX)
+  double* ring = reinterpret_cast<double*>(base);                     // [A0 | B0 | A1 | B1 | ...]
+  double* sY = ring + (size_t)NS * (szA + szB);                       // [FS_YB][YC columns][32 rows], swzr<2>
   uint64_t* bars = reinterpret_cast<uint64_t*>(sY + FS_YB * YC * SR);
-  uint64_t *fullA = bars, *emptyA = bars + 2, *fullB = bars + 4, *emptyB = bars + 6, *ydone = bars + 8,
-           *yfree = bars + 8 + FS_YB, *chain = bars + 8 + 2 * FS_YB;  // chain[(yb * 2 + cb) * 3 + link]
+  uint64_t *fullA = bars, *emptyA = bars + FS_NS_MAX, *fullB = bars + 2 * FS_NS_MAX, *emptyB = bars + 3 * FS_NS_MAX,
+           *ydone = bars + 4 * FS_NS_MAX, *yfree = ydone + FS_YB, *chain = yfree + FS_YB;  // chain[(yb * NCB + cb) * 3 + link]
   const int WSP = w_stride(YC);
   double* sW = ring;  // W staged through slot A0 before the first box lands there
 
   for (int i = tid; i < fs.n4 * 4 * WSP; i += NTHR) {
-    const int pc = i / WSP, o = i % WSP;  // physical panel column (kp_lo == 0), Y column
+    const int pc = fs.colA0 + i / WSP, o = i % WSP;  // physical panel column, Y column
     double v = 0.0;
     if (o < p.w) {
       for (int s = 0; s < p.nseg; ++s) {
@@ -820,17 +821,17 @@ __global__ void __launch_bounds__(NTHR, 1)
   }
   for (int i = tid; i < FS_YB * YC * SR; i += NTHR) sY[i] = 0.0;
   if (tid == 0) {
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NS; ++b) {
       mbar_init(&fullA[b], 1);
       mbar_init(&fullB[b], 1);
-      mbar_init(&emptyA[b], (unsigned)(NCB * FS_NKP));
+      mbar_init(&emptyA[b], (unsigned)max(fs.nA, 1));
       mbar_init(&emptyB[b], (unsigned)max(fs.nB, 1));
     }
     for (int b = 0; b < FS_YB; ++b) {
       mbar_init(&ydone[b], 32u * NCB);
       mbar_init(&yfree[b], (unsigned)max(32 * fs.npy, 1));
     }
-    for (int i = 0; i < FS_YB * 2 * 3; ++i) mbar_init(&chain[i], 32u);
+    for (int i = 0; i < FS_YB * NCB * 3; ++i) mbar_init(&chain[i], 32u);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -854,28 +855,32 @@ __global__ void __launch_bounds__(NTHR, 1)
     if (lane == 0) {
       // one lane feeds both rings: whichever group's slot is free gets its next stage
       int64_t a = 0, b = 0;
+      int pia = 0, pib = 0;       // ring positions of stages a and b
+      unsigned pha = 1, phb = 1;  // parity of the release that frees them: ((stage / NS) - 1) & 1
       while (a < nstage || b < nstage) {
         if (a < nstage) {
-          const int pi = (int)(a & 1);
-          if (a < 2 || mbar_test(&emptyA[pi], (unsigned)(((a >> 1) - 1) & 1))) {
+          const int pi = pia;
+          if (a < NS || mbar_test(&emptyA[pi], pha)) {
             mbar_expect_tx(&fullA[pi], p.dbg == 2 ? 0u : fs.bytesA);  // dbg 2: no loads (compute-only timing)
             double* dst = ring + (size_t)pi * (szA + szB);
             const int r16 = (int)((row_begin + a * SR) / TKS);
             for (int o = 0; o < (p.dbg == 2 ? 0 : fs.nopsA); ++o)
               tma_load_3d(dst + (size_t)fs.opd[o] * SR, &maps.m[fs.opm[o]], 0, r16, fs.opc[o], &fullA[pi]);
             ++a;
+            if (++pia == NS) pia = 0, pha ^= 1u;
           }
         }
         if (fs.nopsB == 0) b = nstage;  // no group B (a recompose)
         if (b < nstage) {
-          const int pi = (int)(b & 1);
-          if (b < 2 || mbar_test(&emptyB[pi], (unsigned)(((b >> 1) - 1) & 1))) {
+          const int pi = pib;
+          if (b < NS || mbar_test(&emptyB[pi], phb)) {
             mbar_expect_tx(&fullB[pi], p.dbg == 2 ? 0u : fs.bytesB);
             double* dst = ring + (size_t)pi * (szA + szB) + szA;
             const int r16 = (int)((row_begin + b * SR) / TKS);
             for (int o = fs.nopsA; o < (p.dbg == 2 ? 0 : fs.nopsA + fs.nopsB); ++o)
               tma_load_3d(dst + (size_t)fs.opd[o] * SR, &maps.m[fs.opm[o]], 0, r16, fs.opc[o], &fullB[pi]);
             ++b;
+            if (++pib == NS) pib = 0, phb ^= 1u;
           }
         }
       }
@@ -885,7 +890,7 @@ __global__ void __launch_bounds__(NTHR, 1)
 
   if (role == FS_Y) {
     const int cb = fs.ycb[warp], kp = fs.ykp[warp], j0 = fs.yj0[warp], nj = fs.ynj[warp];
-    const bool last = kp == FS_NKP - 1;
+    const bool last = kp == fs.nkp - 1;
     const int o0 = cb * 8 + 2 * tq;
     // element (column 4 (j0 + j) + tq, row 16 h + rr) of a stage is unit u = 8 (j0 + j) + 2 tq + h with
     // u & 7 = 2 tq + h whatever j: swzr<2> = a per-lane offset + 128 j, no address arithmetic per load
@@ -904,9 +909,9 @@ __global__ void __launch_bounds__(NTHR, 1)
     double* const yo1 = yo0 + p.ldy;
     auto yrun = [&](auto nj_t) {
       constexpr int NJ = decltype(nj_t)::value;
-      for (int64_t s = 0; s < nstage; ++s) {
-        const int pi = (int)(s & 1);
-        const unsigned ph = (unsigned)((s >> 1) & 1);
+      int pi = 0;
+      unsigned ph = 0;
+      for (int64_t s = 0; s < nstage; ++s, (++pi == NS ? (pi = 0, ph ^= 1u) : 0u)) {
         mbar_wait(&fullA[pi], ph);
         const double* P = ring + (size_t)pi * (szA + szB);
         const double* pq[4] = {P + aoff[0], P + aoff[1], P + aoff[2], P + aoff[3]};
@@ -929,7 +934,7 @@ __global__ void __launch_bounds__(NTHR, 1)
         if (kp == 0) {
           if (s >= FS_YB && fs.npy > 0) mbar_wait(&yfree[yb], yph ^ 1u);  // the tile warps are done with Y of stage s - FS_YB
         } else {
-          mbar_wait(&chain[(yb * 2 + cb) * 3 + kp - 1], yph);  // the partial sum of parts 0 .. kp - 1
+          mbar_wait(&chain[(yb * NCB + cb) * 3 + kp - 1], yph);  // the partial sum of parts 0 .. kp - 1
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             acc[q][0] = Ys[yoff[q][0]] + acc[q][0];
@@ -942,7 +947,7 @@ __global__ void __launch_bounds__(NTHR, 1)
           Ys[yoff[q][1]] = acc[q][1];
         }
         if (!last) {
-          mbar_arrive(&chain[(yb * 2 + cb) * 3 + kp]);
+          mbar_arrive(&chain[(yb * NCB + cb) * 3 + kp]);
           continue;
         }
         mbar_arrive(&ydone[yb]);
@@ -968,6 +973,11 @@ __global__ void __launch_bounds__(NTHR, 1)
 
   if (role == FS_PY) {
     const int sb0 = fs.py_sb0[warp];
+    // the group whose slots this warp's sub-blocks live in (A: e.g. Q^T Y of a projection pass)
+    const bool onA = fs.py_onA[warp] != 0;
+    uint64_t* const fullX = onA ? fullA : fullB;
+    uint64_t* const emptyX = onA ? emptyA : emptyB;
+    const size_t xoff = (onA ? 0 : szA) + 256 * (size_t)sb0;
     auto run = [&](auto na_t, auto yy_t) {
       constexpr int NA = decltype(na_t)::value;
       constexpr bool YY = decltype(yy_t)::value;
@@ -981,13 +991,13 @@ __global__ void __launch_bounds__(NTHR, 1)
       for (int a = 0; a < NCB; ++a)
 #pragma unroll
         for (int c = 0; c < NCB; ++c) accy[a][c][0] = accy[a][c][1] = 0.0;
-      for (int64_t s = 0; s < nstage; ++s) {
-        const int pi = (int)(s & 1);
-        const unsigned ph = (unsigned)((s >> 1) & 1);
+      int pi = 0;
+      unsigned ph = 0;
+      for (int64_t s = 0; s < nstage; ++s, (++pi == NS ? (pi = 0, ph ^= 1u) : 0u)) {
         const int yb = (int)(s % FS_YB);
-        if (NA > 0) mbar_wait(&fullB[pi], ph);
+        if (NA > 0) mbar_wait(&fullX[pi], ph);
         mbar_wait(&ydone[yb], (unsigned)((s / FS_YB) & 1));
-        const double* Bp = ring + (size_t)pi * (szA + szB) + szA + 256 * sb0;
+        const double* Bp = ring + (size_t)pi * (szA + szB) + xoff;
         const double* Ys = sY + (size_t)yb * YC * SR;
 #pragma unroll
         for (int kk = 0; kk < SR / 4; ++kk) {
@@ -1011,21 +1021,31 @@ __global__ void __launch_bounds__(NTHR, 1)
         }
         mbar_arrive(&yfree[yb]);
         __syncwarp();
-        if (NA > 0 && lane == 0) mbar_arrive(&emptyB[pi]);
+        if (NA > 0 && lane == 0) mbar_arrive(&emptyX[pi]);
       }
-      // full 32 x 32 slots (the fixed-order reduce sums every element): zeros where nothing was computed
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        if (t * 4 >= NA) continue;
+      // full 32 x 32 slots (the fixed-order reduce sums every element): sub-block a lands in row block
+      // (rb0 + a) & 3 of the warp's tile (rb0 + a) >> 2, zeros everywhere else
+      const int rb0 = fs.py_rb0[warp], nt = fs.py_nt[warp];
+      for (int t = 0; t < nt; ++t) {
         double* dst = p.partial + ((size_t)blockIdx.x * SLOTS + fs.py_slot[warp][t]) * 1024;
+        for (int rb = 0; rb < 4; ++rb) {
+          const int a = 4 * t + rb - rb0;
+          if (a >= 0 && a < NA) continue;  // written below
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+          for (int c = 0; c < 4; ++c)
+            *reinterpret_cast<double2*>(dst + (rb * 8 + g) * 32 + c * 8 + 2 * tq) = make_double2(0.0, 0.0);
+        }
+      }
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            double v0 = 0.0, v1 = 0.0;
-            if (t * 4 + a < NA && c < NCB) v0 = acc[(t * 4 + a) % NAX][c % NCB][0], v1 = acc[(t * 4 + a) % NAX][c % NCB][1];
-            *reinterpret_cast<double2*>(dst + (a * 8 + g) * 32 + c * 8 + 2 * tq) = make_double2(v0, v1);
-          }
+      for (int a = 0; a < NA; ++a) {
+        double* dst = p.partial + ((size_t)blockIdx.x * SLOTS + fs.py_slot[warp][(rb0 + a) >> 2]) * 1024;
+        const int rb = (rb0 + a) & 3;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          double v0 = 0.0, v1 = 0.0;
+          if (c < NCB) v0 = acc[a % NAX][c % NCB][0], v1 = acc[a % NAX][c % NCB][1];
+          *reinterpret_cast<double2*>(dst + (rb * 8 + g) * 32 + c * 8 + 2 * tq) = make_double2(v0, v1);
+        }
       }
       if (YY) {
         double* dst = p.partial + ((size_t)blockIdx.x * SLOTS + fs.yy_slot) * 1024;
@@ -1057,9 +1077,13 @@ __global__ void __launch_bounds__(NTHR, 1)
         case 3: run(std::integral_constant<int, 3>{}, F{}); break;
         case 4: run(std::integral_constant<int, 4>{}, F{}); break;
         case 5: run(std::integral_constant<int, 5>{}, F{}); break;
-        case 6: run(std::integral_constant<int, 6>{}, F{}); break;
-        case 7: run(std::integral_constant<int, 7>{}, F{}); break;
-        default: run(std::integral_constant<int, 8>{}, F{}); break;
+        default:  // 6 .. 8 sub-blocks: one or two Y column blocks only (the accumulators of three would not fit)
+          if constexpr (NCB <= 2) {
+            if (na == 6) run(std::integral_constant<int, 6>{}, F{});
+            else if (na == 7) run(std::integral_constant<int, 7>{}, F{});
+            else run(std::integral_constant<int, 8>{}, F{});
+          }
+          break;
       }
     }
     return;
@@ -1074,9 +1098,10 @@ __global__ void __launch_bounds__(NTHR, 1)
       for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
     auto run = [&](auto diag_t) {
       constexpr bool DIAG = decltype(diag_t)::value;
-      for (int64_t s = 0; s < nstage; ++s) {
-        const int pi = (int)(s & 1);
-        mbar_wait(&fullB[pi], (unsigned)((s >> 1) & 1));
+      int pi = 0;
+      unsigned ph = 0;
+      for (int64_t s = 0; s < nstage; ++s, (++pi == NS ? (pi = 0, ph ^= 1u) : 0u)) {
+        mbar_wait(&fullB[pi], ph);
         const double* Bp = ring + (size_t)pi * (szA + szB) + szA;
         const double* bI = Bp + 1024 * I;
         const double* bJ = Bp + 1024 * J;
@@ -1111,7 +1136,10 @@ __global__ void __launch_bounds__(NTHR, 1)
 void launch_fused_split(const TallParams& p, const TmaMaps& maps3, const TmaExtra& x, const FusedSplit& fs, int grid,
                         cudaStream_t st) {
   const size_t smem = fused_split_smem_bytes(fs);
-  if (fs.ncb == 2) {
+  if (fs.ncb == 3) {
+    cudaFuncSetAttribute(fused_split_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    fused_split_kernel<3><<<grid, NTHR, smem, st>>>(p, maps3, x, fs);
+  } else if (fs.ncb == 2) {
     cudaFuncSetAttribute(fused_split_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     fused_split_kernel<2><<<grid, NTHR, smem, st>>>(p, maps3, x, fs);
   } else {
@@ -1291,50 +1319,77 @@ int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift, bool
   return 0;
 }
 
-// Split-ring fused pass: qualifies a planned narrow TMA pass (p, x: tma_pass_prepare's box list; map: its
-// reduce map with NB tile columns) and builds the warp roles, the k split and the 3-D tensor maps.
-// off[i] = {I, J}: 32-column block pairs of the last segment's Gram to compute here (full blocks
-// only, I <= J), reduced by offmap into a tile array with off_nb tile columns.  Returns 0 when the
-// pass runs on fused_split_kernel, -1 when it has to stay on pass_tma_kernel.
-int fused_split_prepare(const TallParams& p, const TmaExtra& x, const ReduceMap& map, int NB, const int (*off)[2],
+// Split-ring pass: qualifies a planned narrow TMA pass (p, x: tma_pass_prepare's box list; map: its reduce
+// map with NB tile columns, replaced by the split kernel's own on success) and builds the warp roles, the k
+// split and the 3-D tensor maps.  Group A = the segments W covers (contiguous), group B = the others (all
+// before or all after group A; none for a recompose).  The wanted tiles come from the plan: (I, Y) for the
+// 8-column sub-blocks the plan kept, (Y, Y).  off[i] = {I, J}: 32-column block pairs of group B's (single)
+// segment whose Gram tile is computed here (full blocks only, I <= J), reduced by offmap into a tile array
+// with off_nb tile columns.  Returns 0 when the pass runs on fused_split_kernel, -1 when it stays on
+// pass_tma_kernel.
+int fused_split_prepare(const TallParams& p, const TmaExtra& x, ReduceMap& map, int NB, const int (*off)[2],
                         int noff, FusedSplit& fs, TmaMaps& maps3, ReduceMap& offmap, int off_nb) {
   EncodeTiledFn enc = encode_fn();
   memset(&fs, 0, sizeof(fs));
   memset(&offmap, 0, sizeof(offmap));
-  if (!enc || p.nseg < 1 || p.nslices != 1 || x.pshift != 0 || p.w < 1 || x.kp_lo != 0 || p.M % TKS != 0 ||
-      (p.w_pad != 8 && p.w_pad != 16) || p.colmax != nullptr || p.gate != nullptr || (p.dbg != 0 && p.dbg != 2) || p.wlo != 0)
+  if (!enc || p.nseg < 1 || p.nslices != 1 || x.pshift != 0 || p.w < 1 || p.M % TKS != 0 ||
+      (p.w_pad != 8 && p.w_pad != 16 && p.w_pad != 24) || p.colmax != nullptr || p.gate != nullptr ||
+      (p.dbg != 0 && p.dbg != 2))
     return -1;
-  // the last segment is group B unless W covers it too (a recompose: group A only, Y^T Y the one tile)
-  const bool hasB = x.wrow0[p.nseg - 1] == TMA_NOT_IN_W;
-  const int last = hasB ? p.nseg - 1 : p.nseg;
-  if (last < 1) return -1;
-  for (int s = 0; s < last; ++s)
-    if (x.wrow0[s] == TMA_NOT_IN_W || (p.seg[s].col0 & 7) != 0) return -1;
-  const int colB = hasB ? p.seg[last].col0 : 0;
-  const int endA = p.seg[last - 1].col0 + p.seg[last - 1].ncols;
-  fs.pwA = (endA + 7) / 8 * 8;
-  fs.pwB = hasB ? (p.seg[last].ncols + 7) / 8 * 8 : 0;
+  // groups
+  int a0s = -1, a1s = -1, b0s = -1, b1s = -1;
+  for (int s = 0; s < p.nseg; ++s) {
+    if ((p.seg[s].col0 & 7) != 0) return -1;
+    if (x.wrow0[s] != TMA_NOT_IN_W) {
+      if (a0s < 0) a0s = s;
+      else if (a1s != s - 1) return -1;  // W's segments are contiguous
+      a1s = s;
+    } else {
+      if (b0s < 0) b0s = s;
+      else if (b1s != s - 1) return -1;  // and so are the others: all before or all after group A
+      b1s = s;
+    }
+  }
+  if (a0s < 0) return -1;
+  const bool hasB = b0s >= 0;
+  const int colA0 = p.seg[a0s].col0, endA = p.seg[a1s].col0 + p.seg[a1s].ncols;
+  const int colB0 = hasB ? p.seg[b0s].col0 : 0, endB = hasB ? p.seg[b1s].col0 + p.seg[b1s].ncols : 0;
+  fs.colA0 = colA0;
+  fs.pwA = (endA - colA0 + 7) / 8 * 8;
+  fs.pwB = hasB ? (endB - colB0 + 7) / 8 * 8 : 0;
   fs.ncb = p.w_pad / 8;
-  if (hasB && ((colB & 31) != 0 || colB < fs.pwA || p.seg[last].ncols > 256)) return -1;
-  if (x.kp_hi > fs.pwA) return -1;
-  fs.n4 = x.kp_hi / 4;
-  if (fs.n4 < FS_NKP || fs.n4 > FS_NKP * FS_WR) return -1;
+  if (hasB && !(colB0 >= colA0 + fs.pwA || colA0 >= colB0 + fs.pwB)) return -1;
+  if (x.kp_lo != colA0 || x.kp_hi > colA0 + fs.pwA || fs.pwA > 256 + 8 || fs.pwB > 256 + 8) return -1;
+  fs.n4 = (x.kp_hi - x.kp_lo) / 4;
+  fs.nkp = fs.n4 > 24 ? 4 : fs.n4 > 12 ? 2 : 1;
+  if (fs.n4 < 1 || fs.n4 > fs.nkp * FS_WR) return -1;
+  fs.ns = 2;
   if (fused_split_smem_bytes(fs) > (size_t)(227 * 1024)) return -1;
+  static const int ns_cap = getenv("PSVD_FS_NS") ? std::max(2, std::min(FS_NS_MAX, atoi(getenv("PSVD_FS_NS")))) : FS_NS_MAX;
+  while (fs.ns < ns_cap) {  // as many slots per ring as shared memory holds
+    fs.ns++;
+    if (fused_split_smem_bytes(fs) > (size_t)(227 * 1024)) {
+      fs.ns--;
+      break;
+    }
+  }
+  if ((size_t)fs.n4 * 4 * w_stride(p.w_pad) > (size_t)fs.pwA * 32) return -1;  // W is staged through slot A0
   // boxes: group A first, then group B; every 8-column block of both slots must be covered
   std::vector<char> covA(fs.pwA / 8, 0), covB(fs.pwB / 8, 0);
   int n = 0;
   for (int pass = 0; pass < 2; ++pass)
     for (int o = 0; o < x.nops; ++o) {
       const int m = x.op_seg[o], sidx = m % MAX_SEG;
-      if ((hasB && sidx == last) != (pass == 1)) continue;
-      const int dst = x.op_pcol[o] - (pass == 1 ? colB : 0), bw = x.op_bw[o];
-      if (dst < 0 || (dst & 7) != 0 || x.op_col[o] < 0 || dst + bw > (pass == 1 ? fs.pwB : fs.pwA)) return -1;
+      const bool inB = x.wrow0[sidx] == TMA_NOT_IN_W;
+      if (inB != (pass == 1)) continue;
+      const int dst = x.op_pcol[o] - (inB ? colB0 : colA0), bw = x.op_bw[o];
+      if (dst < 0 || (dst & 7) != 0 || x.op_col[o] < 0 || dst + bw > (inB ? fs.pwB : fs.pwA)) return -1;
       fs.opm[n] = (short)m;
       fs.opc[n] = x.op_col[o];
       fs.opd[n] = (short)dst;
-      for (int q = dst / 8; q < (dst + bw) / 8; ++q) (pass == 1 ? covB : covA)[q] = 1;
-      (pass == 1 ? fs.bytesB : fs.bytesA) += (unsigned)(2 * TKS * bw * sizeof(double));
-      (pass == 1 ? fs.nopsB : fs.nopsA)++;
+      for (int q = dst / 8; q < (dst + bw) / 8; ++q) (inB ? covB : covA)[q] = 1;
+      (inB ? fs.bytesB : fs.bytesA) += (unsigned)(2 * TKS * bw * sizeof(double));
+      (inB ? fs.nopsB : fs.nopsA)++;
       const Seg& sg = p.seg[sidx];
       cuuint64_t dims[3] = {(cuuint64_t)TKS, (cuuint64_t)(p.M / TKS), (cuuint64_t)sg.ncols};
       cuuint64_t strides[2] = {(cuuint64_t)TKS * sizeof(double), (cuuint64_t)sg.ld * sizeof(double)};
@@ -1348,147 +1403,225 @@ int fused_split_prepare(const TallParams& p, const TmaExtra& x, const ReduceMap&
     }
   for (char c : covA) if (!c) return -1;
   for (char c : covB) if (!c) return -1;
-  // output slots of the planned tiles: (colB / 32 + t, Y block) and (Y block, Y block)
+  // the planned tiles: (I, Y block) with the plan's wanted 8-column sub-blocks, and (Y block, Y block)
   const int yblk = p.np_pad / 32;
-  auto slot_of = [&](int I, int J) {
-    for (int o = 0; o < map.nout; ++o)
-      if (map.out_id[o] == I * NB + J && map.nsrc[o] == 1 && map.src[o][0] < SLOTS) return (int)map.src[o][0];
-    return -1;
-  };
-  std::vector<char> used(SLOTS, 0);
-  for (int o = 0; o < map.nout; ++o)
-    for (int i = 0; i < map.nsrc[o]; ++i)
-      if (map.src[o][i] < SLOTS) used[map.src[o][i]] = 1;
-  const int nsbB = fs.pwB / 8, ntB = (nsbB + 3) / 4;
-  if (map.nout != ntB + 1) return -1;  // the planned tiles: A_next^T Y blocks and Y^T Y, nothing else
-  const int yy_slot = slot_of(yblk, yblk);
-  if (yy_slot < 0) return -1;
-  fs.yy_slot = (unsigned char)yy_slot;
-  // fixed items: P^T Y warps of up to 8 sub-blocks, Y^T Y on the lightest of them when it has <= 4
-  // sub-blocks (else a warp of its own), offloaded tiles, the producer
-  struct Item { int kind, cost, a, b; };
-  std::vector<Item> items;
-  const int npyw = (nsbB + 7) / 8;
-  for (int i = 0; i < npyw; ++i) {
-    const int na = std::min(8, nsbB - 8 * i);
-    items.push_back({FS_PY, na * fs.ncb * 8, 8 * i, na});
+  if (NB != yblk + 1) return -1;
+  std::vector<int> wantA, wantB;  // slot-relative sub-blocks
+  bool has_yy = false;
+  for (int w = 0; w < NWARP; ++w) {
+    const WarpPlan& wp = p.plan[0][w];
+    if (wp.ntile == 0) continue;
+    const int I = wp.ti[0], J = wp.tj[0];
+    if (wp.ntile != 1 || J != yblk) return -1;
+    if (I == yblk) { has_yy = true; continue; }
+    if (I > yblk) return -1;
+    const int s0 = wp.sub != 0 ? (wp.sub & 15) : 0;
+    const int na = wp.sub != 0 ? (wp.sub >> 4) : std::min(4, (p.np - I * 32 + 7) / 8);
+    for (int a = 0; a < na; ++a) {
+      const int col = (4 * I + s0 + a) * 8;
+      if (col >= colA0 && col < colA0 + fs.pwA) wantA.push_back((col - colA0) / 8);
+      else if (hasB && col >= colB0 && col < colB0 + fs.pwB) wantB.push_back((col - colB0) / 8);
+      else return -1;
+    }
   }
-  bool yy_own = items.empty() || items.back().b > 4;
-  if (yy_own) items.push_back({FS_PY, fs.ncb * fs.ncb * 8, 0, 0});
-  else items.back().cost += fs.ncb * fs.ncb * 8;
-  const int yy_item = (int)items.size() - 1;
-  const int nfullB = hasB ? p.seg[last].ncols / 32 : 0;
-  int noff_ok = 0;
-  for (int i = 0; i < noff && noff_ok < FS_MAX_OFF; ++i) {
-    const int I = off[i][0], J = off[i][1];
-    if (I < 0 || I > J || J >= nfullB) continue;
-    items.push_back({FS_OFF, (I == J ? 10 : 16) * 8, I, J});
-    ++noff_ok;
-  }
-  items.push_back({FS_PROD, 0, 0, 0});
-  const int nyw = fs.ncb * FS_NKP;
-  if ((int)items.size() + nyw > NWARP) return -1;
-  // longest first onto the least-loaded SMSP (warp w issues on SMSP w % 4) with a free slot
-  std::vector<int> order(items.size());
-  for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
-  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return items[a].cost > items[b].cost; });
-  int load[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
-  int free_slot = 0;
-  for (int it : order) {
-    int q = -1;
-    for (int c = 0; c < 4; ++c)
-      if (cnt[c] < 4 && (q < 0 || load[c] < load[q] || (load[c] == load[q] && cnt[c] < cnt[q]))) q = c;
-    const int w = q + 4 * cnt[q];
-    cnt[q]++;
-    load[q] += items[it].cost;
-    const Item& im = items[it];
-    fs.role[w] = (unsigned char)im.kind;
-    if (im.kind == FS_PY) {
-      fs.py_sb0[w] = (unsigned char)im.a;
-      fs.py_na[w] = (unsigned char)im.b;
-      fs.py_yy[w] = (unsigned char)(it == yy_item);
-      for (int t = 0; t < 2 && 4 * t < im.b; ++t) {
-        const int sl = slot_of(colB / 32 + im.a / 4 + t, yblk);
-        if (sl < 0) return -1;
-        fs.py_slot[w][t] = (unsigned char)sl;
+  if (!has_yy) return -1;
+  std::sort(wantA.begin(), wantA.end());
+  std::sort(wantB.begin(), wantB.end());
+  // Roles are built for every chunk size of the tile warps (namax sub-blocks per warp, up to what the
+  // accumulators allow) and the one with the lightest busiest SMSP is kept
+  const FusedSplit fs0 = fs;
+  ReduceMap nm;
+  auto build = [&](int namax, bool yy_own, FusedSplit& fs, ReduceMap& nm, ReduceMap& offmap) -> double {
+    memset(&nm, 0, sizeof(nm));
+    memset(&offmap, 0, sizeof(offmap));
+    // fixed items: tile warps over runs of wanted sub-blocks, Y^T Y on the lightest of them when its
+    // accumulators fit (else a warp of its own), offloaded tiles, the producer
+    struct Item { int kind, cost, sb0, na, onA, I, J; };
+    std::vector<Item> items;
+    auto add_runs = [&](const std::vector<int>& want, int onA) {
+      size_t i = 0;
+      while (i < want.size()) {
+        size_t j = i + 1;
+        while (j < want.size() && want[j] == want[j - 1] + 1) ++j;
+        // a run of wanted sub-blocks, cut into chunks of namax (the remainder last: it can carry Y^T Y)
+        const int len = (int)(j - i);
+        for (int lo = 0; lo < len; lo += namax) {
+          const int hi = std::min(len, lo + namax);
+          items.push_back({FS_PY, (hi - lo) * fs.ncb * 8, want[i] + lo, hi - lo, onA, 0, 0});
+        }
+        i = j;
       }
-      fs.npy++;
-    } else if (im.kind == FS_OFF) {
-      while (free_slot < SLOTS && used[free_slot]) ++free_slot;
-      if (free_slot >= SLOTS) return -1;
-      used[free_slot] = 1;
-      fs.off_i[w] = (unsigned char)im.a;
-      fs.off_j[w] = (unsigned char)im.b;
-      fs.off_slot[w] = (unsigned char)free_slot;
-      const int o = offmap.nout++;
-      offmap.out_id[o] = (short)(im.a * off_nb + im.b);
-      offmap.nsrc[o] = 1;
-      offmap.src[o][0] = (unsigned char)free_slot;
+    };
+    add_runs(wantB, 0);
+    add_runs(wantA, 1);
+    int yy_item = -1;
+    for (size_t i = 0; i < items.size() && !yy_own; ++i)
+      if (items[i].na <= 4 && items[i].na * fs.ncb + fs.ncb * fs.ncb <= 18 &&
+          (yy_item < 0 || items[i].na < items[yy_item].na))
+        yy_item = (int)i;
+    if (yy_item < 0) {
+      items.push_back({FS_PY, 0, 0, 0, 1, 0, 0});
+      yy_item = (int)items.size() - 1;
+    }
+    items[yy_item].cost += fs.ncb * fs.ncb * 8;
+    const int nfullB = (hasB && b0s == b1s) ? p.seg[b0s].ncols / 32 : 0;
+    for (int i = 0; i < noff && fs.noff < FS_MAX_OFF; ++i) {
+      const int I = off[i][0], J = off[i][1];
+      if (I < 0 || I > J || J >= nfullB) continue;
+      items.push_back({FS_OFF, (I == J ? 10 : 16) * 8, 0, 0, 0, I, J});
       fs.noff++;
     }
-  }
-  // Y warps take the remaining slots; column blocks alternate so that each gets FS_NKP parts
-  std::vector<int> yw;
-  for (int i = 0; i < 4; ++i)
-    for (int q = 0; q < 4; ++q)
-      if (i >= cnt[q] && (int)yw.size() < nyw) yw.push_back(q + 4 * i);
-  if ((int)yw.size() != nyw) return -1;
-  std::sort(yw.begin(), yw.end(), [](int a, int b) { return a % 4 != b % 4 ? a % 4 < b % 4 : a < b; });
-  int ywarps[4] = {0, 0, 0, 0};
-  for (int w : yw) ywarps[w % 4]++;
-  const double target = (load[0] + load[1] + load[2] + load[3] + 4.0 * fs.n4 * fs.ncb) / 4.0;
-  std::vector<int> kpn(fs.ncb, 0);
-  std::vector<std::vector<int>> wcb(fs.ncb);
-  for (size_t i = 0; i < yw.size(); ++i) wcb[i % fs.ncb].push_back(yw[i]);
-  for (int cb = 0; cb < fs.ncb; ++cb) {
-    // a part's weight: what its SMSP has left of the even share, split over the Y warps issuing there
-    std::vector<double> wgt(FS_NKP);
-    double sum = 0.0;
-    for (int kp = 0; kp < FS_NKP; ++kp) {
-      const int q = wcb[cb][kp] % 4;
-      wgt[kp] = std::max(4.0, (target - load[q]) / std::max(1, ywarps[q]));
-      sum += wgt[kp];
-    }
-    std::vector<int> nj(FS_NKP);
-    int tot = 0;
-    for (int kp = 0; kp < FS_NKP; ++kp) {
-      nj[kp] = std::max(1, std::min(FS_WR, (int)(fs.n4 * wgt[kp] / sum + 0.5)));
-      tot += nj[kp];
-    }
-    for (int guard = 0; tot != fs.n4 && guard < 1000; ++guard) {  // fix the rounding, heaviest weights first
-      int best = -1;
-      for (int kp = 0; kp < FS_NKP; ++kp) {
-        if (tot < fs.n4 && nj[kp] >= FS_WR) continue;
-        if (tot > fs.n4 && nj[kp] <= 1) continue;
-        if (best < 0 || (tot < fs.n4 ? wgt[kp] / nj[kp] > wgt[best] / nj[best] : wgt[kp] / nj[kp] < wgt[best] / nj[best]))
-          best = kp;
+    items.push_back({FS_PROD, 0, 0, 0, 0, 0, 0});
+    const int nyw = fs.ncb * fs.nkp;
+    if ((int)items.size() + nyw > NWARP) return -1.0;
+    // longest first onto the least-loaded SMSP (warp w issues on SMSP w % 4) with a free slot
+    std::vector<int> order(items.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = (int)i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return items[a].cost > items[b].cost; });
+    int load[4] = {0, 0, 0, 0}, cnt[4] = {0, 0, 0, 0};
+    int next_slot = 0;
+    auto add_src = [&](int out_id, int slot) {
+      int o = 0;
+      while (o < nm.nout && nm.out_id[o] != out_id) ++o;
+      if (o == nm.nout) {
+        if (nm.nout >= MAX_OUT_TILES) return false;
+        nm.out_id[nm.nout++] = (short)out_id;
       }
-      if (best < 0) return -1;
-      nj[best] += tot < fs.n4 ? 1 : -1;
-      tot += tot < fs.n4 ? 1 : -1;
+      if (nm.nsrc[o] >= NWARP) return false;
+      nm.src[o][nm.nsrc[o]++] = (unsigned char)slot;
+      return true;
+    };
+    for (int it : order) {
+      int q = -1;
+      for (int c = 0; c < 4; ++c)
+        if (cnt[c] < 4 && (q < 0 || load[c] < load[q] || (load[c] == load[q] && cnt[c] < cnt[q]))) q = c;
+      if (q < 0) return -1.0;
+      const int w = q + 4 * cnt[q];
+      cnt[q]++;
+      load[q] += items[it].cost;
+      const Item& im = items[it];
+      fs.role[w] = (unsigned char)im.kind;
+      if (im.kind == FS_PY) {
+        const int g0 = ((im.onA ? colA0 : colB0) / 8) + im.sb0;  // global sub-block of the first one
+        fs.py_sb0[w] = (unsigned char)im.sb0;
+        fs.py_na[w] = (unsigned char)im.na;
+        fs.py_onA[w] = (unsigned char)im.onA;
+        fs.py_rb0[w] = (unsigned char)(g0 & 3);
+        fs.py_yy[w] = (unsigned char)(it == yy_item);
+        const int nt = im.na > 0 ? (g0 + im.na - 1) / 4 - g0 / 4 + 1 : 0;
+        if (nt > 3) return -1.0;
+        fs.py_nt[w] = (unsigned char)nt;
+        for (int t = 0; t < nt; ++t) {
+          if (next_slot >= SLOTS || !add_src((g0 / 4 + t) * NB + yblk, next_slot)) return -1.0;
+          fs.py_slot[w][t] = (unsigned char)next_slot++;
+        }
+        if (it == yy_item) {
+          if (next_slot >= SLOTS || !add_src(yblk * NB + yblk, next_slot)) return -1.0;
+          fs.yy_slot = (unsigned char)next_slot++;
+        }
+        fs.npy++;
+        if (im.na > 0) (im.onA ? fs.nA : fs.nB)++;
+      } else if (im.kind == FS_OFF) {
+        if (next_slot >= SLOTS) return -1.0;
+        fs.off_i[w] = (unsigned char)im.I;
+        fs.off_j[w] = (unsigned char)im.J;
+        fs.off_slot[w] = (unsigned char)next_slot;
+        const int o = offmap.nout++;
+        offmap.out_id[o] = (short)(im.I * off_nb + im.J);
+        offmap.nsrc[o] = 1;
+        offmap.src[o][0] = (unsigned char)next_slot++;
+        fs.nB++;
+      }
     }
-    if (tot != fs.n4) return -1;
-    int j = 0;
-    for (int kp = 0; kp < FS_NKP; ++kp) {
-      const int w = wcb[cb][kp];
-      fs.role[w] = FS_Y;
-      fs.ycb[w] = (unsigned char)cb;
-      fs.ykp[w] = (unsigned char)kp;
-      fs.yj0[w] = (unsigned char)j;
-      fs.ynj[w] = (unsigned char)nj[kp];
-      j += nj[kp];
+    fs.nA += nyw;
+    // Y warps take the remaining slots; column blocks alternate so that each gets nkp parts
+    std::vector<int> yw;
+    for (int i = 0; i < 4; ++i)
+      for (int q = 0; q < 4; ++q)
+        if (i >= cnt[q] && (int)yw.size() < nyw) yw.push_back(q + 4 * i);
+    if ((int)yw.size() != nyw) return -1.0;
+    std::sort(yw.begin(), yw.end(), [](int a, int b) { return a % 4 != b % 4 ? a % 4 < b % 4 : a < b; });
+    int ywarps[4] = {0, 0, 0, 0};
+    for (int w : yw) ywarps[w % 4]++;
+    const double target = (load[0] + load[1] + load[2] + load[3] + 4.0 * fs.n4 * fs.ncb) / 4.0;
+    std::vector<std::vector<int>> wcb(fs.ncb);
+    for (size_t i = 0; i < yw.size(); ++i) wcb[i % fs.ncb].push_back(yw[i]);
+    for (int cb = 0; cb < fs.ncb; ++cb) {
+      // a part's weight: what its SMSP has left of the even share, split over the Y warps issuing there
+      std::vector<double> wgt(fs.nkp);
+      double sum = 0.0;
+      for (int kp = 0; kp < fs.nkp; ++kp) {
+        const int q = wcb[cb][kp] % 4;
+        wgt[kp] = std::max(4.0, (target - load[q]) / std::max(1, ywarps[q]));
+        sum += wgt[kp];
+      }
+      std::vector<int> nj(fs.nkp);
+      int tot = 0;
+      for (int kp = 0; kp < fs.nkp; ++kp) {
+        nj[kp] = std::max(1, std::min(FS_WR, (int)(fs.n4 * wgt[kp] / sum + 0.5)));
+        tot += nj[kp];
+      }
+      for (int guard = 0; tot != fs.n4 && guard < 1000; ++guard) {  // fix the rounding, heaviest weights first
+        int best = -1;
+        for (int kp = 0; kp < fs.nkp; ++kp) {
+          if (tot < fs.n4 && nj[kp] >= FS_WR) continue;
+          if (tot > fs.n4 && nj[kp] <= 1) continue;
+          if (best < 0 || (tot < fs.n4 ? wgt[kp] / nj[kp] > wgt[best] / nj[best] : wgt[kp] / nj[kp] < wgt[best] / nj[best]))
+            best = kp;
+        }
+        if (best < 0) return -1.0;
+        nj[best] += tot < fs.n4 ? 1 : -1;
+        tot += tot < fs.n4 ? 1 : -1;
+      }
+      if (tot != fs.n4) return -1.0;
+      int j = 0;
+      for (int kp = 0; kp < fs.nkp; ++kp) {
+        const int w = wcb[cb][kp];
+        fs.role[w] = FS_Y;
+        fs.ycb[w] = (unsigned char)cb;
+        fs.ykp[w] = (unsigned char)kp;
+        fs.yj0[w] = (unsigned char)j;
+        fs.ynj[w] = (unsigned char)nj[kp];
+        j += nj[kp];
+      }
     }
-  }
-  for (int w = 0; w < NWARP; ++w) fs.nB += fs.role[w] == FS_OFF || (fs.role[w] == FS_PY && fs.py_na[w] > 0);
+
+    // DMMAs per stage of the busiest SMSP; a single warp is a serial chain, so the heaviest tile warp
+    // counts half as much again
+    double mx = 0.0;
+    int yl[4] = {0, 0, 0, 0};
+    for (int w = 0; w < NWARP; ++w)
+      if (fs.role[w] == FS_Y) yl[w % 4] += 4 * fs.ynj[w];
+    for (int q = 0; q < 4; ++q) mx = std::max(mx, (double)load[q] + yl[q]);
+    for (const Item& im : items) mx = std::max(mx, 1.5 * im.cost);
+    return mx;
+  };
+  int best_na = -1;
+  bool best_own = false;
+  double best_load = 0.0;
+  for (int own = 0; own < 2; ++own)
+    for (int namax = fs0.ncb <= 2 ? 8 : 5; namax >= 2; --namax) {
+      FusedSplit t = fs0;
+      ReduceMap m1, m2;
+      const double ld = build(namax, own != 0, t, m1, m2);
+      if (ld >= 0.0 && (best_na < 0 || ld < best_load - 0.5)) best_na = namax, best_own = own != 0, best_load = ld;
+    }
+  if (best_na < 0) return -1;
+  fs = fs0;
+  if (build(best_na, best_own, fs, nm, offmap) < 0.0) return -1;
+  nm.nchunks = map.nchunks;
+  nm.nslices = 1;
+  map = nm;
   offmap.nchunks = map.nchunks;
   offmap.nslices = 1;
   static const bool verbose = getenv("PSVD_PASS_VERBOSE") != nullptr;
   if (verbose) {
-    fprintf(stderr, "fused_split: pwA=%d pwB=%d n4=%d ncb=%d npy=%d noff=%d smem=%zu roles:", fs.pwA, fs.pwB, fs.n4, fs.ncb,
-            fs.npy, fs.noff, fused_split_smem_bytes(fs));
+    fprintf(stderr, "fused_split: ns=%d colA0=%d pwA=%d pwB=%d n4=%d ncb=%d nkp=%d npy=%d noff=%d nA=%d nB=%d smem=%zu roles:",
+            fs.ns, fs.colA0, fs.pwA, fs.pwB, fs.n4, fs.ncb, fs.nkp, fs.npy, fs.noff, fs.nA, fs.nB, fused_split_smem_bytes(fs));
     for (int w = 0; w < NWARP; ++w) {
       if (fs.role[w] == FS_Y) fprintf(stderr, " w%d:Y(cb%d,kp%d,%d+%d)", w, fs.ycb[w], fs.ykp[w], fs.yj0[w], fs.ynj[w]);
-      else if (fs.role[w] == FS_PY) fprintf(stderr, " w%d:PY(sb%d+%d%s)", w, fs.py_sb0[w], fs.py_na[w], fs.py_yy[w] ? ",yy" : "");
+      else if (fs.role[w] == FS_PY)
+        fprintf(stderr, " w%d:PY%s(sb%d+%d%s)", w, fs.py_onA[w] ? "a" : "", fs.py_sb0[w], fs.py_na[w], fs.py_yy[w] ? ",yy" : "");
       else if (fs.role[w] == FS_OFF) fprintf(stderr, " w%d:OFF(%d,%d)", w, fs.off_i[w], fs.off_j[w]);
       else if (fs.role[w] == FS_PROD) fprintf(stderr, " w%d:PROD", w);
     }

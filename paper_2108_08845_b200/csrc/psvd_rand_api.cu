@@ -419,7 +419,11 @@ int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu
       pa.p.Yout = Zt + r0;
       pa.p.ldy = ldq;
       c->path_count[pa.tma ? 0 : 3]++;
-      if (pa.tma)
+      // the split-ring kernel when the pass qualifies (group A = A_j under W, group B = Q for Q^T Z)
+      if (pa.tma && nsub == 1 && try_fused_split(c, pa, {}, 1)) {
+        launch_fused_split(pa.p, pa.maps3, pa.x, pa.fs, pa.grid, lo);
+        first.map = pa.map;  // the split kernel's own slot map
+      } else if (pa.tma)
         launch_pass_tma(pa.p, pa.maps, pa.x, pa.grid, lo);
       else
         launch_tall(pa.p, pa.grid, lo);

@@ -128,28 +128,34 @@ void launch_pass_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x
 constexpr int FS_WR = 20;      // W fragments (k steps of 4 columns) a Y warp holds in registers
 constexpr int FS_NKP = 4;      // k parts per Y column block
 constexpr int FS_MAX_OFF = 3;  // offloaded Gram tiles
+constexpr int FS_NS_MAX = 4;   // slots per ring
 enum { FS_IDLE = 0, FS_Y = 1, FS_PY = 2, FS_OFF = 3, FS_PROD = 4 };
 struct FusedSplit {
+  int colA0;                     // first panel column of group A (= the first k column of W)
   int pwA, pwB;                  // slot widths in columns (multiples of 8)
   int nopsA, nopsB;              // TMA boxes per stage of each group (group A's come first)
   short opm[TMA_MAX_OPS], opc[TMA_MAX_OPS], opd[TMA_MAX_OPS];  // tensor map, tensor column, slot column
   unsigned bytesA, bytesB;       // bytes per stage of each group
-  int ncb;                       // Y column blocks (1 or 2)
+  int ncb;                       // Y column blocks (1 .. 3)
   int n4;                        // k steps of 4 physical panel columns
+  int nkp;                       // k parts per Y column block (1, 2 or FS_NKP)
+  int ns;                        // slots per ring (2 .. FS_NS_MAX, as shared memory allows)
   int npy, noff;                 // warps with P^T Y (or Y^T Y) tiles / offloaded Gram tiles
-  int nB;                        // warps that read group B (release its ring slots)
+  int nA, nB;                    // warps that read group A / group B (they release its ring slots)
   unsigned char role[NWARP];
   unsigned char ycb[NWARP], ykp[NWARP], yj0[NWARP], ynj[NWARP];     // Y warps: column block, part, k steps
-  unsigned char py_sb0[NWARP], py_na[NWARP], py_yy[NWARP];         // P^T Y warps: 8-column sub-blocks of slot B
-  unsigned char py_slot[NWARP][2], yy_slot;                        // partial-tile slots (32-column tiles)
-  unsigned char off_i[NWARP], off_j[NWARP], off_slot[NWARP];       // offloaded tile (I, J) of A_next^T A_next
+  // tile warps: na sub-blocks of 8 columns from sub-block sb0 of their group's slot; rb0 = position of the
+  // first one inside its 32-column tile, nt tiles touched, one partial-tile slot each
+  unsigned char py_sb0[NWARP], py_na[NWARP], py_yy[NWARP], py_onA[NWARP], py_rb0[NWARP], py_nt[NWARP];
+  unsigned char py_slot[NWARP][3], yy_slot;
+  unsigned char off_i[NWARP], off_j[NWARP], off_slot[NWARP];       // offloaded tile (I, J) of the B segment's Gram
 };
 size_t fused_split_smem_bytes(const FusedSplit& fs);
 void launch_fused_split(const TallParams& p, const TmaMaps& maps3, const TmaExtra& x, const FusedSplit& fs, int grid,
                         cudaStream_t st);
 // builds fs and the 3-D tensor maps from a planned narrow TMA pass (p, x, its reduce map); off: wanted
 // offloaded tiles (block pairs of the last segment); returns 0 when the pass qualifies
-int fused_split_prepare(const TallParams& p, const TmaExtra& x, const ReduceMap& map, int NB, const int (*off)[2],
+int fused_split_prepare(const TallParams& p, const TmaExtra& x, ReduceMap& map, int NB, const int (*off)[2],
                         int noff, FusedSplit& fs, TmaMaps& maps3, ReduceMap& offmap, int off_nb);
 
 // TMA-fed Gram-only pass (w == 0, segments on 8-column boundaries, <= NWARP - 1 tiles per slice)
