@@ -137,8 +137,9 @@ int psvd_recompose(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, int K
 /* The fused pass of the pipelined stream as a call of its own (streaming.py:97-103 composed with the next
  * update's projection): U_out = [U | A] * W, UtU = U_out^T U_out (K x K) and AtU = A_next^T U_out
  * (Bn x K, col-major ld Bn) from one read of [U | A | A_next].  mode 0: the narrow TMA pass (16-row
- * stages); mode 1: the split-ring kernel (32-row 3-D TMA boxes; PSVD_EINVAL when the shapes do not
- * qualify: K <= 16, M a multiple of 16, the rings within shared memory).  With mode 1 and noff > 0 the
+ * stages: the round-1 kernel, kept as the fallback and as the A/B reference); mode 1: the split-ring
+ * kernel (32-row 3-D TMA boxes; PSVD_EINVAL when the shapes do not qualify: K <= 24, M a multiple of
+ * 16, the rings within shared memory).  With mode 1 and noff > 0 the
  * pass also forms the 32 x 32 blocks (2t, 2t + 1), t < noff <= 3, of A_next^T A_next (work taken off
  * the look-ahead Gram) into off_tiles, a (ceil(Bn / 32))^2 array of row-major 32 x 32 tiles. */
 int psvd_fused_pass(psvd_ctx* ctx, int64_t M, const double* U, int64_t ldu, int Kc, const double* A, int64_t lda,

@@ -753,16 +753,17 @@ void launch_gram_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x
   gram_tma_kernel<false><<<grid, NTHR, smem, st>>>(p, maps, x);
 }
 
-// ---------------------------------------------------------------- split-ring fused pass
-// The deterministic stream's fused pass over [U | A_b | A_next] (psvd_tall.cuh: FusedSplit).  A
-// 32-row stage of the whole panel does not fit shared memory twice, which left that pass on 16-row
-// stages (128 contiguous bytes per column and request, ~4.5 TB/s).  Here a stage is split by column
-// group: group A = [U | A_b] (read by the Y warps only) and group B = A_next (read by the tile warps
-// only), each group in its own two-slot ring of 3-D boxes {16 rows, 2, columns} (256 contiguous
-// bytes per column).  W lives in the Y warps' registers (FS_NKP k parts per column block, partial
-// sums met in the Y tile in part order, as in pass_tma_kernel), staged once through ring memory.
-// Tile warps: A_next^T Y over up to 8 sub-blocks of 8 columns each, Y^T Y, and offloaded 32 x 32
-// tiles of A_next^T A_next that the look-ahead Gram then skips.
+// ---------------------------------------------------------------- split-ring pass
+// First built for the deterministic stream's fused pass over [U | A_b | A_next] (psvd_tall.cuh:
+// FusedSplit): a 32-row stage of that whole panel does not fit shared memory twice, which had left the
+// pass on 16-row stages (128 contiguous bytes per column and request, ~4.5 TB/s).  Here a stage is split
+// by column group: group A = the segments under W (read by the Y warps) and group B = the others (read
+// by the tile warps), each group in its own ring of 3-D boxes {16 rows, 2, columns} (256 contiguous bytes
+// per column); a slot is released by its own readers.  W lives in the Y warps' registers (nkp k parts per
+// column block, partial sums met in the Y tile in part order, as in pass_tma_kernel), staged once through
+// ring memory.  Tile warps: P^T Y over runs of 8-column sub-blocks of either group, Y^T Y, and offloaded
+// 32 x 32 tiles of group B's Gram that the look-ahead Gram then skips.  Every load address is a per-lane
+// offset plus a compile-time constant (the swizzle phase of a column repeats every 8 columns).
 namespace {
 
 PSVD_DEV bool mbar_test(uint64_t* bar, unsigned parity) {

@@ -120,11 +120,14 @@ bool tma_available();
 size_t tma_pass_smem_bytes(int pwidth, int kp_span, int w_pad, int ns = 3, int ny = 1);
 int tma_pass_prepare(TallParams& p, TmaMaps& maps, TmaExtra& x, int pshift = 0, bool narrow = false);
 void launch_pass_tma(const TallParams& p, const TmaMaps& maps, const TmaExtra& x, int grid, cudaStream_t st);
-// Split-ring fused pass of the pipelined deterministic stream (fused_split_kernel): the panel
-// [U | A_b | A_next] streamed as 32-row stages of two column groups (A = [U | A_b], B = A_next),
-// each in its own two-slot ring of 3-D TMA boxes; Y = [U | A_b] W with W in registers, the tiles
-// A_next^T Y and Y^T Y, and up to FS_MAX_OFF offloaded 32 x 32 tiles of A_next^T A_next (work
-// taken off the look-ahead Gram: the pass is HBM-bound, its DMMA pipe has room).
+// Split-ring pass (fused_split_kernel): a narrow pass Y = P_A W with Gram tiles against Y, streamed as
+// 32-row stages of two column groups -- group A = the segments W covers (read by the Y warps), group B =
+// the others (read by the tile warps) -- each in its own ring of 2 .. FS_NS_MAX slots of 3-D TMA boxes
+// (256 contiguous bytes per column and request).  W lives in the Y warps' registers; tile warps own the
+// P^T Y sub-blocks of either group and Y^T Y; up to FS_MAX_OFF warps compute 32 x 32 tiles of the Gram of
+// group B's segment (the deterministic stream's fused pass over [U | A_b | A_next]: work taken off the
+// look-ahead Gram of A_next, whose pass is DMMA-bound while this one is HBM-bound).  run_pass sends every
+// narrow TMA pass that qualifies here (fused_split_prepare); the others stay on pass_tma_kernel.
 constexpr int FS_WR = 20;      // W fragments (k steps of 4 columns) a Y warp holds in registers
 constexpr int FS_NKP = 4;      // k parts per Y column block
 constexpr int FS_MAX_OFF = 3;  // offloaded Gram tiles

@@ -79,4 +79,4 @@ def test_split_ring_refuses_shapes_it_cannot_take():
     with pytest.raises(ValueError):
         _run(4100, 10, 200, 200, 10, 1, 0)   # M not a multiple of 16
     with pytest.raises(ValueError):
-        _run(4096, 20, 200, 200, 20, 1, 0)   # K > 16
+        _run(4096, 28, 200, 200, 28, 1, 0)   # four Y column blocks (K > 24)
