@@ -885,8 +885,9 @@ int psvd_fused_pass(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, int Kc
     for (int t = 0; 2 * t + 1 < Bn / 32 && t < noff && off_tiles; ++t) off.push_back({2 * t, 2 * t + 1});
     if (!try_fused_split(c, pf, off, off_nb)) return fail(c, PSVD_EINVAL, "the pass does not qualify for the split-ring kernel");
     if ((rc = run_fused_split(c, pf, st, off_tiles))) return rc;
+  } else if (!pf.tma) {  // no narrow TMA plan (e.g. an odd leading dimension): the general tall pass
+    if ((rc = run_pass(c, pf, st))) return rc;
   } else {  // mode 0: the narrow TMA pass itself (run_pass would pick the split-ring kernel)
-    if (!pf.tma) return fail(c, PSVD_EINVAL, "the pass does not plan as a narrow TMA pass");
     c->path_count[0]++;
     launch_pass_tma(pf.p, pf.maps, pf.x, pf.grid, st);
     c->launches += 2;
