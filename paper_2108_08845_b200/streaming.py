@@ -163,19 +163,23 @@ def stream_incorporate(state, a_new, config):
     return StreamState(u.view, s, state.iteration + 1)
 
 
-STREAM_WINDOW = 8  # most batches resident on the device per pipelined run
+STREAM_WINDOW = 8  # most batches resident on the device per pipelined run (host batches: uploads in flight)
+STREAM_WINDOW_RESIDENT = 32  # ... when the batches already are device tensors (nothing to upload)
 STREAM_WINDOW_MEM_FRACTION = 0.25  # ... and at most this share of the device's memory
 
 
 def window_length(batch, device):
-    """Batches per pipelined window: STREAM_WINDOW, fewer when they would take more than
-    STREAM_WINDOW_MEM_FRACTION of HBM (at least 2, so the look-ahead Gram still overlaps)."""
+    """Batches per pipelined window: STREAM_WINDOW (STREAM_WINDOW_RESIDENT for device tensors: every window
+    boundary costs the pipeline its head, the first batch's Gram, and its tail, the last core solve, ~2 ms
+    at config-2 shapes), fewer when they would take more than STREAM_WINDOW_MEM_FRACTION of HBM (at least
+    2, so the look-ahead Gram still overlaps)."""
     shape = getattr(batch, "shape", None)
     if shape is None or len(shape) != 2:
         return STREAM_WINDOW
+    cap = STREAM_WINDOW_RESIDENT if (torch.is_tensor(batch) and batch.is_cuda) else STREAM_WINDOW
     nbytes = 8 * int(shape[0]) * int(shape[1])
     total = torch.cuda.get_device_properties(torch.device(device)).total_memory
-    return int(max(2, min(STREAM_WINDOW, (STREAM_WINDOW_MEM_FRACTION * total) // max(nbytes, 1))))
+    return int(max(2, min(cap, (STREAM_WINDOW_MEM_FRACTION * total) // max(nbytes, 1))))
 
 
 def _run_window(state, mats, config, dev, ready=None, rescue=True, ok=None, on_illcond=None):

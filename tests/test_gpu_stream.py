@@ -235,12 +235,12 @@ def test_stream_all_windows_and_continuation():
     p = _pkg()
     a = oracle.burgers_matrix(6000, 800)
     ref_m, ref_s, ref_h = oracle.ref_stream_all(_batches(a, 50), 10, 0.95)
-    old = p.streaming.STREAM_WINDOW
+    old = (p.streaming.STREAM_WINDOW, p.streaming.STREAM_WINDOW_RESIDENT)
     try:
-        p.streaming.STREAM_WINDOW = 3  # 16 batches -> windows 3,3,3,3,3,1 chained through the state
+        p.streaming.STREAM_WINDOW = p.streaming.STREAM_WINDOW_RESIDENT = 3  # 16 batches -> windows 3,3,3,3,3,1 chained through the state
         st, hist = p.stream_all(_batches(a, 50), p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=50))
     finally:
-        p.streaming.STREAM_WINDOW = old
+        p.streaming.STREAM_WINDOW, p.streaming.STREAM_WINDOW_RESIDENT = old
     m, s = _np(st)
     _assert_parity(m, s, ref_m, ref_s)
     assert st.iteration == 15 and len(hist) == 16
@@ -258,13 +258,13 @@ def test_stream_all_pinned_host_batches_overlap_copies():
     host = torch.empty((800, 8192), dtype=torch.float64).pin_memory()
     host.copy_(torch.from_numpy(a.T.copy()))
     pin_b = [host[c:c + 100].T for c in range(0, 800, 100)]  # column-major pinned views
-    old = p.streaming.STREAM_WINDOW
+    old = (p.streaming.STREAM_WINDOW, p.streaming.STREAM_WINDOW_RESIDENT)
     try:
-        p.streaming.STREAM_WINDOW = 3
+        p.streaming.STREAM_WINDOW = p.streaming.STREAM_WINDOW_RESIDENT = 3
         s1, h1 = p.stream_all(dev_b, cfg)
         s2, h2 = p.stream_all(pin_b, cfg)
     finally:
-        p.streaming.STREAM_WINDOW = old
+        p.streaming.STREAM_WINDOW, p.streaming.STREAM_WINDOW_RESIDENT = old
     assert torch.equal(s1.modes, s2.modes) and torch.equal(s1.singular_values, s2.singular_values)
     assert all(torch.equal(x, y) for x, y in zip(h1, h2))
     ref_m, ref_s, _ = oracle.ref_stream_all(_batches(a, 100), 10, 0.95)
@@ -604,7 +604,7 @@ def _rand_run_rank_worker(rank, world, port, q, qit):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2108_08845_b200 as p
-        p.streaming.STREAM_WINDOW = 2  # 4 batches = two windows: the second starts from a materialized state
+        p.streaming.STREAM_WINDOW = p.streaming.STREAM_WINDOW_RESIDENT = 2  # 4 batches = two windows: the second starts from a materialized state
         a = oracle.burgers_matrix(6001, 800)
         lo, hi = p.partition_bounds(a.shape[0], world)[rank]
         cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200,
@@ -654,12 +654,12 @@ def test_parallel_pipelined_randomized_stream_ranks_match_serial(qit):
     a = oracle.burgers_matrix(6001, 800)
     cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200,
                          sketch=p.RandomSketchConfig(target_rank=10, oversampling=10, power_iterations=qit, seed=0))
-    old = p.streaming.STREAM_WINDOW
+    old = (p.streaming.STREAM_WINDOW, p.streaming.STREAM_WINDOW_RESIDENT)
     try:
-        p.streaming.STREAM_WINDOW = 2
+        p.streaming.STREAM_WINDOW = p.streaming.STREAM_WINDOW_RESIDENT = 2
         st, _ = p.stream_all(_batches(a, 200), cfg)
     finally:
-        p.streaming.STREAM_WINDOW = old
+        p.streaming.STREAM_WINDOW, p.streaming.STREAM_WINDOW_RESIDENT = old
     m1, s1 = _np(st)
     _assert_parity(out[0][2], out[0][0], m1, s1, sig_tol=1e-13, ang_tol=1e-11)
     rm, rs, rh = oracle.ref_rand_stream_all(_batches(a, 200), 10, 0.95, 10, qit, 0)
@@ -991,3 +991,22 @@ def test_library_nccl_exchange_world_one_is_bitwise_serial():
     assert calls1 > calls0
     for x, y in zip(base, viann):
         assert torch.equal(x.modes, y.modes) and torch.equal(x.singular_values, y.singular_values)
+
+
+def test_resident_batches_run_in_longer_windows():
+    """Device tensors need no upload slots, so stream_all keeps up to STREAM_WINDOW_RESIDENT of them in one
+    pipelined window (a window boundary costs the pipeline its head and tail); host batches keep
+    STREAM_WINDOW.  20 resident batches = one window, against the oracle's 20 updates."""
+    p = _pkg()
+    a = oracle.burgers_matrix(4096, 800)
+    dev = torch.device("cuda", 0)
+    dev_b = [torch.from_numpy(np.asfortranarray(a[:, c:c + 40])).cuda() for c in range(0, 800, 40)]
+    assert p.streaming.window_length(dev_b[0], dev) == min(p.streaming.STREAM_WINDOW_RESIDENT, 32)
+    assert p.streaming.window_length(a[:, :40], dev) == p.streaming.STREAM_WINDOW
+    st, hist = p.stream_all(dev_b, p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=40))
+    ref_m, ref_s, ref_h = oracle.ref_stream_all(_batches(a, 40), 10, 0.95)
+    m, s = _np(st)
+    _assert_parity(m, s, ref_m, ref_s)
+    assert st.iteration == 19 and len(hist) == 20
+    for h, rh in zip(hist, ref_h):
+        assert oracle.sigma_rel_err(h.cpu().numpy(), rh) <= SIG_TOL
