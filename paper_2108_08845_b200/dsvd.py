@@ -372,6 +372,14 @@ def parallel_stream_all(ctx, batches_local, config, device=None):
         return st, hist
     c = nat.context(dev)
     wlen = window_length(first, dev)
+    if ctx.world_size > 1:
+        # one window length on every rank (row blocks differ by a row, so the memory bound could round
+        # differently): the windows' exchanges must line up
+        wl = torch.tensor([wlen], dtype=torch.int64)
+        if dist.get_backend(ctx.group) == "nccl":
+            wl = wl.to(dev)
+        dist.all_reduce(wl, op=dist.ReduceOp.MIN, group=ctx.group)
+        wlen = int(wl.item())
     off = None
     ex = None  # exchange_hooks, entered at the first pipelined window
     state, hist = None, []
