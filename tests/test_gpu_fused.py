@@ -57,6 +57,8 @@ def _run(M, Kc, B, Bn, K, mode, noff, seed=0):
     (1 << 15, 16, 120, 136, 16),
     (4112, 12, 36, 40, 12),      # narrow batches: no full 32-column pair to offload
     (8192, 10, 208, 72, 9),
+    (4096, 0, 200, 20, 20),      # the look-ahead sketch's shape: three Y column blocks, a 20-column group B
+    (8192, 20, 24, 200, 20),     # the projection pass's shape: a short W range (one k part), tile warps of <= 5 sub-blocks
 ])
 def test_split_ring_kernel_matches_products_and_narrow_pass(shape):
     M, Kc, B, Bn, K = shape
