@@ -77,6 +77,7 @@ __global__ void __launch_bounds__(GT) tgemm_nn_kernel(int64_t M, ColTable P, int
     for (int b = 0; b < CBW; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
   const int nchunk = (K + BK - 1) / BK;
+  const bool w16 = (ldw & 1) == 0 && (reinterpret_cast<uintptr_t>(W) & 15) == 0;
   auto load = [&](int ch, int buf) {
     const int k0 = ch * BK;
     // P: BK columns x BMT rows in 16-byte pieces
@@ -90,12 +91,22 @@ __global__ void __launch_bounds__(GT) tgemm_nn_kernel(int64_t M, ColTable P, int
       const double* src = (bytes > 0) ? cols[k] + r : P.ptr[0];
       cp_async16(dst, src, bytes);
     }
-    // W: NB columns x BK rows (k), 8-byte pieces (W is small and L2-resident; any ld)
-    for (int q = tid; q < NB * BK; q += GT) {
-      const int nn = q / BK, kk = q % BK;
-      const int n = n0 + nn, k = k0 + kk;
-      const int bytes = (n < N && k < K) ? 8 : 0;
-      cp_async8(&sW[buf][nn * WSTR + kk], (bytes > 0) ? W + (int64_t)n * ldw + k : W, bytes);
+    // W: NB columns x BK rows (k); W is small and L2-resident.  16-byte pieces when every column chunk is
+    // 16-byte aligned (even ld, aligned base; k0 is a multiple of BK), else 8-byte ones (any ld)
+    if (w16) {
+      for (int q = tid; q < NB * (BK / 2); q += GT) {
+        const int nn = q / (BK / 2), kk = 2 * (q % (BK / 2));
+        const int n = n0 + nn, k = k0 + kk;
+        const int bytes = (n < N && k < K) ? (k + 1 < K ? 16 : 8) : 0;
+        cp_async16(&sW[buf][nn * WSTR + kk], (bytes > 0) ? W + (int64_t)n * ldw + k : W, bytes);
+      }
+    } else {
+      for (int q = tid; q < NB * BK; q += GT) {
+        const int nn = q / BK, kk = q % BK;
+        const int n = n0 + nn, k = k0 + kk;
+        const int bytes = (n < N && k < K) ? 8 : 0;
+        cp_async8(&sW[buf][nn * WSTR + kk], (bytes > 0) ? W + (int64_t)n * ldw + k : W, bytes);
+      }
     }
   };
   load(0, 0);
