@@ -46,6 +46,10 @@ extern "C" {
 #define PSVD_ST_CHOLFAIL 16  /* sketch Cholesky needed the shifted retry */
 #define PSVD_ST_ILLCOND 32   /* deterministic Gram route: kept spectrum sigma_1 / sigma_K > 300, so the
                                 update must be redone on the accurate route (psvd_stream_update_accurate) */
+#define PSVD_ST_SKETCHCOND 64 /* randomized update: a sketch (or power-iteration) block had a direction at or below
+                                3e-7 of its largest one, where the Gram-based orthonormalization (SVQB) drops or
+                                blurs it while the reference's Householder qr keeps it (linalg.py:94-104, 143-147):
+                                the caller redoes the update on the accurate route (psvd_qr after every product) */
 
 typedef struct psvd_ctx psvd_ctx;
 

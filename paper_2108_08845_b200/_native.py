@@ -25,7 +25,7 @@ if os.environ.get("PSVD_LIB_VARIANT"):  # diagnostics: an in-tree build variant 
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "psvd.h")
 
 PSVD_OK, PSVD_EINVAL, PSVD_ENOCONV, PSVD_ECUDA = 0, 1, 2, 3
-ST_NONFINITE, ST_NOCONVERGE, ST_RESCUE, ST_RANKDEF, ST_CHOLFAIL, ST_ILLCOND = 1, 2, 4, 8, 16, 32
+ST_NONFINITE, ST_NOCONVERGE, ST_RESCUE, ST_RANKDEF, ST_CHOLFAIL, ST_ILLCOND, ST_SKETCHCOND = 1, 2, 4, 8, 16, 32, 64
 
 _c_i64 = ctypes.c_int64
 _c_int = ctypes.c_int

@@ -158,16 +158,19 @@ size_t jacobi_workspace_doubles(int n, int l) { return (size_t)n * (l + 1); }
 // descending; T = eigenvectors): T[:, k] *= 1 / sqrt(S_k), or 0 for directions with
 // sqrt(S_k) <= tol * sqrt(S_0) (numerically null, dropped).
 __global__ void svqb_scale_kernel(double* __restrict__ T, const double* __restrict__ S, int l, double tol,
-                                  const int* __restrict__ gate) {
+                                  const int* __restrict__ gate, int* __restrict__ status) {
   if (gate != nullptr && *gate == 0) return;
   const int k = blockIdx.x;
   const double s0 = sqrt(fmax(S[0], 0.0)), sk = sqrt(fmax(S[k], 0.0));
   const double inv = (sk > 0.0 && sk > tol * s0) ? 1.0 / sk : 0.0;
+  // a direction this small is dropped or only roughly resolved by the Gram's eigenpairs: the result is a
+  // valid randomized SVD, but no longer the reference's to 1e-10 (its Householder qr keeps the direction)
+  if (status != nullptr && threadIdx.x == 0 && !(sk > 3.0 * tol * s0)) atomicOr(status, PSVD_ST_SKETCHCOND);
   for (int i = threadIdx.x; i < l; i += blockDim.x) T[(size_t)k * l + i] *= inv;
 }
 
-void launch_svqb_scale(double* T, const double* S, int l, double tol, cudaStream_t st, const int* gate) {
-  svqb_scale_kernel<<<l, 32, 0, st>>>(T, S, l, tol, gate);
+void launch_svqb_scale(double* T, const double* S, int l, double tol, cudaStream_t st, const int* gate, int* status) {
+  svqb_scale_kernel<<<l, 32, 0, st>>>(T, S, l, tol, gate, status);
 }
 
 void launch_jacobi_svd(const double* Z, int n, int l, double* S, double* J, double* ws, int* status, cudaStream_t st,

@@ -74,7 +74,7 @@ int svqb(psvd_ctx* c, const double* Gs, int l, double* T, double* sig_scratch, c
   int* illcond = c->d_status + 3;
   launch_chol_inv(Gs, l, T, st, illcond, c->d_status);
   launch_jacobi_svd(Gs, l, l, sig_scratch, T, (double*)c->eigws.ptr, c->d_status, st, illcond);
-  launch_svqb_scale(T, sig_scratch, l, 1e-7, st, illcond);
+  launch_svqb_scale(T, sig_scratch, l, 1e-7, st, illcond, c->d_status);
   c->launches += 3;
   return cuda_check(c, "svqb");
 }

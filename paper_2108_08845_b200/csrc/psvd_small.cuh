@@ -91,7 +91,8 @@ constexpr int CHOL_NMAX = 112;  // chol_inv keeps R and R^-1 in shared memory
 void launch_chol_shift(double* G, int n, int64_t M, cudaStream_t st);
 void launch_colmax_sign(const double* colmax, int nchunks, int K, double* sign, cudaStream_t st);
 void launch_colmax_reduce(const double* colmax, int nchunks, int K, double* out, cudaStream_t st);
-void launch_svqb_scale(double* T, const double* S, int l, double tol, cudaStream_t st, const int* gate = nullptr);
+void launch_svqb_scale(double* T, const double* S, int l, double tol, cudaStream_t st, const int* gate = nullptr,
+                       int* status = nullptr);
 void launch_scale_cols(double* U, int64_t ld, int64_t M, int K, const double* s, cudaStream_t st);
 void launch_scale_rows(const double* X, int ldx, int m, int k, const double* d, double* Y, int ldy, cudaStream_t st);
 

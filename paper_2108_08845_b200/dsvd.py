@@ -260,7 +260,7 @@ def _parallel_rand_update(ctx, U, sigma, A, sketch, ff, dev):
     if ctx.world_size == 1:
         return randomized_update(U, sigma, A, sketch, ff, dev)
     with exchange_hooks(ctx, dev, off):
-        return randomized_update(U, sigma, A, sketch, ff, dev, total_rows=total)
+        return randomized_update(U, sigma, A, sketch, ff, dev, total_rows=total, accurate=False)
 
 
 def _parallel_update(ctx, U, sigma, A, k, ff, dev):
@@ -427,7 +427,9 @@ def parallel_stream_all(ctx, batches_local, config, device=None):
         if sk is None:
             state, h = _run_window(state, window, config, dev, rescue=False, ok=True, on_illcond=per_batch)
         else:
-            state, h = _run_rand_window(state, window, config, dev, supported=True)
+            # (the accurate randomized route is single-rank: with more ranks the pipelined result stands)
+            state, h = _run_rand_window(state, window, config, dev, supported=True,
+                                        redo_illcond=ctx.world_size == 1)
         hist.extend(h)
 
     try:

@@ -65,11 +65,53 @@ def device_omega(n_cols, config, device):
     return om
 
 
-def randomized_update(U, sigma, A, sketch, ff, device, check=True, total_rows=None, omega=None):
+ACCURATE_RAND_UPDATES = 0  # randomized updates redone on the accurate route (diagnostics / tests)
+
+
+def accurate_randomized_update(U, sigma, A, sketch, ff, device, omega=None):
+    """The randomized step on the accurate route: the reference's own sequence (linalg.py:126-162) with
+    a backward-stable qr after every product -- the panel [ff U diag(sigma) | A] materialized, q =
+    randomized_range(panel) (psvd_nn_product / psvd_tn_product / psvd_qr, the rank-robust Householder-quality
+    route included), b^T = panel^T q, the Jacobi svd of b^T (relative accuracy on every value), u = q u_b[:, :K]
+    and the tall sign rule.  Slower than psvd_rand_update (the panel is read once per product and written once);
+    taken when that update reports PSVD_ST_SKETCHCOND.  Returns (DevMat M x K, sigma (K,))."""
+    import torch
+    from . import _native as nat
+    global ACCURATE_RAND_UPDATES
+    ACCURATE_RAND_UPDATES += 1
+    k, l = sketch.target_rank, sketch.sketch_width
+    kc = 0 if U is None else U.cols
+    M, n = A.rows, kc + A.cols
+    ctx, st = nat.context(device), nat.stream_ptr(device)
+    with torch.cuda.device(device):
+        C = nat.DevMat.empty(M, n, device)
+        if kc:
+            torch.mul(U.view, (ff * sigma)[None, :], out=C.view[:, :kc])
+        C.view[:, kc:].copy_(A.view)
+        q = nat.as_device_colmajor(_range_of(C, sketch, device, omega), device, "q")
+        Z = torch.empty((l, n), dtype=torch.float64, device=device).t()  # n x l column-major: b^T = panel^T q
+        nat.call("psvd_tn_product", ctx, M, nat._vp(C.data_ptr()), C.ld, n, nat._vp(q.data_ptr()), q.ld, l,
+                 nat._vp(Z.data_ptr()), n, st)
+        res = svd_full(Z, want_vt=True, device=device)  # b^T = u s vt, so b's left vectors are vt's rows
+        W = torch.empty((k, l), dtype=torch.float64, device=device)  # (l x k) column-major = vt[:k]^T
+        W.copy_(res.vt[:k, :])
+        out = nat.DevMat.empty(M, k, device)
+        nat.call("psvd_nn_product", ctx, M, nat._vp(q.data_ptr()), q.ld, l, nat.ptr(W), l, k,
+                 nat._vp(out.data_ptr()), out.ld, st)
+        nat.call("psvd_sign_by_peak", ctx, nat._vp(out.data_ptr()), out.ld, M, k, st)
+        sig = res.s[:k].clone()
+    return out, sig
+
+
+def randomized_update(U, sigma, A, sketch, ff, device, check=True, total_rows=None, omega=None, accurate=True):
     """One randomized step: low_rank_svd([ff*U*diag(sigma) | A], sketch) on the
     device (linalg.py:150-162 composed per batch).  U: DevMat or None.
     total_rows: rows of the whole (row-partitioned) panel for the width check.
     omega: optional device test matrix (n x l, column-major) replacing the Philox draw.
+    accurate: redo the step on accurate_randomized_update when the device reports
+    PSVD_ST_SKETCHCOND (a sketch direction at or below 3e-7 of the largest: the Gram-based
+    orthonormalization no longer reproduces the reference's Householder qr to 1e-10); the
+    row-partitioned callers pass False (that route is single-rank).
     Returns (DevMat M x K, sigma (K,))."""
     import torch
     from . import _native as nat
@@ -96,6 +138,8 @@ def randomized_update(U, sigma, A, sketch, ff, device, check=True, total_rows=No
             if st & nat.ST_NOCONVERGE:
                 from .errors import ConvergenceError
                 raise ConvergenceError("randomized core SVD did not converge")
+            if accurate and (st & nat.ST_SKETCHCOND):
+                return accurate_randomized_update(U, sigma, A, sketch, ff, device, omega=omega)
     return out, sig
 
 
@@ -277,13 +321,20 @@ def randomized_range(a, config, device=None):
     from . import _native as nat
     dev = _dev(device)
     A = nat.as_device_colmajor(a, dev, "a")
+    return _range_of(A, config, dev, None)
+
+
+def _range_of(A, config, dev, omega):
+    """randomized_range of a DevMat; omega: optional device test matrix (n x width, column-major)."""
+    import torch
+    from . import _native as nat
     m, n = A.rows, A.cols
     w = config.sketch_width
     if w > min(m, n):
         raise ValueError(f"sketch width {w} exceeds min(a.shape) = {min(m, n)}")
     ctx = nat.context(dev)
     st = nat.stream_ptr(dev)
-    om = device_omega(n, config, dev)  # column-major n x w
+    om = device_omega(n, config, dev) if omega is None else omega  # column-major n x w
     Y = nat.DevMat.empty(m, w, dev)
     with torch.cuda.device(dev):
         nat.call("psvd_nn_product", ctx, m, nat._vp(A.data_ptr()), A.ld, n, nat.ptr(om), n, w,

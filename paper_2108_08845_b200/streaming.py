@@ -255,7 +255,7 @@ RAND_STREAM_MAX_WIDTH = 32  # widest sketch of the pipelined randomized run (nar
 RAND_STREAM_MAX_K = 16      # most modes of the pipelined run (its U = Q W argmax kernel)
 
 
-def _run_rand_window(state, mats, config, dev, ready=None, supported=None):
+def _run_rand_window(state, mats, config, dev, ready=None, supported=None, redo_illcond=True):
     """Randomized updates over device batches `mats` through the pipelined
     psvd_rand_stream_run (SURVEY R9 per batch; the next batch's state-independent
     sketch overlaps the current small solves, U is written once at the end)."""
@@ -310,9 +310,18 @@ def _run_rand_window(state, mats, config, dev, ready=None, supported=None):
         nat.call("psvd_rand_stream_run", ctx, M, uptr, uld, sptr, kc, nb, A, lda, B, k, l, q,
                  float(config.forget_factor), Om, nat._vp(out.data_ptr()), out.ld, nat.ptr(hist), rd,
                  nat.stream_ptr(dev))
-        if _check_status(ctx, dev, "a_new") & nat.ST_NOCONVERGE:
+        status = _check_status(ctx, dev, "a_new")
+        if status & nat.ST_NOCONVERGE:
             from .errors import ConvergenceError
             raise ConvergenceError("randomized core SVD did not converge")
+        if status & nat.ST_SKETCHCOND and redo_illcond:
+            # a sketch of the window left the Gram-based orthonormalization's accuracy range: redo the window
+            # from its input state one update at a time (each one gated onto the accurate route as needed)
+            hist2 = []
+            for m in mats:
+                state = stream_initialize(m, config, dev) if state is None else stream_incorporate(state, m, config)
+                hist2.append(state.singular_values.clone())
+            return state, hist2
     it0 = -1 if state is None else state.iteration
     return StreamState(out.view, hist[nb - 1].clone(), it0 + nb), [hist[i] for i in range(nb)]
 

@@ -1,0 +1,54 @@
+"""Random small streams through stream_all (deterministic and randomized) against the oracle: shapes that reach
+the split-ring kernel (rows a multiple of 16) and ones that do not.  python tools/fuzz_stream.py [seed] [count]"""
+import random, sys
+import numpy as np
+import torch
+sys.path.insert(0, ".")
+import oracle
+import paper_2108_08845_b200 as p
+seed = int(sys.argv[1]) if len(sys.argv) > 1 else 0
+count = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+random.seed(seed)
+rng = np.random.Generator(np.random.Philox(seed))
+worst_s = worst_a = 0.0
+for it in range(count):
+    M = random.choice([16 * random.randint(20, 400), random.randint(300, 5000)])
+    K = random.randint(1, 16)
+    nb = random.randint(2, 6)
+    widths = [random.randint(max(K, 8), 120) for _ in range(nb)]
+    ff = random.choice([1.0, 0.95, 0.8])
+    rand = random.random() < 0.4
+    # a decaying spectrum so that modes are separated (angles are only defined for separated modes)
+    cols = sum(widths)
+    r = min(40, cols, M)
+    U, _ = np.linalg.qr(rng.standard_normal((M, r)))
+    V, _ = np.linalg.qr(rng.standard_normal((cols, r)))
+    a = (U * (2.0 ** -np.arange(r))) @ V.T + 1e-9 * rng.standard_normal((M, cols))
+    batches, c0 = [], 0
+    for w in widths:
+        batches.append(np.asfortranarray(a[:, c0:c0 + w]))
+        c0 += w
+    if rand:
+        q = random.randint(0, 1)
+        sk = p.RandomSketchConfig(target_rank=K, oversampling=min(8, min(widths) - K) if min(widths) > K else 0,
+                                  power_iterations=q, seed=seed)
+        if sk.sketch_width > min(M, min(widths)):
+            continue
+        cfg = p.StreamConfig(k_modes=K, forget_factor=ff, batch_columns=widths[0], sketch=sk)
+        ref_m, ref_s, _ = oracle.ref_rand_stream_all(batches, K, ff, sk.oversampling, q, seed)
+    else:
+        cfg = p.StreamConfig(k_modes=K, forget_factor=ff, batch_columns=widths[0])
+        ref_m, ref_s, _ = oracle.ref_stream_all(batches, K, ff)
+    st, _ = p.stream_all(batches, cfg)
+    m, s = st.numpy()
+    es = oracle.sigma_rel_err(s, ref_s)
+    gaps = np.array([min(abs(ref_s[j] - ref_s[i]) for i in range(K) if i != j) / ref_s[j] if K > 1 else 1.0
+                     for j in range(K)])
+    sel = (gaps > 1e-3) & (ref_s > 1e-6 * ref_s[0])
+    ang = oracle.mode_angles(m, ref_m)
+    ea = float(np.max(ang[sel])) if sel.any() else 0.0
+    worst_s, worst_a = max(worst_s, es), max(worst_a, ea)
+    if es > 1e-10 or ea > 1e-8:
+        print("FAIL", dict(M=M, K=K, widths=widths, ff=ff, rand=rand), es, ea)
+        sys.exit(1)
+print(f"{count} streams ok: worst sigma {worst_s:.2e}, worst angle {worst_a:.2e}")
