@@ -280,6 +280,17 @@ def _svd_tall(A, dev, want_vt):
             nat.call("psvd_nn_product", ctx, m, nat._vp(Q.data_ptr()), Q.ld, n, nat._vp(UR.data_ptr()), UR.ld, n,
                      nat._vp(U.data_ptr()), U.ld, st)
             Vb.T.copy_(VR.view)
+        # Left vectors of weak directions: u_j = a v_j / s_j is orthogonal to the others only to
+        # eps s_1 / s_j, and undefined for s_j = 0, while the reference's dgesdd returns an orthonormal u
+        # whatever the spectrum (linalg.py:107-123).  So when the spectrum spans more than 1e8, the columns
+        # of numerically null values are cleared and u is re-orthonormalized by our own qr (diag(r) >= 0:
+        # well-determined columns keep their direction and sign; null ones get an orthonormal completion).
+        sh = s.cpu()
+        if n > 1 and float(sh[-1]) < 1e-8 * float(sh[0]):
+            null = s <= (16.0 * n * torch.finfo(torch.float64).eps) * s[0]
+            if bool(null.any()):
+                U.view[:, null] = 0.0
+            U, _ = _tall_qr(U, dev)
         nat.call("psvd_sign_pair", ctx, nat._vp(U.data_ptr()), U.ld, m, n, nat.ptr(Vb), n, n, st)
     return U, s, Vb.T
 

@@ -315,3 +315,26 @@ def test_kernel_invariants_1000_matrices():
         worst = max(worst, float(np.max(np.abs(ref - s)) / (1 + s[0])))
     assert worst <= 1e-9
     assert time.perf_counter() - t0 < 120.0
+
+
+@pytest.mark.parametrize("m,n,kind", [(65, 48, "deficient"), (86, 48, "deficient"), (74, 64, "steep"),
+                                      (3000, 200, "deficient"), (500, 300, "steep")])
+def test_svd_weak_directions_keep_u_orthonormal(m, n, kind):
+    """Rank-deficient and steep inputs (found by tools/fuzz_linalg.py): u_j = a v_j / s_j is undefined for
+    s_j = 0 and orthogonal only to eps s_1 / s_j otherwise, while the reference's dgesdd returns orthonormal
+    factors whatever the spectrum (linalg.py:107-123).  The factors stay orthonormal, reconstruct a, and the
+    values above 1e-5 s_1 keep their relative accuracy."""
+    rng = _rng(300 + m + n)
+    r = n // 2 if kind == "deficient" else n
+    u0 = oracle.ref_qr(rng.standard_normal((m, r)))[0]
+    v0 = oracle.ref_qr(rng.standard_normal((n, r)))[0]
+    span = 1e-3 if kind == "deficient" else 1e-12
+    a = (u0 * span ** (np.arange(r) / (r - 1))) @ v0.T
+    res = _p().svd_full(a)
+    u, s, vt = _np(res.u), _np(res.s), _np(res.vt)
+    _, rs, _ = oracle.ref_svd(a)
+    assert np.max(np.abs(u.T @ u - np.eye(n))) < 1e-10 and np.max(np.abs(vt @ vt.T - np.eye(n))) < 1e-10
+    assert np.max(np.abs((u * s) @ vt - a)) < 1e-11 * np.abs(a).max()
+    assert np.all(np.diff(s) <= 0) and np.max(np.abs(s - rs)) < 1e-12 * rs[0]
+    big = rs > 1e-5 * rs[0]
+    assert np.max(np.abs(s[big] - rs[big]) / rs[big]) < 1e-10
