@@ -13,14 +13,14 @@ rng = np.random.Generator(np.random.Philox(seed))
 worst_s = worst_a = 0.0
 for it in range(count):
     M = random.choice([16 * random.randint(20, 400), random.randint(300, 5000)])
-    K = random.randint(1, 16)
+    K = random.choice([random.randint(1, 16), random.randint(17, 48)])
     nb = random.randint(2, 6)
-    widths = [random.randint(max(K, 8), 120) for _ in range(nb)]
+    widths = [random.randint(max(K, 8), random.choice([120, 300])) for _ in range(nb)]
     ff = random.choice([1.0, 0.95, 0.8])
     rand = random.random() < 0.4
     # a decaying spectrum so that modes are separated (angles are only defined for separated modes)
     cols = sum(widths)
-    r = min(40, cols, M)
+    r = min(random.choice([40, 90]), cols, M)
     U, _ = np.linalg.qr(rng.standard_normal((M, r)))
     V, _ = np.linalg.qr(rng.standard_normal((cols, r)))
     a = (U * (2.0 ** -np.arange(r))) @ V.T + 1e-9 * rng.standard_normal((M, cols))
@@ -30,7 +30,7 @@ for it in range(count):
         c0 += w
     if rand:
         q = random.randint(0, 1)
-        sk = p.RandomSketchConfig(target_rank=K, oversampling=min(8, min(widths) - K) if min(widths) > K else 0,
+        sk = p.RandomSketchConfig(target_rank=K, oversampling=min(random.choice([8, 12]), min(widths) - K) if min(widths) > K else 0,
                                   power_iterations=q, seed=seed)
         if sk.sketch_width > min(M, min(widths)):
             continue
@@ -41,7 +41,9 @@ for it in range(count):
         ref_m, ref_s, _ = oracle.ref_stream_all(batches, K, ff)
     st, _ = p.stream_all(batches, cfg)
     m, s = st.numpy()
-    es = oracle.sigma_rel_err(s, ref_s)
+    # relative error of each kept value, less what two backward-stable computations may differ by at that size
+    # (the reference's own LAPACK values carry O(eps s_1) absolute error)
+    es = float(np.max(np.abs(s - ref_s) / ref_s - 100 * np.finfo(float).eps * ref_s[0] / ref_s))
     gaps = np.array([min(abs(ref_s[j] - ref_s[i]) for i in range(K) if i != j) / ref_s[j] if K > 1 else 1.0
                      for j in range(K)])
     sel = (gaps > 1e-3) & (ref_s > 1e-6 * ref_s[0])
