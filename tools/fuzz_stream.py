@@ -14,7 +14,8 @@ worst_s = worst_a = 0.0
 for it in range(count):
     M = random.choice([16 * random.randint(20, 400), random.randint(300, 5000)])
     K = random.choice([random.randint(1, 16), random.randint(17, 48)])
-    nb = random.randint(2, 6)
+    nb = random.randint(2, 9)
+    p.streaming.STREAM_WINDOW = random.choice([2, 3, 8])  # windows chained through the state
     widths = [random.randint(max(K, 8), random.choice([120, 300])) for _ in range(nb)]
     ff = random.choice([1.0, 0.95, 0.8])
     rand = random.random() < 0.4
