@@ -259,8 +259,85 @@ def _parallel_rand_update(ctx, U, sigma, A, sketch, ff, dev):
     off, total = _row_offset(ctx, A.rows, dev, A.cols)
     if ctx.world_size == 1:
         return randomized_update(U, sigma, A, sketch, ff, dev)
+    redo = []
     with exchange_hooks(ctx, dev, off):
-        return randomized_update(U, sigma, A, sketch, ff, dev, total_rows=total, accurate=False)
+        # PSVD_ST_SKETCHCOND comes from the summed Grams (identical bits on every rank), so every
+        # rank asks for the redo together; it runs after the hooks of the fast update are released
+        res = randomized_update(U, sigma, A, sketch, ff, dev, total_rows=total,
+                                accurate=lambda: redo.append(True))
+    if redo:
+        return _parallel_accurate_rand_update(ctx, U, sigma, A, sketch, ff, dev, off)
+    return res
+
+
+def _parallel_accurate_rand_update(ctx, U, sigma, A, sketch, ff, dev, off):
+    """The row-partitioned randomized step on the accurate route (linalg.accurate_randomized_update
+    with the rows spread over the ranks): the reference's sequence (linalg.py:126-162) with a
+    backward-stable qr after every product.  Tall factors (the sketch y = c omega, every power
+    iteration's c z) are orthonormalized by parallel_qr; the small ones (z = c^T q, b^T = c^T q)
+    are rank-ordered sums of the local products, so every rank factors identical bits; the tall
+    sign rule takes the global argmax (ties: the lower global row, linalg.py:81-91)."""
+    from . import linalg
+    linalg.ACCURATE_RAND_UPDATES += 1
+    k, l = sketch.target_rank, sketch.sketch_width
+    kc = 0 if U is None else U.cols
+    M, n = A.rows, kc + A.cols
+    c, st = nat.context(dev), nat.stream_ptr(dev)
+    om = linalg.device_omega(n, sketch, dev)
+
+    def nn(X, W, w):  # X (M x X.cols) times a column-major X.cols x w device matrix: local rows only
+        wp, wld = (nat.ptr(W), W.shape[-1]) if torch.is_tensor(W) else (nat._vp(W.data_ptr()), W.ld)
+        Y = nat.DevMat.empty(M, w, dev)
+        nat.call("psvd_nn_product", c, M, nat._vp(X.data_ptr()), X.ld, X.cols, wp, wld, w,
+                 nat._vp(Y.data_ptr()), Y.ld, st)
+        return Y
+
+    def tn(X, Q):  # X^T Q summed over the ranks: (n x l) column-major, the same bits everywhere
+        Z = torch.empty((l, n), dtype=torch.float64, device=dev)
+        nat.call("psvd_tn_product", c, M, nat._vp(X.data_ptr()), X.ld, n, nat._vp(Q.data_ptr()), Q.ld, l,
+                 nat.ptr(Z), n, st)
+        return allreduce_ordered(Z, ctx)
+
+    with torch.cuda.device(dev):
+        C = nat.DevMat.empty(M, n, dev)
+        if kc:
+            torch.mul(U.view, (ff * sigma)[None, :], out=C.view[:, :kc])
+        C.view[:, kc:].copy_(A.view)
+        q = nat.as_device_colmajor(parallel_qr(ctx, nn(C, om, l).view, dev).q, dev, "q")
+        for _ in range(sketch.power_iterations):
+            Z = nat.as_device_colmajor(tn(C, q).t(), dev, "z")
+            z, _ = linalg._tall_qr(Z, dev)
+            q = nat.as_device_colmajor(parallel_qr(ctx, nn(C, z, l).view, dev).q, dev, "q")
+        res = linalg.svd_full(tn(C, q).t(), want_vt=True, device=dev)  # b^T = u s vt: b's left vectors are vt's rows
+        W = torch.empty((k, l), dtype=torch.float64, device=dev)       # (l x k) column-major = vt[:k]^T
+        W.copy_(res.vt[:k, :])
+        out = nn(q, W, k)
+        _sign_by_global_peak(ctx, out, off, dev)
+        sig = res.s[:k].clone()
+        status = nat.read_status(c, reset=True, device=dev)
+    if status & nat.ST_NONFINITE:
+        raise ValueError("a_local contains non-finite entries")
+    return out, sig
+
+
+def _sign_by_global_peak(ctx, X, off, dev):
+    """linalg.py:81-91 on the row-stacked matrix: each column's largest-|.| entry over all ranks
+    (ties keep the lower global row: the lower rank, then torch's first maximal index) made
+    positive.  X: this rank's rows (DevMat), flipped in place."""
+    k = X.cols
+    v = X.view
+    if X.rows:
+        idx = torch.argmax(v.abs(), dim=0)
+        mine = v[idx, torch.arange(k, device=dev)]
+    else:
+        mine = torch.zeros(k, dtype=torch.float64, device=dev)
+    peaks = torch.zeros((ctx.world_size, k), dtype=torch.float64, device=dev)
+    peaks[ctx.rank] = mine
+    peaks = allreduce_ordered(peaks, ctx)          # one rank's value per row, zeros elsewhere: exact
+    best = torch.argmax(peaks.abs(), dim=0)        # first maximal value: the lowest rank
+    signs = torch.sign(peaks[best, torch.arange(k, device=dev)])
+    signs[signs == 0.0] = 1.0
+    v.mul_(signs[None, :])
 
 
 def _parallel_update(ctx, U, sigma, A, k, ff, dev):
@@ -427,9 +504,8 @@ def parallel_stream_all(ctx, batches_local, config, device=None):
         if sk is None:
             state, h = _run_window(state, window, config, dev, rescue=False, ok=True, on_illcond=per_batch)
         else:
-            # (the accurate randomized route is single-rank: with more ranks the pipelined result stands)
             state, h = _run_rand_window(state, window, config, dev, supported=True,
-                                        redo_illcond=ctx.world_size == 1)
+                                        on_illcond=per_batch if ctx.world_size > 1 else None)
         hist.extend(h)
 
     try:

@@ -111,7 +111,8 @@ def randomized_update(U, sigma, A, sketch, ff, device, check=True, total_rows=No
     accurate: redo the step on accurate_randomized_update when the device reports
     PSVD_ST_SKETCHCOND (a sketch direction at or below 3e-7 of the largest: the Gram-based
     orthonormalization no longer reproduces the reference's Householder qr to 1e-10); the
-    row-partitioned callers pass False (that route is single-rank).
+    row-partitioned caller passes its own redo (a callable: dsvd._parallel_accurate_rand_update,
+    the same sequence with the products summed over the ranks).
     Returns (DevMat M x K, sigma (K,))."""
     import torch
     from . import _native as nat
@@ -139,6 +140,8 @@ def randomized_update(U, sigma, A, sketch, ff, device, check=True, total_rows=No
                 from .errors import ConvergenceError
                 raise ConvergenceError("randomized core SVD did not converge")
             if accurate and (st & nat.ST_SKETCHCOND):
+                if callable(accurate):
+                    return accurate()
                 return accurate_randomized_update(U, sigma, A, sketch, ff, device, omega=omega)
     return out, sig
 

@@ -255,7 +255,7 @@ RAND_STREAM_MAX_WIDTH = 32  # widest sketch of the pipelined randomized run (nar
 RAND_STREAM_MAX_K = 16      # most modes of the pipelined run (its U = Q W argmax kernel)
 
 
-def _run_rand_window(state, mats, config, dev, ready=None, supported=None, redo_illcond=True):
+def _run_rand_window(state, mats, config, dev, ready=None, supported=None, on_illcond=None):
     """Randomized updates over device batches `mats` through the pipelined
     psvd_rand_stream_run (SURVEY R9 per batch; the next batch's state-independent
     sketch overlaps the current small solves, U is written once at the end)."""
@@ -314,9 +314,12 @@ def _run_rand_window(state, mats, config, dev, ready=None, supported=None, redo_
         if status & nat.ST_NOCONVERGE:
             from .errors import ConvergenceError
             raise ConvergenceError("randomized core SVD did not converge")
-        if status & nat.ST_SKETCHCOND and redo_illcond:
+        if status & nat.ST_SKETCHCOND:
             # a sketch of the window left the Gram-based orthonormalization's accuracy range: redo the window
-            # from its input state one update at a time (each one gated onto the accurate route as needed)
+            # from its input state one update at a time (each one gated onto the accurate route as needed);
+            # on_illcond(state, mats) is the row-parallel caller's redo
+            if on_illcond is not None:
+                return on_illcond(state, mats)
             hist2 = []
             for m in mats:
                 state = stream_initialize(m, config, dev) if state is None else stream_incorporate(state, m, config)

@@ -84,3 +84,65 @@ def test_low_rank_svd_of_a_steep_matrix():
     res = p.low_rank_svd(a, sk)
     u, s, vt = oracle.ref_low_rank_svd(a, 10, 10, 0, 0)
     _check(res.u.cpu().numpy(), res.s.cpu().numpy(), u, s)
+
+
+def _steep_rank_worker(rank, world, port, q, span, qit):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2108_08845_b200 as p
+        from paper_2108_08845_b200 import linalg
+        b = _steep(span)
+        lo, hi = p.partition_bounds(b[0].shape[0], world)[rank]
+        sk = p.RandomSketchConfig(target_rank=10, oversampling=10, power_iterations=qit, seed=0)
+        cfg = p.StreamConfig(k_modes=10, forget_factor=0.95, batch_columns=200, sketch=sk)
+        ctx = p.RankContext()
+        n0 = linalg.ACCURATE_RAND_UPDATES
+        st, hist = p.parallel_stream_all(ctx, [m[lo:hi] for m in b], cfg)      # pipelined, redone when gated
+        n1 = linalg.ACCURATE_RAND_UPDATES
+        st2 = p.parallel_stream_initialize(ctx, b[0][lo:hi], cfg)              # the per-update calls
+        st2 = p.parallel_stream_incorporate(ctx, st2, b[1][lo:hi], cfg)
+        full, full2 = p.gather_modes(ctx, st), p.gather_modes(ctx, st2)
+        q.put((rank, st.singular_values.cpu().numpy(), st2.singular_values.cpu().numpy(),
+               None if full is None else full.cpu().numpy(), None if full2 is None else full2.cpu().numpy(),
+               (n1 - n0, linalg.ACCURATE_RAND_UPDATES - n1, len(hist))))
+    except Exception as e:
+        q.put((rank, "error", repr(e), None, None, None))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("span,qit", [(1e-8, 0), (1e-10, 1)])
+def test_steep_sketch_row_partitioned_takes_accurate_route(span, qit):
+    """The gate on the row-partitioned path (two processes sharing this GPU, gloo): the status bit comes
+    from the summed Grams, so both ranks redo the update together on dsvd._parallel_accurate_rand_update
+    (parallel_qr after every tall product, rank-ordered sums of the small ones, global sign rule); the
+    result meets the bar against the serial R9 oracle with the reference's signs."""
+    import socket
+    import torch.multiprocessing as mp
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_steep_rank_worker, args=(r, 2, port, q, span, qit)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = {}
+    for _ in range(2):
+        rank, s1, s2, full, full2, counts = q.get(timeout=300)
+        assert not (isinstance(s1, str) and s1 == "error"), s2
+        out[rank] = (s1, s2, full, full2, counts)
+    for pr in procs:
+        pr.join(timeout=120)
+    assert all(pr.exitcode == 0 for pr in procs)
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert out[0][4][0] > 0 and out[0][4][1] > 0 and out[0][4][2] == 2
+    ref_m, ref_s, _ = oracle.ref_rand_stream_all(_steep(span), 10, 0.95, 10, qit, 0)
+    _check(out[0][2], out[0][0], ref_m, ref_s)
+    _check(out[0][3], out[0][1], ref_m, ref_s)
