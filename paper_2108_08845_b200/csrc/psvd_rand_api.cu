@@ -91,8 +91,10 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
   const int n = Kc + B;
   int rc;
   if (M < 1 || B < 1 || Kc < 0 || K < 1 || l < K || q < 0) return fail(c, PSVD_EINVAL, "bad randomized shape");
-  if (l > std::min<int64_t>(M, n))
-    return fail(c, PSVD_EINVAL, "sketch width %d exceeds min(a.shape) = %lld", l, (long long)std::min<int64_t>(M, n));
+  // (row-partitioned: M is this rank's block, which may be shorter than the sketch; the caller checks the global rows)
+  const int64_t rows_chk = ex_active(c) ? std::max<int64_t>(M, l) : M;
+  if (l > std::min<int64_t>(rows_chk, n))
+    return fail(c, PSVD_EINVAL, "sketch width %d exceeds min(a.shape) = %lld", l, (long long)std::min<int64_t>(rows_chk, n));
   if ((rc = check_mat(c, "U", U, ldu, M, Kc)) || (rc = check_mat(c, "A", A, lda, M, B)) ||
       (rc = check_mat(c, "U_out", U_out, ldo, M, K)))
     return rc;
@@ -311,8 +313,9 @@ int psvd_rand_stream_run(psvd_ctx* c, int64_t M, const double* U_in, int64_t ldu
     if (B[b] < 1) return fail(c, PSVD_EINVAL, "empty batch");
     if (!Omega[b]) return fail(c, PSVD_EINVAL, "null Omega");
     const int n = ((b > 0 || Kc > 0) ? K : 0) + B[b];
-    if (l > std::min<int64_t>(M, n))
-      return fail(c, PSVD_EINVAL, "sketch width %d exceeds min(a.shape) = %lld", l, (long long)std::min<int64_t>(M, n));
+    const int64_t rows_chk = ex_active(c) ? std::max<int64_t>(M, l) : M;  // row-partitioned: the caller checks the global rows
+    if (l > std::min<int64_t>(rows_chk, n))
+      return fail(c, PSVD_EINVAL, "sketch width %d exceeds min(a.shape) = %lld", l, (long long)std::min<int64_t>(rows_chk, n));
     bmax = std::max(bmax, B[b]);
   }
   if (Kc == 0 && B[0] < K) return fail(c, PSVD_EINVAL, "initial batch has %d columns, need at least k_modes=%d", B[0], K);

@@ -457,7 +457,7 @@ def parallel_stream_all(ctx, batches_local, config, device=None):
             wl = wl.to(dev)
         dist.all_reduce(wl, op=dist.ReduceOp.MIN, group=ctx.group)
         wlen = int(wl.item())
-    off = None
+    off = total = None
     ex = None  # exchange_hooks, entered at the first pipelined window
     state, hist = None, []
 
@@ -481,7 +481,7 @@ def parallel_stream_all(ctx, batches_local, config, device=None):
                 ex.resume()
 
     def run(window):
-        nonlocal state, off, ex
+        nonlocal state, off, total, ex
         M = window[0].rows
         ok = ctypes.c_int(0)
         if sk is None:
@@ -498,14 +498,15 @@ def parallel_stream_all(ctx, batches_local, config, device=None):
             hist.extend(h)
             return
         if off is None:
-            off, _ = _row_offset(ctx, M, dev)
+            off, total = _row_offset(ctx, M, dev)
             if ctx.world_size > 1:
                 ex = exchange_hooks(ctx, dev, off).__enter__()
         if sk is None:
-            state, h = _run_window(state, window, config, dev, rescue=False, ok=True, on_illcond=per_batch)
+            state, h = _run_window(state, window, config, dev, rescue=False, ok=True, on_illcond=per_batch,
+                                   total_rows=total)
         else:
             state, h = _run_rand_window(state, window, config, dev, supported=True,
-                                        on_illcond=per_batch if ctx.world_size > 1 else None)
+                                        on_illcond=per_batch if ctx.world_size > 1 else None, total_rows=total)
         hist.extend(h)
 
     try:

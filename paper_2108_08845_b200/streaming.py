@@ -182,13 +182,14 @@ def window_length(batch, device):
     return int(max(2, min(cap, (STREAM_WINDOW_MEM_FRACTION * total) // max(nbytes, 1))))
 
 
-def _run_window(state, mats, config, dev, ready=None, rescue=True, ok=None, on_illcond=None):
+def _run_window(state, mats, config, dev, ready=None, rescue=True, ok=None, on_illcond=None, total_rows=None):
     """Deterministic updates over device batches `mats` with look-ahead
     (psvd_stream_run): the next batch's A^T A overlaps the current core solve.
     `ready`: per-batch upload events (or None) the device work waits on.  When an update
     of the window trips the Gram route's conditioning gate, the window is redone batch by
     batch from its input state: on_illcond(state, mats) (the row-parallel caller), else the
-    serial per-update path with its accurate route."""
+    serial per-update path with its accurate route.  total_rows: rows of the whole row-partitioned
+    panel (the shape checks are the global matrix's; a rank's block may be shorter than K)."""
     k = config.k_modes
     M = mats[0].rows
     for m in mats:
@@ -196,8 +197,9 @@ def _run_window(state, mats, config, dev, ready=None, rescue=True, ok=None, on_i
             raise ValueError(f"batch rows {m.rows} != mode rows {M}")
     if state is None and mats[0].cols < k:
         raise ValueError(f"initial batch has {mats[0].cols} columns, need at least k_modes={k}")
-    if state is None and M < k:
-        raise ValueError(f"initial batch has {M} rows, need at least k_modes={k}")
+    rows = M if total_rows is None else total_rows
+    if state is None and rows < k:
+        raise ValueError(f"initial batch has {rows} rows, need at least k_modes={k}")
     ctx = nat.context(dev)
     nb = len(mats)
     if ok is None:
@@ -255,7 +257,7 @@ RAND_STREAM_MAX_WIDTH = 32  # widest sketch of the pipelined randomized run (nar
 RAND_STREAM_MAX_K = 16      # most modes of the pipelined run (its U = Q W argmax kernel)
 
 
-def _run_rand_window(state, mats, config, dev, ready=None, supported=None, on_illcond=None):
+def _run_rand_window(state, mats, config, dev, ready=None, supported=None, on_illcond=None, total_rows=None):
     """Randomized updates over device batches `mats` through the pipelined
     psvd_rand_stream_run (SURVEY R9 per batch; the next batch's state-independent
     sketch overlaps the current small solves, U is written once at the end)."""
@@ -270,8 +272,9 @@ def _run_rand_window(state, mats, config, dev, ready=None, supported=None, on_il
         raise ValueError(f"initial batch has {mats[0].cols} columns, need at least k_modes={k}")
     for i, m in enumerate(mats):
         n = (k if (state is not None or i > 0) else 0) + m.cols
-        if l > min(M, n):
-            raise ValueError(f"sketch width {l} exceeds min(a.shape) = {min(M, n)}")
+        rows = M if total_rows is None else total_rows  # the row-partitioned panel's check is global
+        if l > min(rows, n):
+            raise ValueError(f"sketch width {l} exceeds min(a.shape) = {min(rows, n)}")
     ctx = nat.context(dev)
     nb = len(mats)
     ok = ctypes.c_int(1 if supported else 0)

@@ -318,3 +318,62 @@ def test_parallel_stream_matches_direct_on_gapped_spectrum():
     assert oracle.sigma_rel_err(s, rs) <= SIG_TOL
     assert np.max(oracle.mode_angles(full, rm)) <= ANG_TOL
     assert np.all(np.sum(full * rm, axis=0) > 0)
+
+
+def _short_block_worker(rank, world, port, q, rand):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2108_08845_b200 as p
+        a = p.synthetic_spectrum_matrix(42, 120, 2.0 ** -np.arange(30), seed=5)
+        lo, hi = p.partition_bounds(42, world)[rank]
+        sk = p.RandomSketchConfig(target_rank=12, oversampling=8, power_iterations=1, seed=3) if rand else None
+        cfg = p.StreamConfig(k_modes=20 if not rand else 12, forget_factor=0.95, batch_columns=40, sketch=sk)
+        ctx = p.RankContext()
+        st, hist = p.parallel_stream_all(ctx, [a[lo:hi, c:c + 40] for c in (0, 40, 80)], cfg)
+        full = p.gather_modes(ctx, st)
+        q.put((rank, st.singular_values.cpu().numpy(), None if full is None else full.cpu().numpy(), len(hist)))
+    except Exception as e:
+        q.put((rank, "error", repr(e), 0))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("rand", [False, True])
+def test_parallel_stream_all_short_blocks(rand):
+    """The streaming counterpart of test_dsvd.py:196-211 (short blocks), found by tools/fuzz_parallel.py: 42
+    rows over three ranks leave 14-row blocks, fewer than K = 20 (sketch width 20): the shape checks of the
+    pipelined windows are the global matrix's, and the result is the serial stream's at the bar."""
+    import socket
+    import torch.multiprocessing as mp
+    s_ = socket.socket()
+    s_.bind(("127.0.0.1", 0))
+    port = s_.getsockname()[1]
+    s_.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_short_block_worker, args=(r, 3, port, q, rand)) for r in range(3)]
+    for pr in procs:
+        pr.start()
+    out = {}
+    for _ in range(3):
+        rank, s, full, nh = q.get(timeout=300)
+        assert not (isinstance(s, str) and s == "error"), full
+        out[rank] = (s, full, nh)
+    for pr in procs:
+        pr.join(timeout=120)
+    assert all(pr.exitcode == 0 for pr in procs)
+    p = _p()
+    a = p.synthetic_spectrum_matrix(42, 120, 2.0 ** -np.arange(30), seed=5)
+    b = [a[:, c:c + 40] for c in (0, 40, 80)]
+    rm, rs, _ = oracle.ref_rand_stream_all(b, 12, 0.95, 8, 1, 3) if rand else oracle.ref_stream_all(b, 20, 0.95)
+    s, full, nh = out[0]
+    assert nh == 3 and np.array_equal(s, out[1][0]) and np.array_equal(s, out[2][0])
+    assert oracle.sigma_rel_err(s, rs) <= SIG_TOL
+    live = rs > 1e-6 * rs[0]
+    assert np.max(oracle.mode_angles(full, rm)[live]) <= ANG_TOL
+    assert np.all(np.sum(full * rm, axis=0)[live] > 0)
