@@ -23,12 +23,19 @@ def cases(seed, count):
         r = min(random.choice([40, 90]), cols, M)
         U, _ = np.linalg.qr(rng.standard_normal((M, r)))
         V, _ = np.linalg.qr(rng.standard_normal((cols, r)))
-        a = (U * (2.0 ** -np.arange(r))) @ V.T + 1e-9 * rng.standard_normal((M, cols))
+        kind = random.choice(["decay", "decay", "steep", "gauss"])
+        if kind == "decay":
+            a = (U * (2.0 ** -np.arange(r))) @ V.T + 1e-9 * rng.standard_normal((M, cols))
+        elif kind == "steep":   # spans that trip the conditioning gates (the accurate routes across ranks)
+            a = (U * (random.choice([1e-6, 1e-9, 1e-12]) ** (np.arange(r) / max(r - 1, 1)))) @ V.T
+        else:
+            a = rng.standard_normal((M, cols))
+        per_update = random.random() < 0.3
         batches, c0 = [], 0
         for w in widths:
             batches.append(np.asfortranarray(a[:, c0:c0 + w]))
             c0 += w
-        yield dict(M=M, K=K, widths=widths, ff=ff, rand=rand, q=q, over=over, win=win), batches
+        yield dict(M=M, K=K, widths=widths, ff=ff, rand=rand, q=q, over=over, win=win, kind=kind, per_update=per_update), batches
 
 
 def worker(rank, world, port, seed, count, out):
@@ -53,7 +60,14 @@ def worker(rank, world, port, seed, count, out):
             p.streaming.STREAM_WINDOW = p.streaming.STREAM_WINDOW_RESIDENT = c["win"]
             cfg = p.StreamConfig(k_modes=K, forget_factor=ff, batch_columns=c["widths"][0], sketch=sk)
             lo, hi = p.partition_bounds(c["M"], world)[rank]
-            st, hist = p.parallel_stream_all(ctx, [b[lo:hi] for b in batches], cfg)
+            if c["per_update"]:
+                st = p.parallel_stream_initialize(ctx, batches[0][lo:hi], cfg)
+                hist = [st.singular_values]
+                for b in batches[1:]:
+                    st = p.parallel_stream_incorporate(ctx, st, b[lo:hi], cfg)
+                    hist.append(st.singular_values)
+            else:
+                st, hist = p.parallel_stream_all(ctx, [b[lo:hi] for b in batches], cfg)
             full = p.gather_modes(ctx, st)
             done += 1
             if rank:

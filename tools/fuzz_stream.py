@@ -1,5 +1,5 @@
 """Random small streams through stream_all (deterministic and randomized) against the oracle: shapes that reach
-the split-ring kernel (rows a multiple of 16) and ones that do not.  python tools/fuzz_stream.py [seed] [count]"""
+the split-ring kernel (rows a multiple of 16) and ones that do not.  python tools/fuzz_stream.py [seed] [count] [mixed]"""
 import random, sys
 import numpy as np
 import torch
@@ -24,7 +24,13 @@ for it in range(count):
     r = min(random.choice([40, 90]), cols, M)
     U, _ = np.linalg.qr(rng.standard_normal((M, r)))
     V, _ = np.linalg.qr(rng.standard_normal((cols, r)))
-    a = (U * (2.0 ** -np.arange(r))) @ V.T + 1e-9 * rng.standard_normal((M, cols))
+    kind = random.choice(["decay", "decay", "steep", "gauss"]) if len(sys.argv) > 3 else "decay"   # any 3rd argument: mixed spectra
+    if kind == "decay":
+        a = (U * (2.0 ** -np.arange(r))) @ V.T + 1e-9 * rng.standard_normal((M, cols))
+    elif kind == "steep":   # spans that trip the conditioning gates
+        a = (U * (random.choice([1e-6, 1e-9, 1e-12]) ** (np.arange(r) / max(r - 1, 1)))) @ V.T
+    else:
+        a = rng.standard_normal((M, cols))
     batches, c0 = [], 0
     for w in widths:
         batches.append(np.asfortranarray(a[:, c0:c0 + w]))
@@ -52,6 +58,6 @@ for it in range(count):
     ea = float(np.max(ang[sel])) if sel.any() else 0.0
     worst_s, worst_a = max(worst_s, es), max(worst_a, ea)
     if es > 1e-10 or ea > 1e-8:
-        print("FAIL", dict(M=M, K=K, widths=widths, ff=ff, rand=rand), es, ea)
+        print("FAIL", dict(M=M, K=K, widths=widths, ff=ff, rand=rand, kind=kind), es, ea)
         sys.exit(1)
 print(f"{count} streams ok: worst sigma {worst_s:.2e}, worst angle {worst_a:.2e}")
