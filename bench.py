@@ -25,6 +25,13 @@ import sys
 import threading
 import time
 
+if "reference" in sys.argv and "TORCHELASTIC_RUN_ID" in os.environ:
+    # torchrun exports OMP_NUM_THREADS=1 to its workers and the BLAS reads it when numpy loads: the reference
+    # arm uses every host thread at any N (blas_threads() below raises the pool again in any case)
+    for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
+        if os.environ.get(_v) == "1":
+            os.environ[_v] = str(len(os.sched_getaffinity(0)))
+
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -214,6 +221,18 @@ def host_config2(rows):
     return a
 
 
+def blas_threads():
+    """Give numpy's BLAS / LAPACK every host thread this process may use and return the count it runs with."""
+    want = len(os.sched_getaffinity(0))
+    try:
+        from threadpoolctl import threadpool_info, threadpool_limits
+        threadpool_limits(limits=want)
+        got = [i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") in ("blas", "openmp")]
+        return max(got) if got else want
+    except Exception:
+        return want
+
+
 def run_reference(a):
     """The reference's CPU path (the oracle port of streaming.py / the R9 composition, numpy
     LAPACK on every host thread) on the SAME config as our arm: all 2^20 grid rows.  One step is
@@ -249,6 +268,7 @@ def run_reference(a):
             state["b"] = (b + 1) % nb
         return one
 
+    cores = blas_threads()
     warm = cycle(small)
     for _ in range(a.warmup):
         warm()
@@ -260,7 +280,6 @@ def run_reference(a):
         times.append(time.perf_counter() - t0)
     dt = float(np.mean(times))
     value = 8.0 * rows * BATCH / dt / 1e9  # snapshot bytes of one batch per step
-    cores = os.cpu_count()
     line = {
         "impl": "reference", "metric": metric_name(a.path), "value": round(value, 4), "unit": "GB/s",
         "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(dt * 1e3, 2),
@@ -526,8 +545,8 @@ def run_ours(a):
             line["weak_scaling"] = {"error": repr(e)[:300]}
 
     if world == 1 and rank == 0 and not a.no_cpu:
+        cores = blas_threads()
         g, dt = cpu_reference_gbs(a.cpu_rows, a.path)  # bounded row sample; --impl reference runs all rows
-        cores = os.cpu_count()
         line["cpu_baseline"] = {"value": round(g, 4), "unit": "GB/s", "cores": cores, "kind": "port",
                                 "sample": f"first {a.cpu_rows} grid rows x {SNAPS} snapshots, init + 3 incorporates"
                                           f" ({dt:.1f} s; oracle/core.py numpy LAPACK, {cores} threads)"}
