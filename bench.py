@@ -593,8 +593,16 @@ def time_randomized(a, D, M, dev, c, stream, q):
     ms = t0.elapsed_time(t1) / a.steps
     passes = 2 * (q + 1)
     alg = sum(8.0 * M * (passes * (BATCH + (0 if b == 0 else K)) + K) for b in range(SNAPS // BATCH))
+    # FP64 flops of the R9 composition per update and sketch round: C Omega and C^T Q (2 M n l each), the two
+    # orthonormalization Grams (M l^2 each, symmetric) and Y T (2 M l^2); U = Q W (2 M l K) once per stream
+    flops = sum((q + 1) * M * (4.0 * (BATCH + (0 if b == 0 else K)) * l + 4.0 * l * l) for b in range(nb)) \
+        + 2.0 * M * l * K
     return {"value": round(8.0 * a.rows * SNAPS / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "ms_per_step": round(ms, 4),
-            "sketch": f"K={K} p=10 q={q} seed=0", "hbm_frac": round(alg / (ms * 1e-3) / 1e9 / HBM_PEAK[0], 4)}
+            "sketch": f"K={K} p=10 q={q} seed=0", "hbm_frac": round(alg / (ms * 1e-3) / 1e9 / HBM_PEAK[0], 4),
+            "fp64_frac": round(flops / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
+            "fp64_frac_issued": round(flops * 24.0 / l / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
+            "note": "both roofs at once: algorithmic bytes over the measured HBM peak, useful FP64 flops over the "
+                    "measured DMMA peak; issued = with the sketch's 20 columns padded to three 8-wide DMMA tiles"}
 
 
 def self_check(sigma_dev, a, world):
