@@ -216,6 +216,7 @@ struct JacobiArgs {
   int64_t ldu;
   int* status;
   int* sweeps_out;
+  int presort;       // pair order by decreasing initial column norm
 };
 
 __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(JacobiArgs a) {
@@ -230,6 +231,25 @@ __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(JacobiArgs a) {
   for (size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x; idx < (size_t)n * n;
        idx += (size_t)gridDim.x * blockDim.x)
     a.V[idx] = (idx % n == idx / n) ? 1.0 : 0.0;
+  // pair order by decreasing initial column norm (de Rijk): on a matrix graded the other way (small columns
+  // first, e.g. Burgers rows near x = 1, whose early snapshots are ~1e-80) the cyclic sweeps otherwise stall
+  for (int j = gwarp; j < n; j += nwarps) {
+    const double* xj = a.X + (size_t)j * m;
+    double s = 0.0;
+    for (int64_t k = lane; k < m; k += 32) s = fma(xj[k], xj[k], s);
+    s = warp_sum(s);
+    if (lane == 0) a.norms[j] = s;
+  }
+  grid.sync();
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const double sj = a.norms[j];
+    int rank = 0;
+    for (int i = 0; i < n; ++i) {
+      const double si = a.norms[i];
+      rank += (si > sj) || (si == sj && i < j);
+    }
+    a.perm[a.presort ? rank : j] = j;
+  }
   grid.sync();
   __shared__ int rotated;
   int sweep = 0;
@@ -242,6 +262,8 @@ __global__ void __launch_bounds__(JB_THREADS) jacobi_big_kernel(JacobiArgs a) {
         int i, j;
         rr_pair(r, p, np, i, j);
         if (j >= n) continue;
+        i = a.perm[i];
+        j = a.perm[j];
         double* xi = a.X + (size_t)i * m;
         double* xj = a.X + (size_t)j * m;
         double s_ii = 0.0, s_jj = 0.0, s_ij = 0.0;
@@ -373,7 +395,8 @@ int launch_jacobi_big(const double* X, int64_t ldx, int64_t m, int n, int transp
   double* norms = Vw + (size_t)n * n;
   int* perm = (int*)(norms + n);
   int* flags = (int*)(norms + 2 * (size_t)n);
-  const int max_sweeps = 60;
+  static const char* env_sweeps = getenv("PSVD_JACOBI_SWEEPS");  // diagnostics (at most 128: the flags' room)
+  const int max_sweeps = env_sweeps ? std::max(1, std::min(128, atoi(env_sweeps))) : 100;
   const size_t total = (size_t)m * n;
   pack_cols_kernel<<<(unsigned)std::min<size_t>((total + 255) / 256, 4096), 256, 0, st>>>(X, ldx, m, n, Xw,
                                                                                           transpose);
@@ -399,6 +422,8 @@ int launch_jacobi_big(const double* X, int64_t ldx, int64_t m, int n, int transp
   a.ldu = ldu;
   a.status = status;
   a.sweeps_out = sweeps_out;
+  static const char* env_presort = getenv("PSVD_JACOBI_PRESORT");  // diagnostics: 0 = the plain cyclic order
+  a.presort = env_presort ? atoi(env_presort) != 0 : 1;
   void* args[] = {&a};
   return (int)cudaLaunchCooperativeKernel((const void*)jacobi_big_kernel, dim3(grid), dim3(JB_THREADS), args, 0, st);
 }

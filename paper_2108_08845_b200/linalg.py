@@ -247,10 +247,41 @@ def _svd_tall(A, dev, want_vt):
     Vb = torch.empty((n, n), dtype=torch.float64, device=dev)  # column-major V: Vb.T
     U = nat.DevMat.empty(m, n, dev)
     with torch.cuda.device(dev):
+        # Graded columns (norms spanning more than 1e3) are factored in order of decreasing norm, the
+        # pre-sorting of preconditioned Jacobi (Drmac-Veselic): without it a matrix whose small columns
+        # come first (Burgers rows near x = 1: the early snapshots are ~1e-80) leaves R row-graded the
+        # wrong way for the column rotations, and the sweeps stall (ConvergenceError where the
+        # reference's dgesdd, linalg.py:107-123, converges).  V's rows are put back at the end.
+        perm = colscale = None
+        if n > 1:
+            cn = torch.linalg.vector_norm(A.view, dim=0)
+            if float(cn.min()) < 1e-3 * float(cn.max()):
+                order = torch.argsort(cn, descending=True, stable=True)
+                if not bool((order == torch.arange(n, device=dev)).all()):
+                    perm = order
+                    Ap = nat.DevMat.empty(m, n, dev)
+                    Ap.view.copy_(A.view[:, perm])
+                    A = Ap
+                    cn = cn[perm]
+                # ... and their QR is taken of the unit-norm columns, R's columns scaled back (exact in the
+                # scaling: a = (a D^-1) D): the scaled matrix is as well conditioned as column scaling makes
+                # it (van der Sluis), so CholeskyQR2 returns the triangular, properly graded R a Householder
+                # QR would; the rank-robust route on the unscaled columns leaves rounding-level rows in R that
+                # the sweeps cannot resolve (stall on gradings past ~1e-60)
+                colscale = torch.where(cn > 0, cn, torch.ones_like(cn))
+
+        def graded_qr(X):
+            if colscale is None:
+                return _tall_qr(X, dev)
+            Xs = nat.DevMat.empty(m, n, dev)
+            torch.div(X.view, colscale[None, :], out=Xs.view)
+            Q, R = _tall_qr(Xs, dev)
+            return Q, R * colscale[None, :]
+
         if n <= QR_SMEM_COLS:
             # QR-preconditioned one-sided Jacobi: A = Q R, R = U_R S V^T, U = Q U_R
             if m > n:
-                Q, R = _tall_qr(A, dev)
+                Q, R = graded_qr(A)
                 Rm = nat.as_device_colmajor(R, dev, "r")
             else:
                 Q, Rm = None, A
@@ -274,7 +305,7 @@ def _svd_tall(A, dev, want_vt):
             # Jacobi on R^T (psvd_big.cu): R^T J = U~ S gives R = J S U~^T, so U_R = J (the
             # accumulated rotations) and V_R = U~; U = Q U_R.  Relative accuracy on every
             # singular value, as dgesdd of the reference's R (linalg.py:107-123).
-            Q, R = _tall_qr(A, dev)
+            Q, R = graded_qr(A)
             Rm = nat.as_device_colmajor(R, dev, "r")
             UR = nat.DevMat.empty(n, n, dev)
             VR = nat.DevMat.empty(n, n, dev)
@@ -294,6 +325,10 @@ def _svd_tall(A, dev, want_vt):
             if bool(null.any()):
                 U.view[:, null] = 0.0
             U, _ = _tall_qr(U, dev)
+        if perm is not None:  # a[:, perm] = u s v'^T: v[perm[i], :] = v'[i, :] (Vb holds v's columns as rows)
+            Vp = torch.empty_like(Vb)
+            Vp[:, perm] = Vb
+            Vb = Vp
         nat.call("psvd_sign_pair", ctx, nat._vp(U.data_ptr()), U.ld, m, n, nat.ptr(Vb), n, n, st)
     return U, s, Vb.T
 

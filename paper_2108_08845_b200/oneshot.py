@@ -109,13 +109,31 @@ def _tn(A, Y, dev):
     return X
 
 
+GRAM_EDGE = 1e-4       # s_r / s_1 below which the Gram's eigenvectors no longer give the top-r range to 1e-8
+ACCURATE_FACTORS = 0   # _left_factor calls that took the svd_full route (diagnostics / tests)
+
+
 def _left_factor(A, r, dev):
     """Top-r left singular vectors U (M x r, orthonormal to working precision, peak-positive
     columns) and singular values of A.  The Gram eigenvectors V0 of A^T A give the subspace;
     U is then one randomized-SVD step of A with Omega = V0 (Y = A V0, SVQB + CholeskyQR,
     B = Q^T A, one-sided Jacobi of B^T): the singular values and U are accurate to
-    eps ||A|| like the reference's Householder SVD, not eps ||A||^2 / s_k like the Gram alone."""
-    V0, _ = _topk(_gram(A, dev), A.cols, r, dev)
+    eps ||A|| like the reference's Householder SVD, not eps ||A||^2 / s_k like the Gram alone.
+    Forming A^T A tilts V0's r-th direction by ~eps (s_1 / s_r)^2, and below sqrt(eps) s_1 the
+    directions are lost altogether (mixed with A's null space when A is wide): a truncation
+    (r < rank) whose edge lies below GRAM_EDGE s_1 takes the reference's own route instead, the
+    backward-stable svd_full (linalg.py:107-123), truncated."""
+    V0, s0 = _topk(_gram(A, dev), A.cols, r, dev)
+    if r < min(A.rows, A.cols) and float(s0[r - 1]) < GRAM_EDGE * float(s0[0]):
+        from .errors import ConvergenceError
+        from .linalg import svd_full
+        global ACCURATE_FACTORS
+        try:
+            res = svd_full(A.view, want_vt=False, device=dev)
+            ACCURATE_FACTORS += 1
+            return nat.as_device_colmajor(res.u[:, :r], dev, "u"), res.s[:r].clone()
+        except ConvergenceError:
+            pass  # the Jacobi sweeps ran out (columns graded over ~1e60 and more): the Gram route's result stands
     om = V0.view.t().contiguous()  # (r, n) row-major == column-major n x r, ld n
     sk = RandomSketchConfig(target_rank=r, oversampling=0, power_iterations=0, seed=0)
     return randomized_update(None, None, A, sk, 1.0, dev, omega=om)

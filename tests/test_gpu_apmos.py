@@ -53,6 +53,14 @@ def test_apmos_burgers_emulated_ranks_match_golden(golden):
     assert np.max(oracle.mode_angles(modes, g["burgers_p4_modes"])) <= 1e-8
 
 
+def _steep_matrix():
+    """1904 x 17 with singular values spanning 1e-11 (found by tools/fuzz_parallel_dense.py)."""
+    rng = np.random.Generator(np.random.Philox(77))
+    u, _ = np.linalg.qr(rng.standard_normal((1904, 17)))
+    v, _ = np.linalg.qr(rng.standard_normal((17, 17)))
+    return (u * 1e-11 ** (np.arange(17) / 16)) @ v.T
+
+
 def _apmos_worker(rank, world, port, q, case):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -64,6 +72,9 @@ def _apmos_worker(rank, world, port, q, case):
             rng = np.random.Generator(np.random.Philox(42))
             a = rng.standard_normal((64, 16))
             cfg = p.ApmosConfig(local_rank=6, global_rank=8, k_modes=4)
+        elif case == "steep":
+            a = _steep_matrix()
+            cfg = p.ApmosConfig(local_rank=17, global_rank=15, k_modes=15)
         else:
             a = oracle.burgers_matrix(2048, 200)
             sk = p.RandomSketchConfig(target_rank=30, oversampling=10, power_iterations=1, seed=3)
@@ -81,7 +92,7 @@ def _apmos_worker(rank, world, port, q, case):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case", ["gauss", "burgers_rand"])
+@pytest.mark.parametrize("case", ["gauss", "burgers_rand", "steep"])
 def test_apmos_two_ranks_match_oracle(case):
     import torch.multiprocessing as mp
     s = socket.socket()
@@ -102,6 +113,15 @@ def test_apmos_two_ranks_match_oracle(case):
         rng = np.random.Generator(np.random.Philox(42))
         a = rng.standard_normal((64, 16))
         rm, rs = oracle.ref_apmos(_blocks(a, 2), 6, 8, 4)
+    elif case == "steep":
+        # the stacked exchange matrix is 17 x 34 and truncated at 15 of its 17 values, the kept edge at 2e-10 of
+        # the first: the Gram's eigenvectors cannot give that range (they mix with the null space), so
+        # _left_factor takes svd_full; values at LAPACK's own absolute accuracy, modes above 1e-6 s_1 at the bar
+        rm, rs = oracle.ref_apmos(_blocks(_steep_matrix(), 2), 17, 15, 15)
+        assert np.max(np.abs(sig - rs) / rs - 100 * np.finfo(float).eps * rs[0] / rs) <= 1e-10
+        live = rs > 1e-6 * rs[0]
+        assert np.max(oracle.mode_angles(m, rm)[live]) <= 1e-8
+        return
     else:
         a = oracle.burgers_matrix(2048, 200)
         rm, rs = oracle.ref_apmos(_blocks(a, 2), 40, 30, 10, use_randomized=True, sketch=(30, 10, 1, 3))

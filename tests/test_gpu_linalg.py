@@ -338,3 +338,36 @@ def test_svd_weak_directions_keep_u_orthonormal(m, n, kind):
     assert np.all(np.diff(s) <= 0) and np.max(np.abs(s - rs)) < 1e-12 * rs[0]
     big = rs > 1e-5 * rs[0]
     assert np.max(np.abs(s[big] - rs[big]) / rs[big]) < 1e-10
+
+
+@pytest.mark.parametrize("m,n,span", [(120, 100, 1e-80), (512, 200, 1e-80), (512, 200, 1e-150), (700, 300, 1e-30),
+                                      (40, 60, 1e-40)])
+def test_svd_graded_columns_converge(m, n, span):
+    """Columns graded over tens of orders, the small ones first (found through the Burgers rows near x = 1,
+    whose early snapshots are ~1e-80): the reference's dgesdd converges on any finite input
+    (linalg.py:107-123); ours sorts the columns by norm and takes the QR of the unit-norm columns
+    (linalg._svd_tall) instead of stalling in the Jacobi sweeps.  Values to LAPACK's absolute accuracy,
+    orthonormal factors, reconstruction to eps n s_1."""
+    p = _p()
+    x = _rng(5).standard_normal((m, n)) * span ** (np.arange(n)[::-1] / (n - 1))
+    u, s, vt = (t.cpu().numpy() for t in p.svd_full(x))
+    rs = np.linalg.svd(x, compute_uv=False)
+    k = min(m, n)
+    assert np.max(np.abs(s - rs)) <= 1e-13 * rs[0] and np.all(np.diff(s) <= 0)
+    assert np.max(np.abs(u.T @ u - np.eye(k))) <= 1e-12 and np.max(np.abs(vt @ vt.T - np.eye(k))) <= 1e-12
+    assert np.max(np.abs((u * s) @ vt - x)) <= 1e-12 * rs[0]   # ~ eps n s_1
+
+
+@pytest.mark.parametrize("rows", [300, 512, 2048])
+def test_svd_burgers_tail_rows(rows):
+    """The grid rows nearest x = 1 (the block the last rank of a row partition holds): the leading
+    values at the bar against the reference, the whole spectrum to 1e-13 s_1."""
+    p = _p()
+    x = oracle.burgers_matrix(8192 if rows == 2048 else 2048, 800 if rows == 2048 else 200)[-rows:]
+    res = p.svd_full(x, want_vt=False)
+    u, s = res.u.cpu().numpy(), res.s.cpu().numpy()
+    ru, rs, _ = oracle.ref_svd(x, want_vt=False)
+    assert np.max(np.abs(s - rs)) <= 1e-13 * rs[0]
+    lead = rs >= 1e-5 * rs[0]
+    assert np.max(np.abs(s[lead] - rs[lead]) / rs[lead]) <= 1e-10
+    assert np.max(np.abs(u.T @ u - np.eye(u.shape[1]))) <= 1e-12
