@@ -210,6 +210,26 @@ def _tall_qr(A, dev):
     return Q, R.T
 
 
+def _equilibrated_tall_qr(A, dev):
+    """_tall_qr of a matrix whose column norms span more than 1e3: the factorization is taken of the unit-norm
+    columns and R's columns are scaled back (a = (a D^-1) D; Householder's q does not depend on the scaling,
+    linalg.py:94-104).  The scaled matrix is as well conditioned as column scaling can make it, so a
+    column-graded input stays on CholeskyQR2 and its small columns keep rows of R accurate relative to their
+    own size, as Householder's are, instead of falling to the rank-robust route at rounding level."""
+    import torch
+    from . import _native as nat
+    if A.cols < 2:
+        return _tall_qr(A, dev)
+    cn = torch.linalg.vector_norm(A.view, dim=0)
+    if not float(cn.min()) < 1e-3 * float(cn.max()):  # (also the non-finite case: reported by the kernels)
+        return _tall_qr(A, dev)
+    scale = torch.where(cn > 0, cn, torch.ones_like(cn))
+    Xs = nat.DevMat.empty(A.rows, A.cols, dev)
+    torch.div(A.view, scale[None, :], out=Xs.view)
+    Q, R = _tall_qr(Xs, dev)
+    return Q, R * scale[None, :]
+
+
 def qr_factor(a, device=None):
     """Reduced QR with diag(r) >= 0 (linalg.py:94-104): QrResult(q (m x min(m, n)),
     r (min(m, n) x n)) as CUDA tensors.  Tall inputs run CholeskyQR2 (shifted
@@ -223,11 +243,11 @@ def qr_factor(a, device=None):
     m, n = A.rows, A.cols
     ctx = nat.context(dev)
     if m >= n:
-        Q, R = _tall_qr(A, dev)
+        Q, R = _equilibrated_tall_qr(A, dev)
         _check(ctx, dev, "a")
         return QrResult(Q.view, R)
     lead = nat.DevMat(A.view[:, :m], A.ld)
-    Q, R0 = _tall_qr(lead, dev)
+    Q, R0 = _equilibrated_tall_qr(lead, dev)
     rest = torch.empty((n - m, m), dtype=torch.float64, device=dev)  # column-major (m x (n - m))
     with torch.cuda.device(dev):
         nat.call("psvd_tn_product", ctx, m, nat._vp(Q.data_ptr()), Q.ld, m,

@@ -371,3 +371,24 @@ def test_svd_burgers_tail_rows(rows):
     lead = rs >= 1e-5 * rs[0]
     assert np.max(np.abs(s[lead] - rs[lead]) / rs[lead]) <= 1e-10
     assert np.max(np.abs(u.T @ u - np.eye(u.shape[1]))) <= 1e-12
+
+
+@pytest.mark.parametrize("m,n,span,up", [(300, 40, 1e-12, True), (5000, 150, 1e-30, True), (2000, 300, 1e-80, False),
+                                         (64, 64, 1e-20, True), (30, 50, 1e-20, True)])
+def test_qr_graded_columns_match_reference(m, n, span, up):
+    """Column norms spanning up to 1e80 (either order): the factorization of the unit-norm columns with R
+    scaled back (linalg._equilibrated_tall_qr) reproduces the reference's Householder q to rounding and every
+    column of r relative to that column's own norm (linalg.py:94-104), not just the rows with large pivots."""
+    p = _p()
+    d = span ** (np.arange(n) / (n - 1))
+    x = _rng(3).standard_normal((m, n)) * (d[::-1] if up else d)
+    res = p.qr_factor(x)
+    q, r = res.q.cpu().numpy(), res.r.cpu().numpy()
+    q0, r0 = oracle.ref_qr(x)
+    cn = np.linalg.norm(x, axis=0)
+    k = min(m, n)
+    assert np.max(np.abs(q.T @ q - np.eye(k))) <= 1e-13
+    assert np.max(np.abs(q - q0)) <= 1e-12
+    assert np.max(np.abs(r - r0) / cn[None, :]) <= 1e-12
+    assert np.max(np.abs(q @ r - x) / cn[None, :]) <= 1e-13
+    assert np.all(np.diag(r) >= 0)
