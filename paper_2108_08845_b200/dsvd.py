@@ -577,6 +577,18 @@ def parallel_qr(ctx, a_local, device=None):
 
     nccl = dist.get_backend(ctx.group) == "nccl"
 
+    # column norms spanning more than 1e3 (rank-ordered sum of the local squares: the same bits, so the same
+    # decision, on every rank): the unit-norm columns are factored and r's columns scaled back, as
+    # linalg._equilibrated_tall_qr does on one GPU (Householder's q does not depend on the scaling)
+    scale = None
+    if n > 1:
+        cn = torch.sqrt(allreduce_ordered((A.view * A.view).sum(dim=0), ctx))
+        if float(cn.min()) < 1e-3 * float(cn.max()):
+            scale = torch.where(cn > 0, cn, torch.ones_like(cn))
+            As = nat.DevMat.empty(m, n, dev)
+            torch.div(A.view, scale[None, :], out=As.view)
+            A = As
+
     def gram(X):
         G = torch.empty((n, n), dtype=torch.float64, device=dev)
         nat.call("psvd_gram", c, X.rows, nat._vp(0), 0, nat._vp(0), 1.0, 0, nat._vp(X.data_ptr()), X.ld, n,
@@ -623,4 +635,4 @@ def parallel_qr(ctx, a_local, device=None):
         st_word = nat.read_status(c, reset=True, device=dev)
     if st_word & nat.ST_NONFINITE:
         raise ValueError("a_local contains non-finite entries")
-    return QrResult(Q.view, R.T)
+    return QrResult(Q.view, R.T if scale is None else R.T * scale[None, :])

@@ -15,10 +15,13 @@ def cases(seed, count, world):
         n = random.choice([random.randint(2, 40), random.randint(41, 230)])
         m = random.choice([random.randint(max(n, world), 3 * n + world), random.randint(n, 4000),
                            16 * random.randint(n // 16 + 1, 300)])
-        kind = random.choice(["gauss", "decay", "steep", "deficient"])
+        kind = random.choice(["gauss", "decay", "steep", "deficient", "graded"])
         rnk = n
         if kind == "gauss":
             a = rng.standard_normal((m, n))
+        elif kind == "graded":   # column norms over up to 60 orders, either direction
+            d = random.choice([1e-8, 1e-30, 1e-60]) ** (np.arange(n) / max(n - 1, 1))
+            a = rng.standard_normal((m, n)) * (d if random.random() < 0.5 else d[::-1])
         else:
             u, _ = np.linalg.qr(rng.standard_normal((m, n)))
             v, _ = np.linalg.qr(rng.standard_normal((n, n)))
@@ -66,6 +69,10 @@ def worker(rank, world, port, seed, count):
                 okrow = piv >= 1e-6 * piv[0]
                 bound = 64 * EPS * an * an / np.maximum(piv, 1e-300)
                 dr = float(np.max((np.max(np.abs(r - r0), axis=1) / bound)[okrow]))
+                if c["kind"] == "graded":   # Householder-level: every column of r relative to that column's norm
+                    cn = np.linalg.norm(a, axis=0)
+                    dr = float(np.max(np.abs(r - r0) / cn[None, :]) / 1e-12)
+                    rec = float(np.max(np.abs(q @ r - a) / cn[None, :]))
                 worst.update(orth=max(worst["orth"], orth), rec=max(worst["rec"], rec), r=max(worst["r"], dr))
                 if orth > 1e-12 or rec > 1e-13 or dr > 1.0:
                     print("FAIL parallel_qr", c, orth, rec, dr, flush=True)
