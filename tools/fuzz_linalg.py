@@ -17,9 +17,12 @@ def note(k, v):
 for it in range(count):
     n = random.choice([random.randint(1, 40), random.randint(41, 230), random.randint(231, 420)])
     m = random.choice([n, n + random.randint(0, 50), random.randint(n, 6000)])
-    kind = random.choice(["gauss", "decay", "steep", "deficient"])
+    kind = random.choice(["gauss", "decay", "steep", "deficient", "graded"])
     if kind == "gauss":
         a = rng.standard_normal((m, n))
+    elif kind == "graded":   # column norms over up to 80 orders, either direction
+        d = random.choice([1e-8, 1e-30, 1e-80]) ** (np.arange(n) / max(n - 1, 1))
+        a = rng.standard_normal((m, n)) * (d if random.random() < 0.5 else d[::-1])
     else:
         r = n if kind != "deficient" else max(1, n // 2)
         u, _ = np.linalg.qr(rng.standard_normal((m, r)))

@@ -25,11 +25,14 @@ for it in range(count):
     r = min(random.choice([40, 90]), cols, M)
     U, _ = np.linalg.qr(rng.standard_normal((M, r)))
     V, _ = np.linalg.qr(rng.standard_normal((cols, r)))
-    kind = random.choice(["decay", "decay", "steep", "gauss"]) if len(sys.argv) > 3 else "decay"   # any 3rd argument: mixed spectra
+    kind = random.choice(["decay", "decay", "steep", "gauss", "graded"]) if len(sys.argv) > 3 else "decay"   # any 3rd argument: mixed spectra
     if kind == "decay":
         a = (U * (2.0 ** -np.arange(r))) @ V.T + 1e-9 * rng.standard_normal((M, cols))
     elif kind == "steep":   # spans that trip the conditioning gates
         a = (U * (random.choice([1e-6, 1e-9, 1e-12]) ** (np.arange(r) / max(r - 1, 1)))) @ V.T
+    elif kind == "graded":   # low-rank signal with column norms over up to 40 orders, either direction
+        d = random.choice([1e-6, 1e-20, 1e-40]) ** (np.arange(cols) / max(cols - 1, 1))
+        a = ((U * (2.0 ** -np.arange(r))) @ V.T + 1e-9 * rng.standard_normal((M, cols))) * (d if random.random() < 0.5 else d[::-1])
     else:
         a = rng.standard_normal((M, cols))
     batches, c0 = [], 0
