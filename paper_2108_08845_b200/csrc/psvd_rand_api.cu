@@ -91,6 +91,10 @@ int psvd_rand_update(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const
   const int n = Kc + B;
   int rc;
   if (M < 1 || B < 1 || Kc < 0 || K < 1 || l < K || q < 0) return fail(c, PSVD_EINVAL, "bad randomized shape");
+  // the sketch's Cholesky / SVQB / Jacobi solvers are the one-CTA kernels: wider sketches are the caller's
+  // (linalg.randomized_update composes them from the any-width products, psvd_qr and the multi-CTA Jacobi)
+  if (l > CHOL_NMAX)
+    return fail(c, PSVD_EINVAL, "sketch width %d exceeds the %d columns of psvd_rand_update", l, CHOL_NMAX);
   // (row-partitioned: M is this rank's block, which may be shorter than the sketch; the caller checks the global rows)
   const int64_t rows_chk = ex_active(c) ? std::max<int64_t>(M, l) : M;
   if (l > std::min<int64_t>(rows_chk, n))

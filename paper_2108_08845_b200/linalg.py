@@ -65,6 +65,7 @@ def device_omega(n_cols, config, device):
     return om
 
 
+RAND_MAX_WIDTH = 112  # CHOL_NMAX: the widest sketch of the fused randomized update (psvd_rand_update)
 ACCURATE_RAND_UPDATES = 0  # randomized updates redone on the accurate route (diagnostics / tests)
 
 
@@ -123,6 +124,12 @@ def randomized_update(U, sigma, A, sketch, ff, device, check=True, total_rows=No
     rows = M if total_rows is None else total_rows
     if l > min(rows, n):
         raise ValueError(f"sketch width {l} exceeds min(a.shape) = {min(rows, n)}")
+    if l > RAND_MAX_WIDTH:
+        # wider than the fused update's one-CTA solvers (psvd_rand_update refuses it): the same sequence
+        # composed from the any-width kernels -- the accurate route (the row-partitioned caller's own)
+        if callable(accurate):
+            return accurate()
+        return accurate_randomized_update(U, sigma, A, sketch, ff, device, omega=omega)
     om = device_omega(n, sketch, device) if omega is None else omega
     ctx = nat.context(device)
     with torch.cuda.device(device):
@@ -154,10 +161,18 @@ def low_rank_svd(a, config, device=None):
     from . import _native as nat
     dev = _dev(device)
     A = nat.as_device_colmajor(a, dev, "a")
+    n_acc = ACCURATE_RAND_UPDATES
     u, s = randomized_update(None, None, A, config, 1.0, dev)
     k, l = config.target_rank, config.sketch_width
     ctx = nat.context(dev)
     with torch.cuda.device(dev):
+        if ACCURATE_RAND_UPDATES != n_acc:
+            # the any-width / accurate route ran (no fused update whose small factors psvd_rand_last_vt could
+            # read): b's right vectors are vt_j = u_j^T a / s_j, rows signed with u's columns
+            Z = torch.empty((k, A.cols), dtype=torch.float64, device=dev).t()  # n x k column-major: a^T u
+            nat.call("psvd_tn_product", ctx, A.rows, nat._vp(A.data_ptr()), A.ld, A.cols, nat._vp(u.data_ptr()), u.ld,
+                     k, nat._vp(Z.data_ptr()), A.cols, nat.stream_ptr(dev))
+            return SvdResult(u.view, s, (Z / torch.where(s > 0, s, torch.ones_like(s))[None, :]).T)
         vt = torch.empty((A.cols, k), dtype=torch.float64, device=dev)  # (k x n) column-major
         nat.call("psvd_rand_last_vt", ctx, A.cols, l, k, nat.ptr(vt), k, nat.stream_ptr(dev))
     return SvdResult(u.view, s, vt.T)

@@ -146,3 +146,42 @@ def test_steep_sketch_row_partitioned_takes_accurate_route(span, qit):
     ref_m, ref_s, _ = oracle.ref_rand_stream_all(_steep(span), 10, 0.95, 10, qit, 0)
     _check(out[0][2], out[0][0], ref_m, ref_s)
     _check(out[0][3], out[0][1], ref_m, ref_s)
+
+
+@pytest.mark.parametrize("k,over", [(136, 0), (100, 20), (120, 8)])
+def test_sketches_wider_than_the_fused_update(k, over):
+    """Sketches of more than 112 columns (found by tools/fuzz_stream.py with FUZZ_BIG_K: the fused update's
+    one-CTA solvers returned zeros without an error): psvd_rand_update refuses them and randomized_update
+    composes the same sequence from the any-width kernels; stream, per-update calls and low_rank_svd (u, s
+    and vt) against the oracle at the bar."""
+    p = _pkg()
+    rng = np.random.Generator(np.random.Philox(11))
+    M, w = 3000, k + over + 40
+    U, _ = np.linalg.qr(rng.standard_normal((M, 160)))
+    V, _ = np.linalg.qr(rng.standard_normal((3 * w, 160)))
+    a = (U * (0.93 ** np.arange(160))) @ V.T + 1e-9 * rng.standard_normal((M, 3 * w))
+    b = [np.asfortranarray(a[:, i * w:(i + 1) * w]) for i in range(3)]
+    sk = p.RandomSketchConfig(target_rank=k, oversampling=over, power_iterations=1, seed=2)
+    cfg = p.StreamConfig(k_modes=k, forget_factor=0.95, batch_columns=w, sketch=sk)
+    ref_m, ref_s, _ = oracle.ref_rand_stream_all(b, k, 0.95, over, 1, 2)
+    st, hist = p.stream_all(b, cfg)
+    m, s = st.numpy()
+    assert len(hist) == 3 and oracle.sigma_rel_err(s, ref_s) <= SIG_TOL
+    gaps = np.array([min(abs(ref_s[j] - ref_s[i]) for i in range(k) if i != j) / ref_s[j] for j in range(k)])
+    sel = gaps > 1e-3
+    assert float(np.max(oracle.mode_angles(m, ref_m)[sel])) <= ANG_TOL
+    assert np.all(np.sum(m * ref_m, axis=0)[sel] > 0)
+    res = p.low_rank_svd(b[0], sk)
+    u, s1, vt = oracle.ref_low_rank_svd(b[0], k, over, 1, 2)
+    assert oracle.sigma_rel_err(res.s.cpu().numpy(), s1) <= SIG_TOL
+    assert float(np.max(np.abs(res.vt.cpu().numpy() - vt)[sel])) <= 1e-7
+    import ctypes
+    from paper_2108_08845_b200 import _native as nat
+    with pytest.raises(ValueError):   # the C entry point itself fails loudly
+        dev = st.modes.device
+        A = nat.as_device_colmajor(b[0], dev)
+        out = nat.DevMat.empty(M, k, dev)
+        sig = st.singular_values.clone()
+        om = p.linalg.device_omega(w, sk, dev)
+        nat.call("psvd_rand_update", nat.context(dev), M, nat._vp(0), 0, nat._vp(0), 1.0, 0, nat._vp(A.data_ptr()), A.ld,
+                 w, k, k + over, 1, nat.ptr(om), nat._vp(out.data_ptr()), out.ld, nat.ptr(sig), nat.stream_ptr(dev))

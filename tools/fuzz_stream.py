@@ -1,6 +1,6 @@
 """Random small streams through stream_all (deterministic and randomized) against the oracle: shapes that reach
 the split-ring kernel (rows a multiple of 16) and ones that do not.  python tools/fuzz_stream.py [seed] [count] [mixed]"""
-import random, sys
+import os, random, sys
 import numpy as np
 import torch
 sys.path.insert(0, ".")
@@ -15,9 +15,12 @@ illposed = 0
 for it in range(count):
     M = random.choice([16 * random.randint(20, 400), random.randint(300, 5000)])
     K = random.choice([random.randint(1, 16), random.randint(17, 48)])
+    if os.environ.get("FUZZ_BIG_K") and random.random() < 0.5:   # the wide cores (K up to 150: global-memory solvers)
+        K = random.randint(49, 150)
     nb = random.randint(2, 9)
     p.streaming.STREAM_WINDOW = random.choice([2, 3, 8])  # windows chained through the state
-    widths = [random.randint(max(K, 8), random.choice([120, 300])) for _ in range(nb)]
+    widths = [random.randint(max(K, 8), max(K, 8) + random.choice([120, 300])) for _ in range(nb)] if K > 48 else \
+        [random.randint(max(K, 8), random.choice([120, 300])) for _ in range(nb)]
     ff = random.choice([1.0, 0.95, 0.8])
     rand = random.random() < 0.4
     # a decaying spectrum so that modes are separated (angles are only defined for separated modes)
@@ -50,6 +53,8 @@ for it in range(count):
     else:
         cfg = p.StreamConfig(k_modes=K, forget_factor=ff, batch_columns=widths[0])
         ref_m, ref_s, _ = oracle.ref_stream_all(batches, K, ff)
+    if os.environ.get("FUZZ_ONLY") and it != int(os.environ["FUZZ_ONLY"]):
+        continue
     st, _ = p.stream_all(batches, cfg)
     m, s = st.numpy()
     # relative error of each kept value, less what two backward-stable computations may differ by at that size
@@ -77,6 +82,8 @@ for it in range(count):
                   f"perturbation {cs:.1e} / {ca:.1e}")
             continue
         print("FAIL", dict(M=M, K=K, widths=widths, ff=ff, rand=rand, kind=kind), es, ea)
+        print("  ours", s[:4], "... ref", ref_s[:4], "nan modes", bool(np.isnan(m).any()), "zero modes", bool((m == 0).all()),
+              "status", hex(p.streaming.LAST_STATUS), "sketch", None if not rand else (sk.oversampling, q))
         print("  it", it, "gaps", np.array2string(gaps, precision=1), "\n  angles", np.array2string(ang, precision=1),
               "\n  sigma rel", np.array2string(np.abs(s - ref_s) / ref_s, precision=1))
         sys.exit(1)
