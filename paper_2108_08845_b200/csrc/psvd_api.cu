@@ -732,8 +732,11 @@ int psvd_gram(psvd_ctx* c, int64_t M, const double* U, int64_t ldu, const double
     // too many 32x32 tiles for one pass: the tall-skinny TN GEMM (full n x n, split over rows),
     // [U | A]^T U and [U | A]^T A, then the d_i d_j scaling of the panel [ff U S | A]
     c->path_count[4]++;
-    if ((rc = ensure(c, c->partial, sizeof(double) * tgemm_tn_partial_doubles(M, n, std::max(B, std::max(Kc, 1)),
-                                                                              c->num_sms))))
+    // (one workspace for both products, each sized on its own: a narrower Y splits the rows into more chunks
+    // and can need more partial tiles than the wider one)
+    if ((rc = ensure(c, c->partial,
+                     sizeof(double) * std::max(tgemm_tn_partial_doubles(M, n, std::max(Kc, 1), c->num_sms),
+                                               tgemm_tn_partial_doubles(M, n, std::max(B, 1), c->num_sms)))))
       return rc;
     std::vector<GemmSeg> gp;
     if (Kc > 0) gp.push_back(GemmSeg{U, ldu, Kc});

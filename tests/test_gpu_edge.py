@@ -194,3 +194,25 @@ def test_wide_k_drift_check(k):
     m2, s2 = st2.numpy()
     assert oracle.sigma_rel_err(s2, s1) <= 1e-12
     assert np.max(np.abs(m2.T @ m2 - np.eye(k))) < 1e-12
+
+
+@pytest.mark.parametrize("rows,k,widths", [(3895, 91, (98, 372, 137)), (4445, 87, (144, 153, 252, 130))])
+def test_wide_panel_gram_both_products(rows, k, widths):
+    """Found by tools/fuzz_stream.py (FUZZ_BIG_K): a panel of more than 320 columns takes the tall-skinny GEMM
+    Gram, [U | A]^T U and [U | A]^T A through one workspace that was sized for the wider product only, while the
+    narrower one splits the rows into more chunks (an illegal memory access at K = 91, B = 372).  The stream
+    against the oracle at the bar."""
+    p = _p()
+    rng = np.random.Generator(np.random.Philox(53))
+    u, _ = np.linalg.qr(rng.standard_normal((rows, 200)))
+    v, _ = np.linalg.qr(rng.standard_normal((sum(widths), 200)))
+    a = (u * (0.95 ** np.arange(200))) @ v.T
+    bs, c0 = [], 0
+    for w in widths:
+        bs.append(np.asfortranarray(a[:, c0:c0 + w]))
+        c0 += w
+    cfg = p.StreamConfig(k_modes=k, forget_factor=0.95, batch_columns=widths[0])
+    st, hist = p.stream_all(bs, cfg)
+    ref_m, ref_s, _ = oracle.ref_stream_all(bs, k, 0.95)
+    assert len(hist) == len(widths)
+    _parity(st, ref_m, ref_s)

