@@ -17,7 +17,14 @@ for it in range(count):
     K = random.choice([random.randint(1, 16), random.randint(17, 48)])
     if os.environ.get("FUZZ_BIG_K") and random.random() < 0.5:   # the wide cores (K up to 150: global-memory solvers)
         K = random.randint(49, 150)
+    if os.environ.get("FUZZ_TINY"):   # boundary shapes: a handful of rows, K up to the row count
+        M = random.randint(1, 64)
+        K = random.randint(1, min(M, 12))
     nb = random.randint(2, 9)
+    if os.environ.get("FUZZ_LARGE"):  # many row chunks per CTA, long TMA streams
+        M = random.choice([16 * random.randint(4096, 25000), random.randint(65536, 400000)])
+        K = random.choice([random.randint(1, 16), random.randint(17, 32)])
+        nb = random.randint(2, 4)
     p.streaming.STREAM_WINDOW = random.choice([2, 3, 8])  # windows chained through the state
     widths = [random.randint(max(K, 8), max(K, 8) + random.choice([120, 300])) for _ in range(nb)] if K > 48 else \
         [random.randint(max(K, 8), random.choice([120, 300])) for _ in range(nb)]
