@@ -13,6 +13,8 @@ def cases(seed, count, world):
     rng = np.random.Generator(np.random.Philox(seed))
     for _ in range(count):
         n = random.choice([random.randint(2, 40), random.randint(41, 230)])
+        if os.environ.get("FUZZ_BIG_N") and random.random() < 0.5:   # the global-memory Cholesky / multi-CTA Jacobi
+            n = random.randint(231, 420)
         m = random.choice([random.randint(max(n, world), 3 * n + world), random.randint(n, 4000),
                            16 * random.randint(n // 16 + 1, 300)])
         kind = random.choice(["gauss", "decay", "steep", "deficient", "graded"])
