@@ -52,7 +52,12 @@ for it in range(count):
     e_rec = np.max(np.abs((u_ * s_) @ vt_ - a)) / amax
     e_orth = max(np.max(np.abs(u_.T @ u_ - np.eye(k))), np.max(np.abs(vt_ @ vt_.T - np.eye(k))))
     if e_s > 1e-9 or e_abs > 1e-12 or e_rec > 1e-11 or e_orth > 1e-10 or np.any(np.diff(s_) > 0):
-        print("FAIL svd", tag, e_s, e_abs, e_rec, e_orth); sys.exit(1)
+        print("FAIL svd", tag, e_s, e_abs, e_rec, e_orth)
+        import os
+        os.makedirs("gpurun_out", exist_ok=True)
+        np.save("gpurun_out/fail_svd.npy", a)
+        bad = np.argsort(-np.abs(s_ - rs))[:6]
+        print("  worst values", bad, s_[bad], rs[bad]); sys.exit(1)
     note("svd rel", e_s); note("svd abs", e_abs); note("svd rec", e_rec); note("svd orth", e_orth)
     # low_rank_svd
     if min(m, n) >= 6:
